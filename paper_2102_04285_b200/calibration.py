@@ -1,0 +1,187 @@
+"""Calibration profile: the *input* type of overhead correction.
+
+Mirrors ``CalibrationProfile`` and its ``xstrace-profile v1`` text format from
+``pkg/src/xstrace/calibration.py:28-233`` (the estimators that *build* a
+profile -- delta / difference-of-average calibration -- are off the hot path
+and out of scope).  ``scaled()`` turns the exact
+rational means into integers over one common denominator, which is how the
+device carries ``fractions.Fraction`` arithmetic exactly (K6).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass
+from fractions import Fraction
+from pathlib import Path
+from typing import Sequence, Union
+
+import numpy as np
+
+PROFILE_HEADER = "xstrace-profile v1"
+
+HOOK_ANNOTATION = "annotation"
+HOOK_TRANSITION = "transition"
+HOOK_API_INTERCEPTION = "api_interception"
+HOOK_API_INTERNAL = "api_internal"
+HOOK_KINDS = (HOOK_ANNOTATION, HOOK_TRANSITION, HOOK_API_INTERCEPTION, HOOK_API_INTERNAL)
+
+
+@dataclass(frozen=True)
+class CalibrationProfile:
+    """Mean book-keeping overhead per hook kind (calibration.py:142-220)."""
+
+    annotation_ns: Fraction
+    transition_ns: Fraction
+    api_interception_ns: Fraction
+    api_internal_ns: dict
+    provenance: tuple = ()
+
+    def is_zero(self) -> bool:
+        return (
+            self.annotation_ns == 0
+            and self.transition_ns == 0
+            and self.api_interception_ns == 0
+            and all(v == 0 for v in self.api_internal_ns.values())
+        )
+
+    def to_text(self) -> str:
+        lines = [PROFILE_HEADER]
+        lines.append(f"annotation = {_format_ns(self.annotation_ns)}")
+        lines.append(f"transition = {_format_ns(self.transition_ns)}")
+        lines.append(f"api_interception = {_format_ns(self.api_interception_ns)}")
+        for api in sorted(self.api_internal_ns):
+            lines.append(f"api_internal.{api} = {_format_ns(self.api_internal_ns[api])}")
+        for note in self.provenance:
+            lines.append(f"# {note}")
+        return "\n".join(lines) + "\n"
+
+    @classmethod
+    def from_text(cls, text: str) -> "CalibrationProfile":
+        lines = text.splitlines()
+        if not lines or lines[0].strip() != PROFILE_HEADER:
+            raise ValueError(f"not a calibration profile: expected header '{PROFILE_HEADER}'")
+        values: dict = {}
+        internal: dict = {}
+        provenance: list = []
+        for line in lines[1:]:
+            line = line.strip()
+            if not line:
+                continue
+            if line.startswith("#"):
+                provenance.append(line.lstrip("# "))
+                continue
+            if "=" not in line:
+                raise ValueError(f"bad profile line: {line!r}")
+            key, _, raw = line.partition("=")
+            key = key.strip()
+            value = _parse_ns(raw.strip())
+            if value < 0:
+                raise ValueError(f"negative overhead for {key!r}")
+            if key.startswith("api_internal."):
+                internal[key[len("api_internal."):]] = value
+            elif key in ("annotation", "transition", "api_interception"):
+                values[key] = value
+            else:
+                raise ValueError(f"unknown profile key {key!r}")
+        for required in ("annotation", "transition", "api_interception"):
+            if required not in values:
+                raise ValueError(f"profile missing key {required!r}")
+        return cls(values["annotation"], values["transition"], values["api_interception"],
+                   internal, tuple(provenance))
+
+    def write(self, path: Union[str, os.PathLike]) -> None:
+        Path(path).write_text(self.to_text(), encoding="utf-8")
+
+    @classmethod
+    def read(cls, path: Union[str, os.PathLike]) -> "CalibrationProfile":
+        return cls.from_text(Path(path).read_text(encoding="utf-8"))
+
+    @classmethod
+    def zero(cls, api_names: Sequence[str] = ()) -> "CalibrationProfile":
+        return cls(Fraction(0), Fraction(0), Fraction(0), {n: Fraction(0) for n in api_names},
+                   ("zero profile",))
+
+    def scaled(self, names: Sequence[str]) -> "ScaledProfile":
+        return ScaledProfile.build(self, names)
+
+
+def _format_ns(value: Fraction) -> str:
+    value = Fraction(value)
+    if value.denominator == 1:
+        return str(value.numerator)
+    return f"{value.numerator}/{value.denominator}"
+
+
+def _parse_ns(raw: str) -> Fraction:
+    try:
+        return Fraction(raw)
+    except ValueError as exc:
+        raise ValueError(f"bad overhead value {raw!r}") from exc
+
+
+INT64_MAX = 2**63 - 1
+
+
+@dataclass
+class ScaledProfile:
+    """Amounts as integers over the common denominator ``L``.
+
+    The per-site amounts the reference draws (correction.py:90-100):
+    ``annotation/2`` at ANN_START, ``annotation - annotation/2`` at ANN_END,
+    ``transition``, ``api_interception`` and ``api_internal[name]``.  Every
+    one is ``k / L`` exactly, so ``floor(sum)`` in ``quantize_amounts``
+    (_timeline.py:57-67) equals ``floor(sum_k / L)`` over int128 on the
+    device.
+    """
+
+    L: int
+    ann_start: int
+    ann_end: int
+    transition: int
+    interception: int
+    internal: np.ndarray      # int64 [n_names]
+    has_internal: np.ndarray  # uint8 [n_names]
+
+    @classmethod
+    def build(cls, profile: CalibrationProfile, names: Sequence[str]) -> "ScaledProfile":
+        ann = Fraction(profile.annotation_ns)
+        half = ann / 2
+        rest = ann - half
+        base = [half, rest, Fraction(profile.transition_ns), Fraction(profile.api_interception_ns)]
+        internal = {k: Fraction(v) for k, v in profile.api_internal_ns.items()}
+        den = 1
+        for v in base + [internal[n] for n in names if n in internal]:
+            den = den * v.denominator // math.gcd(den, v.denominator)
+        scaled = [int(v * den) for v in base]
+        ints = np.zeros(len(names), dtype=np.int64)
+        has = np.zeros(len(names), dtype=np.uint8)
+        for i, n in enumerate(names):
+            if n in internal:
+                v = int(internal[n] * den)
+                _check64(v)
+                ints[i] = v
+                has[i] = 1
+        for v in scaled + [den]:
+            _check64(v)
+        return cls(den, scaled[0], scaled[1], scaled[2], scaled[3], ints, has)
+
+    def max_abs(self) -> int:
+        vals = [self.ann_start, self.ann_end, self.transition, self.interception]
+        if self.internal.size:
+            vals += [int(np.abs(self.internal).max())]
+        return max(abs(v) for v in vals)
+
+    def check_int128(self, n_sites: int) -> None:
+        """The device running sum is int128: |sum| <= n_sites * max|amount|."""
+        if (max(n_sites, 1) * max(self.max_abs(), 1)).bit_length() >= 126:
+            raise ValueError(
+                "calibration profile denominators too large for exact int128 accumulation "
+                f"(L={self.L}, {n_sites} sites)"
+            )
+
+
+def _check64(v: int) -> None:
+    if abs(v) > INT64_MAX:
+        raise ValueError("scaled calibration amount exceeds int64; profile denominators too large")

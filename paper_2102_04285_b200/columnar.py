@@ -1,0 +1,149 @@
+"""Columnar (SoA) trace: the layout the device path consumes.
+
+A ``Trace`` of Python ``Event`` objects cannot scale past a few million
+events (~0.9 GB per 1M in the reference), so the engine's
+native input is this structure of arrays.  The interning rules make integer
+comparisons on the device equal the reference's Python comparisons:
+
+* ``pid``  -- index into ``pids`` (sorted numeric pid values: events U metas),
+* ``tid``  -- index into the sorted table of distinct (pid, tid) pairs, so two
+  tids of one pid compare like the reference's ints (Site.order_key,
+  _op_rank_order) and a group index is also the (pid, tid) key,
+* ``name`` -- rank of the name in ``sorted(names)`` (Python str order), so name
+  ties break exactly like ``str`` comparisons,
+* ``corr`` / ``has_corr`` -- correlation id and a presence flag (None).
+
+Row order is the trace's event order; the row index plays the role of the
+reference's event index in every stable-sort tie-break.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .model import Category, Event, ProcessMeta, Trace
+
+
+@dataclass
+class ColumnarTrace:
+    clock_domain: int
+    start: np.ndarray       # int64
+    dur: np.ndarray         # int64
+    pid: np.ndarray         # int32 index into pids
+    tid: np.ndarray         # int32 index into groups
+    cat: np.ndarray         # uint8
+    name: np.ndarray        # int32 rank into names
+    corr: np.ndarray        # int64
+    has_corr: np.ndarray    # uint8
+    pids: np.ndarray        # int64 sorted pid values
+    group_pid: np.ndarray   # int32 pid index of each group
+    group_tid: np.ndarray   # int64 tid value of each group
+    names: list             # sorted names
+    processes: tuple = ()
+    pid_has_meta: Optional[np.ndarray] = None  # uint8 [n_pids]
+    _source: Optional[Trace] = field(default=None, repr=False)
+
+    @property
+    def n(self) -> int:
+        return int(self.start.shape[0])
+
+    @property
+    def n_pids(self) -> int:
+        return int(self.pids.shape[0])
+
+    @property
+    def n_groups(self) -> int:
+        return int(self.group_pid.shape[0])
+
+    def __post_init__(self):
+        if self.pid_has_meta is None:
+            meta = {m.pid for m in self.processes}
+            self.pid_has_meta = np.array([int(p) in meta for p in self.pids], dtype=np.uint8)
+
+    # -- construction --------------------------------------------------------
+    @classmethod
+    def from_trace(cls, trace: Trace) -> "ColumnarTrace":
+        """Intern a Trace of Event-like objects (duck-typed: the reference's
+        own ``xstrace.Event`` works too)."""
+        evs = trace.events
+        n = len(evs)
+        start = np.fromiter((e.start for e in evs), dtype=np.int64, count=n)
+        dur = np.fromiter((e.duration for e in evs), dtype=np.int64, count=n)
+        pid_v = np.fromiter((e.pid for e in evs), dtype=np.int64, count=n)
+        tid_v = np.fromiter((e.tid for e in evs), dtype=np.int64, count=n)
+        cat = np.fromiter((int(e.category) for e in evs), dtype=np.uint8, count=n)
+        corr_list = [e.correlation for e in evs]
+        has_corr = np.fromiter((c is not None for c in corr_list), dtype=np.uint8, count=n)
+        corr = np.fromiter((c if c is not None else 0 for c in corr_list), dtype=np.int64, count=n)
+        name_list = [e.name for e in evs]
+        names = sorted(set(name_list))
+        rank = {s: i for i, s in enumerate(names)}
+        name = np.fromiter((rank[s] for s in name_list), dtype=np.int32, count=n)
+        return cls.from_arrays(trace.clock_domain, start, dur, pid_v, tid_v, cat, name, names,
+                               corr, has_corr, trace.processes, _source=trace)
+
+    @classmethod
+    def from_arrays(cls, clock_domain, start, dur, pid_values, tid_values, cat, name, names,
+                    corr=None, has_corr=None, processes=(), _source=None) -> "ColumnarTrace":
+        """Build from raw columns: pid/tid are *values*, name are ranks into
+        ``names`` (which must be sorted)."""
+        n = int(np.asarray(start).shape[0])
+        start = np.ascontiguousarray(start, dtype=np.int64)
+        dur = np.ascontiguousarray(dur, dtype=np.int64)
+        pid_values = np.asarray(pid_values, dtype=np.int64)
+        tid_values = np.asarray(tid_values, dtype=np.int64)
+        meta_pids = np.array(sorted({m.pid for m in processes}), dtype=np.int64)
+        pids = np.union1d(np.unique(pid_values), meta_pids).astype(np.int64)
+        pid = np.searchsorted(pids, pid_values).astype(np.int32)
+        if n:
+            pairs = np.stack([pid.astype(np.int64), tid_values], axis=1)
+            uniq, inv = np.unique(pairs, axis=0, return_inverse=True)
+            group_pid = uniq[:, 0].astype(np.int32)
+            group_tid = uniq[:, 1].astype(np.int64)
+            tid = inv.reshape(-1).astype(np.int32)
+        else:
+            group_pid = np.zeros(0, np.int32)
+            group_tid = np.zeros(0, np.int64)
+            tid = np.zeros(0, np.int32)
+        if corr is None:
+            corr = np.zeros(n, np.int64)
+            has_corr = np.zeros(n, np.uint8)
+        return cls(clock_domain, start, dur, pid, tid,
+                   np.ascontiguousarray(cat, dtype=np.uint8),
+                   np.ascontiguousarray(name, dtype=np.int32),
+                   np.ascontiguousarray(corr, dtype=np.int64),
+                   np.ascontiguousarray(has_corr, dtype=np.uint8),
+                   pids, group_pid, group_tid, list(names), tuple(processes), _source=_source)
+
+    # -- conversion back ------------------------------------------------------
+    def pid_value(self, idx: int) -> int:
+        return int(self.pids[idx])
+
+    def to_events(self, start: Optional[np.ndarray] = None, dur: Optional[np.ndarray] = None) -> list:
+        start = self.start if start is None else start
+        dur = self.dur if dur is None else dur
+        pid_v = self.pids[self.pid].tolist()
+        tid_v = self.group_tid[self.tid].tolist()
+        names = self.names
+        nm = [names[i] for i in self.name.tolist()]
+        cats = [Category(c) for c in range(6)]
+        cat = [cats[c] for c in self.cat.tolist()]
+        corr = [c if h else None for c, h in zip(self.corr.tolist(), self.has_corr.tolist())]
+        return [Event(p, t, c, s_name, s, d, k) for p, t, c, s_name, s, d, k in
+                zip(pid_v, tid_v, cat, nm, start.tolist(), dur.tolist(), corr)]
+
+    def to_trace(self, start=None, dur=None, processes: Optional[Sequence[ProcessMeta]] = None) -> Trace:
+        return Trace(self.clock_domain, self.to_events(start, dur),
+                     self.processes if processes is None else processes)
+
+    def select_pids(self, pid_indices) -> "ColumnarTrace":
+        """Sub-trace holding only the given pid indices (keeps every table, so
+        pid/tid/name indices stay valid); used for sharding."""
+        keep = np.isin(self.pid, np.asarray(pid_indices, dtype=np.int32))
+        return ColumnarTrace(self.clock_domain, self.start[keep], self.dur[keep], self.pid[keep],
+                             self.tid[keep], self.cat[keep], self.name[keep], self.corr[keep],
+                             self.has_corr[keep], self.pids, self.group_pid, self.group_tid,
+                             self.names, self.processes, self.pid_has_meta)
