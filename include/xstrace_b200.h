@@ -1,0 +1,155 @@
+/*
+ * xstrace_b200.h -- C ABI of the B200-native trace-analysis hot path.
+ *
+ * This is the drop-in boundary: the reference (RL-Scope / xstrace) is a
+ * Python package whose hot path is
+ *     compute_overlap(trace, attribution)    pkg/src/xstrace/overlap.py:106
+ *     correct_trace(trace, profile)          pkg/src/xstrace/correction.py:115
+ *     transition_sites(trace)                pkg/src/xstrace/overlap.py:263
+ *     count_transitions(trace)               pkg/src/xstrace/overlap.py:292
+ *     validate_trace / require_valid         pkg/src/xstrace/model.py:159,231
+ * with its only native plugin point the per-pid sweep kernel
+ *     sweep_pid(...)                         pkg/src/xstrace/_sweep.pyx:17
+ * (selected at overlap.py:30-38 via the ``kernel=`` argument).  The Python
+ * host package (paper_2102_04285_b200) keeps that API and binds these entry
+ * points with ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - All array pointers inside xs_events_t are DEVICE pointers owned by the
+ *     caller (the library never frees them).  Outputs named *_dev are device
+ *     buffers allocated by the caller; everything else is host memory.
+ *   - Every entry point is stream-ordered on `stream` and returns an
+ *     xs_status (0 = ok).  Intermediate buffers live in the context's
+ *     workspace, which grows on demand and is reused across calls.
+ *   - Status codes map 1:1 to the reference's exceptions:
+ *       XS_INVALID_TRACE -> InvalidTraceError   (model.py:115-122)
+ *       XS_UNCALIBRATED  -> UncalibratedHookError (correction.py:38-39)
+ *       XS_BAD_ARGUMENT  -> ValueError
+ */
+#ifndef XSTRACE_B200_H
+#define XSTRACE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct xs_ctx xs_ctx_t;
+typedef void* xs_stream_t; /* cudaStream_t */
+
+typedef enum {
+  XS_OK = 0,
+  XS_INVALID_TRACE = 1,
+  XS_UNCALIBRATED = 2,
+  XS_CUDA_ERROR = 3,
+  XS_BAD_ARGUMENT = 4,
+  XS_UNSUPPORTED = 5,
+  XS_NO_MEMORY = 6
+} xs_status;
+
+/* Columnar events (see paper_2102_04285_b200/columnar.py for the interning
+ * rules that make integer compares equal the reference's Python compares). */
+typedef struct {
+  int64_t n;                  /* number of events (rows, trace order)       */
+  const int64_t* start;       /* [n] ns                                      */
+  const int64_t* dur;         /* [n] ns                                      */
+  const int32_t* pid;         /* [n] dense pid index                         */
+  const int32_t* tid;         /* [n] dense (pid, tid) group index            */
+  const uint8_t* cat;         /* [n] Category 0..5                           */
+  const int32_t* name;        /* [n] rank in the sorted name table           */
+  const int64_t* corr;        /* [n] correlation id                          */
+  const uint8_t* has_corr;    /* [n] 1 when correlation is not None          */
+  int32_t n_pids;
+  int32_t n_groups;
+  int32_t n_names;
+  int32_t reserved;
+  const int32_t* group_pid;   /* [n_groups] pid index of each group          */
+  const uint8_t* pid_has_meta;/* [n_pids] pid has a ProcessMeta              */
+} xs_events_t;
+
+/* Calibration profile as exact integers over one common denominator L
+ * (fractions.Fraction in the reference, calibration.py:142-149). */
+typedef struct {
+  int64_t L;
+  int64_t ann_start;          /* annotation/2 * L            (ANN_START)   */
+  int64_t ann_end;            /* (annotation - annotation/2) * L (ANN_END) */
+  int64_t transition;         /* transition * L                            */
+  int64_t interception;       /* api_interception * L                      */
+  const int64_t* internal;    /* DEVICE [n_names] api_internal[name] * L   */
+  const uint8_t* has_internal;/* DEVICE [n_names]                          */
+} xs_profile_t;
+
+/* Sizes of the last overlap result held by the context. */
+typedef struct {
+  int64_t n_cells;
+  int32_t n_nodes;            /* path trie nodes; node 0 = empty path     */
+  int32_t n_pids;
+} xs_overlap_info_t;
+
+typedef struct {
+  int64_t original_total;     /* CorrectionReport.original_total_ns  */
+  int64_t corrected_total;    /* CorrectionReport.corrected_total_ns */
+  int64_t n_sites;
+  int64_t n_slabs;
+} xs_correct_info_t;
+
+const char* xs_status_str(int status);
+const char* xs_last_error(xs_ctx_t* ctx);
+int xs_version(void);
+
+int xs_ctx_create(int device, xs_ctx_t** out);
+void xs_ctx_destroy(xs_ctx_t* ctx);
+/* bytes currently held by the context workspace */
+int64_t xs_ctx_workspace_bytes(xs_ctx_t* ctx);
+
+/* validate_trace event rules (model.py:159-228) as one device pass plus the
+ * OPERATION nesting check; *n_bad = number of event-level violations found
+ * (0 => valid).  Process-metadata rules are O(#pids) and stay on the host. */
+int xs_validate(xs_ctx_t* ctx, const xs_events_t* ev, int64_t* n_bad, xs_stream_t stream);
+
+/* compute_overlap (overlap.py:106-188).  attribution: 0 INSTANT, 1 CORRELATION.
+ * Results stay in the context until the next call; fetch with
+ * xs_overlap_info / xs_overlap_fetch. */
+int xs_overlap(xs_ctx_t* ctx, const xs_events_t* ev, int attribution, xs_stream_t stream);
+int xs_overlap_info(xs_ctx_t* ctx, xs_overlap_info_t* info);
+/* host outputs: cells (n_cells each), trie (n_nodes each), per-pid arrays (n_pids each) */
+int xs_overlap_fetch(xs_ctx_t* ctx, int32_t* cell_pid, int32_t* cell_node, int32_t* cell_mask,
+                     int64_t* cell_ns, int32_t* node_parent, int32_t* node_name, int64_t* span_lo,
+                     int64_t* span_hi, int64_t* tracked, uint8_t* has_events, xs_stream_t stream);
+
+/* correct_trace (correction.py:115-186): writes corrected start/duration in
+ * trace order to caller device buffers; per-pid removed/shortfall via
+ * xs_correct_report.  *bad_event receives the first ACCEL_API event index
+ * whose name the profile lacks when XS_UNCALIBRATED is returned. */
+int xs_correct(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof,
+               int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, xs_stream_t stream);
+/* removed/shortfall: host [n_pids*4] in HOOK_KINDS order */
+int xs_correct_report(xs_ctx_t* ctx, xs_correct_info_t* info, int64_t* removed, int64_t* shortfall,
+                      xs_stream_t stream);
+/* RemovalMap of the last xs_correct applied to (pid, value) pairs (fork/join
+ * remap, correction.py:166-182); all three arrays are device pointers. */
+int xs_remap(xs_ctx_t* ctx, int64_t n, const int32_t* pid_dev, const int64_t* val_dev,
+             int64_t* out_dev, xs_stream_t stream);
+
+/* correct_trace + compute_overlap(corrected): the `xstrace analyze --profile`
+ * path (cli.py:168-171) in one call; results as for the two calls above. */
+int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
+               int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, xs_stream_t stream);
+
+/* transition_sites (overlap.py:263-289) for the pairs selected by pair_mask
+ * (bit k = TRANSITION_PAIRS[k]).  *n_out = number of sites; fetch the
+ * (pair, event index) list, ordered per pair by Event.sort_key. */
+int xs_transition_sites(xs_ctx_t* ctx, const xs_events_t* ev, int pair_mask, int64_t* n_out,
+                        xs_stream_t stream);
+int xs_transition_fetch(xs_ctx_t* ctx, int32_t* pair, int64_t* event, xs_stream_t stream);
+
+/* Number of kernel launches issued by the library since context creation
+ * (instrumentation for the bench's gpu_launches field). */
+int64_t xs_launch_count(xs_ctx_t* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,288 @@
+"""Device session: uploads columnar traces and drives the C ABI.
+
+PyTorch is used only for device memory and the current CUDA stream; all
+analysis runs in ``libxstrace_b200.so`` (hand-written sm_100a kernels).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .columnar import ColumnarTrace
+
+_engines: dict = {}
+_lock = threading.Lock()
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("xstrace-b200 needs a CUDA device (B200); none is visible")
+    return torch
+
+
+class DeviceTrace:
+    """Columns of a ColumnarTrace resident in device memory."""
+
+    def __init__(self, ct: ColumnarTrace, device: int = 0, non_blocking: bool = False):
+        torch = _torch()
+        dev = torch.device("cuda", device)
+        self.ct = ct
+        self.device = device
+
+        def up(a, dtype):
+            a = np.ascontiguousarray(a, dtype=dtype)
+            if a.size == 0:
+                return torch.zeros(1, dtype=_TORCH[dtype], device=dev)
+            return torch.from_numpy(a).to(dev, non_blocking=non_blocking)
+
+        self.start = up(ct.start, np.int64)
+        self.dur = up(ct.dur, np.int64)
+        self.pid = up(ct.pid, np.int32)
+        self.tid = up(ct.tid, np.int32)
+        self.cat = up(ct.cat, np.uint8)
+        self.name = up(ct.name, np.int32)
+        self.corr = up(ct.corr, np.int64)
+        self.has_corr = up(ct.has_corr, np.uint8)
+        self.group_pid = up(ct.group_pid, np.int32)
+        self.pid_has_meta = up(ct.pid_has_meta, np.uint8)
+
+    @classmethod
+    def from_tensors(cls, ct: ColumnarTrace, tensors: dict, device: int = 0) -> "DeviceTrace":
+        obj = cls.__new__(cls)
+        obj.ct = ct
+        obj.device = device
+        for k, v in tensors.items():
+            setattr(obj, k, v)
+        return obj
+
+    def h2d_bytes(self) -> int:
+        return sum(int(t.numel() * t.element_size()) for t in
+                   (self.start, self.dur, self.pid, self.tid, self.cat, self.name, self.corr, self.has_corr,
+                    self.group_pid, self.pid_has_meta))
+
+    def struct(self, start=None, dur=None) -> _lib.XsEvents:
+        ct = self.ct
+        s = self.start if start is None else start
+        d = self.dur if dur is None else dur
+        return _lib.XsEvents(ct.n, s.data_ptr(), d.data_ptr(), self.pid.data_ptr(), self.tid.data_ptr(),
+                             self.cat.data_ptr(), self.name.data_ptr(), self.corr.data_ptr(),
+                             self.has_corr.data_ptr(), ct.n_pids, ct.n_groups, len(ct.names), 0,
+                             self.group_pid.data_ptr(), self.pid_has_meta.data_ptr())
+
+
+_TORCH = {}
+
+
+def _init_torch_types():
+    import torch
+
+    _TORCH.update({np.int64: torch.int64, np.int32: torch.int32, np.uint8: torch.uint8})
+
+
+class XsError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        self.status = status
+        super().__init__(message)
+
+
+@dataclass
+class OverlapRaw:
+    cell_pid: np.ndarray
+    cell_node: np.ndarray
+    cell_mask: np.ndarray
+    cell_ns: np.ndarray
+    node_parent: np.ndarray
+    node_name: np.ndarray
+    span_lo: np.ndarray
+    span_hi: np.ndarray
+    tracked: np.ndarray
+    has_events: np.ndarray
+
+
+@dataclass
+class CorrectRaw:
+    start: object  # device tensor
+    dur: object
+    removed: np.ndarray     # [n_pids, 4]
+    shortfall: np.ndarray   # [n_pids, 4]
+    original_total: int
+    corrected_total: int
+    n_sites: int
+    n_slabs: int
+
+
+class Engine:
+    """One C-ABI context per device (workspace reused across calls)."""
+
+    def __init__(self, device: int = 0):
+        _torch()
+        if not _TORCH:
+            _init_torch_types()
+        self.lib = _lib.load()
+        self.device = device
+        h = C.c_void_p()
+        st = self.lib.xs_ctx_create(device, C.byref(h))
+        if st != 0:
+            raise RuntimeError(f"xs_ctx_create failed: {self.lib.xs_status_str(st).decode()}")
+        self.ctx = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None):
+                self.lib.xs_ctx_destroy(self.ctx)
+                self.ctx = None
+        except Exception:
+            pass
+
+    # -- helpers ---------------------------------------------------------------
+    def stream(self):
+        torch = _torch()
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def check(self, st: int, what: str):
+        if st != 0:
+            msg = self.lib.xs_last_error(self.ctx).decode(errors="replace")
+            raise XsError(st, f"{what}: {self.lib.xs_status_str(st).decode()} {msg}".strip())
+
+    def launches(self) -> int:
+        return int(self.lib.xs_launch_count(self.ctx))
+
+    # -- entry points ------------------------------------------------------------
+    def validate(self, dt: DeviceTrace) -> int:
+        ev = dt.struct()
+        bad = C.c_int64(0)
+        self.check(self.lib.xs_validate(self.ctx, C.byref(ev), C.byref(bad), self.stream()), "xs_validate")
+        return int(bad.value)
+
+    def overlap(self, dt: DeviceTrace, attribution: int, start=None, dur=None) -> OverlapRaw:
+        ev = dt.struct(start, dur)
+        self.check(self.lib.xs_overlap(self.ctx, C.byref(ev), attribution, self.stream()), "xs_overlap")
+        return self.fetch_overlap()
+
+    def fetch_overlap(self) -> OverlapRaw:
+        info = _lib.XsOverlapInfo()
+        self.check(self.lib.xs_overlap_info(self.ctx, C.byref(info)), "xs_overlap_info")
+        nc, nn, np_ = int(info.n_cells), int(info.n_nodes), int(info.n_pids)
+        r = OverlapRaw(np.zeros(nc, np.int32), np.zeros(nc, np.int32), np.zeros(nc, np.int32),
+                       np.zeros(nc, np.int64), np.zeros(nn, np.int32), np.zeros(nn, np.int32),
+                       np.zeros(np_, np.int64), np.zeros(np_, np.int64), np.zeros(np_, np.int64),
+                       np.zeros(np_, np.uint8))
+
+        def p(a):
+            return a.ctypes.data if a.size else None
+
+        self.check(self.lib.xs_overlap_fetch(self.ctx, p(r.cell_pid), p(r.cell_node), p(r.cell_mask), p(r.cell_ns),
+                                             p(r.node_parent), p(r.node_name), p(r.span_lo), p(r.span_hi),
+                                             p(r.tracked), p(r.has_events), self.stream()), "xs_overlap_fetch")
+        return r
+
+    def _profile(self, dt: DeviceTrace, scaled):
+        torch = _torch()
+        dev = torch.device("cuda", self.device)
+        n_names = max(len(dt.ct.names), 1)
+        internal = torch.zeros(n_names, dtype=torch.int64, device=dev)
+        has = torch.zeros(n_names, dtype=torch.uint8, device=dev)
+        if len(dt.ct.names):
+            internal.copy_(torch.from_numpy(np.ascontiguousarray(scaled.internal, np.int64)))
+            has.copy_(torch.from_numpy(np.ascontiguousarray(scaled.has_internal, np.uint8)))
+        prof = _lib.XsProfile(scaled.L, scaled.ann_start, scaled.ann_end, scaled.transition, scaled.interception,
+                              internal.data_ptr(), has.data_ptr())
+        return prof, (internal, has)
+
+    def correct(self, dt: DeviceTrace, scaled, analyze_attribution: Optional[int] = None) -> CorrectRaw:
+        torch = _torch()
+        dev = torch.device("cuda", self.device)
+        n = max(dt.ct.n, 1)
+        out_s = torch.empty(n, dtype=torch.int64, device=dev)
+        out_d = torch.empty(n, dtype=torch.int64, device=dev)
+        ev = dt.struct()
+        prof, keep = self._profile(dt, scaled)
+        bad = C.c_int64(-1)
+        if analyze_attribution is None:
+            st = self.lib.xs_correct(self.ctx, C.byref(ev), C.byref(prof), out_s.data_ptr(), out_d.data_ptr(),
+                                     C.byref(bad), self.stream())
+        else:
+            st = self.lib.xs_analyze(self.ctx, C.byref(ev), C.byref(prof), analyze_attribution, out_s.data_ptr(),
+                                     out_d.data_ptr(), C.byref(bad), self.stream())
+        if st == _lib.XS_UNCALIBRATED:
+            raise UncalibratedEvent(int(bad.value))
+        self.check(st, "xs_correct")
+        del keep
+        P = dt.ct.n_pids
+        removed = np.zeros(max(P, 1) * 4, np.int64)
+        shortfall = np.zeros(max(P, 1) * 4, np.int64)
+        info = _lib.XsCorrectInfo()
+        self.check(self.lib.xs_correct_report(self.ctx, C.byref(info), removed.ctypes.data, shortfall.ctypes.data,
+                                              self.stream()), "xs_correct_report")
+        return CorrectRaw(out_s[: dt.ct.n], out_d[: dt.ct.n], removed[: P * 4].reshape(P, 4),
+                          shortfall[: P * 4].reshape(P, 4), int(info.original_total), int(info.corrected_total),
+                          int(info.n_sites), int(info.n_slabs))
+
+    def remap(self, pid_idx: np.ndarray, values: np.ndarray) -> np.ndarray:
+        torch = _torch()
+        dev = torch.device("cuda", self.device)
+        if len(values) == 0:
+            return np.zeros(0, np.int64)
+        p = torch.from_numpy(np.ascontiguousarray(pid_idx, np.int32)).to(dev)
+        v = torch.from_numpy(np.ascontiguousarray(values, np.int64)).to(dev)
+        out = torch.empty_like(v)
+        self.check(self.lib.xs_remap(self.ctx, len(values), p.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                     self.stream()), "xs_remap")
+        return out.cpu().numpy()
+
+    def transition_sites(self, dt: DeviceTrace, pair_mask: int):
+        ev = dt.struct()
+        n = C.c_int64(0)
+        self.check(self.lib.xs_transition_sites(self.ctx, C.byref(ev), pair_mask, C.byref(n), self.stream()),
+                   "xs_transition_sites")
+        k = int(n.value)
+        pair = np.zeros(max(k, 1), np.int32)
+        event = np.zeros(max(k, 1), np.int64)
+        self.check(self.lib.xs_transition_fetch(self.ctx, pair.ctypes.data, event.ctypes.data, self.stream()),
+                   "xs_transition_fetch")
+        return pair[:k], event[:k]
+
+
+class UncalibratedEvent(Exception):
+    def __init__(self, index: int):
+        self.index = index
+        super().__init__(index)
+
+
+def get(device: int = 0) -> Engine:
+    with _lock:
+        eng = _engines.get(device)
+        if eng is None:
+            eng = Engine(device)
+            _engines[device] = eng
+        return eng
+
+
+def validate(trace) -> list:
+    """validate_trace: device flag first, reference-style list on the error path."""
+    from .model import format_violations, meta_violations
+
+    if meta_violations(trace.processes):
+        return format_violations(trace)
+    ct = trace if isinstance(trace, ColumnarTrace) else ColumnarTrace.from_trace(trace)
+    eng = get()
+    dt = DeviceTrace(ct, eng.device)
+    try:
+        bad = eng.validate(dt)
+    except XsError as exc:
+        if exc.status == _lib.XS_INVALID_TRACE:
+            bad = 1
+        else:
+            raise
+    if bad == 0:
+        return []
+    src = trace if not isinstance(trace, ColumnarTrace) else ct.to_trace()
+    return format_violations(src)

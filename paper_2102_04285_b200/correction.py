@@ -1,0 +1,157 @@
+"""Overhead correction by timeline surgery (drop-in for
+``pkg/src/xstrace/correction.py``).
+
+``correct_trace`` keeps the reference's signature, output and errors; the
+pipeline (transition sites, hook sites, exact rational quantization, budget
+caps, the (max,+) RemovalMap scan and the per-event remap) runs on the GPU
+(csrc/xs_correct.cu).  ``correct_trace_columnar`` and ``analyze_columnar``
+are the columnar fast paths (the latter is ``xstrace analyze --profile``:
+correction followed by overlap of the corrected trace, cli.py:168-171).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _engine, _lib
+from .calibration import HOOK_KINDS, CalibrationProfile
+from .columnar import ColumnarTrace
+from .model import Event, InvalidTraceError, ProcessMeta, Trace, format_violations, meta_violations
+
+
+class UncalibratedHookError(ValueError):
+    """The trace contains a hook kind the profile does not cover (correction.py:38-39)."""
+
+
+@dataclass
+class CorrectionReport:
+    """Accounting for one correction pass (correction.py:42-60)."""
+
+    removed_ns: dict = field(default_factory=dict)
+    shortfall_ns: dict = field(default_factory=dict)
+    original_total_ns: int = 0
+    corrected_total_ns: int = 0
+    bias: Optional[float] = None
+
+    def removed_total(self, pid: Optional[int] = None) -> int:
+        pids = [pid] if pid is not None else list(self.removed_ns)
+        return sum(sum(self.removed_ns[p].values()) for p in pids)
+
+
+def correction_bias(corrected_total: int, uninstrumented_total: int) -> float:
+    """Signed deviation of the corrected total from uninstrumented reality (correction.py:63-67)."""
+    if uninstrumented_total <= 0:
+        raise ValueError(f"uninstrumented_total must be > 0, got {uninstrumented_total}")
+    return (corrected_total - uninstrumented_total) / uninstrumented_total
+
+
+def _source(trace, ct):
+    if not isinstance(trace, ColumnarTrace):
+        return trace
+    return ct._source if ct._source is not None else ct.to_trace()
+
+
+def _run(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: Optional[int] = None,
+         device_trace=None):
+    if meta_violations(ct.processes):
+        raise InvalidTraceError(format_violations(_source(src, ct)))
+    scaled = profile.scaled(ct.names)
+    scaled.check_int128(3 * ct.n + 8)
+    eng = _engine.get()
+    dt = device_trace if device_trace is not None else _engine.DeviceTrace(ct, eng.device)
+    try:
+        raw = eng.correct(dt, scaled, attribution)
+    except _engine.UncalibratedEvent as exc:
+        name = ct.names[int(ct.name[exc.index])]
+        raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile") from None
+    except _engine.XsError as exc:
+        if exc.status == _lib.XS_INVALID_TRACE:
+            raise InvalidTraceError(format_violations(_source(src, ct))) from None
+        raise
+    return eng, dt, raw
+
+
+def _report(ct: ColumnarTrace, raw) -> CorrectionReport:
+    rep = CorrectionReport()
+    present = np.zeros(ct.n_pids, bool)
+    if ct.n:
+        present[np.unique(ct.pid)] = True
+    pids = ct.pids.tolist()
+    for p in range(ct.n_pids):
+        if present[p]:
+            rep.removed_ns[pids[p]] = dict(zip(HOOK_KINDS, raw.removed[p].tolist()))
+            rep.shortfall_ns[pids[p]] = dict(zip(HOOK_KINDS, raw.shortfall[p].tolist()))
+    rep.original_total_ns = raw.original_total
+    rep.corrected_total_ns = raw.corrected_total
+    return rep
+
+
+def _remap_processes(eng, ct: ColumnarTrace) -> tuple:
+    present = set(np.unique(ct.pid).tolist()) if ct.n else set()
+    pid_index = {int(p): i for i, p in enumerate(ct.pids.tolist())}
+    q_pid, q_val, slots = [], [], []
+    for k, m in enumerate(ct.processes):
+        idx = pid_index.get(m.pid)
+        if idx is None or idx not in present:
+            continue
+        for which, v in (("fork_ns", m.fork_ns), ("join_ns", m.join_ns)):
+            if v is not None:
+                q_pid.append(idx)
+                q_val.append(v)
+                slots.append((k, which))
+    out = eng.remap(np.array(q_pid, np.int32), np.array(q_val, np.int64)) if q_val else []
+    new = {}
+    for (k, which), v in zip(slots, list(out)):
+        new.setdefault(k, {})[which] = int(v)
+    procs = []
+    for k, m in enumerate(ct.processes):
+        if k in new:
+            procs.append(ProcessMeta(m.pid, m.name, m.parent, new[k].get("fork_ns", m.fork_ns),
+                                     new[k].get("join_ns", m.join_ns)))
+        else:
+            procs.append(m)
+    return tuple(procs)
+
+
+def correct_trace_columnar(ct: ColumnarTrace, profile: CalibrationProfile, device_trace=None,
+                           _src=None) -> tuple:
+    """Columnar correct_trace: returns (corrected ColumnarTrace, CorrectionReport)."""
+    eng, dt, raw = _run(ct, profile, _src if _src is not None else ct, None, device_trace)
+    procs = _remap_processes(eng, ct)
+    start = raw.start.cpu().numpy()
+    dur = raw.dur.cpu().numpy()
+    out = ColumnarTrace(ct.clock_domain, start, dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr,
+                        ct.pids, ct.group_pid, ct.group_tid, ct.names, procs, ct.pid_has_meta)
+    return out, _report(ct, raw)
+
+
+def correct_trace(trace, profile: CalibrationProfile) -> tuple:
+    """Remove calibrated overhead at every hook site; returns (trace, report).
+
+    The output keeps the input's event order; GPU events shift without
+    shrinking; fork/join timestamps are remapped with their process.
+    """
+    ct = trace if isinstance(trace, ColumnarTrace) else ColumnarTrace.from_trace(trace)
+    out, rep = correct_trace_columnar(ct, profile, _src=trace)
+    if isinstance(trace, ColumnarTrace):
+        return out, rep
+    events = [Event(e.pid, e.tid, e.category, e.name, s, d, e.correlation)
+              for e, s, d in zip(trace.events, out.start.tolist(), out.dur.tolist())]
+    return Trace(trace.clock_domain, events, out.processes), rep
+
+
+def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution=None, device_trace=None):
+    """``xstrace analyze --profile``: correct, then compute_overlap(corrected).
+
+    Returns (corrected start tensor, corrected duration tensor, report,
+    Breakdown).  One device call (xs_analyze) runs both stages.
+    """
+    from .overlap import Attribution, decode_breakdown
+
+    attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
+    eng, dt, raw = _run(ct, profile, ct, attr, device_trace)
+    bd = decode_breakdown(ct, eng.fetch_overlap())
+    return raw.start, raw.dur, _report(ct, raw), bd

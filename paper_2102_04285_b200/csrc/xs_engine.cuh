@@ -1,0 +1,237 @@
+// xs_engine.cuh -- context, workspace and the host-side pipeline contracts.
+#pragma once
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "xs_common.cuh"
+
+namespace xs {
+
+// Device-side counters filled by the scan passes, copied to pinned host
+// memory at the few points where the host has to size the next stage.
+struct Stats {
+  long long n_bad;          // event-rule + dangling-correlation + nesting violations
+  long long n_nonzero;      // events with duration > 0
+  long long n_ops_nz;       // OPERATION events with duration > 0
+  long long n_ops;          // all OPERATION events
+  long long n_api;          // ACCEL_API events
+  long long n_api_corr;     // ACCEL_API events with a correlation
+  long long n_gpu_corr;     // GPU events with a correlation
+  long long max_span;       // max over pids of (hi - lo)
+  long long bad_api;        // first ACCEL_API index missing from the profile
+  long long max_depth;      // deepest OPERATION nesting (per tid)
+  long long table_full;     // a hash table ran out of slots
+  long long multi_op_pids;  // pids whose OPERATIONs sit on >1 tid
+  long long n_trans;        // wrapper transition sites
+  long long n_sites;        // correction hook sites
+  long long depth_overflow; // merged multi-tid path deeper than the local limit
+  long long n_fixed;        // CORRELATION: GPU events with a fixed path
+  long long n_pieces;       // CORRELATION: own-path pieces
+  long long pad[15];
+};
+
+enum Slot : int {
+  W_STATS = 0,
+  W_SPAN_LO, W_SPAN_HI, W_PID_OPS, W_GROUP_OPS, W_PID_GROUP0,
+  W_CORR_STATE, W_CORR_KEY, W_CORR_PID, W_CORR_START,
+  W_OP_EV, W_OPK0, W_OPK1, W_OPV0, W_OPV1,
+  W_SKEY, W_SVAL, W_SKEY_ALT, W_SVAL_ALT,
+  W_DEPTH_SCAN_DESC, W_DEPTH_SCAN_FLAGS, W_TILE_CTR,
+  W_DOPEN, W_POPEN, W_DCLOSE, W_PARENT, W_NODE, W_READY, W_DKEY, W_DVAL, W_DKEY_ALT, W_DVAL_ALT,
+  W_TRIE_KEYS, W_TRIE_VALS, W_TRIE_PARENT, W_TRIE_NAME, W_TRIE_COUNT,
+  W_GS_OFF, W_PK, W_PK_ALT, W_PIDPATH, W_OPBASE,
+  W_MKEY, W_MKEY_ALT, W_MSCAN_DESC, W_MSCAN_FLAGS,
+  W_HIST, W_CELL_PID, W_CELL_NODE, W_CELL_MASK, W_CELL_NS, W_CELL_COUNT, W_TRACKED,
+  W_CUB_TEMP,
+  // correction
+  W_TQ_KEY, W_TQ_VAL, W_TQ_KEY_ALT, W_TQ_VAL_ALT, W_TSCAN_DESC, W_TSCAN_FLAGS, W_THEAD, W_TSTAT,
+  W_SITE_FLAG, W_SITE_CNT, W_SITE_POS, W_SITE_K, W_SITE_V, W_SITE_K_ALT, W_SITE_V_ALT,
+  W_QSCAN_DESC, W_QSCAN_FLAGS, W_QSLOT, W_LENSLOT, W_REMOVED, W_SHORTFALL,
+  W_RSCAN_DESC, W_RSCAN_FLAGS, W_SLAB_A, W_SLAB_B, W_SLAB_PRE, W_SLAB_CNT, W_SLAB_BASE,
+  W_SITES_LEN, W_TRANS_OUT_PAIR, W_TRANS_OUT_EV,
+  // correlation
+  W_FIXED_LS, W_FIXED_PATH, W_PIECE_KEY, W_FX_KEY, W_FX_KEY_ALT, W_FX_VAL, W_FX_VAL_ALT,
+  W_FXSCAN_DESC, W_FXSCAN_FLAGS, W_FX_OWN, W_RANK_EV,
+  W_NUM_SLOTS
+};
+
+// Lock-free (parent node, name) -> node table: the PathTable of
+// overlap.py:80-93 as a trie (a name tuple and its trie node are in
+// bijection, so ids are internal exactly as in the reference).
+struct TrieView {
+  uint64_t* keys;  // (parent << 32 | name), ~0 = empty
+  int* vals;       // node id, -1 until published
+  int* parent;     // [node_cap]
+  int* name;       // [node_cap]
+  int* count;      // number of nodes (root = 0 pre-created)
+  uint64_t mask;   // table capacity - 1
+  int node_cap;    // grow trigger: count >= node_cap
+  Stats* st;
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+// child of `parent` named `name`, collapsing an adjacent duplicate name
+// (_sweep_py.py:22-24).  Returns the node id (0 on table overflow, with
+// Stats.table_full raised so the host re-runs with a larger table).
+__device__ __forceinline__ int trie_intern(int parent, int name, const TrieView& t) {
+  if (parent > 0 && ((volatile int*)t.name)[parent] == name) return parent;
+  const uint64_t key = ((uint64_t)(uint32_t)parent << 32) | (uint32_t)name;
+  uint64_t h = mix64(key) & t.mask;
+  for (uint64_t probe = 0; probe <= t.mask; probe++) {
+    uint64_t k = ((volatile uint64_t*)t.keys)[h];
+    if (k == ~0ull) {
+      unsigned long long prev = atomicCAS((unsigned long long*)&t.keys[h], ~0ull, (unsigned long long)key);
+      if (prev == ~0ull) {
+        int id = atomicAdd(t.count, 1);
+        if (id >= t.node_cap) {
+          atomicAdd((unsigned long long*)&t.st->table_full, 1ull);
+          id = 0;
+        } else {
+          t.parent[id] = parent;
+          t.name[id] = name;
+        }
+        __threadfence();
+        atomicExch(&t.vals[h], id);
+        return id;
+      }
+      k = prev;
+    }
+    if (k == key) {
+      int id;
+      while ((id = ((volatile int*)t.vals)[h]) < 0) {
+      }
+      __threadfence();
+      return id;
+    }
+    h = (h + 1) & t.mask;
+  }
+  atomicAdd((unsigned long long*)&t.st->table_full, 1ull);
+  return 0;
+}
+
+// Results of stage_ops consumed by the sweep.
+struct OpsState {
+  int64_t m = 0;          // nonzero OPERATION events
+  int tb = 0;             // relative-time bits
+  const uint64_t* skeys = nullptr;  // per-group endpoint stream keys (group|t|open)
+  const uint32_t* svals = nullptr;  // rank of the op at each stream position
+  const int* rank_ev = nullptr;     // event row of each rank
+  const int* parent = nullptr;      // parent rank (-1 = none)
+  const int* node = nullptr;        // trie node of each rank's single-tid chain
+  const uint64_t* pk = nullptr;     // op endpoints in (pid, t) order (pid|t|open)
+  const int* pidpath = nullptr;     // path node after each run end of pk
+  const int64_t* opbase = nullptr;  // [n_pids+1] first pk index of each pid
+  TrieView trie{};
+};
+
+}  // namespace xs
+
+struct xs_ctx {
+  int device = 0;
+  std::string err;
+  std::vector<void*> ptr;
+  std::vector<size_t> cap;
+  xs::Stats* h_stats = nullptr;  // pinned
+  long long launches = 0;
+  // last overlap result
+  long long n_cells = 0;
+  int n_nodes = 0;
+  int res_pids = 0;
+  bool have_overlap = false;
+  // last correction
+  bool have_correct = false;
+  int corr_pids = 0;
+  long long corr_original_total = 0;
+  long long corr_corrected_total = 0;
+  long long corr_sites = 0;
+  long long corr_slabs = 0;
+  // last transitions
+  long long n_trans_out = 0;
+  int trie_cap_log2 = 12;
+  xs::OpsState ops;
+};
+
+namespace xs {
+
+struct Run {
+  xs_ctx* c;
+  cudaStream_t s;
+};
+
+#define XS_TRY(expr)                     \
+  do {                                   \
+    int _st = (expr);                    \
+    if (_st != XS_OK) return _st;        \
+  } while (0)
+
+#define XS_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      ctx->err = std::string(#expr) + ": " + cudaGetErrorString(_e);                   \
+      return XS_CUDA_ERROR;                                                            \
+    }                                                                                  \
+  } while (0)
+
+// launch bookkeeping: every kernel launch in the library goes through this
+#define XS_LAUNCH(ctx, kernel, grid, block, smem, stream, ...)                         \
+  do {                                                                                 \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                        \
+    (ctx)->launches++;                                                                 \
+    cudaError_t _e = cudaGetLastError();                                               \
+    if (_e != cudaSuccess) {                                                           \
+      (ctx)->err = std::string(#kernel) + ": " + cudaGetErrorString(_e);               \
+      return XS_CUDA_ERROR;                                                            \
+    }                                                                                  \
+  } while (0)
+
+// grow-only workspace slot
+int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out);
+template <class T>
+inline int ws(xs_ctx* ctx, int slot, size_t count, cudaStream_t s, T** out) {
+  void* p = nullptr;
+  int st = ws_get(ctx, slot, count * sizeof(T) + 16, s, &p);
+  *out = reinterpret_cast<T*>(p);
+  return st;
+}
+
+int fetch_stats(xs_ctx* ctx, cudaStream_t s);  // D2H of Stats + sync
+
+// stable radix sorts over [0, bits) (CUB onesweep bring-up backend)
+int sort_pairs_u64_u32(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals, uint32_t** vals_alt,
+                       int64_t n, int bits, cudaStream_t s);
+int sort_keys_u64(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, int64_t n, int bits, cudaStream_t s);
+
+// pipeline stages (defined in the .cu files)
+struct EventView {  // by value: columns are device pointers; start/dur may be overridden (corrected trace)
+  xs_events_t ev;
+  const int64_t* start;
+  const int64_t* dur;
+};
+
+int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr_table, bool check_api,
+                 const xs_profile_t* prof);
+int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths);
+int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
+int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mask, cudaStream_t s);
+int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start,
+                  int64_t* out_dur, bool corrected_spans, cudaStream_t s);
+
+inline OpsState& ctx_ops(xs_ctx* c) { return c->ops; }
+int trie_setup(xs_ctx* ctx, cudaStream_t s, TrieView* t);
+
+__global__ void k_iota_u32(uint32_t* v, int64_t n);
+
+int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_bad);
+int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
+
+}  // namespace xs

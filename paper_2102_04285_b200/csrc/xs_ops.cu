@@ -1,0 +1,529 @@
+// xs_ops.cu -- OPERATION machinery: ranks, nesting validation, path interning.
+//
+// Reference semantics:
+//   rank order  = (start, -end, tid, name), stable     overlap.py:96-99
+//   path at t   = dedupe(names of active ops in rank order)   _sweep_py.py:16-26
+//   nesting     = per (pid, tid) no partial overlap         model.py:137-156
+// Device formulation (all integer, parallel, exact):
+//   1. nonzero ops are ranked inside their (pid,tid) group by two stable radix
+//      passes: (desc end, name) then (group, start).  Row order = event index
+//      order, so stable ties follow the reference's stable sort.
+//   2. open/close endpoints per group sorted by (group, t, close<open), closes
+//      inner-first and opens outer-first => a balanced parenthesisation.  The
+//      prefix sum of +-1 is the depth; an op is properly nested iff its depth
+//      after close == depth after open - 1 (equivalent to the reference stack
+//      check).
+//   3. parent(op) = last open at depth-1 before it (binary search in the
+//      depth-sorted opens);  node(op) = trie child of node(parent) (dedupe of
+//      equal adjacent names), interned in a lock-free (parent,name) table by a
+//      dependency-ordered work queue (parents are always dequeued first).
+//   4. the path of every op segment (the state after all op endpoints at one
+//      instant of a pid) is node(innermost) when one tid carries ops, or the
+//      rank-merge of every tid's chain (interned root-down) otherwise.
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include "xs_engine.cuh"
+
+namespace xs {
+
+struct OpPred {
+  const uint8_t* cat;
+  const int64_t* dur;
+  __device__ bool operator()(const int& i) const { return cat[i] == 0 && dur[i] > 0; }
+};
+
+__global__ void k_rank_key1(const int* op_ev, const uint32_t* vals, int64_t m, EventView v, const int64_t* lo,
+                            int tb, int nb, uint64_t* keys) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  int i = op_ev[vals[q]];
+  int p = v.ev.pid[i];
+  uint64_t end_rel = (uint64_t)(v.start[i] + v.dur[i] - lo[p]);
+  uint64_t tmask = tb >= 64 ? ~0ull : ((1ull << tb) - 1);
+  uint64_t desc = tmask - end_rel;  // descending end
+  keys[q] = (desc << nb) | (uint64_t)v.ev.name[i];
+}
+
+__global__ void k_rank_key_name(const int* op_ev, const uint32_t* vals, int64_t m, EventView v, uint64_t* keys) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  keys[q] = (uint64_t)v.ev.name[op_ev[vals[q]]];
+}
+
+__global__ void k_rank_key_end(const int* op_ev, const uint32_t* vals, int64_t m, EventView v, const int64_t* lo,
+                               int tb, uint64_t* keys) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  int i = op_ev[vals[q]];
+  uint64_t end_rel = (uint64_t)(v.start[i] + v.dur[i] - lo[v.ev.pid[i]]);
+  uint64_t tmask = tb >= 64 ? ~0ull : ((1ull << tb) - 1);
+  keys[q] = tmask - end_rel;
+}
+
+__global__ void k_rank_key2(const int* op_ev, const uint32_t* vals, int64_t m, EventView v, const int64_t* lo,
+                            int tb, uint64_t* keys) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  int i = op_ev[vals[q]];
+  int p = v.ev.pid[i];
+  keys[q] = ((uint64_t)v.ev.tid[i] << tb) | (uint64_t)(v.start[i] - lo[p]);
+}
+
+// endpoint stream: slot m+r = open of rank r, slot m-1-r = close of rank r
+__global__ void k_endpoints(const int* op_ev, const uint32_t* ranked, int64_t m, EventView v, const int64_t* lo,
+                            int tb, uint64_t* keys, uint32_t* vals, int* rank_ev) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  int i = op_ev[ranked[r]];
+  rank_ev[r] = i;
+  int p = v.ev.pid[i];
+  uint64_t g = (uint64_t)v.ev.tid[i];
+  uint64_t s = (uint64_t)(v.start[i] - lo[p]);
+  uint64_t e = (uint64_t)(v.start[i] + v.dur[i] - lo[p]);
+  keys[m + r] = (g << (tb + 1)) | (s << 1) | 1ull;
+  vals[m + r] = (uint32_t)r;
+  keys[m - 1 - r] = (g << (tb + 1)) | (e << 1);
+  vals[m - 1 - r] = (uint32_t)r;
+}
+
+struct DepthDelta {
+  __device__ int operator()(const uint64_t& k) const { return (k & 1ull) ? 1 : -1; }
+};
+
+__global__ void k_depth_scatter(const uint64_t* keys, const uint32_t* vals, const int* depth, int64_t n2,
+                                int* d_open, int* pos_open, int* d_close) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n2) return;
+  uint32_t r = vals[j];
+  if (keys[j] & 1ull) {
+    d_open[r] = depth[j];
+    pos_open[r] = (int)j;
+  } else {
+    d_close[r] = depth[j];
+  }
+}
+
+__global__ void k_depth_check(const int* d_open, const int* d_close, int64_t m, Stats* st) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int bad = 0, mx = 0;
+  if (r < m) {
+    bad = d_close[r] != d_open[r] - 1;
+    mx = d_open[r];
+  }
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd((unsigned long long*)&st->n_bad, (unsigned long long)bad);
+    if (mx) atomicMax(&st->max_depth, (long long)mx);
+  }
+}
+
+__global__ void k_depth_keys(const int* d_open, const int* pos_open, int64_t m, uint64_t* dk, uint32_t* dv) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  dk[r] = (uint64_t)d_open[r];
+  dv[r] = (uint32_t)pos_open[r];
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t x) {
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if (a[m] < x) lo = m + 1;
+    else hi = m;
+  }
+  return lo;
+}
+
+__global__ void k_parent(const int* d_open, const int* pos_open, int64_t m, const uint64_t* dk, const uint32_t* dv,
+                         const uint32_t* svals, int* parent) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  int d = d_open[r];
+  if (d < 2) {
+    parent[r] = -1;
+    return;
+  }
+  int64_t a = lower_bound_u64(dk, 0, m, (uint64_t)(d - 1));
+  int64_t b = lower_bound_u64(dk, a, m, (uint64_t)d);
+  uint32_t pos = (uint32_t)pos_open[r];
+  // last q in [a, b) with dv[q] < pos
+  int64_t lo = a, hi = b;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (dv[mid] < pos) lo = mid + 1;
+    else hi = mid;
+  }
+  parent[r] = lo > a ? (int)svals[dv[lo - 1]] : -1;
+}
+
+// dependency-ordered interning of node(op) = child(node(parent), name)
+__global__ void k_nodes(int64_t m, int use_depth_order, const uint32_t* dv, const uint32_t* svals, const int* parent,
+                        const int* rank_ev, const int32_t* name, int* node, int* ready, int* counter, TrieView t) {
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(counter, 32);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= m) return;
+    int64_t q = base + lane;
+    bool done = q >= m;
+    int r = -1, p = -1, nm = 0;
+    if (!done) {
+      r = use_depth_order ? (int)svals[dv[q]] : (int)q;
+      p = parent[r];
+      nm = name[rank_ev[r]];
+    }
+    while (!__all_sync(0xffffffffu, done)) {
+      if (!done) {
+        int pn = 0;
+        bool ok = true;
+        if (p >= 0) {
+          ok = ((volatile int*)ready)[p] != 0;
+          if (ok) {
+            __threadfence();
+            pn = ((volatile int*)node)[p];
+          }
+        }
+        if (ok) {
+          int id = trie_intern(pn, nm, t);
+          node[r] = id;
+          __threadfence();
+          atomicExch(&ready[r], 1);
+          done = true;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int ctx_node_at(const uint64_t* skeys, const uint32_t* svals, int64_t j, const int* parent,
+                                           const int* node) {
+  uint32_t r = svals[j];
+  if (skeys[j] & 1ull) return node[r];
+  int p = parent[r];
+  return p >= 0 ? node[p] : 0;
+}
+
+// single-tid-per-pid case: pid order == group order
+__global__ void k_pidpath_simple(const uint64_t* skeys, const uint32_t* svals, int64_t n2, const int* parent,
+                                 const int* node, int* pidpath) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n2) return;
+  pidpath[j] = ctx_node_at(skeys, svals, j, parent, node);
+}
+
+__global__ void k_pid_keys(const uint64_t* skeys, int64_t n2, const int32_t* group_pid, int tb, uint64_t* pk) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n2) return;
+  uint64_t k = skeys[j];
+  uint64_t g = k >> (tb + 1);
+  uint64_t low = k & ((2ull << tb) - 1);
+  pk[j] = ((uint64_t)group_pid[g] << (tb + 1)) | low;
+}
+
+constexpr int MAXD = 256;
+
+// general case: rank-merge of every tid's chain at each run end of the pid order
+__global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const int* pid_group0, const int* group_ops,
+                                  const int64_t* gs_off, const uint64_t* skeys, const uint32_t* svals,
+                                  const int* parent, const int* node, const int* rank_ev, EventView v,
+                                  int* pidpath, TrieView t, Stats* st) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n2) return;
+  uint64_t key = pk[k] >> 1;
+  if (k + 1 < n2 && (pk[k + 1] >> 1) == key) {
+    pidpath[k] = 0;  // not a run end: never looked up
+    return;
+  }
+  const uint64_t tmask = (1ull << tb) - 1;
+  int p = (int)(key >> tb);
+  uint64_t tt = key & tmask;
+  int ctxs[64];
+  int nctx = 0;
+  int g0 = pid_group0[p], g1 = pid_group0[p + 1];
+  for (int g = g0; g < g1; g++) {
+    int cnt = group_ops[g];
+    if (!cnt) continue;
+    int64_t a = gs_off[g], b = a + 2 * (int64_t)cnt;
+    // last j in [a,b) with time <= tt
+    int64_t lo = a, hi = b;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (((skeys[mid] >> 1) & tmask) <= tt) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo == a) continue;
+    int64_t j = lo - 1;
+    uint32_t r = svals[j];
+    int o = (skeys[j] & 1ull) ? (int)r : parent[r];
+    if (o < 0) continue;
+    if (nctx == 64) {
+      atomicAdd((unsigned long long*)&st->depth_overflow, 1ull);
+      pidpath[k] = 0;
+      return;
+    }
+    ctxs[nctx++] = o;
+  }
+  if (nctx == 0) {
+    pidpath[k] = 0;
+    return;
+  }
+  if (nctx == 1) {
+    pidpath[k] = node[ctxs[0]];
+    return;
+  }
+  // gather all active ops (chains), sort by global rank order, intern root-down
+  int ops[MAXD];
+  int n = 0;
+  for (int c = 0; c < nctx; c++) {
+    for (int o = ctxs[c]; o >= 0; o = parent[o]) {
+      if (n == MAXD) {
+        atomicAdd((unsigned long long*)&st->depth_overflow, 1ull);
+        pidpath[k] = 0;
+        return;
+      }
+      ops[n++] = o;
+    }
+  }
+  // insertion sort by (start, -end, group, r) -- r orders (name, idx) within a group
+  for (int a = 1; a < n; a++) {
+    int x = ops[a];
+    int ix = rank_ev[x];
+    int64_t xs_ = v.start[ix], xe = v.start[ix] + v.dur[ix];
+    int xg = v.ev.tid[ix];
+    int b = a - 1;
+    while (b >= 0) {
+      int y = ops[b];
+      int iy = rank_ev[y];
+      int64_t ys = v.start[iy], ye = v.start[iy] + v.dur[iy];
+      int yg = v.ev.tid[iy];
+      bool greater = (ys != xs_) ? ys > xs_ : (ye != xe) ? ye < xe : (yg != xg) ? yg > xg : y > x;
+      if (!greater) break;
+      ops[b + 1] = y;
+      b--;
+    }
+    ops[b + 1] = x;
+  }
+  int cur = 0;
+  for (int a = 0; a < n; a++) cur = trie_intern(cur, v.ev.name[rank_ev[ops[a]]], t);
+  pidpath[k] = cur;
+}
+
+__global__ void k_trie_init(uint64_t* keys, int* vals, int64_t cap, int* parent, int* name, int* count) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cap) {
+    keys[i] = ~0ull;
+    vals[i] = -1;
+  }
+  if (i == 0) {
+    parent[0] = -1;
+    name[0] = -1;
+    *count = 1;
+  }
+}
+
+__global__ void k_opbase(const int* pid_ops, int np, int64_t* opbase) {
+  // tiny serial scan (np is the number of processes)
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t acc = 0;
+    for (int p = 0; p < np; p++) {
+      opbase[p] = acc;
+      acc += 2 * (int64_t)pid_ops[p];
+    }
+    opbase[np] = acc;
+  }
+}
+
+__global__ void k_gs_off(const int* group_ops, int ng, int64_t* gs_off) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t acc = 0;
+    for (int g = 0; g < ng; g++) {
+      gs_off[g] = acc;
+      acc += 2 * (int64_t)group_ops[g];
+    }
+    gs_off[ng] = acc;
+  }
+}
+
+__global__ void k_iota_u32(uint32_t* v, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (uint32_t)i;
+}
+
+int trie_setup(xs_ctx* ctx, cudaStream_t s, TrieView* t) {
+  int64_t cap = (int64_t)1 << ctx->trie_cap_log2;
+  uint64_t* keys;
+  int *vals, *parent, *name, *count;
+  XS_TRY(ws(ctx, W_TRIE_KEYS, cap, s, &keys));
+  XS_TRY(ws(ctx, W_TRIE_VALS, cap, s, &vals));
+  XS_TRY(ws(ctx, W_TRIE_PARENT, cap, s, &parent));
+  XS_TRY(ws(ctx, W_TRIE_NAME, cap, s, &name));
+  XS_TRY(ws(ctx, W_TRIE_COUNT, 4, s, &count));
+  XS_LAUNCH(ctx, k_trie_init, grid_for(cap), XS_BLOCK, 0, s, keys, vals, cap, parent, name, count);
+  t->keys = keys;
+  t->vals = vals;
+  t->parent = parent;
+  t->name = name;
+  t->count = count;
+  t->mask = (uint64_t)cap - 1;
+  t->node_cap = (int)(cap / 2);
+  t->st = (Stats*)ctx->ptr[W_STATS];
+  return XS_OK;
+}
+
+int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths) {
+  const Stats& H = *ctx->h_stats;
+  const int64_t m = H.n_ops_nz;
+  const int np = v.ev.n_pids, ng = v.ev.n_groups;
+  OpsState& os = ctx_ops(ctx);
+  os.m = m;
+  os.tb = bits_for((uint64_t)(H.max_span > 0 ? H.max_span : 0));
+  int64_t *lo = (int64_t*)ctx->ptr[W_SPAN_LO];
+  int* pid_ops = (int*)ctx->ptr[W_PID_OPS];
+  int* group_ops = (int*)ctx->ptr[W_GROUP_OPS];
+  Stats* st = (Stats*)ctx->ptr[W_STATS];
+  const int tb = os.tb;
+  const int gb = bits_for((uint64_t)(ng > 0 ? ng - 1 : 0));
+  const int pb = bits_for((uint64_t)(np > 0 ? np - 1 : 0));
+  const int nb = bits_for((uint64_t)(v.ev.n_names > 0 ? v.ev.n_names - 1 : 0));
+  int64_t* opbase;
+  XS_TRY(ws(ctx, W_OPBASE, np + 1, s, &opbase));
+  XS_LAUNCH(ctx, k_opbase, 1, 32, 0, s, pid_ops, np, opbase);
+  os.opbase = opbase;
+  os.pidpath = nullptr;
+  os.pk = nullptr;
+  if (m == 0) {
+    if (build_paths) XS_TRY(trie_setup(ctx, s, &os.trie));
+    return XS_OK;
+  }
+  if (gb + tb + 1 > 64 || pb + tb + 1 > 64) {
+    ctx->err = "timeline too wide for 64-bit endpoint keys";
+    return XS_UNSUPPORTED;
+  }
+  // 1. compact nonzero OPERATION rows (index order)
+  int* op_ev;
+  XS_TRY(ws(ctx, W_OP_EV, m + 1, s, &op_ev));
+  {
+    int* nsel;
+    XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &nsel));
+    OpPred pred{v.ev.cat, v.dur};
+    size_t temp = 0;
+    cub::CountingInputIterator<int> it(0);
+    XS_CUDA(cub::DeviceSelect::If(nullptr, temp, it, op_ev, nsel, (int)v.ev.n, pred, s));
+    void* t;
+    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
+    XS_CUDA(cub::DeviceSelect::If(t, temp, it, op_ev, nsel, (int)v.ev.n, pred, s));
+    ctx->launches += 2;
+  }
+  // 2. rank sort inside (pid, tid) groups
+  uint64_t *k0, *k1;
+  uint32_t *v0, *v1;
+  XS_TRY(ws(ctx, W_OPK0, 2 * m + 2, s, &k0));
+  XS_TRY(ws(ctx, W_OPK1, 2 * m + 2, s, &k1));
+  XS_TRY(ws(ctx, W_OPV0, 2 * m + 2, s, &v0));
+  XS_TRY(ws(ctx, W_OPV1, 2 * m + 2, s, &v1));
+  XS_LAUNCH(ctx, k_iota_u32, grid_for(m), XS_BLOCK, 0, s, v0, m);
+  if (tb + nb <= 64) {
+    XS_LAUNCH(ctx, k_rank_key1, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, lo, tb, nb, k0);
+    XS_TRY(sort_pairs_u64_u32(ctx, &k0, &k1, &v0, &v1, m, tb + nb, s));
+  } else {
+    XS_LAUNCH(ctx, k_rank_key_name, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, k0);
+    XS_TRY(sort_pairs_u64_u32(ctx, &k0, &k1, &v0, &v1, m, nb, s));
+    XS_LAUNCH(ctx, k_rank_key_end, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, lo, tb, k0);
+    XS_TRY(sort_pairs_u64_u32(ctx, &k0, &k1, &v0, &v1, m, tb, s));
+  }
+  XS_LAUNCH(ctx, k_rank_key2, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, lo, tb, k0);
+  XS_TRY(sort_pairs_u64_u32(ctx, &k0, &k1, &v0, &v1, m, gb + tb, s));
+  // v0[r] = compacted op id of rank r
+  // 3. endpoint stream per group
+  uint64_t *sk, *sk_alt;
+  uint32_t *sv, *sv_alt;
+  int* rank_ev;
+  XS_TRY(ws(ctx, W_SKEY, 2 * m + 2, s, &sk));
+  XS_TRY(ws(ctx, W_SKEY_ALT, 2 * m + 2, s, &sk_alt));
+  XS_TRY(ws(ctx, W_SVAL, 2 * m + 2, s, &sv));
+  XS_TRY(ws(ctx, W_SVAL_ALT, 2 * m + 2, s, &sv_alt));
+  XS_TRY(ws(ctx, W_RANK_EV, m + 1, s, &rank_ev));
+  XS_LAUNCH(ctx, k_endpoints, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, lo, tb, sk, sv, rank_ev);
+  XS_TRY(sort_pairs_u64_u32(ctx, &sk, &sk_alt, &sv, &sv_alt, 2 * m, gb + tb + 1, s));
+  os.skeys = sk;
+  os.svals = sv;
+  os.rank_ev = rank_ev;
+  // 4. depth = prefix sum of +-1
+  int *depth, *d_open, *pos_open, *d_close, *parent;
+  XS_TRY(ws(ctx, W_DEPTH_SCAN_DESC, 2 * m + 2, s, &depth));
+  XS_TRY(ws(ctx, W_DOPEN, m + 1, s, &d_open));
+  XS_TRY(ws(ctx, W_POPEN, m + 1, s, &pos_open));
+  XS_TRY(ws(ctx, W_DCLOSE, m + 1, s, &d_close));
+  XS_TRY(ws(ctx, W_PARENT, m + 1, s, &parent));
+  {
+    cub::TransformInputIterator<int, DepthDelta, const uint64_t*> it(sk, DepthDelta());
+    size_t temp = 0;
+    XS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, it, depth, (int)(2 * m), s));
+    void* t;
+    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
+    XS_CUDA(cub::DeviceScan::InclusiveSum(t, temp, it, depth, (int)(2 * m), s));
+    ctx->launches += 2;
+  }
+  XS_LAUNCH(ctx, k_depth_scatter, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, depth, 2 * m, d_open, pos_open, d_close);
+  XS_LAUNCH(ctx, k_depth_check, grid_for(m), XS_BLOCK, 0, s, d_open, d_close, m, st);
+  XS_TRY(fetch_stats(ctx, s));
+  if (ctx->h_stats->n_bad) return XS_OK;  // caller reports InvalidTraceError
+  const long long maxd = ctx->h_stats->max_depth;
+  uint64_t *dk = nullptr, *dk_alt;
+  uint32_t *dv = nullptr, *dv_alt;
+  if (maxd >= 2) {
+    XS_TRY(ws(ctx, W_DKEY, m + 1, s, &dk));
+    XS_TRY(ws(ctx, W_DKEY_ALT, m + 1, s, &dk_alt));
+    XS_TRY(ws(ctx, W_DVAL, m + 1, s, &dv));
+    XS_TRY(ws(ctx, W_DVAL_ALT, m + 1, s, &dv_alt));
+    XS_LAUNCH(ctx, k_depth_keys, grid_for(m), XS_BLOCK, 0, s, d_open, pos_open, m, dk, dv);
+    XS_TRY(sort_pairs_u64_u32(ctx, &dk, &dk_alt, &dv, &dv_alt, m, bits_for((uint64_t)maxd), s));
+    XS_LAUNCH(ctx, k_parent, grid_for(m), XS_BLOCK, 0, s, d_open, pos_open, m, dk, dv, sv, parent);
+  } else {
+    XS_CUDA(cudaMemsetAsync(parent, 0xFF, (m + 1) * sizeof(int), s));
+  }
+  os.parent = parent;
+  if (!build_paths) return XS_OK;
+
+  // 5. node(op) by dependency-ordered interning
+  XS_TRY(trie_setup(ctx, s, &os.trie));
+  int *node, *ready, *ctr;
+  XS_TRY(ws(ctx, W_NODE, m + 1, s, &node));
+  XS_TRY(ws(ctx, W_READY, m + 1, s, &ready));
+  XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &ctr));
+  XS_CUDA(cudaMemsetAsync(ready, 0, (m + 1) * sizeof(int), s));
+  XS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), s));
+  {
+    int blocks = (int)std::min<int64_t>((m + 255) / 256, 148 * 8);
+    XS_LAUNCH(ctx, k_nodes, blocks, XS_BLOCK, 0, s, m, maxd >= 2 ? 1 : 0, dv, sv, parent, rank_ev, v.ev.name, node,
+              ready, ctr, os.trie);
+  }
+  os.node = node;
+  // 6. path of every op segment, indexed in (pid, t) order
+  int* pidpath;
+  XS_TRY(ws(ctx, W_PIDPATH, 2 * m + 2, s, &pidpath));
+  os.pidpath = pidpath;
+  if (ctx->h_stats->multi_op_pids == 0) {
+    XS_LAUNCH(ctx, k_pidpath_simple, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, 2 * m, parent, node, pidpath);
+    os.pk = sk;  // group order == pid order; time bits identical
+  } else {
+    uint64_t *pk, *pk_alt;
+    int64_t* gs_off;
+    XS_TRY(ws(ctx, W_PK, 2 * m + 2, s, &pk));
+    XS_TRY(ws(ctx, W_PK_ALT, 2 * m + 2, s, &pk_alt));
+    XS_TRY(ws(ctx, W_GS_OFF, ng + 1, s, &gs_off));
+    XS_LAUNCH(ctx, k_gs_off, 1, 32, 0, s, group_ops, ng, gs_off);
+    XS_LAUNCH(ctx, k_pid_keys, grid_for(2 * m), XS_BLOCK, 0, s, sk, 2 * m, v.ev.group_pid, tb, pk);
+    XS_TRY(sort_keys_u64(ctx, &pk, &pk_alt, 2 * m, pb + tb + 1, s));
+    XS_LAUNCH(ctx, k_pidpath_general, grid_for(2 * m, 128), 128, 0, s, pk, 2 * m, tb, (int*)ctx->ptr[W_PID_GROUP0],
+              group_ops, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st);
+    os.pk = pk;
+  }
+  return XS_OK;
+}
+
+}  // namespace xs

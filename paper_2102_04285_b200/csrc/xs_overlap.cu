@@ -1,0 +1,437 @@
+// xs_overlap.cu -- the boundary sweep (sweep_pid, _sweep.pyx:17-118) as a
+// sort + single-pass scan + reduce-by-key.
+//
+// Endpoint key (64 bit):  pid | t_rel (tb bits) | code (4 bits)
+//   code = cat (0..6) | close<<3.  cat 0 = OPERATION (op-count lane),
+//   1..5 = resource categories, 6 = CORRELATION "tracked-only" lane.
+// After the radix sort the state for [t_i, t_{i+1}) is the state after *all*
+// endpoints at t_i (equivalent to the reference's remove-then-add walk), so
+// only the last endpoint of each equal-(pid, t) run emits.  The per-category
+// counts are a plain prefix sum over the whole sorted array: every pid opens
+// and closes all of its events inside its own key range, so counts return to
+// zero at pid boundaries and no segmentation is needed.  The path of the
+// interval is pidpath[c-1] where c is the running count of OPERATION
+// endpoints (xs_ops.cu).  Cells accumulate in a per-block shared-memory hash
+// and are flushed into a dense int64 histogram [pid][path node][32 masks];
+// mask 0 of path 0 holds the per-pid tracked time.
+//
+// CORRELATION (overlap.py:144-163, _sweep.pyx:70-79), exact decomposition:
+//   * each correlated GPU event gets fp = path at its launch instant;
+//   * per (pid, fp): sort fixed-event endpoints with the op segments whose
+//     path == fp; where both are active the event behaves as an ordinary GPU
+//     event of the current path ("own" pieces, re-injected as GPU endpoints),
+//     elsewhere the union length goes to cell (fp, {GPU}) (set semantics);
+//   * every fixed event also drives the tracked-only lane, so tracked time is
+//     "mask != 0 or any fixed event active" as in the reference.
+#include "xs_engine.cuh"
+
+namespace xs {
+
+struct Cnt {
+  int c[8];  // 0..4 categories 1..5, 5 tracked-only lane, 6 op endpoints
+};
+struct CntAdd {
+  __device__ Cnt operator()(const Cnt& a, const Cnt& b) const {
+    Cnt r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.c[i] = a.c[i] + b.c[i];
+    return r;
+  }
+};
+
+__device__ __forceinline__ void apply_code(Cnt& s, uint32_t code) {
+  const uint32_t cat = code & 7u;
+  const int d = (code & 8u) ? -1 : 1;
+  if (cat == 0) s.c[6] += 1;
+  else if (cat <= 5) s.c[cat - 1] += d;
+  else s.c[5] += d;
+}
+
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(XS_BLOCK) k_keygen(EventView v, int64_t n, const int64_t* __restrict__ lo, int tb,
+                                                     int corr_mode, uint64_t sentinel, uint64_t* __restrict__ keys) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t d = v.dur[i];
+  uint2 out_lo, out_hi;
+  uint64_t k0 = sentinel, k1 = sentinel;
+  if (d > 0) {
+    int p = v.ev.pid[i];
+    uint32_t cat = v.ev.cat[i];
+    if (corr_mode && cat == 5 && v.ev.has_corr[i]) cat = 6;
+    uint64_t base = (uint64_t)p << (tb + 4);
+    uint64_t s = (uint64_t)(v.start[i] - lo[p]);
+    k0 = base | (s << 4) | cat;
+    k1 = base | ((s + (uint64_t)d) << 4) | 8u | cat;
+  }
+  (void)out_lo;
+  (void)out_hi;
+  reinterpret_cast<ulonglong2*>(keys)[i] = make_ulonglong2(k0, k1);
+}
+
+// --------------------------------------------------------------------------
+constexpr int SW_ITEMS = 8;
+constexpr int SW_TILE = XS_BLOCK * SW_ITEMS;
+constexpr int HT = 1024;  // shared hash slots per block
+
+__device__ __forceinline__ void hist_add(unsigned long long* s_key, unsigned long long* s_val,
+                                         unsigned long long* hist, unsigned long long idx, unsigned long long v) {
+  unsigned h = (unsigned)(mix64(idx) & (HT - 1));
+#pragma unroll 1
+  for (int probe = 0; probe < 16; probe++) {
+    unsigned long long k = s_key[h];
+    if (k == idx) {
+      atomicAdd(&s_val[h], v);
+      return;
+    }
+    if (k == ~0ull) {
+      unsigned long long prev = atomicCAS(&s_key[h], ~0ull, idx);
+      if (prev == ~0ull || prev == idx) {
+        atomicAdd(&s_val[h], v);
+        return;
+      }
+    }
+    h = (h + 1) & (HT - 1);
+  }
+  atomicAdd(&hist[idx], v);
+}
+
+__global__ void __launch_bounds__(XS_BLOCK) k_sweep(const uint64_t* __restrict__ keys, int64_t nvalid, int tb,
+                                                    const int* __restrict__ pidpath,
+                                                    const int64_t* __restrict__ opbase, int n_nodes,
+                                                    unsigned long long* __restrict__ hist, TileDesc<Cnt>* desc,
+                                                    int* flags, int* tile_ctr) {
+  __shared__ unsigned long long s_key[HT];
+  __shared__ unsigned long long s_val[HT];
+  for (int i = threadIdx.x; i < HT; i += XS_BLOCK) {
+    s_key[i] = ~0ull;
+    s_val[i] = 0;
+  }
+  const int tile = next_tile(tile_ctr);
+  const int64_t base = (int64_t)tile * SW_TILE + (int64_t)threadIdx.x * SW_ITEMS;
+  uint64_t k[SW_ITEMS + 1];
+  if (base + SW_ITEMS <= nvalid) {
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(keys + base);
+#pragma unroll
+    for (int j = 0; j < SW_ITEMS / 2; j++) {
+      ulonglong2 q = __ldcs(src + j);
+      k[2 * j] = q.x;
+      k[2 * j + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < SW_ITEMS; j++) k[j] = (base + j < nvalid) ? keys[base + j] : ~0ull;
+  }
+  k[SW_ITEMS] = (base + SW_ITEMS < nvalid) ? keys[base + SW_ITEMS] : ~0ull;
+  Cnt agg;
+#pragma unroll
+  for (int i = 0; i < 8; i++) agg.c[i] = 0;
+#pragma unroll
+  for (int j = 0; j < SW_ITEMS; j++)
+    if (base + j < nvalid) apply_code(agg, (uint32_t)(k[j] & 15u));
+  Cnt zero;
+#pragma unroll
+  for (int i = 0; i < 8; i++) zero.c[i] = 0;
+  Cnt cur = grid_exclusive(agg, CntAdd(), zero, tile, desc, flags);
+  const uint64_t tmask = (1ull << tb) - 1;
+  const int pshift = tb + 4;
+#pragma unroll
+  for (int j = 0; j < SW_ITEMS; j++) {
+    if (base + j >= nvalid) break;
+    const uint64_t kj = k[j];
+    apply_code(cur, (uint32_t)(kj & 15u));
+    if (base + j + 1 >= nvalid) break;
+    const uint64_t kn = k[j + 1];
+    if ((kn >> 4) == (kj >> 4) || (kn >> pshift) != (kj >> pshift)) continue;
+    const unsigned long long len = ((kn >> 4) & tmask) - ((kj >> 4) & tmask);
+    const int p = (int)(kj >> pshift);
+    unsigned mask = 0;
+#pragma unroll
+    for (int c = 0; c < 5; c++) mask |= (cur.c[c] > 0 ? 1u : 0u) << c;
+    const unsigned long long prow = (unsigned long long)p * (unsigned long long)n_nodes;
+    if (mask) {
+      const int64_t c = cur.c[6];
+      const int path = c > opbase[p] ? pidpath[c - 1] : 0;
+      hist_add(s_key, s_val, hist, (prow + (unsigned long long)path) * 32ull + mask, len);
+      hist_add(s_key, s_val, hist, prow * 32ull, len);
+    } else if (cur.c[5] > 0) {
+      hist_add(s_key, s_val, hist, prow * 32ull, len);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HT; i += XS_BLOCK) {
+    unsigned long long key = s_key[i];
+    if (key != ~0ull) atomicAdd(&hist[key], s_val[i]);
+  }
+}
+
+// dense histogram -> (pid, node, mask, ns) list + tracked per pid
+__global__ void k_compact_cells(const unsigned long long* hist, int64_t total, int n_nodes, int* cell_pid,
+                                int* cell_node, int* cell_mask, int64_t* cell_ns, int64_t* tracked,
+                                unsigned long long* count) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  unsigned long long vv = hist[i];
+  if (!vv) return;
+  int mask = (int)(i & 31);
+  int64_t row = i >> 5;
+  int p = (int)(row / n_nodes);
+  int node = (int)(row % n_nodes);
+  if (mask == 0) {
+    if (node == 0) tracked[p] = (int64_t)vv;
+    return;
+  }
+  unsigned long long at = atomicAdd(count, 1ull);
+  cell_pid[at] = p;
+  cell_node[at] = node;
+  cell_mask[at] = mask;
+  cell_ns[at] = (int64_t)vv;
+}
+
+__global__ void k_trie_count_to_stats(const int* count, Stats* st) {
+  if (threadIdx.x == 0) st->pad[0] = *count;
+}
+
+// --------------------------------------------------------------------------
+// CORRELATION support
+// --------------------------------------------------------------------------
+__device__ __forceinline__ int path_at(const uint64_t* pk, const int* pidpath, const int64_t* opbase, int p,
+                                       uint64_t t_rel, int tb) {
+  int64_t a = opbase[p], b = opbase[p + 1];
+  const uint64_t tmask = (1ull << tb) - 1;
+  int64_t lo = a, hi = b;
+  while (lo < hi) {  // last index with time <= t
+    int64_t mid = (lo + hi) >> 1;
+    if (((pk[mid] >> 1) & tmask) <= t_rel) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo > a ? pidpath[lo - 1] : 0;
+}
+
+// FX record key: pid | path | t | code2  (code2: 0 S-, 1 S+, 2 F-, 3 F+)
+__global__ void k_fx_fixed(EventView v, int64_t n, const int64_t* lo, const int64_t* launch, const uint64_t* pk,
+                           const int* pidpath, const int64_t* opbase, int tb, int nodeb, uint64_t* fx,
+                           unsigned long long* fx_count) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (v.ev.cat[i] != 5 || !v.ev.has_corr[i] || v.dur[i] <= 0) return;
+  int p = v.ev.pid[i];
+  int64_t ls = launch[i];
+  int fp = path_at(pk, pidpath, opbase, p, (uint64_t)(ls - lo[p]), tb);
+  uint64_t grp = (((uint64_t)p << nodeb) | (uint64_t)fp) << (tb + 2);
+  uint64_t s = (uint64_t)(v.start[i] - lo[p]);
+  uint64_t e = s + (uint64_t)v.dur[i];
+  unsigned long long at = atomicAdd(fx_count, 2ull);
+  fx[at] = grp | (s << 2) | 3u;
+  fx[at + 1] = grp | (e << 2) | 2u;
+}
+
+// op segments: every pk run end opens a segment of its path until the next
+// run of the pid (or +inf); the root path covers [0, first run)
+__global__ void k_fx_segments(const uint64_t* pk, int64_t n2, const int* pidpath, int tb, int nodeb, uint64_t* fx,
+                              unsigned long long* fx_count) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n2) return;
+  const uint64_t tmask = (1ull << tb) - 1;
+  uint64_t key = pk[k] >> 1;
+  if (k + 1 < n2 && (pk[k + 1] >> 1) == key) return;
+  uint64_t p = key >> tb;
+  uint64_t t = key & tmask;
+  uint64_t tn = tmask;
+  if (k + 1 < n2 && (pk[k + 1] >> (tb + 1)) == p) tn = (pk[k + 1] >> 1) & tmask;
+  uint64_t grp = ((p << nodeb) | (uint64_t)pidpath[k]) << (tb + 2);
+  unsigned long long at = atomicAdd(fx_count, 2ull);
+  fx[at] = grp | (t << 2) | 1u;
+  fx[at + 1] = grp | (tn << 2) | 0u;
+}
+
+__global__ void k_fx_root(const uint64_t* pk, const int64_t* opbase, int np, int tb, int nodeb, uint64_t* fx,
+                          unsigned long long* fx_count) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const uint64_t tmask = (1ull << tb) - 1;
+  uint64_t tn = opbase[p] < opbase[p + 1] ? ((pk[opbase[p]] >> 1) & tmask) : tmask;
+  uint64_t grp = ((uint64_t)p << nodeb) << (tb + 2);
+  unsigned long long at = atomicAdd(fx_count, 2ull);
+  fx[at] = grp | 1u;
+  fx[at + 1] = grp | (tn << 2) | 0u;
+}
+
+struct FS {
+  int f, s;
+};
+struct FSAdd {
+  __device__ FS operator()(const FS& a, const FS& b) const { return FS{a.f + b.f, a.s + b.s}; }
+};
+
+constexpr int FX_ITEMS = 4;
+__global__ void __launch_bounds__(XS_BLOCK) k_fx_scan(const uint64_t* fx, int64_t nvalid, int tb, int nodeb,
+                                                      int n_nodes, unsigned long long* hist, uint64_t* pieces,
+                                                      unsigned long long* piece_count, TileDesc<FS>* desc, int* flags,
+                                                      int* tile_ctr) {
+  const int tile = next_tile(tile_ctr);
+  const int64_t base = (int64_t)tile * XS_BLOCK * FX_ITEMS + (int64_t)threadIdx.x * FX_ITEMS;
+  uint64_t k[FX_ITEMS + 1];
+#pragma unroll
+  for (int j = 0; j <= FX_ITEMS; j++) k[j] = (base + j < nvalid) ? fx[base + j] : ~0ull;
+  FS agg{0, 0};
+#pragma unroll
+  for (int j = 0; j < FX_ITEMS; j++) {
+    if (base + j >= nvalid) break;
+    uint32_t c = (uint32_t)(k[j] & 3u);
+    if (c & 2u) agg.f += (c & 1u) ? 1 : -1;
+    else agg.s += (c & 1u) ? 1 : -1;
+  }
+  FS cur = grid_exclusive(agg, FSAdd(), FS{0, 0}, tile, desc, flags);
+  const uint64_t tmask = (1ull << tb) - 1;
+  const uint64_t nmask = (1ull << nodeb) - 1;
+#pragma unroll
+  for (int j = 0; j < FX_ITEMS; j++) {
+    if (base + j >= nvalid) break;
+    uint64_t kj = k[j];
+    uint32_t c = (uint32_t)(kj & 3u);
+    if (c & 2u) cur.f += (c & 1u) ? 1 : -1;
+    else cur.s += (c & 1u) ? 1 : -1;
+    if (base + j + 1 >= nvalid) break;
+    uint64_t kn = k[j + 1];
+    if ((kn >> 2) == (kj >> 2) || (kn >> (tb + 2)) != (kj >> (tb + 2))) continue;
+    if (cur.f <= 0) continue;
+    uint64_t t0 = (kj >> 2) & tmask, t1 = (kn >> 2) & tmask;
+    uint64_t grp = kj >> (tb + 2);
+    uint64_t p = grp >> nodeb, path = grp & nmask;
+    if (cur.s > 0) {  // own piece: behaves as a GPU event of the current path
+      unsigned long long at = atomicAdd(piece_count, 2ull);
+      uint64_t pb = p << (tb + 4);
+      pieces[at] = pb | (t0 << 4) | 5u;
+      pieces[at + 1] = pb | (t1 << 4) | 13u;
+    } else {  // foreign: (fp, {GPU}) gets the union length
+      atomicAdd(&hist[((unsigned long long)p * n_nodes + path) * 32ull + 16ull], (unsigned long long)(t1 - t0));
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s) {
+  OpsState& os = ctx->ops;
+  Stats* st = (Stats*)ctx->ptr[W_STATS];
+  const int64_t n = v.ev.n;
+  const int np = v.ev.n_pids;
+  const int tb = os.tb;
+  const int pb = bits_for((uint64_t)(np > 0 ? np - 1 : 0));
+  if (pb + tb + 4 > 64) {
+    ctx->err = "timeline too wide for 64-bit endpoint keys";
+    return XS_UNSUPPORTED;
+  }
+  // the trie is complete once stage_ops has run: size the histogram
+  XS_LAUNCH(ctx, k_trie_count_to_stats, 1, 32, 0, s, os.trie.count, st);
+  XS_TRY(fetch_stats(ctx, s));
+  const Stats& H = *ctx->h_stats;
+  if (H.table_full || H.depth_overflow || H.n_bad) return XS_OK;
+  int n_nodes = (int)H.pad[0];
+  if (n_nodes < 1) n_nodes = 1;
+  const int64_t hist_n = (int64_t)np * n_nodes * 32;
+  if (hist_n > ((int64_t)1 << 28)) {
+    ctx->err = "overlap histogram too large for the dense layout";
+    return XS_UNSUPPORTED;
+  }
+  unsigned long long* hist;
+  XS_TRY(ws(ctx, W_HIST, hist_n + 1, s, &hist));
+  XS_CUDA(cudaMemsetAsync(hist, 0, (hist_n + 1) * 8, s));
+  const int64_t* lo = (const int64_t*)ctx->ptr[W_SPAN_LO];
+
+  // CORRELATION pre-pass -> own pieces + foreign cells
+  int64_t n_piece_keys = 0;
+  const int corr_mode = attribution == 1 && H.n_gpu_corr > 0;
+  uint64_t* pieces = nullptr;
+  int64_t piece_cap = 0;
+  if (corr_mode) {
+    const int nodeb = bits_for((uint64_t)(n_nodes - 1));
+    if (pb + nodeb + tb + 2 > 64) {
+      ctx->err = "CORRELATION keys too wide";
+      return XS_UNSUPPORTED;
+    }
+    const int64_t n2 = 2 * os.m;
+    const int64_t cap = 2 * H.n_gpu_corr + 2 * n2 + 2 * (int64_t)np + 2;
+    uint64_t *fx, *fx_alt;
+    unsigned long long* cnt;
+    XS_TRY(ws(ctx, W_FX_KEY, cap, s, &fx));
+    XS_TRY(ws(ctx, W_FX_KEY_ALT, cap, s, &fx_alt));
+    XS_TRY(ws(ctx, W_FX_OWN, 4, s, &cnt));
+    XS_CUDA(cudaMemsetAsync(cnt, 0, 32, s));
+    XS_LAUNCH(ctx, k_fx_fixed, grid_for(n), XS_BLOCK, 0, s, v, n, lo, (const int64_t*)ctx->ptr[W_FIXED_LS], os.pk,
+              os.pidpath, os.opbase, tb, nodeb, fx, cnt);
+    if (n2) XS_LAUNCH(ctx, k_fx_segments, grid_for(n2), XS_BLOCK, 0, s, os.pk, n2, os.pidpath, tb, nodeb, fx, cnt);
+    XS_LAUNCH(ctx, k_fx_root, grid_for(np), XS_BLOCK, 0, s, os.pk, os.opbase, np, tb, nodeb, fx, cnt);
+    unsigned long long h_cnt = 0;
+    XS_CUDA(cudaMemcpyAsync(&h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+    XS_CUDA(cudaStreamSynchronize(s));
+    const int64_t nfx = (int64_t)h_cnt;
+    XS_TRY(sort_keys_u64(ctx, &fx, &fx_alt, nfx, pb + nodeb + tb + 2, s));
+    piece_cap = 2 * nfx + 2;
+    XS_TRY(ws(ctx, W_PIECE_KEY, piece_cap, s, &pieces));
+    TileDesc<FS>* desc;
+    int *flags, *tctr;
+    const int64_t tiles = (nfx + XS_BLOCK * FX_ITEMS - 1) / (XS_BLOCK * FX_ITEMS);
+    XS_TRY(ws(ctx, W_FXSCAN_DESC, tiles + 1, s, &desc));
+    XS_TRY(ws(ctx, W_FXSCAN_FLAGS, tiles + 1, s, &flags));
+    XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
+    XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
+    XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+    XS_CUDA(cudaMemsetAsync(cnt + 1, 0, 8, s));
+    if (tiles)
+      XS_LAUNCH(ctx, k_fx_scan, (int)tiles, XS_BLOCK, 0, s, fx, nfx, tb, nodeb, n_nodes, hist, pieces, cnt + 1, desc,
+                flags, tctr);
+    XS_CUDA(cudaMemcpyAsync(&h_cnt, cnt + 1, 8, cudaMemcpyDeviceToHost, s));
+    XS_CUDA(cudaStreamSynchronize(s));
+    n_piece_keys = (int64_t)h_cnt;
+  }
+
+  // main endpoint keys
+  const int key_bits = pb + tb + 4;
+  const uint64_t sentinel = key_bits >= 64 ? ~0ull : ((1ull << key_bits) - 1);
+  const int64_t nkeys = 2 * n + n_piece_keys;
+  uint64_t *mk, *mk_alt;
+  XS_TRY(ws(ctx, W_MKEY, nkeys + SW_TILE, s, &mk));
+  XS_TRY(ws(ctx, W_MKEY_ALT, nkeys + SW_TILE, s, &mk_alt));
+  if (n) XS_LAUNCH(ctx, k_keygen, grid_for(n), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, sentinel, mk);
+  if (n_piece_keys) XS_CUDA(cudaMemcpyAsync(mk + 2 * n, pieces, n_piece_keys * 8, cudaMemcpyDeviceToDevice, s));
+  XS_TRY(sort_keys_u64(ctx, &mk, &mk_alt, nkeys, key_bits, s));
+  const int64_t nvalid = 2 * H.n_nonzero + n_piece_keys;
+  if (nvalid > 0) {
+    const int64_t tiles = (nvalid + SW_TILE - 1) / SW_TILE;
+    TileDesc<Cnt>* desc;
+    int *flags, *tctr;
+    XS_TRY(ws(ctx, W_MSCAN_DESC, tiles + 1, s, &desc));
+    XS_TRY(ws(ctx, W_MSCAN_FLAGS, tiles + 1, s, &flags));
+    XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
+    XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
+    XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+    XS_LAUNCH(ctx, k_sweep, (int)tiles, XS_BLOCK, 0, s, mk, nvalid, tb, os.pidpath, os.opbase, n_nodes, hist, desc,
+              flags, tctr);
+  }
+  // compact
+  int *cp, *cn, *cm;
+  int64_t *cns, *tracked;
+  unsigned long long* ccount;
+  const int64_t cells_cap = hist_n + 1;
+  XS_TRY(ws(ctx, W_CELL_PID, cells_cap, s, &cp));
+  XS_TRY(ws(ctx, W_CELL_NODE, cells_cap, s, &cn));
+  XS_TRY(ws(ctx, W_CELL_MASK, cells_cap, s, &cm));
+  XS_TRY(ws(ctx, W_CELL_NS, cells_cap, s, &cns));
+  XS_TRY(ws(ctx, W_TRACKED, np + 1, s, &tracked));
+  XS_TRY(ws(ctx, W_CELL_COUNT, 1, s, &ccount));
+  XS_CUDA(cudaMemsetAsync(tracked, 0, (np + 1) * 8, s));
+  XS_CUDA(cudaMemsetAsync(ccount, 0, 8, s));
+  if (hist_n)
+    XS_LAUNCH(ctx, k_compact_cells, grid_for(hist_n), XS_BLOCK, 0, s, hist, hist_n, n_nodes, cp, cn, cm, cns, tracked,
+              ccount);
+  unsigned long long h_cells = 0;
+  XS_CUDA(cudaMemcpyAsync(&h_cells, ccount, 8, cudaMemcpyDeviceToHost, s));
+  XS_TRY(fetch_stats(ctx, s));
+  ctx->n_cells = (long long)h_cells;
+  ctx->n_nodes = n_nodes;
+  ctx->res_pids = np;
+  return XS_OK;
+}
+
+}  // namespace xs

@@ -1,0 +1,205 @@
+"""Cross-stack overlap accounting and transition counting (drop-in for
+``pkg/src/xstrace/overlap.py``).
+
+Same public names, signatures and return types as the reference; the work
+runs on the GPU through ``libxstrace_b200.so``:
+
+* ``compute_overlap``   overlap.py:106-188  -> xs_overlap (csrc/xs_overlap.cu)
+* ``transition_sites``  overlap.py:263-289  -> xs_transition_sites (csrc/xs_transitions.cu)
+* ``count_transitions`` overlap.py:292-295
+
+``compute_overlap_columnar`` is the scalable twin taking a ``ColumnarTrace``
+(no Python ``Event`` objects), which is what the bench and multi-GPU path use.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _engine, _lib
+from .columnar import ColumnarTrace
+from .model import Category, InvalidTraceError, Trace, format_violations, meta_violations
+
+
+class Attribution(Enum):
+    """How a GPU event picks its operation path (overlap.py:41-45)."""
+
+    INSTANT = "instant"
+    CORRELATION = "correlation"
+
+
+@dataclass(frozen=True)
+class OverlapKey:
+    pid: int
+    path: tuple
+    categories: frozenset
+
+    def category_label(self) -> str:
+        return "+".join(c.name for c in sorted(self.categories))
+
+    def path_label(self) -> str:
+        return "/".join(self.path) if self.path else "-"
+
+
+@dataclass
+class Breakdown:
+    """Accumulated ns per (pid, operation path, category set) (overlap.py:61-77)."""
+
+    cells: dict = field(default_factory=dict)
+    spans: dict = field(default_factory=dict)
+    untracked: dict = field(default_factory=dict)
+
+    def span_ns(self, pid: int) -> int:
+        lo, hi = self.spans[pid]
+        return hi - lo
+
+    def pid_cells(self, pid: int) -> dict:
+        return {k: v for k, v in self.cells.items() if k.pid == pid}
+
+    def total_attributed(self, pid: int) -> int:
+        return sum(v for k, v in self.cells.items() if k.pid == pid)
+
+
+TRANSITION_PAIRS = (
+    (Category.HIGH_LEVEL, Category.BACKEND),
+    (Category.HIGH_LEVEL, Category.SIMULATOR),
+    (Category.BACKEND, Category.ACCEL_API),
+    (Category.SIMULATOR, Category.ACCEL_API),
+)
+WRAPPER_PAIRS = (
+    (Category.HIGH_LEVEL, Category.BACKEND),
+    (Category.HIGH_LEVEL, Category.SIMULATOR),
+)
+
+
+@dataclass(frozen=True)
+class TransitionCounts:
+    counts: tuple
+
+    def get(self, src, dst) -> int:
+        for f, t, c in self.counts:
+            if f == src and t == dst:
+                return c
+        return 0
+
+    def as_dict(self) -> dict:
+        return {(f, t): c for f, t, c in self.counts}
+
+
+_CATS = [Category(c) for c in range(6)]
+_MASK_CATS = [frozenset(_CATS[c] for c in range(1, 6) if m & (1 << (c - 1))) for m in range(32)]
+
+
+def _as_columnar(trace) -> ColumnarTrace:
+    return trace if isinstance(trace, ColumnarTrace) else ColumnarTrace.from_trace(trace)
+
+
+def _source_trace(trace, ct: ColumnarTrace) -> Trace:
+    if not isinstance(trace, ColumnarTrace):
+        return trace
+    return ct._source if ct._source is not None else ct.to_trace()
+
+
+def _raise_invalid(trace, ct):
+    raise InvalidTraceError(format_violations(_source_trace(trace, ct)))
+
+
+def decode_paths(ct: ColumnarTrace, parents: np.ndarray, names: np.ndarray, needed=None) -> list:
+    """Trie nodes -> name tuples (a parent is always allocated before its child)."""
+    n = int(parents.shape[0])
+    paths: list = [()] * max(n, 1)
+    par = parents.tolist()
+    nm = names.tolist()
+    table = ct.names
+    for i in range(1, n):
+        paths[i] = paths[par[i]] + (table[nm[i]],)
+    return paths
+
+
+def decode_breakdown(ct: ColumnarTrace, raw) -> Breakdown:
+    bd = Breakdown()
+    paths = decode_paths(ct, raw.node_parent, raw.node_name)
+    pids = ct.pids.tolist()
+    for p, node, mask, ns in zip(raw.cell_pid.tolist(), raw.cell_node.tolist(), raw.cell_mask.tolist(),
+                                 raw.cell_ns.tolist()):
+        bd.cells[OverlapKey(pids[p], paths[node], _MASK_CATS[mask])] = ns
+    for p in range(ct.n_pids):
+        if raw.has_events[p]:
+            lo, hi = int(raw.span_lo[p]), int(raw.span_hi[p])
+            bd.spans[pids[p]] = (lo, hi)
+            bd.untracked[pids[p]] = (hi - lo) - int(raw.tracked[p])
+    return bd
+
+
+def compute_overlap_columnar(ct: ColumnarTrace, attribution: Attribution = Attribution.INSTANT,
+                             device_trace=None, _source=None) -> Breakdown:
+    """compute_overlap over a ColumnarTrace (or an already-uploaded DeviceTrace)."""
+    if meta_violations(ct.processes):
+        _raise_invalid(_source if _source is not None else ct, ct)
+    eng = _engine.get()
+    dt = device_trace if device_trace is not None else _engine.DeviceTrace(ct, eng.device)
+    attr = 1 if Attribution(attribution) is Attribution.CORRELATION else 0
+    try:
+        raw = eng.overlap(dt, attr)
+    except _engine.XsError as exc:
+        if exc.status == _lib.XS_INVALID_TRACE:
+            _raise_invalid(_source if _source is not None else ct, ct)
+        raise
+    return decode_breakdown(ct, raw)
+
+
+def compute_overlap(trace, attribution: Attribution = Attribution.INSTANT, kernel=None) -> Breakdown:
+    """Attribute every nanosecond of each pid's timeline to overlap cells.
+
+    Rejects invalid traces with InvalidTraceError carrying the violations.
+    ``kernel`` is accepted for signature compatibility with the reference's
+    plugin point (overlap.py:106-113); the device pipeline is always used.
+    """
+    ct = _as_columnar(trace)
+    return compute_overlap_columnar(ct, attribution, _source=trace)
+
+
+def _transition_lists(trace, pair_mask: int):
+    ct = _as_columnar(trace)
+    if meta_violations(ct.processes):
+        _raise_invalid(trace, ct)
+    eng = _engine.get()
+    dt = _engine.DeviceTrace(ct, eng.device)
+    try:
+        pair, event = eng.transition_sites(dt, pair_mask)
+    except _engine.XsError as exc:
+        if exc.status == _lib.XS_INVALID_TRACE:
+            _raise_invalid(trace, ct)
+        raise
+    return ct, pair, event
+
+
+def transition_sites(trace) -> dict:
+    """Counted transitions per pair: maximal inner events whose start lies
+    inside an active outer-category event on the same tid (overlap.py:263-289)."""
+    ct, pair, event = _transition_lists(trace, 0xF)
+    src = _source_trace(trace, ct)
+    events = src.events
+    out = {p: [] for p in TRANSITION_PAIRS}
+    for k, e in zip(pair.tolist(), event.tolist()):
+        out[TRANSITION_PAIRS[k]].append(events[e])
+    return out
+
+
+def transition_site_indices(trace, pair_mask: int = 0xF) -> dict:
+    """Event row indices per pair (columnar-friendly form of transition_sites)."""
+    _, pair, event = _transition_lists(trace, pair_mask)
+    out = {p: [] for k, p in enumerate(TRANSITION_PAIRS) if (pair_mask >> k) & 1}
+    for k, e in zip(pair.tolist(), event.tolist()):
+        out[TRANSITION_PAIRS[k]].append(e)
+    return out
+
+
+def count_transitions(trace) -> TransitionCounts:
+    """Count language transitions once per counted inner event (overlap.py:292-295)."""
+    _, pair, _ = _transition_lists(trace, 0xF)
+    counts = np.bincount(pair, minlength=4) if len(pair) else np.zeros(4, np.int64)
+    return TransitionCounts(tuple((s, d, int(counts[k])) for k, (s, d) in enumerate(TRANSITION_PAIRS)))

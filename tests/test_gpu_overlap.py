@@ -1,0 +1,68 @@
+"""GPU parity: compute_overlap through the C ABI vs reference golden vectors
+and vs the CPU oracle on synthetic traces (bit-exact int64 cells)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_util import dec_trace, enc_breakdown, load
+from paper_2102_04285_b200 import Attribution, ColumnarTrace, InvalidTraceError, compute_overlap
+from paper_2102_04285_b200 import compute_overlap_columnar, synth
+
+pytestmark = pytest.mark.gpu
+
+OVERLAP = load("overlap_cases.json.gz")
+
+
+def _attr(name):
+    return Attribution.INSTANT if name == "instant" else Attribution.CORRELATION
+
+
+@pytest.mark.parametrize("case", OVERLAP, ids=[c["name"] for c in OVERLAP])
+def test_overlap_matches_reference_golden(case):
+    trace = dec_trace(case["trace"])
+    for attr, exp in case["expect"].items():
+        if "invalid" in exp:
+            with pytest.raises(InvalidTraceError) as ei:
+                compute_overlap(trace, _attr(attr))
+            got = [[v.rule, v.message, list(v.event_indices)] for v in ei.value.violations]
+            assert got == exp["invalid"]
+            continue
+        bd = compute_overlap(trace, _attr(attr))
+        assert enc_breakdown(bd) == exp, attr
+
+
+def _oracle_bd(ct, attr):
+    cells, spans, untracked = oracle.overlap(ct, attr)
+    return cells, spans, untracked
+
+
+def _ours(bd):
+    cells = {(k.pid, k.path, frozenset(int(c) for c in k.categories)): v for k, v in bd.cells.items()}
+    return cells, bd.spans, bd.untracked
+
+
+@pytest.mark.parametrize("iters,procs,outer,tid2", [(2000, 1, None, False), (400, 3, "iteration", False),
+                                                     (300, 2, "iteration", True)])
+def test_overlap_synthetic_vs_oracle(iters, procs, outer, tid2):
+    un, inst = synth.ddpg_trace(iters, processes=procs, outer_op=outer, second_tid_ops=tid2, both=True)
+    for ct in (un, inst):
+        for attr in (0, 1):
+            bd = compute_overlap_columnar(ct, Attribution.CORRELATION if attr else Attribution.INSTANT)
+            assert _ours(bd) == _oracle_bd(ct, attr)
+
+
+def test_overlap_1m_ddpg_vs_oracle():
+    ct = synth.ddpg_trace(27027)
+    bd = compute_overlap_columnar(ct)
+    assert _ours(bd) == _oracle_bd(ct, 0)
+    # conservation (test_overlap.py:177-185)
+    for pid, (lo, hi) in bd.spans.items():
+        assert bd.total_attributed(pid) + bd.untracked[pid] == hi - lo
+
+
+def test_overlap_repeat_calls_reuse_workspace():
+    ct = synth.ddpg_trace(500, processes=2)
+    a = compute_overlap_columnar(ct)
+    b = compute_overlap_columnar(ct)
+    assert a == b
