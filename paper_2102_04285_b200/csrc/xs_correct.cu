@@ -1,17 +1,583 @@
-// xs_correct.cu -- placeholder (correction pipeline lands next)
+// xs_correct.cu -- correct_trace (correction.py:79-186, _timeline.py:57-132).
+//
+// Per pid, in Site.order_key order (anchor, subkind, tid, name; stable):
+//   quantize   out_i = floor(S_i) - floor(S_{i-1}), S = running exact sum
+//              -> segmented int128 scan of amount*L, floor-divided by L
+//   caps       each owner has <= 2 sites, first one fixed by subkind:
+//              c1 = min(q1, dur); c2 = min(q2, dur - c1)      (139-153)
+//   RemovalMap a_i = max(anchor_i, E_{i-1}), b_i = a_i + len_i,
+//              E_i = max(E_{i-1}, b_i) = f_i(E_{i-1}),
+//              f_i(x) = max(x + max(0,len_i), anchor_i + len_i): (max,+)
+//              affine maps compose associatively -> one segmented scan
+//   remap      rmap(y) = y - prefix[k] - (y - a_k if a_k < y), k = #slabs
+//              with b <= y (bisect_right) -> one binary search per endpoint
+// Site order ties follow the reference's stable sort: sites are generated in
+// event-index order (ANN/API sites tie only by index); TRANSITION sites that
+// tie on the full key are re-ordered by (category, correlation or -1, index),
+// which is the order of the H->B list, then H->S, each sorted by
+// Event.sort_key (overlap.py:287-288).
+#include <cub/device/device_scan.cuh>
+
 #include "xs_engine.cuh"
+
 namespace xs {
-int stage_transitions(xs_ctx* ctx, const EventView&, int, int, cudaStream_t) {
-  ctx->err = "not yet built";
-  return XS_UNSUPPORTED;
+
+enum { ANN_START = 0, TRANSITION_HOOK = 1, API_INTERCEPT = 2, API_INTERNAL = 3, ANN_END = 4 };
+enum { H_ANN = 0, H_TRANS = 1, H_IC = 2, H_INT = 3 };
+
+__global__ void k_site_count(EventView v, int64_t n, const uint8_t* tflag, int* cnt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = v.ev.cat[i];
+  cnt[i] = (c == 0 || c == 4) ? 2 : ((tflag[i] & 3) ? 1 : 0);
 }
-int stage_correct(xs_ctx* ctx, const EventView&, const xs_profile_t*, int64_t*, int64_t*, bool, cudaStream_t) {
-  ctx->err = "not yet built";
-  return XS_UNSUPPORTED;
+
+// slot layout: pos[i] (+1) for event i.  sub: subkind per slot.
+__global__ void k_site_gen(EventView v, int64_t n, const int* cnt, const int* pos, const int64_t* lo, int tb, int nb,
+                           int* site_ev, uint8_t* site_sub, uint64_t* k2) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || cnt[i] == 0) return;
+  int c = v.ev.cat[i];
+  int at = pos[i];
+  uint64_t sec = ((uint64_t)v.ev.tid[i] << nb) | (uint64_t)v.ev.name[i];
+  if (c == 0) {
+    site_ev[at] = (int)i;
+    site_sub[at] = ANN_START;
+    site_ev[at + 1] = (int)i;
+    site_sub[at + 1] = ANN_END;
+    k2[at] = sec;
+    k2[at + 1] = sec;
+  } else if (c == 4) {
+    site_ev[at] = (int)i;
+    site_sub[at] = API_INTERCEPT;
+    site_ev[at + 1] = (int)i;
+    site_sub[at + 1] = API_INTERNAL;
+    k2[at] = sec;
+    k2[at + 1] = sec;
+  } else {
+    site_ev[at] = (int)i;
+    site_sub[at] = TRANSITION_HOOK;
+    k2[at] = sec;
+  }
 }
+
+__device__ __forceinline__ int64_t site_anchor(const EventView& v, int i, int sub) {
+  return sub == ANN_END ? v.start[i] + v.dur[i] : v.start[i];
+}
+
+__global__ void k_site_k1(EventView v, const uint32_t* slot, int64_t ns, const int* site_ev, const uint8_t* site_sub,
+                          const int64_t* lo, int tb, uint64_t* k1) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= ns) return;
+  uint32_t sl = slot[q];
+  int i = site_ev[sl];
+  int sub = site_sub[sl];
+  int p = v.ev.pid[i];
+  uint64_t a = (uint64_t)(site_anchor(v, i, sub) - lo[p]);
+  k1[q] = ((uint64_t)p << (tb + 3)) | (a << 3) | (uint64_t)sub;
+}
+
+// TRANSITION runs tying on (pid, anchor, subkind, tid, name): order by
+// (category, correlation or -1, event index)
+__global__ void k_tie_fix(EventView v, const uint64_t* k1, uint32_t* slot, int64_t ns, const int* site_ev) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= ns) return;
+  if ((k1[q] & 7u) != TRANSITION_HOOK) return;
+  auto same = [&](int64_t a, int64_t b) {
+    if (k1[a] != k1[b]) return false;
+    int ia = site_ev[slot[a]], ib = site_ev[slot[b]];
+    return v.ev.tid[ia] == v.ev.tid[ib] && v.ev.name[ia] == v.ev.name[ib];
+  };
+  if (q > 0 && same(q - 1, q)) return;
+  if (q + 1 >= ns || !same(q, q + 1)) return;
+  int64_t e = q + 1;
+  while (e < ns && same(q, e)) e++;
+  // insertion sort of slot[q..e)
+  for (int64_t a = q + 1; a < e; a++) {
+    uint32_t x = slot[a];
+    int ix = site_ev[x];
+    int cx = v.ev.cat[ix];
+    int64_t rx = v.ev.has_corr[ix] ? v.ev.corr[ix] : -1;
+    int64_t b = a - 1;
+    while (b >= q) {
+      uint32_t y = slot[b];
+      int iy = site_ev[y];
+      int cy = v.ev.cat[iy];
+      int64_t ry = v.ev.has_corr[iy] ? v.ev.corr[iy] : -1;
+      bool greater = cy != cx ? cy > cx : (ry != rx ? ry > rx : iy > ix);
+      if (!greater) break;
+      slot[b + 1] = y;
+      b--;
+    }
+    slot[b + 1] = x;
+  }
+}
+
+__device__ __forceinline__ int64_t site_amount(const xs_profile_t& pr, const EventView& v, int i, int sub) {
+  switch (sub) {
+    case ANN_START: return pr.ann_start;
+    case ANN_END: return pr.ann_end;
+    case TRANSITION_HOOK: return pr.transition;
+    case API_INTERCEPT: return pr.interception;
+    default: return pr.internal[v.ev.name[i]];
+  }
+}
+
+constexpr int Q_ITEMS = 4;
+__global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const uint32_t* slot, int64_t ns, int tb,
+                                                       EventView v, xs_profile_t pr, const int* site_ev,
+                                                       const uint8_t* site_sub, int64_t* qslot,
+                                                       TileDesc<SegI128>* desc, int* flags, int* tile_ctr) {
+  const int tile = next_tile(tile_ctr);
+  const int64_t base = (int64_t)tile * XS_BLOCK * Q_ITEMS + (int64_t)threadIdx.x * Q_ITEMS;
+  int64_t amt[Q_ITEMS];
+  int hd[Q_ITEMS];
+  SegI128Op op;
+  SegI128 agg;
+  agg.v = 0;
+  agg.head = 0;
+  agg.pad[0] = agg.pad[1] = agg.pad[2] = 0;
+  const int pshift = tb + 3;
+#pragma unroll
+  for (int j = 0; j < Q_ITEMS; j++) {
+    int64_t q = base + j;
+    amt[j] = 0;
+    hd[j] = 0;
+    if (q < ns) {
+      uint32_t sl = slot[q];
+      int i = site_ev[sl];
+      amt[j] = site_amount(pr, v, i, site_sub[sl]);
+      hd[j] = q == 0 || (k1[q - 1] >> pshift) != (k1[q] >> pshift);
+      SegI128 e;
+      e.v = amt[j];
+      e.head = hd[j];
+      e.pad[0] = e.pad[1] = e.pad[2] = 0;
+      agg = op(agg, e);
+    }
+  }
+  SegI128 id;
+  id.v = 0;
+  id.head = 0;
+  id.pad[0] = id.pad[1] = id.pad[2] = 0;
+  SegI128 cur = grid_exclusive(agg, op, id, tile, desc, flags);
+  __int128 run = cur.v;
+  const int64_t L = pr.L;
+#pragma unroll
+  for (int j = 0; j < Q_ITEMS; j++) {
+    int64_t q = base + j;
+    if (q >= ns) break;
+    __int128 before = hd[j] ? (__int128)0 : run;
+    __int128 after = before + amt[j];
+    int64_t qv;
+    if (L == 1) qv = (int64_t)(after - before);
+    else qv = floor_div(after, L) - floor_div(before, L);
+    qslot[slot[q]] = qv;
+    run = after;
+  }
+}
+
+// per owner: budget caps (correction.py:139-153) + shortfall per (pid, hook)
+__global__ void k_caps(EventView v, int64_t n, const int* cnt, const int* pos, const int64_t* qslot, int64_t* lenslot,
+                       int64_t* shortfall) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || cnt[i] == 0) return;
+  int c = v.ev.cat[i];
+  int at = pos[i];
+  int p = v.ev.pid[i];
+  int64_t budget = v.dur[i];
+  int64_t q1 = qslot[at];
+  int64_t c1 = q1 < budget ? q1 : budget;
+  budget -= c1;
+  lenslot[at] = c1;
+  int h1 = c == 0 ? H_ANN : (c == 4 ? H_IC : H_TRANS);
+  if (q1 != c1) atomic_add_i64(&shortfall[(int64_t)p * 4 + h1], q1 - c1);
+  if (cnt[i] == 2) {
+    int64_t q2 = qslot[at + 1];
+    int64_t c2 = q2 < budget ? q2 : budget;
+    lenslot[at + 1] = c2;
+    int h2 = c == 0 ? H_ANN : H_INT;
+    if (q2 != c2) atomic_add_i64(&shortfall[(int64_t)p * 4 + h2], q2 - c2);
+  }
+}
+
+// (max,+) RemovalMap scan, segmented by pid; slab count is global
+struct RM {
+  int64_t P;  // sum of max(0, len)
+  int64_t Q;  // max-plus offset
+  int64_t cnt;
+  int head;
+  int pad;
+};
+struct RMOp {
+  __device__ RM operator()(const RM& a, const RM& b) const {
+    RM r;
+    r.cnt = a.cnt + b.cnt;
+    r.pad = 0;
+    if (b.head) {
+      r.head = 1;
+      r.P = b.P;
+      r.Q = b.Q;
+    } else {
+      r.head = a.head;
+      r.P = a.P + b.P;
+      int64_t x = a.Q + b.P;
+      r.Q = x > b.Q ? x : b.Q;
+    }
+    return r;
+  }
+};
+
+__device__ __forceinline__ int hook_of(int sub) {
+  return sub == TRANSITION_HOOK ? H_TRANS : sub == API_INTERCEPT ? H_IC : sub == API_INTERNAL ? H_INT : H_ANN;
+}
+
+constexpr int R_ITEMS = 4;
+__global__ void __launch_bounds__(XS_BLOCK) k_removal(const uint64_t* k1, const uint32_t* slot, int64_t ns, int tb,
+                                                      const int64_t* lenslot, const uint8_t* site_sub,
+                                                      const int64_t* lo, const int64_t* hi, int64_t* removed,
+                                                      int64_t* slab_a, int64_t* slab_b, int64_t* slab_pre,
+                                                      int* pid_slabs, int64_t* ptotal, TileDesc<RM>* desc,
+                                                      int* flags, int* tile_ctr) {
+  const int tile = next_tile(tile_ctr);
+  const int64_t base = (int64_t)tile * XS_BLOCK * R_ITEMS + (int64_t)threadIdx.x * R_ITEMS;
+  const int pshift = tb + 3;
+  const uint64_t tmask = (1ull << tb) - 1;
+  int64_t anc[R_ITEMS], len[R_ITEMS];
+  int hd[R_ITEMS], sub[R_ITEMS], pp[R_ITEMS];
+  RMOp op;
+  RM agg{0, kNegInf, 0, 0, 0};
+#pragma unroll
+  for (int j = 0; j < R_ITEMS; j++) {
+    int64_t q = base + j;
+    if (q < ns) {
+      uint64_t kk = k1[q];
+      uint32_t sl = slot[q];
+      anc[j] = (int64_t)((kk >> 3) & tmask);
+      pp[j] = (int)(kk >> pshift);
+      sub[j] = site_sub[sl];
+      len[j] = lenslot[sl];
+      hd[j] = q == 0 || (k1[q - 1] >> pshift) != (kk >> pshift);
+      RM e{len[j] > 0 ? len[j] : 0, anc[j] + len[j], len[j] > 0 ? 1 : 0, hd[j], 0};
+      agg = op(agg, e);
+    }
+  }
+  RM cur = grid_exclusive(agg, op, RM{0, kNegInf, 0, 0, 0}, tile, desc, flags);
+  // per-thread removed accumulation keyed by pid
+  int cp = -1;
+  int64_t acc[4] = {0, 0, 0, 0};
+  int64_t nsl = 0, tot = 0;
+#pragma unroll
+  for (int j = 0; j < R_ITEMS; j++) {
+    int64_t q = base + j;
+    if (q >= ns) break;
+    if (hd[j]) {
+      cur.P = 0;
+      cur.Q = kNegInf;
+    }
+    const int64_t E = cur.Q;
+    const int64_t a = anc[j] > E ? anc[j] : E;
+    const int64_t b = a + len[j];
+    const int p = pp[j];
+    if (p != cp) {
+      if (cp >= 0) {
+        for (int h = 0; h < 4; h++)
+          if (acc[h]) atomic_add_i64(&removed[(int64_t)cp * 4 + h], acc[h]);
+        if (nsl) atomicAdd(&pid_slabs[cp], (int)nsl);
+        if (tot) atomic_add_i64(&ptotal[cp], tot);
+      }
+      cp = p;
+      acc[0] = acc[1] = acc[2] = acc[3] = 0;
+      nsl = tot = 0;
+    }
+    const int64_t span_end = hi[p] - lo[p];
+    const int64_t mb = b < span_end ? b : span_end;
+    const int64_t ma = a < span_end ? a : span_end;
+    acc[hook_of(sub[j])] += mb - ma;
+    if (len[j] > 0) {
+      const int64_t at = cur.cnt;
+      slab_a[at] = a;
+      slab_b[at] = b;
+      slab_pre[at] = cur.P;
+      nsl++;
+      tot += len[j];
+    }
+    RM e{len[j] > 0 ? len[j] : 0, anc[j] + len[j], len[j] > 0 ? 1 : 0, 0, 0};
+    cur = op(cur, e);
+  }
+  if (cp >= 0) {
+    for (int h = 0; h < 4; h++)
+      if (acc[h]) atomic_add_i64(&removed[(int64_t)cp * 4 + h], acc[h]);
+    if (nsl) atomicAdd(&pid_slabs[cp], (int)nsl);
+    if (tot) atomic_add_i64(&ptotal[cp], tot);
+  }
+}
+
+__global__ void k_slab_base(const int* pid_slabs, int np, int64_t* slab_base) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t acc = 0;
+    for (int p = 0; p < np; p++) {
+      slab_base[p] = acc;
+      acc += pid_slabs[p];
+    }
+    slab_base[np] = acc;
+  }
+}
+
+// RemovalMap.__call__ (_timeline.py:112-117) on a relative coordinate
+__device__ __forceinline__ int64_t rmap_removed(int64_t y, const int64_t* sa, const int64_t* sb, const int64_t* spre,
+                                                int64_t base, int64_t K, int64_t total) {
+  int64_t lo = 0, hi = K;  // bisect_right(ends, y)
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (sb[base + mid] <= y) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo == K) return total;
+  int64_t r = spre[base + lo];
+  int64_t a = sa[base + lo];
+  if (a < y) r += y - a;
+  return r;
+}
+
+__global__ void k_remap(EventView v, int64_t n, const int64_t* lo, const int64_t* sa, const int64_t* sb,
+                        const int64_t* spre, const int64_t* slab_base, const int64_t* ptotal, int64_t* out_start,
+                        int64_t* out_dur) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int p = v.ev.pid[i];
+  int64_t base = slab_base[p], K = slab_base[p + 1] - base, tot = ptotal[p];
+  int64_t s = v.start[i], d = v.dur[i];
+  int64_t l = lo[p];
+  int64_t s2 = s - rmap_removed(s - l, sa, sb, spre, base, K, tot);
+  out_start[i] = s2;
+  if (v.ev.cat[i] == 5) {
+    out_dur[i] = d;
+  } else {
+    int64_t e = s + d;
+    out_dur[i] = (e - rmap_removed(e - l, sa, sb, spre, base, K, tot)) - s2;
+  }
+}
+
+__global__ void k_remap_queries(int64_t n, const int32_t* qp, const int64_t* qv, int64_t* out, const int64_t* lo,
+                                const int64_t* sa, const int64_t* sb, const int64_t* spre, const int64_t* slab_base,
+                                const int64_t* ptotal, int np) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int p = qp[i];
+  int64_t y = qv[i];
+  if (p < 0 || p >= np || lo[p] == INT64_MAX) {
+    out[i] = y;
+    return;
+  }
+  int64_t base = slab_base[p], K = slab_base[p + 1] - base;
+  out[i] = y - rmap_removed(y - lo[p], sa, sb, spre, base, K, ptotal[p]);
+}
+
+__global__ void k_totals(const int64_t* lo, const int64_t* hi, int np, Stats* st, int which) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  long long v = 0;
+  if (p < np && lo[p] != INT64_MAX) v = hi[p] - lo[p];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long*)&st->pad[which], (unsigned long long)v);
+}
+
+__global__ void k_zero_pad(Stats* st) {
+  if (threadIdx.x < 4) st->pad[1 + threadIdx.x] = 0;
+}
+
+// corrected per-pid spans (pid_spans(out), correction.py:184-185)
+__global__ void k_out_spans(const int32_t* pid, int64_t n, const int64_t* s, const int64_t* d, int64_t* lo2,
+                            int64_t* hi2) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned full = 0xffffffffu;
+  int p = i < n ? pid[i] : -1;
+  int64_t a = i < n ? s[i] : INT64_MAX;
+  int64_t b = i < n ? s[i] + d[i] : INT64_MIN;
+  int p0 = __shfl_sync(full, p, 0);
+  if (__all_sync(full, p == p0)) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      int64_t a2 = __shfl_xor_sync(full, a, o), b2 = __shfl_xor_sync(full, b, o);
+      a = a2 < a ? a2 : a;
+      b = b2 > b ? b2 : b;
+    }
+    if ((threadIdx.x & 31) == 0 && p0 >= 0) {
+      atomic_min_i64(&lo2[p0], a);
+      atomic_max_i64(&hi2[p0], b);
+    }
+  } else if (p >= 0) {
+    atomic_min_i64(&lo2[p], a);
+    atomic_max_i64(&hi2[p], b);
+  }
+}
+
+__global__ void k_init_span(int64_t* lo, int64_t* hi, int np) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < np) {
+    lo[p] = INT64_MAX;
+    hi[p] = INT64_MIN;
+  }
+}
+
+__global__ void k_tkey_gather_u32(const uint32_t* src, const uint32_t* perm, int64_t m, uint32_t* out) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < m) out[q] = src[perm[q]];
+}
+
+int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start, int64_t* out_dur,
+                  bool corrected_spans, cudaStream_t s) {
+  const int64_t n = v.ev.n;
+  const int np = v.ev.n_pids, ng = v.ev.n_groups;
+  Stats* st = (Stats*)ctx->ptr[W_STATS];
+  const Stats& H = *ctx->h_stats;
+  const int tb = bits_for((uint64_t)(H.max_span > 0 ? H.max_span : 0));
+  const int pb = bits_for((uint64_t)(np > 0 ? np - 1 : 0));
+  const int gb = bits_for((uint64_t)(ng > 0 ? ng - 1 : 0));
+  const int nb = bits_for((uint64_t)(v.ev.n_names > 0 ? v.ev.n_names - 1 : 0));
+  if (pb + tb + 3 > 64 || gb + nb > 64) {
+    ctx->err = "timeline too wide for 64-bit site keys";
+    return XS_UNSUPPORTED;
+  }
+  const int64_t* lo_ev = (const int64_t*)ctx->ptr[W_SPAN_LO];
+  const int64_t* hi_ev = (const int64_t*)ctx->ptr[W_SPAN_HI];
+  // keep this correction's per-pid origin for xs_remap (the overlap pass reuses W_SPAN_*)
+  int64_t *lo, *hi;
+  XS_TRY(ws(ctx, W_CORR_LO, np + 1, s, &lo));
+  XS_TRY(ws(ctx, W_CORR_HI, np + 1, s, &hi));
+  XS_CUDA(cudaMemcpyAsync(lo, lo_ev, (np + 1) * 8, cudaMemcpyDeviceToDevice, s));
+  XS_CUDA(cudaMemcpyAsync(hi, hi_ev, (np + 1) * 8, cudaMemcpyDeviceToDevice, s));
+  const uint8_t* tflag = (const uint8_t*)ctx->ptr[W_SITE_FLAG];
+  int64_t *removed, *shortfall, *ptotal, *slab_base;
+  int* pid_slabs;
+  XS_TRY(ws(ctx, W_REMOVED, (int64_t)np * 4 + 1, s, &removed));
+  XS_TRY(ws(ctx, W_SHORTFALL, (int64_t)np * 4 + 1, s, &shortfall));
+  XS_TRY(ws(ctx, W_PTOTAL, np + 1, s, &ptotal));
+  XS_TRY(ws(ctx, W_SLAB_BASE, np + 2, s, &slab_base));
+  XS_TRY(ws(ctx, W_PID_SLABS, np + 1, s, &pid_slabs));
+  XS_CUDA(cudaMemsetAsync(removed, 0, ((int64_t)np * 4 + 1) * 8, s));
+  XS_CUDA(cudaMemsetAsync(shortfall, 0, ((int64_t)np * 4 + 1) * 8, s));
+  XS_CUDA(cudaMemsetAsync(ptotal, 0, (np + 1) * 8, s));
+  XS_CUDA(cudaMemsetAsync(pid_slabs, 0, (np + 1) * 4, s));
+  XS_LAUNCH(ctx, k_zero_pad, 1, 32, 0, s, st);
+  XS_LAUNCH(ctx, k_totals, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, np, st, 1);
+
+  // 1. hook sites, compacted in event-index order
+  int *cnt, *pos;
+  XS_TRY(ws(ctx, W_SITE_CNT, n + 1, s, &cnt));
+  XS_TRY(ws(ctx, W_SITE_POS, n + 1, s, &pos));
+  int64_t ns = 0;
+  if (n) {
+    XS_LAUNCH(ctx, k_site_count, grid_for(n), XS_BLOCK, 0, s, v, n, tflag, cnt);
+    size_t temp = 0;
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, cnt, pos, (int)n, s));
+    void* t;
+    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, cnt, pos, (int)n, s));
+    ctx->launches += 2;
+    int last_pos = 0, last_cnt = 0;
+    XS_CUDA(cudaMemcpyAsync(&last_pos, pos + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    XS_CUDA(cudaMemcpyAsync(&last_cnt, cnt + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    XS_CUDA(cudaStreamSynchronize(s));
+    ns = (int64_t)last_pos + last_cnt;
+  }
+  ctx->corr_sites = ns;
+  int64_t *slab_a, *slab_b, *slab_pre;
+  XS_TRY(ws(ctx, W_SLAB_A, ns + 1, s, &slab_a));
+  XS_TRY(ws(ctx, W_SLAB_B, ns + 1, s, &slab_b));
+  XS_TRY(ws(ctx, W_SLAB_PRE, ns + 1, s, &slab_pre));
+  if (ns > 0) {
+    int* site_ev;
+    uint8_t* site_sub;
+    uint64_t *k1, *k1_alt;
+    uint32_t *sl, *sl_alt;
+    XS_TRY(ws(ctx, W_SITE_K, ns + 1, s, &k1));
+    XS_TRY(ws(ctx, W_SITE_K_ALT, ns + 1, s, &k1_alt));
+    XS_TRY(ws(ctx, W_SITE_V, ns + 1, s, &sl));
+    XS_TRY(ws(ctx, W_SITE_V_ALT, ns + 1, s, &sl_alt));
+    XS_TRY(ws(ctx, W_SITE_EV, ns + 1, s, &site_ev));
+    XS_TRY(ws(ctx, W_SITE_SUB, ns + 1, s, &site_sub));
+    XS_LAUNCH(ctx, k_site_gen, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, lo, tb, nb, site_ev, site_sub, k1);
+    // 2. Site.order_key sort: (tid, name) then (pid, anchor, subkind), stable
+    XS_LAUNCH(ctx, k_iota_u32, grid_for(ns), XS_BLOCK, 0, s, sl, ns);
+    XS_TRY(sort_pairs_u64_u32(ctx, &k1, &k1_alt, &sl, &sl_alt, ns, gb + nb, s));
+    XS_LAUNCH(ctx, k_site_k1, grid_for(ns), XS_BLOCK, 0, s, v, sl, ns, site_ev, site_sub, lo, tb, k1);
+    XS_TRY(sort_pairs_u64_u32(ctx, &k1, &k1_alt, &sl, &sl_alt, ns, pb + tb + 3, s));
+    XS_LAUNCH(ctx, k_tie_fix, grid_for(ns), XS_BLOCK, 0, s, v, k1, sl, ns, site_ev);
+    // 3. exact quantization (segmented int128 scan)
+    int64_t *qslot, *lenslot;
+    XS_TRY(ws(ctx, W_LENSLOT, ns + 1, s, &lenslot));
+    XS_TRY(ws(ctx, W_QVAL, ns + 1, s, &qslot));
+    {
+      const int64_t tiles = (ns + XS_BLOCK * Q_ITEMS - 1) / (XS_BLOCK * Q_ITEMS);
+      TileDesc<SegI128>* desc;
+      int *flags, *tctr;
+      XS_TRY(ws(ctx, W_QSCAN_DESC, tiles + 1, s, &desc));
+      XS_TRY(ws(ctx, W_QSCAN_FLAGS, tiles + 1, s, &flags));
+      XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
+      XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
+      XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+      XS_LAUNCH(ctx, k_quantize, (int)tiles, XS_BLOCK, 0, s, k1, sl, ns, tb, v, *prof, site_ev, site_sub, qslot, desc,
+                flags, tctr);
+    }
+    // 4. budget caps per owner
+    XS_LAUNCH(ctx, k_caps, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, qslot, lenslot, shortfall);
+    // 5. RemovalMap scan + removed accounting + nonzero slab compaction
+    {
+      const int64_t tiles = (ns + XS_BLOCK * R_ITEMS - 1) / (XS_BLOCK * R_ITEMS);
+      TileDesc<RM>* desc;
+      int *flags, *tctr;
+      XS_TRY(ws(ctx, W_RSCAN_DESC, tiles + 1, s, &desc));
+      XS_TRY(ws(ctx, W_RSCAN_FLAGS, tiles + 1, s, &flags));
+      XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
+      XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
+      XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+      XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, ns, tb, lenslot, site_sub, lo, hi, removed,
+                slab_a, slab_b, slab_pre, pid_slabs, ptotal, desc, flags, tctr);
+    }
+  }
+  XS_LAUNCH(ctx, k_slab_base, 1, 32, 0, s, pid_slabs, np, slab_base);
+  // 6. remap every event (positional, correction.py:158-165)
+  if (n)
+    XS_LAUNCH(ctx, k_remap, grid_for(n), XS_BLOCK, 0, s, v, n, lo, slab_a, slab_b, slab_pre, slab_base, ptotal,
+              out_start, out_dur);
+  if (corrected_spans) {
+    int64_t *lo2, *hi2;
+    XS_TRY(ws(ctx, W_OUT_LO, np + 1, s, &lo2));
+    XS_TRY(ws(ctx, W_OUT_HI, np + 1, s, &hi2));
+    XS_LAUNCH(ctx, k_init_span, grid_for(np + 1), XS_BLOCK, 0, s, lo2, hi2, np);
+    if (n) XS_LAUNCH(ctx, k_out_spans, grid_for(n), XS_BLOCK, 0, s, v.ev.pid, n, out_start, out_dur, lo2, hi2);
+    XS_LAUNCH(ctx, k_totals, grid_for(np + 1), XS_BLOCK, 0, s, lo2, hi2, np, st, 2);
+  }
+  XS_TRY(fetch_stats(ctx, s));
+  ctx->corr_pids = np;
+  ctx->corr_original_total = ctx->h_stats->pad[1];
+  ctx->corr_corrected_total = ctx->h_stats->pad[2];
+  {
+    int64_t h_base = 0;
+    XS_CUDA(cudaMemcpyAsync(&h_base, slab_base + np, 8, cudaMemcpyDeviceToHost, s));
+    XS_CUDA(cudaStreamSynchronize(s));
+    ctx->corr_slabs = h_base;
+  }
+  return XS_OK;
+}
+
 }  // namespace xs
+
+using namespace xs;
+
 extern "C" {
-int xs_transition_sites(xs_ctx_t* ctx, const xs_events_t*, int, int64_t*, xs_stream_t) { return XS_UNSUPPORTED; }
-int xs_transition_fetch(xs_ctx_t* ctx, int32_t*, int64_t*, xs_stream_t) { return XS_UNSUPPORTED; }
-int xs_remap(xs_ctx_t* ctx, int64_t, const int32_t*, const int64_t*, int64_t*, xs_stream_t) { return XS_UNSUPPORTED; }
+
+int xs_remap(xs_ctx_t* ctx, int64_t n, const int32_t* pid_dev, const int64_t* val_dev, int64_t* out_dev,
+             xs_stream_t stream) {
+  if (!ctx || !ctx->have_correct) return XS_BAD_ARGUMENT;
+  if (n <= 0) return XS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  XS_LAUNCH(ctx, k_remap_queries, grid_for(n), XS_BLOCK, 0, s, n, pid_dev, val_dev, out_dev,
+            (const int64_t*)ctx->ptr[W_CORR_LO], (const int64_t*)ctx->ptr[W_SLAB_A],
+            (const int64_t*)ctx->ptr[W_SLAB_B], (const int64_t*)ctx->ptr[W_SLAB_PRE],
+            (const int64_t*)ctx->ptr[W_SLAB_BASE], (const int64_t*)ctx->ptr[W_PTOTAL], ctx->corr_pids);
+  return XS_OK;
 }
+
+}  // extern "C"

@@ -53,6 +53,10 @@ enum Slot : int {
   // correlation
   W_FIXED_LS, W_FIXED_PATH, W_PIECE_KEY, W_FX_KEY, W_FX_KEY_ALT, W_FX_VAL, W_FX_VAL_ALT,
   W_FXSCAN_DESC, W_FXSCAN_FLAGS, W_FX_OWN, W_RANK_EV,
+  // correction (dedicated: xs_remap reads them after an xs_analyze overlap pass)
+  W_CORR_LO, W_CORR_HI, W_PTOTAL, W_PID_SLABS, W_SITE_EV, W_SITE_SUB, W_QVAL, W_OUT_LO, W_OUT_HI,
+  // transitions
+  W_TSKEY, W_TSKEY_ALT, W_HEADPOS, W_TREC_ID, W_TREC_ID_ALT,
   W_NUM_SLOTS
 };
 

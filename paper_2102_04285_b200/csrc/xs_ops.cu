@@ -507,17 +507,19 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   int* pidpath;
   XS_TRY(ws(ctx, W_PIDPATH, 2 * m + 2, s, &pidpath));
   os.pidpath = pidpath;
+  uint64_t *pk, *pk_alt;
+  XS_TRY(ws(ctx, W_PK, 2 * m + 2, s, &pk));
+  XS_TRY(ws(ctx, W_PK_ALT, 2 * m + 2, s, &pk_alt));
+  // op endpoints relabelled group -> pid (monotone, so order is kept)
+  XS_LAUNCH(ctx, k_pid_keys, grid_for(2 * m), XS_BLOCK, 0, s, sk, 2 * m, v.ev.group_pid, tb, pk);
   if (ctx->h_stats->multi_op_pids == 0) {
+    // one op tid per pid: pid order == group order
     XS_LAUNCH(ctx, k_pidpath_simple, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, 2 * m, parent, node, pidpath);
-    os.pk = sk;  // group order == pid order; time bits identical
+    os.pk = pk;
   } else {
-    uint64_t *pk, *pk_alt;
     int64_t* gs_off;
-    XS_TRY(ws(ctx, W_PK, 2 * m + 2, s, &pk));
-    XS_TRY(ws(ctx, W_PK_ALT, 2 * m + 2, s, &pk_alt));
     XS_TRY(ws(ctx, W_GS_OFF, ng + 1, s, &gs_off));
     XS_LAUNCH(ctx, k_gs_off, 1, 32, 0, s, group_ops, ng, gs_off);
-    XS_LAUNCH(ctx, k_pid_keys, grid_for(2 * m), XS_BLOCK, 0, s, sk, 2 * m, v.ev.group_pid, tb, pk);
     XS_TRY(sort_keys_u64(ctx, &pk, &pk_alt, 2 * m, pb + tb + 1, s));
     XS_LAUNCH(ctx, k_pidpath_general, grid_for(2 * m, 128), 128, 0, s, pk, 2 * m, tb, (int*)ctx->ptr[W_PID_GROUP0],
               group_ops, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st);
