@@ -1,0 +1,436 @@
+#!/usr/bin/env python3
+"""Benchmark: trace events/sec analysed (overlap + correction) on B200.
+
+Workload (BASELINE.json configs[1]): a synthetic DDPG-style instrumented trace
+of ~1M events per GPU (3 operation scopes; Python/C/CUDA-API/GPU-kernel
+categories) corrected with the calibrated integer profile {annotation 4000,
+transition 1000, api_interception 1500, launch 3000, memcpy 1000}; one step is
+the ``xstrace analyze --profile`` path: correct_trace + compute_overlap of the
+corrected trace (cli.py:168-171), one ``xs_analyze`` device call.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 runs under torch.distributed.run, one process per GPU; each rank analyses
+its own ~1M-event process (weak scaling) and the per-rank overlap histograms
+are merged with an NCCL all-reduce keyed by a global path table.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ITERATIONS = 27027  # ~1M events per process
+METRIC = "trace events/sec analysed (overlap+correction)"
+UNIT = "events/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iterations", type=int, default=ITERATIONS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_trace(iterations: int, rank: int):
+    """Rank r analyses process r+1 (distinct seed): a weak-scaling shard."""
+    from paper_2102_04285_b200 import synth
+    from paper_2102_04285_b200.columnar import ColumnarTrace
+    from paper_2102_04285_b200.model import ProcessMeta
+
+    ct = synth.ddpg_trace(iterations, processes=1, seed=1234 + rank)
+    if rank:
+        ct = ColumnarTrace(ct.clock_domain, ct.start, ct.dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr,
+                           ct.pids + rank, ct.group_pid, ct.group_tid, ct.names,
+                           tuple(ProcessMeta(m.pid + rank, m.name, m.parent, m.fork_ns, m.join_ns)
+                                 for m in ct.processes), ct.pid_has_meta)
+    return ct
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def stage_bytes(stage: str, n: int, nnz: int, ns: int, key_bits_main: int, key_bits_site: int) -> float:
+    """Algorithmic DRAM bytes of one occurrence of a stage ('Roofline')."""
+    def passes(bits):
+        return max(1, -(-bits // 8))
+    if stage == "endpoint_sort":   # keys-only onesweep over 2n keys: 1 histogram read + P x (read+write)
+        return 2 * n * (8 + 16 * passes(key_bits_main))
+    if stage == "sweep_scan_hist":  # one read of the sorted nonzero endpoints
+        return 2 * nnz * 8
+    if stage == "endpoint_keygen":  # read start/dur/pid/cat/has_corr, write 2 keys
+        return n * (8 + 8 + 4 + 1 + 1) + 2 * n * 8
+    if stage == "site_sort":        # two (key8,val4) pair sorts over the sites + generation
+        return 2 * ns * (8 + 24 * passes(key_bits_site)) + n * 21
+    if stage == "remap":            # read start/dur/pid/cat, write start'/dur'
+        return n * (8 + 8 + 4 + 1) + n * 16
+    if stage == "quantize_scan":
+        return ns * (8 + 4 + 4 + 1 + 8)
+    if stage == "removal_scan":
+        return ns * (8 + 4 + 8 + 1) + ns * 24
+    if stage == "pass1_validate_spans":
+        return n * (8 + 8 + 4 + 4 + 1 + 1 + 4)
+    return 0.0
+
+
+def traffic_from_profiles(stage: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get(stage)
+
+
+def cpu_baseline_port(ct, profile, seconds: float):
+    """The C restatement (oracle/) of correct_trace + compute_overlap(corrected):
+    the reference algorithm, compiled, one thread (the trace is one pid)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    from paper_2102_04285_b200.columnar import ColumnarTrace
+
+    t0 = time.perf_counter()
+    runs = 0
+    while True:
+        s, d, _rep, _ = oracle.correct(ct, profile)
+        ct2 = ColumnarTrace(ct.clock_domain, s, d, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr, ct.pids,
+                            ct.group_pid, ct.group_tid, ct.names, ct.processes, ct.pid_has_meta)
+        oracle.overlap(ct2, 0)
+        runs += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": runs * ct.n / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{runs} x full {ct.n}-event trace, oracle/xs_oracle.c correct+overlap, {dt:.1f}s"}
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    from paper_2102_04285_b200 import _engine, synth
+    from paper_2102_04285_b200.distributed import merge_breakdown_raw
+    from paper_2102_04285_b200.overlap import decode_breakdown
+
+    ct = make_trace(args.iterations, rank)
+    profile = synth.exact_profile()
+    scaled = profile.scaled(ct.names)
+    eng = _engine.get(local)
+    dt_dev = _engine.DeviceTrace(ct, local)
+    n = ct.n
+    nnz = int((ct.dur > 0).sum())
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step_device():
+        raw = eng.correct(dt_dev, scaled, analyze_attribution=0)
+        merged = None
+        if world > 1:
+            merged = merge_breakdown_raw(ct, eng.fetch_overlap(), dev)
+        return raw, merged
+
+    # warmup + correctness spot check against the closure property
+    for _ in range(max(args.warmup, 1)):
+        raw, _ = step_device()
+    torch.cuda.synchronize()
+    launches0 = eng.launches()
+    eng.lib.xs_profile_enable(eng.ctx, 1)
+    times = []
+    stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # L2 flush between steps (inputs 37 MB < L2)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step_device()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    launches = eng.launches() - launches0
+    ms_arr = np.zeros(32)
+    calls_arr = np.zeros(32, np.int64)
+    nst = eng.lib.xs_profile_read(eng.ctx, ms_arr.ctypes.data, calls_arr.ctypes.data, 32)
+    eng.lib.xs_profile_enable(eng.ctx, 0)
+    stage_names = [eng.lib.xs_profile_stage_name(i).decode() for i in range(nst)]
+    total_ms = float(np.sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    total_events = n * world
+    value = total_events / (ms_per_step / 1e3)
+
+    # end-to-end through the public API with host buffers (pinned)
+    host = {k: torch.from_numpy(np.ascontiguousarray(getattr(ct, k))).pin_memory()
+            for k in ("start", "dur", "pid", "tid", "cat", "name", "corr", "has_corr", "group_pid", "pid_has_meta")}
+    out_s = torch.empty(n, dtype=torch.int64).pin_memory()
+    out_d = torch.empty(n, dtype=torch.int64).pin_memory()
+    h2d = sum(int(t.numel() * t.element_size()) for t in host.values())
+
+    def step_e2e():
+        tens = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+        dtr = _engine.DeviceTrace.from_tensors(ct, tens, local)
+        raw = eng.correct(dtr, scaled, analyze_attribution=0)
+        ov = eng.fetch_overlap()
+        out_s.copy_(raw.start, non_blocking=True)
+        out_d.copy_(raw.dur, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        d2h = 16 * n + ov.cell_ns.nbytes * 3 + ov.node_parent.nbytes * 2 + 8 * 4 * ct.n_pids * 2
+        bd = decode_breakdown(ct, ov)
+        return d2h, bd
+
+    for _ in range(2):
+        step_e2e()
+    e2e_ms = []
+    d2h = 0
+    for _ in range(max(3, args.steps // 2)):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h, bd = step_e2e()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_step = float(np.median(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
+
+    # correctness of the measured step: closure against the uninstrumented twin
+    un = synth.ddpg_trace(args.iterations, processes=1, seed=1234 + rank, both=True)[0]
+    closure_ok = bool(np.array_equal(out_s.numpy(), un.start) and np.array_equal(out_d.numpy(), un.dur))
+
+    # roofline for the dominant stage
+    peak, peak_kind = load_peaks()
+    tb = int(max(1, int((ct.start + ct.dur).max() - ct.start.min())).bit_length())
+    key_bits_main = tb + 4 + max(0, (ct.n_pids - 1).bit_length())
+    key_bits_site = tb + 3 + max(0, (ct.n_pids - 1).bit_length())
+    stages = {}
+    for i, nm in enumerate(stage_names):
+        if calls_arr[i]:
+            stages[nm] = {"ms_total": round(float(ms_arr[i]), 4), "occurrences": int(calls_arr[i]),
+                          "ms_avg": round(float(ms_arr[i]) / int(calls_arr[i]), 5)}
+    import ctypes as C
+    from paper_2102_04285_b200 import _lib
+    info = _lib.XsCorrectInfo()
+    eng.lib.xs_correct_report(eng.ctx, C.byref(info), None, None, eng.stream())
+    ns_sites = int(info.n_sites)
+    dom = max(stages, key=lambda k: stages[k]["ms_total"]) if stages else None
+    roof = None
+    if dom:
+        algo = stage_bytes(dom, n, nnz, ns_sites, key_bits_main, key_bits_site)
+        achieved = algo / (stages[dom]["ms_avg"] / 1e3) / 1e9 if algo else None
+        tr = traffic_from_profiles(dom)
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": round(achieved / peak, 4) if achieved else None,
+                "algorithmic_bytes_per_launch": algo, "traffic": tr,
+                "share_of_step": round(stages[dom]["ms_total"] / total_ms, 3) if total_ms else None}
+    pipe_bytes = sum(stage_bytes(k, n, nnz, ns_sites, key_bits_main, key_bits_site) * v["occurrences"]
+                     for k, v in stages.items()) / args.steps
+    pipeline = {"model_bytes_per_event": round(pipe_bytes / n, 1),
+                "achieved_GBps": round(pipe_bytes / (ms_per_step / 1e3) / 1e9, 1),
+                "compulsory_bytes_per_event": 45 + 21}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_port(ct, profile, args.cpu_seconds)
+        cpu["cores_available"] = os.cpu_count()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": "config2: DDPG-style instrumented trace, ~1M events/GPU, 3 operation scopes, "
+                                   "integer calibrated profile; step = correct_trace + compute_overlap(corrected)",
+                       "events_per_gpu": n, "events_total": total_events, "attribution": "instant",
+                       "l2": "flushed (256 MB write) between timed steps; inputs 37 MB/GPU",
+                       "parallelism": f"pid-sharded x{world}" + (", NCCL all-reduce histogram merge" if world > 1
+                                                                   else "")},
+            "e2e": {"value": round(total_events / (e2e_step / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_step, 3),
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
+                    "path": "host pinned columns -> H2D -> xs_analyze -> D2H corrected trace + cells"},
+            "gpu_launches": int(launches / args.steps),
+            "roofline": roof, "pipeline_roofline": pipeline, "stages_ms": stages,
+            "cpu_baseline": cpu, "clocks": clocks.summary(), "closure_exact": closure_ok,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    sample_iters = max(1, args.iterations // 10)
+    if os.path.isdir(os.path.join(ref, "xstrace")):
+        sys.path.insert(0, ref)
+        from xstrace.correction import correct_trace as ref_correct
+        from xstrace.overlap import HAVE_NATIVE_SWEEP, compute_overlap as ref_overlap
+        from xstrace import model as RM
+        from xstrace.calibration import CalibrationProfile as RP
+        from paper_2102_04285_b200 import synth
+
+        ct = make_trace(sample_iters, 0)
+        cats = [RM.Category(c) for c in range(6)]
+        names = ct.names
+        events = [RM.Event(int(ct.pids[p]), int(ct.group_tid[g]), cats[c], names[nm], s, d, k if h else None)
+                  for p, g, c, nm, s, d, k, h in zip(ct.pid.tolist(), ct.tid.tolist(), ct.cat.tolist(),
+                                                     ct.name.tolist(), ct.start.tolist(), ct.dur.tolist(),
+                                                     ct.corr.tolist(), ct.has_corr.tolist())]
+        trace = RM.Trace(ct.clock_domain, events, [RM.ProcessMeta(m.pid, m.name, m.parent, m.fork_ns, m.join_ns)
+                                                    for m in ct.processes])
+        p = synth.exact_profile()
+        prof = RP(p.annotation_ns, p.transition_ns, p.api_interception_ns, dict(p.api_internal_ns))
+
+        def step():
+            out, _ = ref_correct(trace, prof)
+            ref_overlap(out)
+
+        kind, cores = "reference", 1
+        sample = (f"{ct.n}-event DDPG trace ({sample_iters} iterations, 1/10 of the 1M workload), "
+                  f"reference xstrace correct_trace + compute_overlap, native sweep={HAVE_NATIVE_SWEEP}")
+        n_ev = ct.n
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+        from paper_2102_04285_b200 import synth
+
+        ct = make_trace(args.iterations, 0)
+        p = synth.exact_profile()
+
+        from paper_2102_04285_b200.columnar import ColumnarTrace
+
+        def step():
+            s, d, _, _ = oracle.correct(ct, p)
+            oracle.overlap(ColumnarTrace(ct.clock_domain, s, d, ct.pid, ct.tid, ct.cat, ct.name, ct.corr,
+                                         ct.has_corr, ct.pids, ct.group_pid, ct.group_tid, ct.names,
+                                         ct.processes, ct.pid_has_meta), 0)
+
+        kind, cores, n_ev = "port", 1, ct.n
+        sample = f"{ct.n}-event trace, oracle C port (reference not built here)"
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = n_ev * args.steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": "config2: DDPG-style instrumented trace, calibrated integer profile; "
+                               "step = correct_trace + compute_overlap(corrected)", "events_per_step": n_ev},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                         "cores_available": os.cpu_count()},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -149,6 +149,13 @@ int xs_transition_fetch(xs_ctx_t* ctx, int32_t* pair, int64_t* event, xs_stream_
  * (instrumentation for the bench's gpu_launches field). */
 int64_t xs_launch_count(xs_ctx_t* ctx);
 
+/* Per-stage device timing with CUDA events recorded on the launching stream
+ * (bench/roofline instrumentation).  enable resets the counters; read returns
+ * the number of stages and fills accumulated milliseconds / occurrences. */
+int xs_profile_enable(xs_ctx_t* ctx, int on);
+int xs_profile_read(xs_ctx_t* ctx, double* ms, int64_t* calls, int n);
+const char* xs_profile_stage_name(int stage);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,9 @@ SIGNATURES = {
     "xs_transition_sites": (C.c_int, [P, C.POINTER(XsEvents), C.c_int, C.POINTER(C.c_int64), P]),
     "xs_transition_fetch": (C.c_int, [P, P, P, P]),
     "xs_launch_count": (C.c_int64, [P]),
+    "xs_profile_enable": (C.c_int, [P, C.c_int]),
+    "xs_profile_read": (C.c_int, [P, P, P, C.c_int]),
+    "xs_profile_stage_name": (C.c_char_p, [C.c_int]),
 }
 
 _lib = None

@@ -467,6 +467,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
   XS_TRY(ws(ctx, W_SITE_CNT, n + 1, s, &cnt));
   XS_TRY(ws(ctx, W_SITE_POS, n + 1, s, &pos));
   int64_t ns = 0;
+  ProfScope ps_sites(ctx, ST_SITE_SORT, s);
   if (n) {
     XS_LAUNCH(ctx, k_site_count, grid_for(n), XS_BLOCK, 0, s, v, n, tflag, cnt);
     size_t temp = 0;
@@ -504,6 +505,8 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     XS_LAUNCH(ctx, k_site_k1, grid_for(ns), XS_BLOCK, 0, s, v, sl, ns, site_ev, site_sub, lo, tb, k1);
     XS_TRY(sort_pairs_u64_u32(ctx, &k1, &k1_alt, &sl, &sl_alt, ns, pb + tb + 3, s));
     XS_LAUNCH(ctx, k_tie_fix, grid_for(ns), XS_BLOCK, 0, s, v, k1, sl, ns, site_ev);
+    ps_sites.end();
+    ProfScope ps_q(ctx, ST_QUANTIZE, s);
     // 3. exact quantization (segmented int128 scan)
     int64_t *qslot, *lenslot;
     XS_TRY(ws(ctx, W_LENSLOT, ns + 1, s, &lenslot));
@@ -520,7 +523,9 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
       XS_LAUNCH(ctx, k_quantize, (int)tiles, XS_BLOCK, 0, s, k1, sl, ns, tb, v, *prof, site_ev, site_sub, qslot, desc,
                 flags, tctr);
     }
+    ps_q.end();
     // 4. budget caps per owner
+    ProfScope ps_r(ctx, ST_REMOVAL, s);
     XS_LAUNCH(ctx, k_caps, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, qslot, lenslot, shortfall);
     // 5. RemovalMap scan + removed accounting + nonzero slab compaction
     {
@@ -537,7 +542,9 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     }
   }
   XS_LAUNCH(ctx, k_slab_base, 1, 32, 0, s, pid_slabs, np, slab_base);
+  ps_sites.end();
   // 6. remap every event (positional, correction.py:158-165)
+  ProfScope ps_m(ctx, ST_REMAP, s);
   if (n)
     XS_LAUNCH(ctx, k_remap, grid_for(n), XS_BLOCK, 0, s, v, n, lo, slab_a, slab_b, slab_pre, slab_base, ptotal,
               out_start, out_dur);

@@ -32,6 +32,7 @@ int fetch_stats(xs_ctx* ctx, cudaStream_t s) {
   XS_TRY(ws(ctx, W_STATS, 1, s, &d));
   XS_CUDA(cudaMemcpyAsync(ctx->h_stats, d, sizeof(Stats), cudaMemcpyDeviceToHost, s));
   XS_CUDA(cudaStreamSynchronize(s));
+  if (!ctx->pend_stage.empty()) prof_flush(ctx);
   return XS_OK;
 }
 
@@ -310,5 +311,69 @@ int xs_transition_sites(xs_ctx_t* ctx, const xs_events_t* ev, int pair_mask, int
 int xs_transition_fetch(xs_ctx_t* ctx, int32_t* pair, int64_t* event, xs_stream_t stream);
 int xs_remap(xs_ctx_t* ctx, int64_t n, const int32_t* pid_dev, const int64_t* val_dev, int64_t* out_dev,
              xs_stream_t stream);
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// per-stage device timing
+// ---------------------------------------------------------------------------
+namespace xs {
+
+cudaEvent_t prof_event(xs_ctx* ctx) {
+  // events in flight are never reused before prof_flush
+  if (ctx->pool_next == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[ctx->pool_next++];
+}
+
+void prof_flush(xs_ctx* ctx) {
+  for (size_t k = 0; k < ctx->pend_stage.size(); k++) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(ctx->pend_b[k]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, ctx->pend_a[k], ctx->pend_b[k]) == cudaSuccess) {
+      ctx->prof_ms[ctx->pend_stage[k]] += ms;
+      ctx->prof_calls[ctx->pend_stage[k]] += 1;
+    }
+  }
+  ctx->pend_stage.clear();
+  ctx->pend_a.clear();
+  ctx->pend_b.clear();
+  if (ctx->prof_active == 0) ctx->pool_next = 0;  // an open scope still owns its start event
+}
+
+}  // namespace xs
+
+extern "C" {
+
+static const char* kStageNames[xs::ST_NUM] = {
+    "pass1_validate_spans", "operation_paths", "transition_sort", "transition_scan", "site_sort",
+    "quantize_scan",        "removal_scan",    "remap",           "endpoint_keygen", "endpoint_sort",
+    "sweep_scan_hist",      "cell_compact",    "correlation_prepass"};
+
+int xs_profile_enable(xs_ctx_t* ctx, int on) {
+  if (!ctx) return XS_BAD_ARGUMENT;
+  xs::prof_flush(ctx);
+  ctx->prof_on = on != 0;
+  for (int i = 0; i < 32; i++) {
+    ctx->prof_ms[i] = 0;
+    ctx->prof_calls[i] = 0;
+  }
+  return XS_OK;
+}
+
+int xs_profile_read(xs_ctx_t* ctx, double* ms, int64_t* calls, int n) {
+  if (!ctx) return XS_BAD_ARGUMENT;
+  xs::prof_flush(ctx);
+  for (int i = 0; i < n && i < xs::ST_NUM; i++) {
+    if (ms) ms[i] = ctx->prof_ms[i];
+    if (calls) calls[i] = ctx->prof_calls[i];
+  }
+  return xs::ST_NUM;
+}
+
+const char* xs_profile_stage_name(int i) { return (i >= 0 && i < xs::ST_NUM) ? kStageNames[i] : ""; }
 
 }  // extern "C"

@@ -162,7 +162,50 @@ struct xs_ctx {
   long long n_trans_out = 0;
   int trie_cap_log2 = 12;
   xs::OpsState ops;
+  // optional per-stage device timing (CUDA events on the launching stream)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t pool_next = 0;
+  int prof_active = 0;
+  std::vector<int> pend_stage;
+  std::vector<cudaEvent_t> pend_a, pend_b;
+  double prof_ms[32] = {0};
+  long long prof_calls[32] = {0};
 };
+
+namespace xs {
+enum Stage : int {
+  ST_PASS1 = 0, ST_OPS, ST_TRANS_SORT, ST_TRANS_SCAN, ST_SITE_SORT, ST_QUANTIZE, ST_REMOVAL, ST_REMAP,
+  ST_KEYGEN, ST_MAIN_SORT, ST_SWEEP, ST_COMPACT, ST_CORR_FX, ST_NUM
+};
+cudaEvent_t prof_event(xs_ctx* ctx);
+void prof_flush(xs_ctx* ctx);
+struct ProfScope {  // records [begin, end) of one stage on stream s when profiling is on
+  xs_ctx* c;
+  int stage;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  ProfScope(xs_ctx* c_, int st, cudaStream_t s_) : c(c_), stage(st), s(s_) {
+    if (c->prof_on) {
+      a = prof_event(c);
+      cudaEventRecord(a, s);
+      c->prof_active++;
+    }
+  }
+  void end() {
+    if (a) {
+      cudaEvent_t b = prof_event(c);
+      cudaEventRecord(b, s);
+      c->pend_stage.push_back(stage);
+      c->pend_a.push_back(a);
+      c->pend_b.push_back(b);
+      c->prof_active--;
+      a = nullptr;
+    }
+  }
+  ~ProfScope() { end(); }
+};
+}  // namespace xs
 
 namespace xs {
 

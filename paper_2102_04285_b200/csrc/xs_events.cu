@@ -266,6 +266,7 @@ int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr
   XS_LAUNCH(ctx, k_init_pid, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, pid_ops, np + 1);
   XS_CUDA(cudaMemsetAsync(group_ops, 0, (ng + 1) * sizeof(int), s));
   if (n > 0) {
+    ProfScope ps(ctx, ST_PASS1, s);
     const uint8_t* hasint = (check_api && prof) ? prof->has_internal : nullptr;
     int check = (check_api && prof && ev->n_names > 0 && hasint) ? 1 : 0;
     if (check_api && prof && !hasint) check = 0;

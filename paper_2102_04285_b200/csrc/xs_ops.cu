@@ -375,6 +375,7 @@ int trie_setup(xs_ctx* ctx, cudaStream_t s, TrieView* t) {
 }
 
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths) {
+  ProfScope ps(ctx, ST_OPS, s);
   const Stats& H = *ctx->h_stats;
   const int64_t m = H.n_ops_nz;
   const int np = v.ev.n_pids, ng = v.ev.n_groups;

@@ -345,6 +345,7 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   uint64_t* pieces = nullptr;
   int64_t piece_cap = 0;
   if (corr_mode) {
+    ProfScope ps(ctx, ST_CORR_FX, s);
     const int nodeb = bits_for((uint64_t)(n_nodes - 1));
     if (pb + nodeb + tb + 2 > 64) {
       ctx->err = "CORRELATION keys too wide";
@@ -393,9 +394,15 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   uint64_t *mk, *mk_alt;
   XS_TRY(ws(ctx, W_MKEY, nkeys + SW_TILE, s, &mk));
   XS_TRY(ws(ctx, W_MKEY_ALT, nkeys + SW_TILE, s, &mk_alt));
-  if (n) XS_LAUNCH(ctx, k_keygen, grid_for(n), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, sentinel, mk);
-  if (n_piece_keys) XS_CUDA(cudaMemcpyAsync(mk + 2 * n, pieces, n_piece_keys * 8, cudaMemcpyDeviceToDevice, s));
-  XS_TRY(sort_keys_u64(ctx, &mk, &mk_alt, nkeys, key_bits, s));
+  {
+    ProfScope ps(ctx, ST_KEYGEN, s);
+    if (n) XS_LAUNCH(ctx, k_keygen, grid_for(n), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, sentinel, mk);
+    if (n_piece_keys) XS_CUDA(cudaMemcpyAsync(mk + 2 * n, pieces, n_piece_keys * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  {
+    ProfScope ps(ctx, ST_MAIN_SORT, s);
+    XS_TRY(sort_keys_u64(ctx, &mk, &mk_alt, nkeys, key_bits, s));
+  }
   const int64_t nvalid = 2 * H.n_nonzero + n_piece_keys;
   if (nvalid > 0) {
     const int64_t tiles = (nvalid + SW_TILE - 1) / SW_TILE;
@@ -406,6 +413,7 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
     XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
     XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
     XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+    ProfScope ps(ctx, ST_SWEEP, s);
     XS_LAUNCH(ctx, k_sweep, (int)tiles, XS_BLOCK, 0, s, mk, nvalid, tb, os.pidpath, os.opbase, n_nodes, hist, desc,
               flags, tctr);
   }
@@ -422,6 +430,7 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   XS_TRY(ws(ctx, W_CELL_COUNT, 1, s, &ccount));
   XS_CUDA(cudaMemsetAsync(tracked, 0, (np + 1) * 8, s));
   XS_CUDA(cudaMemsetAsync(ccount, 0, 8, s));
+  ProfScope ps_compact(ctx, ST_COMPACT, s);
   if (hist_n)
     XS_LAUNCH(ctx, k_compact_cells, grid_for(hist_n), XS_BLOCK, 0, s, hist, hist_n, n_nodes, cp, cn, cm, cns, tracked,
               ccount);

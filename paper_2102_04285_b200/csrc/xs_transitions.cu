@@ -221,6 +221,7 @@ int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mas
   uint32_t *rid, *rid_alt;
   XS_TRY(ws(ctx, W_TREC_ID, m + 1, s, &rid));
   XS_TRY(ws(ctx, W_TREC_ID_ALT, m + 1, s, &rid_alt));
+  ProfScope ps_sort(ctx, ST_TRANS_SORT, s);
   XS_LAUNCH(ctx, k_iota_u32, grid_for(m), XS_BLOCK, 0, s, rid, m);
   XS_TRY(sort_pairs_u64_u32(ctx, &skey, &skey_alt, &rid, &rid_alt, m, tb, s));
   XS_LAUNCH(ctx, k_tkey_gather, grid_for(m), XS_BLOCK, 0, s, key, rid, m, key_alt);
@@ -240,6 +241,8 @@ int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mas
   XS_TRY(ws(ctx, W_HEADPOS, m + 1, s, &headpos));
   XS_CUDA(cudaMemsetAsync(tflags, 0, (tiles + 1) * sizeof(int), s));
   XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+  ps_sort.end();
+  ProfScope ps(ctx, ST_TRANS_SCAN, s);
   XS_LAUNCH(ctx, k_tscan, (int)tiles, XS_BLOCK, 0, s, k1, v1, m, tb, v, site_flag, headpos, desc, tflags, tctr,
             src_mask);
   XS_LAUNCH(ctx, k_tdup, grid_for(m), XS_BLOCK, 0, s, v1, headpos, k1, m, site_flag);
