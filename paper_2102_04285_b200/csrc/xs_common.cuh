@@ -65,6 +65,119 @@ __device__ __forceinline__ void st_volatile_T(T* p, const T& v) {
   for (int i = 0; i < (int)(sizeof(T) / 4); i++) dst[i] = src[i];
 }
 
+// shuffle any 4-byte-multiple POD
+template <class T>
+__device__ __forceinline__ T shfl_up_T(const T& v, int d) {
+  T out;
+  const int* s = reinterpret_cast<const int*>(&v);
+  int* o = reinterpret_cast<int*>(&out);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 4); i++) o[i] = __shfl_up_sync(0xffffffffu, s[i], d);
+  return out;
+}
+template <class T>
+__device__ __forceinline__ T shfl_down_T(const T& v, int d) {
+  T out;
+  const int* s = reinterpret_cast<const int*>(&v);
+  int* o = reinterpret_cast<int*>(&out);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 4); i++) o[i] = __shfl_down_sync(0xffffffffu, s[i], d);
+  return out;
+}
+template <class T>
+__device__ __forceinline__ T shfl_idx_T(const T& v, int src) {
+  T out;
+  const int* s = reinterpret_cast<const int*>(&v);
+  int* o = reinterpret_cast<int*>(&out);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 4); i++) o[i] = __shfl_sync(0xffffffffu, s[i], src);
+  return out;
+}
+
+// Warp-parallel look-back (called by all 32 lanes of warp 0).  Lane k looks
+// at tile (pred - k); the window stops at the nearest inclusive prefix and the
+// aggregates in between are folded oldest-first (op may be non-commutative).
+template <class T, class Op>
+__device__ T lookback_warp(int tile, const T& agg, TileDesc<T>* desc, int* flags, Op op, const T& identity) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) {
+      st_volatile_T(&desc[0].incl, agg);
+      __threadfence();
+      flag_store(&flags[0], 2);
+    }
+    return identity;
+  }
+  if (lane == 0) {
+    st_volatile_T(&desc[tile].agg, agg);
+    __threadfence();
+    flag_store(&flags[tile], 1);
+  }
+  T excl = identity;
+  int pred = tile - 1;
+  while (true) {
+    const int idx = pred - lane;
+    int f = 2;
+    if (idx >= 0) {
+      int spins = 0;
+      while ((f = flag_load(&flags[idx])) == 0) {
+        if (++spins > 32) __nanosleep(20);
+      }
+    }
+    const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
+    const int stop = m2 ? (__ffs(m2) - 1) : 32;
+    T v = identity;
+    if (idx >= 0 && lane <= stop) v = (lane == stop) ? ld_volatile_T(&desc[idx].incl) : ld_volatile_T(&desc[idx].agg);
+    // ordered reduction: result = v[31] . v[30] . ... . v[0]  (older on the left)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T other = shfl_down_T(v, o);
+      if ((lane & (2 * o - 1)) == 0) v = op(other, v);
+    }
+    v = shfl_idx_T(v, 0);
+    excl = op(v, excl);
+    if (m2) break;
+    pred -= 32;
+  }
+  if (lane == 0) {
+    T incl = op(excl, agg);
+    st_volatile_T(&desc[tile].incl, incl);
+    __threadfence();
+    flag_store(&flags[tile], 2);
+  }
+  return excl;
+}
+
+// Block-wide exclusive scan with warp shuffles (2 barriers).
+template <class T, class Op>
+__device__ T block_exclusive_fast(T v, Op op, const T& identity, T* s_warp /*[32]*/, T* agg_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = XS_BLOCK / 32;
+  T incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T other = shfl_up_T(incl, o);
+    if (lane >= o) incl = op(other, incl);
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < NW ? s_warp[lane] : identity;
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+      T other = shfl_up_T(w, o);
+      if (lane >= o) w = op(other, w);
+    }
+    if (lane < NW) s_warp[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  T warp_pre = warp ? s_warp[warp - 1] : identity;
+  *agg_out = s_warp[NW - 1];
+  T excl_in_warp = shfl_up_T(incl, 1);
+  if (lane == 0) excl_in_warp = identity;
+  return op(warp_pre, excl_in_warp);
+}
+
 // Called by thread 0 only.  Returns the exclusive prefix of `tile`.
 template <class T, class Op>
 __device__ T lookback(int tile, const T& agg, TileDesc<T>* desc, int* flags, Op op, const T& identity) {
@@ -127,17 +240,92 @@ __device__ T block_exclusive(T v, Op op, const T& identity, T* s, T* agg_out) {
 // the exclusive prefix of its own value across the whole grid.
 template <class T, class Op>
 __device__ T grid_exclusive(T v, Op op, const T& identity, int tile, TileDesc<T>* desc, int* flags) {
-  __shared__ __align__(16) unsigned char s_raw[XS_BLOCK * sizeof(T)];
+  __shared__ __align__(16) unsigned char s_raw[32 * sizeof(T)];
   __shared__ __align__(16) unsigned char s_pref_raw[sizeof(T)];
   T* s = reinterpret_cast<T*>(s_raw);
   T* s_pref = reinterpret_cast<T*>(s_pref_raw);
   T agg;
-  T excl = block_exclusive(v, op, identity, s, &agg);
-  if (threadIdx.x == 0) *s_pref = lookback(tile, agg, desc, flags, op, identity);
+  T excl = block_exclusive_fast(v, op, identity, s, &agg);
+  if (threadIdx.x < 32) {
+    T pre = lookback_warp(tile, agg, desc, flags, op, identity);
+    if (threadIdx.x == 0) *s_pref = pre;
+  }
   __syncthreads();
   T pre = *s_pref;
   __syncthreads();
   return op(pre, excl);
+}
+
+// Warp-aggregated atomicAdd on one counter (all 32 lanes must call; lanes
+// with nothing to write pass k = 0).  Returns this lane's first slot.
+__device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* counter, unsigned k) {
+  const int lane = threadIdx.x & 31;
+  unsigned x = k;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  unsigned long long base = 0;
+  if (lane == 31 && x) base = atomicAdd(counter, (unsigned long long)x);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + (x - k);
+}
+
+// Keyed block reduction for per-pid totals: every thread passes its running
+// (key, v[NV]) (key < 0 = nothing).  Warps that agree on one key reduce with
+// shuffles and thread 0 merges equal keys across warps, so a block emits one
+// update per distinct key instead of one per thread.  All threads must call.
+template <int NV, class Emit>
+__device__ __forceinline__ void block_keyed_flush(int key, long long (&v)[NV], Emit emit) {
+  constexpr int NW = XS_BLOCK / 32;
+  __shared__ int s_key[NW];
+  __shared__ long long s_v[NW][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k0 = __shfl_sync(0xffffffffu, key, 0);
+  if (__all_sync(0xffffffffu, key == k0)) {
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    }
+    if (lane == 0) {
+      s_key[warp] = k0;
+#pragma unroll
+      for (int i = 0; i < NV; i++) s_v[warp][i] = v[i];
+    }
+  } else {
+    if (key >= 0) emit(key, v);
+    if (lane == 0) s_key[warp] = -1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ck = -1;
+    long long acc[NV];
+    for (int w = 0; w < NW; w++) {
+      if (s_key[w] < 0) continue;
+      if (s_key[w] != ck) {
+        if (ck >= 0) emit(ck, acc);
+        ck = s_key[w];
+#pragma unroll
+        for (int i = 0; i < NV; i++) acc[i] = 0;
+      }
+#pragma unroll
+      for (int i = 0; i < NV; i++) acc[i] += s_v[w][i];
+    }
+    if (ck >= 0) emit(ck, acc);
+  }
+  __syncthreads();
+}
+
+// Sum `v` over the warp for lanes whose key equals lane 0's key when the
+// whole warp agrees (returns true and the sum on lane 0); otherwise false.
+__device__ __forceinline__ bool warp_uniform_sum(int key, long long& v) {
+  const int k0 = __shfl_sync(0xffffffffu, key, 0);
+  if (!__all_sync(0xffffffffu, key == k0)) return false;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return true;
 }
 
 __device__ __forceinline__ int next_tile(int* counter) {

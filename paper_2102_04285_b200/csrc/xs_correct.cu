@@ -123,7 +123,7 @@ __device__ __forceinline__ int64_t site_amount(const xs_profile_t& pr, const Eve
   }
 }
 
-constexpr int Q_ITEMS = 4;
+constexpr int Q_ITEMS = 8;
 __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const uint32_t* slot, int64_t ns, int tb,
                                                        EventView v, xs_profile_t pr, const int* site_ev,
                                                        const uint8_t* site_sub, int64_t* qslot,
@@ -231,7 +231,7 @@ __device__ __forceinline__ int hook_of(int sub) {
   return sub == TRANSITION_HOOK ? H_TRANS : sub == API_INTERCEPT ? H_IC : sub == API_INTERNAL ? H_INT : H_ANN;
 }
 
-constexpr int R_ITEMS = 4;
+constexpr int R_ITEMS = 8;
 __global__ void __launch_bounds__(XS_BLOCK) k_removal(const uint64_t* k1, const uint32_t* slot, int64_t ns, int tb,
                                                       const int64_t* lenslot, const uint8_t* site_sub,
                                                       const int64_t* lo, const int64_t* hi, int64_t* removed,
@@ -304,12 +304,13 @@ __global__ void __launch_bounds__(XS_BLOCK) k_removal(const uint64_t* k1, const 
     RM e{len[j] > 0 ? len[j] : 0, anc[j] + len[j], len[j] > 0 ? 1 : 0, 0, 0};
     cur = op(cur, e);
   }
-  if (cp >= 0) {
+  long long fv[6] = {acc[0], acc[1], acc[2], acc[3], nsl, tot};
+  block_keyed_flush<6>(cp, fv, [&](int p, const long long* x) {
     for (int h = 0; h < 4; h++)
-      if (acc[h]) atomic_add_i64(&removed[(int64_t)cp * 4 + h], acc[h]);
-    if (nsl) atomicAdd(&pid_slabs[cp], (int)nsl);
-    if (tot) atomic_add_i64(&ptotal[cp], tot);
-  }
+      if (x[h]) atomic_add_i64(&removed[(int64_t)p * 4 + h], x[h]);
+    if (x[4]) atomicAdd(&pid_slabs[p], (int)x[4]);
+    if (x[5]) atomic_add_i64(&ptotal[p], x[5]);
+  });
 }
 
 __global__ void k_slab_base(const int* pid_slabs, int np, int64_t* slab_base) {

@@ -128,7 +128,12 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
     atomic_max_i64(&hi_out[cur_p], hi);
     if (cur_pops) atomicAdd(&pid_ops[cur_p], cur_pops);
   }
-  if (cur_g >= 0 && cur_gops) atomicAdd(&group_ops[cur_g], cur_gops);
+  {
+    long long gv[1] = {cur_gops};
+    block_keyed_flush<1>(cur_gops ? cur_g : -1, gv, [&](int g, const long long* x) {
+      if (x[0]) atomicAdd(&group_ops[g], (int)x[0]);
+    });
+  }
 
   bad = warp_sum(bad);
   nz = warp_sum(nz);

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(XS_BLOCK) k_keygen(EventView v, int64_t n, con
 }
 
 // --------------------------------------------------------------------------
-constexpr int SW_ITEMS = 8;
+constexpr int SW_ITEMS = 16;
 constexpr int SW_TILE = XS_BLOCK * SW_ITEMS;
 constexpr int HT = 1024;  // shared hash slots per block
 
@@ -135,6 +135,10 @@ __global__ void __launch_bounds__(XS_BLOCK) k_sweep(const uint64_t* __restrict__
   Cnt cur = grid_exclusive(agg, CntAdd(), zero, tile, desc, flags);
   const uint64_t tmask = (1ull << tb) - 1;
   const int pshift = tb + 4;
+  // running per-thread accumulators: one cell key and the pid's tracked time
+  unsigned long long run_idx = ~0ull, run_len = 0;
+  int tr_pid = -1;
+  long long tr_len[1] = {0};
 #pragma unroll
   for (int j = 0; j < SW_ITEMS; j++) {
     if (base + j >= nvalid) break;
@@ -149,15 +153,31 @@ __global__ void __launch_bounds__(XS_BLOCK) k_sweep(const uint64_t* __restrict__
 #pragma unroll
     for (int c = 0; c < 5; c++) mask |= (cur.c[c] > 0 ? 1u : 0u) << c;
     const unsigned long long prow = (unsigned long long)p * (unsigned long long)n_nodes;
+    if (mask || cur.c[5] > 0) {
+      if (p != tr_pid) {
+        if (tr_pid >= 0 && tr_len[0]) hist_add(s_key, s_val, hist, (unsigned long long)tr_pid * n_nodes * 32ull,
+                                               (unsigned long long)tr_len[0]);
+        tr_pid = p;
+        tr_len[0] = 0;
+      }
+      tr_len[0] += (long long)len;
+    }
     if (mask) {
       const int64_t c = cur.c[6];
       const int path = c > opbase[p] ? pidpath[c - 1] : 0;
-      hist_add(s_key, s_val, hist, (prow + (unsigned long long)path) * 32ull + mask, len);
-      hist_add(s_key, s_val, hist, prow * 32ull, len);
-    } else if (cur.c[5] > 0) {
-      hist_add(s_key, s_val, hist, prow * 32ull, len);
+      const unsigned long long idx = (prow + (unsigned long long)path) * 32ull + mask;
+      if (idx != run_idx) {
+        if (run_idx != ~0ull) hist_add(s_key, s_val, hist, run_idx, run_len);
+        run_idx = idx;
+        run_len = 0;
+      }
+      run_len += len;
     }
   }
+  if (run_idx != ~0ull) hist_add(s_key, s_val, hist, run_idx, run_len);
+  block_keyed_flush<1>(tr_pid, tr_len, [&](int p, const long long* x) {
+    if (x[0]) hist_add(s_key, s_val, hist, (unsigned long long)p * n_nodes * 32ull, (unsigned long long)x[0]);
+  });
   __syncthreads();
   for (int i = threadIdx.x; i < HT; i += XS_BLOCK) {
     unsigned long long key = s_key[i];

@@ -54,18 +54,17 @@ __device__ __forceinline__ TState t_identity() {
 __global__ void k_trec(EventView v, int64_t n, const int64_t* lo, int tb, int src_mask, int dst_mask, uint64_t* key,
                        uint64_t* skey, uint32_t* val, unsigned long long* count) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int c = v.ev.cat[i];
-  bool is_src = c >= 1 && c <= 3 && ((src_mask >> c) & 1) && v.dur[i] > 0;
-  bool is_dst = c >= 2 && c <= 4 && ((dst_mask >> c) & 1);
-  if (!is_src && !is_dst) return;
+  int c = i < n ? v.ev.cat[i] : 0;
+  bool is_src = i < n && c >= 1 && c <= 3 && ((src_mask >> c) & 1) && v.dur[i] > 0;
+  bool is_dst = i < n && c >= 2 && c <= 4 && ((dst_mask >> c) & 1);
+  int k = (is_src ? 2 : 0) + (is_dst ? 1 : 0);
+  unsigned long long at = warp_reserve(count, (unsigned)k);  // whole warp participates
+  if (!k) return;
   int p = v.ev.pid[i];
   uint64_t g = (uint64_t)v.ev.tid[i];
   uint64_t s = (uint64_t)(v.start[i] - lo[p]);
   uint64_t e = s + (uint64_t)v.dur[i];
   const uint64_t tmask = (1ull << tb) - 1;
-  int k = (is_src ? 2 : 0) + (is_dst ? 1 : 0);
-  unsigned long long at = atomicAdd(count, (unsigned long long)k);
   if (is_src) {
     key[at] = (g << (tb + 4)) | (e << 4) | (uint64_t)(c - 1);
     skey[at] = 0;
