@@ -1,0 +1,123 @@
+// xs_bucket.cuh -- bucketed sort fused with its consumer.
+//
+// A full LSD radix sort costs one histogram read plus P read+write passes over
+// the keys, and at config-2 sizes each onesweep pass is latency-bound (see
+// profiles/r01_ncu_full_summary.txt).  Consumers here only need the keys in
+// order *inside* contiguous key ranges, so:
+//   1. histogram the keys into 2^BB fine buckets (key >> shift)   [1 read]
+//   2. exclusive scan -> bucket offsets; group consecutive buckets into
+//      chunks of <= CAP keys (CAP = one CTA's shared-memory tile)
+//   3. scatter keys into bucket order                              [1 read, 1 write]
+//   4. one CTA per chunk: load, sort in shared memory on the few low bits that
+//      differ inside the chunk, and run the consumer's scan right there with
+//      decoupled look-back across chunks                          [1 read]
+// A bucket larger than CAP/2 sets an overflow flag; the host re-runs that call
+// through the LSD path (never silently wrong).
+#pragma once
+#include "xs_engine.cuh"
+
+namespace xs {
+
+constexpr int BK_THREADS = 256;
+constexpr int BK_ITEMS = 16;
+constexpr int BK_CAP = BK_THREADS * BK_ITEMS;  // keys per chunk tile
+constexpr int BK_T = BK_CAP / 2;                // chunk split granule (max bucket)
+
+struct BucketGeom {
+  int key_bits;  // keys occupy [0, key_bits)
+  int bb;        // bucket bits
+  int shift;     // bucket = key >> shift
+  int64_t nbuckets;
+};
+
+inline BucketGeom bucket_geom(int key_bits, int max_bb = 20) {
+  BucketGeom g;
+  g.key_bits = key_bits;
+  g.bb = key_bits < max_bb ? key_bits : max_bb;
+  g.shift = key_bits - g.bb;
+  g.nbuckets = (int64_t)1 << g.bb;
+  return g;
+}
+
+// warp-aggregated histogram increment (lanes that share a bucket add once)
+__device__ __forceinline__ void bucket_count(unsigned* counts, uint32_t b, bool valid) {
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const unsigned peers = __match_any_sync(act, b);
+  const int lane = threadIdx.x & 31;
+  if (lane == __ffs(peers) - 1) atomicAdd(&counts[b], (unsigned)__popc(peers));
+}
+
+// warp-aggregated slot reservation inside a bucket.  Counts down the
+// histogram itself (slots fill the bucket from its end), so the counts are
+// back to zero when the scatter finishes -- no second array, no extra memset.
+__device__ __forceinline__ int64_t bucket_slot(unsigned* counts, const int64_t* offs, uint32_t b, bool valid) {
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return -1;
+  const unsigned peers = __match_any_sync(act, b);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  const unsigned k = (unsigned)__popc(peers);
+  unsigned top = 0;
+  if (lane == leader) top = atomicSub(&counts[b], k);  // old value: slots [top-k, top) are ours
+  top = __shfl_sync(peers, top, leader);
+  return offs[b] + (top - k) + __popc(peers & ((1u << lane) - 1));
+}
+
+// buckets ~ one per key over the occupied key space (SURVEY 8d key layout)
+inline int bucket_bits_for(int64_t nkeys, int key_bits) {
+  int b = 1;
+  while (b < 62 && ((int64_t)1 << b) < nkeys) b++;
+  b += 1;
+  if (b < 10) b = 10;
+  if (b > 24) b = 24;
+  return b < key_bits ? b : key_bits;
+}
+
+// Chunk c = the buckets whose exclusive offset lies in [c*T, (c+1)*T); its
+// first bucket is lower_bound(offs, c*T) when that bucket's offset is still in
+// range, otherwise chunk c is empty (a bucket spanning several granules).  A
+// chunk holds < 2T = CAP keys whenever no bucket exceeds T (the consumer
+// flags overflow otherwise).
+__device__ __forceinline__ int64_t upper_bound_i64(const int64_t* a, int64_t lo, int64_t hi, int64_t x) {
+  while (lo < hi) {  // first index with a[i] > x
+    int64_t m = (lo + hi) >> 1;
+    if (a[m] <= x) lo = m + 1;
+    else hi = m;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int64_t lo, int64_t hi, int64_t x) {
+  while (lo < hi) {  // first index with a[i] >= x
+    int64_t m = (lo + hi) >> 1;
+    if (a[m] < x) lo = m + 1;
+    else hi = m;
+  }
+  return lo;
+}
+
+// One thread per chunk, all chunks in parallel: key range [start, end) and
+// the tight bucket range [b0, b1) (first / last nonempty bucket) so each
+// consumer CTA starts with four loads instead of serial searches.
+// offs has nb+1 entries (offs[nb] = total).
+__global__ void k_bucket_chunks(const int64_t* offs, int64_t nb, int64_t n_chunks, int64_t total, int64_t* chunk) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_chunks) return;
+  const int64_t b = lower_bound_i64(offs, 0, nb, c * BK_T);
+  int64_t s = -1, e = -1, b0 = 0, b1 = 0;
+  if (b < nb && offs[b] < total && offs[b] / BK_T == c) {
+    s = offs[b];
+    const int64_t bn = lower_bound_i64(offs, b, nb, (c + 1) * BK_T);
+    e = bn < nb ? offs[bn] : total;
+    b0 = upper_bound_i64(offs, b, nb + 1, s) - 1;   // bucket holding key s
+    b1 = upper_bound_i64(offs, b0, nb + 1, e - 1);  // bucket holding key e-1, plus one
+  }
+  chunk[4 * c + 0] = s;
+  chunk[4 * c + 1] = e;
+  chunk[4 * c + 2] = b0;
+  chunk[4 * c + 3] = b1;
+}
+
+
+}  // namespace xs

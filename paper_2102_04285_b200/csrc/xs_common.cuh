@@ -148,6 +148,61 @@ __device__ T lookback_warp(int tile, const T& agg, TileDesc<T>* desc, int* flags
   return excl;
 }
 
+// Split look-back for tiles whose aggregate is known before their own
+// per-thread prefixes (order-independent aggregates): publish early, walk
+// later.  Both are called by lane(s) of warp 0 only.
+template <class T>
+__device__ __forceinline__ void tile_publish_agg(int tile, const T& agg, TileDesc<T>* desc, int* flags) {
+  if (tile == 0) {
+    st_volatile_T(&desc[0].incl, agg);
+    __threadfence();
+    flag_store(&flags[0], 2);
+  } else {
+    st_volatile_T(&desc[tile].agg, agg);
+    __threadfence();
+    flag_store(&flags[tile], 1);
+  }
+}
+
+template <class T, class Op>
+__device__ T tile_lookback_published(int tile, const T& agg, TileDesc<T>* desc, int* flags, Op op,
+                                     const T& identity) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) return identity;
+  T excl = identity;
+  int pred = tile - 1;
+  while (true) {
+    const int idx = pred - lane;
+    int f = 2;
+    if (idx >= 0) {
+      int spins = 0;
+      while ((f = flag_load(&flags[idx])) == 0) {
+        if (++spins > 32) __nanosleep(20);
+      }
+    }
+    const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
+    const int stop = m2 ? (__ffs(m2) - 1) : 32;
+    T v = identity;
+    if (idx >= 0 && lane <= stop) v = (lane == stop) ? ld_volatile_T(&desc[idx].incl) : ld_volatile_T(&desc[idx].agg);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T other = shfl_down_T(v, o);
+      if ((lane & (2 * o - 1)) == 0) v = op(other, v);
+    }
+    v = shfl_idx_T(v, 0);
+    excl = op(v, excl);
+    if (m2) break;
+    pred -= 32;
+  }
+  if (lane == 0) {
+    T incl = op(excl, agg);
+    st_volatile_T(&desc[tile].incl, incl);
+    __threadfence();
+    flag_store(&flags[tile], 2);
+  }
+  return excl;
+}
+
 // Block-wide exclusive scan with warp shuffles (2 barriers).
 template <class T, class Op>
 __device__ T block_exclusive_fast(T v, Op op, const T& identity, T* s_warp /*[32]*/, T* agg_out) {

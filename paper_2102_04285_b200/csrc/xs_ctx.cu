@@ -96,12 +96,18 @@ int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s
       ctx->err = "merged multi-tid operation path deeper than the device limit";
       return XS_UNSUPPORTED;
     }
+    if (ctx->h_stats->pad[3]) {  // a bucket overflowed a chunk: redo this call via the LSD sort
+      ctx->force_lsd = true;
+      continue;
+    }
     if (!ctx->h_stats->table_full) {
       ctx->have_overlap = true;
+      ctx->force_lsd = false;
       return XS_OK;
     }
     ctx->trie_cap_log2 += 2;
   }
+  ctx->force_lsd = false;
   ctx->err = "path table could not be sized";
   return XS_NO_MEMORY;
 }

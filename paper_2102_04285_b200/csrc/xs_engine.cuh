@@ -57,6 +57,8 @@ enum Slot : int {
   W_CORR_LO, W_CORR_HI, W_PTOTAL, W_PID_SLABS, W_SITE_EV, W_SITE_SUB, W_QVAL, W_OUT_LO, W_OUT_HI,
   // transitions
   W_TSKEY, W_TSKEY_ALT, W_HEADPOS, W_TREC_ID, W_TREC_ID_ALT,
+  // bucketed sorts
+  W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
   W_NUM_SLOTS
 };
 
@@ -161,6 +163,7 @@ struct xs_ctx {
   // last transitions
   long long n_trans_out = 0;
   int trie_cap_log2 = 12;
+  bool force_lsd = false;  // bucketed sort overflowed on this input: use the LSD path
   xs::OpsState ops;
   // optional per-stage device timing (CUDA events on the launching stream)
   bool prof_on = false;

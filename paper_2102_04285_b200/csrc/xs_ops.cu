@@ -5,11 +5,11 @@
 //   path at t   = dedupe(names of active ops in rank order)   _sweep_py.py:16-26
 //   nesting     = per (pid, tid) no partial overlap         model.py:137-156
 // Device formulation (all integer, parallel, exact):
-//   1. nonzero ops are ranked inside their (pid,tid) group by two stable radix
-//      passes: (desc end, name) then (group, start).  Row order = event index
-//      order, so stable ties follow the reference's stable sort.
-//   2. open/close endpoints per group sorted by (group, t, close<open), closes
-//      inner-first and opens outer-first => a balanced parenthesisation.  The
+//   1-2. open/close endpoints of the nonzero ops sorted once by
+//      (group, t, close<open); the only unordered runs are endpoints at one
+//      instant, which a local tie pass puts outer-first for opens and
+//      inner-first for closes using the rank order (start, -end, name, index)
+//      => a balanced parenthesisation in the reference's rank order.  The
 //      prefix sum of +-1 is the depth; an op is properly nested iff its depth
 //      after close == depth after open - 1 (equivalent to the reference stack
 //      check).
@@ -35,58 +35,60 @@ struct OpPred {
   __device__ bool operator()(const int& i) const { return cat[i] == 0 && dur[i] > 0; }
 };
 
-__global__ void k_rank_key1(const int* op_ev, const uint32_t* vals, int64_t m, EventView v, const int64_t* lo,
-                            int tb, int nb, uint64_t* keys) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= m) return;
-  int i = op_ev[vals[q]];
-  int p = v.ev.pid[i];
-  uint64_t end_rel = (uint64_t)(v.start[i] + v.dur[i] - lo[p]);
-  uint64_t tmask = tb >= 64 ? ~0ull : ((1ull << tb) - 1);
-  uint64_t desc = tmask - end_rel;  // descending end
-  keys[q] = (desc << nb) | (uint64_t)v.ev.name[i];
-}
-
-__global__ void k_rank_key_name(const int* op_ev, const uint32_t* vals, int64_t m, EventView v, uint64_t* keys) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= m) return;
-  keys[q] = (uint64_t)v.ev.name[op_ev[vals[q]]];
-}
-
-__global__ void k_rank_key_end(const int* op_ev, const uint32_t* vals, int64_t m, EventView v, const int64_t* lo,
-                               int tb, uint64_t* keys) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= m) return;
-  int i = op_ev[vals[q]];
-  uint64_t end_rel = (uint64_t)(v.start[i] + v.dur[i] - lo[v.ev.pid[i]]);
-  uint64_t tmask = tb >= 64 ? ~0ull : ((1ull << tb) - 1);
-  keys[q] = tmask - end_rel;
-}
-
-__global__ void k_rank_key2(const int* op_ev, const uint32_t* vals, int64_t m, EventView v, const int64_t* lo,
-                            int tb, uint64_t* keys) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= m) return;
-  int i = op_ev[vals[q]];
-  int p = v.ev.pid[i];
-  keys[q] = ((uint64_t)v.ev.tid[i] << tb) | (uint64_t)(v.start[i] - lo[p]);
-}
-
-// endpoint stream: slot m+r = open of rank r, slot m-1-r = close of rank r
-__global__ void k_endpoints(const int* op_ev, const uint32_t* ranked, int64_t m, EventView v, const int64_t* lo,
-                            int tb, uint64_t* keys, uint32_t* vals, int* rank_ev) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  int i = op_ev[ranked[r]];
-  rank_ev[r] = i;
+// endpoint stream: slot m+j = open of op j, slot j = close of op j (op j =
+// j-th nonzero OPERATION in event order).  Key = group | t | open.
+__global__ void k_endpoints(const int* op_ev, int64_t m, EventView v, const int64_t* lo, int tb, uint64_t* keys,
+                            uint32_t* vals) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  int i = op_ev[j];
   int p = v.ev.pid[i];
   uint64_t g = (uint64_t)v.ev.tid[i];
   uint64_t s = (uint64_t)(v.start[i] - lo[p]);
   uint64_t e = (uint64_t)(v.start[i] + v.dur[i] - lo[p]);
-  keys[m + r] = (g << (tb + 1)) | (s << 1) | 1ull;
-  vals[m + r] = (uint32_t)r;
-  keys[m - 1 - r] = (g << (tb + 1)) | (e << 1);
-  vals[m - 1 - r] = (uint32_t)r;
+  keys[m + j] = (g << (tb + 1)) | (s << 1) | 1ull;
+  vals[m + j] = (uint32_t)j;
+  keys[j] = (g << (tb + 1)) | (e << 1);
+  vals[j] = (uint32_t)j;
+}
+
+// Rank order inside a (pid, tid) group is (start, -end, name, index)
+// (overlap.py:96-99).  After the (group, t, open) sort, only runs of equal
+// keys are unordered: opens at one instant go outer-first (rank order),
+// closes at one instant inner-first (reverse rank order).  Runs are tiny, so
+// one thread per run insertion-sorts it.
+__device__ __forceinline__ bool rank_less(const EventView& v, const int* op_ev, uint32_t a, uint32_t b) {
+  const int ia = op_ev[a], ib = op_ev[b];
+  const int64_t sa = v.start[ia], sb = v.start[ib];
+  if (sa != sb) return sa < sb;
+  const int64_t ea = sa + v.dur[ia], eb = sb + v.dur[ib];
+  if (ea != eb) return ea > eb;
+  const int na = v.ev.name[ia], nb = v.ev.name[ib];
+  if (na != nb) return na < nb;
+  return ia < ib;
+}
+
+__global__ void k_op_tiefix(const uint64_t* keys, uint32_t* vals, int64_t n2, const int* op_ev, EventView v) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n2) return;
+  const uint64_t k = keys[q];
+  if (q > 0 && keys[q - 1] == k) return;
+  if (q + 1 >= n2 || keys[q + 1] != k) return;
+  int64_t e = q + 1;
+  while (e < n2 && keys[e] == k) e++;
+  const bool open = k & 1ull;
+  for (int64_t a = q + 1; a < e; a++) {
+    const uint32_t x = vals[a];
+    int64_t b = a - 1;
+    while (b >= q) {
+      const uint32_t y = vals[b];
+      const bool out_of_order = open ? rank_less(v, op_ev, x, y) : rank_less(v, op_ev, y, x);
+      if (!out_of_order) break;
+      vals[b + 1] = y;
+      b--;
+    }
+    vals[b + 1] = x;
+  }
 }
 
 struct DepthDelta {
@@ -121,10 +123,13 @@ __global__ void k_depth_check(const int* d_open, const int* d_close, int64_t m, 
   }
 }
 
-__global__ void k_depth_keys(const int* d_open, const int* pos_open, int64_t m, uint64_t* dk, uint32_t* dv) {
+// opens keyed by (depth, stream position): the parent of an op at depth d is
+// the last depth-(d-1) open before it
+__global__ void k_depth_keys(const int* d_open, const int* pos_open, int64_t m, int pbits, uint64_t* dk,
+                             uint32_t* dv) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
-  dk[r] = (uint64_t)d_open[r];
+  dk[r] = ((uint64_t)d_open[r] << pbits) | (uint64_t)pos_open[r];
   dv[r] = (uint32_t)pos_open[r];
 }
 
@@ -137,8 +142,8 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo
   return lo;
 }
 
-__global__ void k_parent(const int* d_open, const int* pos_open, int64_t m, const uint64_t* dk, const uint32_t* dv,
-                         const uint32_t* svals, int* parent) {
+__global__ void k_parent(const int* d_open, const int* pos_open, int64_t m, int pbits, const uint64_t* dk,
+                         const uint32_t* dv, const uint32_t* svals, int* parent) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   int d = d_open[r];
@@ -146,17 +151,10 @@ __global__ void k_parent(const int* d_open, const int* pos_open, int64_t m, cons
     parent[r] = -1;
     return;
   }
-  int64_t a = lower_bound_u64(dk, 0, m, (uint64_t)(d - 1));
-  int64_t b = lower_bound_u64(dk, a, m, (uint64_t)d);
-  uint32_t pos = (uint32_t)pos_open[r];
-  // last q in [a, b) with dv[q] < pos
-  int64_t lo = a, hi = b;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (dv[mid] < pos) lo = mid + 1;
-    else hi = mid;
-  }
-  parent[r] = lo > a ? (int)svals[dv[lo - 1]] : -1;
+  const uint64_t lo_key = (uint64_t)(d - 1) << pbits;
+  const uint64_t target = lo_key | (uint64_t)pos_open[r];
+  const int64_t q = lower_bound_u64(dk, 0, m, target);  // first >= (d-1, pos)
+  parent[r] = (q > 0 && dk[q - 1] >= lo_key) ? (int)svals[dv[q - 1]] : -1;
 }
 
 // dependency-ordered interning of node(op) = child(node(parent), name)
@@ -300,7 +298,8 @@ __global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const 
       int iy = rank_ev[y];
       int64_t ys = v.start[iy], ye = v.start[iy] + v.dur[iy];
       int yg = v.ev.tid[iy];
-      bool greater = (ys != xs_) ? ys > xs_ : (ye != xe) ? ye < xe : (yg != xg) ? yg > xg : y > x;
+      const int ny = v.ev.name[iy], nx = v.ev.name[ix];
+      bool greater = (ys != xs_) ? ys > xs_ : (ye != xe) ? ye < xe : (yg != xg) ? yg > xg : (ny != nx) ? ny > nx : iy > ix;
       if (!greater) break;
       ops[b + 1] = y;
       b--;
@@ -376,6 +375,12 @@ int trie_setup(xs_ctx* ctx, cudaStream_t s, TrieView* t) {
 
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths) {
   ProfScope ps(ctx, ST_OPS, s);
+  {  // retry-able flags start clear on every attempt
+    Stats* stp = (Stats*)ctx->ptr[W_STATS];
+    XS_CUDA(cudaMemsetAsync(&stp->table_full, 0, sizeof(long long), s));
+    XS_CUDA(cudaMemsetAsync(&stp->depth_overflow, 0, sizeof(long long), s));
+    XS_CUDA(cudaMemsetAsync(&stp->pad[3], 0, sizeof(long long), s));
+  }
   const Stats& H = *ctx->h_stats;
   const int64_t m = H.n_ops_nz;
   const int np = v.ev.n_pids, ng = v.ev.n_groups;
@@ -419,37 +424,17 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
     XS_CUDA(cub::DeviceSelect::If(t, temp, it, op_ev, nsel, (int)v.ev.n, pred, s));
     ctx->launches += 2;
   }
-  // 2. rank sort inside (pid, tid) groups
-  uint64_t *k0, *k1;
-  uint32_t *v0, *v1;
-  XS_TRY(ws(ctx, W_OPK0, 2 * m + 2, s, &k0));
-  XS_TRY(ws(ctx, W_OPK1, 2 * m + 2, s, &k1));
-  XS_TRY(ws(ctx, W_OPV0, 2 * m + 2, s, &v0));
-  XS_TRY(ws(ctx, W_OPV1, 2 * m + 2, s, &v1));
-  XS_LAUNCH(ctx, k_iota_u32, grid_for(m), XS_BLOCK, 0, s, v0, m);
-  if (tb + nb <= 64) {
-    XS_LAUNCH(ctx, k_rank_key1, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, lo, tb, nb, k0);
-    XS_TRY(sort_pairs_u64_u32(ctx, &k0, &k1, &v0, &v1, m, tb + nb, s));
-  } else {
-    XS_LAUNCH(ctx, k_rank_key_name, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, k0);
-    XS_TRY(sort_pairs_u64_u32(ctx, &k0, &k1, &v0, &v1, m, nb, s));
-    XS_LAUNCH(ctx, k_rank_key_end, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, lo, tb, k0);
-    XS_TRY(sort_pairs_u64_u32(ctx, &k0, &k1, &v0, &v1, m, tb, s));
-  }
-  XS_LAUNCH(ctx, k_rank_key2, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, lo, tb, k0);
-  XS_TRY(sort_pairs_u64_u32(ctx, &k0, &k1, &v0, &v1, m, gb + tb, s));
-  // v0[r] = compacted op id of rank r
-  // 3. endpoint stream per group
+  // 2. endpoint stream per (pid, tid) group: one sort + local tie order
   uint64_t *sk, *sk_alt;
   uint32_t *sv, *sv_alt;
-  int* rank_ev;
   XS_TRY(ws(ctx, W_SKEY, 2 * m + 2, s, &sk));
   XS_TRY(ws(ctx, W_SKEY_ALT, 2 * m + 2, s, &sk_alt));
   XS_TRY(ws(ctx, W_SVAL, 2 * m + 2, s, &sv));
   XS_TRY(ws(ctx, W_SVAL_ALT, 2 * m + 2, s, &sv_alt));
-  XS_TRY(ws(ctx, W_RANK_EV, m + 1, s, &rank_ev));
-  XS_LAUNCH(ctx, k_endpoints, grid_for(m), XS_BLOCK, 0, s, op_ev, v0, m, v, lo, tb, sk, sv, rank_ev);
+  XS_LAUNCH(ctx, k_endpoints, grid_for(m), XS_BLOCK, 0, s, op_ev, m, v, lo, tb, sk, sv);
   XS_TRY(sort_pairs_u64_u32(ctx, &sk, &sk_alt, &sv, &sv_alt, 2 * m, gb + tb + 1, s));
+  XS_LAUNCH(ctx, k_op_tiefix, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, 2 * m, op_ev, v);
+  const int* rank_ev = op_ev;  // op ids index every per-op array
   os.skeys = sk;
   os.svals = sv;
   os.rank_ev = rank_ev;
@@ -481,9 +466,10 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
     XS_TRY(ws(ctx, W_DKEY_ALT, m + 1, s, &dk_alt));
     XS_TRY(ws(ctx, W_DVAL, m + 1, s, &dv));
     XS_TRY(ws(ctx, W_DVAL_ALT, m + 1, s, &dv_alt));
-    XS_LAUNCH(ctx, k_depth_keys, grid_for(m), XS_BLOCK, 0, s, d_open, pos_open, m, dk, dv);
-    XS_TRY(sort_pairs_u64_u32(ctx, &dk, &dk_alt, &dv, &dv_alt, m, bits_for((uint64_t)maxd), s));
-    XS_LAUNCH(ctx, k_parent, grid_for(m), XS_BLOCK, 0, s, d_open, pos_open, m, dk, dv, sv, parent);
+    const int pbits = bits_for((uint64_t)(2 * m));
+    XS_LAUNCH(ctx, k_depth_keys, grid_for(m), XS_BLOCK, 0, s, d_open, pos_open, m, pbits, dk, dv);
+    XS_TRY(sort_pairs_u64_u32(ctx, &dk, &dk_alt, &dv, &dv_alt, m, bits_for((uint64_t)maxd) + pbits, s));
+    XS_LAUNCH(ctx, k_parent, grid_for(m), XS_BLOCK, 0, s, d_open, pos_open, m, pbits, dk, dv, sv, parent);
   } else {
     XS_CUDA(cudaMemsetAsync(parent, 0xFF, (m + 1) * sizeof(int), s));
   }

@@ -23,7 +23,10 @@
 //     elsewhere the union length goes to cell (fp, {GPU}) (set semantics);
 //   * every fixed event also drives the tracked-only lane, so tracked time is
 //     "mask != 0 or any fixed event active" as in the reference.
-#include "xs_engine.cuh"
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "xs_bucket.cuh"
 
 namespace xs {
 
@@ -39,12 +42,15 @@ struct CntAdd {
   }
 };
 
+// lane update with compile-time indices only (a runtime index would put the
+// state in local memory): cat 1..5 -> lanes 0..4, cat 6 -> lane 5, cat 0 ->
+// op-endpoint count (lane 6, +1 for opens and closes)
 __device__ __forceinline__ void apply_code(Cnt& s, uint32_t code) {
   const uint32_t cat = code & 7u;
   const int d = (code & 8u) ? -1 : 1;
-  if (cat == 0) s.c[6] += 1;
-  else if (cat <= 5) s.c[cat - 1] += d;
-  else s.c[5] += d;
+#pragma unroll
+  for (int i = 0; i < 6; i++) s.c[i] += (cat == (uint32_t)(i + 1)) ? d : 0;
+  s.c[6] += cat == 0 ? 1 : 0;
 }
 
 // --------------------------------------------------------------------------
@@ -331,6 +337,516 @@ __global__ void __launch_bounds__(XS_BLOCK) k_fx_scan(const uint64_t* fx, int64_
 }
 
 // --------------------------------------------------------------------------
+// Bucketed sort fused with the sweep (xs_bucket.cuh)
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void event_keys(const EventView& v, int64_t i, const int64_t* lo, int tb, int corr_mode,
+                                           uint64_t& k0, uint64_t& k1, bool& valid) {
+  const int64_t d = v.dur[i];
+  valid = d > 0;
+  k0 = k1 = 0;
+  if (!valid) return;
+  const int p = v.ev.pid[i];
+  uint32_t cat = v.ev.cat[i];
+  if (corr_mode && cat == 5 && v.ev.has_corr[i]) cat = 6;
+  const uint64_t base = (uint64_t)p << (tb + 4);
+  const uint64_t st = (uint64_t)(v.start[i] - lo[p]);
+  k0 = base | (st << 4) | cat;
+  k1 = base | ((st + (uint64_t)d) << 4) | 8u | cat;
+}
+
+__global__ void __launch_bounds__(XS_BLOCK) k_bk_hist(EventView v, int64_t n, const int64_t* __restrict__ lo, int tb,
+                                                      int corr_mode, const uint64_t* extra, int64_t n_extra,
+                                                      int shift, unsigned* counts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t k0 = 0, k1 = 0;
+  bool v0 = false, v1 = false;
+  if (i < n) {
+    bool valid;
+    event_keys(v, i, lo, tb, corr_mode, k0, k1, valid);
+    v0 = v1 = valid;
+  } else if (i - n < (n_extra + 1) / 2) {
+    const int64_t q = 2 * (i - n);
+    k0 = extra[q];
+    v0 = true;
+    v1 = q + 1 < n_extra;
+    k1 = v1 ? extra[q + 1] : 0;
+  }
+  // warp-collective: every lane reaches both calls
+  bucket_count(counts, (uint32_t)(k0 >> shift), v0);
+  bucket_count(counts, (uint32_t)(k1 >> shift), v1);
+}
+
+__global__ void __launch_bounds__(XS_BLOCK) k_bk_scatter(EventView v, int64_t n, const int64_t* __restrict__ lo, int tb,
+                                                         int corr_mode, const uint64_t* extra, int64_t n_extra,
+                                                         int shift, unsigned* counts, const int64_t* offs,
+                                                         uint64_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t k0 = 0, k1 = 0;
+  bool v0 = false, v1 = false;
+  if (i < n) {
+    bool valid;
+    event_keys(v, i, lo, tb, corr_mode, k0, k1, valid);
+    v0 = v1 = valid;
+  } else if (i - n < (n_extra + 1) / 2) {
+    const int64_t q = 2 * (i - n);
+    k0 = extra[q];
+    v0 = true;
+    v1 = q + 1 < n_extra;
+    k1 = v1 ? extra[q + 1] : 0;
+  }
+  const int64_t s0 = bucket_slot(counts, offs, (uint32_t)(k0 >> shift), v0);
+  if (v0) out[s0] = k0;
+  const int64_t s1 = bucket_slot(counts, offs, (uint32_t)(k1 >> shift), v1);
+  if (v1) out[s1] = k1;
+}
+
+struct SwState {
+  int c[8];  // as Cnt
+  unsigned long long last;
+  int has;
+  int pad;
+};
+struct SwOp {
+  __device__ SwState operator()(const SwState& a, const SwState& b) const {
+    SwState r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.c[i] = a.c[i] + b.c[i];
+    r.last = b.has ? b.last : a.last;
+    r.has = a.has | b.has;
+    r.pad = 0;
+    return r;
+  }
+};
+
+__device__ __forceinline__ void sw_apply(SwState& s, uint32_t code) {
+  const uint32_t cat = code & 7u;
+  const int d = (code & 8u) ? -1 : 1;
+#pragma unroll
+  for (int i = 0; i < 6; i++) s.c[i] += (cat == (uint32_t)(i + 1)) ? d : 0;
+  s.c[6] += cat == 0 ? 1 : 0;
+}
+
+constexpr int BK_RANK_MAX = 64;  // buckets up to this size are ranked by direct comparison
+
+// Shared-memory cell table with native 32-bit adds (a 64-bit shared atomicAdd
+// is a CAS loop on sm_100): value = hi:lo, the carry of each add goes to hi.
+__device__ __forceinline__ void smem_add64(unsigned* lo, unsigned* hi, unsigned long long v) {
+  const unsigned vl = (unsigned)v, vh = (unsigned)(v >> 32);
+  const unsigned old = atomicAdd(lo, vl);
+  const unsigned carry = (old + vl) < old ? 1u : 0u;
+  if (vh | carry) atomicAdd(hi, vh + carry);
+}
+
+struct CellTable {  // open addressing in shared memory, spill to global
+  unsigned long long* key;
+  unsigned* lo;
+  unsigned* hi;
+  __device__ void add(unsigned long long idx, unsigned long long v, unsigned long long* hist) {
+    unsigned h = (unsigned)(mix64(idx) & (HT - 1));
+#pragma unroll 1
+    for (int probe = 0; probe < 16; probe++) {
+      unsigned long long k = key[h];
+      if (k != idx && k == ~0ull) {
+        unsigned long long prev = atomicCAS(&key[h], ~0ull, idx);
+        k = prev == ~0ull ? idx : prev;
+      }
+      if (k == idx) {
+        smem_add64(&lo[h], &hi[h], v);
+        return;
+      }
+      h = (h + 1) & (HT - 1);
+    }
+    atomicAdd(&hist[idx], v);
+  }
+};
+
+// Per-thread register cache of a few cells, flushed with a warp-level
+// reduce-by-key so a block touches each shared slot once per warp.
+template <int K>
+struct CellCache {
+  unsigned long long k[K];
+  unsigned long long v[K];
+  int n = 0;
+  __device__ void add(unsigned long long idx, unsigned long long len, CellTable& T, unsigned long long* hist) {
+#pragma unroll
+    for (int i = 0; i < K; i++)
+      if (i < n && k[i] == idx) {
+        v[i] += len;
+        return;
+      }
+    if (n < K) {
+#pragma unroll
+      for (int i = 0; i < K; i++)
+        if (i == n) {
+          k[i] = idx;
+          v[i] = len;
+        }
+      n++;
+      return;
+    }
+    T.add(k[0], v[0], hist);  // evict the oldest
+#pragma unroll
+    for (int i = 0; i + 1 < K; i++) {
+      k[i] = k[i + 1];
+      v[i] = v[i + 1];
+    }
+    k[K - 1] = idx;
+    v[K - 1] = len;
+  }
+  // all 32 lanes must call
+  __device__ void flush(CellTable& T, unsigned long long* hist) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      const bool has = i < n;
+      const unsigned long long key = has ? k[i] : ~0ull;
+      const unsigned act = __ballot_sync(0xffffffffu, has);
+      unsigned long long val = has ? v[i] : 0;
+      if (has) {
+        const unsigned peers = __match_any_sync(act, key);
+        const int leader = __ffs(peers) - 1;
+        unsigned long long sum = 0;
+        for (unsigned m = peers; m; m &= m - 1) sum += __shfl_sync(peers, val, __ffs(m) - 1);
+        if (lane == leader) T.add(key, sum, hist);
+      }
+    }
+  }
+};
+
+struct BkSmem {
+  uint32_t k[BK_CAP];       // chunk keys relative to the chunk base, bucket order (as scattered)
+  uint32_t sorted[BK_CAP];  // fully sorted (also block-radix-sort scratch together with k[])
+  unsigned long long h_key[HT];
+  unsigned h_lo[HT];
+  unsigned h_hi[HT];
+  uint32_t last[BK_THREADS];
+  SwState warp_agg[BK_THREADS / 32];
+  SwState tile_pre;
+  int big;
+};
+
+struct SwMaxOp {  // chunk aggregate: counts add, last = max key (order independent)
+  __device__ SwState operator()(const SwState& a, const SwState& b) const {
+    SwState r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.c[i] = a.c[i] + b.c[i];
+    r.last = a.last > b.last ? a.last : b.last;
+    r.has = a.has | b.has;
+    r.pad = 0;
+    return r;
+  }
+};
+
+__device__ __forceinline__ SwState sw_identity() {
+  SwState id;
+#pragma unroll
+  for (int i = 0; i < 8; i++) id.c[i] = 0;
+  id.last = 0;
+  id.has = 0;
+  id.pad = 0;
+  return id;
+}
+
+// One CTA per chunk.  The chunk arrives grouped by fine bucket (scatter
+// order), keys stored 32-bit relative to the chunk's first bucket.  Keys are
+// ranked inside their bucket (singletons directly, small buckets by direct
+// comparison, a block radix sort if some bucket is large), then the sweep
+// runs on the sorted tile.  The chunk aggregate (counts, max key) does not
+// depend on order and is published before sorting, so the look-back chain
+// never waits on a sort.  Every interval [t_prev, t) is accounted by the first
+// endpoint of the run at t with the state after everything up to t_prev;
+// across chunk boundaries t_prev and that state come from the look-back.
+__global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
+    const uint64_t* __restrict__ keys, int64_t total, const int64_t* __restrict__ chunk, int shift, int tb,
+    const int* __restrict__ pidpath, const int64_t* __restrict__ opbase, int n_nodes,
+    unsigned long long* __restrict__ hist, TileDesc<SwState>* desc, int* flags, int* tile_ctr, Stats* st,
+    unsigned long long* ptrace) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  unsigned long long tstamp[8];
+#define XS_STAMP(i) if (ptrace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tstamp[i]));
+  XS_STAMP(0);
+  for (int i = t; i < HT; i += BK_THREADS) {
+    S.h_key[i] = ~0ull;
+    S.h_lo[i] = 0;
+    S.h_hi[i] = 0;
+  }
+  if (t == 0) S.big = 0;
+  CellTable T{S.h_key, S.h_lo, S.h_hi};
+  const int64_t c = next_tile(tile_ctr);  // (barrier inside)
+  XS_STAMP(1);
+  const int64_t s0 = chunk[4 * c + 0];
+  int cnt = s0 < 0 ? 0 : (int)(chunk[4 * c + 1] - s0);
+  const int64_t b0 = chunk[4 * c + 2], b1 = chunk[4 * c + 3];
+  // base aligned to 16 (keeps the 4-bit endpoint code) and to 2^shift (keeps
+  // bucket grouping of the relative keys)
+  const uint64_t base = ((uint64_t)b0 << shift) & ~15ull;
+  const int lbits = bits_for(((uint64_t)(b1 > b0 ? b1 : b0 + 1) << shift) - 1 - base);
+  if (cnt > BK_CAP || (cnt > 0 && lbits > 32)) {  // host re-runs this call through the LSD path
+    if (t == 0) atomicAdd((unsigned long long*)&st->pad[3], 1ull);
+    cnt = 0;
+  }
+  // 1. load (striped, coalesced) + order-independent aggregate
+  SwState agg = sw_identity();
+  uint32_t kmax = 0;
+#pragma unroll
+  for (int j = 0; j < BK_ITEMS; j++) {
+    const int idx = j * BK_THREADS + t;
+    if (idx < cnt) {
+      const uint64_t k = keys[s0 + idx];
+      const uint32_t kr = (uint32_t)(k - base);
+      S.k[idx] = kr;
+      sw_apply(agg, kr & 15u);
+      kmax = kr > kmax ? kr : kmax;
+      agg.has = 1;
+    }
+  }
+  agg.last = base + kmax;
+  SwMaxOp mop;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    SwState other = shfl_down_T(agg, o);
+    agg = mop(agg, other);
+  }
+  if (lane == 0) S.warp_agg[warp] = agg;
+  __syncthreads();
+  SwState tile_agg = sw_identity();
+  if (warp == 0) {
+    SwState w = lane < BK_THREADS / 32 ? S.warp_agg[lane] : sw_identity();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      SwState other = shfl_down_T(w, o);
+      w = mop(w, other);
+    }
+    tile_agg = shfl_idx_T(w, 0);
+    if (lane == 0) tile_publish_agg((int)c, tile_agg, desc, flags);
+  }
+  XS_STAMP(2);
+  // 2. rank inside buckets (a bucket is the run of equal k >> shift in k[])
+  bool big = false;
+#pragma unroll 2
+  for (int j = 0; j < BK_ITEMS; j++) {
+    const int idx = j * BK_THREADS + t;
+    if (idx >= cnt) break;
+    const uint32_t k = S.k[idx];
+    const uint32_t bk = k >> shift;
+    const bool left = idx > 0 && (S.k[idx - 1] >> shift) == bk;
+    const bool right = idx + 1 < cnt && (S.k[idx + 1] >> shift) == bk;
+    if (!left && !right) {
+      S.sorted[idx] = k;
+      continue;
+    }
+    int r = 0, q = idx - 1, steps = 0;
+    for (; q >= 0 && steps < BK_RANK_MAX && (S.k[q] >> shift) == bk; q--, steps++) r += S.k[q] <= k;
+    big |= steps == BK_RANK_MAX && q >= 0 && (S.k[q] >> shift) == bk;
+    const int start = q + 1;
+    int q2 = idx + 1;
+    steps = 0;
+    for (; q2 < cnt && steps < BK_RANK_MAX && (S.k[q2] >> shift) == bk; q2++, steps++) r += S.k[q2] < k;
+    big |= steps == BK_RANK_MAX && q2 < cnt && (S.k[q2] >> shift) == bk;
+    S.sorted[start + r] = k;
+  }
+  if (big) S.big = 1;
+  __syncthreads();
+  if (S.big) {  // a dense bucket: block radix sort of the whole chunk on lbits
+    using BRS = cub::BlockRadixSort<uint32_t, BK_THREADS, BK_ITEMS, cub::NullType, 4>;
+    static_assert(sizeof(typename BRS::TempStorage) <= 2 * sizeof(uint32_t) * BK_CAP, "radix scratch");
+    typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(S.k);
+    uint32_t kk[BK_ITEMS];
+#pragma unroll
+    for (int j = 0; j < BK_ITEMS; j++) {
+      const int idx = j * BK_THREADS + t;
+      kk[j] = idx < cnt ? S.k[idx] : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    BRS(tmp).Sort(kk, 0, lbits < 1 ? 1 : lbits);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < BK_ITEMS; j++) {
+      const int idx = t * BK_ITEMS + j;  // blocked output
+      if (idx < cnt) S.sorted[idx] = kk[j];
+    }
+  }
+  __syncthreads();
+  XS_STAMP(3);
+  // 3. thread prefix over the sorted (blocked) items + chunk prefix
+  uint32_t kb[BK_ITEMS];
+  SwState ta = sw_identity();
+  const int my0 = t * BK_ITEMS;
+  uint32_t tlast = 0;
+#pragma unroll
+  for (int j = 0; j < BK_ITEMS; j++) {
+    kb[j] = my0 + j < cnt ? S.sorted[my0 + j] : 0;
+    if (my0 + j < cnt) {
+      sw_apply(ta, kb[j] & 15u);
+      tlast = kb[j];
+      ta.has = 1;
+    }
+  }
+  ta.last = base + tlast;
+  S.last[t] = tlast;
+  SwState dummy;
+  SwState excl = block_exclusive_fast(ta, SwOp(), sw_identity(), S.warp_agg, &dummy);
+  if (warp == 0) {
+    SwState pre = tile_lookback_published((int)c, tile_agg, desc, flags, SwOp(), sw_identity());
+    if (lane == 0) S.tile_pre = pre;
+  }
+  __syncthreads();
+  XS_STAMP(4);
+  SwState cur = SwOp()(S.tile_pre, excl);
+  uint64_t prev = 0;
+  bool have_prev = false;
+  if (t == 0) {
+    have_prev = S.tile_pre.has;
+    prev = S.tile_pre.last;
+  } else if (my0 < cnt) {
+    have_prev = true;
+    prev = base + S.last[t - 1];
+  }
+  // 4. the sweep over this thread's items
+  const uint64_t tmask = (1ull << tb) - 1;
+  const int pshift = tb + 4;
+  CellCache<4> cache;
+  int tr_pid = -1;
+  long long tr_len[1] = {0};
+  int c_pid = -1;
+  int64_t c_ob = 0, c_oc = -1;
+  int c_path = 0;
+#pragma unroll
+  for (int j = 0; j < BK_ITEMS; j++) {
+    if (my0 + j >= cnt) break;
+    const uint64_t k = base + kb[j];
+    if (have_prev && (prev >> 4) != (k >> 4) && (prev >> pshift) == (k >> pshift)) {
+      const unsigned long long len = ((k >> 4) & tmask) - ((prev >> 4) & tmask);
+      const int p = (int)(k >> pshift);
+      unsigned mask = 0;
+#pragma unroll
+      for (int q = 0; q < 5; q++) mask |= (cur.c[q] > 0 ? 1u : 0u) << q;
+      if (mask || cur.c[5] > 0) {
+        if (p != tr_pid) {
+          if (tr_pid >= 0 && tr_len[0])
+            T.add((unsigned long long)tr_pid * n_nodes * 32ull, (unsigned long long)tr_len[0], hist);
+          tr_pid = p;
+          tr_len[0] = 0;
+        }
+        tr_len[0] += (long long)len;
+      }
+      if (mask) {
+        if (p != c_pid) {  // op count base of the pid, cached
+          c_pid = p;
+          c_ob = opbase[p];
+          c_oc = -1;
+        }
+        const int64_t oc = cur.c[6];
+        if (oc != c_oc) {  // the path only changes at OPERATION endpoints
+          c_oc = oc;
+          c_path = oc > c_ob ? pidpath[oc - 1] : 0;
+        }
+        cache.add(((unsigned long long)p * n_nodes + (unsigned long long)c_path) * 32ull + mask, len, T, hist);
+      }
+    }
+    sw_apply(cur, (uint32_t)(k & 15u));
+    prev = k;
+    have_prev = true;
+  }
+  XS_STAMP(5);
+  cache.flush(T, hist);
+  block_keyed_flush<1>(tr_pid, tr_len, [&](int p, const long long* x) {
+    if (x[0]) T.add((unsigned long long)p * n_nodes * 32ull, (unsigned long long)x[0], hist);
+  });
+  __syncthreads();
+  XS_STAMP(6);
+  for (int i = t; i < HT; i += BK_THREADS) {
+    const unsigned long long key = S.h_key[i];
+    if (key != ~0ull) atomicAdd(&hist[key], ((unsigned long long)S.h_hi[i] << 32) | S.h_lo[i]);
+  }
+  __syncthreads();
+  XS_STAMP(7);
+  if (ptrace && t == 0) {
+    for (int i = 0; i < 8; i++) ptrace[c * 8 + i] = tstamp[i];
+  }
+#undef XS_STAMP
+}
+
+__global__ void k_set_i64(int64_t* p, int64_t v) {
+  if (threadIdx.x == 0) *p = v;
+}
+
+// host driver for the bucketed endpoint sort + sweep
+static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, int tb, int corr_mode,
+                            const uint64_t* extra, int64_t n_extra, int64_t nvalid, int key_bits, int n_nodes,
+                            unsigned long long* hist, cudaStream_t s) {
+  OpsState& os = ctx->ops;
+  Stats* st = (Stats*)ctx->ptr[W_STATS];
+  const int64_t n = v.ev.n;
+  const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(nvalid, key_bits));
+  unsigned* counts;
+  int64_t *offs, *chunk;
+  uint64_t* keys;
+  XS_TRY(ws(ctx, W_BK_COUNTS, g.nbuckets + 1, s, &counts));
+  XS_TRY(ws(ctx, W_BK_OFFS, g.nbuckets + 1, s, &offs));
+  XS_TRY(ws(ctx, W_MKEY, nvalid + 1, s, &keys));
+  const int64_t n_chunks = (nvalid + BK_T - 1) / BK_T;
+  XS_TRY(ws(ctx, W_BK_CSTART, 4 * n_chunks + 4, s, &chunk));
+  XS_CUDA(cudaMemsetAsync(counts, 0, g.nbuckets * 4, s));
+  const int64_t threads = n + (n_extra + 1) / 2;
+  {
+    ProfScope ps(ctx, ST_KEYGEN, s);
+    XS_LAUNCH(ctx, k_bk_hist, grid_for(threads), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, extra, n_extra, g.shift,
+              counts);
+  }
+  {
+    ProfScope ps(ctx, ST_MAIN_SORT, s);
+    size_t temp = 0;
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, counts, offs, (int)g.nbuckets, s));
+    void* t;
+    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, counts, offs, (int)g.nbuckets, s));
+    XS_LAUNCH(ctx, k_set_i64, 1, 32, 0, s, offs + g.nbuckets, (int64_t)nvalid);  // offs[nb] = total
+    ctx->launches += 2;
+    XS_LAUNCH(ctx, k_bucket_chunks, grid_for(n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, (int64_t)nvalid,
+              chunk);
+    XS_LAUNCH(ctx, k_bk_scatter, grid_for(threads), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, extra, n_extra, g.shift,
+              counts, offs, keys);
+  }
+  TileDesc<SwState>* desc;
+  int *flags, *tctr;
+  XS_TRY(ws(ctx, W_MSCAN_DESC, n_chunks + 1, s, &desc));
+  XS_TRY(ws(ctx, W_MSCAN_FLAGS, n_chunks + 1, s, &flags));
+  XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
+  XS_CUDA(cudaMemsetAsync(flags, 0, (n_chunks + 1) * sizeof(int), s));
+  XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+  ProfScope ps(ctx, ST_SWEEP, s);
+  static bool attr_set = false;
+  if (!attr_set) {
+    XS_CUDA(cudaFuncSetAttribute(k_bk_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BkSmem)));
+    attr_set = true;
+  }
+  unsigned long long* ptrace = nullptr;
+  if (getenv("XS_TRACE_SWEEP")) XS_CUDA(cudaMallocAsync(&ptrace, n_chunks * 64, s));
+  XS_LAUNCH(ctx, k_bk_sweep, (int)n_chunks, BK_THREADS, sizeof(BkSmem), s, keys, nvalid, chunk, g.shift, tb,
+            os.pidpath, os.opbase, n_nodes, hist, desc, flags, tctr, st, ptrace);
+  if (ptrace) {  // developer timing: per-phase globaltimer stamps of every CTA
+    std::vector<unsigned long long> h(n_chunks * 8);
+    XS_CUDA(cudaMemcpyAsync(h.data(), ptrace, n_chunks * 64, cudaMemcpyDeviceToHost, s));
+    XS_CUDA(cudaStreamSynchronize(s));
+    cudaFreeAsync(ptrace, s);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double ph[7] = {0};
+    for (int64_t c = 0; c < n_chunks; c++) {
+      t0 = std::min(t0, h[c * 8]);
+      t1 = std::max(t1, h[c * 8 + 7]);
+      for (int i = 0; i < 7; i++) ph[i] += (double)(h[c * 8 + i + 1] - h[c * 8 + i]);
+    }
+    fprintf(stderr, "k_bk_sweep trace: chunks %lld span %.1f us; avg per CTA (us): tile %.2f load+pub %.2f rank %.2f "
+            "scan+lookback %.2f walk %.2f flush %.2f table %.2f\n", (long long)n_chunks, (t1 - t0) / 1e3,
+            ph[0] / n_chunks / 1e3, ph[1] / n_chunks / 1e3, ph[2] / n_chunks / 1e3, ph[3] / n_chunks / 1e3,
+            ph[4] / n_chunks / 1e3, ph[5] / n_chunks / 1e3, ph[6] / n_chunks / 1e3);
+  }
+  return XS_OK;
+}
+
 int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s) {
   OpsState& os = ctx->ops;
   Stats* st = (Stats*)ctx->ptr[W_STATS];
@@ -411,6 +927,10 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   const int key_bits = pb + tb + 4;
   const uint64_t sentinel = key_bits >= 64 ? ~0ull : ((1ull << key_bits) - 1);
   const int64_t nkeys = 2 * n + n_piece_keys;
+  const int64_t nvalid_b = 2 * H.n_nonzero + n_piece_keys;
+  if (!ctx->force_lsd && nvalid_b > 0) {
+    XS_TRY(run_bucket_sweep(ctx, v, lo, tb, corr_mode, pieces, n_piece_keys, nvalid_b, key_bits, n_nodes, hist, s));
+  } else {
   uint64_t *mk, *mk_alt;
   XS_TRY(ws(ctx, W_MKEY, nkeys + SW_TILE, s, &mk));
   XS_TRY(ws(ctx, W_MKEY_ALT, nkeys + SW_TILE, s, &mk_alt));
@@ -437,6 +957,7 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
     XS_LAUNCH(ctx, k_sweep, (int)tiles, XS_BLOCK, 0, s, mk, nvalid, tb, os.pidpath, os.opbase, n_nodes, hist, desc,
               flags, tctr);
   }
+  }  // LSD fallback
   // compact
   int *cp, *cn, *cm;
   int64_t *cns, *tracked;

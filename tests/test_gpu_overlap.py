@@ -66,3 +66,29 @@ def test_overlap_repeat_calls_reuse_workspace():
     a = compute_overlap_columnar(ct)
     b = compute_overlap_columnar(ct)
     assert a == b
+
+
+def _dense_trace(n_same: int, seed: int = 0):
+    """Many endpoints on a few identical timestamps: forces dense buckets."""
+    from paper_2102_04285_b200.columnar import ColumnarTrace
+    from paper_2102_04285_b200.model import ProcessMeta
+
+    rng = np.random.default_rng(seed)
+    start = np.concatenate([np.zeros(n_same, np.int64), rng.integers(0, 10**9, 4000)])
+    dur = np.concatenate([rng.integers(1, 50, n_same), rng.integers(1, 10**6, 4000)])
+    cat = rng.integers(1, 6, start.shape[0]).astype(np.uint8)
+    cat[:3] = 0  # a few ops at t=0 (nested: equal start, distinct ends)
+    dur[:3] = [10**9 + 10, 10**9 + 5, 10**9]
+    n = start.shape[0]
+    names = ["a", "b", "c", "x"]
+    name = np.where(cat == 0, np.arange(n) % 3, 3).astype(np.int32)
+    return ColumnarTrace.from_arrays(1, start, dur, np.ones(n, np.int64), np.zeros(n, np.int64), cat, name, names,
+                                     processes=(ProcessMeta(1, "p"),))
+
+
+@pytest.mark.parametrize("n_same", [200, 5000])
+def test_overlap_dense_buckets_vs_oracle(n_same):
+    """200 identical starts -> in-block radix sort branch; 5000 -> bucket overflow -> LSD fallback."""
+    ct = _dense_trace(n_same)
+    bd = compute_overlap_columnar(ct)
+    assert _ours(bd) == _oracle_bd(ct, 0)
