@@ -32,32 +32,35 @@ __global__ void k_site_count(EventView v, int64_t n, const uint8_t* tflag, int* 
   cnt[i] = (c == 0 || c == 4) ? 2 : ((tflag[i] & 3) ? 1 : 0);
 }
 
-// slot layout: pos[i] (+1) for event i.  sub: subkind per slot.
-__global__ void k_site_gen(EventView v, int64_t n, const int* cnt, const int* pos, const int64_t* lo, int tb, int nb,
-                           int* site_ev, uint8_t* site_sub, uint64_t* k2) {
+// slot layout: pos[i] (+1) for event i; primary key (pid | anchor | subkind)
+__global__ void k_site_gen(EventView v, int64_t n, const int* cnt, const int* pos, const int64_t* lo, int tb,
+                           int* site_ev, uint8_t* site_sub, uint64_t* k1) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || cnt[i] == 0) return;
-  int c = v.ev.cat[i];
-  int at = pos[i];
-  uint64_t sec = ((uint64_t)v.ev.tid[i] << nb) | (uint64_t)v.ev.name[i];
+  const int c = v.ev.cat[i];
+  const int at = pos[i];
+  const int p = v.ev.pid[i];
+  const uint64_t pb = (uint64_t)p << (tb + 3);
+  const uint64_t s_rel = (uint64_t)(v.start[i] - lo[p]);
   if (c == 0) {
+    const uint64_t e_rel = s_rel + (uint64_t)v.dur[i];
     site_ev[at] = (int)i;
     site_sub[at] = ANN_START;
+    k1[at] = pb | (s_rel << 3) | ANN_START;
     site_ev[at + 1] = (int)i;
     site_sub[at + 1] = ANN_END;
-    k2[at] = sec;
-    k2[at + 1] = sec;
+    k1[at + 1] = pb | (e_rel << 3) | ANN_END;
   } else if (c == 4) {
     site_ev[at] = (int)i;
     site_sub[at] = API_INTERCEPT;
+    k1[at] = pb | (s_rel << 3) | API_INTERCEPT;
     site_ev[at + 1] = (int)i;
     site_sub[at + 1] = API_INTERNAL;
-    k2[at] = sec;
-    k2[at + 1] = sec;
+    k1[at + 1] = pb | (s_rel << 3) | API_INTERNAL;
   } else {
     site_ev[at] = (int)i;
     site_sub[at] = TRANSITION_HOOK;
-    k2[at] = sec;
+    k1[at] = pb | (s_rel << 3) | TRANSITION_HOOK;
   }
 }
 
@@ -65,47 +68,43 @@ __device__ __forceinline__ int64_t site_anchor(const EventView& v, int i, int su
   return sub == ANN_END ? v.start[i] + v.dur[i] : v.start[i];
 }
 
-__global__ void k_site_k1(EventView v, const uint32_t* slot, int64_t ns, const int* site_ev, const uint8_t* site_sub,
-                          const int64_t* lo, int tb, uint64_t* k1) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= ns) return;
-  uint32_t sl = slot[q];
-  int i = site_ev[sl];
-  int sub = site_sub[sl];
-  int p = v.ev.pid[i];
-  uint64_t a = (uint64_t)(site_anchor(v, i, sub) - lo[p]);
-  k1[q] = ((uint64_t)p << (tb + 3)) | (a << 3) | (uint64_t)sub;
+// After the (pid, anchor, subkind) sort, sites tying on it are ordered by the
+// rest of Site.order_key, (tid, name), then by the reference's insertion
+// order: event index for ANN/API sites; (category, corr or -1, index) for
+// TRANSITION sites (the H->B list, then H->S, each Event.sort_key-ordered).
+// Runs are tiny (nested ops starting together, APIs on several tids), so one
+// thread insertion-sorts each run.
+__device__ __forceinline__ bool site_less(const EventView& v, int ix, int iy, bool transition) {
+  const int tx = v.ev.tid[ix], ty = v.ev.tid[iy];
+  if (tx != ty) return tx < ty;
+  const int nx = v.ev.name[ix], ny = v.ev.name[iy];
+  if (nx != ny) return nx < ny;
+  if (transition) {
+    const int cx = v.ev.cat[ix], cy = v.ev.cat[iy];
+    if (cx != cy) return cx < cy;
+    const int64_t rx = v.ev.has_corr[ix] ? v.ev.corr[ix] : -1;
+    const int64_t ry = v.ev.has_corr[iy] ? v.ev.corr[iy] : -1;
+    if (rx != ry) return rx < ry;
+  }
+  return ix < iy;
 }
 
-// TRANSITION runs tying on (pid, anchor, subkind, tid, name): order by
-// (category, correlation or -1, event index)
 __global__ void k_tie_fix(EventView v, const uint64_t* k1, uint32_t* slot, int64_t ns, const int* site_ev) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= ns) return;
-  if ((k1[q] & 7u) != TRANSITION_HOOK) return;
-  auto same = [&](int64_t a, int64_t b) {
-    if (k1[a] != k1[b]) return false;
-    int ia = site_ev[slot[a]], ib = site_ev[slot[b]];
-    return v.ev.tid[ia] == v.ev.tid[ib] && v.ev.name[ia] == v.ev.name[ib];
-  };
-  if (q > 0 && same(q - 1, q)) return;
-  if (q + 1 >= ns || !same(q, q + 1)) return;
+  const uint64_t k = k1[q];
+  if (q > 0 && k1[q - 1] == k) return;
+  if (q + 1 >= ns || k1[q + 1] != k) return;
   int64_t e = q + 1;
-  while (e < ns && same(q, e)) e++;
-  // insertion sort of slot[q..e)
+  while (e < ns && k1[e] == k) e++;
+  const bool transition = (k & 7u) == TRANSITION_HOOK;
   for (int64_t a = q + 1; a < e; a++) {
-    uint32_t x = slot[a];
-    int ix = site_ev[x];
-    int cx = v.ev.cat[ix];
-    int64_t rx = v.ev.has_corr[ix] ? v.ev.corr[ix] : -1;
+    const uint32_t x = slot[a];
+    const int ix = site_ev[x];
     int64_t b = a - 1;
     while (b >= q) {
-      uint32_t y = slot[b];
-      int iy = site_ev[y];
-      int cy = v.ev.cat[iy];
-      int64_t ry = v.ev.has_corr[iy] ? v.ev.corr[iy] : -1;
-      bool greater = cy != cx ? cy > cx : (ry != rx ? ry > rx : iy > ix);
-      if (!greater) break;
+      const uint32_t y = slot[b];
+      if (!site_less(v, ix, site_ev[y], transition)) break;
       slot[b + 1] = y;
       b--;
     }
@@ -499,11 +498,9 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     XS_TRY(ws(ctx, W_SITE_V_ALT, ns + 1, s, &sl_alt));
     XS_TRY(ws(ctx, W_SITE_EV, ns + 1, s, &site_ev));
     XS_TRY(ws(ctx, W_SITE_SUB, ns + 1, s, &site_sub));
-    XS_LAUNCH(ctx, k_site_gen, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, lo, tb, nb, site_ev, site_sub, k1);
-    // 2. Site.order_key sort: (tid, name) then (pid, anchor, subkind), stable
+    XS_LAUNCH(ctx, k_site_gen, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, lo, tb, site_ev, site_sub, k1);
+    // 2. Site.order_key: one sort on (pid, anchor, subkind) + local tie order
     XS_LAUNCH(ctx, k_iota_u32, grid_for(ns), XS_BLOCK, 0, s, sl, ns);
-    XS_TRY(sort_pairs_u64_u32(ctx, &k1, &k1_alt, &sl, &sl_alt, ns, gb + nb, s));
-    XS_LAUNCH(ctx, k_site_k1, grid_for(ns), XS_BLOCK, 0, s, v, sl, ns, site_ev, site_sub, lo, tb, k1);
     XS_TRY(sort_pairs_u64_u32(ctx, &k1, &k1_alt, &sl, &sl_alt, ns, pb + tb + 3, s));
     XS_LAUNCH(ctx, k_tie_fix, grid_for(ns), XS_BLOCK, 0, s, v, k1, sl, ns, site_ev);
     ps_sites.end();

@@ -29,6 +29,8 @@ struct Stats {
   long long n_fixed;        // CORRELATION: GPU events with a fixed path
   long long n_pieces;       // CORRELATION: own-path pieces
   long long pad[15];
+  long long cat_all[8];     // events per category
+  long long cat_nz[8];      // events per category with duration > 0
 };
 
 enum Slot : int {

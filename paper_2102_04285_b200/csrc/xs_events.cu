@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
   const uint8_t* __restrict__ has_corr = v.ev.has_corr;
 
   long long bad = 0, nz = 0, opsnz = 0, ops = 0, api = 0, apic = 0, gpuc = 0;
+  long long cat_cnt[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // [0..5] all, [6..11] nonzero
   long long bad_api = INT64_MAX;
   int cur_p = -1, cur_g = -1, cur_pops = 0, cur_gops = 0;
   long long lo = 0, hi = 0;
@@ -84,6 +85,11 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
       hi = e > hi ? e : hi;
     }
     nz += d > 0;
+#pragma unroll
+    for (int q = 0; q < 6; q++) {
+      cat_cnt[q] += c == q;
+      cat_cnt[6 + q] += (c == q) & (d > 0);
+    }
     if (c == 0) {
       ops++;
       if (d > 0) {
@@ -134,6 +140,13 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
       if (x[0]) atomicAdd(&group_ops[g], (int)x[0]);
     });
   }
+
+  block_keyed_flush<12>(0, cat_cnt, [&](int, const long long* x) {
+    for (int q = 0; q < 6; q++) {
+      if (x[q]) atomicAdd((unsigned long long*)&st->cat_all[q], (unsigned long long)x[q]);
+      if (x[6 + q]) atomicAdd((unsigned long long*)&st->cat_nz[q], (unsigned long long)x[6 + q]);
+    }
+  });
 
   bad = warp_sum(bad);
   nz = warp_sum(nz);

@@ -9,9 +9,9 @@
 //     count of src events with start <= t < end is > 0.
 // One sorted record stream per call: key = group | t_rel | kind with kinds
 //   0..2 src close (H,B,S), 3..5 src open, 6..8 query (B,S,A)
-// so at one instant closes precede opens precede queries; queries are
-// pre-sorted by descending end (stable LSD), so inside a same-start block the
-// head has the largest end.  One decoupled-lookback scan carries the three
+// so at one instant closes precede opens precede queries; queries that tie
+// on the key are put in descending-end order by a local pass, so inside a
+// same-start block the head has the largest end.  One decoupled-lookback scan carries the three
 // coverage counts and, per query category, a group-segmented running max of
 // ends; an event is contained iff the exclusive max at the head of its run of
 // identical (start, end) is >= its end.
@@ -52,7 +52,7 @@ __device__ __forceinline__ TState t_identity() {
 
 // records: src endpoints (nonzero src events) + queries (all dst events)
 __global__ void k_trec(EventView v, int64_t n, const int64_t* lo, int tb, int src_mask, int dst_mask, uint64_t* key,
-                       uint64_t* skey, uint32_t* val, unsigned long long* count) {
+                       uint32_t* val, unsigned long long* count) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int c = i < n ? v.ev.cat[i] : 0;
   bool is_src = i < n && c >= 1 && c <= 3 && ((src_mask >> c) & 1) && v.dur[i] > 0;
@@ -64,28 +64,42 @@ __global__ void k_trec(EventView v, int64_t n, const int64_t* lo, int tb, int sr
   uint64_t g = (uint64_t)v.ev.tid[i];
   uint64_t s = (uint64_t)(v.start[i] - lo[p]);
   uint64_t e = s + (uint64_t)v.dur[i];
-  const uint64_t tmask = (1ull << tb) - 1;
   if (is_src) {
     key[at] = (g << (tb + 4)) | (e << 4) | (uint64_t)(c - 1);
-    skey[at] = 0;
     val[at] = (uint32_t)i;
     key[at + 1] = (g << (tb + 4)) | (s << 4) | (uint64_t)(c - 1 + 3);
-    skey[at + 1] = 0;
     val[at + 1] = (uint32_t)i;
     at += 2;
   }
   if (is_dst) {
     key[at] = (g << (tb + 4)) | (s << 4) | (uint64_t)(c - 2 + 6);
-    skey[at] = tmask - e;  // descending end
     val[at] = (uint32_t)i;
   }
 }
 
-__global__ void k_tkey_gather_u32(const uint32_t* src, const uint32_t* perm, int64_t m, uint32_t* out);
-
-__global__ void k_tkey_gather(const uint64_t* key_by_rec, const uint32_t* perm, int64_t m, uint64_t* out) {
+// queries with equal (group, start, category): descending end (ties in end
+// are identical intervals, whose order does not matter)
+__global__ void k_trec_tiefix(const uint64_t* key, uint32_t* val, int64_t m, EventView v) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < m) out[q] = key_by_rec[perm[q]];
+  if (q >= m) return;
+  const uint64_t k = key[q];
+  if ((k & 15u) < 6) return;
+  if (q > 0 && key[q - 1] == k) return;
+  if (q + 1 >= m || key[q + 1] != k) return;
+  int64_t e = q + 1;
+  while (e < m && key[e] == k) e++;
+  for (int64_t a = q + 1; a < e; a++) {
+    const uint32_t x = val[a];
+    const int64_t ex = v.start[x] + v.dur[x];
+    int64_t b = a - 1;
+    while (b >= q) {
+      const uint32_t y = val[b];
+      if (v.start[y] + v.dur[y] >= ex) break;
+      val[b + 1] = y;
+      b--;
+    }
+    val[b + 1] = x;
+  }
 }
 
 constexpr int T_ITEMS = 4;
@@ -95,7 +109,6 @@ __global__ void __launch_bounds__(XS_BLOCK) k_tscan(const uint64_t* __restrict__
                                                     int* tile_ctr, int src_mask) {
   const int tile = next_tile(tile_ctr);
   const int64_t base = (int64_t)tile * XS_BLOCK * T_ITEMS + (int64_t)threadIdx.x * T_ITEMS;
-  const uint64_t tmask = (1ull << tb) - 1;
   uint64_t k[T_ITEMS];
   uint32_t ev[T_ITEMS];
   int64_t en[T_ITEMS];
@@ -197,39 +210,31 @@ int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mas
     ctx->err = "timeline too wide for 64-bit transition keys";
     return XS_UNSUPPORTED;
   }
-  const int64_t cap = 3 * n + 1;
-  uint64_t *key, *key_alt, *skey, *skey_alt;
+  // record count is known from pass-1 category counts: no device->host sync
+  int64_t m = 0;
+  for (int c = 1; c <= 3; c++)
+    if ((src_mask >> c) & 1) m += 2 * H.cat_nz[c];
+  for (int c = 2; c <= 4; c++)
+    if ((dst_mask >> c) & 1) m += H.cat_all[c];
+  if (m == 0) return XS_OK;
+  uint64_t *key, *key_alt;
   uint32_t *val, *val_alt;
   unsigned long long* cnt;
-  XS_TRY(ws(ctx, W_TQ_KEY, cap, s, &key));
-  XS_TRY(ws(ctx, W_TQ_KEY_ALT, cap, s, &key_alt));
-  XS_TRY(ws(ctx, W_TSKEY, cap, s, &skey));
-  XS_TRY(ws(ctx, W_TSKEY_ALT, cap, s, &skey_alt));
-  XS_TRY(ws(ctx, W_TQ_VAL, cap, s, &val));
-  XS_TRY(ws(ctx, W_TQ_VAL_ALT, cap, s, &val_alt));
+  XS_TRY(ws(ctx, W_TQ_KEY, m + 1, s, &key));
+  XS_TRY(ws(ctx, W_TQ_KEY_ALT, m + 1, s, &key_alt));
+  XS_TRY(ws(ctx, W_TQ_VAL, m + 1, s, &val));
+  XS_TRY(ws(ctx, W_TQ_VAL_ALT, m + 1, s, &val_alt));
   XS_TRY(ws(ctx, W_TSTAT, 4, s, &cnt));
   XS_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
   const int64_t* lo = (const int64_t*)ctx->ptr[W_SPAN_LO];
-  XS_LAUNCH(ctx, k_trec, grid_for(n), XS_BLOCK, 0, s, v, n, lo, tb, src_mask, dst_mask, key, skey, val, cnt);
-  unsigned long long hm = 0;
-  XS_CUDA(cudaMemcpyAsync(&hm, cnt, 8, cudaMemcpyDeviceToHost, s));
-  XS_CUDA(cudaStreamSynchronize(s));
-  const int64_t m = (int64_t)hm;
-  if (m == 0) return XS_OK;
-  // LSD: descending end, then (group, t, kind).  Values carry the record id.
-  uint32_t *rid, *rid_alt;
-  XS_TRY(ws(ctx, W_TREC_ID, m + 1, s, &rid));
-  XS_TRY(ws(ctx, W_TREC_ID_ALT, m + 1, s, &rid_alt));
   ProfScope ps_sort(ctx, ST_TRANS_SORT, s);
-  XS_LAUNCH(ctx, k_iota_u32, grid_for(m), XS_BLOCK, 0, s, rid, m);
-  XS_TRY(sort_pairs_u64_u32(ctx, &skey, &skey_alt, &rid, &rid_alt, m, tb, s));
-  XS_LAUNCH(ctx, k_tkey_gather, grid_for(m), XS_BLOCK, 0, s, key, rid, m, key_alt);
-  XS_LAUNCH(ctx, k_tkey_gather_u32, grid_for(m), XS_BLOCK, 0, s, val, rid, m, val_alt);
-  uint64_t* k1 = key_alt;
-  uint64_t* k1_alt = key;
-  uint32_t* v1 = val_alt;
-  uint32_t* v1_alt = val;
-  XS_TRY(sort_pairs_u64_u32(ctx, &k1, &k1_alt, &v1, &v1_alt, m, gb + tb + 4, s));
+  XS_LAUNCH(ctx, k_trec, grid_for(n), XS_BLOCK, 0, s, v, n, lo, tb, src_mask, dst_mask, key, val, cnt);
+  // one sort on (group, t, kind); queries tying on it are put in descending
+  // end order locally (the head of a same-start run has the largest end)
+  XS_TRY(sort_pairs_u64_u32(ctx, &key, &key_alt, &val, &val_alt, m, gb + tb + 4, s));
+  XS_LAUNCH(ctx, k_trec_tiefix, grid_for(m), XS_BLOCK, 0, s, key, val, m, v);
+  uint64_t* k1 = key;
+  uint32_t* v1 = val;
   TileDesc<TState>* desc;
   int *tflags, *tctr;
   int32_t* headpos;
