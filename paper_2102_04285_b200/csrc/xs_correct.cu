@@ -93,6 +93,7 @@ __global__ void k_tie_fix(EventView v, const uint64_t* k1, uint32_t* slot, int64
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= ns) return;
   const uint64_t k = k1[q];
+  if (k == ~0ull) return;  // unused upper-bound slots sort last
   if (q > 0 && k1[q - 1] == k) return;
   if (q + 1 >= ns || k1[q + 1] != k) return;
   int64_t e = q + 1;
@@ -123,11 +124,13 @@ __device__ __forceinline__ int64_t site_amount(const xs_profile_t& pr, const Eve
 }
 
 constexpr int Q_ITEMS = 8;
-__global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const uint32_t* slot, int64_t ns, int tb,
+__global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
                                                        EventView v, xs_profile_t pr, const int* site_ev,
                                                        const uint8_t* site_sub, int64_t* qslot,
                                                        TileDesc<SegI128>* desc, int* flags, int* tile_ctr) {
   const int tile = next_tile(tile_ctr);
+  const int64_t ns = *d_ns;
+  if ((int64_t)tile * XS_BLOCK * Q_ITEMS >= ns) return;  // tail tiles of the upper-bound grid
   const int64_t base = (int64_t)tile * XS_BLOCK * Q_ITEMS + (int64_t)threadIdx.x * Q_ITEMS;
   int64_t amt[Q_ITEMS];
   int hd[Q_ITEMS];
@@ -231,13 +234,15 @@ __device__ __forceinline__ int hook_of(int sub) {
 }
 
 constexpr int R_ITEMS = 8;
-__global__ void __launch_bounds__(XS_BLOCK) k_removal(const uint64_t* k1, const uint32_t* slot, int64_t ns, int tb,
+__global__ void __launch_bounds__(XS_BLOCK) k_removal(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
                                                       const int64_t* lenslot, const uint8_t* site_sub,
                                                       const int64_t* lo, const int64_t* hi, int64_t* removed,
                                                       int64_t* slab_a, int64_t* slab_b, int64_t* slab_pre,
                                                       int* pid_slabs, int64_t* ptotal, TileDesc<RM>* desc,
                                                       int* flags, int* tile_ctr) {
   const int tile = next_tile(tile_ctr);
+  const int64_t ns = *d_ns;
+  if ((int64_t)tile * XS_BLOCK * R_ITEMS >= ns) return;  // tail tiles of the upper-bound grid
   const int64_t base = (int64_t)tile * XS_BLOCK * R_ITEMS + (int64_t)threadIdx.x * R_ITEMS;
   const int pshift = tb + 3;
   const uint64_t tmask = (1ull << tb) - 1;
@@ -420,9 +425,28 @@ __global__ void k_init_span(int64_t* lo, int64_t* hi, int np) {
   }
 }
 
-__global__ void k_tkey_gather_u32(const uint32_t* src, const uint32_t* perm, int64_t m, uint32_t* out) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < m) out[q] = src[perm[q]];
+__global__ void k_site_total(const int* pos, const int* cnt, int64_t n, int64_t* d_ns) {
+  if (threadIdx.x == 0) *d_ns = n ? (int64_t)pos[n - 1] + cnt[n - 1] : 0;
+}
+
+// report totals stay on the device: [original, corrected, n_sites, n_slabs]
+__global__ void k_corr_finalize(const Stats* st, const int64_t* d_ns, const int64_t* slab_base, int np,
+                                int corrected_spans, int64_t* totals) {
+  if (threadIdx.x == 0) {
+    totals[0] = st->pad[1];
+    totals[1] = corrected_spans ? st->pad[2] : 0;
+    totals[2] = *d_ns;
+    totals[3] = slab_base[np];
+  }
+}
+
+__global__ void k_span_total(const int64_t* lo, const int64_t* hi, int np, int64_t* out) {
+  long long v = 0;
+  for (int p = threadIdx.x; p < np; p += blockDim.x)
+    if (lo[p] != INT64_MAX) v += hi[p] - lo[p];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long*)out, (unsigned long long)v);
 }
 
 int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start, int64_t* out_dur,
@@ -466,7 +490,13 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
   int *cnt, *pos;
   XS_TRY(ws(ctx, W_SITE_CNT, n + 1, s, &cnt));
   XS_TRY(ws(ctx, W_SITE_POS, n + 1, s, &pos));
-  int64_t ns = 0;
+  // site count bound from pass-1 counts (2 per OPERATION, 2 per ACCEL_API,
+  // <= 1 per BACKEND/SIMULATOR); the exact count stays on the device
+  const Stats& Hc = *ctx->h_stats;
+  const int64_t ns = 2 * Hc.cat_all[0] + 2 * Hc.cat_all[4] + Hc.cat_all[2] + Hc.cat_all[3];
+  int64_t* d_ns;
+  XS_TRY(ws(ctx, W_NS_DEV, 1, s, &d_ns));
+  XS_CUDA(cudaMemsetAsync(d_ns, 0, 8, s));
   ProfScope ps_sites(ctx, ST_SITE_SORT, s);
   if (n) {
     XS_LAUNCH(ctx, k_site_count, grid_for(n), XS_BLOCK, 0, s, v, n, tflag, cnt);
@@ -476,13 +506,8 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
     XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, cnt, pos, (int)n, s));
     ctx->launches += 2;
-    int last_pos = 0, last_cnt = 0;
-    XS_CUDA(cudaMemcpyAsync(&last_pos, pos + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    XS_CUDA(cudaMemcpyAsync(&last_cnt, cnt + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    XS_CUDA(cudaStreamSynchronize(s));
-    ns = (int64_t)last_pos + last_cnt;
+    XS_LAUNCH(ctx, k_site_total, 1, 32, 0, s, pos, cnt, n, d_ns);
   }
-  ctx->corr_sites = ns;
   int64_t *slab_a, *slab_b, *slab_pre;
   XS_TRY(ws(ctx, W_SLAB_A, ns + 1, s, &slab_a));
   XS_TRY(ws(ctx, W_SLAB_B, ns + 1, s, &slab_b));
@@ -498,6 +523,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     XS_TRY(ws(ctx, W_SITE_V_ALT, ns + 1, s, &sl_alt));
     XS_TRY(ws(ctx, W_SITE_EV, ns + 1, s, &site_ev));
     XS_TRY(ws(ctx, W_SITE_SUB, ns + 1, s, &site_sub));
+    XS_CUDA(cudaMemsetAsync(k1, 0xFF, ns * 8, s));  // unused slots: sentinel keys sort last
     XS_LAUNCH(ctx, k_site_gen, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, lo, tb, site_ev, site_sub, k1);
     // 2. Site.order_key: one sort on (pid, anchor, subkind) + local tie order
     XS_LAUNCH(ctx, k_iota_u32, grid_for(ns), XS_BLOCK, 0, s, sl, ns);
@@ -518,7 +544,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
       XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
       XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
       XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
-      XS_LAUNCH(ctx, k_quantize, (int)tiles, XS_BLOCK, 0, s, k1, sl, ns, tb, v, *prof, site_ev, site_sub, qslot, desc,
+      XS_LAUNCH(ctx, k_quantize, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, v, *prof, site_ev, site_sub, qslot, desc,
                 flags, tctr);
     }
     ps_q.end();
@@ -535,7 +561,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
       XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
       XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
       XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
-      XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, ns, tb, lenslot, site_sub, lo, hi, removed,
+      XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, lenslot, site_sub, lo, hi, removed,
                 slab_a, slab_b, slab_pre, pid_slabs, ptotal, desc, flags, tctr);
     }
   }
@@ -554,16 +580,19 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     if (n) XS_LAUNCH(ctx, k_out_spans, grid_for(n), XS_BLOCK, 0, s, v.ev.pid, n, out_start, out_dur, lo2, hi2);
     XS_LAUNCH(ctx, k_totals, grid_for(np + 1), XS_BLOCK, 0, s, lo2, hi2, np, st, 2);
   }
-  XS_TRY(fetch_stats(ctx, s));
+  int64_t* totals;
+  XS_TRY(ws(ctx, W_CORR_TOTALS, 4, s, &totals));
+  XS_LAUNCH(ctx, k_corr_finalize, 1, 32, 0, s, st, d_ns, slab_base, np, corrected_spans ? 1 : 0, totals);
   ctx->corr_pids = np;
-  ctx->corr_original_total = ctx->h_stats->pad[1];
-  ctx->corr_corrected_total = ctx->h_stats->pad[2];
-  {
-    int64_t h_base = 0;
-    XS_CUDA(cudaMemcpyAsync(&h_base, slab_base + np, 8, cudaMemcpyDeviceToHost, s));
-    XS_CUDA(cudaStreamSynchronize(s));
-    ctx->corr_slabs = h_base;
-  }
+  return XS_OK;
+}
+
+int corrected_total_from_spans(xs_ctx* ctx, cudaStream_t s) {
+  int64_t* totals;
+  XS_TRY(ws(ctx, W_CORR_TOTALS, 4, s, &totals));
+  XS_CUDA(cudaMemsetAsync(totals + 1, 0, 8, s));
+  XS_LAUNCH(ctx, k_span_total, 1, 256, 0, s, (const int64_t*)ctx->ptr[W_SPAN_LO], (const int64_t*)ctx->ptr[W_SPAN_HI],
+            ctx->res_pids, totals + 1);
   return XS_OK;
 }
 

@@ -72,21 +72,21 @@ int sort_keys_u64(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, int64_t n, 
 }
 
 int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_bad) {
-  XS_TRY(stage_events(ctx, v, s, true, false, nullptr));
-  XS_TRY(fetch_stats(ctx, s));
-  if (ctx->h_stats->n_bad == 0) {
-    XS_TRY(stage_ops(ctx, v, s, false));
-    XS_TRY(fetch_stats(ctx, s));
+  int st = stage_events(ctx, v, s, true, false, nullptr);
+  if (st == XS_INVALID_TRACE) {
+    *n_bad = ctx->h_stats->n_bad;
+    return XS_OK;
   }
+  XS_TRY(st);
+  XS_TRY(stage_ops(ctx, v, s, false));
+  XS_TRY(fetch_stats(ctx, s));
   *n_bad = ctx->h_stats->n_bad;
   return XS_OK;
 }
 
 int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s) {
   ctx->have_overlap = false;
-  XS_TRY(stage_events(ctx, v, s, true, false, nullptr));
-  XS_TRY(fetch_stats(ctx, s));
-  if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;
+  XS_TRY(stage_events(ctx, v, s, true, false, nullptr));  // syncs once; per-event rule violations stop here
   for (int attempt = 0; attempt < 8; attempt++) {
     XS_TRY(stage_ops(ctx, v, s, true));
     XS_TRY(stage_overlap(ctx, v, attribution, s));
@@ -249,18 +249,18 @@ static int correct_common(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile
   if (!prof || prof->L <= 0) return XS_BAD_ARGUMENT;
   if (ev->n > 0 && (!out_start || !out_dur)) return XS_BAD_ARGUMENT;
   EventView v{*ev, ev->start, ev->dur};
-  XS_TRY(stage_events(ctx, v, s, true, true, prof));
+  XS_TRY(stage_events(ctx, v, s, true, true, prof));  // (sync: sizes; per-event rule violations stop here)
+  XS_TRY(stage_ops(ctx, v, s, false));                // OPERATION nesting is part of require_valid
+  // the pipeline is safe on a trace whose nesting / correlations / API names
+  // turn out bad, so the verdict is read once, after it
+  XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, s));
+  XS_TRY(stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, s));
   XS_TRY(fetch_stats(ctx, s));
-  if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;
-  XS_TRY(stage_ops(ctx, v, s, false));  // OPERATION nesting is part of require_valid
-  XS_TRY(fetch_stats(ctx, s));
-  if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;
+  if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;   // require_valid runs first in the reference
   if (ctx->h_stats->bad_api != INT64_MAX) {
     if (bad_event) *bad_event = ctx->h_stats->bad_api;
     return XS_UNCALIBRATED;
   }
-  XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, s));
-  XS_TRY(stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, s));
   ctx->have_correct = true;
   return XS_OK;
 }
@@ -282,29 +282,23 @@ int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, i
   EventView v{*ev, out_start_dev, out_dur_dev};
   int st = run_overlap(ctx, v, attribution, s);
   if (st != XS_OK) return st;
-  // corrected_total_ns = sum of the corrected pid spans the overlap pass computed
-  std::vector<int64_t> lo(ctx->res_pids), hi(ctx->res_pids);
-  if (ctx->res_pids) {
-    XS_CUDA(cudaMemcpyAsync(lo.data(), ctx->ptr[W_SPAN_LO], lo.size() * 8, cudaMemcpyDeviceToHost, s));
-    XS_CUDA(cudaMemcpyAsync(hi.data(), ctx->ptr[W_SPAN_HI], hi.size() * 8, cudaMemcpyDeviceToHost, s));
-    XS_CUDA(cudaStreamSynchronize(s));
-  }
-  long long tot = 0;
-  for (int p = 0; p < ctx->res_pids; p++)
-    if (lo[p] != INT64_MAX) tot += hi[p] - lo[p];
-  ctx->corr_corrected_total = tot;
-  return XS_OK;
+  // corrected_total_ns = sum of the corrected pid spans the overlap pass
+  // computed; stays on the device until xs_correct_report
+  return corrected_total_from_spans(ctx, s);
 }
 
 int xs_correct_report(xs_ctx_t* ctx, xs_correct_info_t* info, int64_t* removed, int64_t* shortfall,
                       xs_stream_t stream) {
   if (!ctx || !ctx->have_correct) return XS_BAD_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
-  if (info) {
-    info->original_total = ctx->corr_original_total;
-    info->corrected_total = ctx->corr_corrected_total;
-    info->n_sites = ctx->corr_sites;
-    info->n_slabs = ctx->corr_slabs;
+  if (info) {  // [original_total, corrected_total, n_sites, n_slabs] written by the pipeline
+    int64_t tot[4] = {0, 0, 0, 0};
+    XS_CUDA(cudaMemcpyAsync(tot, ctx->ptr[W_CORR_TOTALS], sizeof(tot), cudaMemcpyDeviceToHost, s));
+    XS_CUDA(cudaStreamSynchronize(s));
+    info->original_total = tot[0];
+    info->corrected_total = tot[1];
+    info->n_sites = tot[2];
+    info->n_slabs = tot[3];
   }
   size_t b = (size_t)ctx->corr_pids * 4 * 8;
   if (removed && b) XS_CUDA(cudaMemcpyAsync(removed, ctx->ptr[W_REMOVED], b, cudaMemcpyDeviceToHost, s));

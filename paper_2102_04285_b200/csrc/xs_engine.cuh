@@ -61,6 +61,7 @@ enum Slot : int {
   W_TSKEY, W_TSKEY_ALT, W_HEADPOS, W_TREC_ID, W_TREC_ID_ALT,
   // bucketed sorts
   W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
+  W_CORR_TOTALS, W_NS_DEV,
   W_NUM_SLOTS
 };
 
@@ -158,10 +159,6 @@ struct xs_ctx {
   // last correction
   bool have_correct = false;
   int corr_pids = 0;
-  long long corr_original_total = 0;
-  long long corr_corrected_total = 0;
-  long long corr_sites = 0;
-  long long corr_slabs = 0;
   // last transitions
   long long n_trans_out = 0;
   int trie_cap_log2 = 12;
@@ -284,6 +281,7 @@ int trie_setup(xs_ctx* ctx, cudaStream_t s, TrieView* t);
 __global__ void k_iota_u32(uint32_t* v, int64_t n);
 
 int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_bad);
+int corrected_total_from_spans(xs_ctx* ctx, cudaStream_t s);
 int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
 
 }  // namespace xs

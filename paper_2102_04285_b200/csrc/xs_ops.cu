@@ -123,16 +123,6 @@ __global__ void k_depth_check(const int* d_open, const int* d_close, int64_t m, 
   }
 }
 
-// opens keyed by (depth, stream position): the parent of an op at depth d is
-// the last depth-(d-1) open before it
-__global__ void k_depth_keys(const int* d_open, const int* pos_open, int64_t m, int pbits, uint64_t* dk,
-                             uint32_t* dv) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  dk[r] = ((uint64_t)d_open[r] << pbits) | (uint64_t)pos_open[r];
-  dv[r] = (uint32_t)pos_open[r];
-}
-
 __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t x) {
   while (lo < hi) {
     int64_t m = (lo + hi) >> 1;
@@ -142,55 +132,79 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo
   return lo;
 }
 
-__global__ void k_parent(const int* d_open, const int* pos_open, int64_t m, int pbits, const uint64_t* dk,
-                         const uint32_t* dv, const uint32_t* svals, int* parent) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  int d = d_open[r];
-  if (d < 2) {
-    parent[r] = -1;
-    return;
-  }
-  const uint64_t lo_key = (uint64_t)(d - 1) << pbits;
-  const uint64_t target = lo_key | (uint64_t)pos_open[r];
-  const int64_t q = lower_bound_u64(dk, 0, m, target);  // first >= (d-1, pos)
-  parent[r] = (q > 0 && dk[q - 1] >= lo_key) ? (int)svals[dv[q - 1]] : -1;
-}
-
-// dependency-ordered interning of node(op) = child(node(parent), name)
-__global__ void k_nodes(int64_t m, int use_depth_order, const uint32_t* dv, const uint32_t* svals, const int* parent,
-                        const int* rank_ev, const int32_t* name, int* node, int* ready, int* counter, TrieView t) {
+// Parents and trie nodes in one pass over the endpoint stream, in stream
+// order (a dynamic work queue, so every dependency points at an earlier,
+// already-dequeued position).  For an open at j with depth d >= 2 the parent
+// is the op opened at the nearest previous position whose depth is d-1: if
+// j-1 is an open that is it; if j-1 closes a sibling y, skip y's subtree
+// (jump to pos_open[y]-1).  After 32 hops the sibling's own parent (already
+// resolved or being resolved earlier in the queue) is copied instead, so a
+// wide fan-out costs O(fan-out / 32) waits.  node(o) = child(node(parent),
+// name) with adjacent-name dedupe (trie_intern).
+__global__ void k_parent_nodes(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t n2,
+                               const int* __restrict__ depth, const int* __restrict__ pos_open,
+                               const int* __restrict__ op_ev, const int32_t* __restrict__ name, int tb, int* parent,
+                               int* node, int* pready, int* nready, int* counter, TrieView t) {
   const int lane = threadIdx.x & 31;
   while (true) {
     int base = 0;
     if (lane == 0) base = atomicAdd(counter, 32);
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= m) return;
-    int64_t q = base + lane;
-    bool done = q >= m;
-    int r = -1, p = -1, nm = 0;
+    if (base >= n2) return;
+    const int64_t j = base + lane;
+    bool done = j >= n2 || !(sk[j] & 1ull);  // closes need no work
+    int o = -1, p = -2, nm = 0, wait_on = -1;
     if (!done) {
-      r = use_depth_order ? (int)svals[dv[q]] : (int)q;
-      p = parent[r];
-      nm = name[rank_ev[r]];
+      o = (int)sv[j];
+      nm = name[op_ev[o]];
+      const int d = depth[j];
+      if (d <= 1) {
+        p = -1;
+      } else {
+        const uint64_t g = sk[j] >> (tb + 1);
+        int64_t q = j - 1;
+        for (int hop = 0;; hop++) {
+          if (q < 0 || (sk[q] >> (tb + 1)) != g) {  // only on invalid nesting
+            p = -1;
+            break;
+          }
+          const uint32_t y = sv[q];
+          if (sk[q] & 1ull) {
+            p = (int)y;
+            break;
+          }
+          if (hop >= 32) {  // copy the sibling's parent once it is published
+            wait_on = (int)y;
+            break;
+          }
+          q = (int64_t)pos_open[y] - 1;
+        }
+      }
     }
+    int pn = -1;  // parent's node, -1 = not yet known
     while (!__all_sync(0xffffffffu, done)) {
       if (!done) {
-        int pn = 0;
-        bool ok = true;
-        if (p >= 0) {
-          ok = ((volatile int*)ready)[p] != 0;
-          if (ok) {
+        if (p == -2) {
+          if (((volatile int*)pready)[wait_on]) {
             __threadfence();
-            pn = ((volatile int*)node)[p];
+            p = ((volatile int*)parent)[wait_on];
           }
         }
-        if (ok) {
-          int id = trie_intern(pn, nm, t);
-          node[r] = id;
-          __threadfence();
-          atomicExch(&ready[r], 1);
-          done = true;
+        if (p != -2) {
+          if (p >= 0 && pn < 0) {
+            if (((volatile int*)nready)[p]) {
+              __threadfence();
+              pn = ((volatile int*)node)[p];
+            }
+          }
+          if (p < 0 || pn >= 0) {
+            parent[o] = p;
+            node[o] = trie_intern(p < 0 ? 0 : pn, nm, t);
+            __threadfence();
+            atomicExch(&pready[o], 1);
+            atomicExch(&nready[o], 1);
+            done = true;
+          }
         }
       }
     }
@@ -456,39 +470,23 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   }
   XS_LAUNCH(ctx, k_depth_scatter, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, depth, 2 * m, d_open, pos_open, d_close);
   XS_LAUNCH(ctx, k_depth_check, grid_for(m), XS_BLOCK, 0, s, d_open, d_close, m, st);
-  XS_TRY(fetch_stats(ctx, s));
-  if (ctx->h_stats->n_bad) return XS_OK;  // caller reports InvalidTraceError
-  const long long maxd = ctx->h_stats->max_depth;
-  uint64_t *dk = nullptr, *dk_alt;
-  uint32_t *dv = nullptr, *dv_alt;
-  if (maxd >= 2) {
-    XS_TRY(ws(ctx, W_DKEY, m + 1, s, &dk));
-    XS_TRY(ws(ctx, W_DKEY_ALT, m + 1, s, &dk_alt));
-    XS_TRY(ws(ctx, W_DVAL, m + 1, s, &dv));
-    XS_TRY(ws(ctx, W_DVAL_ALT, m + 1, s, &dv_alt));
-    const int pbits = bits_for((uint64_t)(2 * m));
-    XS_LAUNCH(ctx, k_depth_keys, grid_for(m), XS_BLOCK, 0, s, d_open, pos_open, m, pbits, dk, dv);
-    XS_TRY(sort_pairs_u64_u32(ctx, &dk, &dk_alt, &dv, &dv_alt, m, bits_for((uint64_t)maxd) + pbits, s));
-    XS_LAUNCH(ctx, k_parent, grid_for(m), XS_BLOCK, 0, s, d_open, pos_open, m, pbits, dk, dv, sv, parent);
-  } else {
-    XS_CUDA(cudaMemsetAsync(parent, 0xFF, (m + 1) * sizeof(int), s));
-  }
-  os.parent = parent;
-  if (!build_paths) return XS_OK;
+  if (!build_paths) return XS_OK;  // nesting verdict is read at the caller's next sync
 
-  // 5. node(op) by dependency-ordered interning
+  // 3-5. parents + node(op) in one dependency-ordered pass over the stream
   XS_TRY(trie_setup(ctx, s, &os.trie));
-  int *node, *ready, *ctr;
+  int *node, *pready, *nready, *ctr;
   XS_TRY(ws(ctx, W_NODE, m + 1, s, &node));
-  XS_TRY(ws(ctx, W_READY, m + 1, s, &ready));
+  XS_TRY(ws(ctx, W_READY, 2 * m + 2, s, &pready));
+  nready = pready + (m + 1);
   XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &ctr));
-  XS_CUDA(cudaMemsetAsync(ready, 0, (m + 1) * sizeof(int), s));
+  XS_CUDA(cudaMemsetAsync(pready, 0, (2 * m + 2) * sizeof(int), s));
   XS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), s));
   {
-    int blocks = (int)std::min<int64_t>((m + 255) / 256, 148 * 8);
-    XS_LAUNCH(ctx, k_nodes, blocks, XS_BLOCK, 0, s, m, maxd >= 2 ? 1 : 0, dv, sv, parent, rank_ev, v.ev.name, node,
-              ready, ctr, os.trie);
+    int blocks = (int)std::min<int64_t>((2 * m + 255) / 256, 148 * 8);
+    XS_LAUNCH(ctx, k_parent_nodes, blocks, XS_BLOCK, 0, s, sk, sv, 2 * m, depth, pos_open, op_ev, v.ev.name, tb,
+              parent, node, pready, nready, ctr, os.trie);
   }
+  os.parent = parent;
   os.node = node;
   // 6. path of every op segment, indexed in (pid, t) order
   int* pidpath;

@@ -858,12 +858,18 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
     ctx->err = "timeline too wide for 64-bit endpoint keys";
     return XS_UNSUPPORTED;
   }
-  // the trie is complete once stage_ops has run: size the histogram
-  XS_LAUNCH(ctx, k_trie_count_to_stats, 1, 32, 0, s, os.trie.count, st);
-  XS_TRY(fetch_stats(ctx, s));
+  // histogram row stride: the trie's node capacity when that is small
+  // (no sync), else the real node count (one sync)
   const Stats& H = *ctx->h_stats;
-  if (H.table_full || H.depth_overflow || H.n_bad) return XS_OK;
-  int n_nodes = (int)H.pad[0];
+  int n_nodes;
+  if ((int64_t)np * os.trie.node_cap * 32 <= ((int64_t)1 << 21)) {
+    n_nodes = os.trie.node_cap;
+  } else {
+    XS_LAUNCH(ctx, k_trie_count_to_stats, 1, 32, 0, s, os.trie.count, st);
+    XS_TRY(fetch_stats(ctx, s));
+    if (H.table_full || H.depth_overflow || H.n_bad) return XS_OK;
+    n_nodes = (int)H.pad[0];
+  }
   if (n_nodes < 1) n_nodes = 1;
   const int64_t hist_n = (int64_t)np * n_nodes * 32;
   if (hist_n > ((int64_t)1 << 28)) {
@@ -977,9 +983,11 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
               ccount);
   unsigned long long h_cells = 0;
   XS_CUDA(cudaMemcpyAsync(&h_cells, ccount, 8, cudaMemcpyDeviceToHost, s));
+  XS_LAUNCH(ctx, k_trie_count_to_stats, 1, 32, 0, s, os.trie.count, st);
   XS_TRY(fetch_stats(ctx, s));
   ctx->n_cells = (long long)h_cells;
-  ctx->n_nodes = n_nodes;
+  ctx->n_nodes = (int)ctx->h_stats->pad[0];  // trie nodes actually allocated
+  if (ctx->n_nodes < 1) ctx->n_nodes = 1;
   ctx->res_pids = np;
   return XS_OK;
 }
