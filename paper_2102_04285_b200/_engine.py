@@ -128,6 +128,7 @@ class Engine:
             _init_torch_types()
         self.lib = _lib.load()
         self.device = device
+        self._prof_cache = None
         h = C.c_void_p()
         st = self.lib.xs_ctx_create(device, C.byref(h))
         if st != 0:
@@ -185,14 +186,24 @@ class Engine:
         return r
 
     def _profile(self, dt: DeviceTrace, scaled):
+        # the per-name tables stay resident for the last profile seen (a
+        # ScaledProfile is immutable), so repeated calls copy nothing
+        hit = self._prof_cache
+        if hit is not None and hit[0] is scaled and hit[3] == len(dt.ct.names):
+            return hit[1], hit[2]
+        prof, keep = self._profile_upload(dt, scaled)
+        self._prof_cache = (scaled, prof, keep, len(dt.ct.names))
+        return prof, keep
+
+    def _profile_upload(self, dt: DeviceTrace, scaled):
         torch = _torch()
         dev = torch.device("cuda", self.device)
         n_names = max(len(dt.ct.names), 1)
         internal = torch.zeros(n_names, dtype=torch.int64, device=dev)
         has = torch.zeros(n_names, dtype=torch.uint8, device=dev)
         if len(dt.ct.names):
-            internal.copy_(torch.from_numpy(np.ascontiguousarray(scaled.internal, np.int64)))
-            has.copy_(torch.from_numpy(np.ascontiguousarray(scaled.has_internal, np.uint8)))
+            internal.copy_(torch.from_numpy(np.array(scaled.internal, np.int64)))
+            has.copy_(torch.from_numpy(np.array(scaled.has_internal, np.uint8)))
         prof = _lib.XsProfile(scaled.L, scaled.ann_start, scaled.ann_end, scaled.transition, scaled.interception,
                               internal.data_ptr(), has.data_ptr())
         return prof, (internal, has)

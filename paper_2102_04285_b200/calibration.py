@@ -124,7 +124,7 @@ def _parse_ns(raw: str) -> Fraction:
 INT64_MAX = 2**63 - 1
 
 
-@dataclass
+@dataclass(frozen=True)
 class ScaledProfile:
     """Amounts as integers over the common denominator ``L``.
 
@@ -165,6 +165,8 @@ class ScaledProfile:
                 has[i] = 1
         for v in scaled + [den]:
             _check64(v)
+        ints.flags.writeable = False  # immutable: engines keep a device copy per profile
+        has.flags.writeable = False
         return cls(den, scaled[0], scaled[1], scaled[2], scaled[3], ints, has)
 
     def max_abs(self) -> int:

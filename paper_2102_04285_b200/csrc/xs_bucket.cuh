@@ -101,9 +101,10 @@ __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int64_t lo,
 // the tight bucket range [b0, b1) (first / last nonempty bucket) so each
 // consumer CTA starts with four loads instead of serial searches.
 // offs has nb+1 entries (offs[nb] = total).
-__global__ void k_bucket_chunks(const int64_t* offs, int64_t nb, int64_t n_chunks, int64_t total, int64_t* chunk) {
+__global__ void k_bucket_chunks(const int64_t* offs, int64_t nb, int64_t n_chunks, int64_t* chunk) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_chunks) return;
+  const int64_t total = offs[nb];
   const int64_t b = lower_bound_i64(offs, 0, nb, c * BK_T);
   int64_t s = -1, e = -1, b0 = 0, b1 = 0;
   if (b < nb && offs[b] < total && offs[b] / BK_T == c) {

@@ -10,6 +10,8 @@ namespace xs {
 int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
   if (bytes < 256) bytes = 256;
   if (ctx->cap[slot] < bytes) {
+    if (ctx->capturing) return XS_CAPTURE_ABORT;  // never allocate inside a graph capture
+    ctx->ws_generation++;
     if (ctx->ptr[slot]) XS_CUDA(cudaFreeAsync(ctx->ptr[slot], s));
     size_t nb = bytes + bytes / 4;
     void* p = nullptr;
@@ -86,11 +88,19 @@ int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_b
 
 int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s) {
   ctx->have_overlap = false;
-  XS_TRY(stage_events(ctx, v, s, true, false, nullptr));  // syncs once; per-event rule violations stop here
+  // pass 1 (+ its sync: sizes and per-event rule violations)
+  XS_TRY(stage_events(ctx, v, s, false, false, nullptr));
   for (int attempt = 0; attempt < 8; attempt++) {
-    XS_TRY(stage_ops(ctx, v, s, true));
-    XS_TRY(stage_overlap(ctx, v, attribution, s));
-    // stage_overlap ends with fetch_stats
+    // sync-free segment: correlation table, op paths, sort + sweep + compact
+    std::string key = segment_key(ctx, "overlap", &v, sizeof(v));
+    key.append(reinterpret_cast<const char*>(&attribution), sizeof(attribution));
+    XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
+      XS_TRY(stage_corr_table(ctx, v, w));
+      XS_TRY(stage_ops(ctx, v, w, true));
+      return stage_overlap(ctx, v, attribution, w);
+    }));
+    ctx->res_pids = v.ev.n_pids;
+    XS_TRY(fetch_stats(ctx, s));
     if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;
     if (ctx->h_stats->depth_overflow) {
       ctx->err = "merged multi-tid operation path deeper than the device limit";
@@ -103,6 +113,8 @@ int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s
     if (!ctx->h_stats->table_full) {
       ctx->have_overlap = true;
       ctx->force_lsd = false;
+      ctx->n_cells = ctx->h_stats->pad[4];
+      ctx->n_nodes = ctx->h_stats->pad[0] > 0 ? (int)ctx->h_stats->pad[0] : 1;  // trie nodes allocated
       return XS_OK;
     }
     ctx->trie_cap_log2 += 2;
@@ -144,12 +156,13 @@ int xs_ctx_create(int device, xs_ctx_t** out) {
   c->device = device;
   c->ptr.assign(W_NUM_SLOTS, nullptr);
   c->cap.assign(W_NUM_SLOTS, 0);
-  e = cudaMallocHost(&c->h_stats, sizeof(Stats));
+  e = cudaMallocHost(&c->h_stats, 2 * sizeof(Stats) + 4 * sizeof(int64_t));
   if (e != cudaSuccess) {
     delete c;
     return XS_CUDA_ERROR;
   }
-  memset(c->h_stats, 0, sizeof(Stats));
+  memset(c->h_stats, 0, 2 * sizeof(Stats) + 4 * sizeof(int64_t));
+  c->h_totals = reinterpret_cast<int64_t*>(c->h_stats + 2);
   *out = c;
   return XS_OK;
 }
@@ -158,9 +171,17 @@ void xs_ctx_destroy(xs_ctx_t* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  for (auto& kv : ctx->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (ctx->priv_stream) cudaStreamDestroy(ctx->priv_stream);
+  if (ctx->join_in) cudaEventDestroy(ctx->join_in);
+  if (ctx->join_out) cudaEventDestroy(ctx->join_out);
+  for (cudaEvent_t e : ctx->graph_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   for (void* p : ctx->ptr)
     if (p) cudaFree(p);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
+  if (ctx->h_report) cudaFreeHost(ctx->h_report);
   delete ctx;
 }
 
@@ -242,6 +263,42 @@ int xs_overlap_fetch(xs_ctx_t* ctx, int32_t* cell_pid, int32_t* cell_node, int32
   return XS_OK;
 }
 
+static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start,
+                        int64_t* out_dur, bool corrected_spans, cudaStream_t w) {
+  XS_TRY(stage_corr_table(ctx, v, w));
+  XS_TRY(stage_ops(ctx, v, w, false));  // OPERATION nesting is part of require_valid
+  XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, w));
+  return stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, w);
+}
+
+static int correct_verdict(xs_ctx* ctx, const Stats* h, int64_t* bad_event) {
+  if (h->n_bad) return XS_INVALID_TRACE;  // require_valid runs first in the reference
+  if (h->bad_api != INT64_MAX) {
+    if (bad_event) *bad_event = h->bad_api;
+    return XS_UNCALIBRATED;
+  }
+  ctx->have_correct = true;
+  return XS_OK;
+}
+
+// queue the D2H of what xs_correct_report returns, to land with the next sync
+static int prefetch_report(xs_ctx* ctx, cudaStream_t s) {
+  const size_t b = (size_t)ctx->corr_pids * 4 * 8;
+  if (2 * b > ctx->h_report_cap) {
+    if (ctx->h_report) XS_CUDA(cudaFreeHost(ctx->h_report));
+    ctx->h_report = nullptr;
+    ctx->h_report_cap = 0;
+    XS_CUDA(cudaMallocHost(&ctx->h_report, 2 * b));
+    ctx->h_report_cap = 2 * b;
+  }
+  XS_CUDA(cudaMemcpyAsync(ctx->h_totals, ctx->ptr[W_CORR_TOTALS], 4 * 8, cudaMemcpyDeviceToHost, s));
+  if (b) {
+    XS_CUDA(cudaMemcpyAsync(ctx->h_report, ctx->ptr[W_REMOVED], b, cudaMemcpyDeviceToHost, s));
+    XS_CUDA(cudaMemcpyAsync(ctx->h_report + b / 8, ctx->ptr[W_SHORTFALL], b, cudaMemcpyDeviceToHost, s));
+  }
+  return XS_OK;
+}
+
 static int correct_common(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int64_t* out_start,
                           int64_t* out_dur, int64_t* bad_event, cudaStream_t s, bool corrected_spans) {
   ctx->have_correct = false;
@@ -249,20 +306,21 @@ static int correct_common(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile
   if (!prof || prof->L <= 0) return XS_BAD_ARGUMENT;
   if (ev->n > 0 && (!out_start || !out_dur)) return XS_BAD_ARGUMENT;
   EventView v{*ev, ev->start, ev->dur};
-  XS_TRY(stage_events(ctx, v, s, true, true, prof));  // (sync: sizes; per-event rule violations stop here)
-  XS_TRY(stage_ops(ctx, v, s, false));                // OPERATION nesting is part of require_valid
+  XS_TRY(stage_events(ctx, v, s, false, true, prof));  // (sync: sizes; per-event rule violations stop here)
   // the pipeline is safe on a trace whose nesting / correlations / API names
-  // turn out bad, so the verdict is read once, after it
-  XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, s));
-  XS_TRY(stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, s));
+  // turn out bad, so the verdict is read once, after this sync-free segment
+  std::string key = segment_key(ctx, "correct", &v, sizeof(v));
+  key.append(reinterpret_cast<const char*>(prof), sizeof(*prof));
+  key.append(reinterpret_cast<const char*>(&out_start), sizeof(out_start));
+  key.append(reinterpret_cast<const char*>(&out_dur), sizeof(out_dur));
+  key.push_back(corrected_spans ? 1 : 0);
+  XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
+    return correct_body(ctx, v, prof, out_start, out_dur, corrected_spans, w);
+  }));
+  ctx->corr_pids = v.ev.n_pids;
+  XS_TRY(prefetch_report(ctx, s));
   XS_TRY(fetch_stats(ctx, s));
-  if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;   // require_valid runs first in the reference
-  if (ctx->h_stats->bad_api != INT64_MAX) {
-    if (bad_event) *bad_event = ctx->h_stats->bad_api;
-    return XS_UNCALIBRATED;
-  }
-  ctx->have_correct = true;
-  return XS_OK;
+  return correct_verdict(ctx, ctx->h_stats, bad_event);
 }
 
 int xs_correct(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int64_t* out_start_dev,
@@ -272,38 +330,105 @@ int xs_correct(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, i
   return correct_common(ctx, ev, prof, out_start_dev, out_dur_dev, bad_event, (cudaStream_t)stream, true);
 }
 
+struct SpecScope {  // speculative-pass switches, cleared on every exit path
+  xs_ctx* c;
+  SpecScope(xs_ctx* c_, const int64_t* dur, const long long* a, const long long* b) : c(c_) {
+    c->spec_select_dur = dur;
+    c->spec_guard_a = a;
+    c->spec_guard_b = b;
+    c->spec_keep_counts = true;
+  }
+  ~SpecScope() {
+    c->spec_select_dur = nullptr;
+    c->spec_guard_a = c->spec_guard_b = nullptr;
+    c->spec_keep_counts = false;
+  }
+};
+
+// correct_trace followed by compute_overlap of the corrected trace.  The
+// corrected trace has the original's events, categories, pids and threads, so
+// its overlap pass is launched speculatively in the same sync-free segment as
+// the correction, sized by the original's pass-1 statistics; the corrected
+// trace's own statistics come back with the segment's single sync and any
+// difference that matters for sizing (an interval shrunk to zero length, a
+// retry flag) sends the overlap pass through the ordinary path instead.
 int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
                int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, xs_stream_t stream) {
   XS_TRY(check_events(ctx, ev));
   if (attribution != 0 && attribution != 1) return XS_BAD_ARGUMENT;
   cudaSetDevice(ctx->device);
   cudaStream_t s = (cudaStream_t)stream;
-  XS_TRY(correct_common(ctx, ev, prof, out_start_dev, out_dur_dev, bad_event, s, false));
-  EventView v{*ev, out_start_dev, out_dur_dev};
-  int st = run_overlap(ctx, v, attribution, s);
-  if (st != XS_OK) return st;
-  // corrected_total_ns = sum of the corrected pid spans the overlap pass
-  // computed; stays on the device until xs_correct_report
-  return corrected_total_from_spans(ctx, s);
+  ctx->have_correct = false;
+  ctx->have_overlap = false;
+  if (bad_event) *bad_event = -1;
+  if (!prof || prof->L <= 0) return XS_BAD_ARGUMENT;
+  if (ev->n > 0 && (!out_start_dev || !out_dur_dev)) return XS_BAD_ARGUMENT;
+  EventView v{*ev, ev->start, ev->dur};
+  EventView vc{*ev, out_start_dev, out_dur_dev};
+  XS_TRY(stage_events(ctx, v, s, false, true, prof));  // (sync: sizes; per-event rule violations stop here)
+  const Stats orig = *ctx->h_stats;
+  Stats* st = nullptr;
+  Stats* saved = nullptr;
+  XS_TRY(ws(ctx, W_STATS, 1, s, &st));
+  XS_TRY(ws(ctx, W_STATS_SAVE, 1, s, &saved));
+  const bool spec = !ctx->force_lsd && !getenv("XS_NO_SPECULATE");  // (the env switch is for tests)
+  std::string key = segment_key(ctx, "analyze", &v, sizeof(v));
+  key.append(reinterpret_cast<const char*>(prof), sizeof(*prof));
+  key.append(reinterpret_cast<const char*>(&vc), sizeof(vc));
+  key.append(reinterpret_cast<const char*>(&attribution), sizeof(attribution));
+  key.push_back(spec ? 1 : 0);
+  XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
+    XS_TRY(correct_body(ctx, v, prof, out_start_dev, out_dur_dev, false, w));
+    if (!spec) return XS_OK;
+    XS_CUDA(cudaMemcpyAsync(saved, st, sizeof(Stats), cudaMemcpyDeviceToDevice, w));
+    SpecScope sp(ctx, ev->dur, &st->n_ops_nz, &saved->n_ops_nz);
+    XS_TRY(stage_events_async(ctx, vc, w, false, nullptr));
+    XS_TRY(stage_corr_table(ctx, vc, w));
+    XS_TRY(stage_ops(ctx, vc, w, true));
+    XS_TRY(stage_overlap(ctx, vc, attribution, w));
+    ctx->res_pids = ev->n_pids;
+    return corrected_total_from_spans(ctx, w);
+  }));
+  ctx->corr_pids = ev->n_pids;
+  if (spec) XS_CUDA(cudaMemcpyAsync(ctx->h_stats + 1, saved, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  XS_TRY(prefetch_report(ctx, s));
+  XS_TRY(fetch_stats(ctx, s));
+  XS_TRY(correct_verdict(ctx, spec ? ctx->h_stats + 1 : ctx->h_stats, bad_event));
+  if (spec) {
+    const Stats& c = *ctx->h_stats;  // the corrected trace's pass 1 + the overlap flags
+    bool same = c.n_bad == 0 && !c.table_full && !c.depth_overflow && !c.pad[3] && c.n_ops_nz == orig.n_ops_nz &&
+                c.n_nonzero == orig.n_nonzero && c.multi_op_pids == orig.multi_op_pids &&
+                c.n_api_corr == orig.n_api_corr && c.n_gpu_corr == orig.n_gpu_corr && c.max_span <= orig.max_span;
+    for (int k = 0; k < 8; k++) same = same && c.cat_nz[k] == orig.cat_nz[k];
+    if (same) {
+      ctx->have_overlap = true;
+      ctx->n_cells = c.pad[4];
+      ctx->n_nodes = c.pad[0] > 0 ? (int)c.pad[0] : 1;  // trie nodes allocated
+      return XS_OK;
+    }
+  }
+  int st2 = run_overlap(ctx, vc, attribution, s);
+  if (st2 != XS_OK) return st2;
+  // corrected_total_ns = sum of the corrected pid spans the overlap pass computed
+  XS_TRY(corrected_total_from_spans(ctx, s));
+  XS_CUDA(cudaMemcpyAsync(ctx->h_totals, ctx->ptr[W_CORR_TOTALS], 4 * 8, cudaMemcpyDeviceToHost, s));
+  XS_CUDA(cudaStreamSynchronize(s));
+  return XS_OK;
 }
 
 int xs_correct_report(xs_ctx_t* ctx, xs_correct_info_t* info, int64_t* removed, int64_t* shortfall,
                       xs_stream_t stream) {
+  (void)stream;  // everything arrived with the correction's own final sync
   if (!ctx || !ctx->have_correct) return XS_BAD_ARGUMENT;
-  cudaStream_t s = (cudaStream_t)stream;
   if (info) {  // [original_total, corrected_total, n_sites, n_slabs] written by the pipeline
-    int64_t tot[4] = {0, 0, 0, 0};
-    XS_CUDA(cudaMemcpyAsync(tot, ctx->ptr[W_CORR_TOTALS], sizeof(tot), cudaMemcpyDeviceToHost, s));
-    XS_CUDA(cudaStreamSynchronize(s));
-    info->original_total = tot[0];
-    info->corrected_total = tot[1];
-    info->n_sites = tot[2];
-    info->n_slabs = tot[3];
+    info->original_total = ctx->h_totals[0];
+    info->corrected_total = ctx->h_totals[1];
+    info->n_sites = ctx->h_totals[2];
+    info->n_slabs = ctx->h_totals[3];
   }
-  size_t b = (size_t)ctx->corr_pids * 4 * 8;
-  if (removed && b) XS_CUDA(cudaMemcpyAsync(removed, ctx->ptr[W_REMOVED], b, cudaMemcpyDeviceToHost, s));
-  if (shortfall && b) XS_CUDA(cudaMemcpyAsync(shortfall, ctx->ptr[W_SHORTFALL], b, cudaMemcpyDeviceToHost, s));
-  XS_CUDA(cudaStreamSynchronize(s));
+  const size_t b = (size_t)ctx->corr_pids * 4 * 8;
+  if (removed && b) memcpy(removed, ctx->h_report, b);
+  if (shortfall && b) memcpy(shortfall, ctx->h_report + b / 8, b);
   return XS_OK;
 }
 
@@ -320,6 +445,12 @@ int xs_remap(xs_ctx_t* ctx, int64_t n, const int32_t* pid_dev, const int64_t* va
 namespace xs {
 
 cudaEvent_t prof_event(xs_ctx* ctx) {
+  if (ctx->capturing) {  // owned by the graph being captured, never pooled
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->graph_events.push_back(e);
+    return e;
+  }
   // events in flight are never reused before prof_flush
   if (ctx->pool_next == ctx->ev_pool.size()) {
     cudaEvent_t e;
@@ -336,6 +467,8 @@ void prof_flush(xs_ctx* ctx) {
         cudaEventElapsedTime(&ms, ctx->pend_a[k], ctx->pend_b[k]) == cudaSuccess) {
       ctx->prof_ms[ctx->pend_stage[k]] += ms;
       ctx->prof_calls[ctx->pend_stage[k]] += 1;
+    } else {
+      cudaGetLastError();  // a timing miss must not surface as a later launch error
     }
   }
   ctx->pend_stage.clear();

@@ -1,6 +1,9 @@
 // xs_engine.cuh -- context, workspace and the host-side pipeline contracts.
 #pragma once
 #include <cstdio>
+#include <functional>
+#include <map>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -61,7 +64,7 @@ enum Slot : int {
   W_TSKEY, W_TSKEY_ALT, W_HEADPOS, W_TREC_ID, W_TREC_ID_ALT,
   // bucketed sorts
   W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
-  W_CORR_TOTALS, W_NS_DEV,
+  W_CORR_TOTALS, W_NS_DEV, W_STATS_SAVE, W_PID_OPS_ALT, W_GROUP_OPS_ALT, W_PID_GROUP0_ALT,
   W_NUM_SLOTS
 };
 
@@ -149,7 +152,10 @@ struct xs_ctx {
   std::string err;
   std::vector<void*> ptr;
   std::vector<size_t> cap;
-  xs::Stats* h_stats = nullptr;  // pinned
+  xs::Stats* h_stats = nullptr;  // pinned: [0] last fetch, [1] saved correction stats
+  int64_t* h_totals = nullptr;   // pinned [4]: W_CORR_TOTALS as of the last correction
+  int64_t* h_report = nullptr;   // pinned: removed[np*4] then shortfall[np*4] of the last correction
+  size_t h_report_cap = 0;
   long long launches = 0;
   // last overlap result
   long long n_cells = 0;
@@ -173,6 +179,27 @@ struct xs_ctx {
   std::vector<cudaEvent_t> pend_a, pend_b;
   double prof_ms[32] = {0};
   long long prof_calls[32] = {0};
+  // CUDA-graph replay of sync-free pipeline segments (xs::run_segment)
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<int> prof_stage;
+    std::vector<cudaEvent_t> prof_a, prof_b;
+    long long launches = 0;
+    xs::OpsState ops;
+  };
+  std::map<std::string, GraphEntry> graphs;
+  std::set<std::string> graph_seen, graph_bad;
+  std::vector<cudaEvent_t> graph_events;  // events owned by captured graphs
+  bool capturing = false;
+  // speculative overlap pass of xs_analyze: ops selected by the original
+  // durations, pass-1 counts kept from the original, k_parent_nodes guarded
+  const int64_t* spec_select_dur = nullptr;
+  const long long* spec_guard_a = nullptr;
+  const long long* spec_guard_b = nullptr;
+  bool spec_keep_counts = false;
+  long long ws_generation = 0;  // bumped on every workspace reallocation
+  cudaStream_t priv_stream = nullptr;
+  cudaEvent_t join_in = nullptr, join_out = nullptr;
 };
 
 namespace xs {
@@ -190,14 +217,20 @@ struct ProfScope {  // records [begin, end) of one stage on stream s when profil
   ProfScope(xs_ctx* c_, int st, cudaStream_t s_) : c(c_), stage(st), s(s_) {
     if (c->prof_on) {
       a = prof_event(c);
-      cudaEventRecord(a, s);
+      record(a);
       c->prof_active++;
     }
+  }
+  // inside a stream capture a plain record is only a dependency edge: the
+  // external flag makes the graph record the event each time it is replayed
+  void record(cudaEvent_t e) {
+    if (c->capturing) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
   }
   void end() {
     if (a) {
       cudaEvent_t b = prof_event(c);
-      cudaEventRecord(b, s);
+      record(b);
       c->pend_stage.push_back(stage);
       c->pend_a.push_back(a);
       c->pend_b.push_back(b);
@@ -267,8 +300,10 @@ struct EventView {  // by value: columns are device pointers; start/dur may be o
   const int64_t* dur;
 };
 
+int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool check_api, const xs_profile_t* prof);
 int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr_table, bool check_api,
                  const xs_profile_t* prof);
+int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s);
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths);
 int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
 int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mask, cudaStream_t s);
@@ -281,6 +316,12 @@ int trie_setup(xs_ctx* ctx, cudaStream_t s, TrieView* t);
 __global__ void k_iota_u32(uint32_t* v, int64_t n);
 
 int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_bad);
+// run `body` (a sync-free stream of launches) eagerly the first time a key is
+// seen, capture it into a CUDA graph the second time, replay it afterwards
+int run_segment(xs_ctx* ctx, cudaStream_t s, const std::string& key, bool capturable,
+                const std::function<int(cudaStream_t)>& body);
+std::string segment_key(xs_ctx* ctx, const char* tag, const void* extra, size_t extra_bytes);
+constexpr int XS_CAPTURE_ABORT = 100;  // internal: an allocation was needed while capturing
 int corrected_total_from_spans(xs_ctx* ctx, cudaStream_t s);
 int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
 

@@ -266,8 +266,8 @@ __global__ void k_corr_query(EventView v, int64_t n, const int* state, const int
   if (launch_start) launch_start[i] = INT64_MIN;
 }
 
-int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr_table, bool check_api,
-                 const xs_profile_t* prof) {
+// pass 1 without its sync: the statistics stay on the device
+int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool check_api, const xs_profile_t* prof) {
   const xs_events_t* ev = &v.ev;
   const int64_t n = ev->n;
   const int np = ev->n_pids, ng = ev->n_groups;
@@ -277,9 +277,11 @@ int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr
   XS_TRY(ws(ctx, W_STATS, 1, s, &st));
   XS_TRY(ws(ctx, W_SPAN_LO, np + 1, s, &lo));
   XS_TRY(ws(ctx, W_SPAN_HI, np + 1, s, &hi));
-  XS_TRY(ws(ctx, W_PID_OPS, np + 1, s, &pid_ops));
-  XS_TRY(ws(ctx, W_GROUP_OPS, ng + 1, s, &group_ops));
-  XS_TRY(ws(ctx, W_PID_GROUP0, np + 2, s, &pid_group0));
+  // (a speculative pass keeps the original trace's op counts: its own go to scratch)
+  const bool alt = ctx->spec_keep_counts;
+  XS_TRY(ws(ctx, alt ? W_PID_OPS_ALT : W_PID_OPS, np + 1, s, &pid_ops));
+  XS_TRY(ws(ctx, alt ? W_GROUP_OPS_ALT : W_GROUP_OPS, ng + 1, s, &group_ops));
+  XS_TRY(ws(ctx, alt ? W_PID_GROUP0_ALT : W_PID_GROUP0, np + 2, s, &pid_group0));
   XS_LAUNCH(ctx, k_init_stats, 1, 32, 0, s, st);
   XS_LAUNCH(ctx, k_init_pid, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, pid_ops, np + 1);
   XS_CUDA(cudaMemsetAsync(group_ops, 0, (ng + 1) * sizeof(int), s));
@@ -293,9 +295,23 @@ int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr
   }
   XS_LAUNCH(ctx, k_pid_finish, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, np, ev->group_pid, group_ops, ng,
             pid_group0, st);
+  return XS_OK;
+}
+
+int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr_table, bool check_api,
+                 const xs_profile_t* prof) {
+  XS_TRY(stage_events_async(ctx, v, s, check_api, prof));
   XS_TRY(fetch_stats(ctx, s));
   if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;
   if (!need_corr_table) return XS_OK;
+  return stage_corr_table(ctx, v, s);
+}
+
+// (pid, correlation) table build + GPU-event query; no host sync (capturable)
+int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
+  const xs_events_t* ev = &v.ev;
+  const int64_t n = ev->n;
+  Stats* st = (Stats*)ctx->ptr[W_STATS];
   long long napi = ctx->h_stats->n_api_corr;
   long long ngpu = ctx->h_stats->n_gpu_corr;
   if (ngpu == 0) return XS_OK;

@@ -1,0 +1,112 @@
+// xs_graph.cu -- CUDA-graph capture and replay of sync-free pipeline segments.
+//
+// At config-2 sizes the pipeline is a few dozen short kernels between a
+// handful of host syncs, so host launch latency, not the GPU, bounds the step.
+// Each segment between syncs is a deterministic function of what the host
+// knows at its start: the input/output pointers and sizes, the statistics of
+// the preceding sync, the workspace generation and the retry flags.  Keyed on
+// exactly that, the first sighting runs eagerly (and sizes the workspace), the
+// second is captured into a graph, and later calls replay the graph.  A
+// segment that tries to allocate or synchronize while being captured is
+// marked non-capturable and keeps running eagerly.
+#include "xs_engine.cuh"
+
+namespace xs {
+
+std::string segment_key(xs_ctx* ctx, const char* tag, const void* extra, size_t extra_bytes) {
+  std::string k(tag);
+  k.push_back('\0');
+  k.append(reinterpret_cast<const char*>(ctx->h_stats), sizeof(Stats));
+  k.append(reinterpret_cast<const char*>(extra), extra_bytes);
+  const long long misc[4] = {ctx->ws_generation, ctx->trie_cap_log2, ctx->force_lsd ? 1 : 0, ctx->prof_on ? 1 : 0};
+  k.append(reinterpret_cast<const char*>(misc), sizeof(misc));
+  return k;
+}
+
+static bool graphs_enabled() {
+  static int en = -1;
+  if (en < 0) en = getenv("XS_NO_GRAPHS") ? 0 : 1;
+  return en == 1;
+}
+
+static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
+                          const std::function<int(cudaStream_t)>& body0) {
+  auto body = [&]() { return body0(s); };
+  if (ctx->graph_bad.count(key)) return body();
+  auto it = ctx->graphs.find(key);
+  if (it != ctx->graphs.end()) {
+    XS_CUDA(cudaGraphLaunch(it->second.exec, s));
+    ctx->ops = it->second.ops;
+    ctx->launches += it->second.launches;
+    if (ctx->prof_on)
+      for (size_t i = 0; i < it->second.prof_stage.size(); i++) {
+        ctx->pend_stage.push_back(it->second.prof_stage[i]);
+        ctx->pend_a.push_back(it->second.prof_a[i]);
+        ctx->pend_b.push_back(it->second.prof_b[i]);
+      }
+    return XS_OK;
+  }
+  if (!ctx->graph_seen.count(key)) {  // first sighting: eager (sizes the workspace)
+    ctx->graph_seen.insert(key);
+    return body();
+  }
+  const long long l0 = ctx->launches;
+  const size_t p0 = ctx->pend_stage.size();
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->graph_bad.insert(key);
+    return body();
+  }
+  ctx->capturing = true;
+  const int st = body();
+  ctx->capturing = false;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  cudaGraphExec_t exec = nullptr;
+  if (st == XS_OK && e == cudaSuccess && g) e = cudaGraphInstantiate(&exec, g, 0);
+  if (g) cudaGraphDestroy(g);
+  // timing entries recorded while capturing belong to the graph, not to this call
+  xs_ctx::GraphEntry ge;
+  for (size_t i = p0; i < ctx->pend_stage.size(); i++) {
+    ge.prof_stage.push_back(ctx->pend_stage[i]);
+    ge.prof_a.push_back(ctx->pend_a[i]);
+    ge.prof_b.push_back(ctx->pend_b[i]);
+  }
+  ctx->pend_stage.resize(p0);
+  ctx->pend_a.resize(p0);
+  ctx->pend_b.resize(p0);
+  if (st != XS_OK || e != cudaSuccess || !exec) {  // not capturable: eager from now on
+    cudaGetLastError();
+    ctx->err.clear();
+    ctx->launches = l0;
+    ctx->graph_bad.insert(key);
+    return body();
+  }
+  ge.exec = exec;
+  ge.launches = ctx->launches - l0;
+  ge.ops = ctx->ops;
+  ctx->launches = l0;
+  ctx->graphs[key] = ge;
+  return run_segment_on(ctx, s, key, body0);  // replay it now
+}
+
+// The legacy default stream cannot be captured: segments then run on a
+// private stream joined to the caller's stream by events.
+int run_segment(xs_ctx* ctx, cudaStream_t s, const std::string& key, bool capturable,
+                const std::function<int(cudaStream_t)>& body) {
+  if (!capturable || !graphs_enabled()) return body(s);
+  if (s != 0 && s != cudaStreamLegacy) return run_segment_on(ctx, s, key, body);
+  if (!ctx->priv_stream) {
+    XS_CUDA(cudaStreamCreateWithFlags(&ctx->priv_stream, cudaStreamNonBlocking));
+    XS_CUDA(cudaEventCreateWithFlags(&ctx->join_in, cudaEventDisableTiming));
+    XS_CUDA(cudaEventCreateWithFlags(&ctx->join_out, cudaEventDisableTiming));
+  }
+  XS_CUDA(cudaEventRecord(ctx->join_in, s));
+  XS_CUDA(cudaStreamWaitEvent(ctx->priv_stream, ctx->join_in, 0));
+  const int st = run_segment_on(ctx, ctx->priv_stream, key, body);
+  XS_CUDA(cudaEventRecord(ctx->join_out, ctx->priv_stream));
+  XS_CUDA(cudaStreamWaitEvent(s, ctx->join_out, 0));
+  return st;
+}
+
+}  // namespace xs

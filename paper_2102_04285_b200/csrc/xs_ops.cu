@@ -144,8 +144,21 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo
 __global__ void k_parent_nodes(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t n2,
                                const int* __restrict__ depth, const int* __restrict__ pos_open,
                                const int* __restrict__ op_ev, const int32_t* __restrict__ name, int tb, int* parent,
-                               int* node, int* pready, int* nready, int* counter, TrieView t) {
+                               int* node, int* pready, int* nready, int* counter, TrieView t,
+                               const long long* guard_a, const long long* guard_b) {
   const int lane = threadIdx.x & 31;
+  // speculative pass (xs_analyze): the op set was taken from the original
+  // trace; if an op shrank to zero length the stream is not a valid nesting,
+  // nothing may wait on it, and the pass's result is discarded
+  if (guard_a && *guard_a != *guard_b) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n2; j += (int64_t)gridDim.x * blockDim.x) {
+      if (sk[j] & 1ull) {
+        parent[sv[j]] = -1;
+        node[sv[j]] = 0;
+      }
+    }
+    return;
+  }
   while (true) {
     int base = 0;
     if (lane == 0) base = atomicAdd(counter, 32);
@@ -429,7 +442,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   {
     int* nsel;
     XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &nsel));
-    OpPred pred{v.ev.cat, v.dur};
+    OpPred pred{v.ev.cat, ctx->spec_select_dur ? ctx->spec_select_dur : v.dur};
     size_t temp = 0;
     cub::CountingInputIterator<int> it(0);
     XS_CUDA(cub::DeviceSelect::If(nullptr, temp, it, op_ev, nsel, (int)v.ev.n, pred, s));
@@ -484,7 +497,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   {
     int blocks = (int)std::min<int64_t>((2 * m + 255) / 256, 148 * 8);
     XS_LAUNCH(ctx, k_parent_nodes, blocks, XS_BLOCK, 0, s, sk, sv, 2 * m, depth, pos_open, op_ev, v.ev.name, tb,
-              parent, node, pready, nready, ctr, os.trie);
+              parent, node, pready, nready, ctr, os.trie, ctx->spec_guard_a, ctx->spec_guard_b);
   }
   os.parent = parent;
   os.node = node;

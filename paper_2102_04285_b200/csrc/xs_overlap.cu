@@ -769,8 +769,10 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
 #undef XS_STAMP
 }
 
-__global__ void k_set_i64(int64_t* p, int64_t v) {
-  if (threadIdx.x == 0) *p = v;
+// offs[nb] = number of keys, from the device counts: the host's figure is
+// only an upper bound when the pass was launched speculatively (xs_analyze)
+__global__ void k_bk_total(int64_t* offs, const unsigned* counts, int64_t nb) {
+  if (threadIdx.x == 0) offs[nb] = nb ? offs[nb - 1] + counts[nb - 1] : 0;
 }
 
 // host driver for the bucketed endpoint sort + sweep
@@ -803,10 +805,9 @@ static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, 
     void* t;
     XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
     XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, counts, offs, (int)g.nbuckets, s));
-    XS_LAUNCH(ctx, k_set_i64, 1, 32, 0, s, offs + g.nbuckets, (int64_t)nvalid);  // offs[nb] = total
+    XS_LAUNCH(ctx, k_bk_total, 1, 32, 0, s, offs, counts, (int64_t)g.nbuckets);
     ctx->launches += 2;
-    XS_LAUNCH(ctx, k_bucket_chunks, grid_for(n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, (int64_t)nvalid,
-              chunk);
+    XS_LAUNCH(ctx, k_bucket_chunks, grid_for(n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, chunk);
     XS_LAUNCH(ctx, k_bk_scatter, grid_for(threads), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, extra, n_extra, g.shift,
               counts, offs, keys);
   }
@@ -967,29 +968,22 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   // compact
   int *cp, *cn, *cm;
   int64_t *cns, *tracked;
-  unsigned long long* ccount;
+  unsigned long long* ccount = (unsigned long long*)&st->pad[4];  // read at the caller's final fetch
   const int64_t cells_cap = hist_n + 1;
   XS_TRY(ws(ctx, W_CELL_PID, cells_cap, s, &cp));
   XS_TRY(ws(ctx, W_CELL_NODE, cells_cap, s, &cn));
   XS_TRY(ws(ctx, W_CELL_MASK, cells_cap, s, &cm));
   XS_TRY(ws(ctx, W_CELL_NS, cells_cap, s, &cns));
   XS_TRY(ws(ctx, W_TRACKED, np + 1, s, &tracked));
-  XS_TRY(ws(ctx, W_CELL_COUNT, 1, s, &ccount));
   XS_CUDA(cudaMemsetAsync(tracked, 0, (np + 1) * 8, s));
   XS_CUDA(cudaMemsetAsync(ccount, 0, 8, s));
   ProfScope ps_compact(ctx, ST_COMPACT, s);
   if (hist_n)
     XS_LAUNCH(ctx, k_compact_cells, grid_for(hist_n), XS_BLOCK, 0, s, hist, hist_n, n_nodes, cp, cn, cm, cns, tracked,
               ccount);
-  unsigned long long h_cells = 0;
-  XS_CUDA(cudaMemcpyAsync(&h_cells, ccount, 8, cudaMemcpyDeviceToHost, s));
   XS_LAUNCH(ctx, k_trie_count_to_stats, 1, 32, 0, s, os.trie.count, st);
-  XS_TRY(fetch_stats(ctx, s));
-  ctx->n_cells = (long long)h_cells;
-  ctx->n_nodes = (int)ctx->h_stats->pad[0];  // trie nodes actually allocated
-  if (ctx->n_nodes < 1) ctx->n_nodes = 1;
   ctx->res_pids = np;
-  return XS_OK;
+  return XS_OK;  // cells count (pad[4]) and trie size (pad[0]) arrive with the caller's fetch
 }
 
 }  // namespace xs

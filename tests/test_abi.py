@@ -29,7 +29,7 @@ def test_header_declares_expected_entry_points():
 def test_library_exports_every_header_symbol():
     if not os.path.exists(_lib.LIB_PATH):
         pytest.skip("library not built (run __graft_entry__.build())")
-    lib = ctypes.CDLL(_lib.LIB_PATH)
+    lib = ctypes.CDLL(_lib.LIB_PATH, mode=os.RTLD_NOW)  # resolve every symbol now
     missing = [s for s in header_symbols() if not hasattr(lib, s)]
     assert not missing, missing
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
