@@ -1,0 +1,249 @@
+// xs_bsort.cu -- bucketed (key, value) sort for the pipeline's record sorts.
+//
+// The op-endpoint, transition-record and site sorts hold 0.1-2 M keys of
+// 35-45 bits: CUB's onesweep needs 5-6 latency-bound passes for them.  Their
+// keys are (group, time, code) with time spread over the trace span, so the
+// bucket scheme of xs_bucket.cuh sorts them in one scatter plus one
+// shared-memory pass:
+//   1. histogram of key >> shift into ~2 buckets per key       [read keys]
+//   2. exclusive scan -> bucket offsets, chunk table
+//   3. scatter (key, value) into bucket order                   [read, write]
+//   4. one CTA per chunk (<= BK_CAP records): rank each record inside its
+//      bucket (direct comparison; a block radix sort when some bucket is
+//      dense) and write the chunk back in order                 [read, write]
+// Keys >= 2^key_bits (the callers' "unused slot" sentinels) go to the tail,
+// after every real key, in any order.  The order among equal keys is
+// unspecified: every caller breaks ties with its own total order afterwards
+// (k_op_tiefix, k_trec_tiefix, k_tie_fix).  A chunk that cannot be sorted in
+// shared memory raises Stats.pad[3]; the host then re-runs the call with
+// CUB's radix sort (never silently wrong).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "xs_bucket.cuh"
+
+namespace xs {
+
+
+__global__ void __launch_bounds__(XS_BLOCK) k_bs_hist(const uint64_t* __restrict__ keys, int64_t n, int key_bits,
+                                                      int shift, unsigned* counts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t k = i < n ? keys[i] : 0;
+  const bool valid = i < n && (key_bits >= 64 || (k >> key_bits) == 0);
+  bucket_count(counts, (uint32_t)(k >> shift), valid);
+}
+
+__global__ void __launch_bounds__(XS_BLOCK) k_bs_scatter(const uint64_t* __restrict__ keys,
+                                                         const uint32_t* __restrict__ vals, int64_t n, int key_bits,
+                                                         int shift, unsigned* counts, const int64_t* offs, int64_t nb,
+                                                         unsigned long long* tail, uint64_t* okeys, uint32_t* ovals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = i < n;
+  const uint64_t k = in ? keys[i] : 0;
+  const bool valid = in && (key_bits >= 64 || (k >> key_bits) == 0);
+  const int64_t slot = bucket_slot(counts, offs, (uint32_t)(k >> shift), valid);
+  if (valid) {
+    okeys[slot] = k;
+    ovals[slot] = vals[i];
+  } else if (in) {  // sentinel: after all real keys
+    const int64_t at = offs[nb] + (int64_t)atomicAdd(tail, 1ull);
+    okeys[at] = k;
+    ovals[at] = vals[i];
+  }
+}
+
+// the sentinel tail [offs[nb], n) unchanged from the scatter buffer
+__global__ void k_bs_tail(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n,
+                          const int64_t* total, uint64_t* okeys, uint32_t* ovals) {
+  for (int64_t i = *total + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    okeys[i] = keys[i];
+    ovals[i] = vals[i];
+  }
+}
+
+struct BsSmem {
+  uint64_t k[BK_CAP];  // keys relative to the chunk base, bucket order (as scattered); radix scratch with v[]
+  uint32_t v[BK_CAP];
+  uint64_t sk[BK_CAP];  // sorted
+  uint32_t sv[BK_CAP];
+  int big;
+};
+
+__global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __restrict__ keys,
+                                                           const uint32_t* __restrict__ vals,
+                                                           const int64_t* __restrict__ chunk, int shift,
+                                                           uint64_t* okeys, uint32_t* ovals, Stats* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BsSmem& S = *reinterpret_cast<BsSmem*>(smem_raw);
+  const int t = threadIdx.x;
+  const int64_t c = blockIdx.x;
+  const int64_t s0 = chunk[4 * c + 0];
+  if (s0 < 0) return;
+  const int cnt = (int)(chunk[4 * c + 1] - s0);
+  const int64_t b0 = chunk[4 * c + 2], b1 = chunk[4 * c + 3];
+  const uint64_t base = (uint64_t)b0 << shift;
+  const int lbits = bits_for(((uint64_t)(b1 > b0 ? b1 : b0 + 1) << shift) - 1 - base);
+  if (cnt > BK_CAP) {  // a bucket larger than BK_T: the host re-runs the call through CUB
+    if (t == 0) atomicAdd((unsigned long long*)&st->pad[3], 1ull);
+    return;
+  }
+  if (t == 0) S.big = 0;
+#pragma unroll
+  for (int j = 0; j < BK_ITEMS; j++) {
+    const int idx = j * BK_THREADS + t;
+    if (idx < cnt) {
+      S.k[idx] = keys[s0 + idx] - base;
+      S.v[idx] = vals[s0 + idx];
+    }
+  }
+  __syncthreads();
+  // rank inside the bucket (a bucket is a run of equal k >> shift in k[])
+  bool big = false;
+  for (int j = 0; j < BK_ITEMS; j++) {
+    const int idx = j * BK_THREADS + t;
+    if (idx >= cnt) break;
+    const uint64_t k = S.k[idx];
+    const uint64_t bk = k >> shift;
+    const bool left = idx > 0 && (S.k[idx - 1] >> shift) == bk;
+    const bool right = idx + 1 < cnt && (S.k[idx + 1] >> shift) == bk;
+    if (!left && !right) {
+      S.sk[idx] = k;
+      S.sv[idx] = S.v[idx];
+      continue;
+    }
+    int r = 0, q = idx - 1, steps = 0;
+    for (; q >= 0 && steps < BK_RANK_MAX && (S.k[q] >> shift) == bk; q--, steps++) r += S.k[q] <= k;
+    big |= steps == BK_RANK_MAX && q >= 0 && (S.k[q] >> shift) == bk;
+    const int start = q + 1;
+    int q2 = idx + 1;
+    steps = 0;
+    for (; q2 < cnt && steps < BK_RANK_MAX && (S.k[q2] >> shift) == bk; q2++, steps++) r += S.k[q2] < k;
+    big |= steps == BK_RANK_MAX && q2 < cnt && (S.k[q2] >> shift) == bk;
+    S.sk[start + r] = k;
+    S.sv[start + r] = S.v[idx];
+  }
+  if (big) S.big = 1;
+  __syncthreads();
+  if (S.big) {  // a dense bucket: block radix sort of the whole chunk on lbits
+    using BRS = cub::BlockRadixSort<uint64_t, BK_THREADS, BK_ITEMS, uint32_t, 4>;
+    static_assert(sizeof(typename BRS::TempStorage) <= sizeof(S.k) + sizeof(S.v), "radix scratch");
+    uint64_t kk[BK_ITEMS];
+    uint32_t vv[BK_ITEMS];
+#pragma unroll
+    for (int j = 0; j < BK_ITEMS; j++) {
+      const int idx = t * BK_ITEMS + j;  // blocked
+      kk[j] = idx < cnt ? S.k[idx] : ~0ull;
+      vv[j] = idx < cnt ? S.v[idx] : 0u;
+    }
+    __syncthreads();
+    typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(S.k);
+    // padding (~0, blocked at the end) stays after equal real keys: the sort is stable
+    BRS(tmp).Sort(kk, vv, 0, lbits < 1 ? 1 : lbits);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < BK_ITEMS; j++) {
+      const int idx = t * BK_ITEMS + j;
+      if (idx < cnt) {
+        S.sk[idx] = kk[j];
+        S.sv[idx] = vv[j];
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < BK_ITEMS; j++) {
+    const int idx = j * BK_THREADS + t;
+    if (idx < cnt) {
+      okeys[s0 + idx] = base + S.sk[idx];
+      ovals[s0 + idx] = S.sv[idx];
+    }
+  }
+}
+
+static int bucket_sort_pairs_impl(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals,
+                                  uint32_t** vals_alt, int64_t n, int key_bits, cudaStream_t s);
+
+// XS_CHECK_BSORT=1 (debugging, eager only): compare against a host sort
+int bucket_sort_pairs(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals, uint32_t** vals_alt,
+                      int64_t n, int key_bits, cudaStream_t s) {
+  static const bool check = getenv("XS_CHECK_BSORT") != nullptr;
+  if (!check) return bucket_sort_pairs_impl(ctx, keys, keys_alt, vals, vals_alt, n, key_bits, s);
+  std::vector<uint64_t> in(n), out(n);
+  std::vector<uint32_t> vin(n), vout(n);
+  XS_CUDA(cudaMemcpyAsync(in.data(), *keys, n * 8, cudaMemcpyDeviceToHost, s));
+  XS_CUDA(cudaMemcpyAsync(vin.data(), *vals, n * 4, cudaMemcpyDeviceToHost, s));
+  XS_CUDA(cudaStreamSynchronize(s));
+  XS_TRY(bucket_sort_pairs_impl(ctx, keys, keys_alt, vals, vals_alt, n, key_bits, s));
+  XS_CUDA(cudaMemcpyAsync(out.data(), *keys, n * 8, cudaMemcpyDeviceToHost, s));
+  XS_CUDA(cudaMemcpyAsync(vout.data(), *vals, n * 4, cudaMemcpyDeviceToHost, s));
+  XS_CUDA(cudaStreamSynchronize(s));
+  {  // same (key, value) multiset?
+    std::vector<std::pair<uint64_t, uint32_t>> a(n), b(n);
+    for (int64_t i = 0; i < n; i++) a[i] = {in[i], vin[i]}, b[i] = {out[i], vout[i]};
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    fprintf(stderr, "bsort pairs %s\n", a == b ? "same" : "DIFFER");
+  }
+  const uint64_t lim = key_bits >= 64 ? ~0ull : (1ull << key_bits);
+  std::vector<uint64_t> ref(in);
+  std::stable_sort(ref.begin(), ref.end(), [&](uint64_t a, uint64_t b) {
+    const bool va = a < lim, vb = b < lim;
+    if (va != vb) return va;
+    return va && a < b;
+  });
+  int64_t bad = -1, nsent = 0;
+  for (int64_t i = 0; i < n; i++) {
+    if (ref[i] >= lim) nsent++;
+    if (bad < 0 && ref[i] < lim && ref[i] != out[i]) bad = i;
+  }
+  fprintf(stderr, "bsort check n=%lld bits=%d sentinels=%lld first_mismatch=%lld\n", (long long)n, key_bits,
+          (long long)nsent, (long long)bad);
+  if (bad >= 0)
+    fprintf(stderr, "  ref %llx got %llx\n", (unsigned long long)ref[bad], (unsigned long long)out[bad]);
+  return XS_OK;
+}
+
+static int bucket_sort_pairs_impl(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals,
+                                  uint32_t** vals_alt, int64_t n, int key_bits, cudaStream_t s) {
+  Stats* st = (Stats*)ctx->ptr[W_STATS];
+  const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(n, key_bits));
+  unsigned* counts;
+  int64_t *offs, *chunk;
+  unsigned long long* tail;
+  XS_TRY(ws(ctx, W_BS_COUNTS, g.nbuckets + 1, s, &counts));
+  XS_TRY(ws(ctx, W_BS_OFFS, g.nbuckets + 1, s, &offs));
+  XS_TRY(ws(ctx, W_BS_TAIL, 1, s, &tail));
+  const int64_t n_chunks = (n + BK_T - 1) / BK_T;
+  XS_TRY(ws(ctx, W_BS_CHUNK, 4 * n_chunks + 4, s, &chunk));
+  XS_CUDA(cudaMemsetAsync(counts, 0, g.nbuckets * 4, s));
+  XS_CUDA(cudaMemsetAsync(tail, 0, 8, s));
+  XS_LAUNCH(ctx, k_bs_hist, grid_for(n), XS_BLOCK, 0, s, *keys, n, key_bits, g.shift, counts);
+  {
+    size_t temp = 0;
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, counts, offs, (int)g.nbuckets, s));
+    void* t;
+    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, counts, offs, (int)g.nbuckets, s));
+    ctx->launches += 2;
+  }
+  XS_LAUNCH(ctx, k_bk_total, 1, 32, 0, s, offs, counts, (int64_t)g.nbuckets);
+  XS_LAUNCH(ctx, k_bucket_chunks, grid_for(32 * n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, chunk);
+  XS_LAUNCH(ctx, k_bs_scatter, grid_for(n), XS_BLOCK, 0, s, *keys, *vals, n, key_bits, g.shift, counts, offs,
+            g.nbuckets, tail, *keys_alt, *vals_alt);
+  static bool attr_set = false;
+  if (!attr_set) {
+    XS_CUDA(cudaFuncSetAttribute(k_bs_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BsSmem)));
+    attr_set = true;
+  }
+  // chunks sort from the alt buffers back into the primary ones; the sentinel
+  // tail is copied over unchanged
+  XS_LAUNCH(ctx, k_bs_local, (int)n_chunks, BK_THREADS, sizeof(BsSmem), s, *keys_alt, *vals_alt, chunk, g.shift, *keys,
+            *vals, st);
+  XS_LAUNCH(ctx, k_bs_tail, 148, XS_BLOCK, 0, s, *keys_alt, *vals_alt, n, offs + g.nbuckets, *keys, *vals);
+  return XS_OK;
+}
+
+}  // namespace xs

@@ -22,6 +22,7 @@ constexpr int BK_THREADS = 256;
 constexpr int BK_ITEMS = 16;
 constexpr int BK_CAP = BK_THREADS * BK_ITEMS;  // keys per chunk tile
 constexpr int BK_T = BK_CAP / 2;                // chunk split granule (max bucket)
+constexpr int BK_RANK_MAX = 64;                 // buckets up to this size are ranked by direct comparison
 
 struct BucketGeom {
   int key_bits;  // keys occupy [0, key_bits)
@@ -66,9 +67,13 @@ __device__ __forceinline__ int64_t bucket_slot(unsigned* counts, const int64_t* 
 
 // buckets ~ one per key over the occupied key space (SURVEY 8d key layout)
 inline int bucket_bits_for(int64_t nkeys, int key_bits) {
+  static int adj = [] {
+    const char* e = getenv("XS_BK_BITS_ADJ");  // (tuning experiments)
+    return e ? atoi(e) : 1;
+  }();
   int b = 1;
   while (b < 62 && ((int64_t)1 << b) < nkeys) b++;
-  b += 1;
+  b += adj;
   if (b < 10) b = 10;
   if (b > 24) b = 24;
   return b < key_bits ? b : key_bits;
@@ -97,27 +102,66 @@ __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int64_t lo,
   return lo;
 }
 
-// One thread per chunk, all chunks in parallel: key range [start, end) and
+// offs[nb] = number of keys, from the device counts: the host's figure is
+// only an upper bound when the pass was launched speculatively (xs_analyze)
+static __global__ void k_bk_total(int64_t* offs, const unsigned* counts, int64_t nb) {
+  if (threadIdx.x == 0) offs[nb] = nb ? offs[nb - 1] + counts[nb - 1] : 0;
+}
+
+// Warp-cooperative searches: 32 probes per step shrink the range 32x, so a
+// search over millions of bucket offsets takes ~5 dependent loads, not ~22.
+template <bool kUpper>  // kUpper: first index with a[i] > x, else a[i] >= x
+__device__ __forceinline__ int64_t warp_search_i64(const int64_t* a, int64_t lo, int64_t hi, int64_t x) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t q = lo + lane * step;
+    const bool in = q < hi;
+    const int64_t av = in ? a[q] : 0;
+    const bool pred = in && (kUpper ? av > x : av >= x);
+    const unsigned bal = __ballot_sync(0xffffffffu, pred);
+    if (bal == 0) {
+      const unsigned inb = __ballot_sync(0xffffffffu, in);
+      const int last = 31 - __clz(inb);
+      lo = lo + last * step + 1;
+    } else {
+      const int f = __ffs(bal) - 1;
+      if (f == 0) return lo;
+      const int64_t nhi = lo + f * step;
+      lo = lo + (f - 1) * step + 1;
+      hi = nhi;
+    }
+  }
+  const int64_t q = lo + lane;
+  const bool pred = q < hi && (kUpper ? a[q] > x : a[q] >= x);
+  const unsigned bal = __ballot_sync(0xffffffffu, pred);
+  return bal ? lo + (__ffs(bal) - 1) : hi;
+}
+
+// One warp per chunk, all chunks in parallel: key range [start, end) and
 // the tight bucket range [b0, b1) (first / last nonempty bucket) so each
 // consumer CTA starts with four loads instead of serial searches.
 // offs has nb+1 entries (offs[nb] = total).
-__global__ void k_bucket_chunks(const int64_t* offs, int64_t nb, int64_t n_chunks, int64_t* chunk) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n_chunks) return;
+static __global__ void k_bucket_chunks(const int64_t* offs, int64_t nb, int64_t n_chunks, int64_t* chunk) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= n_chunks) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
   const int64_t total = offs[nb];
-  const int64_t b = lower_bound_i64(offs, 0, nb, c * BK_T);
+  const int64_t b = warp_search_i64<false>(offs, 0, nb, c * BK_T);
   int64_t s = -1, e = -1, b0 = 0, b1 = 0;
   if (b < nb && offs[b] < total && offs[b] / BK_T == c) {
     s = offs[b];
-    const int64_t bn = lower_bound_i64(offs, b, nb, (c + 1) * BK_T);
+    const int64_t bn = warp_search_i64<false>(offs, b, nb, (c + 1) * BK_T);
     e = bn < nb ? offs[bn] : total;
-    b0 = upper_bound_i64(offs, b, nb + 1, s) - 1;   // bucket holding key s
-    b1 = upper_bound_i64(offs, b0, nb + 1, e - 1);  // bucket holding key e-1, plus one
+    b0 = warp_search_i64<true>(offs, b, nb + 1, s) - 1;   // bucket holding key s
+    b1 = warp_search_i64<true>(offs, b0, nb + 1, e - 1);  // bucket holding key e-1, plus one
   }
-  chunk[4 * c + 0] = s;
-  chunk[4 * c + 1] = e;
-  chunk[4 * c + 2] = b0;
-  chunk[4 * c + 3] = b1;
+  if (lane == 0) {
+    chunk[4 * c + 0] = s;
+    chunk[4 * c + 1] = e;
+    chunk[4 * c + 2] = b0;
+    chunk[4 * c + 3] = b1;
+  }
 }
 
 

@@ -387,8 +387,8 @@ __global__ void k_totals(const int64_t* lo, const int64_t* hi, int np, Stats* st
   if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long*)&st->pad[which], (unsigned long long)v);
 }
 
-__global__ void k_zero_pad(Stats* st) {
-  if (threadIdx.x < 4) st->pad[1 + threadIdx.x] = 0;
+__global__ void k_zero_pad(Stats* st) {  // the two span totals (pad[3] is the sort-overflow flag)
+  if (threadIdx.x < 2) st->pad[1 + threadIdx.x] = 0;
 }
 
 // corrected per-pid spans (pid_spans(out), correction.py:184-185)

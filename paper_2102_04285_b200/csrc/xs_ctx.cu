@@ -42,6 +42,9 @@ int sort_pairs_u64_u32(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32
                        int64_t n, int bits, cudaStream_t s) {
   if (n <= 1 || bits <= 0) return XS_OK;
   if (bits > 64) bits = 64;
+  static const bool no_bsort = getenv("XS_NO_BSORT") != nullptr;  // (debug switch)
+  if (!ctx->force_lsd && !no_bsort && n >= 2 * 4096 && n < ((int64_t)1 << 31))
+    return bucket_sort_pairs(ctx, keys, keys_alt, vals, vals_alt, n, bits, s);
   cub::DoubleBuffer<uint64_t> k(*keys, *keys_alt);
   cub::DoubleBuffer<uint32_t> v(*vals, *vals_alt);
   size_t temp = 0;
@@ -73,7 +76,7 @@ int sort_keys_u64(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, int64_t n, 
   return XS_OK;
 }
 
-int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_bad) {
+static int run_validate_once(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_bad) {
   int st = stage_events(ctx, v, s, true, false, nullptr);
   if (st == XS_INVALID_TRACE) {
     *n_bad = ctx->h_stats->n_bad;
@@ -82,8 +85,13 @@ int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_b
   XS_TRY(st);
   XS_TRY(stage_ops(ctx, v, s, false));
   XS_TRY(fetch_stats(ctx, s));
+  if (ctx->h_stats->pad[3] && !ctx->force_lsd) return XS_RETRY_LSD;
   *n_bad = ctx->h_stats->n_bad;
   return XS_OK;
+}
+
+int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_bad) {
+  return with_lsd_retry(ctx, [&] { return run_validate_once(ctx, v, s, n_bad); });
 }
 
 int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s) {
@@ -299,7 +307,7 @@ static int prefetch_report(xs_ctx* ctx, cudaStream_t s) {
   return XS_OK;
 }
 
-static int correct_common(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int64_t* out_start,
+static int correct_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int64_t* out_start,
                           int64_t* out_dur, int64_t* bad_event, cudaStream_t s, bool corrected_spans) {
   ctx->have_correct = false;
   if (bad_event) *bad_event = -1;
@@ -320,6 +328,7 @@ static int correct_common(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile
   ctx->corr_pids = v.ev.n_pids;
   XS_TRY(prefetch_report(ctx, s));
   XS_TRY(fetch_stats(ctx, s));
+  if (ctx->h_stats->pad[3] && !ctx->force_lsd) return XS_RETRY_LSD;  // (before the verdict: order matters to it)
   return correct_verdict(ctx, ctx->h_stats, bad_event);
 }
 
@@ -327,7 +336,9 @@ int xs_correct(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, i
                int64_t* out_dur_dev, int64_t* bad_event, xs_stream_t stream) {
   XS_TRY(check_events(ctx, ev));
   cudaSetDevice(ctx->device);
-  return correct_common(ctx, ev, prof, out_start_dev, out_dur_dev, bad_event, (cudaStream_t)stream, true);
+  return with_lsd_retry(ctx, [&] {
+    return correct_once(ctx, ev, prof, out_start_dev, out_dur_dev, bad_event, (cudaStream_t)stream, true);
+  });
 }
 
 struct SpecScope {  // speculative-pass switches, cleared on every exit path
@@ -352,12 +363,21 @@ struct SpecScope {  // speculative-pass switches, cleared on every exit path
 // trace's own statistics come back with the segment's single sync and any
 // difference that matters for sizing (an interval shrunk to zero length, a
 // retry flag) sends the overlap pass through the ordinary path instead.
+static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
+                        int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, cudaStream_t s);
+
 int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
                int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, xs_stream_t stream) {
   XS_TRY(check_events(ctx, ev));
   if (attribution != 0 && attribution != 1) return XS_BAD_ARGUMENT;
   cudaSetDevice(ctx->device);
-  cudaStream_t s = (cudaStream_t)stream;
+  return with_lsd_retry(ctx, [&] {
+    return analyze_once(ctx, ev, prof, attribution, out_start_dev, out_dur_dev, bad_event, (cudaStream_t)stream);
+  });
+}
+
+static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
+                        int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, cudaStream_t s) {
   ctx->have_correct = false;
   ctx->have_overlap = false;
   if (bad_event) *bad_event = -1;
@@ -383,7 +403,9 @@ int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, i
     XS_CUDA(cudaMemcpyAsync(saved, st, sizeof(Stats), cudaMemcpyDeviceToDevice, w));
     SpecScope sp(ctx, ev->dur, &st->n_ops_nz, &saved->n_ops_nz);
     XS_TRY(stage_events_async(ctx, vc, w, false, nullptr));
-    XS_TRY(stage_corr_table(ctx, vc, w));
+    // correlations are untouched by the correction: the original's dangling
+    // check stands, and only CORRELATION attribution needs launch instants
+    if (attribution == 1) XS_TRY(stage_corr_table(ctx, vc, w));
     XS_TRY(stage_ops(ctx, vc, w, true));
     XS_TRY(stage_overlap(ctx, vc, attribution, w));
     ctx->res_pids = ev->n_pids;
@@ -393,7 +415,9 @@ int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, i
   if (spec) XS_CUDA(cudaMemcpyAsync(ctx->h_stats + 1, saved, sizeof(Stats), cudaMemcpyDeviceToHost, s));
   XS_TRY(prefetch_report(ctx, s));
   XS_TRY(fetch_stats(ctx, s));
-  XS_TRY(correct_verdict(ctx, spec ? ctx->h_stats + 1 : ctx->h_stats, bad_event));
+  const Stats* hc = spec ? ctx->h_stats + 1 : ctx->h_stats;  // the correction part's statistics
+  if (hc->pad[3] && !ctx->force_lsd) return XS_RETRY_LSD;
+  XS_TRY(correct_verdict(ctx, hc, bad_event));
   if (spec) {
     const Stats& c = *ctx->h_stats;  // the corrected trace's pass 1 + the overlap flags
     bool same = c.n_bad == 0 && !c.table_full && !c.depth_overflow && !c.pad[3] && c.n_ops_nz == orig.n_ops_nz &&

@@ -65,6 +65,7 @@ enum Slot : int {
   // bucketed sorts
   W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
   W_CORR_TOTALS, W_NS_DEV, W_STATS_SAVE, W_PID_OPS_ALT, W_GROUP_OPS_ALT, W_PID_GROUP0_ALT,
+  W_BS_COUNTS, W_BS_OFFS, W_BS_TAIL, W_BS_CHUNK,
   W_NUM_SLOTS
 };
 
@@ -291,6 +292,8 @@ int fetch_stats(xs_ctx* ctx, cudaStream_t s);  // D2H of Stats + sync
 // stable radix sorts over [0, bits) (CUB onesweep bring-up backend)
 int sort_pairs_u64_u32(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals, uint32_t** vals_alt,
                        int64_t n, int bits, cudaStream_t s);
+int bucket_sort_pairs(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals, uint32_t** vals_alt,
+                      int64_t n, int key_bits, cudaStream_t s);
 int sort_keys_u64(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, int64_t n, int bits, cudaStream_t s);
 
 // pipeline stages (defined in the .cu files)
@@ -321,7 +324,24 @@ int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_b
 int run_segment(xs_ctx* ctx, cudaStream_t s, const std::string& key, bool capturable,
                 const std::function<int(cudaStream_t)>& body);
 std::string segment_key(xs_ctx* ctx, const char* tag, const void* extra, size_t extra_bytes);
-constexpr int XS_CAPTURE_ABORT = 100;  // internal: an allocation was needed while capturing
+constexpr int XS_CAPTURE_ABORT = 100;
+constexpr int XS_RETRY_LSD = 101;  // a bucketed sort overflowed: re-run the call with CUB radix sorts
+// runs f; on XS_RETRY_LSD runs it once more with every sort on the LSD path
+template <class F>
+int with_lsd_retry(xs_ctx* ctx, F&& f) {
+  int st = f();
+  if (st != XS_RETRY_LSD) return st;
+  if (getenv("XS_CHECK_BSORT")) fprintf(stderr, "lsd retry\n");
+  const bool prev = ctx->force_lsd;
+  ctx->force_lsd = true;
+  st = f();
+  ctx->force_lsd = prev;
+  if (st == XS_RETRY_LSD) {
+    ctx->err = "radix sort overflow on the LSD path";
+    return XS_UNSUPPORTED;
+  }
+  return st;
+}  // internal: an allocation was needed while capturing
 int corrected_total_from_spans(xs_ctx* ctx, cudaStream_t s);
 int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
 

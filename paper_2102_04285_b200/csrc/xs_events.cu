@@ -16,7 +16,7 @@
 
 namespace xs {
 
-constexpr int P1_ITEMS = 16;
+constexpr int P1_ITEMS = 4;
 
 __global__ void k_init_pid(int64_t* lo, int64_t* hi, int* pid_ops, int np) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;

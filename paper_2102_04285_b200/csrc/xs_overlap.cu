@@ -426,7 +426,6 @@ __device__ __forceinline__ void sw_apply(SwState& s, uint32_t code) {
   s.c[6] += cat == 0 ? 1 : 0;
 }
 
-constexpr int BK_RANK_MAX = 64;  // buckets up to this size are ranked by direct comparison
 
 // Shared-memory cell table with native 32-bit adds (a 64-bit shared atomicAdd
 // is a CAS loop on sm_100): value = hi:lo, the carry of each add goes to hi.
@@ -769,11 +768,7 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
 #undef XS_STAMP
 }
 
-// offs[nb] = number of keys, from the device counts: the host's figure is
-// only an upper bound when the pass was launched speculatively (xs_analyze)
-__global__ void k_bk_total(int64_t* offs, const unsigned* counts, int64_t nb) {
-  if (threadIdx.x == 0) offs[nb] = nb ? offs[nb - 1] + counts[nb - 1] : 0;
-}
+
 
 // host driver for the bucketed endpoint sort + sweep
 static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, int tb, int corr_mode,
@@ -807,7 +802,7 @@ static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, 
     XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, counts, offs, (int)g.nbuckets, s));
     XS_LAUNCH(ctx, k_bk_total, 1, 32, 0, s, offs, counts, (int64_t)g.nbuckets);
     ctx->launches += 2;
-    XS_LAUNCH(ctx, k_bucket_chunks, grid_for(n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, chunk);
+    XS_LAUNCH(ctx, k_bucket_chunks, grid_for(32 * n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, chunk);
     XS_LAUNCH(ctx, k_bk_scatter, grid_for(threads), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, extra, n_extra, g.shift,
               counts, offs, keys);
   }

@@ -319,6 +319,12 @@ int xs_transition_sites(xs_ctx_t* ctx, const xs_events_t* ev, int pair_mask, int
   *n_out = 0;
   ctx->n_trans_out = 0;
   EventView v{*ev, ev->start, ev->dur};
+  struct LsdScope {  // not a hot path: CUB radix sorts only, no overflow retries
+    xs_ctx* c;
+    bool prev;
+    ~LsdScope() { c->force_lsd = prev; }
+  } lsd{ctx, ctx->force_lsd};
+  ctx->force_lsd = true;
   XS_TRY(stage_events(ctx, v, s, true, false, nullptr));
   XS_TRY(stage_ops(ctx, v, s, false));
   XS_TRY(fetch_stats(ctx, s));

@@ -150,3 +150,39 @@ def test_stage_profiling_survives_graph_replay():
         assert n > 0 and calls[:n].sum() > 0 and np.all(ms[:n] >= 0)
     finally:
         eng.lib.xs_profile_enable(eng.ctx, 0)
+
+
+def _stretched(ct, gap):
+    """Append one short OPERATION far after the trace: the time span grows by
+    `gap`, so the real records crowd into a few fine buckets of the bucketed
+    sorts (dense-bucket radix branch, or chunk overflow -> CUB re-run)."""
+    import dataclasses
+    i = int(np.flatnonzero(ct.cat == 0)[0])
+    t_end = int((ct.start + ct.dur).max())
+    add = lambda a, v: np.concatenate([a, np.asarray([v], dtype=a.dtype)])  # noqa: E731
+    return dataclasses.replace(
+        ct, start=add(ct.start, t_end + gap), dur=add(ct.dur, 10), pid=add(ct.pid, ct.pid[i]),
+        tid=add(ct.tid, ct.tid[i]), cat=add(ct.cat, 0), name=add(ct.name, ct.name[i]), corr=add(ct.corr, 0),
+        has_corr=add(ct.has_corr, 0), _source=None)
+
+
+@pytest.mark.parametrize("gap", [2**24, 2**30, 2**36, 2**42])
+def test_correction_dense_buckets_vs_oracle(gap):
+    _, inst = synth.ddpg_trace(2500, processes=1, second_tid_ops=True, both=True)
+    ct = _stretched(inst, gap)
+    for prof in (synth.exact_profile(), _frac_profile()):
+        out, rep = correct_trace_columnar(ct, prof)
+        s, d, orep, _ = oracle.correct(ct, prof)
+        assert np.array_equal(out.start, s) and np.array_equal(out.dur, d)
+        assert rep.removed_ns == orep["removed_ns"]
+    s2, d2, _, bd = analyze_columnar(ct, synth.exact_profile())
+    s, d, _, _ = oracle.correct(ct, synth.exact_profile())
+    assert np.array_equal(s2.cpu().numpy(), s) and np.array_equal(d2.cpu().numpy(), d)
+    cells = {(k.pid, k.path, frozenset(int(c) for c in k.categories)): v for k, v in bd.cells.items()}
+    ref_cells, _, _ = oracle.overlap(dataclasses_replace_times(ct, s, d), 0)
+    assert cells == ref_cells
+
+
+def dataclasses_replace_times(ct, start, dur):
+    import dataclasses
+    return dataclasses.replace(ct, start=np.ascontiguousarray(start), dur=np.ascontiguousarray(dur), _source=None)
