@@ -344,22 +344,74 @@ __device__ __forceinline__ int64_t rmap_removed(int64_t y, const int64_t* sa, co
   return r;
 }
 
-__global__ void k_remap(EventView v, int64_t n, const int64_t* lo, const int64_t* sa, const int64_t* sb,
-                        const int64_t* spre, const int64_t* slab_base, const int64_t* ptotal, int64_t* out_start,
-                        int64_t* out_dur) {
+// Sampled index over each pid's slab ends: the pid's time range [0, span]
+// is cut into W = 2^logw windows of 2^shift ns; idx[p*W + w] =
+// bisect_right(ends, w << shift).  A query y in window w then bisects only
+// [idx[w], idx[w+1]] -- a few slabs instead of all of them.
+__device__ __forceinline__ int rmap_shift(const int64_t* lo, const int64_t* hi, int p, int logw) {
+  const int64_t span = hi[p] > lo[p] ? hi[p] - lo[p] : 0;
+  const int b = bits_for((uint64_t)span);
+  return b > logw ? b - logw : 0;
+}
+
+__global__ void k_rmap_index(int np, int logw, const int64_t* lo, const int64_t* hi, const int64_t* sb,
+                             const int64_t* slab_base, int32_t* idx) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t W = (int64_t)1 << logw;
+  if (t >= (int64_t)np * W) return;
+  const int p = (int)(t >> logw);
+  const int64_t w = t & (W - 1);
+  const int64_t base = slab_base[p], K = slab_base[p + 1] - base;
+  if (lo[p] == INT64_MAX) {
+    idx[t] = 0;
+    return;
+  }
+  const uint64_t x = (uint64_t)w << rmap_shift(lo, hi, p, logw);
+  int64_t a = 0, b = K;  // bisect_right(ends, x)
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if ((uint64_t)sb[base + m] <= x) a = m + 1;
+    else b = m;
+  }
+  idx[t] = (int32_t)a;
+}
+
+__device__ __forceinline__ int64_t rmap_removed_idx(int64_t y, const int64_t* sa, const int64_t* sb,
+                                                    const int64_t* spre, int64_t base, int64_t K, int64_t total,
+                                                    const int32_t* pidx, int logw, int shift) {
+  const int64_t W = (int64_t)1 << logw;
+  const int64_t w = y >> shift;  // y in [0, span]: w < W
+  int64_t a = pidx[w], b = w + 1 < W ? pidx[w + 1] : K;
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (sb[base + m] <= y) a = m + 1;
+    else b = m;
+  }
+  if (a == K) return total;
+  int64_t r = spre[base + a];
+  const int64_t s = sa[base + a];
+  if (s < y) r += y - s;
+  return r;
+}
+
+__global__ void k_remap(EventView v, int64_t n, const int64_t* lo, const int64_t* hi, const int64_t* sa,
+                        const int64_t* sb, const int64_t* spre, const int64_t* slab_base, const int64_t* ptotal,
+                        const int32_t* idx, int logw, int64_t* out_start, int64_t* out_dur) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int p = v.ev.pid[i];
   int64_t base = slab_base[p], K = slab_base[p + 1] - base, tot = ptotal[p];
   int64_t s = v.start[i], d = v.dur[i];
   int64_t l = lo[p];
-  int64_t s2 = s - rmap_removed(s - l, sa, sb, spre, base, K, tot);
+  const int shift = rmap_shift(lo, hi, p, logw);
+  const int32_t* pidx = idx + ((int64_t)p << logw);
+  int64_t s2 = s - rmap_removed_idx(s - l, sa, sb, spre, base, K, tot, pidx, logw, shift);
   out_start[i] = s2;
   if (v.ev.cat[i] == 5) {
     out_dur[i] = d;
   } else {
     int64_t e = s + d;
-    out_dur[i] = (e - rmap_removed(e - l, sa, sb, spre, base, K, tot)) - s2;
+    out_dur[i] = (e - rmap_removed_idx(e - l, sa, sb, spre, base, K, tot, pidx, logw, shift)) - s2;
   }
 }
 
@@ -569,9 +621,17 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
   ps_sites.end();
   // 6. remap every event (positional, correction.py:158-165)
   ProfScope ps_m(ctx, ST_REMAP, s);
-  if (n)
-    XS_LAUNCH(ctx, k_remap, grid_for(n), XS_BLOCK, 0, s, v, n, lo, slab_a, slab_b, slab_pre, slab_base, ptotal,
-              out_start, out_dur);
+  if (n) {
+    int logw = bits_for((uint64_t)(ns / (np > 0 ? np : 1)));
+    logw = logw < 4 ? 4 : (logw > 16 ? 16 : logw);
+    while (logw > 4 && ((int64_t)np << logw) > ((int64_t)1 << 24)) logw--;
+    int32_t* ridx;
+    XS_TRY(ws(ctx, W_RMAP_IDX, ((int64_t)np << logw) + 1, s, &ridx));
+    XS_LAUNCH(ctx, k_rmap_index, grid_for((int64_t)np << logw), XS_BLOCK, 0, s, np, logw, lo, hi, slab_b, slab_base,
+              ridx);
+    XS_LAUNCH(ctx, k_remap, grid_for(n), XS_BLOCK, 0, s, v, n, lo, hi, slab_a, slab_b, slab_pre, slab_base, ptotal,
+              ridx, logw, out_start, out_dur);
+  }
   if (corrected_spans) {
     int64_t *lo2, *hi2;
     XS_TRY(ws(ctx, W_OUT_LO, np + 1, s, &lo2));

@@ -65,7 +65,7 @@ enum Slot : int {
   // bucketed sorts
   W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
   W_CORR_TOTALS, W_NS_DEV, W_STATS_SAVE, W_PID_OPS_ALT, W_GROUP_OPS_ALT, W_PID_GROUP0_ALT,
-  W_BS_COUNTS, W_BS_OFFS, W_BS_TAIL, W_BS_CHUNK,
+  W_BS_COUNTS, W_BS_OFFS, W_BS_TAIL, W_BS_CHUNK, W_RMAP_IDX,
   W_NUM_SLOTS
 };
 

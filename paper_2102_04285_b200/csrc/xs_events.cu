@@ -16,7 +16,7 @@
 
 namespace xs {
 
-constexpr int P1_ITEMS = 4;
+constexpr int P1_ITEMS = 16;
 
 __global__ void k_init_pid(int64_t* lo, int64_t* hi, int* pid_ops, int np) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -40,135 +40,203 @@ __device__ __forceinline__ long long warp_sum(long long v) {
   return v;
 }
 
+// Per-thread pass-1 accumulators.  Small counts are packed four to a 64-bit
+// word in 16-bit lanes (a thread sees P1_ITEMS <= 64 events, a warp <= 2048,
+// so no lane overflows a warp reduction) and unpacked once per warp.
+struct P1Acc {
+  unsigned long long cat_all0 = 0, cat_all1 = 0, cat_nz0 = 0, cat_nz1 = 0;  // categories 0-3 / 4-5
+  unsigned long long cnt0 = 0;  // bad, nonzero, ops_nz, ops
+  unsigned long long cnt1 = 0;  // api, api_corr, gpu_corr
+  long long bad_api = INT64_MAX;
+  int cur_p = -1, cur_g = -1, cur_pops = 0, cur_gops = 0;
+  long long lo = 0, hi = 0;
+};
+
+__device__ __forceinline__ void p1_visit(P1Acc& A, int64_t i, int64_t s, int64_t d, int p, int c, bool meta,
+                                         int64_t* lo_out, int64_t* hi_out, int* pid_ops, int* group_ops,
+                                         const EventView& v, const uint8_t* has_internal, int check_api) {
+  const int64_t dd = d > 0 ? d : 0;
+  const unsigned bad = (d < 0) + (s < 0) + (s > 0 && dd > INT64_MAX - s) + !meta;
+  const int64_t e = (int64_t)((uint64_t)s + (uint64_t)d);
+  if (p != A.cur_p) {
+    if (A.cur_p >= 0) {
+      atomic_min_i64(&lo_out[A.cur_p], A.lo);
+      atomic_max_i64(&hi_out[A.cur_p], A.hi);
+      if (A.cur_pops) atomicAdd(&pid_ops[A.cur_p], A.cur_pops);
+    }
+    A.cur_p = p;
+    A.lo = s;
+    A.hi = e;
+    A.cur_pops = 0;
+  } else {
+    A.lo = s < A.lo ? s : A.lo;
+    A.hi = e > A.hi ? e : A.hi;
+  }
+  const bool nzd = d > 0;
+  const unsigned long long one = 1ull << (16 * (c & 3));
+  if (c < 4) {
+    A.cat_all0 += one;
+    A.cat_nz0 += nzd ? one : 0ull;
+  } else {
+    A.cat_all1 += one;
+    A.cat_nz1 += nzd ? one : 0ull;
+  }
+  A.cnt0 += (unsigned long long)bad | ((unsigned long long)nzd << 16) |
+            ((unsigned long long)(c == 0 && nzd) << 32) | ((unsigned long long)(c == 0) << 48);
+  if (c == 0) {
+    if (nzd) {
+      A.cur_pops++;
+      const int g = v.ev.tid[i];
+      if (g != A.cur_g) {
+        if (A.cur_g >= 0 && A.cur_gops) atomicAdd(&group_ops[A.cur_g], A.cur_gops);
+        A.cur_g = g;
+        A.cur_gops = 0;
+      }
+      A.cur_gops++;
+    }
+  } else if (c == 4) {
+    A.cnt1 += 1ull | ((unsigned long long)v.ev.has_corr[i] << 16);
+    if (check_api && !has_internal[v.ev.name[i]]) A.bad_api = i < A.bad_api ? i : A.bad_api;
+  } else if (c == 5) {
+    A.cnt1 += (unsigned long long)v.ev.has_corr[i] << 32;
+  }
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+constexpr int P1_VEC = 4;  // events per vector step (16-byte loads)
+
+// One streaming pass; each thread takes P1_ITEMS consecutive events in
+// vector steps of 4 (16-byte loads of start/dur/pid, one 4-byte load of the
+// categories) when the columns are aligned for it.  Counters reduce per warp
+// into shared memory, then one global atomic per counter per CTA.
+template <bool kVec>
 __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, const uint8_t* __restrict__ has_meta,
                                                     const uint8_t* __restrict__ has_internal, int check_api,
                                                     Stats* st, int64_t* lo_out, int64_t* hi_out, int* pid_ops,
                                                     int* group_ops) {
-  const int64_t* __restrict__ start = v.start;
-  const int64_t* __restrict__ dur = v.dur;
-  const int32_t* __restrict__ pid = v.ev.pid;
-  const int32_t* __restrict__ tid = v.ev.tid;
-  const uint8_t* __restrict__ cat = v.ev.cat;
-  const int32_t* __restrict__ name = v.ev.name;
-  const uint8_t* __restrict__ has_corr = v.ev.has_corr;
-
-  long long bad = 0, nz = 0, opsnz = 0, ops = 0, api = 0, apic = 0, gpuc = 0;
-  long long cat_cnt[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // [0..5] all, [6..11] nonzero
-  long long bad_api = INT64_MAX;
-  int cur_p = -1, cur_g = -1, cur_pops = 0, cur_gops = 0;
-  long long lo = 0, hi = 0;
-  const int64_t base = (int64_t)blockIdx.x * XS_BLOCK * P1_ITEMS + threadIdx.x;
-#pragma unroll 4
-  for (int k = 0; k < P1_ITEMS; k++) {
-    int64_t i = base + (int64_t)k * XS_BLOCK;
-    if (i >= n) break;
-    int64_t s = start[i], d = dur[i];
-    int p = pid[i];
-    int c = cat[i];
-    bad += (d < 0) + (s < 0);
-    int64_t dd = d > 0 ? d : 0;
-    bad += (s > 0 && dd > INT64_MAX - s);
-    bad += !has_meta[p];
-    int64_t e = (int64_t)((uint64_t)s + (uint64_t)d);
-    if (p != cur_p) {
-      if (cur_p >= 0) {
-        atomic_min_i64(&lo_out[cur_p], lo);
-        atomic_max_i64(&hi_out[cur_p], hi);
-        if (cur_pops) atomicAdd(&pid_ops[cur_p], cur_pops);
-      }
-      cur_p = p;
-      lo = s;
-      hi = e;
-      cur_pops = 0;
+  __shared__ unsigned long long s_cnt[20];  // cat_all[6], cat_nz[6], bad, nz, ops_nz, ops, api, api_corr, gpu_corr
+  __shared__ long long s_bad_api;
+  if (threadIdx.x < 20) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_bad_api = INT64_MAX;
+  P1Acc A;
+  const int64_t tbase = ((int64_t)blockIdx.x * XS_BLOCK + threadIdx.x) * P1_ITEMS;
+#pragma unroll 1
+  for (int step = 0; step < P1_ITEMS / P1_VEC; step++) {
+    const int64_t i0 = tbase + step * P1_VEC;
+    if (i0 >= n) break;
+    int64_t s[4], d[4];
+    int p[4], c[4];
+    int cnt = 4;
+    if (kVec && i0 + 4 <= n) {
+      const longlong2 s01 = *reinterpret_cast<const longlong2*>(v.start + i0);
+      const longlong2 s23 = *reinterpret_cast<const longlong2*>(v.start + i0 + 2);
+      const longlong2 d01 = *reinterpret_cast<const longlong2*>(v.dur + i0);
+      const longlong2 d23 = *reinterpret_cast<const longlong2*>(v.dur + i0 + 2);
+      const int4 p4 = *reinterpret_cast<const int4*>(v.ev.pid + i0);
+      const uint32_t c4 = *reinterpret_cast<const uint32_t*>(v.ev.cat + i0);
+      s[0] = s01.x, s[1] = s01.y, s[2] = s23.x, s[3] = s23.y;
+      d[0] = d01.x, d[1] = d01.y, d[2] = d23.x, d[3] = d23.y;
+      p[0] = p4.x, p[1] = p4.y, p[2] = p4.z, p[3] = p4.w;
+#pragma unroll
+      for (int k = 0; k < 4; k++) c[k] = (int)((c4 >> (8 * k)) & 0xFFu);
     } else {
-      lo = s < lo ? s : lo;
-      hi = e > hi ? e : hi;
-    }
-    nz += d > 0;
+      cnt = (int)(n - i0 < 4 ? n - i0 : 4);
 #pragma unroll
-    for (int q = 0; q < 6; q++) {
-      cat_cnt[q] += c == q;
-      cat_cnt[6 + q] += (c == q) & (d > 0);
-    }
-    if (c == 0) {
-      ops++;
-      if (d > 0) {
-        opsnz++;
-        cur_pops++;
-        int g = tid[i];
-        if (g != cur_g) {
-          if (cur_g >= 0 && cur_gops) atomicAdd(&group_ops[cur_g], cur_gops);
-          cur_g = g;
-          cur_gops = 0;
+      for (int k = 0; k < 4; k++) {
+        if (k < cnt) {
+          s[k] = v.start[i0 + k];
+          d[k] = v.dur[i0 + k];
+          p[k] = v.ev.pid[i0 + k];
+          c[k] = v.ev.cat[i0 + k];
         }
-        cur_gops++;
       }
-    } else if (c == 4) {
-      api++;
-      apic += has_corr[i];
-      if (check_api && !has_internal[name[i]]) bad_api = i < bad_api ? i : bad_api;
-    } else if (c == 5) {
-      gpuc += has_corr[i];
     }
-  }
-  // flush the running per-pid reduction: warp-aggregate when the warp agrees
-  const unsigned full = 0xffffffffu;
-  int p0 = __shfl_sync(full, cur_p, 0);
-  bool uniform = __all_sync(full, cur_p == p0);
-  if (uniform && p0 >= 0) {
-    long long l = lo, h = hi;
+    int mp = -1;
+    bool meta = false;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      long long l2 = __shfl_xor_sync(full, l, o), h2 = __shfl_xor_sync(full, h, o);
-      l = l2 < l ? l2 : l;
-      h = h2 > h ? h2 : h;
+    for (int k = 0; k < 4; k++) {
+      if (k < cnt) {
+        if (p[k] != mp) {
+          mp = p[k];
+          meta = has_meta[mp] != 0;
+        }
+        p1_visit(A, i0 + k, s[k], d[k], p[k], c[k], meta, lo_out, hi_out, pid_ops, group_ops, v, has_internal,
+                 check_api);
+      }
     }
-    long long po = warp_sum(cur_pops);
-    if ((threadIdx.x & 31) == 0) {
-      atomic_min_i64(&lo_out[p0], l);
-      atomic_max_i64(&hi_out[p0], h);
-      if (po) atomicAdd(&pid_ops[p0], (int)po);
-    }
-  } else if (cur_p >= 0) {
-    atomic_min_i64(&lo_out[cur_p], lo);
-    atomic_max_i64(&hi_out[cur_p], hi);
-    if (cur_pops) atomicAdd(&pid_ops[cur_p], cur_pops);
   }
-  {
-    long long gv[1] = {cur_gops};
-    block_keyed_flush<1>(cur_gops ? cur_g : -1, gv, [&](int g, const long long* x) {
-      if (x[0]) atomicAdd(&group_ops[g], (int)x[0]);
-    });
-  }
-
-  block_keyed_flush<12>(0, cat_cnt, [&](int, const long long* x) {
-    for (int q = 0; q < 6; q++) {
-      if (x[q]) atomicAdd((unsigned long long*)&st->cat_all[q], (unsigned long long)x[q]);
-      if (x[6 + q]) atomicAdd((unsigned long long*)&st->cat_nz[q], (unsigned long long)x[6 + q]);
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  // running per-pid span / op count: warp-aggregate when the warp agrees
+  const int p0 = __shfl_sync(full, A.cur_p, 0);
+  if (__all_sync(full, A.cur_p == p0)) {
+    if (p0 >= 0) {
+      long long l = A.lo, h = A.hi;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const long long l2 = __shfl_xor_sync(full, l, o), h2 = __shfl_xor_sync(full, h, o);
+        l = l2 < l ? l2 : l;
+        h = h2 > h ? h2 : h;
+      }
+      const long long po = warp_sum(A.cur_pops);
+      if (lane == 0) {
+        atomic_min_i64(&lo_out[p0], l);
+        atomic_max_i64(&hi_out[p0], h);
+        if (po) atomicAdd(&pid_ops[p0], (int)po);
+      }
     }
-  });
-
-  bad = warp_sum(bad);
-  nz = warp_sum(nz);
-  opsnz = warp_sum(opsnz);
-  ops = warp_sum(ops);
-  api = warp_sum(api);
-  apic = warp_sum(apic);
-  gpuc = warp_sum(gpuc);
+  } else if (A.cur_p >= 0) {
+    atomic_min_i64(&lo_out[A.cur_p], A.lo);
+    atomic_max_i64(&hi_out[A.cur_p], A.hi);
+    if (A.cur_pops) atomicAdd(&pid_ops[A.cur_p], A.cur_pops);
+  }
+  {  // running per-group op count
+    const int gk = A.cur_gops ? A.cur_g : -1;
+    const int g0 = __shfl_sync(full, gk, 0);
+    if (__all_sync(full, gk == g0)) {
+      const long long go = warp_sum(A.cur_gops);
+      if (lane == 0 && g0 >= 0 && go) atomicAdd(&group_ops[g0], (int)go);
+    } else if (gk >= 0) {
+      atomicAdd(&group_ops[gk], A.cur_gops);
+    }
+  }
+  // packed counters: warp sums, then lane q unpacks counter q into shared memory
+  const unsigned long long w0 = warp_sum_u64(A.cat_all0), w1 = warp_sum_u64(A.cat_all1),
+                           w2 = warp_sum_u64(A.cat_nz0), w3 = warp_sum_u64(A.cat_nz1), w4 = warp_sum_u64(A.cnt0),
+                           w5 = warp_sum_u64(A.cnt1);
+  long long bad_api = A.bad_api;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    long long b2 = __shfl_xor_sync(full, bad_api, o);
+    const long long b2 = __shfl_xor_sync(full, bad_api, o);
     bad_api = b2 < bad_api ? b2 : bad_api;
   }
-  if ((threadIdx.x & 31) == 0) {
-    if (bad) atomicAdd((unsigned long long*)&st->n_bad, (unsigned long long)bad);
-    if (nz) atomicAdd((unsigned long long*)&st->n_nonzero, (unsigned long long)nz);
-    if (opsnz) atomicAdd((unsigned long long*)&st->n_ops_nz, (unsigned long long)opsnz);
-    if (ops) atomicAdd((unsigned long long*)&st->n_ops, (unsigned long long)ops);
-    if (api) atomicAdd((unsigned long long*)&st->n_api, (unsigned long long)api);
-    if (apic) atomicAdd((unsigned long long*)&st->n_api_corr, (unsigned long long)apic);
-    if (gpuc) atomicAdd((unsigned long long*)&st->n_gpu_corr, (unsigned long long)gpuc);
-    if (bad_api != INT64_MAX) atomicMin(&st->bad_api, bad_api);
+  __syncthreads();  // s_cnt initialised
+  if (lane < 19) {
+    // counter layout: 0-5 cat_all, 6-11 cat_nz, 12-15 cnt0 lanes, 16-18 cnt1 lanes
+    const unsigned long long word = lane < 4 ? w0 : lane < 6 ? w1 : lane < 10 ? w2 : lane < 12 ? w3 : lane < 16 ? w4 : w5;
+    const int sub = lane < 6 ? (lane & 3) : lane < 12 ? ((lane - 6) & 3) : lane < 16 ? lane - 12 : lane - 16;
+    const unsigned long long x = (word >> (16 * sub)) & 0xFFFFull;
+    if (x) atomicAdd(&s_cnt[lane], x);
+  }
+  if (lane == 0 && bad_api != INT64_MAX) atomicMin(&s_bad_api, bad_api);
+  __syncthreads();
+  if (threadIdx.x < 19) {
+    const unsigned long long x = s_cnt[threadIdx.x];
+    if (x) {
+      const int q = threadIdx.x;
+      long long* f = q < 6 ? &st->cat_all[q] : q < 12 ? &st->cat_nz[q - 6] : q == 12 ? &st->n_bad
+                   : q == 13 ? &st->n_nonzero : q == 14 ? &st->n_ops_nz : q == 15 ? &st->n_ops
+                   : q == 16 ? &st->n_api : q == 17 ? &st->n_api_corr : &st->n_gpu_corr;
+      unsigned long long* dst = (unsigned long long*)f;
+      atomicAdd(dst, x);
+    }
+  } else if (threadIdx.x == 32 && s_bad_api != INT64_MAX) {
+    atomicMin(&st->bad_api, s_bad_api);
   }
 }
 
@@ -290,8 +358,14 @@ int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool che
     const uint8_t* hasint = (check_api && prof) ? prof->has_internal : nullptr;
     int check = (check_api && prof && ev->n_names > 0 && hasint) ? 1 : 0;
     if (check_api && prof && !hasint) check = 0;
-    XS_LAUNCH(ctx, k_pass1, grid_for(n, XS_BLOCK * P1_ITEMS), XS_BLOCK, 0, s, v, n, ev->pid_has_meta, hasint,
-              check, st, lo, hi, pid_ops, group_ops);
+    const bool vec = ((uintptr_t)v.start % 16 == 0) && ((uintptr_t)v.dur % 16 == 0) &&
+                     ((uintptr_t)ev->pid % 16 == 0) && ((uintptr_t)ev->cat % 4 == 0);
+    if (vec)
+      XS_LAUNCH(ctx, k_pass1<true>, grid_for(n, XS_BLOCK * P1_ITEMS), XS_BLOCK, 0, s, v, n, ev->pid_has_meta, hasint,
+                check, st, lo, hi, pid_ops, group_ops);
+    else
+      XS_LAUNCH(ctx, k_pass1<false>, grid_for(n, XS_BLOCK * P1_ITEMS), XS_BLOCK, 0, s, v, n, ev->pid_has_meta,
+                hasint, check, st, lo, hi, pid_ops, group_ops);
   }
   XS_LAUNCH(ctx, k_pid_finish, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, np, ev->group_pid, group_ops, ng,
             pid_group0, st);
