@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--iterations", type=int, default=ITERATIONS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
+                    help="BASELINE.json config: 2 (default, the metric's workload), 3 (100M events, 100 pids, "
+                         "nested), 5 (adversarial 10M)")
+    ap.add_argument("--events", type=int, default=0, help="events per GPU for --config 3/5 (default 100M / 10M)")
     return ap.parse_args()
 
 
@@ -55,19 +59,52 @@ def dist_env():
     return rank, world, local
 
 
-def make_trace(iterations: int, rank: int):
+WORKLOADS = {
+    2: "config2: DDPG-style instrumented trace, ~1M events/GPU, 3 operation scopes, integer calibrated profile; "
+       "step = correct_trace + compute_overlap(corrected)",
+    3: "config3: multi-process multi-phase DDPG-style instrumented trace, 1M events per pid, outer op around 3 "
+       "phase ops (depth 2), ops on 2 tids, 6 categories, integer calibrated profile; step = correct_trace + "
+       "compute_overlap(corrected)",
+    5: "config5: adversarial trace, 64 Zipf(1.5)-sized pids, recursive ops to depth 64, 256 GPU streams of long "
+       "concurrent kernels, 1% zero-duration, 10% duplicate correlation ids, fractional calibrated profile; "
+       "step = correct_trace + compute_overlap(corrected)",
+}
+
+
+def make_workload(args, rank: int):
+    """(instrumented trace, uninstrumented twin or None, profile) for this rank's shard."""
+    from paper_2102_04285_b200 import synth
+    workers = os.cpu_count() or 1
+    if args.config == 2:
+        un, inst = make_trace(args.iterations, rank, both=True)
+        return inst, un, synth.exact_profile()
+    if args.config == 3:
+        ev = args.events or 100_000_000
+        procs = max(1, ev // 1_000_000)
+        un, inst = synth.config3_trace(processes=procs, events_per_pid=ev // procs, both=True, workers=workers,
+                                       first_pid=rank * procs + 1)
+        return inst, un, synth.exact_profile()
+    ev = args.events or 10_000_000
+    return synth.adversarial_trace(ev, pids=64, seed=1234 + rank, workers=workers), None, \
+        synth.adversarial_profile()
+
+
+def make_trace(iterations: int, rank: int, both: bool = False):
     """Rank r analyses process r+1 (distinct seed): a weak-scaling shard."""
     from paper_2102_04285_b200 import synth
     from paper_2102_04285_b200.columnar import ColumnarTrace
     from paper_2102_04285_b200.model import ProcessMeta
 
-    ct = synth.ddpg_trace(iterations, processes=1, seed=1234 + rank)
+    out = synth.ddpg_trace(iterations, processes=1, seed=1234 + rank, both=both)
     if rank:
-        ct = ColumnarTrace(ct.clock_domain, ct.start, ct.dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr,
-                           ct.pids + rank, ct.group_pid, ct.group_tid, ct.names,
-                           tuple(ProcessMeta(m.pid + rank, m.name, m.parent, m.fork_ns, m.join_ns)
-                                 for m in ct.processes), ct.pid_has_meta)
-    return ct
+        out = tuple(ColumnarTrace(ct.clock_domain, ct.start, ct.dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr,
+                                  ct.has_corr, ct.pids + rank, ct.group_pid, ct.group_tid, ct.names,
+                                  tuple(ProcessMeta(m.pid + rank, m.name, m.parent, m.fork_ns, m.join_ns)
+                                        for m in ct.processes), ct.pid_has_meta)
+                    for ct in (out if both else (out,)))
+        if not both:
+            out = out[0]
+    return out
 
 
 class ClockSampler:
@@ -166,13 +203,52 @@ def traffic_from_profiles(stage: str):
     return d.get(stage)
 
 
-def cpu_baseline_port(ct, profile, seconds: float):
-    """The C restatement (oracle/) of correct_trace + compute_overlap(corrected):
-    the reference algorithm, compiled, one thread (the trace is one pid)."""
+def pid_sample(ct, budget_events: int):
+    """Sub-trace of the smallest pids whose events total <= budget (per-pid
+    results are independent: overlap.py:126, correction.py:132)."""
+    counts = np.bincount(ct.pid, minlength=ct.n_pids)
+    keep, tot = [], 0
+    for p in np.argsort(counts, kind="stable"):
+        if counts[p] == 0:
+            continue
+        if tot + counts[p] > budget_events and keep:
+            break
+        keep.append(int(p))
+        tot += int(counts[p])
+    return (ct.select_pids(keep) if len(keep) < ct.n_pids else ct), keep
+
+
+def oracle_sample_check(ct, profile, out_s, out_d, bd, budget=1_500_000):
+    """Config 5: the measured step's corrected columns and cells vs the oracle
+    on a bounded sample of pids."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
 
     from paper_2102_04285_b200.columnar import ColumnarTrace
+    sub, keep = pid_sample(ct, budget)
+    rows = np.isin(ct.pid, np.asarray(keep, np.int32))
+    s, d, _, _ = oracle.correct(sub, profile)
+    ok = bool(np.array_equal(out_s[rows], s) and np.array_equal(out_d[rows], d))
+    cor = ColumnarTrace(sub.clock_domain, s, d, sub.pid, sub.tid, sub.cat, sub.name, sub.corr, sub.has_corr,
+                        sub.pids, sub.group_pid, sub.group_tid, sub.names, sub.processes, sub.pid_has_meta)
+    cells, spans, untracked = oracle.overlap(cor, 0)
+    pv = {int(ct.pids[p]) for p in keep}
+    ours = {(k.pid, k.path, frozenset(int(c) for c in k.categories)): v for k, v in bd.cells.items() if k.pid in pv}
+    ok = ok and ours == cells and {p: bd.spans[p] for p in pv} == spans and \
+        {p: bd.untracked[p] for p in pv} == untracked
+    return ok, f"{len(keep)} of {ct.n_pids} pids, {sub.n} events: corrected columns + cells/spans/untracked"
+
+
+def cpu_baseline_port(ct, profile, seconds: float):
+    """The C restatement (oracle/) of correct_trace + compute_overlap(corrected):
+    the reference algorithm, compiled, one thread, on a bounded sample of pids
+    (the whole trace at config 2)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    from paper_2102_04285_b200.columnar import ColumnarTrace
+    full_n = ct.n
+    ct, _ = pid_sample(ct, 2_000_000)
 
     t0 = time.perf_counter()
     runs = 0
@@ -185,8 +261,9 @@ def cpu_baseline_port(ct, profile, seconds: float):
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
+    what = "full" if ct.n == full_n else f"pid sample of the {full_n}-event"
     return {"value": runs * ct.n / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{runs} x full {ct.n}-event trace, oracle/xs_oracle.c correct+overlap, {dt:.1f}s"}
+            "sample": f"{runs} x {ct.n}-event {what} trace, oracle/xs_oracle.c correct+overlap, {dt:.1f}s"}
 
 
 # ---------------------------------------------------------------------------
@@ -205,8 +282,7 @@ def run_ours(args):
     from paper_2102_04285_b200.distributed import merge_breakdown_raw
     from paper_2102_04285_b200.overlap import decode_breakdown
 
-    ct = make_trace(args.iterations, rank)
-    profile = synth.exact_profile()
+    ct, un, profile = make_workload(args, rank)
     scaled = profile.scaled(ct.names)
     eng = _engine.get(local)
     dt_dev = _engine.DeviceTrace(ct, local)
@@ -300,8 +376,13 @@ def run_ours(args):
         e2e_step = float(t.item())
 
     # correctness of the measured step: closure against the uninstrumented twin
-    un = synth.ddpg_trace(args.iterations, processes=1, seed=1234 + rank, both=True)[0]
-    closure_ok = bool(np.array_equal(out_s.numpy(), un.start) and np.array_equal(out_d.numpy(), un.dur))
+    # (configs 2/3), or the oracle on a bounded sample of pids (config 5)
+    check = {}
+    if un is not None:
+        check["closure_exact"] = bool(np.array_equal(out_s.numpy(), un.start) and np.array_equal(out_d.numpy(), un.dur))
+    else:
+        check["oracle_sample_exact"], check["oracle_sample"] = oracle_sample_check(ct, profile, out_s.numpy(),
+                                                                                   out_d.numpy(), bd)
 
     # roofline for the dominant stage
     peak, peak_kind = load_peaks()
@@ -341,15 +422,16 @@ def run_ours(args):
         cpu = cpu_baseline_port(ct, profile, args.cpu_seconds)
         cpu["cores_available"] = os.cpu_count()
 
+    in_mb = h2d / 1e6
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": "config2: DDPG-style instrumented trace, ~1M events/GPU, 3 operation scopes, "
-                                   "integer calibrated profile; step = correct_trace + compute_overlap(corrected)",
-                       "events_per_gpu": n, "events_total": total_events, "attribution": "instant",
-                       "l2": "flushed (256 MB write) between timed steps; inputs 37 MB/GPU",
+            "config": {"workload": WORKLOADS[args.config],
+                       "events_per_gpu": n, "pids_per_gpu": ct.n_pids, "events_total": total_events,
+                       "attribution": "instant",
+                       "l2": f"flushed (256 MB write) between timed steps; inputs {in_mb:.0f} MB/GPU",
                        "parallelism": f"pid-sharded x{world}" + (", NCCL all-reduce histogram merge" if world > 1
                                                                    else "")},
             "e2e": {"value": round(total_events / (e2e_step / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_step, 3),
@@ -357,7 +439,7 @@ def run_ours(args):
                     "path": "host pinned columns -> H2D -> xs_analyze -> D2H corrected trace + cells"},
             "gpu_launches": int(launches / args.steps),
             "roofline": roof, "pipeline_roofline": pipeline, "stages_ms": stages,
-            "cpu_baseline": cpu, "clocks": clocks.summary(), "closure_exact": closure_ok,
+            "cpu_baseline": cpu, "clocks": clocks.summary(), **check,
         }
         print(json.dumps(line))
     if world > 1:
@@ -366,73 +448,89 @@ def run_ours(args):
 
 
 # ---------------------------------------------------------------------------
+def _ref_sample(config: int, worker: int, iterations: int, events: int):
+    """Worker w's bounded sample of the bench workload (distinct seeds/pids)."""
+    from paper_2102_04285_b200 import synth
+    if config == 2:  # 1/10 of the 1M-event trace
+        return make_trace(max(1, iterations // 10), worker), synth.exact_profile(), "1/10 of the config-2 trace"
+    if config == 3:  # one 100k-event pid of config 3
+        return (synth.config3_trace(processes=1, events_per_pid=100_000, first_pid=worker + 1),
+                synth.exact_profile(), "one 100k-event config-3 pid")
+    n = max(64 * 32, (events or 10_000_000) // 100)
+    return (synth.adversarial_trace(n, pids=64, seed=1234 + worker), synth.adversarial_profile(),
+            f"1/100 of the config-5 trace ({n} events, 64 pids)")
+
+
+def _ref_worker(args):
+    """One host core: build the reference's own Trace of Event objects
+    (untimed), then time correct_trace + compute_overlap(corrected) through
+    the unmodified reference package (oracle/_ref, native Cython sweep)."""
+    config, worker, iterations, events, warmup, steps, barrier = args
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    sys.path.insert(0, ref)
+    from xstrace import model as RM
+    from xstrace.calibration import CalibrationProfile as RP
+    from xstrace.correction import correct_trace as ref_correct
+    from xstrace.overlap import HAVE_NATIVE_SWEEP, compute_overlap as ref_overlap
+
+    ct, p, what = _ref_sample(config, worker, iterations, events)
+    cats = [RM.Category(c) for c in range(6)]
+    names = ct.names
+    events_ = [RM.Event(int(ct.pids[pp]), int(ct.group_tid[g]), cats[c], names[nm], s, d, k if h else None)
+               for pp, g, c, nm, s, d, k, h in zip(ct.pid.tolist(), ct.tid.tolist(), ct.cat.tolist(),
+                                                   ct.name.tolist(), ct.start.tolist(), ct.dur.tolist(),
+                                                   ct.corr.tolist(), ct.has_corr.tolist())]
+    trace = RM.Trace(ct.clock_domain, events_, [RM.ProcessMeta(m.pid, m.name, m.parent, m.fork_ns, m.join_ns)
+                                                for m in ct.processes])
+    prof = RP(p.annotation_ns, p.transition_ns, p.api_interception_ns, dict(p.api_internal_ns))
+
+    def step():
+        out, _ = ref_correct(trace, prof)
+        ref_overlap(out)
+
+    for _ in range(warmup):
+        step()
+    barrier.wait()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    t1 = time.perf_counter()
+    return ct.n * steps, t0, t1, what, HAVE_NATIVE_SWEEP, ct.n
+
+
 def run_reference(args):
+    """The reference's own CPU implementation of the path on all host cores:
+    one worker process per core, each analysing its own bounded sample of the
+    workload through the unmodified reference package; throughput = all
+    events / wall time of the common timed phase."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     ref = os.path.join(ROOT, "oracle", "_ref")
-    sample_iters = max(1, args.iterations // 10)
-    if os.path.isdir(os.path.join(ref, "xstrace")):
-        sys.path.insert(0, ref)
-        from xstrace.correction import correct_trace as ref_correct
-        from xstrace.overlap import HAVE_NATIVE_SWEEP, compute_overlap as ref_overlap
-        from xstrace import model as RM
-        from xstrace.calibration import CalibrationProfile as RP
-        from paper_2102_04285_b200 import synth
-
-        ct = make_trace(sample_iters, 0)
-        cats = [RM.Category(c) for c in range(6)]
-        names = ct.names
-        events = [RM.Event(int(ct.pids[p]), int(ct.group_tid[g]), cats[c], names[nm], s, d, k if h else None)
-                  for p, g, c, nm, s, d, k, h in zip(ct.pid.tolist(), ct.tid.tolist(), ct.cat.tolist(),
-                                                     ct.name.tolist(), ct.start.tolist(), ct.dur.tolist(),
-                                                     ct.corr.tolist(), ct.has_corr.tolist())]
-        trace = RM.Trace(ct.clock_domain, events, [RM.ProcessMeta(m.pid, m.name, m.parent, m.fork_ns, m.join_ns)
-                                                    for m in ct.processes])
-        p = synth.exact_profile()
-        prof = RP(p.annotation_ns, p.transition_ns, p.api_interception_ns, dict(p.api_internal_ns))
-
-        def step():
-            out, _ = ref_correct(trace, prof)
-            ref_overlap(out)
-
-        kind, cores = "reference", 1
-        sample = (f"{ct.n}-event DDPG trace ({sample_iters} iterations, 1/10 of the 1M workload), "
-                  f"reference xstrace correct_trace + compute_overlap, native sweep={HAVE_NATIVE_SWEEP}")
-        n_ev = ct.n
-    else:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import oracle
-        from paper_2102_04285_b200 import synth
-
-        ct = make_trace(args.iterations, 0)
-        p = synth.exact_profile()
-
-        from paper_2102_04285_b200.columnar import ColumnarTrace
-
-        def step():
-            s, d, _, _ = oracle.correct(ct, p)
-            oracle.overlap(ColumnarTrace(ct.clock_domain, s, d, ct.pid, ct.tid, ct.cat, ct.name, ct.corr,
-                                         ct.has_corr, ct.pids, ct.group_pid, ct.group_tid, ct.names,
-                                         ct.processes, ct.pid_has_meta), 0)
-
-        kind, cores, n_ev = "port", 1, ct.n
-        sample = f"{ct.n}-event trace, oracle C port (reference not built here)"
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = time.perf_counter() - t0
-    value = n_ev * args.steps / dt
+    if not os.path.isdir(os.path.join(ref, "xstrace")):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (run oracle/build_ref.sh)"}))
+        return
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    mgr = ctx.Manager()
+    barrier = mgr.Barrier(cores)
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_ref_worker, [(args.config, w, args.iterations, args.events, max(args.warmup, 1), args.steps,
+                                      barrier) for w in range(cores)], chunksize=1)
+    total = sum(r[0] for r in res)
+    wall = max(r[2] for r in res) - min(r[1] for r in res)
+    value = total / wall
+    per_step_events = sum(r[5] for r in res)
+    sample = (f"{cores} worker processes x {res[0][3]} ({res[0][5]} events each), reference xstrace "
+              f"correct_trace + compute_overlap, native sweep={res[0][4]}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": "config2: DDPG-style instrumented trace, calibrated integer profile; "
-                               "step = correct_trace + compute_overlap(corrected)", "events_per_step": n_ev},
-        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
-                         "cores_available": os.cpu_count()},
+        "config": {"workload": WORKLOADS[args.config], "events_per_step": per_step_events},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 

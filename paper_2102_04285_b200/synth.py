@@ -181,50 +181,250 @@ def instrument(tl: PidTimeline, start: np.ndarray, dur: np.ndarray, cat: np.ndar
     return s2, np.where(cat == GPU, dur, e2 - s2)
 
 
+def _pid_columns(tl: PidTimeline, name_rank: dict) -> tuple:
+    """Concatenate one pid's blocks: (start, dur, cat, tid value, global name rank, corr, has_corr)."""
+    bl = tl.blocks
+    start = np.concatenate([b.start for b in bl])
+    end = np.concatenate([b.end for b in bl])
+    cat = np.concatenate([np.full(b.start.shape[0], b.cat, np.uint8) for b in bl])
+    tid = np.concatenate([np.full(b.start.shape[0], b.tid, np.int64) for b in bl])
+    name = np.concatenate([np.asarray([name_rank[x] for x in b.names], np.int32)[b.name_sel] for b in bl])
+    corr = np.concatenate([b.corr if b.corr is not None else np.zeros(b.start.shape[0], np.int64) for b in bl])
+    hasc = np.concatenate([b.has_corr if b.has_corr is not None else np.zeros(b.start.shape[0], np.uint8)
+                           for b in bl])
+    return start, end - start, cat, tid, name, corr, hasc
+
+
+def ddpg_names(outer_op: str = None, phases=DDPG_PHASES) -> list:
+    names = {"kernel", "script", *API_NAMES}
+    for op, level, _, _ in phases:
+        names.add(op)
+        names.add(f"{op}_{'backend' if level == BACKEND else 'sim'}")
+    if outer_op:
+        names.add(outer_op)
+    return sorted(names)
+
+
+def assemble(parts: list, names: list, metas: list, clock_domain: int = 1) -> ColumnarTrace:
+    """Per-pid column tuples (pid value, start, dur, cat, tid value, name rank,
+    corr, has_corr), pids ascending, rows already in the wanted order ->
+    ColumnarTrace, interning (pid, tid) groups per pid (no global sort)."""
+    pids = np.array(sorted({p[0] for p in parts} | {m.pid for m in metas}), np.int64)
+    pidx = {int(v): i for i, v in enumerate(pids.tolist())}
+    g_pid, g_tid, tid_cols, pid_cols = [], [], [], []
+    for p in sorted(parts, key=lambda x: x[0]):
+        tids = p[4]
+        uniq, inv = np.unique(tids, return_inverse=True)
+        base = len(g_pid)
+        g_pid.extend([pidx[p[0]]] * len(uniq))
+        g_tid.extend(uniq.tolist())
+        tid_cols.append((inv.reshape(-1) + base).astype(np.int32))
+        pid_cols.append(np.full(tids.shape[0], pidx[p[0]], np.int32))
+    parts = sorted(parts, key=lambda x: x[0])
+
+    def cat_(k, dt):
+        return np.ascontiguousarray(np.concatenate([q[k] for q in parts]) if parts else np.zeros(0, dt), dtype=dt)
+
+    return ColumnarTrace(clock_domain, cat_(1, np.int64), cat_(2, np.int64),
+                         np.concatenate(pid_cols) if parts else np.zeros(0, np.int32),
+                         np.concatenate(tid_cols) if parts else np.zeros(0, np.int32),
+                         cat_(3, np.uint8), cat_(5, np.int32), cat_(6, np.int64), cat_(7, np.uint8), pids,
+                         np.array(g_pid, np.int32), np.array(g_tid, np.int64), list(names), tuple(metas))
+
+
+def _ddpg_pid(args):
+    seed, pid, iterations, outer_op, second_tid_ops, processes, want = args
+    names = ddpg_names(outer_op)
+    rank = {n: i for i, n in enumerate(names)}
+    tl = build_pid(np.random.default_rng([seed, pid]), iterations, outer_op=outer_op, second_tid_ops=second_tid_ops)
+    start, dur, cat, tid, name, corr, hasc = _pid_columns(tl, rank)
+    order = np.lexsort((dur, start))  # one row order for both twins
+    out = {}
+    for inst in want:
+        s, d = instrument(tl, start, dur, cat) if inst else (start, dur)
+        lo, hi = (int(s.min()), int((s + d).max())) if s.size else (0, 0)
+        if pid == 1 or processes == 1:
+            meta = ProcessMeta(pid, "ddpg_root" if processes > 1 else "ddpg")
+        else:
+            meta = ProcessMeta(pid, f"ddpg_worker_{pid - 2}", parent=1, fork_ns=lo, join_ns=hi)
+        out[inst] = ((pid, s[order], d[order], cat[order], tid[order], name[order], corr[order], hasc[order]), meta)
+    return out
+
+
+def _map(fn, jobs, workers: int):
+    if workers and workers > 1 and len(jobs) > 1:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(min(workers, len(jobs))) as pool:
+            return pool.map(fn, jobs, chunksize=1)
+    return [fn(j) for j in jobs]
+
+
 def ddpg_trace(iterations: int, processes: int = 1, seed: int = 1234, outer_op: str = None,
-               second_tid_ops: bool = False, both: bool = False):
+               second_tid_ops: bool = False, both: bool = False, workers: int = 0, first_pid: int = 1):
     """DDPG-style trace (configs 1-2: iterations=27027 -> ~1M events).
 
     Returns the instrumented ColumnarTrace, or (uninstrumented, instrumented)
     when ``both``.  Rows are ordered by (pid, start, dur) like read_trace.
+    ``workers`` > 1 builds the pids in a process pool (configs 3-4).
     """
-    per = {False: [], True: []}
-    metas = {False: [], True: []}
-    names_all = set()
-    for pid in range(1, processes + 1):
-        tl = build_pid(np.random.default_rng([seed, pid]), iterations, outer_op=outer_op,
-                       second_tid_ops=second_tid_ops)
-        start = np.concatenate([b.start for b in tl.blocks])
-        end = np.concatenate([b.end for b in tl.blocks])
-        dur = end - start
-        cat = np.concatenate([np.full(b.start.shape[0], b.cat, np.uint8) for b in tl.blocks])
-        tid = np.concatenate([np.full(b.start.shape[0], b.tid, np.int64) for b in tl.blocks])
-        name_s = np.concatenate([np.asarray(b.names, dtype=object)[b.name_sel] for b in tl.blocks])
-        corr = np.concatenate([b.corr if b.corr is not None else np.zeros(b.start.shape[0], np.int64)
-                               for b in tl.blocks])
-        hasc = np.concatenate([b.has_corr if b.has_corr is not None else np.zeros(b.start.shape[0], np.uint8)
-                               for b in tl.blocks])
-        for b in tl.blocks:
-            names_all.update(b.names)
-        order = np.lexsort((dur, start))  # one row order for both twins
-        for inst in (False, True):
-            s, d = instrument(tl, start, dur, cat) if inst else (start, dur)
-            per[inst].append((pid, s[order], d[order], cat[order], tid[order], name_s[order], corr[order],
-                              hasc[order]))
-            lo, hi = (int(s.min()), int((s + d).max())) if s.size else (0, 0)
-            if pid == 1 or processes == 1:
-                metas[inst].append(ProcessMeta(pid, "ddpg_root" if processes > 1 else "ddpg"))
-            else:
-                metas[inst].append(ProcessMeta(pid, f"ddpg_worker_{pid - 2}", parent=1, fork_ns=lo, join_ns=hi))
-    names = sorted(names_all)
-    rank = {n: i for i, n in enumerate(names)}
-    out = []
-    for inst in (False, True):
-        parts = per[inst]
-        cols = [np.concatenate([p[k] for p in parts]) for k in range(1, 8)]
-        pidv = np.concatenate([np.full(p[1].shape[0], p[0], np.int64) for p in parts])
-        uniq, inv = np.unique(cols[4], return_inverse=True)
-        name = np.array([rank[x] for x in uniq.tolist()], np.int32)[inv.reshape(-1)]
-        out.append(ColumnarTrace.from_arrays(1, cols[0], cols[1], pidv, cols[3], cols[2], name, names, cols[5],
-                                             cols[6], tuple(metas[inst])))
-    return (out[0], out[1]) if both else out[1]
+    want = (False, True) if both else (True,)
+    pids = range(first_pid, first_pid + processes)
+    jobs = [(seed, pid, iterations, outer_op, second_tid_ops, processes, want) for pid in pids]
+    res = _map(_ddpg_pid, jobs, workers)
+    names = ddpg_names(outer_op)
+    out = [assemble([r[inst][0] for r in res], names, [r[inst][1] for r in res]) for inst in want]
+    return (out[0], out[1]) if both else out[0]
+
+
+# ---------------------------------------------------------------------------
+# Config 3: multi-process, multi-phase, nested (SURVEY.md 8d)
+
+CONFIG3_ITERS_PER_1M = 24510  # ~1.0M events per pid with outer_op + second_tid_ops
+
+
+def config3_trace(processes: int = 100, events_per_pid: int = 1_000_000, seed: int = 1234, both: bool = False,
+                  workers: int = 0, first_pid: int = 1):
+    """Config 3: ``processes`` pids x ~``events_per_pid`` events, an outer
+    per-iteration op around the three phase ops (depth 2), every phase op
+    mirrored on a second tid (cross-tid path merge), all six categories."""
+    iters = max(1, round(events_per_pid * CONFIG3_ITERS_PER_1M / 1_000_000))
+    return ddpg_trace(iters, processes=processes, seed=seed, outer_op="iteration", second_tid_ops=True, both=both,
+                      workers=workers, first_pid=first_pid)
+
+
+# ---------------------------------------------------------------------------
+# Config 5: adversarial (SURVEY.md 8d)
+
+ADV_API_NAMES = ("launch", "memcpy", "sync")
+
+
+def adversarial_profile() -> CalibrationProfile:
+    """Fractional calibration for config 5 (exercises quantize_amounts' drift)."""
+    return CalibrationProfile(Fraction(12345, 7), Fraction(1000, 3), Fraction(3001, 2),
+                              {"launch": Fraction(5999, 2), "memcpy": Fraction(1000), "sync": Fraction(7, 3)})
+
+
+def _adv_pid(args):
+    """One adversarial process: recursive ops to ``depth`` on tid 0, shallow
+    ops on tids 1-3, heavily overlapping CPU events, ``streams`` GPU streams of
+    long concurrent kernels, 1% zero-duration events, 10% duplicate
+    correlation ids, timestamps on a coarse grid (many equal endpoints)."""
+    seed, pid, n, depth, streams = args
+    rng = np.random.default_rng([seed, pid, 5])
+    gran = 64
+    T = max(n, 16) * 2000
+    n_deep = max(1, int(0.03 * n))
+    n_sh = max(3, int(0.03 * n)) // 3 * 3
+    n_gpu = max(1, int(0.22 * n))
+    n_dup = n_gpu // 10
+    n_api = n_gpu + n_dup + n_gpu // 10
+    n_cpu = max(0, n - n_deep - n_sh - n_gpu - n_api - 1)
+    S, D, C, TID, NM, CO, HC = [], [], [], [], [], [], []
+    names = adversarial_names(depth)
+    rank = {x: i for i, x in enumerate(names)}
+
+    def add(s, d, cat, tid, name, corr=None, hasc=None):
+        k = s.shape[0]
+        S.append(s.astype(np.int64))
+        D.append(d.astype(np.int64))
+        C.append(np.full(k, cat, np.uint8))
+        TID.append(np.broadcast_to(np.asarray(tid, np.int64), (k,)).copy())
+        NM.append(np.broadcast_to(np.asarray(name, np.int32), (k,)).copy())
+        CO.append(np.zeros(k, np.int64) if corr is None else corr.astype(np.int64))
+        HC.append(np.zeros(k, np.uint8) if hasc is None else hasc.astype(np.uint8))
+
+    # deep recursive ops on tid 0: a reflecting random walk over the depth
+    t = np.sort(rng.integers(0, T, 2 * n_deep)) // gran * gran
+    coin = rng.random(2 * n_deep).tolist()
+    pick = rng.integers(0, 3, 2 * n_deep).tolist()
+    stack, ops_s, ops_e, ops_n = [], [], [], []
+    pushes = n_deep
+    tl = t.tolist()
+    for i in range(2 * n_deep):
+        d = len(stack)
+        push = pushes > 0 and (d == 0 or (d < depth and coin[i] < 0.5))
+        if push:
+            parent = stack[-1][1] if stack else -1
+            nm = parent if (parent >= 0 and pick[i] == 0 and coin[i] < 0.1) else rank[f"L{d % 6}_{pick[i]}"]
+            stack.append((tl[i], nm))
+            pushes -= 1
+        else:
+            s0, nm = stack.pop()
+            ops_s.append(s0)
+            ops_e.append(tl[i])
+            ops_n.append(nm)
+    ops_s, ops_e = np.array(ops_s, np.int64), np.array(ops_e, np.int64)
+    add(ops_s, ops_e - ops_s, OPERATION, 0, np.array(ops_n, np.int32))
+    # shallow ops on tids 1..3 (depth <= 2; some names shared with tid 0)
+    for tid in (1, 2, 3):
+        m = n_sh // 3
+        tt = np.sort(rng.integers(0, T, 2 * m)) // gran * gran
+        a, b = tt[0::2], tt[1::2]
+        nm = np.where(rng.random(m) < 0.3, rank["L0_0"], rank[f"sh{tid}"]).astype(np.int32)
+        add(a, b - a, OPERATION, tid, nm)
+        kid = rng.random(m) < 0.5
+        ca = (a + (b - a) // 4)[kid] // gran * gran
+        cb = np.maximum(ca, (b - (b - a) // 4)[kid] // gran * gran)
+        add(ca, cb - ca, OPERATION, tid, rank["inner"])
+    # ambient HIGH_LEVEL
+    add(np.array([0]), np.array([T + 4 * gran]), HIGH_LEVEL, 0, rank["script"])
+    # CPU events, heavy-tailed durations, all four CPU tids
+    cs = rng.integers(0, T, n_cpu) // gran * gran
+    cd = np.minimum((rng.pareto(1.5, n_cpu) + 1) * 2000, T / 10).astype(np.int64) // gran * gran
+    ccat = np.where(rng.random(n_cpu) < 0.5, BACKEND, SIMULATOR)
+    ctid = rng.integers(0, 4, n_cpu)
+    for cat in (BACKEND, SIMULATOR):
+        sel = ccat == cat
+        add(cs[sel], cd[sel], cat, ctid[sel], rank["backend_call" if cat == BACKEND else "sim_step"])
+    # ACCEL_API: ids 1..n_gpu, n_dup duplicate ids, some without correlation
+    as_ = rng.integers(0, T, n_api) // gran * gran
+    ad = rng.integers(1, 200, n_api) * gran
+    acorr = np.zeros(n_api, np.int64)
+    ahas = np.zeros(n_api, np.uint8)
+    acorr[:n_gpu] = np.arange(1, n_gpu + 1)
+    acorr[n_gpu:n_gpu + n_dup] = rng.integers(1, n_gpu + 1, n_dup)
+    ahas[:n_gpu + n_dup] = 1
+    aname = np.array([rank[x] for x in ADV_API_NAMES], np.int32)[rng.integers(0, 3, n_api)]
+    add(as_, ad, ACCEL_API, rng.integers(0, 4, n_api), aname, acorr, ahas)
+    # GPU: long concurrent kernels on `streams` streams
+    Dk = int(min(T // 2, 10_000 * T // max(n_gpu, 1)))
+    gs = rng.integers(0, T, n_gpu) // gran * gran
+    gd = (rng.random(n_gpu) * Dk + Dk // 2).astype(np.int64) // gran * gran
+    add(gs, gd, GPU, 1000 + rng.integers(0, streams, n_gpu), rank["kernel"], np.arange(1, n_gpu + 1),
+        np.ones(n_gpu, np.uint8))
+    start, dur, cat = np.concatenate(S), np.concatenate(D), np.concatenate(C)
+    tid, name, corr, hasc = np.concatenate(TID), np.concatenate(NM), np.concatenate(CO), np.concatenate(HC)
+    # 1% zero-duration resource events
+    res = np.nonzero(cat != OPERATION)[0]
+    zero = res[rng.random(res.shape[0]) < 0.01]
+    dur[zero] = 0
+    order = np.lexsort((dur, start))
+    lo, hi = int(start.min()), int((start + dur).max())
+    meta = ProcessMeta(pid, f"adv_{pid}", parent=None if pid == 1 else 1, fork_ns=None if pid == 1 else lo,
+                       join_ns=None if pid == 1 else hi)
+    return (pid, start[order], dur[order], cat[order], tid[order], name[order], corr[order], hasc[order]), meta
+
+
+def adversarial_names(depth: int = 64) -> list:
+    names = {"script", "backend_call", "sim_step", "kernel", "inner", *ADV_API_NAMES}
+    names.update(f"L{d}_{k}" for d in range(6) for k in range(3))
+    names.update(f"sh{t}" for t in (1, 2, 3))
+    return sorted(names)
+
+
+def zipf_sizes(total: int, pids: int, s: float) -> list:
+    w = np.arange(1, pids + 1, dtype=np.float64) ** -s
+    sizes = np.floor(w / w.sum() * total).astype(np.int64)
+    sizes[0] += total - int(sizes.sum())
+    return [max(32, int(x)) for x in sizes]
+
+
+def adversarial_trace(n_events: int = 10_000_000, pids: int = 64, seed: int = 1234, zipf: float = 1.5,
+                      depth: int = 64, streams: int = 256, workers: int = 0) -> ColumnarTrace:
+    """Config 5: ``n_events`` over ``pids`` processes with Zipf(``zipf``)
+    sizes (s=1.5 puts ~42% of the events in the largest pid at 64 pids),
+    recursive ops to ``depth``, ``streams`` concurrent GPU streams, 1%
+    zero-duration events, 10% duplicate correlation ids."""
+    sizes = zipf_sizes(n_events, pids, zipf)
+    res = _map(_adv_pid, [(seed, p + 1, sizes[p], depth, streams) for p in range(pids)], workers)
+    return assemble([r[0] for r in res], adversarial_names(depth), [r[1] for r in res])
