@@ -145,6 +145,23 @@ int xs_transition_sites(xs_ctx_t* ctx, const xs_events_t* ev, int pair_mask, int
                         xs_stream_t stream);
 int xs_transition_fetch(xs_ctx_t* ctx, int32_t* pair, int64_t* event, xs_stream_t stream);
 
+/* Union time of one category (0..5): metrics._union_ns
+ * (metrics.py:41-58).  per_pid = 0: one trace-wide union (busy_fraction,
+ * metrics.py:87-91) -> out_ns[0]; per_pid = 1: one union per pid, the
+ * gpu_busy_ns of procview.build_process_tree (procview.py:68-77) ->
+ * out_ns[n_pids].  *span_lo / *span_hi receive the trace span
+ * (metrics._trace_span, metrics.py:31-38; lo > hi when there are no events).
+ * All outputs are host memory. */
+int xs_union(xs_ctx_t* ctx, const xs_events_t* ev, int category, int per_pid, int64_t* out_ns, int64_t* span_lo,
+             int64_t* span_hi, xs_stream_t stream);
+/* sampled_utilization (metrics.py:61-84): *utilized = number of periods
+ * [lo + kP, lo + (k+1)P) intersecting a GPU event of nonzero duration;
+ * *n_intervals = number of disjoint GPU union intervals (fetch them, sorted,
+ * with xs_union_intervals_fetch for utilization_samples). */
+int xs_utilization(xs_ctx_t* ctx, const xs_events_t* ev, int64_t period_ns, int64_t* utilized, int64_t* n_intervals,
+                   int64_t* span_lo, int64_t* span_hi, xs_stream_t stream);
+int xs_union_intervals_fetch(xs_ctx_t* ctx, int64_t* out_lo, int64_t* out_hi, xs_stream_t stream);
+
 /* Number of kernel launches issued by the library since context creation
  * (instrumentation for the bench's gpu_launches field). */
 int64_t xs_launch_count(xs_ctx_t* ctx);

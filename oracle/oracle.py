@@ -213,3 +213,56 @@ def correct(ct, profile, queries=()):
         "corrected_total_ns": int(rep.corrected_total),
     }
     return out_s[: ct.n], out_d[: ct.n], report, q_out[: len(queries)].tolist()
+
+
+# ---------------------------------------------------------------------------
+# metrics (numpy restatement; test infrastructure only)
+
+def union_ns(ct, category: int, per_pid: bool = False):
+    """metrics._union_ns (metrics.py:41-58): sort (start, end) of the
+    category's nonzero events, merge overlapping/touching, sum lengths --
+    trace-wide, or {pid value: ns} per pid (procview.py:75)."""
+    sel = (ct.cat == category) & (ct.dur > 0)
+    groups = [(None, sel)] if not per_pid else [(int(ct.pids[p]), sel & (ct.pid == p)) for p in range(ct.n_pids)]
+    out = {}
+    for key, m in groups:
+        s = ct.start[m]
+        e = s + ct.dur[m]
+        order = np.lexsort((e, s))
+        total, cur_lo, cur_hi = 0, None, 0
+        for lo, hi in zip(s[order].tolist(), e[order].tolist()):
+            if cur_lo is None:
+                cur_lo, cur_hi = lo, hi
+            elif lo <= cur_hi:
+                cur_hi = max(cur_hi, hi)
+            else:
+                total += cur_hi - cur_lo
+                cur_lo, cur_hi = lo, hi
+        if cur_lo is not None:
+            total += cur_hi - cur_lo
+        out[key] = total
+    return out[None] if not per_pid else out
+
+
+def trace_span(ct):
+    if ct.n == 0:
+        return None
+    return int(ct.start.min()), int((ct.start + ct.dur).max())
+
+
+def utilization_flags(ct, period_ns: int):
+    """metrics.utilization_samples (metrics.py:61-79): per period, does it
+    intersect a nonzero-duration GPU event (the reference's two-pointer walk)."""
+    lo, hi = trace_span(ct)
+    sel = (ct.cat == 5) & (ct.dur > 0)
+    s = ct.start[sel]
+    e = s + ct.dur[sel]
+    order = np.lexsort((e, s))
+    gpu = list(zip(s[order].tolist(), e[order].tolist()))
+    flags, idx, start = [], 0, lo
+    while start < hi:
+        while idx < len(gpu) and gpu[idx][1] <= start:
+            idx += 1
+        flags.append(idx < len(gpu) and gpu[idx][0] < start + period_ns)
+        start += period_ns
+    return flags

@@ -28,6 +28,15 @@ from .model import (
     traces_equal,
     validate_trace,
 )
+from .metrics import (
+    ReportRow,
+    UtilizationSample,
+    busy_fraction,
+    sampled_utilization,
+    summarize,
+    utilization_samples,
+)
+from .procview import ProcessNode, ProcessTree, build_process_tree, render_tree, to_dot
 from .overlap import (
     Attribution,
     Breakdown,
@@ -44,6 +53,17 @@ from .overlap import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "ProcessNode",
+    "ProcessTree",
+    "ReportRow",
+    "UtilizationSample",
+    "build_process_tree",
+    "busy_fraction",
+    "render_tree",
+    "sampled_utilization",
+    "summarize",
+    "to_dot",
+    "utilization_samples",
     "Attribution",
     "Breakdown",
     "CalibrationProfile",

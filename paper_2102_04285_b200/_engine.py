@@ -262,6 +262,33 @@ class Engine:
         return pair[:k], event[:k]
 
 
+    def union(self, dt: DeviceTrace, category: int, per_pid: bool):
+        """(union ns per pid or [trace-wide], span lo, span hi)."""
+        ev = dt.struct()
+        out = np.zeros(max(dt.ct.n_pids if per_pid else 1, 1), np.int64)
+        lo, hi = C.c_int64(0), C.c_int64(0)
+        self.check(self.lib.xs_union(self.ctx, C.byref(ev), int(category), 1 if per_pid else 0, out.ctypes.data,
+                                     C.byref(lo), C.byref(hi), self.stream()), "xs_union")
+        return out, int(lo.value), int(hi.value)
+
+    def utilization(self, dt: DeviceTrace, period_ns: int, intervals: bool = False):
+        """(utilized periods, span lo, span hi[, union interval lo/hi arrays])."""
+        ev = dt.struct()
+        util, nint, lo, hi = C.c_int64(0), C.c_int64(0), C.c_int64(0), C.c_int64(0)
+        self.check(self.lib.xs_utilization(self.ctx, C.byref(ev), int(period_ns), C.byref(util), C.byref(nint),
+                                           C.byref(lo), C.byref(hi), self.stream()), "xs_utilization")
+        res = (int(util.value), int(lo.value), int(hi.value))
+        if not intervals:
+            return res
+        k = int(nint.value)
+        ilo = np.zeros(max(k, 1), np.int64)
+        ihi = np.zeros(max(k, 1), np.int64)
+        if k:
+            self.check(self.lib.xs_union_intervals_fetch(self.ctx, ilo.ctypes.data, ihi.ctypes.data, self.stream()),
+                       "xs_union_intervals_fetch")
+        return res + (ilo[:k], ihi[:k])
+
+
 class UncalibratedEvent(Exception):
     def __init__(self, index: int):
         self.index = index

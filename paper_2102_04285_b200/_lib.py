@@ -70,6 +70,11 @@ SIGNATURES = {
                              C.POINTER(C.c_int64), P]),
     "xs_transition_sites": (C.c_int, [P, C.POINTER(XsEvents), C.c_int, C.POINTER(C.c_int64), P]),
     "xs_transition_fetch": (C.c_int, [P, P, P, P]),
+    "xs_union": (C.c_int, [P, C.POINTER(XsEvents), C.c_int, C.c_int, P, C.POINTER(C.c_int64),
+                           C.POINTER(C.c_int64), P]),
+    "xs_utilization": (C.c_int, [P, C.POINTER(XsEvents), C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int64), C.POINTER(C.c_int64), P]),
+    "xs_union_intervals_fetch": (C.c_int, [P, P, P, P]),
     "xs_launch_count": (C.c_int64, [P]),
     "xs_profile_enable": (C.c_int, [P, C.c_int]),
     "xs_profile_read": (C.c_int, [P, P, P, C.c_int]),

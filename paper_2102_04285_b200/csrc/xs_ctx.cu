@@ -96,6 +96,11 @@ int run_validate(xs_ctx* ctx, const EventView& v, cudaStream_t s, long long* n_b
 
 int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s) {
   ctx->have_overlap = false;
+  struct LsdRestore {  // an LSD retry applies to this call only, whatever the exit
+    xs_ctx* c;
+    bool prev;
+    ~LsdRestore() { c->force_lsd = prev; }
+  } lsd_restore{ctx, ctx->force_lsd};
   // pass 1 (+ its sync: sizes and per-event rule violations)
   XS_TRY(stage_events(ctx, v, s, false, false, nullptr));
   for (int attempt = 0; attempt < 8; attempt++) {
@@ -109,25 +114,35 @@ int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s
     }));
     ctx->res_pids = v.ev.n_pids;
     XS_TRY(fetch_stats(ctx, s));
+    if (getenv("XS_DEBUG_STATS")) {  // developer diagnostics
+      const Stats& h = *ctx->h_stats;
+      fprintf(stderr, "xs_overlap attempt %d: bad %lld nz %lld ops_nz %lld api_corr %lld gpu_corr %lld span %lld "
+              "depth %lld full %lld multi %lld depth_ovf %lld lsd %lld nodes %lld\n", attempt, h.n_bad, h.n_nonzero,
+              h.n_ops_nz, h.n_api_corr, h.n_gpu_corr, h.max_span, h.max_depth, h.table_full, h.multi_op_pids,
+              h.depth_overflow, h.pad[3], h.pad[0]);
+    }
+    // a bucket overflowed a chunk: every verdict of this attempt (nesting
+    // included) came from an unsorted stream -- redo the call via the LSD sort
+    if (ctx->h_stats->pad[3] && !ctx->force_lsd) {
+      ctx->force_lsd = true;
+      // pass 1 found no violation (else stage_events returned): clear what
+      // the failed attempt's nesting check counted
+      XS_CUDA(cudaMemsetAsync(&((Stats*)ctx->ptr[W_STATS])->n_bad, 0, sizeof(long long), s));
+      continue;
+    }
     if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;
     if (ctx->h_stats->depth_overflow) {
       ctx->err = "merged multi-tid operation path deeper than the device limit";
       return XS_UNSUPPORTED;
     }
-    if (ctx->h_stats->pad[3]) {  // a bucket overflowed a chunk: redo this call via the LSD sort
-      ctx->force_lsd = true;
-      continue;
-    }
     if (!ctx->h_stats->table_full) {
       ctx->have_overlap = true;
-      ctx->force_lsd = false;
       ctx->n_cells = ctx->h_stats->pad[4];
       ctx->n_nodes = ctx->h_stats->pad[0] > 0 ? (int)ctx->h_stats->pad[0] : 1;  // trie nodes allocated
       return XS_OK;
     }
     ctx->trie_cap_log2 += 2;
   }
-  ctx->force_lsd = false;
   ctx->err = "path table could not be sized";
   return XS_NO_MEMORY;
 }

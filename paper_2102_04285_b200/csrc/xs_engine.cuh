@@ -47,7 +47,7 @@ enum Slot : int {
   W_TRIE_KEYS, W_TRIE_VALS, W_TRIE_PARENT, W_TRIE_NAME, W_TRIE_COUNT,
   W_GS_OFF, W_PK, W_PK_ALT, W_PIDPATH, W_OPBASE,
   W_MKEY, W_MKEY_ALT, W_MSCAN_DESC, W_MSCAN_FLAGS,
-  W_HIST, W_CELL_PID, W_CELL_NODE, W_CELL_MASK, W_CELL_NS, W_CELL_COUNT, W_TRACKED,
+  W_HIST, W_HIST_KEY, W_CELL_PID, W_CELL_NODE, W_CELL_MASK, W_CELL_NS, W_CELL_COUNT, W_TRACKED,
   W_CUB_TEMP,
   // correction
   W_TQ_KEY, W_TQ_VAL, W_TQ_KEY_ALT, W_TQ_VAL_ALT, W_TSCAN_DESC, W_TSCAN_FLAGS, W_THEAD, W_TSTAT,
@@ -66,6 +66,7 @@ enum Slot : int {
   W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
   W_CORR_TOTALS, W_NS_DEV, W_STATS_SAVE, W_PID_OPS_ALT, W_GROUP_OPS_ALT, W_PID_GROUP0_ALT,
   W_BS_COUNTS, W_BS_OFFS, W_BS_TAIL, W_BS_CHUNK, W_RMAP_IDX,
+  W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
   W_NUM_SLOTS
 };
 
@@ -201,6 +202,12 @@ struct xs_ctx {
   long long ws_generation = 0;  // bumped on every workspace reallocation
   cudaStream_t priv_stream = nullptr;
   cudaEvent_t join_in = nullptr, join_out = nullptr;
+  // last union (xs_union / xs_utilization), kept for xs_union_intervals_fetch
+  const uint64_t* un_keys = nullptr;
+  const int* un_depth = nullptr;
+  int64_t un_m = 0;
+  int un_tb = 0;
+  int64_t un_intervals = -1;
 };
 
 namespace xs {

@@ -80,8 +80,43 @@ constexpr int SW_ITEMS = 16;
 constexpr int SW_TILE = XS_BLOCK * SW_ITEMS;
 constexpr int HT = 1024;  // shared hash slots per block
 
+// The overlap histogram in global memory, keyed by
+// idx = ((pid * n_nodes + node) * 32 + mask) (mask 0 of node 0 = tracked).
+// Dense (key == nullptr): val[idx].  Hashed: an open-addressing table of
+// mask + 1 slots, used when the dense [pid][node][32] layout would be too
+// large (deep recursive operation scopes: hundreds of thousands of paths
+// that each occur in one pid).  Its capacity is >= 2x a proven bound on the
+// number of distinct cells, so probing terminates; `full` records the
+// impossible case instead of dropping time.
+struct GHist {
+  unsigned long long* val;
+  unsigned long long* key;
+  unsigned long long mask;
+  unsigned long long* full;
+  __device__ __forceinline__ void add(unsigned long long idx, unsigned long long v) const {
+    if (!key) {
+      atomicAdd(&val[idx], v);
+      return;
+    }
+    unsigned long long h = mix64(idx) & mask;
+    for (unsigned long long probe = 0; probe <= mask; probe++) {
+      unsigned long long k = ((volatile unsigned long long*)key)[h];
+      if (k == ~0ull) {
+        k = atomicCAS(&key[h], ~0ull, idx);
+        if (k == ~0ull) k = idx;
+      }
+      if (k == idx) {
+        atomicAdd(&val[h], v);
+        return;
+      }
+      h = (h + 1) & mask;
+    }
+    atomicAdd(full, 1ull);
+  }
+};
+
 __device__ __forceinline__ void hist_add(unsigned long long* s_key, unsigned long long* s_val,
-                                         unsigned long long* hist, unsigned long long idx, unsigned long long v) {
+                                         const GHist& hist, unsigned long long idx, unsigned long long v) {
   unsigned h = (unsigned)(mix64(idx) & (HT - 1));
 #pragma unroll 1
   for (int probe = 0; probe < 16; probe++) {
@@ -99,13 +134,13 @@ __device__ __forceinline__ void hist_add(unsigned long long* s_key, unsigned lon
     }
     h = (h + 1) & (HT - 1);
   }
-  atomicAdd(&hist[idx], v);
+  hist.add(idx, v);
 }
 
 __global__ void __launch_bounds__(XS_BLOCK) k_sweep(const uint64_t* __restrict__ keys, int64_t nvalid, int tb,
                                                     const int* __restrict__ pidpath,
                                                     const int64_t* __restrict__ opbase, int n_nodes,
-                                                    unsigned long long* __restrict__ hist, TileDesc<Cnt>* desc,
+                                                    GHist hist, TileDesc<Cnt>* desc,
                                                     int* flags, int* tile_ctr) {
   __shared__ unsigned long long s_key[HT];
   __shared__ unsigned long long s_val[HT];
@@ -187,18 +222,19 @@ __global__ void __launch_bounds__(XS_BLOCK) k_sweep(const uint64_t* __restrict__
   __syncthreads();
   for (int i = threadIdx.x; i < HT; i += XS_BLOCK) {
     unsigned long long key = s_key[i];
-    if (key != ~0ull) atomicAdd(&hist[key], s_val[i]);
+    if (key != ~0ull) hist.add(key, s_val[i]);
   }
 }
 
 // dense histogram -> (pid, node, mask, ns) list + tracked per pid
-__global__ void k_compact_cells(const unsigned long long* hist, int64_t total, int n_nodes, int* cell_pid,
+__global__ void k_compact_cells(GHist hist, int64_t total, int n_nodes, int* cell_pid,
                                 int* cell_node, int* cell_mask, int64_t* cell_ns, int64_t* tracked,
                                 unsigned long long* count) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  unsigned long long vv = hist[i];
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= total) return;
+  const unsigned long long vv = hist.val[slot];
   if (!vv) return;
+  const int64_t i = hist.key ? (int64_t)hist.key[slot] : slot;
   int mask = (int)(i & 31);
   int64_t row = i >> 5;
   int p = (int)(row / n_nodes);
@@ -292,7 +328,7 @@ struct FSAdd {
 
 constexpr int FX_ITEMS = 4;
 __global__ void __launch_bounds__(XS_BLOCK) k_fx_scan(const uint64_t* fx, int64_t nvalid, int tb, int nodeb,
-                                                      int n_nodes, unsigned long long* hist, uint64_t* pieces,
+                                                      int n_nodes, GHist hist, uint64_t* pieces,
                                                       unsigned long long* piece_count, TileDesc<FS>* desc, int* flags,
                                                       int* tile_ctr) {
   const int tile = next_tile(tile_ctr);
@@ -331,7 +367,7 @@ __global__ void __launch_bounds__(XS_BLOCK) k_fx_scan(const uint64_t* fx, int64_
       pieces[at] = pb | (t0 << 4) | 5u;
       pieces[at + 1] = pb | (t1 << 4) | 13u;
     } else {  // foreign: (fp, {GPU}) gets the union length
-      atomicAdd(&hist[((unsigned long long)p * n_nodes + path) * 32ull + 16ull], (unsigned long long)(t1 - t0));
+      hist.add(((unsigned long long)p * n_nodes + path) * 32ull + 16ull, (unsigned long long)(t1 - t0));
     }
   }
 }
@@ -440,7 +476,7 @@ struct CellTable {  // open addressing in shared memory, spill to global
   unsigned long long* key;
   unsigned* lo;
   unsigned* hi;
-  __device__ void add(unsigned long long idx, unsigned long long v, unsigned long long* hist) {
+  __device__ void add(unsigned long long idx, unsigned long long v, const GHist& hist) {
     unsigned h = (unsigned)(mix64(idx) & (HT - 1));
 #pragma unroll 1
     for (int probe = 0; probe < 16; probe++) {
@@ -455,7 +491,7 @@ struct CellTable {  // open addressing in shared memory, spill to global
       }
       h = (h + 1) & (HT - 1);
     }
-    atomicAdd(&hist[idx], v);
+    hist.add(idx, v);
   }
 };
 
@@ -466,7 +502,7 @@ struct CellCache {
   unsigned long long k[K];
   unsigned long long v[K];
   int n = 0;
-  __device__ void add(unsigned long long idx, unsigned long long len, CellTable& T, unsigned long long* hist) {
+  __device__ void add(unsigned long long idx, unsigned long long len, CellTable& T, const GHist& hist) {
 #pragma unroll
     for (int i = 0; i < K; i++)
       if (i < n && k[i] == idx) {
@@ -493,7 +529,7 @@ struct CellCache {
     v[K - 1] = len;
   }
   // all 32 lanes must call
-  __device__ void flush(CellTable& T, unsigned long long* hist) {
+  __device__ void flush(CellTable& T, const GHist& hist) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < K; i++) {
@@ -558,7 +594,7 @@ __device__ __forceinline__ SwState sw_identity() {
 __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
     const uint64_t* __restrict__ keys, int64_t total, const int64_t* __restrict__ chunk, int shift, int tb,
     const int* __restrict__ pidpath, const int64_t* __restrict__ opbase, int n_nodes,
-    unsigned long long* __restrict__ hist, TileDesc<SwState>* desc, int* flags, int* tile_ctr, Stats* st,
+    GHist hist, TileDesc<SwState>* desc, int* flags, int* tile_ctr, Stats* st,
     unsigned long long* ptrace) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
@@ -758,7 +794,7 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
   XS_STAMP(6);
   for (int i = t; i < HT; i += BK_THREADS) {
     const unsigned long long key = S.h_key[i];
-    if (key != ~0ull) atomicAdd(&hist[key], ((unsigned long long)S.h_hi[i] << 32) | S.h_lo[i]);
+    if (key != ~0ull) hist.add(key, ((unsigned long long)S.h_hi[i] << 32) | S.h_lo[i]);
   }
   __syncthreads();
   XS_STAMP(7);
@@ -773,7 +809,7 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
 // host driver for the bucketed endpoint sort + sweep
 static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, int tb, int corr_mode,
                             const uint64_t* extra, int64_t n_extra, int64_t nvalid, int key_bits, int n_nodes,
-                            unsigned long long* hist, cudaStream_t s) {
+                            const GHist& hist, cudaStream_t s) {
   OpsState& os = ctx->ops;
   Stats* st = (Stats*)ctx->ptr[W_STATS];
   const int64_t n = v.ev.n;
@@ -867,14 +903,28 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
     n_nodes = (int)H.pad[0];
   }
   if (n_nodes < 1) n_nodes = 1;
-  const int64_t hist_n = (int64_t)np * n_nodes * 32;
-  if (hist_n > ((int64_t)1 << 28)) {
-    ctx->err = "overlap histogram too large for the dense layout";
-    return XS_UNSUPPORTED;
+  // dense [pid][node][32] while it is small, else a hash table sized by a
+  // bound on the distinct cells: one per interval between consecutive
+  // endpoints (2n), one tracked entry per pid, and in CORRELATION mode one
+  // foreign cell per fixed-event endpoint interval
+  const int64_t dense_n = (int64_t)np * n_nodes * 32;
+  const int64_t cell_bound = 2 * n + np + 64 + (attribution == 1 ? 8 * (H.n_gpu_corr + 2 * os.m + np + 1) : 0);
+  GHist hist{nullptr, nullptr, 0, (unsigned long long*)&st->table_full};
+  int64_t hist_n = dense_n;
+  static const int dense_max_log2 = [] {  // XS_HIST_DENSE_MAX_LOG2: tests force the hashed layout
+    const char* e = getenv("XS_HIST_DENSE_MAX_LOG2");
+    return e ? atoi(e) : 24;
+  }();
+  if (dense_n > ((int64_t)1 << dense_max_log2) && (dense_n > 2 * cell_bound || dense_max_log2 < 24)) {
+    int lg = 10;
+    while (((int64_t)1 << lg) < 2 * cell_bound) lg++;
+    hist_n = (int64_t)1 << lg;
+    XS_TRY(ws(ctx, W_HIST_KEY, hist_n, s, &hist.key));
+    XS_CUDA(cudaMemsetAsync(hist.key, 0xFF, hist_n * 8, s));
+    hist.mask = (unsigned long long)hist_n - 1;
   }
-  unsigned long long* hist;
-  XS_TRY(ws(ctx, W_HIST, hist_n + 1, s, &hist));
-  XS_CUDA(cudaMemsetAsync(hist, 0, (hist_n + 1) * 8, s));
+  XS_TRY(ws(ctx, W_HIST, hist_n + 1, s, &hist.val));
+  XS_CUDA(cudaMemsetAsync(hist.val, 0, (hist_n + 1) * 8, s));
   const int64_t* lo = (const int64_t*)ctx->ptr[W_SPAN_LO];
 
   // CORRELATION pre-pass -> own pieces + foreign cells
