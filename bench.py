@@ -340,23 +340,19 @@ def run_ours(args):
     total_events = n * world
     value = total_events / (ms_per_step / 1e3)
 
-    # end-to-end through the public API with host buffers (pinned)
-    host = {k: torch.from_numpy(np.ascontiguousarray(getattr(ct, k))).pin_memory()
-            for k in ("start", "dur", "pid", "tid", "cat", "name", "corr", "has_corr", "group_pid", "pid_has_meta")}
+    # end-to-end through the public API (analyze_columnar) with host buffers:
+    # the user's columns in pinned memory, uploaded every step, the corrected
+    # columns read back into pinned buffers, the Breakdown decoded on the host
+    from paper_2102_04285_b200 import analyze_columnar
+    ct_host = ct.pinned()
     out_s = torch.empty(n, dtype=torch.int64).pin_memory()
     out_d = torch.empty(n, dtype=torch.int64).pin_memory()
-    h2d = sum(int(t.numel() * t.element_size()) for t in host.values())
+    h2d = sum(int(t.numel() * t.element_size()) for t in ct_host._pinned.values())
 
     def step_e2e():
-        tens = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
-        dtr = _engine.DeviceTrace.from_tensors(ct, tens, local)
-        raw = eng.correct(dtr, scaled, analyze_attribution=0)
-        ov = eng.fetch_overlap()
-        out_s.copy_(raw.start, non_blocking=True)
-        out_d.copy_(raw.dur, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
-        d2h = 16 * n + ov.cell_ns.nbytes * 3 + ov.node_parent.nbytes * 2 + 8 * 4 * ct.n_pids * 2
-        bd = decode_breakdown(ct, ov)
+        s_, d_, rep, bd = analyze_columnar(ct_host, profile, out=(out_s, out_d))
+        nc, nn, npp = eng.overlap_info()  # sizes of what analyze_columnar read back
+        d2h = 16 * n + nc * (4 + 4 + 4 + 8) + nn * (4 + 4) + npp * (8 + 8 + 8 + 1) + 8 * 4 * npp * 2
         return d2h, bd
 
     for _ in range(2):
@@ -436,7 +432,8 @@ def run_ours(args):
                                                                    else "")},
             "e2e": {"value": round(total_events / (e2e_step / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_step, 3),
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
-                    "path": "host pinned columns -> H2D -> xs_analyze -> D2H corrected trace + cells"},
+                    "path": "analyze_columnar(pinned host columns): H2D -> xs_analyze_to_host (corrected columns D2H "
+                            "overlapped with the overlap pass) -> D2H cells -> Breakdown"},
             "gpu_launches": int(launches / args.steps),
             "roofline": roof, "pipeline_roofline": pipeline, "stages_ms": stages,
             "cpu_baseline": cpu, "clocks": clocks.summary(), **check,

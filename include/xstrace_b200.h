@@ -138,6 +138,14 @@ int xs_remap(xs_ctx_t* ctx, int64_t n, const int32_t* pid_dev, const int64_t* va
 int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
                int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, xs_stream_t stream);
 
+/* xs_analyze plus the D2H of the corrected columns into caller host buffers
+ * (pinned for the copy to overlap): the copy is issued on a side stream as
+ * soon as the correction is final and overlaps the overlap pass; both are
+ * complete when the call returns. */
+int xs_analyze_to_host(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
+                       int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* out_start_host, int64_t* out_dur_host,
+                       int64_t* bad_event, xs_stream_t stream);
+
 /* transition_sites (overlap.py:263-289) for the pairs selected by pair_mask
  * (bit k = TRANSITION_PAIRS[k]).  *n_out = number of sites; fetch the
  * (pair, event index) list, ordered per pair by Event.sort_key. */

@@ -37,22 +37,28 @@ class DeviceTrace:
         self.ct = ct
         self.device = device
 
-        def up(a, dtype):
-            a = np.ascontiguousarray(a, dtype=dtype)
+        pinned = ct._pinned or {}
+
+        def up(key, dtype):
+            t = pinned.get(key)
+            a = getattr(ct, key)
             if a.size == 0:
                 return torch.zeros(1, dtype=_TORCH[dtype], device=dev)
+            if t is not None and t.dtype == _TORCH[dtype]:  # page-locked: asynchronous DMA
+                return t.to(dev, non_blocking=True)
+            a = np.ascontiguousarray(a, dtype=dtype)
             return torch.from_numpy(a).to(dev, non_blocking=non_blocking)
 
-        self.start = up(ct.start, np.int64)
-        self.dur = up(ct.dur, np.int64)
-        self.pid = up(ct.pid, np.int32)
-        self.tid = up(ct.tid, np.int32)
-        self.cat = up(ct.cat, np.uint8)
-        self.name = up(ct.name, np.int32)
-        self.corr = up(ct.corr, np.int64)
-        self.has_corr = up(ct.has_corr, np.uint8)
-        self.group_pid = up(ct.group_pid, np.int32)
-        self.pid_has_meta = up(ct.pid_has_meta, np.uint8)
+        self.start = up("start", np.int64)
+        self.dur = up("dur", np.int64)
+        self.pid = up("pid", np.int32)
+        self.tid = up("tid", np.int32)
+        self.cat = up("cat", np.uint8)
+        self.name = up("name", np.int32)
+        self.corr = up("corr", np.int64)
+        self.has_corr = up("has_corr", np.uint8)
+        self.group_pid = up("group_pid", np.int32)
+        self.pid_has_meta = up("pid_has_meta", np.uint8)
 
     @classmethod
     def from_tensors(cls, ct: ColumnarTrace, tensors: dict, device: int = 0) -> "DeviceTrace":
@@ -168,6 +174,12 @@ class Engine:
         self.check(self.lib.xs_overlap(self.ctx, C.byref(ev), attribution, self.stream()), "xs_overlap")
         return self.fetch_overlap()
 
+    def overlap_info(self) -> tuple:
+        """(n_cells, n_nodes, n_pids) of the last overlap result (host-side, no copy)."""
+        info = _lib.XsOverlapInfo()
+        self.check(self.lib.xs_overlap_info(self.ctx, C.byref(info)), "xs_overlap_info")
+        return int(info.n_cells), int(info.n_nodes), int(info.n_pids)
+
     def fetch_overlap(self) -> OverlapRaw:
         info = _lib.XsOverlapInfo()
         self.check(self.lib.xs_overlap_info(self.ctx, C.byref(info)), "xs_overlap_info")
@@ -208,7 +220,12 @@ class Engine:
                               internal.data_ptr(), has.data_ptr())
         return prof, (internal, has)
 
-    def correct(self, dt: DeviceTrace, scaled, analyze_attribution: Optional[int] = None) -> CorrectRaw:
+    def correct(self, dt: DeviceTrace, scaled, analyze_attribution: Optional[int] = None,
+                host_out=None) -> CorrectRaw:
+        """xs_correct, or xs_analyze when analyze_attribution is given.  With
+        ``host_out`` = (start, dur) host int64 buffers (pinned for overlap)
+        the corrected columns are also copied there, overlapped with the
+        overlap pass (xs_analyze_to_host)."""
         torch = _torch()
         dev = torch.device("cuda", self.device)
         n = max(dt.ct.n, 1)
@@ -220,6 +237,10 @@ class Engine:
         if analyze_attribution is None:
             st = self.lib.xs_correct(self.ctx, C.byref(ev), C.byref(prof), out_s.data_ptr(), out_d.data_ptr(),
                                      C.byref(bad), self.stream())
+        elif host_out is not None:
+            st = self.lib.xs_analyze_to_host(self.ctx, C.byref(ev), C.byref(prof), analyze_attribution,
+                                             out_s.data_ptr(), out_d.data_ptr(), _host_ptr(host_out[0]),
+                                             _host_ptr(host_out[1]), C.byref(bad), self.stream())
         else:
             st = self.lib.xs_analyze(self.ctx, C.byref(ev), C.byref(prof), analyze_attribution, out_s.data_ptr(),
                                      out_d.data_ptr(), C.byref(bad), self.stream())
@@ -287,6 +308,15 @@ class Engine:
             self.check(self.lib.xs_union_intervals_fetch(self.ctx, ilo.ctypes.data, ihi.ctypes.data, self.stream()),
                        "xs_union_intervals_fetch")
         return res + (ilo[:k], ihi[:k])
+
+
+def _host_ptr(a) -> int:
+    """Address of a host int64 buffer: a numpy array or a CPU torch tensor."""
+    if isinstance(a, np.ndarray):
+        assert a.dtype == np.int64 and a.flags.c_contiguous
+        return a.ctypes.data
+    assert a.device.type == "cpu" and a.is_contiguous()
+    return a.data_ptr()
 
 
 class UncalibratedEvent(Exception):

@@ -68,6 +68,8 @@ SIGNATURES = {
     "xs_remap": (C.c_int, [P, C.c_int64, P, P, P, P]),
     "xs_analyze": (C.c_int, [P, C.POINTER(XsEvents), C.POINTER(XsProfile), C.c_int, P, P,
                              C.POINTER(C.c_int64), P]),
+    "xs_analyze_to_host": (C.c_int, [P, C.POINTER(XsEvents), C.POINTER(XsProfile), C.c_int, P, P, P, P,
+                                     C.POINTER(C.c_int64), P]),
     "xs_transition_sites": (C.c_int, [P, C.POINTER(XsEvents), C.c_int, C.POINTER(C.c_int64), P]),
     "xs_transition_fetch": (C.c_int, [P, P, P, P]),
     "xs_union": (C.c_int, [P, C.POINTER(XsEvents), C.c_int, C.c_int, P, C.POINTER(C.c_int64),

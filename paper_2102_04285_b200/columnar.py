@@ -45,6 +45,7 @@ class ColumnarTrace:
     processes: tuple = ()
     pid_has_meta: Optional[np.ndarray] = None  # uint8 [n_pids]
     _source: Optional[Trace] = field(default=None, repr=False)
+    _pinned: Optional[dict] = field(default=None, repr=False)  # column -> pinned host tensor (see pinned())
 
     @property
     def n(self) -> int:
@@ -117,6 +118,24 @@ class ColumnarTrace:
                    np.ascontiguousarray(corr, dtype=np.int64),
                    np.ascontiguousarray(has_corr, dtype=np.uint8),
                    pids, group_pid, group_tid, list(names), tuple(processes), _source=_source)
+
+    _COLUMNS = ("start", "dur", "pid", "tid", "cat", "name", "corr", "has_corr", "group_pid", "pid_has_meta")
+
+    def pinned(self) -> "ColumnarTrace":
+        """The same trace with every column in page-locked host memory, so the
+        device upload of each call is an asynchronous DMA at full PCIe rate
+        (the arrays are numpy views of pinned torch tensors)."""
+        import torch
+
+        tens, arrs = {}, {}
+        for k in self._COLUMNS:
+            a = np.ascontiguousarray(getattr(self, k))
+            t = torch.from_numpy(a).pin_memory() if a.size else torch.from_numpy(a.copy())
+            tens[k] = t
+            arrs[k] = t.numpy()
+        return ColumnarTrace(self.clock_domain, arrs["start"], arrs["dur"], arrs["pid"], arrs["tid"], arrs["cat"],
+                             arrs["name"], arrs["corr"], arrs["has_corr"], self.pids, arrs["group_pid"],
+                             self.group_tid, self.names, self.processes, arrs["pid_has_meta"], self._source, tens)
 
     # -- conversion back ------------------------------------------------------
     def pid_value(self, idx: int) -> int:

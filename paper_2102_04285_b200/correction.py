@@ -55,7 +55,7 @@ def _source(trace, ct):
 
 
 def _run(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: Optional[int] = None,
-         device_trace=None):
+         device_trace=None, host_out=None):
     if meta_violations(ct.processes):
         raise InvalidTraceError(format_violations(_source(src, ct)))
     scaled = profile.scaled(ct.names)
@@ -63,7 +63,7 @@ def _run(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: Optio
     eng = _engine.get()
     dt = device_trace if device_trace is not None else _engine.DeviceTrace(ct, eng.device)
     try:
-        raw = eng.correct(dt, scaled, attribution)
+        raw = eng.correct(dt, scaled, attribution, host_out=host_out)
     except _engine.UncalibratedEvent as exc:
         name = ct.names[int(ct.name[exc.index])]
         raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile") from None
@@ -143,15 +143,21 @@ def correct_trace(trace, profile: CalibrationProfile) -> tuple:
     return Trace(trace.clock_domain, events, out.processes), rep
 
 
-def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution=None, device_trace=None):
+def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution=None, device_trace=None,
+                     out=None):
     """``xstrace analyze --profile``: correct, then compute_overlap(corrected).
 
-    Returns (corrected start tensor, corrected duration tensor, report,
-    Breakdown).  One device call (xs_analyze) runs both stages.
+    Returns (corrected start, corrected duration, report, Breakdown).  One
+    device call (xs_analyze) runs both stages; the columns are device tensors,
+    or, with ``out`` = (start, dur) host int64 buffers of length n (pinned:
+    e.g. ``torch.empty(n, dtype=torch.int64).pin_memory()``), those buffers,
+    filled by a copy that overlaps the overlap pass (xs_analyze_to_host).
     """
     from .overlap import Attribution, decode_breakdown
 
     attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
-    eng, dt, raw = _run(ct, profile, ct, attr, device_trace)
+    eng, dt, raw = _run(ct, profile, ct, attr, device_trace, host_out=out)
     bd = decode_breakdown(ct, eng.fetch_overlap())
+    if out is not None:
+        return out[0], out[1], _report(ct, raw), bd
     return raw.start, raw.dur, _report(ct, raw), bd

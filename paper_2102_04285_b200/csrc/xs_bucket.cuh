@@ -164,5 +164,53 @@ static __global__ void k_bucket_chunks(const int64_t* offs, int64_t nb, int64_t 
   }
 }
 
+// Pid-aligned chunking for the endpoint sort (keys = pid | t | code): a chunk
+// never straddles two pids, so its relative key range stays within one pid's
+// timeline (the fused sweep keeps 32-bit relative keys; across a pid boundary
+// the gap up to the next pid's range would not fit).  Pid p owns buckets
+// [p*PB, (p+1)*PB) and gets ceil(keys_p / BK_T) chunks; cpre[p] is the
+// exclusive prefix of those counts (cpre[np_b] = total chunks).
+static __global__ void k_pid_chunk_counts(const int64_t* offs, int64_t nb, int64_t pb_buckets, int64_t np_b,
+                                          int64_t* cnt) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > np_b) return;
+  if (p == np_b) {  // the scan's last input: cpre[np_b] becomes the total
+    cnt[p] = 0;
+    return;
+  }
+  const int64_t b0 = p * pb_buckets, b1 = (p + 1) * pb_buckets < nb ? (p + 1) * pb_buckets : nb;
+  const int64_t k = offs[b1] - offs[b0];
+  cnt[p] = (k + BK_T - 1) / BK_T;
+}
+
+static __global__ void k_bucket_chunks_pid(const int64_t* offs, int64_t nb, int64_t pb_buckets, int64_t np_b,
+                                           const int64_t* cpre, int64_t n_chunks, int64_t* chunk) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= n_chunks) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  int64_t s = -1, e = -1, b0 = 0, b1 = 0;
+  if (c < cpre[np_b]) {
+    const int64_t p = warp_search_i64<true>(cpre, 0, np_b + 1, c) - 1;  // last pid with cpre[p] <= c
+    const int64_t j = c - cpre[p];
+    const int64_t pb0 = p * pb_buckets;
+    const int64_t pb1 = (p + 1) * pb_buckets < nb ? (p + 1) * pb_buckets : nb;
+    const int64_t kend = offs[pb1];
+    const int64_t g0 = offs[pb0] + j * BK_T, g1 = g0 + BK_T;
+    const int64_t b = warp_search_i64<false>(offs, pb0, pb1, g0);
+    if (b < pb1 && offs[b] < kend && offs[b] < g1) {
+      s = offs[b];
+      const int64_t bn = warp_search_i64<false>(offs, b, pb1, g1);
+      e = offs[bn];  // bn <= pb1 and offs[pb1] = kend
+      b0 = warp_search_i64<true>(offs, b, pb1 + 1, s) - 1;   // bucket holding key s
+      b1 = warp_search_i64<true>(offs, b0, pb1 + 1, e - 1);  // bucket holding key e-1, plus one
+    }
+  }
+  if (lane == 0) {
+    chunk[4 * c + 0] = s;
+    chunk[4 * c + 1] = e;
+    chunk[4 * c + 2] = b0;
+    chunk[4 * c + 3] = b1;
+  }
+}
 
 }  // namespace xs

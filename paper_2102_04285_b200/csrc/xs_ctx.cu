@@ -197,6 +197,9 @@ void xs_ctx_destroy(xs_ctx_t* ctx) {
   for (auto& kv : ctx->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (ctx->priv_stream) cudaStreamDestroy(ctx->priv_stream);
+  if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+  if (ctx->d2h_fork) cudaEventDestroy(ctx->d2h_fork);
+  if (ctx->d2h_join) cudaEventDestroy(ctx->d2h_join);
   if (ctx->join_in) cudaEventDestroy(ctx->join_in);
   if (ctx->join_out) cudaEventDestroy(ctx->join_out);
   for (cudaEvent_t e : ctx->graph_events) cudaEventDestroy(e);
@@ -379,7 +382,8 @@ struct SpecScope {  // speculative-pass switches, cleared on every exit path
 // difference that matters for sizing (an interval shrunk to zero length, a
 // retry flag) sends the overlap pass through the ordinary path instead.
 static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
-                        int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, cudaStream_t s);
+                        int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* out_start_host,
+                        int64_t* out_dur_host, int64_t* bad_event, cudaStream_t s);
 
 int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
                int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, xs_stream_t stream) {
@@ -387,12 +391,32 @@ int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, i
   if (attribution != 0 && attribution != 1) return XS_BAD_ARGUMENT;
   cudaSetDevice(ctx->device);
   return with_lsd_retry(ctx, [&] {
-    return analyze_once(ctx, ev, prof, attribution, out_start_dev, out_dur_dev, bad_event, (cudaStream_t)stream);
+    return analyze_once(ctx, ev, prof, attribution, out_start_dev, out_dur_dev, nullptr, nullptr, bad_event,
+                        (cudaStream_t)stream);
+  });
+}
+
+int xs_analyze_to_host(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
+                       int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* out_start_host, int64_t* out_dur_host,
+                       int64_t* bad_event, xs_stream_t stream) {
+  XS_TRY(check_events(ctx, ev));
+  if (attribution != 0 && attribution != 1) return XS_BAD_ARGUMENT;
+  if (ev->n > 0 && (!out_start_host || !out_dur_host)) return XS_BAD_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (!ctx->d2h_stream) {
+    XS_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    XS_CUDA(cudaEventCreateWithFlags(&ctx->d2h_fork, cudaEventDisableTiming));
+    XS_CUDA(cudaEventCreateWithFlags(&ctx->d2h_join, cudaEventDisableTiming));
+  }
+  return with_lsd_retry(ctx, [&] {
+    return analyze_once(ctx, ev, prof, attribution, out_start_dev, out_dur_dev, out_start_host, out_dur_host,
+                        bad_event, (cudaStream_t)stream);
   });
 }
 
 static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
-                        int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* bad_event, cudaStream_t s) {
+                        int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* out_start_host,
+                        int64_t* out_dur_host, int64_t* bad_event, cudaStream_t s) {
   ctx->have_correct = false;
   ctx->have_overlap = false;
   if (bad_event) *bad_event = -1;
@@ -412,8 +436,26 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
   key.append(reinterpret_cast<const char*>(&vc), sizeof(vc));
   key.append(reinterpret_cast<const char*>(&attribution), sizeof(attribution));
   key.push_back(spec ? 1 : 0);
+  key.append(reinterpret_cast<const char*>(&out_start_host), sizeof(out_start_host));
+  key.append(reinterpret_cast<const char*>(&out_dur_host), sizeof(out_dur_host));
+  const bool to_host = out_start_host && ev->n > 0;
   XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
     XS_TRY(correct_body(ctx, v, prof, out_start_dev, out_dur_dev, false, w));
+    if (to_host) {  // the corrected columns are final: their D2H overlaps the overlap pass
+      XS_CUDA(cudaEventRecord(ctx->d2h_fork, w));
+      XS_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->d2h_fork, 0));
+      XS_CUDA(cudaMemcpyAsync(out_start_host, out_start_dev, ev->n * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+      XS_CUDA(cudaMemcpyAsync(out_dur_host, out_dur_dev, ev->n * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+      XS_CUDA(cudaEventRecord(ctx->d2h_join, ctx->d2h_stream));
+    }
+    struct Join {  // the copy stream rejoins the segment's stream on every exit
+      xs_ctx* c;
+      cudaStream_t w;
+      bool on;
+      ~Join() {
+        if (on) cudaStreamWaitEvent(w, c->d2h_join, 0);
+      }
+    } join{ctx, w, to_host};
     if (!spec) return XS_OK;
     XS_CUDA(cudaMemcpyAsync(saved, st, sizeof(Stats), cudaMemcpyDeviceToDevice, w));
     SpecScope sp(ctx, ev->dur, &st->n_ops_nz, &saved->n_ops_nz);
@@ -439,6 +481,9 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
                 c.n_nonzero == orig.n_nonzero && c.multi_op_pids == orig.multi_op_pids &&
                 c.n_api_corr == orig.n_api_corr && c.n_gpu_corr == orig.n_gpu_corr && c.max_span <= orig.max_span;
     for (int k = 0; k < 8; k++) same = same && c.cat_nz[k] == orig.cat_nz[k];
+    if (getenv("XS_DEBUG_STATS"))
+      fprintf(stderr, "xs_analyze speculative overlap %s: bad %lld full %lld depth_ovf %lld lsd %lld\n",
+              same ? "kept" : "redone", c.n_bad, c.table_full, c.depth_overflow, c.pad[3]);
     if (same) {
       ctx->have_overlap = true;
       ctx->n_cells = c.pad[4];

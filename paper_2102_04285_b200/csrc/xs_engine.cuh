@@ -66,7 +66,7 @@ enum Slot : int {
   W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
   W_CORR_TOTALS, W_NS_DEV, W_STATS_SAVE, W_PID_OPS_ALT, W_GROUP_OPS_ALT, W_PID_GROUP0_ALT,
   W_BS_COUNTS, W_BS_OFFS, W_BS_TAIL, W_BS_CHUNK, W_RMAP_IDX,
-  W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
+  W_CUB_TEMP2, W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
   W_NUM_SLOTS
 };
 
@@ -202,6 +202,9 @@ struct xs_ctx {
   long long ws_generation = 0;  // bumped on every workspace reallocation
   cudaStream_t priv_stream = nullptr;
   cudaEvent_t join_in = nullptr, join_out = nullptr;
+  // copy stream of xs_analyze_to_host
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t d2h_fork = nullptr, d2h_join = nullptr;
   // last union (xs_union / xs_utilization), kept for xs_union_intervals_fetch
   const uint64_t* un_keys = nullptr;
   const int* un_depth = nullptr;

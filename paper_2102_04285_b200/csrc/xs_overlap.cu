@@ -820,7 +820,12 @@ static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, 
   XS_TRY(ws(ctx, W_BK_COUNTS, g.nbuckets + 1, s, &counts));
   XS_TRY(ws(ctx, W_BK_OFFS, g.nbuckets + 1, s, &offs));
   XS_TRY(ws(ctx, W_MKEY, nvalid + 1, s, &keys));
-  const int64_t n_chunks = (nvalid + BK_T - 1) / BK_T;
+  // chunks never straddle pids when a pid spans whole buckets (tb + 4 >= shift)
+  const int pid_shift = tb + 4;
+  const bool pid_chunks = pid_shift >= g.shift && (key_bits > pid_shift);
+  const int64_t pb_buckets = pid_chunks ? ((int64_t)1 << (pid_shift - g.shift)) : 0;
+  const int64_t np_b = pid_chunks ? (g.nbuckets + pb_buckets - 1) / pb_buckets : 0;
+  const int64_t n_chunks = (nvalid + BK_T - 1) / BK_T + np_b;
   XS_TRY(ws(ctx, W_BK_CSTART, 4 * n_chunks + 4, s, &chunk));
   XS_CUDA(cudaMemsetAsync(counts, 0, g.nbuckets * 4, s));
   const int64_t threads = n + (n_extra + 1) / 2;
@@ -838,7 +843,23 @@ static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, 
     XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, counts, offs, (int)g.nbuckets, s));
     XS_LAUNCH(ctx, k_bk_total, 1, 32, 0, s, offs, counts, (int64_t)g.nbuckets);
     ctx->launches += 2;
-    XS_LAUNCH(ctx, k_bucket_chunks, grid_for(32 * n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, chunk);
+    if (pid_chunks) {
+      int64_t *ccnt, *cpre;
+      XS_TRY(ws(ctx, W_BK_CFIRST, 2 * np_b + 4, s, &ccnt));
+      cpre = ccnt + np_b + 2;
+      XS_LAUNCH(ctx, k_pid_chunk_counts, grid_for(np_b + 1), XS_BLOCK, 0, s, offs, (int64_t)g.nbuckets, pb_buckets,
+                np_b, ccnt);
+      size_t temp2 = 0;
+      XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp2, ccnt, cpre, (int)(np_b + 1), s));
+      void* t2;
+      XS_TRY(ws_get(ctx, W_CUB_TEMP2, temp2, s, &t2));
+      XS_CUDA(cub::DeviceScan::ExclusiveSum(t2, temp2, ccnt, cpre, (int)(np_b + 1), s));
+      ctx->launches += 2;
+      XS_LAUNCH(ctx, k_bucket_chunks_pid, grid_for(32 * n_chunks), XS_BLOCK, 0, s, offs, (int64_t)g.nbuckets,
+                pb_buckets, np_b, cpre, n_chunks, chunk);
+    } else {
+      XS_LAUNCH(ctx, k_bucket_chunks, grid_for(32 * n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, chunk);
+    }
     XS_LAUNCH(ctx, k_bk_scatter, grid_for(threads), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, extra, n_extra, g.shift,
               counts, offs, keys);
   }

@@ -186,3 +186,21 @@ def test_correction_dense_buckets_vs_oracle(gap):
 def dataclasses_replace_times(ct, start, dur):
     import dataclasses
     return dataclasses.replace(ct, start=np.ascontiguousarray(start), dur=np.ascontiguousarray(dur), _source=None)
+
+
+def test_analyze_to_host_pinned_matches_device_outputs():
+    """xs_analyze_to_host: the corrected columns land in pinned host buffers
+    (copy overlapped with the overlap pass) and equal xs_analyze's."""
+    import torch
+    from paper_2102_04285_b200 import analyze_columnar
+
+    un, inst = synth.ddpg_trace(3000, processes=2, outer_op="iteration", both=True)
+    s, d, rep, bd = analyze_columnar(inst, synth.exact_profile())
+    pin = inst.pinned()
+    assert pin._pinned["start"].is_pinned() and np.array_equal(pin.start, inst.start)
+    for _ in range(3):  # eager, capture, replay
+        hs = torch.empty(inst.n, dtype=torch.int64).pin_memory()
+        hd = torch.empty(inst.n, dtype=torch.int64).pin_memory()
+        s2, d2, rep2, bd2 = analyze_columnar(pin, synth.exact_profile(), out=(hs, hd))
+        assert s2 is hs and np.array_equal(hs.numpy(), s.cpu().numpy()) and np.array_equal(hd.numpy(), un.dur)
+        assert bd2.cells == bd.cells and rep2.removed_ns == rep.removed_ns
