@@ -170,6 +170,27 @@ int xs_utilization(xs_ctx_t* ctx, const xs_events_t* ev, int64_t period_ns, int6
                    int64_t* span_lo, int64_t* span_hi, xs_stream_t stream);
 int xs_union_intervals_fetch(xs_ctx_t* ctx, int64_t* out_lo, int64_t* out_hi, xs_stream_t stream);
 
+/* XSTRACE1 chunk decoding (traceio._decode_chunk, traceio.py:214-240;
+ * docs/trace-format.md:20-50), host memory in and out.  xs_chunk_info parses
+ * the header and string table (str_off/str_len may be NULL for a sizes-only
+ * pass); xs_chunk_decode writes the n_records rows into the columns, mapping
+ * each chunk-local string index through name_map.  Non-zero returns carry the
+ * reference's TraceFormatError message in err (xs_chunk_info returns 2 for a
+ * bad magic, 3 for a bad version). */
+typedef struct {
+  int64_t clock_domain;
+  int32_t chunk_index;
+  int32_t n_records;
+  int32_t n_strings;
+  int32_t version;
+  int64_t records_offset;
+} xs_chunk_info_t;
+int xs_chunk_info(const uint8_t* buf, int64_t len, const char* context, xs_chunk_info_t* info, int64_t* str_off,
+                  int64_t* str_len, char* err, int errlen);
+int xs_chunk_decode(const uint8_t* buf, int64_t len, const char* context, const xs_chunk_info_t* info,
+                    const int32_t* name_map, int64_t* pid, int64_t* tid, uint8_t* cat, int32_t* name, int64_t* start,
+                    int64_t* dur, int64_t* corr, uint8_t* has_corr, char* err, int errlen);
+
 /* Number of kernel launches issued by the library since context creation
  * (instrumentation for the bench's gpu_launches field). */
 int64_t xs_launch_count(xs_ctx_t* ctx);

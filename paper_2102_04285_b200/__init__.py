@@ -36,6 +36,14 @@ from .metrics import (
     summarize,
     utilization_samples,
 )
+from .traceio import (
+    IncompleteTraceError,
+    TraceFormatError,
+    TruncatedTraceError,
+    read_trace,
+    read_trace_columnar,
+    write_trace,
+)
 from .procview import ProcessNode, ProcessTree, build_process_tree, render_tree, to_dot
 from .overlap import (
     Attribution,
@@ -53,6 +61,12 @@ from .overlap import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "IncompleteTraceError",
+    "TraceFormatError",
+    "TruncatedTraceError",
+    "read_trace",
+    "read_trace_columnar",
+    "write_trace",
     "ProcessNode",
     "ProcessTree",
     "ReportRow",

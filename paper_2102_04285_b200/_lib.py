@@ -77,6 +77,8 @@ SIGNATURES = {
     "xs_utilization": (C.c_int, [P, C.POINTER(XsEvents), C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                  C.POINTER(C.c_int64), C.POINTER(C.c_int64), P]),
     "xs_union_intervals_fetch": (C.c_int, [P, P, P, P]),
+    "xs_chunk_info": (C.c_int, [P, C.c_int64, C.c_char_p, P, P, P, C.c_char_p, C.c_int]),
+    "xs_chunk_decode": (C.c_int, [P, C.c_int64, C.c_char_p, P, P, P, P, P, P, P, P, P, P, C.c_char_p, C.c_int]),
     "xs_launch_count": (C.c_int64, [P]),
     "xs_profile_enable": (C.c_int, [P, C.c_int]),
     "xs_profile_read": (C.c_int, [P, P, P, C.c_int]),

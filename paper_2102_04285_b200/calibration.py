@@ -104,7 +104,20 @@ class CalibrationProfile:
                    ("zero profile",))
 
     def scaled(self, names: Sequence[str]) -> "ScaledProfile":
-        return ScaledProfile.build(self, names)
+        """Integer form for one name table, memoised per (profile, names): a
+        repeated analysis of the same trace re-uses the resident device tables."""
+        key = (id(self), tuple(names))
+        hit = _SCALED_CACHE.get(key)
+        if hit is not None and hit[0] is self:
+            return hit[1]
+        sp = ScaledProfile.build(self, names)
+        if len(_SCALED_CACHE) >= 8:
+            _SCALED_CACHE.pop(next(iter(_SCALED_CACHE)))
+        _SCALED_CACHE[key] = (self, sp)
+        return sp
+
+
+_SCALED_CACHE: dict = {}
 
 
 def _format_ns(value: Fraction) -> str:

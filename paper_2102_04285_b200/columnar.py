@@ -27,6 +27,19 @@ import numpy as np
 from .model import Category, Event, ProcessMeta, Trace
 
 
+def _intern(values: np.ndarray):
+    """(sorted distinct values, index of each value among them): a hash
+    factorisation (O(n)) when pandas is present, else a sort."""
+    values = np.asarray(values, dtype=np.int64)
+    try:
+        import pandas as pd
+    except ImportError:  # pragma: no cover
+        uniq, inv = np.unique(values, return_inverse=True)
+        return uniq, inv.reshape(-1).astype(np.int64)
+    codes, uniq = pd.factorize(values, sort=True)
+    return np.asarray(uniq, dtype=np.int64), codes.astype(np.int64)
+
+
 @dataclass
 class ColumnarTrace:
     clock_domain: int
@@ -97,14 +110,16 @@ class ColumnarTrace:
         pid_values = np.asarray(pid_values, dtype=np.int64)
         tid_values = np.asarray(tid_values, dtype=np.int64)
         meta_pids = np.array(sorted({m.pid for m in processes}), dtype=np.int64)
-        pids = np.union1d(np.unique(pid_values), meta_pids).astype(np.int64)
-        pid = np.searchsorted(pids, pid_values).astype(np.int32)
+        ev_pids, pid_codes = _intern(pid_values)
+        pids = np.union1d(ev_pids, meta_pids).astype(np.int64)
+        pid = np.searchsorted(pids, ev_pids).astype(np.int32)[pid_codes] if n else np.zeros(0, np.int32)
         if n:
-            pairs = np.stack([pid.astype(np.int64), tid_values], axis=1)
-            uniq, inv = np.unique(pairs, axis=0, return_inverse=True)
-            group_pid = uniq[:, 0].astype(np.int32)
-            group_tid = uniq[:, 1].astype(np.int64)
-            tid = inv.reshape(-1).astype(np.int32)
+            tids, tid_codes = _intern(tid_values)
+            key = pid.astype(np.int64) * max(tids.shape[0], 1) + tid_codes  # (pid, tid) order = key order
+            uniq, inv = _intern(key)
+            group_pid = (uniq // max(tids.shape[0], 1)).astype(np.int32)
+            group_tid = tids[uniq % max(tids.shape[0], 1)].astype(np.int64)
+            tid = inv.astype(np.int32)
         else:
             group_pid = np.zeros(0, np.int32)
             group_tid = np.zeros(0, np.int64)
@@ -118,6 +133,15 @@ class ColumnarTrace:
                    np.ascontiguousarray(corr, dtype=np.int64),
                    np.ascontiguousarray(has_corr, dtype=np.uint8),
                    pids, group_pid, group_tid, list(names), tuple(processes), _source=_source)
+
+    def present_pid_mask(self) -> np.ndarray:
+        """bool[n_pids]: pids with at least one event (memoised per trace)."""
+        m = self.__dict__.get("_present_mask")
+        if m is None:
+            m = np.bincount(self.pid, minlength=self.n_pids)[: self.n_pids] > 0 if self.n else \
+                np.zeros(self.n_pids, bool)
+            self.__dict__["_present_mask"] = m
+        return m
 
     _COLUMNS = ("start", "dur", "pid", "tid", "cat", "name", "corr", "has_corr", "group_pid", "pid_has_meta")
 

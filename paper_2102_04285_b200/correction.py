@@ -76,9 +76,7 @@ def _run(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: Optio
 
 def _report(ct: ColumnarTrace, raw) -> CorrectionReport:
     rep = CorrectionReport()
-    present = np.zeros(ct.n_pids, bool)
-    if ct.n:
-        present[np.unique(ct.pid)] = True
+    present = ct.present_pid_mask()
     pids = ct.pids.tolist()
     for p in range(ct.n_pids):
         if present[p]:
@@ -90,7 +88,7 @@ def _report(ct: ColumnarTrace, raw) -> CorrectionReport:
 
 
 def _remap_processes(eng, ct: ColumnarTrace) -> tuple:
-    present = set(np.unique(ct.pid).tolist()) if ct.n else set()
+    present = set(np.nonzero(ct.present_pid_mask())[0].tolist())
     pid_index = {int(p): i for i, p in enumerate(ct.pids.tolist())}
     q_pid, q_val, slots = [], [], []
     for k, m in enumerate(ct.processes):
