@@ -105,19 +105,222 @@ def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
     return bd
 
 
-def compute_overlap_sharded(ct: ColumnarTrace, attribution=None, device=None) -> Breakdown:
-    """Each rank analyses its LPT share of the pids; returns the merged Breakdown."""
+def compute_overlap_sharded(ct: ColumnarTrace, attribution=None, device=None, split: int = 2) -> Breakdown:
+    """compute_overlap over ``world`` ranks (one GPU each): pids LPT-packed,
+    giant pids cut into operation-free time windows (INSTANT attribution);
+    every rank returns the merged Breakdown.  Invalid traces raise
+    InvalidTraceError on every rank (the verdict is all-reduced first)."""
     import torch
     import torch.distributed as dist
 
-    from . import _engine
+    from . import _engine, _lib
+    from .model import InvalidTraceError, format_violations
     from .overlap import Attribution
 
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
-    mine = shard_pids(ct, world)[rank]
-    local = ct.select_pids(mine)
+    corr = attribution is not None and Attribution(attribution) is Attribution.CORRELATION
+    plan = plan_shards(ct, world, 0 if corr else split)
+    split_pids = sorted({p for sh in plan for p, a, b in sh if a is not None or b is not None})
+    bad = 0 if check_split_correlations(ct, split_pids) else 1
+    local = shard_trace(ct, plan[rank])
     eng = _engine.get(torch.cuda.current_device())
-    attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
-    raw = eng.overlap(_engine.DeviceTrace(local, eng.device), attr)
-    return merge_breakdown_raw(local, raw, device or torch.device("cuda", eng.device))
+    dev = device or torch.device("cuda", eng.device)
+    raw = None
+    if not bad:
+        try:
+            raw = eng.overlap(_engine.DeviceTrace(local, eng.device), 1 if corr else 0)
+        except _engine.XsError as exc:
+            if exc.status != _lib.XS_INVALID_TRACE:
+                raise
+            bad = 1
+    if world > 1:
+        flag = torch.tensor([bad], dtype=torch.int64, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        bad = int(flag.item())
+    if bad:
+        raise InvalidTraceError(format_violations(ct.to_trace()))
+    return merge_breakdown_raw(local, raw, dev)
+
+
+# ---------------------------------------------------------------------------
+# Time-window splitting of giant pids (SURVEY.md 8e, partitioning (2))
+#
+# A pid with more than n / (world * split) events is cut into time windows at
+# operation-free instants: cut c is valid when no OPERATION event of the pid
+# (any tid) has start < c < end.  Then every operation lies inside one window,
+# so a window's operation ranks, nesting checks and paths are those of the
+# whole pid (overlap.py:96-99, 132-142 only compare operations active at one
+# instant).  Resource events are clipped to each window they overlap; the
+# sweep of a window then accounts exactly the window's part of the timeline
+# (_sweep_py.py:29-115 is a function of the active set at each instant), so
+# cells and tracked time add up over windows and spans merge by MIN/MAX.
+# Zero-duration events go to the window holding their start (they only feed
+# the spans).  INSTANT attribution only: CORRELATION pins a GPU event to its
+# launcher's path, which may sit in another window; such traces shard by pid.
+
+
+def op_free_gaps(ct: ColumnarTrace, p: int) -> np.ndarray:
+    """[k, 2] closed intervals of valid cut instants for pid index p (the gaps
+    between the union of its operations, plus the unbounded ends)."""
+    sel = (ct.pid == p) & (ct.cat == 0)
+    s = ct.start[sel]
+    e = s + ct.dur[sel]
+    big = np.iinfo(np.int64).max
+    if s.size == 0:
+        return np.array([[-big, big]], np.int64)
+    o = np.argsort(s, kind="stable")
+    s, e = s[o], e[o]
+    run = np.maximum.accumulate(e)  # max end of ops starting up to here
+    # a gap opens after op i when every op so far has ended by the next start
+    gap_after = np.nonzero(run[:-1] <= s[1:])[0]
+    lo = np.concatenate([[-big], run[gap_after], [run[-1]]])
+    hi = np.concatenate([[s[0]], s[gap_after + 1], [big]])
+    return np.stack([lo, hi], axis=1)
+
+
+def window_cuts(ct: ColumnarTrace, p: int, parts: int) -> list:
+    """Up to parts-1 cut instants for pid index p, near the event-count
+    quantiles, each snapped into an operation-free gap."""
+    if parts <= 1:
+        return []
+    starts = np.sort(ct.start[ct.pid == p])
+    if starts.size == 0:
+        return []
+    gaps = op_free_gaps(ct, p)
+    cuts = []
+    for j in range(1, parts):
+        q = int(starts[min(starts.size - 1, j * starts.size // parts)])
+        k = int(np.searchsorted(gaps[:, 0], q, side="right")) - 1  # last gap opening at or before q
+        best = None
+        for g in (k, k + 1):
+            if 0 <= g < gaps.shape[0]:
+                c = min(max(q, int(gaps[g, 0])), int(gaps[g, 1]))
+                if best is None or abs(c - q) < abs(best - q):
+                    best = c
+        if best is not None and (not cuts or best > cuts[-1]):
+            cuts.append(best)
+    return cuts
+
+
+def plan_shards(ct: ColumnarTrace, world: int, split: int = 2) -> list:
+    """Per rank, a list of shards (pid index, lo, hi): whole pids (lo = hi =
+    None) or time windows [lo, hi) of giant pids; LPT-packed by event count."""
+    counts = np.bincount(ct.pid, minlength=ct.n_pids) if ct.n else np.zeros(ct.n_pids, np.int64)
+    target = max(1, -(-ct.n // max(1, world * split)))
+    items = []
+    for p in range(ct.n_pids):
+        c = int(counts[p])
+        if c == 0:
+            continue
+        parts = min(world * split, -(-c // target)) if world > 1 and split > 0 else 1
+        cuts = window_cuts(ct, p, parts) if parts > 1 else []
+        if not cuts:
+            items.append((c, p, None, None))
+            continue
+        bounds = [None] + cuts + [None]
+        st = ct.start[ct.pid == p]
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            m = np.ones(st.shape[0], bool)
+            if a is not None:
+                m &= st >= a
+            if b is not None:
+                m &= st < b
+            items.append((int(m.sum()), p, a, b))
+    loads = [0] * world
+    out: list = [[] for _ in range(world)]
+    for c, p, a, b in sorted(items, key=lambda x: (-x[0], x[1], -(2**63) if x[2] is None else x[2])):
+        r = min(range(world), key=lambda k: (loads[k], k))
+        out[r].append((p, a, b))
+        loads[r] += c
+    return out
+
+
+def check_split_correlations(ct: ColumnarTrace, pids: list) -> bool:
+    """Dangling-correlation rule (model.py:207-217) for pids whose windows
+    land on different ranks: every GPU correlation must name an ACCEL_API
+    correlation of the same pid.  Host numpy over the split pids only."""
+    for p in pids:
+        sel = ct.pid == p
+        api = np.unique(ct.corr[sel & (ct.cat == 4) & (ct.has_corr == 1)])
+        gpu = ct.corr[sel & (ct.cat == 5) & (ct.has_corr == 1)]
+        if gpu.size and not np.isin(gpu, api).all():
+            return False
+    return True
+
+
+def shard_trace(ct: ColumnarTrace, shards: list) -> ColumnarTrace:
+    """The rows (and clipped intervals) one rank analyses; row order is kept,
+    so the reference's index tie-breaks are unchanged inside every pid."""
+    n = ct.n
+    keep = np.zeros(n, bool)
+    lo_c = np.full(n, np.iinfo(np.int64).min, np.int64)
+    hi_c = np.full(n, np.iinfo(np.int64).max, np.int64)
+    split = np.zeros(n, bool)
+    whole = [p for p, a, b in shards if a is None and b is None]
+    if whole:
+        keep |= np.isin(ct.pid, np.asarray(whole, np.int32))
+    start = ct.start.copy()
+    dur = ct.dur.copy()
+    end = ct.start + ct.dur
+    out_rows = []
+    for p, a, b in shards:
+        if a is None and b is None:
+            continue
+        lo = np.iinfo(np.int64).min if a is None else a
+        hi = np.iinfo(np.int64).max if b is None else b
+        sel = ct.pid == p
+        point = sel & ((ct.dur == 0) | (ct.cat == 0)) & (ct.start >= lo) & (ct.start < hi)
+        span = sel & (ct.dur > 0) & (ct.cat != 0) & (ct.start < hi) & (end > lo)
+        rows = np.nonzero(point | span)[0]
+        out_rows.append((rows, lo, hi))
+        split |= sel
+    # a pid with several windows on this rank contributes one piece per window
+    idx = [np.nonzero(keep)[0]] + [r for r, _, _ in out_rows]
+    lo_l = [np.full(idx[0].shape[0], np.iinfo(np.int64).min, np.int64)] + \
+        [np.full(r.shape[0], lo, np.int64) for r, lo, _ in out_rows]
+    hi_l = [np.full(idx[0].shape[0], np.iinfo(np.int64).max, np.int64)] + \
+        [np.full(r.shape[0], hi, np.int64) for r, _, hi in out_rows]
+    rows = np.concatenate(idx)
+    lo_a, hi_a = np.concatenate(lo_l), np.concatenate(hi_l)
+    order = np.argsort(rows, kind="stable")  # trace order (windows of one pid interleave by row)
+    rows, lo_a, hi_a = rows[order], lo_a[order], hi_a[order]
+    s = ct.start[rows]
+    e = end[rows]
+    clip = ct.cat[rows] != 0
+    s2 = np.where(clip & (ct.dur[rows] > 0), np.maximum(s, lo_a), s)
+    e2 = np.where(clip & (ct.dur[rows] > 0), np.minimum(e, hi_a), e)
+    has_corr = ct.has_corr[rows].copy()
+    # INSTANT never reads GPU correlations beyond the dangling rule, checked
+    # on the host for split pids (check_split_correlations)
+    has_corr[split[rows] & (ct.cat[rows] == 5)] = 0
+    del start, dur, lo_c, hi_c
+    return ColumnarTrace(ct.clock_domain, s2, e2 - s2, ct.pid[rows], ct.tid[rows], ct.cat[rows], ct.name[rows],
+                         ct.corr[rows], has_corr, ct.pids, ct.group_pid, ct.group_tid, ct.names, ct.processes,
+                         ct.pid_has_meta)
+
+
+def merge_raw_list(parts: list) -> Breakdown:
+    """Host merge of several (local trace, OverlapRaw) results -- the same sums
+    and MIN/MAX as merge_breakdown_raw, without a process group (one GPU
+    running every shard in turn, and the tests)."""
+    cells: dict = {}
+    spans: dict = {}
+    tracked: dict = {}
+    for ct, raw in parts:
+        rows, per_pid = local_cells(ct, raw)
+        for pv, path, m, ns in rows:
+            k = (pv, path, m)
+            cells[k] = cells.get(k, 0) + ns
+        for pv, (a, b, t) in per_pid.items():
+            lo, hi = spans.get(pv, (a, b))
+            spans[pv] = (min(lo, a), max(hi, b))
+            tracked[pv] = tracked.get(pv, 0) + t
+    bd = Breakdown()
+    for (pv, path, m), ns in cells.items():
+        if ns:
+            bd.cells[OverlapKey(pv, path, _MASK_CATS[m])] = ns
+    for pv, (a, b) in spans.items():
+        bd.spans[pv] = (a, b)
+        bd.untracked[pv] = (b - a) - tracked[pv]
+    return bd

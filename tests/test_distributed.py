@@ -114,3 +114,90 @@ def test_shard_pids_lpt_balance():
     sh = shard_pids(ct, 2)
     loads = [sum(sizes[p] for p in s) for s in sh]
     assert abs(loads[0] - loads[1]) <= max(sizes) // 4  # LPT bound, not optimal
+
+
+# ---------------------------------------------------------------------------
+# time-window splitting of giant pids (partitioning (2))
+
+@pytest.mark.parametrize("world,split", [(2, 2), (3, 2), (4, 3), (8, 2)])
+def test_window_split_merge_equals_whole_trace(world, split):
+    sys.path[:0] = [os.path.join(ROOT, "oracle")]
+    import oracle
+    from paper_2102_04285_b200 import synth
+    from paper_2102_04285_b200.distributed import merge_raw_list, plan_shards, shard_trace
+
+    for ct in (synth.adversarial_trace(40_000, pids=6, streams=32),
+               synth.ddpg_trace(200, processes=3, outer_op="iteration", second_tid_ops=True)):
+        plan = plan_shards(ct, world, split)
+        assert any(a is not None or b is not None for sh in plan for _, a, b in sh)  # something was cut
+        parts = [(local, _raw_from_oracle(local, 0)) for local in (shard_trace(ct, sh) for sh in plan)]
+        bd = merge_raw_list(parts)
+        cells = {(k.pid, k.path, frozenset(int(c) for c in k.categories)): v for k, v in bd.cells.items()}
+        assert (cells, bd.spans, bd.untracked) == oracle.overlap(ct, 0)
+
+
+def test_window_cuts_are_operation_free():
+    from paper_2102_04285_b200 import synth
+    from paper_2102_04285_b200.distributed import window_cuts
+
+    ct = synth.adversarial_trace(50_000, pids=4)
+    p = int(np.argmax(np.bincount(ct.pid)))
+    cuts = window_cuts(ct, p, 6)
+    assert cuts == sorted(set(cuts)) and len(cuts) >= 2
+    sel = (ct.pid == p) & (ct.cat == 0)
+    s, e = ct.start[sel], ct.start[sel] + ct.dur[sel]
+    for c in cuts:
+        assert not np.any((s < c) & (c < e))
+
+
+def test_split_dangling_correlation_detected_on_host():
+    from paper_2102_04285_b200 import synth
+    from paper_2102_04285_b200.distributed import check_split_correlations
+
+    ct = synth.adversarial_trace(20_000, pids=2)
+    assert check_split_correlations(ct, [0, 1])
+    g = np.nonzero((ct.cat == 5) & (ct.has_corr == 1) & (ct.pid == 0))[0][0]
+    ct.corr[g] = 10**12
+    assert not check_split_correlations(ct, [0])
+
+
+def _window_worker(rank, world, port, q):
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")]
+    import torch
+    import torch.distributed as dist
+
+    from paper_2102_04285_b200 import synth
+    from paper_2102_04285_b200.distributed import merge_breakdown_raw, plan_shards, shard_trace
+    from test_distributed import _raw_from_oracle
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        ct = synth.adversarial_trace(30_000, pids=5, streams=16)
+        plan = plan_shards(ct, world, 2)
+        local = shard_trace(ct, plan[rank])
+        bd = merge_breakdown_raw(local, _raw_from_oracle(local, 0), torch.device("cpu"))
+        cells = {(k.pid, k.path, frozenset(int(c) for c in k.categories)): v for k, v in bd.cells.items()}
+        q.put((rank, cells, bd.spans, bd.untracked))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_window_split_collective_merge():
+    sys.path[:0] = [os.path.join(ROOT, "oracle")]
+    import oracle
+    from paper_2102_04285_b200 import synth
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_window_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    exp = oracle.overlap(synth.adversarial_trace(30_000, pids=5, streams=16), 0)
+    for _, c, s, u in results:
+        assert (c, s, u) == exp

@@ -108,3 +108,22 @@ def test_config5_analyze_vs_oracle(cfg5):
 def test_config5_full_10m_overlap_vs_oracle():
     ct = synth.adversarial_trace(10_000_000, pids=64, workers=16)
     assert _ours(compute_overlap_columnar(ct)) == oracle.overlap(ct, 0)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_config5_window_split_shards_on_device(world):
+    """The multi-GPU plan (giant pids cut into operation-free windows, LPT
+    packing) run shard by shard on this GPU: the merged Breakdown equals the
+    single-call one bit for bit."""
+    from paper_2102_04285_b200 import _engine
+    from paper_2102_04285_b200.distributed import merge_raw_list, plan_shards, shard_trace
+
+    ct = synth.adversarial_trace(400_000, pids=16, workers=8)
+    whole = compute_overlap_columnar(ct)
+    eng = _engine.get(0)
+    parts = []
+    for sh in plan_shards(ct, world, 2):
+        local = shard_trace(ct, sh)
+        parts.append((local, eng.overlap(_engine.DeviceTrace(local, 0), 0)))
+    bd = merge_raw_list(parts)
+    assert bd.cells == whole.cells and bd.spans == whole.spans and bd.untracked == whole.untracked
