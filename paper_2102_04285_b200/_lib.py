@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libxstrace_b200.so")
+LIB_PATH = os.environ.get("XS_LIB_PATH") or os.path.join(HERE, "libxstrace_b200.so")  # (override: A/B experiments)
 
 XS_OK = 0
 XS_INVALID_TRACE = 1

@@ -2,8 +2,8 @@
 # Build libxstrace_b200.so for sm_100a (B200).  Cross-compiles without a GPU.
 set -euo pipefail
 HERE="$(cd "$(dirname "$0")" && pwd)"
-OUT="$HERE/../libxstrace_b200.so"
-OBJ="$HERE/../../build/obj"
+OUT="${XS_OUT:-$HERE/../libxstrace_b200.so}"
+OBJ="${XS_OBJ:-$HERE/../../build/obj}"
 mkdir -p "$OBJ"
 NVCC=${NVCC:-nvcc}
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wno-deprecated-declarations -Wno-deprecated-declarations --expt-relaxed-constexpr -I$HERE/../../include ${XS_NVCC_EXTRA:-}"

@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
     const uint64_t* __restrict__ keys, int64_t total, const int64_t* __restrict__ chunk, int shift, int tb,
     const int* __restrict__ pidpath, const int64_t* __restrict__ opbase, int n_nodes,
     GHist hist, TileDesc<SwState>* desc, int* flags, int* tile_ctr, Stats* st,
-    unsigned long long* ptrace) {
+    unsigned long long* ptrace, int direct) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -742,7 +742,17 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
   // 4. the sweep over this thread's items
   const uint64_t tmask = (1ull << tb) - 1;
   const int pshift = tb + 4;
-  CellCache<4> cache;
+  // cells: every lane merges runs of consecutive equal cells in registers;
+  // a finished run goes to the block table: direct-indexed shared counters
+  // (cell - pid base) when the chunk holds one pid and its paths fit the
+  // table, else the shared hash (CellTable) -- no probing, no CAS on the
+  // direct path.
+  const unsigned long long pbase = (unsigned long long)(base >> pshift) * (unsigned long long)n_nodes * 32ull;
+  unsigned long long run_k = ~0ull, run_v = 0;
+  auto add_cell = [&](unsigned long long key, unsigned long long v) {
+    if (direct) smem_add64(&S.h_lo[key - pbase], &S.h_hi[key - pbase], v);
+    else T.add(key, v, hist);
+  };
   int tr_pid = -1;
   long long tr_len[1] = {0};
   int c_pid = -1;
@@ -750,9 +760,11 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
   int c_path = 0;
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
-    if (my0 + j >= cnt) break;
+    const bool in = my0 + j < cnt;  // (no early exit: the warp steps together)
     const uint64_t k = base + kb[j];
-    if (have_prev && (prev >> 4) != (k >> 4) && (prev >> pshift) == (k >> pshift)) {
+    bool fin = false;
+    unsigned long long fin_k = 0, fin_v = 0;
+    if (in && have_prev && (prev >> 4) != (k >> 4) && (prev >> pshift) == (k >> pshift)) {
       const unsigned long long len = ((k >> 4) & tmask) - ((prev >> 4) & tmask);
       const int p = (int)(k >> pshift);
       unsigned mask = 0;
@@ -760,8 +772,7 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
       for (int q = 0; q < 5; q++) mask |= (cur.c[q] > 0 ? 1u : 0u) << q;
       if (mask || cur.c[5] > 0) {
         if (p != tr_pid) {
-          if (tr_pid >= 0 && tr_len[0])
-            T.add((unsigned long long)tr_pid * n_nodes * 32ull, (unsigned long long)tr_len[0], hist);
+          if (tr_pid >= 0 && tr_len[0]) add_cell((unsigned long long)tr_pid * n_nodes * 32ull, (unsigned long long)tr_len[0]);
           tr_pid = p;
           tr_len[0] = 0;
         }
@@ -778,23 +789,40 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
           c_oc = oc;
           c_path = oc > c_ob ? pidpath[oc - 1] : 0;
         }
-        cache.add(((unsigned long long)p * n_nodes + (unsigned long long)c_path) * 32ull + mask, len, T, hist);
+        const unsigned long long key = ((unsigned long long)p * n_nodes + (unsigned long long)c_path) * 32ull + mask;
+        if (key == run_k) {
+          run_v += len;
+        } else {
+          fin = run_k != ~0ull;
+          fin_k = run_k;
+          fin_v = run_v;
+          run_k = key;
+          run_v = len;
+        }
       }
     }
-    sw_apply(cur, (uint32_t)(k & 15u));
-    prev = k;
-    have_prev = true;
+    if (in) {
+      sw_apply(cur, (uint32_t)(k & 15u));
+      prev = k;
+      have_prev = true;
+    }
+    if (fin) add_cell(fin_k, fin_v);
   }
   XS_STAMP(5);
-  cache.flush(T, hist);
+  if (run_k != ~0ull) add_cell(run_k, run_v);
   block_keyed_flush<1>(tr_pid, tr_len, [&](int p, const long long* x) {
-    if (x[0]) T.add((unsigned long long)p * n_nodes * 32ull, (unsigned long long)x[0], hist);
+    if (x[0]) add_cell((unsigned long long)p * n_nodes * 32ull, (unsigned long long)x[0]);
   });
   __syncthreads();
   XS_STAMP(6);
   for (int i = t; i < HT; i += BK_THREADS) {
-    const unsigned long long key = S.h_key[i];
-    if (key != ~0ull) hist.add(key, ((unsigned long long)S.h_hi[i] << 32) | S.h_lo[i]);
+    const unsigned long long v = ((unsigned long long)S.h_hi[i] << 32) | S.h_lo[i];
+    if (direct) {
+      if (v) hist.add(pbase + (unsigned long long)i, v);
+    } else {
+      const unsigned long long key = S.h_key[i];
+      if (key != ~0ull) hist.add(key, v);
+    }
   }
   __syncthreads();
   XS_STAMP(7);
@@ -876,10 +904,13 @@ static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, 
     XS_CUDA(cudaFuncSetAttribute(k_bk_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BkSmem)));
     attr_set = true;
   }
+  // direct-indexed block table: every chunk holds one pid and a pid's cells fit
+  static const bool no_direct = getenv("XS_NO_DIRECT_CELLS") != nullptr;  // (A/B switch)
+  const int direct = !no_direct && (int64_t)n_nodes * 32 <= HT && (v.ev.n_pids <= 1 || pid_chunks) ? 1 : 0;
   unsigned long long* ptrace = nullptr;
   if (getenv("XS_TRACE_SWEEP")) XS_CUDA(cudaMallocAsync(&ptrace, n_chunks * 64, s));
   XS_LAUNCH(ctx, k_bk_sweep, (int)n_chunks, BK_THREADS, sizeof(BkSmem), s, keys, nvalid, chunk, g.shift, tb,
-            os.pidpath, os.opbase, n_nodes, hist, desc, flags, tctr, st, ptrace);
+            os.pidpath, os.opbase, n_nodes, hist, desc, flags, tctr, st, ptrace, direct);
   if (ptrace) {  // developer timing: per-phase globaltimer stamps of every CTA
     std::vector<unsigned long long> h(n_chunks * 8);
     XS_CUDA(cudaMemcpyAsync(h.data(), ptrace, n_chunks * 64, cudaMemcpyDeviceToHost, s));
