@@ -55,6 +55,7 @@ from .overlap import (
     compute_overlap,
     compute_overlap_columnar,
     count_transitions,
+    sweep_pid,
     transition_sites,
 )
 
@@ -76,6 +77,7 @@ __all__ = [
     "render_tree",
     "sampled_utilization",
     "summarize",
+    "sweep_pid",
     "to_dot",
     "utilization_samples",
     "Attribution",

@@ -8,6 +8,17 @@ using namespace xs;
 namespace xs {
 
 int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
+  if (ctx->bank == 1) {  // a concurrent branch's private scratch
+    switch (slot) {
+      case W_TILE_CTR: slot = W_TILE_CTR_B; break;
+      case W_CUB_TEMP: slot = W_CUB_TEMP_B; break;
+      case W_BS_COUNTS: slot = W_BS_COUNTS_B; break;
+      case W_BS_OFFS: slot = W_BS_OFFS_B; break;
+      case W_BS_TAIL: slot = W_BS_TAIL_B; break;
+      case W_BS_CHUNK: slot = W_BS_CHUNK_B; break;
+      default: break;
+    }
+  }
   if (bytes < 256) bytes = 256;
   if (ctx->cap[slot] < bytes) {
     if (ctx->capturing) return XS_CAPTURE_ABORT;  // never allocate inside a graph capture
@@ -197,6 +208,11 @@ void xs_ctx_destroy(xs_ctx_t* ctx) {
   for (auto& kv : ctx->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (ctx->priv_stream) cudaStreamDestroy(ctx->priv_stream);
+  for (int b = 0; b < 2; b++) {
+    if (ctx->br_stream[b]) cudaStreamDestroy(ctx->br_stream[b]);
+    if (ctx->br_join[b]) cudaEventDestroy(ctx->br_join[b]);
+  }
+  if (ctx->br_fork) cudaEventDestroy(ctx->br_fork);
   if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
   if (ctx->d2h_fork) cudaEventDestroy(ctx->d2h_fork);
   if (ctx->d2h_join) cudaEventDestroy(ctx->d2h_join);
@@ -291,9 +307,47 @@ int xs_overlap_fetch(xs_ctx_t* ctx, int32_t* cell_pid, int32_t* cell_node, int32
 
 static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start,
                         int64_t* out_dur, bool corrected_spans, cudaStream_t w) {
-  XS_TRY(stage_corr_table(ctx, v, w));
-  XS_TRY(stage_ops(ctx, v, w, false));  // OPERATION nesting is part of require_valid
-  XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, w));
+  // three independent latency-bound stages run as concurrent branches (graph
+  // branches when captured): the correlation table, the OPERATION nesting
+  // check (part of require_valid) and the wrapper-transition sites; the
+  // correction proper joins them
+  if (!ctx->br_fork) {
+    for (int b = 0; b < 2; b++) {
+      XS_CUDA(cudaStreamCreateWithFlags(&ctx->br_stream[b], cudaStreamNonBlocking));
+      XS_CUDA(cudaEventCreateWithFlags(&ctx->br_join[b], cudaEventDisableTiming));
+    }
+    XS_CUDA(cudaEventCreateWithFlags(&ctx->br_fork, cudaEventDisableTiming));
+  }
+  {  // flags the branches raise start clear before they fork
+    Stats* stp = (Stats*)ctx->ptr[W_STATS];
+    XS_CUDA(cudaMemsetAsync(&stp->table_full, 0, sizeof(long long), w));
+    XS_CUDA(cudaMemsetAsync(&stp->depth_overflow, 0, sizeof(long long), w));
+    XS_CUDA(cudaMemsetAsync(&stp->pad[3], 0, sizeof(long long), w));
+  }
+  XS_CUDA(cudaEventRecord(ctx->br_fork, w));
+  XS_CUDA(cudaStreamWaitEvent(ctx->br_stream[0], ctx->br_fork, 0));
+  XS_CUDA(cudaStreamWaitEvent(ctx->br_stream[1], ctx->br_fork, 0));
+  struct Join {  // branches rejoin w on every exit (a capture must end joined)
+    xs_ctx* c;
+    cudaStream_t w;
+    ~Join() {
+      c->bank = 0;
+      c->skip_ops_reset = false;
+      for (int b = 0; b < 2; b++) {
+        cudaEventRecord(c->br_join[b], c->br_stream[b]);
+        cudaStreamWaitEvent(w, c->br_join[b], 0);
+      }
+    }
+  };
+  {
+    Join join{ctx, w};
+    XS_TRY(stage_corr_table(ctx, v, ctx->br_stream[0]));
+    ctx->skip_ops_reset = true;
+    XS_TRY(stage_ops(ctx, v, ctx->br_stream[1], false));  // OPERATION nesting is part of require_valid
+    ctx->skip_ops_reset = false;
+    ctx->bank = 1;
+    XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, w));
+  }
   return stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, w);
 }
 

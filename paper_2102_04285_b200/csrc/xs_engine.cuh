@@ -66,7 +66,8 @@ enum Slot : int {
   W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
   W_CORR_TOTALS, W_NS_DEV, W_STATS_SAVE, W_PID_OPS_ALT, W_GROUP_OPS_ALT, W_PID_GROUP0_ALT,
   W_BS_COUNTS, W_BS_OFFS, W_BS_TAIL, W_BS_CHUNK, W_RMAP_IDX,
-  W_CUB_TEMP2, W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
+  W_CUB_TEMP2, W_TILE_CTR_B, W_CUB_TEMP_B, W_BS_COUNTS_B, W_BS_OFFS_B, W_BS_TAIL_B, W_BS_CHUNK_B,
+  W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
   W_NUM_SLOTS
 };
 
@@ -202,6 +203,14 @@ struct xs_ctx {
   long long ws_generation = 0;  // bumped on every workspace reallocation
   cudaStream_t priv_stream = nullptr;
   cudaEvent_t join_in = nullptr, join_out = nullptr;
+  // concurrent pipeline branches (correct_body): side streams, fork/join
+  // events, and the scratch bank of the branch being issued (bank 1 remaps the
+  // shared scratch slots -- tile counters, CUB temp, bucket-sort tables -- to
+  // private copies so two branches never share them)
+  cudaStream_t br_stream[2] = {nullptr, nullptr};
+  cudaEvent_t br_fork = nullptr, br_join[2] = {nullptr, nullptr};
+  int bank = 0;
+  bool skip_ops_reset = false;
   // copy stream of xs_analyze_to_host
   cudaStream_t d2h_stream = nullptr;
   cudaEvent_t d2h_fork = nullptr, d2h_join = nullptr;

@@ -402,7 +402,7 @@ int trie_setup(xs_ctx* ctx, cudaStream_t s, TrieView* t) {
 
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths) {
   ProfScope ps(ctx, ST_OPS, s);
-  {  // retry-able flags start clear on every attempt
+  if (!ctx->skip_ops_reset) {  // retry-able flags start clear on every attempt
     Stats* stp = (Stats*)ctx->ptr[W_STATS];
     XS_CUDA(cudaMemsetAsync(&stp->table_full, 0, sizeof(long long), s));
     XS_CUDA(cudaMemsetAsync(&stp->depth_overflow, 0, sizeof(long long), s));

@@ -203,3 +203,49 @@ def count_transitions(trace) -> TransitionCounts:
     _, pair, _ = _transition_lists(trace, 0xF)
     counts = np.bincount(pair, minlength=4) if len(pair) else np.zeros(4, np.int64)
     return TransitionCounts(tuple((s, d, int(counts[k])) for k, (s, d) in enumerate(TRANSITION_PAIRS)))
+
+
+def sweep_pid(starts, ends, cats, ranks, fixed_paths, add_order, rem_order, rank_name_ids, path_table):
+    """The reference's kernel plugin protocol (overlap.py:30-38, 106-113;
+    _sweep_py.py:29-115) served by the device pipeline: one pid's boundary
+    walk -> ``(cells {(path_id << 6) | mask: ns}, tracked_ns)``, path ids
+    interned in the caller's ``path_table`` (tuples of name ids).
+
+    The pid's nonzero-duration events (``add_order``) become a one-pid
+    ColumnarTrace; each operation sits on its own tid numbered by its rank,
+    so the device's (start, -end, tid, name) rank order reproduces the given
+    ``ranks`` and its multi-tid path merge is ``path_of``'s rank-ordered,
+    adjacent-deduplicated name list.  GPU events pinned to launch-site paths
+    (``fixed_paths`` >= 0, CORRELATION) are computed by compute_overlap
+    itself from correlations; this shim serves INSTANT inputs.
+    """
+    if any(fp >= 0 for fp in fixed_paths):
+        raise NotImplementedError("sweep_pid shim: fixed (CORRELATION) paths are resolved inside compute_overlap")
+    cur = path_table.get_id(())
+    idx = list(add_order)
+    n = len(idx)
+    if n == 0:
+        return {}, 0
+    s = np.array([starts[i] for i in idx], np.int64)
+    e = np.array([ends[i] for i in idx], np.int64)
+    c = np.array([cats[i] for i in idx], np.uint8)
+    is_op = c == 0
+    rk = np.array([ranks[i] for i in idx], np.int64)
+    nid = np.array([rank_name_ids[r] if op else 0 for r, op in zip(rk.tolist(), is_op.tolist())], np.int64)
+    names = sorted({str(x) for x in nid[is_op].tolist()} | {"_"})
+    nrank = {x: k for k, x in enumerate(names)}
+    name = np.array([nrank[str(x)] if op else nrank["_"] for x, op in zip(nid.tolist(), is_op.tolist())], np.int32)
+    tid = np.where(is_op, rk + 1, 0)
+    from .model import ProcessMeta
+    ct = ColumnarTrace.from_arrays(0, s, e - s, np.ones(n, np.int64), tid, c, name, names,
+                                   processes=(ProcessMeta(1, "pid"),))
+    bd = compute_overlap_columnar(ct)
+    cells = {}
+    for key, ns in bd.cells.items():
+        pid_path = path_table.get_id(tuple(int(x) for x in key.path))
+        mask = sum(1 << (int(cc) - 1) for cc in key.categories)
+        cells[(pid_path << 6) | mask] = ns
+    lo, hi = bd.spans[1]
+    tracked = (hi - lo) - bd.untracked[1]
+    del cur
+    return cells, tracked

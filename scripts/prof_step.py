@@ -1,4 +1,8 @@
-"""One short workload for ncu captures: N xs_analyze calls on the bench trace."""
+"""One short workload for ncu captures: N xs_analyze calls on a bench trace.
+
+    XS_CONFIG=2 (default): the config-2 DDPG trace (XS_ITERS iterations)
+    XS_CONFIG=3: config 3 with XS_EVENTS events (100 pids of 1M by default)
+"""
 import os
 import sys
 
@@ -7,9 +11,14 @@ sys.path.insert(0, ROOT)
 
 from paper_2102_04285_b200 import _engine, synth  # noqa: E402
 
-iters = int(os.environ.get("XS_ITERS", "27027"))
+cfg = int(os.environ.get("XS_CONFIG", "2"))
 calls = int(os.environ.get("XS_CALLS", "2"))
-ct = synth.ddpg_trace(iters)
+if cfg == 3:
+    ev = int(os.environ.get("XS_EVENTS", "100000000"))
+    procs = max(1, ev // 1_000_000)
+    ct = synth.config3_trace(processes=procs, events_per_pid=ev // procs, workers=os.cpu_count())
+else:
+    ct = synth.ddpg_trace(int(os.environ.get("XS_ITERS", "27027")))
 eng = _engine.get(0)
 dt = _engine.DeviceTrace(ct, 0)
 scaled = synth.exact_profile().scaled(ct.names)

@@ -92,3 +92,30 @@ def test_overlap_dense_buckets_vs_oracle(n_same):
     ct = _dense_trace(n_same)
     bd = compute_overlap_columnar(ct)
     assert _ours(bd) == _oracle_bd(ct, 0)
+
+
+SWEEP = load("sweep_pid_cases.json.gz")
+
+
+class _PathTable:  # the reference's PathTable protocol (overlap.py:80-93)
+    def __init__(self):
+        self._ids, self.paths = {}, []
+
+    def get_id(self, key):
+        if key not in self._ids:
+            self._ids[key] = len(self.paths)
+            self.paths.append(key)
+        return self._ids[key]
+
+
+@pytest.mark.parametrize("k", range(len(SWEEP)))
+def test_sweep_pid_plugin_shim_matches_reference_kernel(k):
+    """paper_2102_04285_b200.sweep_pid is a drop-in for the reference's
+    `kernel=` plugin (the inputs recorded from the reference's compute_overlap)."""
+    from paper_2102_04285_b200 import sweep_pid
+
+    case = SWEEP[k]
+    pt = _PathTable()
+    cells, tracked = sweep_pid(*case["args"], pt)
+    got = sorted([list(pt.paths[key >> 6]), key & 63, v] for key, v in cells.items())
+    assert got == case["cells"] and tracked == case["tracked"]
