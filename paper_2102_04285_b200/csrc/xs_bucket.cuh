@@ -24,12 +24,6 @@ constexpr int BK_CAP = BK_THREADS * BK_ITEMS;  // keys per chunk tile
 constexpr int BK_T = BK_CAP / 2;                // chunk split granule (max bucket)
 constexpr int BK_RANK_MAX = 64;                 // buckets up to this size are ranked by direct comparison
 
-struct BucketGeom {
-  int key_bits;  // keys occupy [0, key_bits)
-  int bb;        // bucket bits
-  int shift;     // bucket = key >> shift
-  int64_t nbuckets;
-};
 
 inline BucketGeom bucket_geom(int key_bits, int max_bb = 20) {
   BucketGeom g;

@@ -120,7 +120,7 @@ int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s
     key.append(reinterpret_cast<const char*>(&attribution), sizeof(attribution));
     XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
       XS_TRY(stage_corr_table(ctx, v, w));
-      XS_TRY(stage_ops(ctx, v, w, true));
+      XS_TRY(ops_with_overlap_pre(ctx, v, attribution, w));
       return stage_overlap(ctx, v, attribution, w);
     }));
     ctx->res_pids = v.ev.n_pids;
@@ -156,6 +156,40 @@ int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s
   }
   ctx->err = "path table could not be sized";
   return XS_NO_MEMORY;
+}
+
+static int ensure_branches(xs_ctx* ctx) {
+  if (!ctx->br_fork) {
+    for (int b = 0; b < 2; b++) {
+      XS_CUDA(cudaStreamCreateWithFlags(&ctx->br_stream[b], cudaStreamNonBlocking));
+      XS_CUDA(cudaEventCreateWithFlags(&ctx->br_join[b], cudaEventDisableTiming));
+    }
+    XS_CUDA(cudaEventCreateWithFlags(&ctx->br_fork, cudaEventDisableTiming));
+  }
+  return XS_OK;
+}
+
+// stage_ops (paths) on a side branch while the INSTANT endpoint sort's first
+// phase (histogram, offsets, chunk table, scatter) runs on w: the two only
+// meet in the sweep kernel
+int ops_with_overlap_pre(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t w) {
+  static const bool serial = getenv("XS_NO_BRANCHES") != nullptr;  // (A/B switch)
+  if (attribution != 0 || ctx->force_lsd || serial) return stage_ops(ctx, v, w, true);
+  XS_TRY(ensure_branches(ctx));
+  XS_CUDA(cudaEventRecord(ctx->br_fork, w));
+  XS_CUDA(cudaStreamWaitEvent(ctx->br_stream[1], ctx->br_fork, 0));
+  struct Join {
+    xs_ctx* c;
+    cudaStream_t w;
+    ~Join() {
+      c->bank = 0;
+      cudaEventRecord(c->br_join[1], c->br_stream[1]);
+      cudaStreamWaitEvent(w, c->br_join[1], 0);
+    }
+  } join{ctx, w};
+  XS_TRY(stage_ops(ctx, v, ctx->br_stream[1], true));
+  ctx->bank = 1;
+  return stage_overlap_pre(ctx, v, w);
 }
 
 }  // namespace xs
@@ -311,13 +345,7 @@ static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* pro
   // branches when captured): the correlation table, the OPERATION nesting
   // check (part of require_valid) and the wrapper-transition sites; the
   // correction proper joins them
-  if (!ctx->br_fork) {
-    for (int b = 0; b < 2; b++) {
-      XS_CUDA(cudaStreamCreateWithFlags(&ctx->br_stream[b], cudaStreamNonBlocking));
-      XS_CUDA(cudaEventCreateWithFlags(&ctx->br_join[b], cudaEventDisableTiming));
-    }
-    XS_CUDA(cudaEventCreateWithFlags(&ctx->br_fork, cudaEventDisableTiming));
-  }
+  XS_TRY(ensure_branches(ctx));
   {  // flags the branches raise start clear before they fork
     Stats* stp = (Stats*)ctx->ptr[W_STATS];
     XS_CUDA(cudaMemsetAsync(&stp->table_full, 0, sizeof(long long), w));
@@ -517,7 +545,7 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     // correlations are untouched by the correction: the original's dangling
     // check stands, and only CORRELATION attribution needs launch instants
     if (attribution == 1) XS_TRY(stage_corr_table(ctx, vc, w));
-    XS_TRY(stage_ops(ctx, vc, w, true));
+    XS_TRY(ops_with_overlap_pre(ctx, vc, attribution, w));
     XS_TRY(stage_overlap(ctx, vc, attribution, w));
     ctx->res_pids = ev->n_pids;
     return corrected_total_from_spans(ctx, w);

@@ -150,6 +150,25 @@ struct OpsState {
 
 }  // namespace xs
 
+namespace xs {
+struct BucketGeom {  // bucketed sorts (xs_bucket.cuh)
+  int key_bits;  // keys occupy [0, key_bits)
+  int bb;        // bucket bits
+  int shift;     // bucket = key >> shift
+  int64_t nbuckets;
+};
+struct BkPlan {  // a prepared bucketed endpoint sort (xs_overlap.cu)
+  bool ready = false;
+  BucketGeom g{};
+  int64_t nvalid = 0, n_chunks = 0, n = 0;
+  bool pid_chunks = false;
+  uint64_t* keys = nullptr;
+  int64_t* chunk = nullptr;
+  int tb = 0, key_bits = 0;
+  const int64_t* start = nullptr;
+};
+}  // namespace xs
+
 struct xs_ctx {
   int device = 0;
   std::string err;
@@ -203,6 +222,8 @@ struct xs_ctx {
   long long ws_generation = 0;  // bumped on every workspace reallocation
   cudaStream_t priv_stream = nullptr;
   cudaEvent_t join_in = nullptr, join_out = nullptr;
+  // endpoint-sort plan issued ahead of the OPERATION stage (stage_overlap_pre)
+  xs::BkPlan bk_plan;
   // concurrent pipeline branches (correct_body): side streams, fork/join
   // events, and the scratch bank of the branch being issued (bank 1 remaps the
   // shared scratch slots -- tile counters, CUB temp, bucket-sort tables -- to
@@ -327,6 +348,8 @@ int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr
                  const xs_profile_t* prof);
 int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s);
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths);
+int stage_overlap_pre(xs_ctx* ctx, const EventView& v, cudaStream_t s);
+int ops_with_overlap_pre(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t w);
 int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
 int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mask, cudaStream_t s);
 int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start,

@@ -835,11 +835,11 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
 
 
 // host driver for the bucketed endpoint sort + sweep
-static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, int tb, int corr_mode,
-                            const uint64_t* extra, int64_t n_extra, int64_t nvalid, int key_bits, int n_nodes,
-                            const GHist& hist, cudaStream_t s) {
-  OpsState& os = ctx->ops;
-  Stats* st = (Stats*)ctx->ptr[W_STATS];
+// phase 1: endpoint keys histogrammed, bucket offsets, chunk table, scatter
+// (needs pass 1 only, so it can overlap the OPERATION stage)
+static int bucket_prepare(xs_ctx* ctx, const EventView& v, const int64_t* lo, int tb, int corr_mode,
+                          const uint64_t* extra, int64_t n_extra, int64_t nvalid, int key_bits, cudaStream_t s,
+                          BkPlan* plan) {
   const int64_t n = v.ev.n;
   const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(nvalid, key_bits));
   unsigned* counts;
@@ -891,6 +891,31 @@ static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, 
     XS_LAUNCH(ctx, k_bk_scatter, grid_for(threads), XS_BLOCK, 0, s, v, n, lo, tb, corr_mode, extra, n_extra, g.shift,
               counts, offs, keys);
   }
+  plan->ready = true;
+  plan->g = g;
+  plan->nvalid = nvalid;
+  plan->n_chunks = n_chunks;
+  plan->pid_chunks = pid_chunks;
+  plan->keys = keys;
+  plan->chunk = chunk;
+  plan->tb = tb;
+  plan->key_bits = key_bits;
+  plan->start = v.start;
+  plan->n = n;
+  return XS_OK;
+}
+
+// phase 2: the fused per-chunk sort + sweep (needs the op paths)
+static int bucket_sweep(xs_ctx* ctx, const EventView& v, const BkPlan& plan, int n_nodes, const GHist& hist,
+                        cudaStream_t s) {
+  OpsState& os = ctx->ops;
+  Stats* st = (Stats*)ctx->ptr[W_STATS];
+  const BucketGeom g = plan.g;
+  const int64_t n_chunks = plan.n_chunks, nvalid = plan.nvalid;
+  const bool pid_chunks = plan.pid_chunks;
+  const int tb = plan.tb;
+  uint64_t* keys = plan.keys;
+  int64_t* chunk = plan.chunk;
   TileDesc<SwState>* desc;
   int *flags, *tctr;
   XS_TRY(ws(ctx, W_MSCAN_DESC, n_chunks + 1, s, &desc));
@@ -929,6 +954,28 @@ static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, 
             ph[4] / n_chunks / 1e3, ph[5] / n_chunks / 1e3, ph[6] / n_chunks / 1e3);
   }
   return XS_OK;
+}
+
+static int run_bucket_sweep(xs_ctx* ctx, const EventView& v, const int64_t* lo, int tb, int corr_mode,
+                            const uint64_t* extra, int64_t n_extra, int64_t nvalid, int key_bits, int n_nodes,
+                            const GHist& hist, cudaStream_t s) {
+  BkPlan plan;
+  XS_TRY(bucket_prepare(ctx, v, lo, tb, corr_mode, extra, n_extra, nvalid, key_bits, s, &plan));
+  return bucket_sweep(ctx, v, plan, n_nodes, hist, s);
+}
+
+// INSTANT overlap, phase 1 ahead of stage_ops (concurrent branch): the plan
+// is picked up by the next stage_overlap on the same events
+int stage_overlap_pre(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
+  ctx->bk_plan.ready = false;
+  const Stats& H = *ctx->h_stats;
+  const int np = v.ev.n_pids;
+  const int tb = bits_for((uint64_t)(H.max_span > 0 ? H.max_span : 0));
+  const int pb = bits_for((uint64_t)(np > 0 ? np - 1 : 0));
+  const int64_t nvalid = 2 * H.n_nonzero;
+  if (ctx->force_lsd || nvalid <= 0 || pb + tb + 4 > 64) return XS_OK;
+  return bucket_prepare(ctx, v, (const int64_t*)ctx->ptr[W_SPAN_LO], tb, 0, nullptr, 0, nvalid, pb + tb + 4, s,
+                        &ctx->bk_plan);
 }
 
 int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s) {
@@ -1032,7 +1079,13 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   const uint64_t sentinel = key_bits >= 64 ? ~0ull : ((1ull << key_bits) - 1);
   const int64_t nkeys = 2 * n + n_piece_keys;
   const int64_t nvalid_b = 2 * H.n_nonzero + n_piece_keys;
-  if (!ctx->force_lsd && nvalid_b > 0) {
+  BkPlan& pre = ctx->bk_plan;
+  const bool use_pre = pre.ready && !corr_mode && pre.start == v.start && pre.n == n && pre.tb == tb &&
+                       pre.key_bits == key_bits && pre.nvalid == nvalid_b;
+  pre.ready = false;
+  if (!ctx->force_lsd && nvalid_b > 0 && use_pre) {
+    XS_TRY(bucket_sweep(ctx, v, pre, n_nodes, hist, s));
+  } else if (!ctx->force_lsd && nvalid_b > 0) {
     XS_TRY(run_bucket_sweep(ctx, v, lo, tb, corr_mode, pieces, n_piece_keys, nvalid_b, key_bits, n_nodes, hist, s));
   } else {
   uint64_t *mk, *mk_alt;
