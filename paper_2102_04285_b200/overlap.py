@@ -31,11 +31,27 @@ class Attribution(Enum):
     CORRELATION = "correlation"
 
 
-@dataclass(frozen=True)
-class OverlapKey:
-    pid: int
-    path: tuple
-    categories: frozenset
+class OverlapKey(tuple):
+    """(pid, operation path, category set) of one overlap cell (overlap.py:48-58).
+
+    Same fields, hashing-by-value, equality and labels as the reference's
+    frozen dataclass; stored as a tuple so decoding millions of cells from the
+    device stays cheap (config 5 produces ~4M cells)."""
+
+    __slots__ = ()
+
+    def __new__(cls, pid, path, categories):
+        return tuple.__new__(cls, (pid, path, categories))
+
+    pid = property(lambda self: self[0])
+    path = property(lambda self: self[1])
+    categories = property(lambda self: self[2])
+
+    def __repr__(self) -> str:
+        return f"OverlapKey(pid={self[0]!r}, path={self[1]!r}, categories={self[2]!r})"
+
+    def __reduce__(self):
+        return (OverlapKey, tuple(self))
 
     def category_label(self) -> str:
         return "+".join(c.name for c in sorted(self.categories))
@@ -123,9 +139,10 @@ def decode_breakdown(ct: ColumnarTrace, raw) -> Breakdown:
     bd = Breakdown()
     paths = decode_paths(ct, raw.node_parent, raw.node_name)
     pids = ct.pids.tolist()
-    for p, node, mask, ns in zip(raw.cell_pid.tolist(), raw.cell_node.tolist(), raw.cell_mask.tolist(),
-                                 raw.cell_ns.tolist()):
-        bd.cells[OverlapKey(pids[p], paths[node], _MASK_CATS[mask])] = ns
+    mk = tuple.__new__
+    pv = [pids[p] for p in raw.cell_pid.tolist()] if len(pids) != 1 else [pids[0]] * raw.cell_pid.shape[0]
+    bd.cells = dict(zip((mk(OverlapKey, (p, paths[nd], _MASK_CATS[m])) for p, nd, m in
+                         zip(pv, raw.cell_node.tolist(), raw.cell_mask.tolist())), raw.cell_ns.tolist()))
     for p in range(ct.n_pids):
         if raw.has_events[p]:
             lo, hi = int(raw.span_lo[p]), int(raw.span_hi[p])
