@@ -48,13 +48,17 @@ struct P1Acc {
   unsigned long long cnt0 = 0;  // bad, nonzero, ops_nz, ops
   unsigned long long cnt1 = 0;  // api, api_corr, gpu_corr
   long long bad_api = INT64_MAX;
-  int cur_p = -1, cur_g = -1, cur_pops = 0, cur_gops = 0;
+  int cur_p = -1, cur_pops = 0;
+  // per-(pid, tid) group op counts: a 4-entry register cache (ops of several
+  // tids interleave in row order; flushing on every group switch would hammer
+  // a handful of global counters with atomics)
+  int gk[4] = {-1, -1, -1, -1}, gc[4] = {0, 0, 0, 0};
   long long lo = 0, hi = 0;
 };
 
 __device__ __forceinline__ void p1_visit(P1Acc& A, int64_t i, int64_t s, int64_t d, int p, int c, bool meta,
-                                         int64_t* lo_out, int64_t* hi_out, int* pid_ops, int* group_ops,
-                                         const EventView& v, const uint8_t* has_internal, int check_api) {
+                                         int g, unsigned hc, int nm, int64_t* lo_out, int64_t* hi_out,
+                                         int* pid_ops, int* group_ops, const uint8_t* has_internal, int check_api) {
   const int64_t dd = d > 0 ? d : 0;
   const unsigned bad = (d < 0) + (s < 0) + (s > 0 && dd > INT64_MAX - s) + !meta;
   const int64_t e = (int64_t)((uint64_t)s + (uint64_t)d);
@@ -86,19 +90,27 @@ __device__ __forceinline__ void p1_visit(P1Acc& A, int64_t i, int64_t s, int64_t
   if (c == 0) {
     if (nzd) {
       A.cur_pops++;
-      const int g = v.ev.tid[i];
-      if (g != A.cur_g) {
-        if (A.cur_g >= 0 && A.cur_gops) atomicAdd(&group_ops[A.cur_g], A.cur_gops);
-        A.cur_g = g;
-        A.cur_gops = 0;
+      if (g == A.gk[0]) {
+        A.gc[0]++;
+      } else if (g == A.gk[1]) {
+        A.gc[1]++;
+      } else if (g == A.gk[2]) {
+        A.gc[2]++;
+      } else if (g == A.gk[3]) {
+        A.gc[3]++;
+      } else {  // evict the last slot, insert at the front
+        if (A.gk[3] >= 0 && A.gc[3]) atomicAdd(&group_ops[A.gk[3]], A.gc[3]);
+        A.gk[3] = A.gk[2], A.gc[3] = A.gc[2];
+        A.gk[2] = A.gk[1], A.gc[2] = A.gc[1];
+        A.gk[1] = A.gk[0], A.gc[1] = A.gc[0];
+        A.gk[0] = g, A.gc[0] = 1;
       }
-      A.cur_gops++;
     }
   } else if (c == 4) {
-    A.cnt1 += 1ull | ((unsigned long long)v.ev.has_corr[i] << 16);
-    if (check_api && !has_internal[v.ev.name[i]]) A.bad_api = i < A.bad_api ? i : A.bad_api;
+    A.cnt1 += 1ull | ((unsigned long long)hc << 16);
+    if (check_api && !has_internal[nm]) A.bad_api = i < A.bad_api ? i : A.bad_api;
   } else if (c == 5) {
-    A.cnt1 += (unsigned long long)v.ev.has_corr[i] << 32;
+    A.cnt1 += (unsigned long long)hc << 32;
   }
 }
 
@@ -108,7 +120,11 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x)
   return x;
 }
 
-constexpr int P1_VEC = 4;  // events per vector step (16-byte loads)
+constexpr int P1_VEC = 4;
+#ifndef XS_P1_UNROLL
+#define XS_P1_UNROLL 2
+#endif
+constexpr int kP1Unroll = XS_P1_UNROLL;  // vector steps in flight per thread  // events per vector step (16-byte loads)
 
 // One streaming pass; each thread takes P1_ITEMS consecutive events in
 // vector steps of 4 (16-byte loads of start/dur/pid, one 4-byte load of the
@@ -124,15 +140,38 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
   if (threadIdx.x < 20) s_cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_bad_api = INT64_MAX;
   P1Acc A;
-  const int64_t tbase = ((int64_t)blockIdx.x * XS_BLOCK + threadIdx.x) * P1_ITEMS;
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  __syncthreads();  // s_cnt initialised
+  // persistent CTAs over "virtual blocks" of XS_BLOCK * P1_ITEMS events: the
+  // per-CTA global atomics on the ~20 shared counters happen once per CTA,
+  // not once per 4096 events (same-address atomics serialise in L2)
+  const int64_t nvb = (n + (int64_t)XS_BLOCK * P1_ITEMS - 1) / ((int64_t)XS_BLOCK * P1_ITEMS);
+  // each CTA walks a contiguous run of virtual blocks, so a thread's running
+  // pid only changes at pid boundaries (every change costs global atomics)
+  const int64_t per = (nvb + gridDim.x - 1) / gridDim.x;
+  const int64_t vb_end = (blockIdx.x + 1) * per < nvb ? (blockIdx.x + 1) * per : nvb;
 #pragma unroll 1
+  for (int64_t vb = blockIdx.x * per; vb < vb_end; vb++) {
+  const int64_t tbase = (vb * XS_BLOCK + threadIdx.x) * P1_ITEMS;
+#pragma unroll kP1Unroll
   for (int step = 0; step < P1_ITEMS / P1_VEC; step++) {
     const int64_t i0 = tbase + step * P1_VEC;
     if (i0 >= n) break;
     int64_t s[4], d[4];
-    int p[4], c[4];
+    int p[4], c[4], g[4], nm[4];
+    unsigned hc[4];
     int cnt = 4;
     if (kVec && i0 + 4 <= n) {
+      // every column the visit may need, loaded up front (independent vector
+      // loads instead of per-event dependent ones)
+      const int4 g4 = *reinterpret_cast<const int4*>(v.ev.tid + i0);
+      const int4 n4 = *reinterpret_cast<const int4*>(v.ev.name + i0);
+      const uint32_t h4 = *reinterpret_cast<const uint32_t*>(v.ev.has_corr + i0);
+      g[0] = g4.x, g[1] = g4.y, g[2] = g4.z, g[3] = g4.w;
+      nm[0] = n4.x, nm[1] = n4.y, nm[2] = n4.z, nm[3] = n4.w;
+#pragma unroll
+      for (int k = 0; k < 4; k++) hc[k] = (h4 >> (8 * k)) & 0xFFu;
       const longlong2 s01 = *reinterpret_cast<const longlong2*>(v.start + i0);
       const longlong2 s23 = *reinterpret_cast<const longlong2*>(v.start + i0 + 2);
       const longlong2 d01 = *reinterpret_cast<const longlong2*>(v.dur + i0);
@@ -153,6 +192,9 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
           d[k] = v.dur[i0 + k];
           p[k] = v.ev.pid[i0 + k];
           c[k] = v.ev.cat[i0 + k];
+          g[k] = v.ev.tid[i0 + k];
+          nm[k] = v.ev.name[i0 + k];
+          hc[k] = v.ev.has_corr[i0 + k];
         }
       }
     }
@@ -165,63 +207,91 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
           mp = p[k];
           meta = has_meta[mp] != 0;
         }
-        p1_visit(A, i0 + k, s[k], d[k], p[k], c[k], meta, lo_out, hi_out, pid_ops, group_ops, v, has_internal,
-                 check_api);
+        p1_visit(A, i0 + k, s[k], d[k], p[k], c[k], meta, g[k], hc[k], nm[k], lo_out, hi_out, pid_ops, group_ops,
+                 has_internal, check_api);
       }
     }
   }
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  // running per-pid span / op count: warp-aggregate when the warp agrees
+  // fold this virtual block's packed counters (16-bit lanes) into shared memory
+  {
+    const unsigned long long w0 = warp_sum_u64(A.cat_all0), w1 = warp_sum_u64(A.cat_all1),
+                             w2 = warp_sum_u64(A.cat_nz0), w3 = warp_sum_u64(A.cat_nz1),
+                             w4 = warp_sum_u64(A.cnt0), w5 = warp_sum_u64(A.cnt1);
+    if (lane < 19) {
+      // counter layout: 0-5 cat_all, 6-11 cat_nz, 12-15 cnt0 lanes, 16-18 cnt1 lanes
+      const unsigned long long word = lane < 4 ? w0 : lane < 6 ? w1 : lane < 10 ? w2 : lane < 12 ? w3 : lane < 16 ? w4 : w5;
+      const int sub = lane < 6 ? (lane & 3) : lane < 12 ? ((lane - 6) & 3) : lane < 16 ? lane - 12 : lane - 16;
+      const unsigned long long x = (word >> (16 * sub)) & 0xFFFFull;
+      if (x) atomicAdd(&s_cnt[lane], x);
+    }
+    A.cat_all0 = A.cat_all1 = A.cat_nz0 = A.cat_nz1 = A.cnt0 = A.cnt1 = 0;
+  }
+  }  // virtual blocks
+  // running per-pid span / op count: warp-aggregate when the warp agrees,
+  // then block-aggregate warps that share a pid (one atomic per pid per CTA)
+  __shared__ int s_wp[XS_BLOCK / 32];
+  __shared__ long long s_wl[XS_BLOCK / 32], s_wh[XS_BLOCK / 32], s_wo[XS_BLOCK / 32];
   const int p0 = __shfl_sync(full, A.cur_p, 0);
+  const int warp = threadIdx.x >> 5;
   if (__all_sync(full, A.cur_p == p0)) {
-    if (p0 >= 0) {
-      long long l = A.lo, h = A.hi;
+    long long l = A.lo, h = A.hi;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const long long l2 = __shfl_xor_sync(full, l, o), h2 = __shfl_xor_sync(full, h, o);
-        l = l2 < l ? l2 : l;
-        h = h2 > h ? h2 : h;
-      }
-      const long long po = warp_sum(A.cur_pops);
-      if (lane == 0) {
-        atomic_min_i64(&lo_out[p0], l);
-        atomic_max_i64(&hi_out[p0], h);
-        if (po) atomicAdd(&pid_ops[p0], (int)po);
-      }
+    for (int o = 16; o; o >>= 1) {
+      const long long l2 = __shfl_xor_sync(full, l, o), h2 = __shfl_xor_sync(full, h, o);
+      l = l2 < l ? l2 : l;
+      h = h2 > h ? h2 : h;
     }
-  } else if (A.cur_p >= 0) {
-    atomic_min_i64(&lo_out[A.cur_p], A.lo);
-    atomic_max_i64(&hi_out[A.cur_p], A.hi);
-    if (A.cur_pops) atomicAdd(&pid_ops[A.cur_p], A.cur_pops);
-  }
-  {  // running per-group op count
-    const int gk = A.cur_gops ? A.cur_g : -1;
-    const int g0 = __shfl_sync(full, gk, 0);
-    if (__all_sync(full, gk == g0)) {
-      const long long go = warp_sum(A.cur_gops);
-      if (lane == 0 && g0 >= 0 && go) atomicAdd(&group_ops[g0], (int)go);
-    } else if (gk >= 0) {
-      atomicAdd(&group_ops[gk], A.cur_gops);
+    const long long po = warp_sum(A.cur_pops);
+    if (lane == 0) {
+      s_wp[warp] = p0;
+      s_wl[warp] = l;
+      s_wh[warp] = h;
+      s_wo[warp] = po;
+    }
+  } else {
+    if (lane == 0) s_wp[warp] = -1;
+    if (A.cur_p >= 0) {
+      atomic_min_i64(&lo_out[A.cur_p], A.lo);
+      atomic_max_i64(&hi_out[A.cur_p], A.hi);
+      if (A.cur_pops) atomicAdd(&pid_ops[A.cur_p], A.cur_pops);
     }
   }
-  // packed counters: warp sums, then lane q unpacks counter q into shared memory
-  const unsigned long long w0 = warp_sum_u64(A.cat_all0), w1 = warp_sum_u64(A.cat_all1),
-                           w2 = warp_sum_u64(A.cat_nz0), w3 = warp_sum_u64(A.cat_nz1), w4 = warp_sum_u64(A.cnt0),
-                           w5 = warp_sum_u64(A.cnt1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int cp = -1;
+    long long cl = 0, ch = 0, co = 0;
+    for (int w = 0; w <= XS_BLOCK / 32; w++) {
+      const int wp = w < XS_BLOCK / 32 ? s_wp[w] : -2;
+      if (wp != cp || w == XS_BLOCK / 32) {
+        if (cp >= 0) {
+          atomic_min_i64(&lo_out[cp], cl);
+          atomic_max_i64(&hi_out[cp], ch);
+          if (co) atomicAdd(&pid_ops[cp], (int)co);
+        }
+        cp = wp;
+        if (wp >= 0) cl = s_wl[w], ch = s_wh[w], co = s_wo[w];
+      } else if (wp >= 0) {
+        cl = s_wl[w] < cl ? s_wl[w] : cl;
+        ch = s_wh[w] > ch ? s_wh[w] : ch;
+        co += s_wo[w];
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; q++) {  // group op counts: one add per distinct group per warp
+    const int gk = A.gc[q] ? A.gk[q] : -1;
+    const unsigned act = __ballot_sync(full, gk >= 0);
+    if (gk >= 0) {
+      const unsigned peers = __match_any_sync(act, gk);
+      const int sum = (int)__reduce_add_sync(peers, (unsigned)A.gc[q]);
+      if (lane == __ffs(peers) - 1) atomicAdd(&group_ops[gk], sum);
+    }
+  }
   long long bad_api = A.bad_api;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     const long long b2 = __shfl_xor_sync(full, bad_api, o);
     bad_api = b2 < bad_api ? b2 : bad_api;
-  }
-  __syncthreads();  // s_cnt initialised
-  if (lane < 19) {
-    // counter layout: 0-5 cat_all, 6-11 cat_nz, 12-15 cnt0 lanes, 16-18 cnt1 lanes
-    const unsigned long long word = lane < 4 ? w0 : lane < 6 ? w1 : lane < 10 ? w2 : lane < 12 ? w3 : lane < 16 ? w4 : w5;
-    const int sub = lane < 6 ? (lane & 3) : lane < 12 ? ((lane - 6) & 3) : lane < 16 ? lane - 12 : lane - 16;
-    const unsigned long long x = (word >> (16 * sub)) & 0xFFFFull;
-    if (x) atomicAdd(&s_cnt[lane], x);
   }
   if (lane == 0 && bad_api != INT64_MAX) atomicMin(&s_bad_api, bad_api);
   __syncthreads();
@@ -358,13 +428,16 @@ int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool che
     const uint8_t* hasint = (check_api && prof) ? prof->has_internal : nullptr;
     int check = (check_api && prof && ev->n_names > 0 && hasint) ? 1 : 0;
     if (check_api && prof && !hasint) check = 0;
+    const int p1_grid = std::min(grid_for(n, XS_BLOCK * P1_ITEMS), 148 * 8);  // persistent CTAs
     const bool vec = ((uintptr_t)v.start % 16 == 0) && ((uintptr_t)v.dur % 16 == 0) &&
-                     ((uintptr_t)ev->pid % 16 == 0) && ((uintptr_t)ev->cat % 4 == 0);
+                     ((uintptr_t)ev->pid % 16 == 0) && ((uintptr_t)ev->cat % 4 == 0) &&
+                     ((uintptr_t)ev->tid % 16 == 0) && ((uintptr_t)ev->name % 16 == 0) &&
+                     ((uintptr_t)ev->has_corr % 4 == 0);
     if (vec)
-      XS_LAUNCH(ctx, k_pass1<true>, grid_for(n, XS_BLOCK * P1_ITEMS), XS_BLOCK, 0, s, v, n, ev->pid_has_meta, hasint,
+      XS_LAUNCH(ctx, k_pass1<true>, p1_grid, XS_BLOCK, 0, s, v, n, ev->pid_has_meta, hasint,
                 check, st, lo, hi, pid_ops, group_ops);
     else
-      XS_LAUNCH(ctx, k_pass1<false>, grid_for(n, XS_BLOCK * P1_ITEMS), XS_BLOCK, 0, s, v, n, ev->pid_has_meta,
+      XS_LAUNCH(ctx, k_pass1<false>, p1_grid, XS_BLOCK, 0, s, v, n, ev->pid_has_meta,
                 hasint, check, st, lo, hi, pid_ops, group_ops);
   }
   XS_LAUNCH(ctx, k_pid_finish, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, np, ev->group_pid, group_ops, ng,
