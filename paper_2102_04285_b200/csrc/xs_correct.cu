@@ -443,29 +443,61 @@ __global__ void k_zero_pad(Stats* st) {  // the two span totals (pad[3] is the s
   if (threadIdx.x < 2) st->pad[1 + threadIdx.x] = 0;
 }
 
-// corrected per-pid spans (pid_spans(out), correction.py:184-185)
+// corrected per-pid spans (pid_spans(out), correction.py:184-185): warp
+// then block aggregation, one min/max atomic pair per pid per block
 __global__ void k_out_spans(const int32_t* pid, int64_t n, const int64_t* s, const int64_t* d, int64_t* lo2,
                             int64_t* hi2) {
+  constexpr int NW = XS_BLOCK / 32;
+  __shared__ int s_p[NW];
+  __shared__ int64_t s_a[NW], s_b[NW];
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int p = i < n ? pid[i] : -1;
   int64_t a = i < n ? s[i] : INT64_MAX;
   int64_t b = i < n ? s[i] + d[i] : INT64_MIN;
-  int p0 = __shfl_sync(full, p, 0);
-  if (__all_sync(full, p == p0)) {
+  const int lane0_p = __shfl_sync(full, p, 0);
+  const int pv = p >= 0 ? p : lane0_p;  // (tail lanes join their warp's pid)
+  const int p0 = __shfl_sync(full, pv, 0);
+  if (__all_sync(full, pv == p0)) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       int64_t a2 = __shfl_xor_sync(full, a, o), b2 = __shfl_xor_sync(full, b, o);
       a = a2 < a ? a2 : a;
       b = b2 > b ? b2 : b;
     }
-    if ((threadIdx.x & 31) == 0 && p0 >= 0) {
-      atomic_min_i64(&lo2[p0], a);
-      atomic_max_i64(&hi2[p0], b);
+    if (lane == 0) {
+      s_p[warp] = p0;
+      s_a[warp] = a;
+      s_b[warp] = b;
     }
-  } else if (p >= 0) {
-    atomic_min_i64(&lo2[p], a);
-    atomic_max_i64(&hi2[p], b);
+  } else {
+    if (lane == 0) s_p[warp] = -1;
+    if (p >= 0) {
+      atomic_min_i64(&lo2[p], a);
+      atomic_max_i64(&hi2[p], b);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int cp = -1;
+    int64_t ca = INT64_MAX, cb = INT64_MIN;
+    for (int w = 0; w <= NW; w++) {
+      const int wp = w < NW ? s_p[w] : -2;
+      if (wp != cp) {
+        if (cp >= 0) {
+          atomic_min_i64(&lo2[cp], ca);
+          atomic_max_i64(&hi2[cp], cb);
+        }
+        cp = wp;
+        ca = INT64_MAX;
+        cb = INT64_MIN;
+      }
+      if (wp >= 0) {
+        ca = s_a[w] < ca ? s_a[w] : ca;
+        cb = s_b[w] > cb ? s_b[w] : cb;
+      }
+    }
   }
 }
 

@@ -77,6 +77,8 @@ __global__ void k_union_reduce(const uint64_t* keys, const int* depth, int64_t m
                                int64_t* iv_lo, int64_t* iv_hi) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   long long util = 0, nint = 0;
+  int seg_k = -1;
+  long long seg_v[1] = {0};
   if (i < m) {
     const uint64_t k = keys[i];
     const uint64_t tmask = tb >= 63 ? ~0ull : ((1ull << (tb + 1)) - 1);
@@ -87,7 +89,10 @@ __global__ void k_union_reduce(const uint64_t* keys, const int* depth, int64_t m
       const uint64_t kn = keys[i + 1];
       const int segn = per_pid ? (int)(kn >> (tb + 1)) : 0;
       const int64_t tn = (int64_t)((kn & tmask) >> 1);
-      if (segn == seg && tn > t) atomicAdd(&seg_ns[seg], (unsigned long long)(tn - t));
+      if (segn == seg && tn > t) {
+        seg_k = seg;
+        seg_v[0] = tn - t;
+      }
     }
     if (!per_pid) {
       const int dp = i > 0 ? depth[i - 1] : 0;
@@ -110,6 +115,10 @@ __global__ void k_union_reduce(const uint64_t* keys, const int* depth, int64_t m
       }
     }
   }
+  // one add per segment per block (segments are contiguous in key order)
+  block_keyed_flush<1>(seg_k, seg_v, [&](int k, const long long* x) {
+    if (x[0]) atomicAdd(&seg_ns[k], (unsigned long long)x[0]);
+  });
   typedef cub::BlockReduce<long long, XS_BLOCK> BR;
   __shared__ typename BR::TempStorage tmp;
   const long long u = BR(tmp).Sum(util);
