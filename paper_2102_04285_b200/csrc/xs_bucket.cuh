@@ -60,7 +60,10 @@ __device__ __forceinline__ int64_t bucket_slot(unsigned* counts, const int64_t* 
 }
 
 // buckets ~ one per key over the occupied key space (SURVEY 8d key layout)
-inline int bucket_bits_for(int64_t nkeys, int key_bits) {
+// max_bits: the record sorts stay at 2^24 buckets (their offsets scan would
+// outweigh the smaller in-chunk ranks); the endpoint sort, whose per-chunk
+// rank is the sweep's hot phase, goes to 2^26 (<= 768 MB of tables)
+inline int bucket_bits_for(int64_t nkeys, int key_bits, int max_bits = 24) {
   static int adj = [] {
     const char* e = getenv("XS_BK_BITS_ADJ");  // (tuning experiments)
     return e ? atoi(e) : 1;
@@ -69,7 +72,7 @@ inline int bucket_bits_for(int64_t nkeys, int key_bits) {
   while (b < 62 && ((int64_t)1 << b) < nkeys) b++;
   b += adj;
   if (b < 10) b = 10;
-  if (b > 24) b = 24;
+  if (b > max_bits) b = max_bits;
   return b < key_bits ? b : key_bits;
 }
 

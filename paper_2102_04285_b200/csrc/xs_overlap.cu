@@ -841,7 +841,7 @@ static int bucket_prepare(xs_ctx* ctx, const EventView& v, const int64_t* lo, in
                           const uint64_t* extra, int64_t n_extra, int64_t nvalid, int key_bits, cudaStream_t s,
                           BkPlan* plan) {
   const int64_t n = v.ev.n;
-  const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(nvalid, key_bits));
+  const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(nvalid, key_bits, 26));
   unsigned* counts;
   int64_t *offs, *chunk;
   uint64_t* keys;
