@@ -345,8 +345,17 @@ __device__ __forceinline__ uint64_t corr_hash(int p, int64_t corr) {
   return x;
 }
 
-__global__ void k_corr_insert(EventView v, int64_t n, int* state, int64_t* key, int* kpid, int64_t* kstart,
-                              uint64_t mask, Stats* st) {
+// One 32-byte slot per entry (one DRAM sector per probe: key, pid, claim
+// state and the min launch start live together).
+struct __align__(32) CorrSlot {
+  int64_t key;
+  int64_t start;
+  int pid;
+  int state;  // 0 empty, 1 being claimed, 2 published
+  int64_t pad;
+};
+
+__global__ void k_corr_insert(EventView v, int64_t n, CorrSlot* tab, uint64_t mask, Stats* st) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (v.ev.cat[i] != 4 || !v.ev.has_corr[i]) return;
@@ -355,23 +364,24 @@ __global__ void k_corr_insert(EventView v, int64_t n, int* state, int64_t* key, 
   int64_t s = v.start[i];
   uint64_t h = corr_hash(p, corr) & mask;
   for (uint64_t probe = 0; probe <= mask; probe++) {
-    volatile int* sp = state + h;
+    CorrSlot* e = tab + h;
+    volatile int* sp = &e->state;
     int cur = *sp;
     if (cur == 0) {
-      if (atomicCAS(state + h, 0, 1) == 0) {
-        key[h] = corr;
-        kpid[h] = p;
-        kstart[h] = s;
+      if (atomicCAS(&e->state, 0, 1) == 0) {
+        e->key = corr;
+        e->pid = p;
+        e->start = s;
         __threadfence();
-        atomicExch(state + h, 2);
+        atomicExch(&e->state, 2);
         return;
       }
       cur = *sp;
     }
     while (cur == 1) cur = *sp;
     __threadfence();
-    if (((volatile int64_t*)key)[h] == corr && ((volatile int*)kpid)[h] == p) {
-      atomic_min_i64(&kstart[h], s);
+    if (((volatile int64_t*)&e->key)[0] == corr && ((volatile int*)&e->pid)[0] == p) {
+      atomic_min_i64(&e->start, s);
       return;
     }
     h = (h + 1) & mask;
@@ -380,8 +390,8 @@ __global__ void k_corr_insert(EventView v, int64_t n, int* state, int64_t* key, 
 }
 
 // GPU events: dangling check; in CORRELATION mode record the launch instant
-__global__ void k_corr_query(EventView v, int64_t n, const int* state, const int64_t* key, const int* kpid,
-                             const int64_t* kstart, uint64_t mask, Stats* st, int64_t* launch_start) {
+__global__ void k_corr_query(EventView v, int64_t n, const CorrSlot* tab, uint64_t mask, Stats* st,
+                             int64_t* launch_start) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (v.ev.cat[i] != 5) return;
@@ -393,9 +403,10 @@ __global__ void k_corr_query(EventView v, int64_t n, const int* state, const int
   int64_t corr = v.ev.corr[i];
   uint64_t h = corr_hash(p, corr) & mask;
   for (uint64_t probe = 0; probe <= mask; probe++) {
-    if (state[h] == 0) break;
-    if (key[h] == corr && kpid[h] == p) {
-      if (launch_start) launch_start[i] = kstart[h];
+    const CorrSlot e = tab[h];
+    if (e.state == 0) break;
+    if (e.key == corr && e.pid == p) {
+      if (launch_start) launch_start[i] = e.start;
       return;
     }
     h = (h + 1) & mask;
@@ -464,17 +475,13 @@ int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
   if (ngpu == 0) return XS_OK;
   uint64_t cap = 64;
   while (cap < (uint64_t)(2 * napi + 2)) cap <<= 1;
-  int *state, *kpid;
-  int64_t *key, *kstart;
-  XS_TRY(ws(ctx, W_CORR_STATE, cap, s, &state));
-  XS_TRY(ws(ctx, W_CORR_KEY, cap, s, &key));
-  XS_TRY(ws(ctx, W_CORR_PID, cap, s, &kpid));
-  XS_TRY(ws(ctx, W_CORR_START, cap, s, &kstart));
-  XS_CUDA(cudaMemsetAsync(state, 0, cap * sizeof(int), s));
+  CorrSlot* tab;
+  XS_TRY(ws(ctx, W_CORR_STATE, cap, s, &tab));
+  XS_CUDA(cudaMemsetAsync(tab, 0, cap * sizeof(CorrSlot), s));
   int64_t* launch = nullptr;
   XS_TRY(ws(ctx, W_FIXED_LS, n + 1, s, &launch));
-  if (napi) XS_LAUNCH(ctx, k_corr_insert, grid_for(n), XS_BLOCK, 0, s, v, n, state, key, kpid, kstart, cap - 1, st);
-  XS_LAUNCH(ctx, k_corr_query, grid_for(n), XS_BLOCK, 0, s, v, n, state, key, kpid, kstart, cap - 1, st, launch);
+  if (napi) XS_LAUNCH(ctx, k_corr_insert, grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st);
+  XS_LAUNCH(ctx, k_corr_query, grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st, launch);
   return XS_OK;
 }
 
