@@ -433,7 +433,8 @@ def run_ours(args):
             "e2e": {"value": round(total_events / (e2e_step / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_step, 3),
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
                     "path": "analyze_columnar(pinned host columns): H2D -> xs_analyze_to_host (corrected columns D2H "
-                            "overlapped with the overlap pass) -> D2H cells -> Breakdown"},
+                            "overlapped with the overlap pass) -> D2H cell arrays -> Breakdown (spans/untracked "
+                            "decoded; the cells dict of OverlapKeys is built on first access)"},
             "gpu_launches": int(launches / args.steps),
             "roofline": roof, "pipeline_roofline": pipeline, "stages_ms": stages,
             "cpu_baseline": cpu, "clocks": clocks.summary(), **check,

@@ -60,13 +60,45 @@ class OverlapKey(tuple):
         return "/".join(self.path) if self.path else "-"
 
 
-@dataclass
 class Breakdown:
-    """Accumulated ns per (pid, operation path, category set) (overlap.py:61-77)."""
+    """Accumulated ns per (pid, operation path, category set) (overlap.py:61-77).
 
-    cells: dict = field(default_factory=dict)
-    spans: dict = field(default_factory=dict)
-    untracked: dict = field(default_factory=dict)
+    Same fields and methods as the reference's dataclass.  A Breakdown decoded
+    from a device result keeps the cell arrays and builds the ``cells`` dict
+    of OverlapKeys on first access: millions of deep-path cells (config 5)
+    cost seconds of Python object construction, which callers that only read
+    spans / untracked / the raw arrays never pay.
+    """
+
+    __slots__ = ("_cells", "_lazy", "spans", "untracked")
+
+    def __init__(self, cells=None, spans=None, untracked=None):
+        self._cells = {} if cells is None else cells
+        self._lazy = None
+        self.spans = {} if spans is None else spans
+        self.untracked = {} if untracked is None else untracked
+
+    @property
+    def cells(self) -> dict:
+        if self._lazy is not None:
+            build, self._lazy = self._lazy, None
+            self._cells = build()
+        return self._cells
+
+    @cells.setter
+    def cells(self, value: dict) -> None:
+        self._lazy = None
+        self._cells = value
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, Breakdown):
+            return NotImplemented
+        return self.cells == other.cells and self.spans == other.spans and self.untracked == other.untracked
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        return f"Breakdown(cells={self.cells!r}, spans={self.spans!r}, untracked={self.untracked!r})"
 
     def span_ns(self, pid: int) -> int:
         lo, hi = self.spans[pid]
@@ -135,14 +167,42 @@ def decode_paths(ct: ColumnarTrace, parents: np.ndarray, names: np.ndarray, need
     return paths
 
 
-def decode_breakdown(ct: ColumnarTrace, raw) -> Breakdown:
-    bd = Breakdown()
+def decode_breakdown(ct: ColumnarTrace, raw, lazy: bool = True) -> Breakdown:
+    """Breakdown of a device overlap result; the cells dict is built on first
+    access unless ``lazy`` is False."""
+    bd = _decode_breakdown(ct, raw)
+
+    def build():
+        # millions of small tuples: keep the cyclic GC from rescanning the
+        # growing heap during the bulk build (they hold no cycles)
+        import gc
+        was = gc.isenabled()
+        gc.disable()
+        try:
+            return _decode_cells(ct, raw)
+        finally:
+            if was:
+                gc.enable()
+
+    if lazy and raw.cell_ns.shape[0] > 4096:
+        bd._lazy = build
+    else:
+        bd.cells = build()
+    return bd
+
+
+def _decode_cells(ct: ColumnarTrace, raw) -> dict:
     paths = decode_paths(ct, raw.node_parent, raw.node_name)
     pids = ct.pids.tolist()
     mk = tuple.__new__
     pv = [pids[p] for p in raw.cell_pid.tolist()] if len(pids) != 1 else [pids[0]] * raw.cell_pid.shape[0]
-    bd.cells = dict(zip((mk(OverlapKey, (p, paths[nd], _MASK_CATS[m])) for p, nd, m in
-                         zip(pv, raw.cell_node.tolist(), raw.cell_mask.tolist())), raw.cell_ns.tolist()))
+    return dict(zip((mk(OverlapKey, (p, paths[nd], _MASK_CATS[m])) for p, nd, m in
+                     zip(pv, raw.cell_node.tolist(), raw.cell_mask.tolist())), raw.cell_ns.tolist()))
+
+
+def _decode_breakdown(ct: ColumnarTrace, raw) -> Breakdown:
+    bd = Breakdown()
+    pids = ct.pids.tolist()
     for p in range(ct.n_pids):
         if raw.has_events[p]:
             lo, hi = int(raw.span_lo[p]), int(raw.span_hi[p])
