@@ -12,6 +12,7 @@ from .correction import (
     CorrectionReport,
     UncalibratedHookError,
     analyze_columnar,
+    analyze_columnar_pipelined,
     correct_trace,
     correct_trace_columnar,
     correction_bias,
@@ -62,6 +63,7 @@ from .overlap import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "analyze_columnar_pipelined",
     "IncompleteTraceError",
     "TraceFormatError",
     "TruncatedTraceError",

@@ -135,6 +135,7 @@ class Engine:
         self.lib = _lib.load()
         self.device = device
         self._prof_cache = None
+        self.fetched_bytes = 0  # D2H bytes of overlap results read back (bench accounting)
         h = C.c_void_p()
         st = self.lib.xs_ctx_create(device, C.byref(h))
         if st != 0:
@@ -195,6 +196,8 @@ class Engine:
         self.check(self.lib.xs_overlap_fetch(self.ctx, p(r.cell_pid), p(r.cell_node), p(r.cell_mask), p(r.cell_ns),
                                              p(r.node_parent), p(r.node_name), p(r.span_lo), p(r.span_hi),
                                              p(r.tracked), p(r.has_events), self.stream()), "xs_overlap_fetch")
+        self.fetched_bytes += sum(a.nbytes for a in (r.cell_pid, r.cell_node, r.cell_mask, r.cell_ns, r.node_parent,
+                                                     r.node_name, r.span_lo, r.span_hi, r.tracked, r.has_events))
         return r
 
     def _profile(self, dt: DeviceTrace, scaled):

@@ -159,3 +159,118 @@ def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution
     if out is not None:
         return out[0], out[1], _report(ct, raw), bd
     return raw.start, raw.dur, _report(ct, raw), bd
+
+
+def _pid_batches(ct: ColumnarTrace, batches: int) -> list:
+    """Contiguous row ranges holding whole pids (pid column non-decreasing),
+    about n / batches rows each; [] when the rows are not pid-contiguous."""
+    if ct.n == 0 or ct.n_pids < 2:
+        return []
+    memo = ct.__dict__.get("_pid_starts")  # (checked once per trace object)
+    if memo is None:
+        contiguous = not np.any(ct.pid[1:] < ct.pid[:-1])
+        memo = np.searchsorted(ct.pid, np.arange(ct.n_pids + 1, dtype=np.int32)) if contiguous else False
+        ct.__dict__["_pid_starts"] = memo
+    if memo is False:
+        return []
+    starts = memo  # first row of every pid
+    cuts = [0]
+    for b in range(1, batches):
+        r = int(starts[np.searchsorted(starts, b * ct.n // batches)])  # next pid boundary
+        if cuts[-1] < r < ct.n:
+            cuts.append(r)
+    cuts.append(ct.n)
+    return list(zip(cuts[:-1], cuts[1:]))
+
+
+def _row_slice(ct: ColumnarTrace, a: int, b: int) -> ColumnarTrace:
+    """Rows [a, b) with every table kept (pid/tid/name indices stay valid);
+    pinned columns stay pinned (views)."""
+    pin = None
+    if ct._pinned is not None:
+        pin = {k: (t[a:b] if k in ("start", "dur", "pid", "tid", "cat", "name", "corr", "has_corr") else t)
+               for k, t in ct._pinned.items()}
+    return ColumnarTrace(ct.clock_domain, ct.start[a:b], ct.dur[a:b], ct.pid[a:b], ct.tid[a:b], ct.cat[a:b],
+                         ct.name[a:b], ct.corr[a:b], ct.has_corr[a:b], ct.pids, ct.group_pid, ct.group_tid, ct.names,
+                         ct.processes, ct.pid_has_meta, None, pin)
+
+
+def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, out, attribution=None,
+                               batches: int = 8):
+    """analyze_columnar for host-resident traces of many processes, with the
+    upload of the next batch of pids overlapping the analysis of the current
+    one (per-pid independence: overlap.py:126, correction.py:132).  Needs
+    pid-contiguous rows (e.g. ``synth``/per-process ingest) and host output
+    buffers ``out`` = (start, dur); falls back to one call otherwise.
+    Returns (start, dur, report, Breakdown) like analyze_columnar."""
+    import torch
+
+    from .overlap import Attribution, _decode_breakdown, _decode_cells
+
+    parts = _pid_batches(ct, batches)
+    # a dominant pid (skewed traces) leaves nothing to overlap: one call is cheaper
+    if len(parts) < 2 or max(b - a for a, b in parts) > 0.4 * ct.n:
+        return analyze_columnar(ct, profile, attribution, out=out)
+    if meta_violations(ct.processes):
+        raise InvalidTraceError(format_violations(ct.to_trace()))
+    attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
+    eng = _engine.get()
+    dev = torch.device("cuda", eng.device)
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    scaled = profile.scaled(ct.names)
+    scaled.check_int128(3 * ct.n + 8)
+    subs = [_row_slice(ct, a, b) for a, b in parts]
+    starts = ct.__dict__["_pid_starts"]
+    has = starts[1:] > starts[:-1]
+    for sub, (a, b) in zip(subs, parts):  # pids present in each batch, from the pid row ranges
+        sub.__dict__["_present_mask"] = has & (starts[:-1] >= a) & (starts[:-1] < b)
+
+    def upload(k):
+        with torch.cuda.stream(copy):
+            dt = _engine.DeviceTrace(subs[k], eng.device, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        return dt, ev
+
+    rep = CorrectionReport()
+    bd_all = None
+    raws = []
+    nxt = upload(0)
+    for k, (a, b) in enumerate(parts):
+        dt, ev = nxt
+        compute.wait_event(ev)
+        if k + 1 < len(parts):
+            nxt = upload(k + 1)  # overlaps the analysis below
+        try:
+            raw = eng.correct(dt, scaled, attr, host_out=(out[0][a:b], out[1][a:b]))
+        except _engine.UncalibratedEvent as exc:
+            name = ct.names[int(subs[k].name[exc.index])]
+            raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile") from None
+        except _engine.XsError as exc:
+            if exc.status == _lib.XS_INVALID_TRACE:
+                raise InvalidTraceError(format_violations(ct.to_trace())) from None
+            raise
+        r = _report(subs[k], raw)
+        rep.removed_ns.update(r.removed_ns)
+        rep.shortfall_ns.update(r.shortfall_ns)
+        rep.original_total_ns += r.original_total_ns
+        rep.corrected_total_ns += r.corrected_total_ns
+        ov = eng.fetch_overlap()
+        raws.append((subs[k], ov))
+        bd = _decode_breakdown(subs[k], ov)
+        if bd_all is None:
+            bd_all = bd
+        else:
+            bd_all.spans.update(bd.spans)
+            bd_all.untracked.update(bd.untracked)
+        del dt
+
+    def build():  # the cells dict, on first access (pids are disjoint across batches)
+        cells = {}
+        for sub, ov in raws:
+            cells.update(_decode_cells(sub, ov))
+        return cells
+
+    bd_all._lazy = build
+    return out[0], out[1], rep, bd_all

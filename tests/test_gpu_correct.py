@@ -204,3 +204,23 @@ def test_analyze_to_host_pinned_matches_device_outputs():
         s2, d2, rep2, bd2 = analyze_columnar(pin, synth.exact_profile(), out=(hs, hd))
         assert s2 is hs and np.array_equal(hs.numpy(), s.cpu().numpy()) and np.array_equal(hd.numpy(), un.dur)
         assert bd2.cells == bd.cells and rep2.removed_ns == rep.removed_ns
+
+
+def test_pipelined_analyze_equals_one_call():
+    """analyze_columnar_pipelined (pid batches, next upload overlapping the
+    current analysis) returns exactly analyze_columnar's results."""
+    import torch
+    from paper_2102_04285_b200 import analyze_columnar, analyze_columnar_pipelined
+
+    for ct, prof in ((synth.config3_trace(processes=7, events_per_pid=30_000), synth.exact_profile()),
+                     (synth.adversarial_trace(150_000, pids=12), synth.adversarial_profile())):
+        s0, d0, rep0, bd0 = analyze_columnar(ct, prof)
+        pin = ct.pinned()
+        hs = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+        hd = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+        s1, d1, rep1, bd1 = analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=4)
+        assert np.array_equal(hs.numpy(), s0.cpu().numpy()) and np.array_equal(hd.numpy(), d0.cpu().numpy())
+        assert rep1.removed_ns == rep0.removed_ns and rep1.shortfall_ns == rep0.shortfall_ns
+        assert rep1.original_total_ns == rep0.original_total_ns
+        assert rep1.corrected_total_ns == rep0.corrected_total_ns
+        assert bd1 == bd0
