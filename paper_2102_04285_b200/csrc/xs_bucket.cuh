@@ -19,7 +19,10 @@
 namespace xs {
 
 constexpr int BK_THREADS = 256;
-constexpr int BK_ITEMS = 16;
+#ifndef XS_BK_ITEMS
+#define XS_BK_ITEMS 16
+#endif
+constexpr int BK_ITEMS = XS_BK_ITEMS;
 constexpr int BK_CAP = BK_THREADS * BK_ITEMS;  // keys per chunk tile
 constexpr int BK_T = BK_CAP / 2;                // chunk split granule (max bucket)
 constexpr int BK_RANK_MAX = 64;                 // buckets up to this size are ranked by direct comparison

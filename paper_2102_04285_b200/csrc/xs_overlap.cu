@@ -591,7 +591,10 @@ __device__ __forceinline__ SwState sw_identity() {
 // never waits on a sort.  Every interval [t_prev, t) is accounted by the first
 // endpoint of the run at t with the state after everything up to t_prev;
 // across chunk boundaries t_prev and that state come from the look-back.
-__global__ void __launch_bounds__(BK_THREADS, 3) k_bk_sweep(
+#ifndef XS_SWEEP_MINB
+#define XS_SWEEP_MINB 4  // 4 CTAs per SM (64 registers, small spills): more chunks in flight
+#endif
+__global__ void __launch_bounds__(BK_THREADS, XS_SWEEP_MINB) k_bk_sweep(
     const uint64_t* __restrict__ keys, int64_t total, const int64_t* __restrict__ chunk, int shift, int tb,
     const int* __restrict__ pidpath, const int64_t* __restrict__ opbase, int n_nodes,
     GHist hist, TileDesc<SwState>* desc, int* flags, int* tile_ctr, Stats* st,
