@@ -51,57 +51,71 @@ def local_cells(ct: ColumnarTrace, raw) -> tuple:
     return rows, per_pid
 
 
+_TABLES = {"paths": (), "pids": ()}  # global path / pid tables agreed by earlier merges (identical on all ranks)
+
+
 def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
-    """Merge every rank's overlap result into one Breakdown (all ranks get it)."""
+    """Merge every rank's overlap result into one Breakdown (all ranks get it).
+
+    Path ids are per-rank trie nodes, so ranks agree on a global table of path
+    tuples (and pid values).  The table is cached across calls: once every
+    rank's paths are in it (one MIN all-reduce of a flag says so) a merge is
+    two tensor collectives -- SUM of the dense histogram + tracked, MIN of
+    (lo, -hi) -- and no object all-gather.  Integer sums commute, so the
+    merge is bit-exact."""
     import torch
     import torch.distributed as dist
 
     rows, per_pid = local_cells(ct, raw)
     world = dist.get_world_size() if dist.is_initialized() else 1
-    # global tables: pid values and path tuples (tiny; object all-gather)
-    mine = (sorted({r[1] for r in rows}), sorted(per_pid))
-    gathered = [None] * world
+    my_paths = {r[1] for r in rows} | {()}
+    my_pids = set(per_pid)
+    known = my_paths <= set(_TABLES["paths"]) and my_pids <= set(_TABLES["pids"])
     if world > 1:
-        dist.all_gather_object(gathered, mine)
-    else:
-        gathered = [mine]
-    all_paths = sorted({p for g in gathered for p in g[0]} | {()})
-    all_pids = sorted({p for g in gathered for p in g[1]})
+        flag = torch.tensor([1 if known else 0], dtype=torch.int64, device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        known = bool(flag.item())
+    if not known:  # grow the tables (first merge, or new paths): tiny object all-gather
+        mine = (sorted(my_paths), sorted(my_pids))
+        gathered = [None] * world
+        if world > 1:
+            dist.all_gather_object(gathered, mine)
+        else:
+            gathered = [mine]
+        _TABLES["paths"] = tuple(sorted(set(_TABLES["paths"]) | {p for g in gathered for p in g[0]}))
+        _TABLES["pids"] = tuple(sorted(set(_TABLES["pids"]) | {p for g in gathered for p in g[1]}))
+    all_paths, all_pids = _TABLES["paths"], _TABLES["pids"]
     path_ix = {p: i for i, p in enumerate(all_paths)}
     pid_ix = {p: i for i, p in enumerate(all_pids)}
     P, Q = len(all_pids), len(all_paths)
-    hist = torch.zeros(P * Q * 32, dtype=torch.int64, device=device)
+    # one SUM buffer: histogram [pid][path][32] then tracked[pid]; one MIN buffer: lo[pid] then -hi[pid]
+    sums = np.zeros(P * Q * 32 + P, np.int64)
+    mins = np.full(2 * max(P, 1), np.iinfo(np.int64).max, np.int64)
     if rows:
-        idx = torch.tensor([(pid_ix[r[0]] * Q + path_ix[r[1]]) * 32 + r[2] for r in rows], dtype=torch.int64)
-        val = torch.tensor([r[3] for r in rows], dtype=torch.int64)
-        hist.index_add_(0, idx.to(device), val.to(device))
-    span = torch.full((2, max(P, 1)), 0, dtype=torch.int64, device=device)
-    lo = torch.full((max(P, 1),), 2**63 - 1, dtype=torch.int64)
-    hi = torch.full((max(P, 1),), -(2**63), dtype=torch.int64)
-    tracked = torch.zeros(max(P, 1), dtype=torch.int64)
+        idx = np.array([(pid_ix[r[0]] * Q + path_ix[r[1]]) * 32 + r[2] for r in rows], np.int64)
+        np.add.at(sums, idx, np.array([r[3] for r in rows], np.int64))
     for pv, (a, b, t) in per_pid.items():
-        lo[pid_ix[pv]] = a
-        hi[pid_ix[pv]] = b
-        tracked[pid_ix[pv]] = t
-    lo, hi, tracked = lo.to(device), hi.to(device), tracked.to(device)
+        k = pid_ix[pv]
+        sums[P * Q * 32 + k] += t
+        mins[k] = a
+        mins[max(P, 1) + k] = -b
     if world > 1:
-        dist.all_reduce(hist, op=dist.ReduceOp.SUM)
-        dist.all_reduce(tracked, op=dist.ReduceOp.SUM)
-        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
-    del span
-    h = hist.cpu().numpy()
-    lo_n, hi_n, tr_n = lo.cpu().numpy(), hi.cpu().numpy(), tracked.cpu().numpy()
+        ts = torch.from_numpy(sums).to(device)
+        tm = torch.from_numpy(mins).to(device)
+        dist.all_reduce(ts, op=dist.ReduceOp.SUM)
+        dist.all_reduce(tm, op=dist.ReduceOp.MIN)
+        sums, mins = ts.cpu().numpy(), tm.cpu().numpy()
     bd = Breakdown()
-    nz = np.nonzero(h)[0]
-    for i in nz.tolist():
-        m = i & 31
-        row = i >> 5
-        p, q = divmod(row, Q)
-        bd.cells[OverlapKey(all_pids[p], all_paths[q], _MASK_CATS[m])] = int(h[i])
+    h = sums[: P * Q * 32]
+    for i in np.nonzero(h)[0].tolist():
+        p, q = divmod(i >> 5, Q)
+        bd.cells[OverlapKey(all_pids[p], all_paths[q], _MASK_CATS[i & 31])] = int(h[i])
     for k, pv in enumerate(all_pids):
-        bd.spans[pv] = (int(lo_n[k]), int(hi_n[k]))
-        bd.untracked[pv] = int(hi_n[k] - lo_n[k]) - int(tr_n[k])
+        lo, hi = int(mins[k]), -int(mins[max(P, 1) + k])
+        if lo == np.iinfo(np.int64).max:
+            continue  # (a pid in the table that no rank has events for)
+        bd.spans[pv] = (lo, hi)
+        bd.untracked[pv] = (hi - lo) - int(sums[P * Q * 32 + k])
     return bd
 
 

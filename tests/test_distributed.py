@@ -71,6 +71,8 @@ def _worker(rank, world, port, attr, q):
         local = ct.select_pids(shards[rank])
         raw = _raw_from_oracle(local, attr)
         bd = merge_breakdown_raw(local, raw, torch.device("cpu"))
+        bd2 = merge_breakdown_raw(local, raw, torch.device("cpu"))  # cached global tables: no object gather
+        assert bd2 == bd
         cells = {(k.pid, k.path, frozenset(int(c) for c in k.categories)): v for k, v in bd.cells.items()}
         q.put((rank, cells, bd.spans, bd.untracked, shards))
     finally:
