@@ -138,23 +138,68 @@ __device__ __forceinline__ int64_t warp_search_i64(const int64_t* a, int64_t lo,
   return bal ? lo + (__ffs(bal) - 1) : hi;
 }
 
+// 16-lane search: lanes [16h, 16h+16) of a warp search `a` together (two
+// independent searches per warp run side by side).
+template <bool kUpper>  // kUpper: first index with a[i] > x, else a[i] >= x
+__device__ __forceinline__ int64_t half_search_i64(const int64_t* a, int64_t lo, int64_t hi, int64_t x) {
+  // all 32 lanes keep calling the ballots until both halves are done
+  const int hl = threadIdx.x & 15;
+  const int sh = threadIdx.x & 16;
+  const unsigned hm = 0xFFFFu << sh;
+  while (__any_sync(0xffffffffu, hi - lo > 16)) {
+    const bool act = hi - lo > 16;
+    const int64_t step = act ? (hi - lo + 15) / 16 : 1;
+    const int64_t q = lo + hl * step;
+    const bool in = act && q < hi;
+    const int64_t av = in ? a[q] : 0;
+    const bool pred = in && (kUpper ? av > x : av >= x);
+    const unsigned bal = (__ballot_sync(0xffffffffu, pred) & hm) >> sh;
+    const unsigned inb = (__ballot_sync(0xffffffffu, in) & hm) >> sh;
+    if (act) {
+      if (bal == 0) {
+        lo = lo + (31 - __clz(inb)) * step + 1;
+      } else {
+        const int f = __ffs(bal) - 1;
+        if (f == 0) {
+          hi = lo;  // a[lo] qualifies
+        } else {
+          const int64_t nhi = lo + f * step;
+          lo = lo + (f - 1) * step + 1;
+          hi = nhi;
+        }
+      }
+    }
+  }
+  const int64_t q = lo + hl;
+  const bool pred = q < hi && (kUpper ? a[q] > x : a[q] >= x);
+  const unsigned bal = (__ballot_sync(0xffffffffu, pred) & hm) >> sh;
+  return bal ? lo + (__ffs(bal) - 1) : hi;
+}
+
 // One warp per chunk, all chunks in parallel: key range [start, end) and
 // the tight bucket range [b0, b1) (first / last nonempty bucket) so each
 // consumer CTA starts with four loads instead of serial searches.
-// offs has nb+1 entries (offs[nb] = total).
+// offs has nb+1 entries (offs[nb] = total).  The two half-warps search the
+// chunk's two granule boundaries at once, then its first / last buckets.
 static __global__ void k_bucket_chunks(const int64_t* offs, int64_t nb, int64_t n_chunks, int64_t* chunk) {
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= n_chunks) return;  // warp-uniform
   const int lane = threadIdx.x & 31;
+  const bool h1 = lane >= 16;
   const int64_t total = offs[nb];
-  const int64_t b = warp_search_i64<false>(offs, 0, nb, c * BK_T);
+  // half 0: b = first bucket with offs >= c*T; half 1: bn = first with offs >= (c+1)*T
+  const int64_t r = half_search_i64<false>(offs, 0, nb, (c + (h1 ? 1 : 0)) * BK_T);
+  const int64_t b = __shfl_sync(0xffffffffu, r, 0), bn = __shfl_sync(0xffffffffu, r, 16);
   int64_t s = -1, e = -1, b0 = 0, b1 = 0;
-  if (b < nb && offs[b] < total && offs[b] / BK_T == c) {
+  const bool live = b < nb && offs[b] < total && offs[b] / BK_T == c;  // (warp-uniform)
+  if (live) {
     s = offs[b];
-    const int64_t bn = warp_search_i64<false>(offs, b, nb, (c + 1) * BK_T);
     e = bn < nb ? offs[bn] : total;
-    b0 = warp_search_i64<true>(offs, b, nb + 1, s) - 1;   // bucket holding key s
-    b1 = warp_search_i64<true>(offs, b0, nb + 1, e - 1);  // bucket holding key e-1, plus one
+    // half 0: bucket holding key s; half 1: bucket holding key e-1, plus one
+    const int64_t r2 = h1 ? half_search_i64<true>(offs, b, nb + 1, e - 1)
+                          : half_search_i64<true>(offs, b, nb + 1, s) - 1;
+    b0 = __shfl_sync(0xffffffffu, r2, 0);
+    b1 = __shfl_sync(0xffffffffu, r2, 16);
   }
   if (lane == 0) {
     chunk[4 * c + 0] = s;
