@@ -243,6 +243,12 @@ static int bucket_sort_pairs_impl(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_
   XS_LAUNCH(ctx, k_bs_local, (int)n_chunks, BK_THREADS, sizeof(BsSmem), s, *keys_alt, *vals_alt, chunk, g.shift, *keys,
             *vals, st);
   XS_LAUNCH(ctx, k_bs_tail, 148, XS_BLOCK, 0, s, *keys_alt, *vals_alt, n, offs + g.nbuckets, *keys, *vals);
+  if (getenv("XS_DEBUG_OVF") && !ctx->capturing) {  // developer diagnostics (eager runs only)
+    long long f = 0;
+    cudaMemcpyAsync(&f, &st->pad[3], 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "bsort n=%lld key_bits=%d bb=%d overflow=%lld\n", (long long)n, key_bits, g.bb, f);
+  }
   return XS_OK;
 }
 

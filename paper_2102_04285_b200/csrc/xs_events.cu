@@ -330,6 +330,7 @@ __global__ void k_pid_finish(const int64_t* lo, const int64_t* hi, int np, const
     int cnt = 0;
     for (int g = a; g < ng && group_pid[g] == p; g++) cnt += group_ops[g] > 0;
     if (cnt > 1) atomicAdd((unsigned long long*)&st->multi_op_pids, 1ull);
+    if (cnt) atomicAdd((unsigned long long*)&st->pad[5], (unsigned long long)cnt);  // groups carrying ops
   }
 }
 

@@ -20,6 +20,7 @@
 //   4. the path of every op segment (the state after all op endpoints at one
 //      instant of a pid) is node(innermost) when one tid carries ops, or the
 //      rank-merge of every tid's chain (interned root-down) otherwise.
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -37,13 +38,26 @@ struct OpPred {
 
 // endpoint stream: slot m+j = open of op j, slot j = close of op j (op j =
 // j-th nonzero OPERATION in event order).  Key = group | t | open.
-__global__ void k_endpoints(const int* op_ev, int64_t m, EventView v, const int64_t* lo, int tb, uint64_t* keys,
-                            uint32_t* vals) {
+// (pid, tid) groups are renumbered densely over the groups that carry
+// operations (opg, order-preserving): the sort key then spends bits on the
+// few op groups, not on every GPU stream of the trace (config 5: 16k groups,
+// 256 with ops), which keeps the bucket sort's buckets fine.
+__global__ void k_op_groups(const int* group_ops, int ng, const int* opg, int* opg_inv) {
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < ng && group_ops[g] > 0) opg_inv[opg[g]] = g;
+}
+
+struct HasOps {
+  __device__ int operator()(const int& c) const { return c > 0 ? 1 : 0; }
+};
+
+__global__ void k_endpoints(const int* op_ev, int64_t m, EventView v, const int64_t* lo, int tb, const int* opg,
+                            uint64_t* keys, uint32_t* vals) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
   int i = op_ev[j];
   int p = v.ev.pid[i];
-  uint64_t g = (uint64_t)v.ev.tid[i];
+  uint64_t g = (uint64_t)opg[v.ev.tid[i]];
   uint64_t s = (uint64_t)(v.start[i] - lo[p]);
   uint64_t e = (uint64_t)(v.start[i] + v.dur[i] - lo[p]);
   keys[m + j] = (g << (tb + 1)) | (s << 1) | 1ull;
@@ -240,11 +254,12 @@ __global__ void k_pidpath_simple(const uint64_t* skeys, const uint32_t* svals, i
   pidpath[j] = ctx_node_at(skeys, svals, j, parent, node);
 }
 
-__global__ void k_pid_keys(const uint64_t* skeys, int64_t n2, const int32_t* group_pid, int tb, uint64_t* pk) {
+__global__ void k_pid_keys(const uint64_t* skeys, int64_t n2, const int32_t* group_pid, const int* opg_inv, int tb,
+                           uint64_t* pk) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n2) return;
   uint64_t k = skeys[j];
-  uint64_t g = k >> (tb + 1);
+  uint64_t g = (uint64_t)opg_inv[k >> (tb + 1)];
   uint64_t low = k & ((2ull << tb) - 1);
   pk[j] = ((uint64_t)group_pid[g] << (tb + 1)) | low;
 }
@@ -363,15 +378,22 @@ __global__ void k_opbase(const int* pid_ops, int np, int64_t* opbase) {
   }
 }
 
-__global__ void k_gs_off(const int* group_ops, int ng, int64_t* gs_off) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int64_t acc = 0;
-    for (int g = 0; g < ng; g++) {
-      gs_off[g] = acc;
-      acc += 2 * (int64_t)group_ops[g];
-    }
-    gs_off[ng] = acc;
+// exclusive offsets of 2*group_ops (one block; a serial loop over ~16k
+// groups cost ~0.9 ms on config 5)
+__global__ void __launch_bounds__(1024) k_gs_off(const int* group_ops, int ng, int64_t* gs_off) {
+  typedef cub::BlockScan<long long, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const int per = (ng + 1023) / 1024;
+  const int a = threadIdx.x * per, b = a + per < ng ? a + per : ng;
+  long long sum = 0;
+  for (int g = a; g < b; g++) sum += 2LL * group_ops[g];
+  long long excl;
+  BS(tmp).ExclusiveSum(sum, excl);
+  for (int g = a; g < b; g++) {
+    gs_off[g] = excl;
+    excl += 2LL * group_ops[g];
   }
+  if (threadIdx.x == 1023) gs_off[ng] = excl;
 }
 
 __global__ void k_iota_u32(uint32_t* v, int64_t n) {
@@ -432,7 +454,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
     if (build_paths) XS_TRY(trie_setup(ctx, s, &os.trie));
     return XS_OK;
   }
-  if (gb + tb + 1 > 64 || pb + tb + 1 > 64) {
+  if (gb + tb + 1 > 64 || pb + tb + 1 > 64) {  // (op-group keys use <= gb bits)
     ctx->err = "timeline too wide for 64-bit endpoint keys";
     return XS_UNSUPPORTED;
   }
@@ -458,8 +480,24 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   XS_TRY(ws(ctx, W_SKEY_ALT, 2 * m + 2, s, &sk_alt));
   XS_TRY(ws(ctx, W_SVAL, 2 * m + 2, s, &sv));
   XS_TRY(ws(ctx, W_SVAL_ALT, 2 * m + 2, s, &sv_alt));
-  XS_LAUNCH(ctx, k_endpoints, grid_for(m), XS_BLOCK, 0, s, op_ev, m, v, lo, tb, sk, sv);
-  XS_TRY(sort_pairs_u64_u32(ctx, &sk, &sk_alt, &sv, &sv_alt, 2 * m, gb + tb + 1, s));
+  // dense numbering of the op-carrying groups (order-preserving)
+  int *opg, *opg_inv;
+  const int64_t nog = H.pad[5] > 0 ? H.pad[5] : 1;
+  const int gbo = bits_for((uint64_t)(nog - 1));
+  XS_TRY(ws(ctx, W_OPG, ng + 1, s, &opg));
+  XS_TRY(ws(ctx, W_OPG_INV, nog + 1, s, &opg_inv));
+  {
+    cub::TransformInputIterator<int, HasOps, const int*> it(group_ops, HasOps());
+    size_t temp = 0;
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, it, opg, ng, s));
+    void* t;
+    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, it, opg, ng, s));
+    ctx->launches += 2;
+  }
+  XS_LAUNCH(ctx, k_op_groups, grid_for(ng), XS_BLOCK, 0, s, group_ops, ng, opg, opg_inv);
+  XS_LAUNCH(ctx, k_endpoints, grid_for(m), XS_BLOCK, 0, s, op_ev, m, v, lo, tb, opg, sk, sv);
+  XS_TRY(sort_pairs_u64_u32(ctx, &sk, &sk_alt, &sv, &sv_alt, 2 * m, gbo + tb + 1, s));
   XS_LAUNCH(ctx, k_op_tiefix, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, 2 * m, op_ev, v);
   const int* rank_ev = op_ev;  // op ids index every per-op array
   os.skeys = sk;
@@ -509,7 +547,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   XS_TRY(ws(ctx, W_PK, 2 * m + 2, s, &pk));
   XS_TRY(ws(ctx, W_PK_ALT, 2 * m + 2, s, &pk_alt));
   // op endpoints relabelled group -> pid (monotone, so order is kept)
-  XS_LAUNCH(ctx, k_pid_keys, grid_for(2 * m), XS_BLOCK, 0, s, sk, 2 * m, v.ev.group_pid, tb, pk);
+  XS_LAUNCH(ctx, k_pid_keys, grid_for(2 * m), XS_BLOCK, 0, s, sk, 2 * m, v.ev.group_pid, opg_inv, tb, pk);
   if (ctx->h_stats->multi_op_pids == 0) {
     // one op tid per pid: pid order == group order
     XS_LAUNCH(ctx, k_pidpath_simple, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, 2 * m, parent, node, pidpath);
@@ -517,7 +555,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   } else {
     int64_t* gs_off;
     XS_TRY(ws(ctx, W_GS_OFF, ng + 1, s, &gs_off));
-    XS_LAUNCH(ctx, k_gs_off, 1, 32, 0, s, group_ops, ng, gs_off);
+    XS_LAUNCH(ctx, k_gs_off, 1, 1024, 0, s, group_ops, ng, gs_off);
     XS_TRY(sort_keys_u64(ctx, &pk, &pk_alt, 2 * m, pb + tb + 1, s));
     XS_LAUNCH(ctx, k_pidpath_general, grid_for(2 * m, 128), 128, 0, s, pk, 2 * m, tb, (int*)ctx->ptr[W_PID_GROUP0],
               group_ops, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st);

@@ -939,6 +939,13 @@ static int bucket_sweep(xs_ctx* ctx, const EventView& v, const BkPlan& plan, int
   if (getenv("XS_TRACE_SWEEP")) XS_CUDA(cudaMallocAsync(&ptrace, n_chunks * 64, s));
   XS_LAUNCH(ctx, k_bk_sweep, (int)n_chunks, BK_THREADS, sizeof(BkSmem), s, keys, nvalid, chunk, g.shift, tb,
             os.pidpath, os.opbase, n_nodes, hist, desc, flags, tctr, st, ptrace, direct);
+  if (getenv("XS_DEBUG_OVF") && !ctx->capturing) {  // developer diagnostics (eager runs only)
+    long long f = 0;
+    cudaMemcpyAsync(&f, &st->pad[3], 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "bk_sweep nvalid=%lld key_bits=%d bb=%d pid_chunks=%d overflow=%lld\n", (long long)nvalid,
+            g.key_bits, g.bb, (int)pid_chunks, f);
+  }
   if (ptrace) {  // developer timing: per-phase globaltimer stamps of every CTA
     std::vector<unsigned long long> h(n_chunks * 8);
     XS_CUDA(cudaMemcpyAsync(h.data(), ptrace, n_chunks * 64, cudaMemcpyDeviceToHost, s));

@@ -13,7 +13,9 @@ from paper_2102_04285_b200 import _engine, synth  # noqa: E402
 
 cfg = int(os.environ.get("XS_CONFIG", "2"))
 calls = int(os.environ.get("XS_CALLS", "2"))
-if cfg == 3:
+if cfg == 5:
+    ct = synth.adversarial_trace(int(os.environ.get("XS_EVENTS", "10000000")), pids=64, workers=os.cpu_count())
+elif cfg == 3:
     ev = int(os.environ.get("XS_EVENTS", "100000000"))
     procs = max(1, ev // 1_000_000)
     ct = synth.config3_trace(processes=procs, events_per_pid=ev // procs, workers=os.cpu_count())
@@ -21,7 +23,7 @@ else:
     ct = synth.ddpg_trace(int(os.environ.get("XS_ITERS", "27027")))
 eng = _engine.get(0)
 dt = _engine.DeviceTrace(ct, 0)
-scaled = synth.exact_profile().scaled(ct.names)
+scaled = (synth.adversarial_profile() if cfg == 5 else synth.exact_profile()).scaled(ct.names)
 for _ in range(calls):
     eng.correct(dt, scaled, analyze_attribution=0)
 print("events", ct.n)
