@@ -1,3 +1,4 @@
+#include <algorithm>
 // xs_ctx.cu -- C ABI entry points, workspace and sort plumbing.
 #include <cub/device/device_radix_sort.cuh>
 
@@ -152,7 +153,11 @@ int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s
       ctx->n_nodes = ctx->h_stats->pad[0] > 0 ? (int)ctx->h_stats->pad[0] : 1;  // trie nodes allocated
       return XS_OK;
     }
-    ctx->trie_cap_log2 += 2;
+    {  // the path trie ran out of slots: jump to a capacity that holds a node
+       // per op segment (the distinct paths are at most that many)
+      const int need = bits_for((uint64_t)(4 * ctx->h_stats->n_ops_nz + 4)) + 1;
+      ctx->trie_cap_log2 = std::max(ctx->trie_cap_log2 + 2, std::min(need, 30));
+    }
   }
   ctx->err = "path table could not be sized";
   return XS_NO_MEMORY;

@@ -315,10 +315,14 @@ __global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const 
     pidpath[k] = node[ctxs[0]];
     return;
   }
-  // gather all active ops (chains), sort by global rank order, intern root-down
+  // every chain is already in rank order (a parent precedes its children);
+  // k-way merge of the chains from their roots, interning root-down as we go
+  // (was: gather + insertion sort, O(depth^2) rank comparisons per endpoint)
   int ops[MAXD];
+  int cs[64], head[64];
   int n = 0;
   for (int c = 0; c < nctx; c++) {
+    cs[c] = n;
     for (int o = ctxs[c]; o >= 0; o = parent[o]) {
       if (n == MAXD) {
         atomicAdd((unsigned long long*)&st->depth_overflow, 1ull);
@@ -327,29 +331,33 @@ __global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const 
       }
       ops[n++] = o;
     }
-  }
-  // insertion sort by (start, -end, group, r) -- r orders (name, idx) within a group
-  for (int a = 1; a < n; a++) {
-    int x = ops[a];
-    int ix = rank_ev[x];
-    int64_t xs_ = v.start[ix], xe = v.start[ix] + v.dur[ix];
-    int xg = v.ev.tid[ix];
-    int b = a - 1;
-    while (b >= 0) {
-      int y = ops[b];
-      int iy = rank_ev[y];
-      int64_t ys = v.start[iy], ye = v.start[iy] + v.dur[iy];
-      int yg = v.ev.tid[iy];
-      const int ny = v.ev.name[iy], nx = v.ev.name[ix];
-      bool greater = (ys != xs_) ? ys > xs_ : (ye != xe) ? ye < xe : (yg != xg) ? yg > xg : (ny != nx) ? ny > nx : iy > ix;
-      if (!greater) break;
-      ops[b + 1] = y;
-      b--;
-    }
-    ops[b + 1] = x;
+    head[c] = n - 1;  // root end of chain c (chain c is ops[cs[c] .. n), leaf first)
   }
   int cur = 0;
-  for (int a = 0; a < n; a++) cur = trie_intern(cur, v.ev.name[rank_ev[ops[a]]], t);
+  for (int done = 0; done < n; done++) {
+    int best = -1;
+    int64_t bs = 0, be = 0;
+    int bg = 0, bn = 0, bi = 0;
+    for (int c = 0; c < nctx; c++) {
+      if (head[c] < cs[c]) continue;
+      const int ix = rank_ev[ops[head[c]]];
+      const int64_t xs_ = v.start[ix], xe = v.start[ix] + v.dur[ix];
+      const int xg = v.ev.tid[ix], xn = v.ev.name[ix];
+      // rank order (start, -end, group, name, index) -- overlap.py:96-99
+      const bool less = best < 0 || (xs_ != bs ? xs_ < bs : xe != be ? xe > be : xg != bg ? xg < bg
+                                                                  : xn != bn ? xn < bn : ix < bi);
+      if (less) {
+        best = c;
+        bs = xs_;
+        be = xe;
+        bg = xg;
+        bn = xn;
+        bi = ix;
+      }
+    }
+    head[best]--;
+    cur = trie_intern(cur, bn, t);
+  }
   pidpath[k] = cur;
 }
 
