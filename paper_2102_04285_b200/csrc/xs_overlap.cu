@@ -1017,7 +1017,7 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   // endpoints (2n), one tracked entry per pid, and in CORRELATION mode one
   // foreign cell per fixed-event endpoint interval
   const int64_t dense_n = (int64_t)np * n_nodes * 32;
-  const int64_t cell_bound = 2 * n + np + 64 + (attribution == 1 ? 8 * (H.n_gpu_corr + 2 * os.m + np + 1) : 0);
+  const int64_t cell_bound = 2 * H.n_nonzero + np + 64 + (attribution == 1 ? 8 * (H.n_gpu_corr + 2 * os.m + np + 1) : 0);
   GHist hist{nullptr, nullptr, 0, (unsigned long long*)&st->table_full};
   int64_t hist_n = dense_n;
   static const int dense_max_log2 = [] {  // XS_HIST_DENSE_MAX_LOG2: tests force the hashed layout
@@ -1026,7 +1026,7 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   }();
   if (dense_n > ((int64_t)1 << dense_max_log2) && (dense_n > 2 * cell_bound || dense_max_log2 < 24)) {
     int lg = 10;
-    while (((int64_t)1 << lg) < 2 * cell_bound) lg++;
+    while (((int64_t)1 << lg) < cell_bound + cell_bound / 4) lg++;  // load <= 0.8 even if every interval were a cell
     hist_n = (int64_t)1 << lg;
     XS_TRY(ws(ctx, W_HIST_KEY, hist_n, s, &hist.key));
     XS_CUDA(cudaMemsetAsync(hist.key, 0xFF, hist_n * 8, s));
