@@ -53,3 +53,20 @@ def test_generators_deterministic_and_pool_equal():
     c = synth.config3_trace(processes=2, events_per_pid=5_000, workers=2)
     d = synth.config3_trace(processes=2, events_per_pid=5_000)
     assert np.array_equal(c.start, d.start) and np.array_equal(c.tid, d.tid)
+
+
+def test_pid_batches_are_contiguous_whole_pids():
+    from paper_2102_04285_b200.correction import _pid_batches
+
+    ct = synth.config3_trace(processes=9, events_per_pid=5_000)
+    parts = _pid_batches(ct, 4)
+    assert parts[0][0] == 0 and parts[-1][1] == ct.n and len(parts) >= 2
+    for (a, b), (c, _) in zip(parts, parts[1:]):
+        assert b == c and ct.pid[b - 1] != ct.pid[b]  # cuts only at pid boundaries
+    shuffled = ct.select_pids(list(range(ct.n_pids)))
+    rev = np.argsort(-shuffled.start, kind="stable")  # rows no longer pid-contiguous
+    from paper_2102_04285_b200.columnar import ColumnarTrace
+    t2 = ColumnarTrace(ct.clock_domain, ct.start[rev], ct.dur[rev], ct.pid[rev], ct.tid[rev], ct.cat[rev],
+                       ct.name[rev], ct.corr[rev], ct.has_corr[rev], ct.pids, ct.group_pid, ct.group_tid,
+                       ct.names, ct.processes, ct.pid_has_meta)
+    assert _pid_batches(t2, 4) == []
