@@ -495,59 +495,6 @@ struct CellTable {  // open addressing in shared memory, spill to global
   }
 };
 
-// Per-thread register cache of a few cells, flushed with a warp-level
-// reduce-by-key so a block touches each shared slot once per warp.
-template <int K>
-struct CellCache {
-  unsigned long long k[K];
-  unsigned long long v[K];
-  int n = 0;
-  __device__ void add(unsigned long long idx, unsigned long long len, CellTable& T, const GHist& hist) {
-#pragma unroll
-    for (int i = 0; i < K; i++)
-      if (i < n && k[i] == idx) {
-        v[i] += len;
-        return;
-      }
-    if (n < K) {
-#pragma unroll
-      for (int i = 0; i < K; i++)
-        if (i == n) {
-          k[i] = idx;
-          v[i] = len;
-        }
-      n++;
-      return;
-    }
-    T.add(k[0], v[0], hist);  // evict the oldest
-#pragma unroll
-    for (int i = 0; i + 1 < K; i++) {
-      k[i] = k[i + 1];
-      v[i] = v[i + 1];
-    }
-    k[K - 1] = idx;
-    v[K - 1] = len;
-  }
-  // all 32 lanes must call
-  __device__ void flush(CellTable& T, const GHist& hist) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int i = 0; i < K; i++) {
-      const bool has = i < n;
-      const unsigned long long key = has ? k[i] : ~0ull;
-      const unsigned act = __ballot_sync(0xffffffffu, has);
-      unsigned long long val = has ? v[i] : 0;
-      if (has) {
-        const unsigned peers = __match_any_sync(act, key);
-        const int leader = __ffs(peers) - 1;
-        unsigned long long sum = 0;
-        for (unsigned m = peers; m; m &= m - 1) sum += __shfl_sync(peers, val, __ffs(m) - 1);
-        if (lane == leader) T.add(key, sum, hist);
-      }
-    }
-  }
-};
-
 struct BkSmem {
   uint32_t k[BK_CAP];       // chunk keys relative to the chunk base, bucket order (as scattered)
   uint32_t sorted[BK_CAP];  // fully sorted (also block-radix-sort scratch together with k[])
