@@ -69,7 +69,7 @@ __device__ __forceinline__ int64_t bucket_slot(unsigned* counts, const int64_t* 
 inline int bucket_bits_for(int64_t nkeys, int key_bits, int max_bits = 24) {
   static int adj = [] {
     const char* e = getenv("XS_BK_BITS_ADJ");  // (tuning experiments)
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 1;  // ~2 buckets per key (adj 0: +2% at config 2 but config 5 overflows to LSD)
   }();
   int b = 1;
   while (b < 62 && ((int64_t)1 << b) < nkeys) b++;
