@@ -93,6 +93,14 @@ def _init_torch_types():
     _TORCH.update({np.int64: torch.int64, np.int32: torch.int32, np.uint8: torch.uint8})
 
 
+def torch_dtype(np_dtype):
+    """torch dtype of a numpy column dtype (int64 / int32 / uint8)."""
+    _torch()
+    if not _TORCH:
+        _init_torch_types()
+    return _TORCH[np.dtype(np_dtype).type]
+
+
 class XsError(RuntimeError):
     def __init__(self, status: int, message: str):
         self.status = status

@@ -161,6 +161,9 @@ def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution
     return raw.start, raw.dur, _report(ct, raw), bd
 
 
+_PIPE_BUFS: dict = {}  # analyze_columnar_pipelined's double buffers, kept across calls
+
+
 def _pid_batches(ct: ColumnarTrace, batches: int) -> list:
     """Contiguous row ranges holding whole pids (pid column non-decreasing),
     about n / batches rows each; [] when the rows are not pid-contiguous."""
@@ -226,12 +229,34 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     for sub, (a, b) in zip(subs, parts):  # pids present in each batch, from the pid row ranges
         sub.__dict__["_present_mask"] = has & (starts[:-1] >= a) & (starts[:-1] < b)
 
+    # two persistent device buffer sets (double buffering): stable addresses
+    # keep every batch's captured pipeline graph valid across calls
+    cols = ("start", "dur", "pid", "tid", "cat", "name", "corr", "has_corr")
+    rows_max = max(b - a for a, b in parts)
+    key = (eng.device, rows_max)
+    bufs = _PIPE_BUFS.get(key)
+    if bufs is None:
+        _PIPE_BUFS.clear()
+        bufs = [{c: torch.empty(rows_max, dtype=_engine.torch_dtype(getattr(ct, c).dtype), device=dev) for c in cols}
+                for _ in range(2)]
+        _PIPE_BUFS[key] = bufs
+    tables = {"group_pid": torch.from_numpy(np.ascontiguousarray(ct.group_pid, np.int32)).to(dev),
+              "pid_has_meta": torch.from_numpy(np.ascontiguousarray(ct.pid_has_meta, np.uint8)).to(dev)}
+
     def upload(k):
+        a, b = parts[k]
+        buf = bufs[k % 2]
         with torch.cuda.stream(copy):
-            dt = _engine.DeviceTrace(subs[k], eng.device, non_blocking=True)
+            tens = {}
+            for c in cols:
+                src = subs[k]._pinned[c] if subs[k]._pinned is not None else torch.from_numpy(getattr(subs[k], c))
+                dst = buf[c][: b - a]
+                dst.copy_(src, non_blocking=True)
+                tens[c] = dst
+            tens.update(tables)
             ev = torch.cuda.Event()
             ev.record(copy)
-        return dt, ev
+        return _engine.DeviceTrace.from_tensors(subs[k], tens, eng.device), ev
 
     rep = CorrectionReport()
     bd_all = None
