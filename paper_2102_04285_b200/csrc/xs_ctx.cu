@@ -458,6 +458,7 @@ struct SpecScope {  // speculative-pass switches, cleared on every exit path
     c->spec_select_dur = nullptr;
     c->spec_guard_a = c->spec_guard_b = nullptr;
     c->spec_keep_counts = false;
+    c->spec_zero_sentinel = false;
   }
 };
 
@@ -545,7 +546,11 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     } join{ctx, w, to_host};
     if (!spec) return XS_OK;
     XS_CUDA(cudaMemcpyAsync(saved, st, sizeof(Stats), cudaMemcpyDeviceToDevice, w));
-    SpecScope sp(ctx, ev->dur, &st->n_ops_nz, &saved->n_ops_nz);
+    // INSTANT: ops shrunk to zero length are excluded by sentinel keys, so the
+    // pass stays valid; CORRELATION keeps the guard (discard and redo)
+    SpecScope sp(ctx, ev->dur, attribution == 1 ? &st->n_ops_nz : nullptr,
+                 attribution == 1 ? &saved->n_ops_nz : nullptr);
+    ctx->spec_zero_sentinel = attribution == 0;
     XS_TRY(stage_events_async(ctx, vc, w, false, nullptr));
     // correlations are untouched by the correction: the original's dangling
     // check stands, and only CORRELATION attribution needs launch instants
@@ -564,10 +569,15 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
   XS_TRY(correct_verdict(ctx, hc, bad_event));
   if (spec) {
     const Stats& c = *ctx->h_stats;  // the corrected trace's pass 1 + the overlap flags
-    bool same = c.n_bad == 0 && !c.table_full && !c.depth_overflow && !c.pad[3] && c.n_ops_nz == orig.n_ops_nz &&
-                c.n_nonzero == orig.n_nonzero && c.multi_op_pids == orig.multi_op_pids &&
+    // everything the pass was sized by (the original's pass 1) bounds the
+    // corrected trace's counts; INSTANT tolerates ops shrunk to zero length
+    const bool shrink_ok = attribution == 0;
+    bool same = c.n_bad == 0 && !c.table_full && !c.depth_overflow && !c.pad[3] &&
+                (shrink_ok ? c.n_ops_nz <= orig.n_ops_nz : c.n_ops_nz == orig.n_ops_nz) &&
+                (shrink_ok ? c.n_nonzero <= orig.n_nonzero : c.n_nonzero == orig.n_nonzero) &&
+                (shrink_ok ? c.multi_op_pids <= orig.multi_op_pids : c.multi_op_pids == orig.multi_op_pids) &&
                 c.n_api_corr == orig.n_api_corr && c.n_gpu_corr == orig.n_gpu_corr && c.max_span <= orig.max_span;
-    for (int k = 0; k < 8; k++) same = same && c.cat_nz[k] == orig.cat_nz[k];
+    for (int k = 0; k < 8; k++) same = same && (shrink_ok ? c.cat_nz[k] <= orig.cat_nz[k] : c.cat_nz[k] == orig.cat_nz[k]);
     if (getenv("XS_DEBUG_STATS"))
       fprintf(stderr, "xs_analyze speculative overlap %s: bad %lld full %lld depth_ovf %lld lsd %lld\n",
               same ? "kept" : "redone", c.n_bad, c.table_full, c.depth_overflow, c.pad[3]);

@@ -219,6 +219,10 @@ struct xs_ctx {
   const long long* spec_guard_a = nullptr;
   const long long* spec_guard_b = nullptr;
   bool spec_keep_counts = false;
+  // speculative INSTANT pass: operations the correction shrank to zero length
+  // get sentinel endpoint keys (sorted to the tail, outside every real path)
+  // and the op counts come from the corrected pass 1
+  bool spec_zero_sentinel = false;
   long long ws_generation = 0;  // bumped on every workspace reallocation
   cudaStream_t priv_stream = nullptr;
   cudaEvent_t join_in = nullptr, join_out = nullptr;

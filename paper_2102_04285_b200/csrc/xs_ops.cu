@@ -52,10 +52,17 @@ struct HasOps {
 };
 
 __global__ void k_endpoints(const int* op_ev, int64_t m, EventView v, const int64_t* lo, int tb, const int* opg,
-                            uint64_t* keys, uint32_t* vals) {
+                            int zero_sentinel, uint64_t* keys, uint32_t* vals) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
   int i = op_ev[j];
+  if (zero_sentinel && v.dur[i] == 0) {  // shrunk to zero length: out of every path (tail of the sort)
+    keys[m + j] = ~0ull;
+    keys[j] = ~0ull;
+    vals[m + j] = (uint32_t)j;
+    vals[j] = (uint32_t)j;
+    return;
+  }
   int p = v.ev.pid[i];
   uint64_t g = (uint64_t)opg[v.ev.tid[i]];
   uint64_t s = (uint64_t)(v.start[i] - lo[p]);
@@ -86,6 +93,7 @@ __global__ void k_op_tiefix(const uint64_t* keys, uint32_t* vals, int64_t n2, co
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n2) return;
   const uint64_t k = keys[q];
+  if (k == ~0ull) return;  // sentinel tail
   if (q > 0 && keys[q - 1] == k) return;
   if (q + 1 >= n2 || keys[q + 1] != k) return;
   int64_t e = q + 1;
@@ -114,7 +122,11 @@ __global__ void k_depth_scatter(const uint64_t* keys, const uint32_t* vals, cons
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n2) return;
   uint32_t r = vals[j];
-  if (keys[j] & 1ull) {
+  if (keys[j] == ~0ull) {  // sentinel op (zero length): consistent, never referenced
+    d_open[r] = 1;
+    d_close[r] = 0;
+    pos_open[r] = (int)j;
+  } else if (keys[j] & 1ull) {
     d_open[r] = depth[j];
     pos_open[r] = (int)j;
   } else {
@@ -179,7 +191,14 @@ __global__ void k_parent_nodes(const uint64_t* __restrict__ sk, const uint32_t* 
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= n2) return;
     const int64_t j = base + lane;
-    bool done = j >= n2 || !(sk[j] & 1ull);  // closes need no work
+    if (j < n2 && sk[j] == ~0ull) {  // sentinel op (zero length, speculative pass): no path
+      parent[sv[j]] = -1;
+      node[sv[j]] = 0;
+      __threadfence();
+      atomicExch(&pready[sv[j]], 1);
+      atomicExch(&nready[sv[j]], 1);
+    }
+    bool done = j >= n2 || !(sk[j] & 1ull) || sk[j] == ~0ull;  // closes need no work
     int o = -1, p = -2, nm = 0, wait_on = -1;
     if (!done) {
       o = (int)sv[j];
@@ -259,6 +278,10 @@ __global__ void k_pid_keys(const uint64_t* skeys, int64_t n2, const int32_t* gro
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n2) return;
   uint64_t k = skeys[j];
+  if (k == ~0ull) {
+    pk[j] = ~0ull;
+    return;
+  }
   uint64_t g = (uint64_t)opg_inv[k >> (tb + 1)];
   uint64_t low = k & ((2ull << tb) - 1);
   pk[j] = ((uint64_t)group_pid[g] << (tb + 1)) | low;
@@ -273,6 +296,10 @@ __global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const 
                                   int* pidpath, TrieView t, Stats* st) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n2) return;
+  if (pk[k] == ~0ull) {  // sentinel tail
+    pidpath[k] = 0;
+    return;
+  }
   uint64_t key = pk[k] >> 1;
   if (k + 1 < n2 && (pk[k + 1] >> 1) == key) {
     pidpath[k] = 0;  // not a run end: never looked up
@@ -447,6 +474,10 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   int64_t *lo = (int64_t*)ctx->ptr[W_SPAN_LO];
   int* pid_ops = (int*)ctx->ptr[W_PID_OPS];
   int* group_ops = (int*)ctx->ptr[W_GROUP_OPS];
+  // positions in the sorted stream count only the ops that kept a nonzero
+  // length: in the speculative sentinel mode those are the corrected pass 1's
+  int* pid_ops_pos = ctx->spec_zero_sentinel ? (int*)ctx->ptr[W_PID_OPS_ALT] : pid_ops;
+  int* group_ops_pos = ctx->spec_zero_sentinel ? (int*)ctx->ptr[W_GROUP_OPS_ALT] : group_ops;
   Stats* st = (Stats*)ctx->ptr[W_STATS];
   const int tb = os.tb;
   const int gb = bits_for((uint64_t)(ng > 0 ? ng - 1 : 0));
@@ -454,7 +485,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   const int nb = bits_for((uint64_t)(v.ev.n_names > 0 ? v.ev.n_names - 1 : 0));
   int64_t* opbase;
   XS_TRY(ws(ctx, W_OPBASE, np + 1, s, &opbase));
-  XS_LAUNCH(ctx, k_opbase, 1, 32, 0, s, pid_ops, np, opbase);
+  XS_LAUNCH(ctx, k_opbase, 1, 32, 0, s, pid_ops_pos, np, opbase);
   os.opbase = opbase;
   os.pidpath = nullptr;
   os.pk = nullptr;
@@ -504,7 +535,8 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
     ctx->launches += 2;
   }
   XS_LAUNCH(ctx, k_op_groups, grid_for(ng), XS_BLOCK, 0, s, group_ops, ng, opg, opg_inv);
-  XS_LAUNCH(ctx, k_endpoints, grid_for(m), XS_BLOCK, 0, s, op_ev, m, v, lo, tb, opg, sk, sv);
+  XS_LAUNCH(ctx, k_endpoints, grid_for(m), XS_BLOCK, 0, s, op_ev, m, v, lo, tb, opg, ctx->spec_zero_sentinel ? 1 : 0,
+            sk, sv);
   XS_TRY(sort_pairs_u64_u32(ctx, &sk, &sk_alt, &sv, &sv_alt, 2 * m, gbo + tb + 1, s));
   XS_LAUNCH(ctx, k_op_tiefix, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, 2 * m, op_ev, v);
   const int* rank_ev = op_ev;  // op ids index every per-op array
@@ -563,10 +595,10 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   } else {
     int64_t* gs_off;
     XS_TRY(ws(ctx, W_GS_OFF, ng + 1, s, &gs_off));
-    XS_LAUNCH(ctx, k_gs_off, 1, 1024, 0, s, group_ops, ng, gs_off);
+    XS_LAUNCH(ctx, k_gs_off, 1, 1024, 0, s, group_ops_pos, ng, gs_off);
     XS_TRY(sort_keys_u64(ctx, &pk, &pk_alt, 2 * m, pb + tb + 1, s));
     XS_LAUNCH(ctx, k_pidpath_general, grid_for(2 * m, 128), 128, 0, s, pk, 2 * m, tb, (int*)ctx->ptr[W_PID_GROUP0],
-              group_ops, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st);
+              group_ops_pos, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st);
     os.pk = pk;
   }
   return XS_OK;
