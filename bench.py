@@ -347,7 +347,7 @@ def run_ours(args):
     ct_host = ct.pinned()
     out_s = torch.empty(n, dtype=torch.int64).pin_memory()
     out_d = torch.empty(n, dtype=torch.int64).pin_memory()
-    h2d = sum(int(t.numel() * t.element_size()) for t in ct_host._pinned.values())
+    h2d = int(ct_host._pinned["_block"].numel())  # the one pinned block uploaded per step
 
     from paper_2102_04285_b200 import analyze_columnar_pipelined
     pipelined = ct.n_pids >= 8  # many processes: upload the next pid batch while analysing this one

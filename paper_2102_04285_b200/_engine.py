@@ -38,6 +38,17 @@ class DeviceTrace:
         self.device = device
 
         pinned = ct._pinned or {}
+        block = pinned.get("_block")
+        if block is not None:  # one pinned block (ColumnarTrace.pinned): one DMA, device views
+            dblock = block.to(dev, non_blocking=True)
+            self._dblock = dblock
+            for k, o in zip(ColumnarTrace._COLUMNS, pinned["_offsets"]):
+                a = getattr(ct, k)
+                if a.size == 0:
+                    setattr(self, k, torch.zeros(1, dtype=_TORCH[a.dtype.type], device=dev))
+                else:
+                    setattr(self, k, dblock[o:o + a.nbytes].view(_TORCH[a.dtype.type]))
+            return
 
         def up(key, dtype):
             t = pinned.get(key)

@@ -147,16 +147,24 @@ class ColumnarTrace:
 
     def pinned(self) -> "ColumnarTrace":
         """The same trace with every column in page-locked host memory, so the
-        device upload of each call is an asynchronous DMA at full PCIe rate
-        (the arrays are numpy views of pinned torch tensors)."""
+        device upload of each call is an asynchronous DMA at full PCIe rate.
+        The columns are 16-byte-aligned views of ONE pinned block (the
+        upload is a single copy); the arrays are numpy views of it."""
         import torch
 
-        tens, arrs = {}, {}
-        for k in self._COLUMNS:
-            a = np.ascontiguousarray(getattr(self, k))
-            t = torch.from_numpy(a).pin_memory() if a.size else torch.from_numpy(a.copy())
-            tens[k] = t
-            arrs[k] = t.numpy()
+        cols = [np.ascontiguousarray(getattr(self, k)) for k in self._COLUMNS]
+        offs, total = [], 0
+        for a in cols:
+            offs.append(total)
+            total += (a.nbytes + 15) // 16 * 16
+        block = torch.empty(max(total, 16), dtype=torch.uint8).pin_memory()
+        raw = block.numpy()
+        tens, arrs = {"_block": block, "_offsets": offs}, {}
+        for k, a, o in zip(self._COLUMNS, cols, offs):
+            view = raw[o:o + a.nbytes].view(a.dtype)
+            view[...] = a
+            arrs[k] = view
+            tens[k] = block[o:o + a.nbytes].view(torch.from_numpy(a[:0]).dtype)
         return ColumnarTrace(self.clock_domain, arrs["start"], arrs["dur"], arrs["pid"], arrs["tid"], arrs["cat"],
                              arrs["name"], arrs["corr"], arrs["has_corr"], self.pids, arrs["group_pid"],
                              self.group_tid, self.names, self.processes, arrs["pid_has_meta"], self._source, tens)

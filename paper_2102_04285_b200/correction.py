@@ -192,7 +192,7 @@ def _row_slice(ct: ColumnarTrace, a: int, b: int) -> ColumnarTrace:
     pin = None
     if ct._pinned is not None:
         pin = {k: (t[a:b] if k in ("start", "dur", "pid", "tid", "cat", "name", "corr", "has_corr") else t)
-               for k, t in ct._pinned.items()}
+               for k, t in ct._pinned.items() if not k.startswith("_")}  # (the whole-block DMA is per trace)
     return ColumnarTrace(ct.clock_domain, ct.start[a:b], ct.dur[a:b], ct.pid[a:b], ct.tid[a:b], ct.cat[a:b],
                          ct.name[a:b], ct.corr[a:b], ct.has_corr[a:b], ct.pids, ct.group_pid, ct.group_tid, ct.names,
                          ct.processes, ct.pid_has_meta, None, pin)
