@@ -431,7 +431,7 @@ int xo_overlap(const xo_events_t* ev, int attribution, xo_overlap_t* out) {
     for (int64_t i = 0; i < n; i++)
       if (ev->cat[E[i]] == 0) ranked[k++] = i;
     stable_sort(ranked, n_ops, cmp_rank, &L);
-    int64_t* ranks = (int64_t*)calloc((size_t)n, sizeof(int64_t));
+    int64_t* ranks = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
     int32_t* rank_name = (int32_t*)malloc((size_t)(n_ops + 1) * sizeof(int32_t));
     for (int64_t r = 0; r < n_ops; r++) {
       ranks[ranked[r]] = r;
