@@ -146,10 +146,12 @@ __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const
     amt[j] = 0;
     hd[j] = 0;
     if (q < ns) {
-      uint32_t sl = slot[q];
-      int i = site_ev[sl];
-      amt[j] = site_amount(pr, v, i, site_sub[sl]);
-      hd[j] = q == 0 || (k1[q - 1] >> pshift) != (k1[q] >> pshift);
+      // the subkind is the key's low 3 bits: only API_INTERNAL sites gather
+      // their event (for the API name); the rest are profile constants
+      const uint64_t kq = k1[q];
+      const int sub = (int)(kq & 7u);
+      amt[j] = sub == API_INTERNAL ? pr.internal[v.ev.name[site_ev[slot[q]]]] : site_amount(pr, v, 0, sub);
+      hd[j] = q == 0 || (k1[q - 1] >> pshift) != (kq >> pshift);
       SegI128 e;
       e.v = amt[j];
       e.head = hd[j];
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(XS_BLOCK) k_removal(const uint64_t* k1, const 
       uint32_t sl = slot[q];
       anc[j] = (int64_t)((kk >> 3) & tmask);
       pp[j] = (int)(kk >> pshift);
-      sub[j] = site_sub[sl];
+      sub[j] = (int)(kk & 7u);  // (the key's subkind bits; no gather)
       len[j] = lenslot[sl];
       hd[j] = q == 0 || (k1[q - 1] >> pshift) != (kk >> pshift);
       RM e{len[j] > 0 ? len[j] : 0, anc[j] + len[j], len[j] > 0 ? 1 : 0, hd[j], 0};
