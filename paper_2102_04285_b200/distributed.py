@@ -76,6 +76,8 @@ def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         known = bool(flag.item())
     if not known:  # grow the tables (first merge, or new paths): tiny object all-gather
+        if len(_TABLES["paths"]) * max(len(_TABLES["pids"]), 1) > (1 << 20):  # bound the dense merge buffer
+            _TABLES["paths"], _TABLES["pids"] = (), ()
         mine = (sorted(my_paths), sorted(my_pids))
         gathered = [None] * world
         if world > 1:
