@@ -472,12 +472,13 @@ __device__ __forceinline__ void smem_add64(unsigned* lo, unsigned* hi, unsigned 
   if (vh | carry) atomicAdd(hi, vh + carry);
 }
 
-struct CellTable {  // open addressing in shared memory, spill to global
+template <int kHT>
+struct CellTableT {  // open addressing in shared memory, spill to global
   unsigned long long* key;
   unsigned* lo;
   unsigned* hi;
   __device__ void add(unsigned long long idx, unsigned long long v, const GHist& hist) {
-    unsigned h = (unsigned)(mix64(idx) & (HT - 1));
+    unsigned h = (unsigned)(mix64(idx) & (kHT - 1));
 #pragma unroll 1
     for (int probe = 0; probe < 16; probe++) {
       unsigned long long k = key[h];
@@ -489,23 +490,29 @@ struct CellTable {  // open addressing in shared memory, spill to global
         smem_add64(&lo[h], &hi[h], v);
         return;
       }
-      h = (h + 1) & (HT - 1);
+      h = (h + 1) & (kHT - 1);
     }
     hist.add(idx, v);
   }
 };
 
-struct BkSmem {
+template <int kHT>
+struct BkSmemT {
   uint32_t k[BK_CAP];       // chunk keys relative to the chunk base, bucket order (as scattered)
   uint32_t sorted[BK_CAP];  // fully sorted (also block-radix-sort scratch together with k[])
-  unsigned long long h_key[HT];
-  unsigned h_lo[HT];
-  unsigned h_hi[HT];
+  unsigned long long h_key[kHT];
+  unsigned h_lo[kHT];
+  unsigned h_hi[kHT];
   uint32_t last[BK_THREADS];
   SwState warp_agg[BK_THREADS / 32];
   SwState tile_pre;
   int big;
 };
+
+// the shared cell table of the fused sweep: 1K slots (4 CTAs/SM) when a chunk's
+// cells index it directly, 4K slots (2 CTAs/SM) for many-path traces whose
+// cells must hash (deep recursive operations: fewer spills to the global table)
+constexpr int HT_SMALL = 1024, HT_BIG = 4096;
 
 struct SwMaxOp {  // chunk aggregate: counts add, last = max key (order independent)
   __device__ SwState operator()(const SwState& a, const SwState& b) const {
@@ -541,14 +548,22 @@ __device__ __forceinline__ SwState sw_identity() {
 #ifndef XS_SWEEP_MINB
 #define XS_SWEEP_MINB 4  // 4 CTAs per SM (64 registers, small spills): more chunks in flight
 #endif
-__global__ void __launch_bounds__(BK_THREADS, XS_SWEEP_MINB) k_bk_sweep(
+template <int kHT, int kMinB>
+__global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
     const uint64_t* __restrict__ keys, int64_t total, const int64_t* __restrict__ chunk, int shift, int tb,
     const int* __restrict__ pidpath, const int64_t* __restrict__ opbase, int n_nodes,
     GHist hist, TileDesc<SwState>* desc, int* flags, int* tile_ctr, Stats* st,
-    unsigned long long* ptrace, int direct) {
+    unsigned long long* ptrace, int direct_ok, const int* trie_count) {
+  using BkSmem = BkSmemT<kHT>;
+  using CellTable = CellTableT<kHT>;
+  constexpr int HT = kHT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  // direct-indexed cells (path * 32 + mask) when the chunk holds one pid and
+  // the paths actually interned fit the table (decided on the device: the
+  // host only knows the trie's capacity without a sync)
+  const int direct = direct_ok && trie_count && (int64_t)(*trie_count) * 32 <= kHT;
   unsigned long long tstamp[8];
 #define XS_STAMP(i) if (ptrace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tstamp[i]));
   XS_STAMP(0);
@@ -876,16 +891,28 @@ static int bucket_sweep(xs_ctx* ctx, const EventView& v, const BkPlan& plan, int
   ProfScope ps(ctx, ST_SWEEP, s);
   static bool attr_set = false;
   if (!attr_set) {
-    XS_CUDA(cudaFuncSetAttribute(k_bk_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BkSmem)));
+    XS_CUDA(cudaFuncSetAttribute(k_bk_sweep<HT_SMALL, XS_SWEEP_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(BkSmemT<HT_SMALL>)));
+    XS_CUDA(cudaFuncSetAttribute(k_bk_sweep<HT_BIG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(BkSmemT<HT_BIG>)));
     attr_set = true;
   }
-  // direct-indexed block table: every chunk holds one pid and a pid's cells fit
+  // direct-indexed block table when every chunk holds one pid (the path-count
+  // condition is checked in the kernel); the big hashed table for traces whose
+  // cells go to the hashed global histogram (many deep paths)
   static const bool no_direct = getenv("XS_NO_DIRECT_CELLS") != nullptr;  // (A/B switch)
-  const int direct = !no_direct && (int64_t)n_nodes * 32 <= HT && (v.ev.n_pids <= 1 || pid_chunks) ? 1 : 0;
+  const int direct_ok = !no_direct && (v.ev.n_pids <= 1 || pid_chunks) ? 1 : 0;
+  const bool big_table = hist.key != nullptr;
   unsigned long long* ptrace = nullptr;
   if (getenv("XS_TRACE_SWEEP")) XS_CUDA(cudaMallocAsync(&ptrace, n_chunks * 64, s));
-  XS_LAUNCH(ctx, k_bk_sweep, (int)n_chunks, BK_THREADS, sizeof(BkSmem), s, keys, nvalid, chunk, g.shift, tb,
-            os.pidpath, os.opbase, n_nodes, hist, desc, flags, tctr, st, ptrace, direct);
+  if (!big_table)
+    XS_LAUNCH(ctx, (k_bk_sweep<HT_SMALL, XS_SWEEP_MINB>), (int)n_chunks, BK_THREADS, sizeof(BkSmemT<HT_SMALL>), s,
+              keys, nvalid, chunk, g.shift, tb, os.pidpath, os.opbase, n_nodes, hist, desc, flags, tctr, st, ptrace,
+              direct_ok, os.trie.count);
+  else
+    XS_LAUNCH(ctx, (k_bk_sweep<HT_BIG, 2>), (int)n_chunks, BK_THREADS, sizeof(BkSmemT<HT_BIG>), s, keys, nvalid,
+              chunk, g.shift, tb, os.pidpath, os.opbase, n_nodes, hist, desc, flags, tctr, st, ptrace, direct_ok,
+              os.trie.count);
   if (getenv("XS_DEBUG_OVF") && !ctx->capturing) {  // developer diagnostics (eager runs only)
     long long f = 0;
     cudaMemcpyAsync(&f, &st->pad[3], 8, cudaMemcpyDeviceToHost, s);
