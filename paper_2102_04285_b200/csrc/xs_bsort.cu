@@ -209,7 +209,7 @@ int bucket_sort_pairs(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_
 static int bucket_sort_pairs_impl(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals,
                                   uint32_t** vals_alt, int64_t n, int key_bits, cudaStream_t s) {
   Stats* st = (Stats*)ctx->ptr[W_STATS];
-  const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(n, key_bits));
+  const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(n, key_bits, 24, true));
   unsigned* counts;
   int64_t *offs, *chunk;
   unsigned long long* tail;

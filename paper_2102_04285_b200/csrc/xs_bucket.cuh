@@ -66,14 +66,18 @@ __device__ __forceinline__ int64_t bucket_slot(unsigned* counts, const int64_t* 
 // max_bits: the record sorts stay at 2^24 buckets (their offsets scan would
 // outweigh the smaller in-chunk ranks); the endpoint sort, whose per-chunk
 // rank is the sweep's hot phase, goes to 2^26 (<= 768 MB of tables)
-inline int bucket_bits_for(int64_t nkeys, int key_bits, int max_bits = 24) {
+inline int bucket_bits_for(int64_t nkeys, int key_bits, int max_bits = 24, bool record_sort = false) {
   static int adj = [] {
     const char* e = getenv("XS_BK_BITS_ADJ");  // (tuning experiments)
     return e ? atoi(e) : 1;  // ~2 buckets per key (adj 0: +2% at config 2 but config 5 overflows to LSD)
   }();
+  static int adj_rec = [] {
+    const char* e = getenv("XS_BK_BITS_ADJ_REC");  // (tuning experiments: record sorts)
+    return e ? atoi(e) : 1;
+  }();
   int b = 1;
   while (b < 62 && ((int64_t)1 << b) < nkeys) b++;
-  b += adj;
+  b += record_sort ? adj_rec : adj;
   if (b < 10) b = 10;
   if (b > max_bits) b = max_bits;
   return b < key_bits ? b : key_bits;

@@ -66,7 +66,7 @@ enum Slot : int {
   W_BK_COUNTS, W_BK_FILL, W_BK_OFFS, W_BK_CSTART, W_BK_CFIRST,
   W_CORR_TOTALS, W_NS_DEV, W_STATS_SAVE, W_PID_OPS_ALT, W_GROUP_OPS_ALT, W_PID_GROUP0_ALT,
   W_BS_COUNTS, W_BS_OFFS, W_BS_TAIL, W_BS_CHUNK, W_RMAP_IDX,
-  W_CUB_TEMP2, W_OPG, W_OPG_INV, W_TILE_CTR_B, W_CUB_TEMP_B, W_BS_COUNTS_B, W_BS_OFFS_B, W_BS_TAIL_B, W_BS_CHUNK_B,
+  W_CUB_TEMP2, W_OPG, W_OPG_INV, W_TGRP_FLAG, W_TGRP_IDX, W_TILE_CTR_B, W_CUB_TEMP_B, W_BS_COUNTS_B, W_BS_OFFS_B, W_BS_TAIL_B, W_BS_CHUNK_B,
   W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
   W_NUM_SLOTS
 };

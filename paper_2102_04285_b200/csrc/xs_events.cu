@@ -134,12 +134,13 @@ template <bool kVec>
 __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, const uint8_t* __restrict__ has_meta,
                                                     const uint8_t* __restrict__ has_internal, int check_api,
                                                     Stats* st, int64_t* lo_out, int64_t* hi_out, int* pid_ops,
-                                                    int* group_ops) {
+                                                    int* group_ops, uint8_t* tflag) {
   __shared__ unsigned long long s_cnt[20];  // cat_all[6], cat_nz[6], bad, nz, ops_nz, ops, api, api_corr, gpu_corr
   __shared__ long long s_bad_api;
   if (threadIdx.x < 20) s_cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_bad_api = INT64_MAX;
   P1Acc A;
+  int last_tg = -1;
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   __syncthreads();  // s_cnt initialised
@@ -209,6 +210,12 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
         }
         p1_visit(A, i0 + k, s[k], d[k], p[k], c[k], meta, g[k], hc[k], nm[k], lo_out, hi_out, pid_ops, group_ops,
                  has_internal, check_api);
+        // group carries transition records: a cached read first, so the hot
+        // groups are written once, not by every event
+        if (c[k] >= 1 && c[k] <= 4 && g[k] != last_tg) {
+          last_tg = g[k];
+          if (!tflag[last_tg]) tflag[last_tg] = 1;
+        }
       }
     }
   }
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
 
 // per-pid span reduction for the max key width; also counts multi-tid op pids
 __global__ void k_pid_finish(const int64_t* lo, const int64_t* hi, int np, const int32_t* group_pid,
-                             const int* group_ops, int ng, int* pid_group0, Stats* st) {
+                             const int* group_ops, const uint8_t* tflag, int ng, int* pid_group0, Stats* st) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < np && lo[p] != INT64_MAX) atomicMax(&st->max_span, (long long)(hi[p] - lo[p]));
   // first group of each pid (groups are sorted by pid): binary search
@@ -328,7 +335,12 @@ __global__ void k_pid_finish(const int64_t* lo, const int64_t* hi, int np, const
   if (p < np) {
     int a = pid_group0[p];
     int cnt = 0;
-    for (int g = a; g < ng && group_pid[g] == p; g++) cnt += group_ops[g] > 0;
+    int tcnt = 0;
+    for (int g = a; g < ng && group_pid[g] == p; g++) {
+      cnt += group_ops[g] > 0;
+      tcnt += tflag[g] != 0;
+    }
+    if (tcnt) atomicAdd((unsigned long long*)&st->pad[6], (unsigned long long)tcnt);  // transition-key groups
     if (cnt > 1) atomicAdd((unsigned long long*)&st->multi_op_pids, 1ull);
     if (cnt) atomicAdd((unsigned long long*)&st->pad[5], (unsigned long long)cnt);  // groups carrying ops
   }
@@ -435,6 +447,9 @@ int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool che
   XS_LAUNCH(ctx, k_init_stats, 1, 32, 0, s, st);
   XS_LAUNCH(ctx, k_init_pid, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, pid_ops, np + 1);
   XS_CUDA(cudaMemsetAsync(group_ops, 0, (ng + 1) * sizeof(int), s));
+  uint8_t* tflag;  // groups with HIGH_LEVEL/BACKEND/SIMULATOR/ACCEL_API events (dense transition-key groups)
+  XS_TRY(ws(ctx, W_TGRP_FLAG, ng + 1, s, &tflag));
+  XS_CUDA(cudaMemsetAsync(tflag, 0, ng + 1, s));
   if (n > 0) {
     ProfScope ps(ctx, ST_PASS1, s);
     const uint8_t* hasint = (check_api && prof) ? prof->has_internal : nullptr;
@@ -447,12 +462,12 @@ int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool che
                      ((uintptr_t)ev->has_corr % 4 == 0);
     if (vec)
       XS_LAUNCH(ctx, k_pass1<true>, p1_grid, XS_BLOCK, 0, s, v, n, ev->pid_has_meta, hasint,
-                check, st, lo, hi, pid_ops, group_ops);
+                check, st, lo, hi, pid_ops, group_ops, tflag);
     else
       XS_LAUNCH(ctx, k_pass1<false>, p1_grid, XS_BLOCK, 0, s, v, n, ev->pid_has_meta,
-                hasint, check, st, lo, hi, pid_ops, group_ops);
+                hasint, check, st, lo, hi, pid_ops, group_ops, tflag);
   }
-  XS_LAUNCH(ctx, k_pid_finish, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, np, ev->group_pid, group_ops, ng,
+  XS_LAUNCH(ctx, k_pid_finish, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, np, ev->group_pid, group_ops, tflag, ng,
             pid_group0, st);
   return XS_OK;
 }

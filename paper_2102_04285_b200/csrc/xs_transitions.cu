@@ -16,6 +16,7 @@
 // ends; an event is contained iff the exclusive max at the head of its run of
 // identical (start, end) is >= its end.
 #include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
 
 #include "xs_engine.cuh"
 
@@ -51,8 +52,8 @@ __device__ __forceinline__ TState t_identity() {
 }
 
 // records: src endpoints (nonzero src events) + queries (all dst events)
-__global__ void k_trec(EventView v, int64_t n, const int64_t* lo, int tb, int src_mask, int dst_mask, uint64_t* key,
-                       uint32_t* val, unsigned long long* count) {
+__global__ void k_trec(EventView v, int64_t n, const int64_t* lo, int tb, int src_mask, int dst_mask, const int* tg,
+                       uint64_t* key, uint32_t* val, unsigned long long* count) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int c = i < n ? v.ev.cat[i] : 0;
   bool is_src = i < n && c >= 1 && c <= 3 && ((src_mask >> c) & 1) && v.dur[i] > 0;
@@ -61,7 +62,7 @@ __global__ void k_trec(EventView v, int64_t n, const int64_t* lo, int tb, int sr
   unsigned long long at = warp_reserve(count, (unsigned)k);  // whole warp participates
   if (!k) return;
   int p = v.ev.pid[i];
-  uint64_t g = (uint64_t)v.ev.tid[i];
+  uint64_t g = (uint64_t)tg[v.ev.tid[i]];  // dense over the groups carrying such events (order kept)
   uint64_t s = (uint64_t)(v.start[i] - lo[p]);
   uint64_t e = s + (uint64_t)v.dur[i];
   if (is_src) {
@@ -196,6 +197,10 @@ __global__ void k_tdup(const uint32_t* val, const int32_t* headpos, const uint64
   if (h >= 0) flags_out[val[q]] = flags_out[val[h]];
 }
 
+struct FlagToInt {
+  __device__ int operator()(const uint8_t& f) const { return f ? 1 : 0; }
+};
+
 int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mask, cudaStream_t s) {
   const int64_t n = v.ev.n;
   const int ng = v.ev.n_groups;
@@ -228,10 +233,25 @@ int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mas
   XS_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
   const int64_t* lo = (const int64_t*)ctx->ptr[W_SPAN_LO];
   ProfScope ps_sort(ctx, ST_TRANS_SORT, s);
-  XS_LAUNCH(ctx, k_trec, grid_for(n), XS_BLOCK, 0, s, v, n, lo, tb, src_mask, dst_mask, key, val, cnt);
+  // groups renumbered densely over those with HIGH_LEVEL..ACCEL_API events
+  // (pass 1's flags): the key spends its bits on time, not on GPU streams
+  int* tg;
+  XS_TRY(ws(ctx, W_TGRP_IDX, ng + 1, s, &tg));
+  {
+    const uint8_t* tflag = (const uint8_t*)ctx->ptr[W_TGRP_FLAG];
+    cub::TransformInputIterator<int, FlagToInt, const uint8_t*> it(tflag, FlagToInt());
+    size_t temp = 0;
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, it, tg, ng, s));
+    void* t;
+    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
+    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, it, tg, ng, s));
+    ctx->launches += 2;
+  }
+  const int tgb = bits_for((uint64_t)(H.pad[6] > 1 ? H.pad[6] - 1 : 0));
+  XS_LAUNCH(ctx, k_trec, grid_for(n), XS_BLOCK, 0, s, v, n, lo, tb, src_mask, dst_mask, tg, key, val, cnt);
   // one sort on (group, t, kind); queries tying on it are put in descending
   // end order locally (the head of a same-start run has the largest end)
-  XS_TRY(sort_pairs_u64_u32(ctx, &key, &key_alt, &val, &val_alt, m, gb + tb + 4, s));
+  XS_TRY(sort_pairs_u64_u32(ctx, &key, &key_alt, &val, &val_alt, m, tgb + tb + 4, s));
   XS_LAUNCH(ctx, k_trec_tiefix, grid_for(m), XS_BLOCK, 0, s, key, val, m, v);
   uint64_t* k1 = key;
   uint32_t* v1 = val;
