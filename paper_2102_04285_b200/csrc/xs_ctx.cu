@@ -120,7 +120,7 @@ int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s
     std::string key = segment_key(ctx, "overlap", &v, sizeof(v));
     key.append(reinterpret_cast<const char*>(&attribution), sizeof(attribution));
     XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
-      XS_TRY(stage_corr_table(ctx, v, w));
+      XS_TRY(stage_corr_table(ctx, v, w, attribution == 1));
       XS_TRY(ops_with_overlap_pre(ctx, v, attribution, w));
       return stage_overlap(ctx, v, attribution, w);
     }));
@@ -374,7 +374,7 @@ static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* pro
   };
   {
     Join join{ctx, w};
-    XS_TRY(stage_corr_table(ctx, v, ctx->br_stream[0]));
+    XS_TRY(stage_corr_table(ctx, v, ctx->br_stream[0], false));
     ctx->skip_ops_reset = true;
     XS_TRY(stage_ops(ctx, v, ctx->br_stream[1], false));  // OPERATION nesting is part of require_valid
     ctx->skip_ops_reset = false;
@@ -554,7 +554,7 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     XS_TRY(stage_events_async(ctx, vc, w, false, nullptr));
     // correlations are untouched by the correction: the original's dangling
     // check stands, and only CORRELATION attribution needs launch instants
-    if (attribution == 1) XS_TRY(stage_corr_table(ctx, vc, w));
+    if (attribution == 1) XS_TRY(stage_corr_table(ctx, vc, w, true));
     XS_TRY(ops_with_overlap_pre(ctx, vc, attribution, w));
     XS_TRY(stage_overlap(ctx, vc, attribution, w));
     ctx->res_pids = ev->n_pids;

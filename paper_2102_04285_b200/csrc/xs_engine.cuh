@@ -350,7 +350,9 @@ struct EventView {  // by value: columns are device pointers; start/dur may be o
 int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool check_api, const xs_profile_t* prof);
 int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr_table, bool check_api,
                  const xs_profile_t* prof);
-int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s);
+// (pid, correlation) table: the dangling-correlation rule, plus per-GPU-event
+// launch instants when need_start (CORRELATION attribution)
+int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_start);
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths);
 int stage_overlap_pre(xs_ctx* ctx, const EventView& v, cudaStream_t s);
 int ops_with_overlap_pre(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t w);

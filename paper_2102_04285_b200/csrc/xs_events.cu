@@ -358,8 +358,10 @@ __device__ __forceinline__ uint64_t corr_hash(int p, int64_t corr) {
   return x;
 }
 
-// One 32-byte slot per entry (one DRAM sector per probe: key, pid, claim
-// state and the min launch start live together).
+// One slot per entry, one DRAM sector per probe: key, pid and claim state
+// (+ the min launch start when CORRELATION needs it) live together.  The
+// dangling-correlation check alone (INSTANT, validation, correction) uses
+// 16-byte slots: half the table to clear and probe.
 struct __align__(32) CorrSlot {
   int64_t key;
   int64_t start;
@@ -367,24 +369,29 @@ struct __align__(32) CorrSlot {
   int state;  // 0 empty, 1 being claimed, 2 published
   int64_t pad;
 };
+struct __align__(16) CorrSlot16 {
+  int64_t key;
+  int pid;
+  int state;
+};
 
-__global__ void k_corr_insert(EventView v, int64_t n, CorrSlot* tab, uint64_t mask, Stats* st) {
+template <class Slot, bool kStart>
+__global__ void k_corr_insert(EventView v, int64_t n, Slot* tab, uint64_t mask, Stats* st) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (v.ev.cat[i] != 4 || !v.ev.has_corr[i]) return;
   int p = v.ev.pid[i];
   int64_t corr = v.ev.corr[i];
-  int64_t s = v.start[i];
   uint64_t h = corr_hash(p, corr) & mask;
   for (uint64_t probe = 0; probe <= mask; probe++) {
-    CorrSlot* e = tab + h;
+    Slot* e = tab + h;
     volatile int* sp = &e->state;
     int cur = *sp;
     if (cur == 0) {
       if (atomicCAS(&e->state, 0, 1) == 0) {
         e->key = corr;
         e->pid = p;
-        e->start = s;
+        if constexpr (kStart) reinterpret_cast<CorrSlot*>(e)->start = v.start[i];
         __threadfence();
         atomicExch(&e->state, 2);
         return;
@@ -394,7 +401,7 @@ __global__ void k_corr_insert(EventView v, int64_t n, CorrSlot* tab, uint64_t ma
     while (cur == 1) cur = *sp;
     __threadfence();
     if (((volatile int64_t*)&e->key)[0] == corr && ((volatile int*)&e->pid)[0] == p) {
-      atomic_min_i64(&e->start, s);
+      if constexpr (kStart) atomic_min_i64(&reinterpret_cast<CorrSlot*>(e)->start, v.start[i]);
       return;
     }
     h = (h + 1) & mask;
@@ -403,29 +410,30 @@ __global__ void k_corr_insert(EventView v, int64_t n, CorrSlot* tab, uint64_t ma
 }
 
 // GPU events: dangling check; in CORRELATION mode record the launch instant
-__global__ void k_corr_query(EventView v, int64_t n, const CorrSlot* tab, uint64_t mask, Stats* st,
+template <class Slot, bool kStart>
+__global__ void k_corr_query(EventView v, int64_t n, const Slot* tab, uint64_t mask, Stats* st,
                              int64_t* launch_start) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (v.ev.cat[i] != 5) return;
   if (!v.ev.has_corr[i]) {
-    if (launch_start) launch_start[i] = INT64_MIN;
+    if (kStart) launch_start[i] = INT64_MIN;
     return;
   }
   int p = v.ev.pid[i];
   int64_t corr = v.ev.corr[i];
   uint64_t h = corr_hash(p, corr) & mask;
   for (uint64_t probe = 0; probe <= mask; probe++) {
-    const CorrSlot e = tab[h];
+    const Slot e = tab[h];
     if (e.state == 0) break;
     if (e.key == corr && e.pid == p) {
-      if (launch_start) launch_start[i] = e.start;
+      if constexpr (kStart) launch_start[i] = reinterpret_cast<const CorrSlot&>(e).start;
       return;
     }
     h = (h + 1) & mask;
   }
   atomicAdd((unsigned long long*)&st->n_bad, 1ull);
-  if (launch_start) launch_start[i] = INT64_MIN;
+  if (kStart) launch_start[i] = INT64_MIN;
 }
 
 // pass 1 without its sync: the statistics stay on the device
@@ -478,11 +486,11 @@ int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr
   XS_TRY(fetch_stats(ctx, s));
   if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;
   if (!need_corr_table) return XS_OK;
-  return stage_corr_table(ctx, v, s);
+  return stage_corr_table(ctx, v, s, false);
 }
 
 // (pid, correlation) table build + GPU-event query; no host sync (capturable)
-int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
+int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_start) {
   const xs_events_t* ev = &v.ev;
   const int64_t n = ev->n;
   Stats* st = (Stats*)ctx->ptr[W_STATS];
@@ -491,13 +499,22 @@ int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
   if (ngpu == 0) return XS_OK;
   uint64_t cap = 64;
   while (cap < (uint64_t)(2 * napi + 2)) cap <<= 1;
-  CorrSlot* tab;
-  XS_TRY(ws(ctx, W_CORR_STATE, cap, s, &tab));
-  XS_CUDA(cudaMemsetAsync(tab, 0, cap * sizeof(CorrSlot), s));
-  int64_t* launch = nullptr;
-  XS_TRY(ws(ctx, W_FIXED_LS, n + 1, s, &launch));
-  if (napi) XS_LAUNCH(ctx, k_corr_insert, grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st);
-  XS_LAUNCH(ctx, k_corr_query, grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st, launch);
+  if (need_start) {  // CORRELATION: launch instants per GPU event
+    CorrSlot* tab;
+    XS_TRY(ws(ctx, W_CORR_STATE, cap, s, &tab));
+    XS_CUDA(cudaMemsetAsync(tab, 0, cap * sizeof(CorrSlot), s));
+    int64_t* launch = nullptr;
+    XS_TRY(ws(ctx, W_FIXED_LS, n + 1, s, &launch));
+    if (napi) XS_LAUNCH(ctx, (k_corr_insert<CorrSlot, true>), grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st);
+    XS_LAUNCH(ctx, (k_corr_query<CorrSlot, true>), grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st, launch);
+  } else {  // the dangling-correlation rule only
+    CorrSlot16* tab;
+    XS_TRY(ws(ctx, W_CORR_KEY, cap, s, &tab));
+    XS_CUDA(cudaMemsetAsync(tab, 0, cap * sizeof(CorrSlot16), s));
+    if (napi) XS_LAUNCH(ctx, (k_corr_insert<CorrSlot16, false>), grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st);
+    XS_LAUNCH(ctx, (k_corr_query<CorrSlot16, false>), grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st,
+              (int64_t*)nullptr);
+  }
   return XS_OK;
 }
 
