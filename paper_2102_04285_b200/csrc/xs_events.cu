@@ -361,18 +361,13 @@ __device__ __forceinline__ uint64_t corr_hash(int p, int64_t corr) {
 // One slot per entry, one DRAM sector per probe: key, pid and claim state
 // (+ the min launch start when CORRELATION needs it) live together.  The
 // dangling-correlation check alone (INSTANT, validation, correction) uses
-// 16-byte slots: half the table to clear and probe.
+// the 16-byte set slots below: half the table to clear and probe.
 struct __align__(32) CorrSlot {
   int64_t key;
   int64_t start;
   int pid;
   int state;  // 0 empty, 1 being claimed, 2 published
   int64_t pad;
-};
-struct __align__(16) CorrSlot16 {
-  int64_t key;
-  int pid;
-  int state;
 };
 
 template <class Slot, bool kStart>
@@ -407,6 +402,58 @@ __global__ void k_corr_insert(EventView v, int64_t n, Slot* tab, uint64_t mask, 
     h = (h + 1) & mask;
   }
   atomicAdd((unsigned long long*)&st->table_full, 1ull);
+}
+
+// Set-only table (the dangling check): a slot is {correlation id, pid tag};
+// one 128-bit compare-and-swap claims or matches it (no claim state, no
+// fences).  The tag is never 0, so {0, 0} marks an empty slot.
+__device__ __forceinline__ uint64_t corr_tag(int p) { return (uint64_t)(uint32_t)p | (1ull << 32); }
+
+__device__ __forceinline__ void cas_b128(longlong2* addr, long long cmp_lo, long long cmp_hi, long long new_lo,
+                                         long long new_hi, long long* old_lo, long long* old_hi) {
+  asm volatile(
+      "{\n\t.reg .b128 d, c, n;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 n, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, n;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(*old_lo), "=l"(*old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
+      : "memory");
+}
+
+__global__ void k_corr_set_insert(EventView v, int64_t n, longlong2* tab, uint64_t mask, Stats* st) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (v.ev.cat[i] != 4 || !v.ev.has_corr[i]) return;
+  int p = v.ev.pid[i];
+  long long corr = v.ev.corr[i];
+  long long tag = (long long)corr_tag(p);
+  uint64_t h = corr_hash(p, corr) & mask;
+  for (uint64_t probe = 0; probe <= mask; probe++) {
+    long long lo, hi;
+    cas_b128(tab + h, 0, 0, corr, tag, &lo, &hi);
+    if (hi == 0 || (lo == corr && hi == tag)) return;
+    h = (h + 1) & mask;
+  }
+  atomicAdd((unsigned long long*)&st->table_full, 1ull);
+}
+
+__global__ void k_corr_set_query(EventView v, int64_t n, const longlong2* tab, uint64_t mask, Stats* st) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (v.ev.cat[i] != 5 || !v.ev.has_corr[i]) return;
+  int p = v.ev.pid[i];
+  long long corr = v.ev.corr[i];
+  long long tag = (long long)corr_tag(p);
+  uint64_t h = corr_hash(p, corr) & mask;
+  for (uint64_t probe = 0; probe <= mask; probe++) {
+    const longlong2 e = tab[h];
+    if (e.y == 0) break;
+    if (e.x == corr && e.y == tag) return;
+    h = (h + 1) & mask;
+  }
+  atomicAdd((unsigned long long*)&st->n_bad, 1ull);
 }
 
 // GPU events: dangling check; in CORRELATION mode record the launch instant
@@ -508,12 +555,11 @@ int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_
     if (napi) XS_LAUNCH(ctx, (k_corr_insert<CorrSlot, true>), grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st);
     XS_LAUNCH(ctx, (k_corr_query<CorrSlot, true>), grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st, launch);
   } else {  // the dangling-correlation rule only
-    CorrSlot16* tab;
+    longlong2* tab;
     XS_TRY(ws(ctx, W_CORR_KEY, cap, s, &tab));
-    XS_CUDA(cudaMemsetAsync(tab, 0, cap * sizeof(CorrSlot16), s));
-    if (napi) XS_LAUNCH(ctx, (k_corr_insert<CorrSlot16, false>), grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st);
-    XS_LAUNCH(ctx, (k_corr_query<CorrSlot16, false>), grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st,
-              (int64_t*)nullptr);
+    XS_CUDA(cudaMemsetAsync(tab, 0, cap * sizeof(longlong2), s));
+    if (napi) XS_LAUNCH(ctx, k_corr_set_insert, grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st);
+    XS_LAUNCH(ctx, k_corr_set_query, grid_for(n), XS_BLOCK, 0, s, v, n, tab, cap - 1, st);
   }
   return XS_OK;
 }
