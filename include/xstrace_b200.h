@@ -191,6 +191,40 @@ int xs_chunk_decode(const uint8_t* buf, int64_t len, const char* context, const 
                     const int32_t* name_map, int64_t* pid, int64_t* tid, uint8_t* cat, int32_t* name, int64_t* start,
                     int64_t* dur, int64_t* corr, uint8_t* has_corr, char* err, int errlen);
 
+/* Packed upload format (the host -> device wire layout of a columnar trace;
+ * ColumnarTrace.pinned builds it).  Every column keeps its exact values in
+ * the narrowest width that holds them: start as a per-256-row int64 base
+ * plus a 32-bit offset (or raw int64), dur / corr as 32 or 64 bits, pid / tid
+ * / name indices as 8, 16 or 32 bits, and cat | has_corr << 7 in one byte.
+ * A 32-bit start / dur / corr column may hold a few values that do not fit:
+ * their slot holds 0xFFFFFFFF and the exact value sits in the exception
+ * table (global row, column 0 start / 1 dur / 2 corr, value), sorted by row;
+ * pass the exceptions whose rows fall in [row0, row0 + n).
+ * xs_unpack widens rows [row0, row0 + n) of a packed trace (device pointers,
+ * possibly a slice) into the xs_events_t columns (device buffers of n rows).
+ * Replaces the per-column host -> device copies of the reference's in-process
+ * Trace (model.py:92): the result is bit-identical to the unpacked columns. */
+typedef struct {
+  int64_t n;                 /* rows to widen                                     */
+  int64_t row0;              /* global row of the first (start bases are per 256 */
+                             /* global rows; start_base[0] is block row0 >> 8)   */
+  const void* start;         /* [n] uint32 offsets (start_w 4) or int64 (8)       */
+  const int64_t* start_base; /* per 256-row block when start_w == 4               */
+  const void* dur;           /* [n] uint32 / int64                                 */
+  const void* pid;           /* [n] uint8 / uint16 / int32                         */
+  const void* tid;
+  const void* name;
+  const void* corr;          /* [n] uint32 / int64                                 */
+  const uint8_t* catf;       /* [n] cat | has_corr << 7                            */
+  int32_t start_w, dur_w, pid_w, tid_w, name_w, corr_w;
+  int64_t n_exc;             /* exceptions in this row range                      */
+  const int64_t* exc_row;    /* [n_exc] global rows                               */
+  const int64_t* exc_val;    /* [n_exc] exact values                              */
+  const uint8_t* exc_col;    /* [n_exc] 0 start, 1 dur, 2 corr                    */
+} xs_packed_t;
+int xs_unpack(xs_ctx_t* ctx, const xs_packed_t* pk, int64_t* start, int64_t* dur, int32_t* pid, int32_t* tid,
+              uint8_t* cat, int32_t* name, int64_t* corr, uint8_t* has_corr, xs_stream_t stream);
+
 /* Number of kernel launches issued by the library since context creation
  * (instrumentation for the bench's gpu_launches field). */
 int64_t xs_launch_count(xs_ctx_t* ctx);

@@ -28,6 +28,37 @@ def _torch():
     return torch
 
 
+def packed_ptrs(lay, dblock, a: int = 0) -> dict:
+    """Device addresses of row ``a`` of every packed column (and of the start
+    base of row a's 256-row block) in a device copy of the whole packed block."""
+    base = dblock.data_ptr()
+    p = {k: base + lay.offsets[k] + a * lay.widths[k] for k in ("start", "dur", "pid", "tid", "name", "corr", "catf")}
+    p["start_base"] = base + lay.offsets["start_base"] + (a // 256) * 8
+    for k in ("exc_row", "exc_val", "exc_col"):  # (the whole table: xs_unpack skips rows outside the range)
+        p[k] = base + lay.offsets[k]
+    return p
+
+
+def unpack_into(eng, lay, ptrs: dict, a: int, b: int, dst, stream=None) -> None:
+    """xs_unpack rows [a, b) of a packed trace (``ptrs``: device addresses of
+    row a of each packed column, see packed_ptrs) into the wide device
+    columns of ``dst`` (rows from 0)."""
+    torch = _torch()
+    w = lay.widths
+    pk = _lib.XsPacked()
+    pk.n, pk.row0 = b - a, a
+    for k in ("start", "start_base", "dur", "pid", "tid", "name", "corr", "catf"):
+        setattr(pk, k, ptrs[k])
+    pk.start_w, pk.dur_w, pk.pid_w, pk.tid_w, pk.name_w, pk.corr_w = (w["start"], w["dur"], w["pid"], w["tid"],
+                                                                      w["name"], w["corr"])
+    pk.n_exc = lay.n_exc
+    pk.exc_row, pk.exc_val, pk.exc_col = ptrs["exc_row"], ptrs["exc_val"], ptrs["exc_col"]
+    s = torch.cuda.current_stream(eng.device) if stream is None else stream
+    eng.check(eng.lib.xs_unpack(eng.ctx, C.byref(pk), dst.start.data_ptr(), dst.dur.data_ptr(), dst.pid.data_ptr(),
+                                dst.tid.data_ptr(), dst.cat.data_ptr(), dst.name.data_ptr(), dst.corr.data_ptr(),
+                                dst.has_corr.data_ptr(), C.c_void_p(s.cuda_stream)), "xs_unpack")
+
+
 class DeviceTrace:
     """Columns of a ColumnarTrace resident in device memory."""
 
@@ -39,6 +70,27 @@ class DeviceTrace:
 
         pinned = ct._pinned or {}
         block = pinned.get("_block")
+        lay = pinned.get("_packed")
+        if lay is not None:  # packed pinned block: one DMA of ~17-22 B/event, widened by xs_unpack
+            dblock = block.to(dev, non_blocking=True)
+            self._dblock = dblock
+            n = ct.n
+            self._wide = torch.empty(max(n, 1) * 38 + 64, dtype=torch.uint8, device=dev)
+            cols = {}
+            off = 0
+            for k, dt, w in (("start", torch.int64, 8), ("dur", torch.int64, 8), ("corr", torch.int64, 8),
+                             ("pid", torch.int32, 4), ("tid", torch.int32, 4), ("name", torch.int32, 4),
+                             ("cat", torch.uint8, 1), ("has_corr", torch.uint8, 1)):
+                cols[k] = self._wide[off:off + max(n, 1) * w].view(dt)
+                off += (max(n, 1) * w + 15) // 16 * 16
+            for k, t in cols.items():
+                setattr(self, k, t)
+            for k, dt in (("group_pid", torch.int32), ("pid_has_meta", torch.uint8)):
+                o, nb = lay.offsets[k], lay.nbytes[k]
+                setattr(self, k, dblock[o:o + nb].view(dt) if nb else torch.zeros(1, dtype=dt, device=dev))
+            if n:
+                unpack_into(get(device), lay, packed_ptrs(lay, dblock), 0, n, self)
+            return
         if block is not None:  # one pinned block (ColumnarTrace.pinned): one DMA, device views
             dblock = block.to(dev, non_blocking=True)
             self._dblock = dblock

@@ -32,6 +32,17 @@ class XsEvents(C.Structure):
     ]
 
 
+class XsPacked(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("row0", C.c_int64),
+        ("start", C.c_void_p), ("start_base", C.c_void_p), ("dur", C.c_void_p), ("pid", C.c_void_p),
+        ("tid", C.c_void_p), ("name", C.c_void_p), ("corr", C.c_void_p), ("catf", C.c_void_p),
+        ("start_w", C.c_int32), ("dur_w", C.c_int32), ("pid_w", C.c_int32), ("tid_w", C.c_int32),
+        ("name_w", C.c_int32), ("corr_w", C.c_int32),
+        ("n_exc", C.c_int64), ("exc_row", C.c_void_p), ("exc_val", C.c_void_p), ("exc_col", C.c_void_p),
+    ]
+
+
 class XsProfile(C.Structure):
     _fields_ = [
         ("L", C.c_int64), ("ann_start", C.c_int64), ("ann_end", C.c_int64),
@@ -79,6 +90,7 @@ SIGNATURES = {
     "xs_union_intervals_fetch": (C.c_int, [P, P, P, P]),
     "xs_chunk_info": (C.c_int, [P, C.c_int64, C.c_char_p, P, P, P, C.c_char_p, C.c_int]),
     "xs_chunk_decode": (C.c_int, [P, C.c_int64, C.c_char_p, P, P, P, P, P, P, P, P, P, P, C.c_char_p, C.c_int]),
+    "xs_unpack": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P]),
     "xs_launch_count": (C.c_int64, [P]),
     "xs_profile_enable": (C.c_int, [P, C.c_int]),
     "xs_profile_read": (C.c_int, [P, P, P, C.c_int]),

@@ -12,6 +12,7 @@ correction followed by overlap of the corrected trace, cli.py:168-171).
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+from types import SimpleNamespace
 from typing import Optional
 
 import numpy as np
@@ -242,17 +243,43 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
         _PIPE_BUFS[key] = bufs
     tables = {"group_pid": torch.from_numpy(np.ascontiguousarray(ct.group_pid, np.int32)).to(dev),
               "pid_has_meta": torch.from_numpy(np.ascontiguousarray(ct.pid_has_meta, np.uint8)).to(dev)}
+    lay = (ct._pinned or {}).get("_packed")
+    if lay is not None:  # packed pinned block: per batch, DMA the row slices, widen on the copy stream
+        pcols = ("start", "dur", "pid", "tid", "name", "corr", "catf")
+        pkey = (eng.device, rows_max, tuple(lay.widths[c] for c in pcols))
+        pbufs = _PIPE_BUFS.get(pkey)
+        if pbufs is None:
+            pbufs = [{c: torch.empty(rows_max * lay.widths[c] + 16, dtype=torch.uint8, device=dev) for c in pcols}
+                     for _ in range(2)]
+            for pb in pbufs:
+                pb["start_base"] = torch.empty((rows_max // 256 + 2) * 8, dtype=torch.uint8, device=dev)
+            _PIPE_BUFS[pkey] = pbufs
+        block = ct._pinned["_block"]
+        e0 = lay.offsets["exc_row"]  # the exception table (rows, values, columns: adjacent), whole, once per call
+        exc_dev = block[e0:e0 + max(lay.offsets["exc_col"] + lay.nbytes["exc_col"] - e0, 16)].to(dev, non_blocking=True)
 
     def upload(k):
         a, b = parts[k]
         buf = bufs[k % 2]
         with torch.cuda.stream(copy):
-            tens = {}
-            for c in cols:
-                src = subs[k]._pinned[c] if subs[k]._pinned is not None else torch.from_numpy(getattr(subs[k], c))
-                dst = buf[c][: b - a]
-                dst.copy_(src, non_blocking=True)
-                tens[c] = dst
+            tens = {c: buf[c][: b - a] for c in cols}
+            if lay is not None:
+                pb = pbufs[k % 2]
+                for c in pcols:
+                    o, w = lay.offsets[c], lay.widths[c]
+                    pb[c][: (b - a) * w].copy_(block[o + a * w:o + b * w], non_blocking=True)
+                o, b0, b1 = lay.offsets["start_base"], a // 256, (b - 1) // 256 + 1
+                if lay.widths["start"] == 4:
+                    pb["start_base"][: (b1 - b0) * 8].copy_(block[o + b0 * 8:o + b1 * 8], non_blocking=True)
+                ptrs = {c: t.data_ptr() for c, t in pb.items()}
+                ptrs.update({c: exc_dev.data_ptr() + lay.offsets[c] - lay.offsets["exc_row"]
+                             for c in ("exc_row", "exc_val", "exc_col")})
+                _engine.unpack_into(eng, lay, ptrs, a, b, SimpleNamespace(**tens), stream=copy)
+            else:
+                for c in cols:
+                    src = subs[k]._pinned[c] if subs[k]._pinned is not None else \
+                        torch.from_numpy(getattr(subs[k], c))
+                    tens[c].copy_(src, non_blocking=True)
             tens.update(tables)
             ev = torch.cuda.Event()
             ev.record(copy)

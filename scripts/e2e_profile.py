@@ -17,7 +17,7 @@ if os.environ.get("XS_CONFIG") == "5":
 else:
     ct = synth.ddpg_trace(27027)
     prof = synth.exact_profile()
-pin = ct.pinned()
+pin = ct.pinned(packed=os.environ.get("XS_PACKED", "1") == "1")
 hs = torch.empty(ct.n, dtype=torch.int64).pin_memory()
 hd = torch.empty(ct.n, dtype=torch.int64).pin_memory()
 for _ in range(2 if os.environ.get("XS_CONFIG") == "5" else 5):

@@ -196,14 +196,17 @@ def test_analyze_to_host_pinned_matches_device_outputs():
 
     un, inst = synth.ddpg_trace(3000, processes=2, outer_op="iteration", both=True)
     s, d, rep, bd = analyze_columnar(inst, synth.exact_profile())
-    pin = inst.pinned()
-    assert pin._pinned["start"].is_pinned() and np.array_equal(pin.start, inst.start)
-    for _ in range(3):  # eager, capture, replay
-        hs = torch.empty(inst.n, dtype=torch.int64).pin_memory()
-        hd = torch.empty(inst.n, dtype=torch.int64).pin_memory()
-        s2, d2, rep2, bd2 = analyze_columnar(pin, synth.exact_profile(), out=(hs, hd))
-        assert s2 is hs and np.array_equal(hs.numpy(), s.cpu().numpy()) and np.array_equal(hd.numpy(), un.dur)
-        assert bd2.cells == bd.cells and rep2.removed_ns == rep.removed_ns
+    wide = inst.pinned(packed=False)
+    assert wide._pinned["start"].is_pinned() and np.array_equal(wide.start, inst.start)
+    packed = inst.pinned()
+    assert packed._pinned["_block"].is_pinned() and packed._pinned["_block"].numel() < 20 * inst.n
+    for pin in (wide, packed):
+        for _ in range(3):  # eager, capture, replay
+            hs = torch.empty(inst.n, dtype=torch.int64).pin_memory()
+            hd = torch.empty(inst.n, dtype=torch.int64).pin_memory()
+            s2, d2, rep2, bd2 = analyze_columnar(pin, synth.exact_profile(), out=(hs, hd))
+            assert s2 is hs and np.array_equal(hs.numpy(), s.cpu().numpy()) and np.array_equal(hd.numpy(), un.dur)
+            assert bd2.cells == bd.cells and rep2.removed_ns == rep.removed_ns
 
 
 def test_pipelined_analyze_equals_one_call():
@@ -215,12 +218,12 @@ def test_pipelined_analyze_equals_one_call():
     for ct, prof in ((synth.config3_trace(processes=7, events_per_pid=30_000), synth.exact_profile()),
                      (synth.adversarial_trace(150_000, pids=12), synth.adversarial_profile())):
         s0, d0, rep0, bd0 = analyze_columnar(ct, prof)
-        pin = ct.pinned()
-        hs = torch.empty(ct.n, dtype=torch.int64).pin_memory()
-        hd = torch.empty(ct.n, dtype=torch.int64).pin_memory()
-        s1, d1, rep1, bd1 = analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=4)
-        assert np.array_equal(hs.numpy(), s0.cpu().numpy()) and np.array_equal(hd.numpy(), d0.cpu().numpy())
-        assert rep1.removed_ns == rep0.removed_ns and rep1.shortfall_ns == rep0.shortfall_ns
-        assert rep1.original_total_ns == rep0.original_total_ns
-        assert rep1.corrected_total_ns == rep0.corrected_total_ns
-        assert bd1 == bd0
+        for pin in (ct.pinned(), ct.pinned(packed=False), ct):
+            hs = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+            hd = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+            s1, d1, rep1, bd1 = analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=4)
+            assert np.array_equal(hs.numpy(), s0.cpu().numpy()) and np.array_equal(hd.numpy(), d0.cpu().numpy())
+            assert rep1.removed_ns == rep0.removed_ns and rep1.shortfall_ns == rep0.shortfall_ns
+            assert rep1.original_total_ns == rep0.original_total_ns
+            assert rep1.corrected_total_ns == rep0.corrected_total_ns
+            assert bd1 == bd0
