@@ -256,10 +256,17 @@ class Engine:
         info = _lib.XsOverlapInfo()
         self.check(self.lib.xs_overlap_info(self.ctx, C.byref(info)), "xs_overlap_info")
         nc, nn, np_ = int(info.n_cells), int(info.n_nodes), int(info.n_pids)
-        r = OverlapRaw(np.zeros(nc, np.int32), np.zeros(nc, np.int32), np.zeros(nc, np.int32),
-                       np.zeros(nc, np.int64), np.zeros(nn, np.int32), np.zeros(nn, np.int32),
-                       np.zeros(np_, np.int64), np.zeros(np_, np.int64), np.zeros(np_, np.int64),
-                       np.zeros(np_, np.uint8))
+        # one page-locked block (torch's caching host allocator: reused once
+        # the arrays of an earlier result are dropped) so the copy runs at
+        # DMA rate instead of through pageable staging; the arrays keep it alive
+        shapes = ((nc, np.int32), (nc, np.int32), (nc, np.int32), (nc, np.int64), (nn, np.int32), (nn, np.int32),
+                  (np_, np.int64), (np_, np.int64), (np_, np.int64), (np_, np.uint8))
+        offs, total = [], 0
+        for m, dt in shapes:
+            offs.append(total)
+            total += (m * np.dtype(dt).itemsize + 15) // 16 * 16
+        raw = _torch().empty(max(total, 16), dtype=_torch().uint8, pin_memory=True).numpy()
+        r = OverlapRaw(*[raw[o:o + m * np.dtype(dt).itemsize].view(dt) for o, (m, dt) in zip(offs, shapes)])
 
         def p(a):
             return a.ctypes.data if a.size else None
