@@ -180,28 +180,48 @@ __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const
   }
 }
 
-// per owner: budget caps (correction.py:139-153) + shortfall per (pid, hook)
+// per owner: budget caps (correction.py:139-153) + shortfall per (pid, hook);
+// shortfalls are summed per warp when the warp's owners share a pid (one
+// atomic per hook instead of one per capped site: skewed traces cap often)
 __global__ void k_caps(EventView v, int64_t n, const int* cnt, const int* pos, const int64_t* qslot, int64_t* lenslot,
                        int64_t* shortfall) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || cnt[i] == 0) return;
-  int c = v.ev.cat[i];
-  int at = pos[i];
-  int p = v.ev.pid[i];
-  int64_t budget = v.dur[i];
-  int64_t q1 = qslot[at];
-  int64_t c1 = q1 < budget ? q1 : budget;
-  budget -= c1;
-  lenslot[at] = c1;
-  int h1 = c == 0 ? H_ANN : (c == 4 ? H_IC : H_TRANS);
-  if (q1 != c1) atomic_add_i64(&shortfall[(int64_t)p * 4 + h1], q1 - c1);
-  if (cnt[i] == 2) {
-    int64_t q2 = qslot[at + 1];
-    int64_t c2 = q2 < budget ? q2 : budget;
-    lenslot[at + 1] = c2;
-    int h2 = c == 0 ? H_ANN : H_INT;
-    if (q2 != c2) atomic_add_i64(&shortfall[(int64_t)p * 4 + h2], q2 - c2);
+  if (i - threadIdx.x % 32 >= n) return;  // (whole warps leave together)
+  int64_t sf[4] = {0, 0, 0, 0};
+  int p = -1;
+  if (i < n && cnt[i] != 0) {
+    int c = v.ev.cat[i];
+    int at = pos[i];
+    p = v.ev.pid[i];
+    int64_t budget = v.dur[i];
+    int64_t q1 = qslot[at];
+    int64_t c1 = q1 < budget ? q1 : budget;
+    budget -= c1;
+    lenslot[at] = c1;
+    sf[c == 0 ? H_ANN : (c == 4 ? H_IC : H_TRANS)] += q1 - c1;
+    if (cnt[i] == 2) {
+      int64_t q2 = qslot[at + 1];
+      int64_t c2 = q2 < budget ? q2 : budget;
+      lenslot[at + 1] = c2;
+      sf[c == 0 ? H_ANN : H_INT] += q2 - c2;
+    }
   }
+  const bool any = sf[0] | sf[1] | sf[2] | sf[3];
+  const unsigned who = __ballot_sync(0xffffffffu, any);
+  if (!who) return;
+  const int leader_p = __shfl_sync(0xffffffffu, p, __ffs(who) - 1);
+  if (__all_sync(0xffffffffu, !any || p == leader_p)) {
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      int64_t x = sf[h];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (threadIdx.x % 32 == 0 && x) atomic_add_i64(&shortfall[(int64_t)leader_p * 4 + h], x);
+    }
+    return;
+  }
+  for (int h = 0; h < 4; h++)
+    if (sf[h]) atomic_add_i64(&shortfall[(int64_t)p * 4 + h], sf[h]);
 }
 
 // (max,+) RemovalMap scan, segmented by pid; slab count is global

@@ -317,33 +317,38 @@ __global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, cons
   }
 }
 
-// per-pid span reduction for the max key width; also counts multi-tid op pids
+// per-pid span reduction for the max key width; also counts multi-tid op pids.
+// One warp per pid: a pid's groups (hundreds of GPU-stream tids in skewed
+// traces) are counted lane-strided.
 __global__ void k_pid_finish(const int64_t* lo, const int64_t* hi, int np, const int32_t* group_pid,
                              const int* group_ops, const uint8_t* tflag, int ng, int* pid_group0, Stats* st) {
-  int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < np && lo[p] != INT64_MAX) atomicMax(&st->max_span, (long long)(hi[p] - lo[p]));
+  const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p > np) return;
+  if (lane == 0 && p < np && lo[p] != INT64_MAX) atomicMax(&st->max_span, (long long)(hi[p] - lo[p]));
   // first group of each pid (groups are sorted by pid): binary search
-  if (p <= np) {
-    int a = 0, b = ng;
-    while (a < b) {
-      int m = (a + b) >> 1;
-      if (group_pid[m] < p) a = m + 1;
-      else b = m;
-    }
-    pid_group0[p] = a;
+  int a = 0, b = ng;
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (group_pid[m] < p) a = m + 1;
+    else b = m;
   }
-  if (p < np) {
-    int a = pid_group0[p];
-    int cnt = 0;
-    int tcnt = 0;
-    for (int g = a; g < ng && group_pid[g] == p; g++) {
-      cnt += group_ops[g] > 0;
-      tcnt += tflag[g] != 0;
-    }
-    if (tcnt) atomicAdd((unsigned long long*)&st->pad[6], (unsigned long long)tcnt);  // transition-key groups
-    if (cnt > 1) atomicAdd((unsigned long long*)&st->multi_op_pids, 1ull);
-    if (cnt) atomicAdd((unsigned long long*)&st->pad[5], (unsigned long long)cnt);  // groups carrying ops
+  if (lane == 0) pid_group0[p] = a;
+  if (p == np) return;
+  int cnt = 0, tcnt = 0;
+  for (int g = a + lane; g < ng && group_pid[g] == p; g += 32) {
+    cnt += group_ops[g] > 0;
+    tcnt += tflag[g] != 0;
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    tcnt += __shfl_xor_sync(0xffffffffu, tcnt, o);
+  }
+  if (lane) return;
+  if (tcnt) atomicAdd((unsigned long long*)&st->pad[6], (unsigned long long)tcnt);  // transition-key groups
+  if (cnt > 1) atomicAdd((unsigned long long*)&st->multi_op_pids, 1ull);
+  if (cnt) atomicAdd((unsigned long long*)&st->pad[5], (unsigned long long)cnt);  // groups carrying ops
 }
 
 // ---------------------------------------------------------------------------
@@ -522,7 +527,7 @@ int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool che
       XS_LAUNCH(ctx, k_pass1<false>, p1_grid, XS_BLOCK, 0, s, v, n, ev->pid_has_meta,
                 hasint, check, st, lo, hi, pid_ops, group_ops, tflag);
   }
-  XS_LAUNCH(ctx, k_pid_finish, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, np, ev->group_pid, group_ops, tflag, ng,
+  XS_LAUNCH(ctx, k_pid_finish, grid_for((int64_t)(np + 1) * 32), XS_BLOCK, 0, s, lo, hi, np, ev->group_pid, group_ops, tflag, ng,
             pid_group0, st);
   return XS_OK;
 }

@@ -42,9 +42,12 @@ struct OpPred {
 // operations (opg, order-preserving): the sort key then spends bits on the
 // few op groups, not on every GPU stream of the trace (config 5: 16k groups,
 // 256 with ops), which keeps the bucket sort's buckets fine.
-__global__ void k_op_groups(const int* group_ops, int ng, const int* opg, int* opg_inv) {
+__global__ void k_op_groups(const int* group_ops, int ng, int* opg, int* opg_inv) {
   int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < ng && group_ops[g] > 0) opg_inv[opg[g]] = g;
+  if (g >= ng) return;
+  const int has = group_ops[g] > 0;
+  if (has) opg_inv[opg[g]] = g;
+  if (g == ng - 1) opg[ng] = opg[g] + has;  // (per-pid op-group ranges: opg[first group of p .. of p+1])
 }
 
 struct HasOps {
@@ -290,7 +293,8 @@ __global__ void k_pid_keys(const uint64_t* skeys, int64_t n2, const int32_t* gro
 constexpr int MAXD = 256;
 
 // general case: rank-merge of every tid's chain at each run end of the pid order
-__global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const int* pid_group0, const int* group_ops,
+__global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const int* pid_group0, const int* opg,
+                                  const int* opg_inv, const int* group_ops,
                                   const int64_t* gs_off, const uint64_t* skeys, const uint32_t* svals,
                                   const int* parent, const int* node, const int* rank_ev, EventView v,
                                   int* pidpath, TrieView t, Stats* st) {
@@ -310,8 +314,11 @@ __global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const 
   uint64_t tt = key & tmask;
   int ctxs[64];
   int nctx = 0;
-  int g0 = pid_group0[p], g1 = pid_group0[p + 1];
-  for (int g = g0; g < g1; g++) {
+  // only the pid's op-carrying groups (dense numbering): a pid with hundreds
+  // of GPU-stream tids has a handful of op tids
+  const int x0 = opg[pid_group0[p]], x1 = opg[pid_group0[p + 1]];
+  for (int x = x0; x < x1; x++) {
+    const int g = opg_inv[x];
     int cnt = group_ops[g];
     if (!cnt) continue;
     int64_t a = gs_off[g], b = a + 2 * (int64_t)cnt;
@@ -598,7 +605,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
     XS_LAUNCH(ctx, k_gs_off, 1, 1024, 0, s, group_ops_pos, ng, gs_off);
     XS_TRY(sort_keys_u64(ctx, &pk, &pk_alt, 2 * m, pb + tb + 1, s));
     XS_LAUNCH(ctx, k_pidpath_general, grid_for(2 * m, 128), 128, 0, s, pk, 2 * m, tb, (int*)ctx->ptr[W_PID_GROUP0],
-              group_ops_pos, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st);
+              opg, opg_inv, group_ops_pos, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st);
     os.pk = pk;
   }
   return XS_OK;
