@@ -1,4 +1,5 @@
 #include <algorithm>
+#include <cstdio>
 // xs_ctx.cu -- C ABI entry points, workspace and sort plumbing.
 #include <cub/device/device_radix_sort.cuh>
 
@@ -23,6 +24,8 @@ int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
   if (bytes < 256) bytes = 256;
   if (ctx->cap[slot] < bytes) {
     if (ctx->capturing) return XS_CAPTURE_ABORT;  // never allocate inside a graph capture
+    static const bool dbg = getenv("XS_DEBUG_GRAPH") != nullptr;
+    if (dbg) fprintf(stderr, "[xs ws] slot %d grows %zu -> %zu\n", slot, ctx->cap[slot], bytes);
     ctx->ws_generation++;
     if (ctx->ptr[slot]) XS_CUDA(cudaFreeAsync(ctx->ptr[slot], s));
     size_t nb = bytes + bytes / 4;

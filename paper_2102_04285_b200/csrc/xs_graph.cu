@@ -11,6 +11,9 @@
 // marked non-capturable and keeps running eagerly.
 #include "xs_engine.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace xs {
 
 std::string segment_key(xs_ctx* ctx, const char* tag, const void* extra, size_t extra_bytes) {
@@ -46,10 +49,11 @@ static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
       }
     return XS_OK;
   }
-  if (!ctx->graph_seen.count(key)) {  // first sighting: eager (sizes the workspace)
-    ctx->graph_seen.insert(key);
-    return body();
-  }
+  static const bool dbg = getenv("XS_DEBUG_GRAPH") != nullptr;
+  if (dbg) fprintf(stderr, "[xs graph] %s miss (%zu graphs)\n", key.c_str(), ctx->graphs.size());
+  // A miss is captured at once.  If the workspace must grow, the capture
+  // aborts at the first allocation (ws_get) and the segment runs eagerly,
+  // sizing the workspace; the next call (new generation in its key) captures.
   const long long l0 = ctx->launches;
   const size_t p0 = ctx->pend_stage.size();
   if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
@@ -75,11 +79,12 @@ static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
   ctx->pend_stage.resize(p0);
   ctx->pend_a.resize(p0);
   ctx->pend_b.resize(p0);
-  if (st != XS_OK || e != cudaSuccess || !exec) {  // not capturable: eager from now on
+  if (st != XS_OK || e != cudaSuccess || !exec) {  // workspace growth, or not capturable: eager
+    if (exec) cudaGraphExecDestroy(exec);
     cudaGetLastError();
     ctx->err.clear();
     ctx->launches = l0;
-    ctx->graph_bad.insert(key);
+    if (st != XS_CAPTURE_ABORT) ctx->graph_bad.insert(key);  // (eager from now on)
     return body();
   }
   ge.exec = exec;
