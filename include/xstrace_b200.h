@@ -145,6 +145,14 @@ int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, i
 int xs_analyze_to_host(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
                        int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* out_start_host, int64_t* out_dur_host,
                        int64_t* bad_event, xs_stream_t stream);
+/* The same, returning with the D2H still in flight on the context's copy
+ * stream: it overlaps the caller's next call (batched analyses).  The device
+ * outputs must stay allocated and the host buffers unread until
+ * xs_host_copy_wait, which waits for every copy issued so far. */
+int xs_analyze_to_host_async(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
+                             int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* out_start_host,
+                             int64_t* out_dur_host, int64_t* bad_event, xs_stream_t stream);
+int xs_host_copy_wait(xs_ctx_t* ctx);
 
 /* transition_sites (overlap.py:263-289) for the pairs selected by pair_mask
  * (bit k = TRANSITION_PAIRS[k]).  *n_out = number of sites; fetch the

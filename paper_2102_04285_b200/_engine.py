@@ -302,7 +302,7 @@ class Engine:
         return prof, (internal, has)
 
     def correct(self, dt: DeviceTrace, scaled, analyze_attribution: Optional[int] = None,
-                host_out=None) -> CorrectRaw:
+                host_out=None, dev_out=None, async_copy: bool = False) -> CorrectRaw:
         """xs_correct, or xs_analyze when analyze_attribution is given.  With
         ``host_out`` = (start, dur) host int64 buffers (pinned for overlap)
         the corrected columns are also copied there, overlapped with the
@@ -310,8 +310,11 @@ class Engine:
         torch = _torch()
         dev = torch.device("cuda", self.device)
         n = max(dt.ct.n, 1)
-        out_s = torch.empty(n, dtype=torch.int64, device=dev)
-        out_d = torch.empty(n, dtype=torch.int64, device=dev)
+        if dev_out is not None:  # caller-owned (async_copy: must outlive the copy, see host_copy_wait)
+            out_s, out_d = dev_out
+        else:
+            out_s = torch.empty(n, dtype=torch.int64, device=dev)
+            out_d = torch.empty(n, dtype=torch.int64, device=dev)
         ev = dt.struct()
         prof, keep = self._profile(dt, scaled)
         bad = C.c_int64(-1)
@@ -319,7 +322,8 @@ class Engine:
             st = self.lib.xs_correct(self.ctx, C.byref(ev), C.byref(prof), out_s.data_ptr(), out_d.data_ptr(),
                                      C.byref(bad), self.stream())
         elif host_out is not None:
-            st = self.lib.xs_analyze_to_host(self.ctx, C.byref(ev), C.byref(prof), analyze_attribution,
+            fn = self.lib.xs_analyze_to_host_async if async_copy else self.lib.xs_analyze_to_host
+            st = fn(self.ctx, C.byref(ev), C.byref(prof), analyze_attribution,
                                              out_s.data_ptr(), out_d.data_ptr(), _host_ptr(host_out[0]),
                                              _host_ptr(host_out[1]), C.byref(bad), self.stream())
         else:
@@ -338,6 +342,10 @@ class Engine:
         return CorrectRaw(out_s[: dt.ct.n], out_d[: dt.ct.n], removed[: P * 4].reshape(P, 4),
                           shortfall[: P * 4].reshape(P, 4), int(info.original_total), int(info.corrected_total),
                           int(info.n_sites), int(info.n_slabs))
+
+    def host_copy_wait(self) -> None:
+        """Wait for every corrected-column copy of correct(async_copy=True)."""
+        self.check(self.lib.xs_host_copy_wait(self.ctx), "xs_host_copy_wait")
 
     def remap(self, pid_idx: np.ndarray, values: np.ndarray) -> np.ndarray:
         torch = _torch()

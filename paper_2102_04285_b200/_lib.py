@@ -81,6 +81,9 @@ SIGNATURES = {
                              C.POINTER(C.c_int64), P]),
     "xs_analyze_to_host": (C.c_int, [P, C.POINTER(XsEvents), C.POINTER(XsProfile), C.c_int, P, P, P, P,
                                      C.POINTER(C.c_int64), P]),
+    "xs_analyze_to_host_async": (C.c_int, [P, C.POINTER(XsEvents), C.POINTER(XsProfile), C.c_int, P, P, P, P,
+                                           C.POINTER(C.c_int64), P]),
+    "xs_host_copy_wait": (C.c_int, [P]),
     "xs_transition_sites": (C.c_int, [P, C.POINTER(XsEvents), C.c_int, C.POINTER(C.c_int64), P]),
     "xs_transition_fetch": (C.c_int, [P, P, P, P]),
     "xs_union": (C.c_int, [P, C.POINTER(XsEvents), C.c_int, C.c_int, P, C.POINTER(C.c_int64),

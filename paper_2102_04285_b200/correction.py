@@ -285,17 +285,42 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
             ev.record(copy)
         return _engine.DeviceTrace.from_tensors(subs[k], tens, eng.device), ev
 
+    okey = (eng.device, "out", ct.n)  # corrected columns of every batch (disjoint slices: no reuse while copying)
+    dev_out = _PIPE_BUFS.get(okey)
+    if dev_out is None:
+        dev_out = tuple(torch.empty(ct.n, dtype=torch.int64, device=dev) for _ in range(2))
+        _PIPE_BUFS[okey] = dev_out
     rep = CorrectionReport()
     bd_all = None
     raws = []
+    try:
+        bd_all = _pipelined_batches(ct, eng, parts, subs, upload, compute, scaled, attr, out, dev_out, rep, raws)
+    finally:  # every batch's corrected columns are in `out` (also when a batch raised)
+        eng.host_copy_wait()
+
+    def build():  # the cells dict, on first access (pids are disjoint across batches)
+        cells = {}
+        for sub, ov in raws:
+            cells.update(_decode_cells(sub, ov))
+        return cells
+
+    bd_all._lazy = build
+    return out[0], out[1], rep, bd_all
+
+
+def _pipelined_batches(ct, eng, parts, subs, upload, compute, scaled, attr, out, dev_out, rep, raws):
+    from .overlap import _decode_breakdown
+
+    bd_all = None
     nxt = upload(0)
     for k, (a, b) in enumerate(parts):
         dt, ev = nxt
         compute.wait_event(ev)
         if k + 1 < len(parts):
             nxt = upload(k + 1)  # overlaps the analysis below
-        try:
-            raw = eng.correct(dt, scaled, attr, host_out=(out[0][a:b], out[1][a:b]))
+        try:  # the batch's D2H overlaps the next batch's analysis (waited for once, below)
+            raw = eng.correct(dt, scaled, attr, host_out=(out[0][a:b], out[1][a:b]),
+                              dev_out=(dev_out[0][a:b], dev_out[1][a:b]), async_copy=True)
         except _engine.UncalibratedEvent as exc:
             name = ct.names[int(subs[k].name[exc.index])]
             raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile") from None
@@ -317,12 +342,4 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
             bd_all.spans.update(bd.spans)
             bd_all.untracked.update(bd.untracked)
         del dt
-
-    def build():  # the cells dict, on first access (pids are disjoint across batches)
-        cells = {}
-        for sub, ov in raws:
-            cells.update(_decode_cells(sub, ov))
-        return cells
-
-    bd_all._lazy = build
-    return out[0], out[1], rep, bd_all
+    return bd_all

@@ -487,6 +487,15 @@ int xs_analyze(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, i
   });
 }
 
+static int ensure_d2h(xs_ctx* ctx) {
+  if (!ctx->d2h_stream) {
+    XS_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    XS_CUDA(cudaEventCreateWithFlags(&ctx->d2h_fork, cudaEventDisableTiming));
+    XS_CUDA(cudaEventCreateWithFlags(&ctx->d2h_join, cudaEventDisableTiming));
+  }
+  return XS_OK;
+}
+
 int xs_analyze_to_host(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
                        int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* out_start_host, int64_t* out_dur_host,
                        int64_t* bad_event, xs_stream_t stream) {
@@ -494,15 +503,34 @@ int xs_analyze_to_host(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t*
   if (attribution != 0 && attribution != 1) return XS_BAD_ARGUMENT;
   if (ev->n > 0 && (!out_start_host || !out_dur_host)) return XS_BAD_ARGUMENT;
   cudaSetDevice(ctx->device);
-  if (!ctx->d2h_stream) {
-    XS_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
-    XS_CUDA(cudaEventCreateWithFlags(&ctx->d2h_fork, cudaEventDisableTiming));
-    XS_CUDA(cudaEventCreateWithFlags(&ctx->d2h_join, cudaEventDisableTiming));
-  }
+  XS_TRY(ensure_d2h(ctx));
+  const int st = with_lsd_retry(ctx, [&] {
+    return analyze_once(ctx, ev, prof, attribution, out_start_dev, out_dur_dev, out_start_host, out_dur_host,
+                        bad_event, (cudaStream_t)stream);
+  });
+  if (ev->n > 0) XS_CUDA(cudaEventSynchronize(ctx->d2h_join));  // (host buffers complete on return)
+  return st;
+}
+
+int xs_analyze_to_host_async(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
+                             int64_t* out_start_dev, int64_t* out_dur_dev, int64_t* out_start_host,
+                             int64_t* out_dur_host, int64_t* bad_event, xs_stream_t stream) {
+  XS_TRY(check_events(ctx, ev));
+  if (attribution != 0 && attribution != 1) return XS_BAD_ARGUMENT;
+  if (ev->n > 0 && (!out_start_host || !out_dur_host)) return XS_BAD_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  XS_TRY(ensure_d2h(ctx));
   return with_lsd_retry(ctx, [&] {
     return analyze_once(ctx, ev, prof, attribution, out_start_dev, out_dur_dev, out_start_host, out_dur_host,
                         bad_event, (cudaStream_t)stream);
   });
+}
+
+int xs_host_copy_wait(xs_ctx_t* ctx) {
+  if (!ctx) return XS_BAD_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (ctx->d2h_join) XS_CUDA(cudaEventSynchronize(ctx->d2h_join));
+  return XS_OK;
 }
 
 static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int attribution,
@@ -530,24 +558,7 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
   key.append(reinterpret_cast<const char*>(&out_start_host), sizeof(out_start_host));
   key.append(reinterpret_cast<const char*>(&out_dur_host), sizeof(out_dur_host));
   const bool to_host = out_start_host && ev->n > 0;
-  XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
-    XS_TRY(correct_body(ctx, v, prof, out_start_dev, out_dur_dev, false, w));
-    if (to_host) {  // the corrected columns are final: their D2H overlaps the overlap pass
-      XS_CUDA(cudaEventRecord(ctx->d2h_fork, w));
-      XS_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->d2h_fork, 0));
-      XS_CUDA(cudaMemcpyAsync(out_start_host, out_start_dev, ev->n * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
-      XS_CUDA(cudaMemcpyAsync(out_dur_host, out_dur_dev, ev->n * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
-      XS_CUDA(cudaEventRecord(ctx->d2h_join, ctx->d2h_stream));
-    }
-    struct Join {  // the copy stream rejoins the segment's stream on every exit
-      xs_ctx* c;
-      cudaStream_t w;
-      bool on;
-      ~Join() {
-        if (on) cudaStreamWaitEvent(w, c->d2h_join, 0);
-      }
-    } join{ctx, w, to_host};
-    if (!spec) return XS_OK;
+  auto spec_body = [&](cudaStream_t w) -> int {
     XS_CUDA(cudaMemcpyAsync(saved, st, sizeof(Stats), cudaMemcpyDeviceToDevice, w));
     // INSTANT: ops shrunk to zero length are excluded by sentinel keys, so the
     // pass stays valid; CORRELATION keeps the guard (discard and redo)
@@ -562,7 +573,26 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     XS_TRY(stage_overlap(ctx, vc, attribution, w));
     ctx->res_pids = ev->n_pids;
     return corrected_total_from_spans(ctx, w);
-  }));
+  };
+  if (!to_host) {
+    XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
+      XS_TRY(correct_body(ctx, v, prof, out_start_dev, out_dur_dev, false, w));
+      return spec ? spec_body(w) : XS_OK;
+    }));
+  } else {
+    // two graph segments: the corrected columns are final after the first,
+    // and their D2H on the copy stream overlaps the overlap pass -- and, for
+    // xs_analyze_to_host_async, the caller's next call
+    XS_TRY(run_segment(ctx, s, key + "C", true, [&](cudaStream_t w) -> int {
+      return correct_body(ctx, v, prof, out_start_dev, out_dur_dev, false, w);
+    }));
+    XS_CUDA(cudaEventRecord(ctx->d2h_fork, s));
+    XS_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->d2h_fork, 0));
+    XS_CUDA(cudaMemcpyAsync(out_start_host, out_start_dev, ev->n * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    XS_CUDA(cudaMemcpyAsync(out_dur_host, out_dur_dev, ev->n * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    XS_CUDA(cudaEventRecord(ctx->d2h_join, ctx->d2h_stream));
+    if (spec) XS_TRY(run_segment(ctx, s, key + "O", true, spec_body));
+  }
   ctx->corr_pids = ev->n_pids;
   if (spec) XS_CUDA(cudaMemcpyAsync(ctx->h_stats + 1, saved, sizeof(Stats), cudaMemcpyDeviceToHost, s));
   XS_TRY(prefetch_report(ctx, s));
