@@ -414,6 +414,22 @@ class UncalibratedEvent(Exception):
         super().__init__(index)
 
 
+_aux: dict = {}
+
+
+def get_aux(device: int, k: int) -> Engine:
+    """The k-th extra context on a device (k >= 1; k = 0 is get(device)):
+    concurrent analyses each need their own workspace and graphs."""
+    if k == 0:
+        return get(device)
+    with _lock:
+        eng = _aux.get((device, k))
+        if eng is None:
+            eng = Engine(device)
+            _aux[(device, k)] = eng
+        return eng
+
+
 def get(device: int = 0) -> Engine:
     with _lock:
         eng = _engines.get(device)

@@ -200,7 +200,7 @@ def _row_slice(ct: ColumnarTrace, a: int, b: int) -> ColumnarTrace:
 
 
 def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, out, attribution=None,
-                               batches: int = 8):
+                               batches: int = 8, workers: int = 2):
     """analyze_columnar for host-resident traces of many processes, with the
     upload of the next batch of pids overlapping the analysis of the current
     one (per-pid independence: overlap.py:126, correction.py:132).  Needs
@@ -209,7 +209,7 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     Returns (start, dur, report, Breakdown) like analyze_columnar."""
     import torch
 
-    from .overlap import Attribution, _decode_breakdown, _decode_cells
+    from .overlap import Attribution, _decode_cells
 
     parts = _pid_batches(ct, batches)
     # a dominant pid (skewed traces) leaves nothing to overlap: one call is cheaper
@@ -220,8 +220,6 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
     eng = _engine.get()
     dev = torch.device("cuda", eng.device)
-    compute = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
     scaled = profile.scaled(ct.names)
     scaled.check_int128(3 * ct.n + 8)
     subs = [_row_slice(ct, a, b) for a, b in parts]
@@ -230,51 +228,62 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     for sub, (a, b) in zip(subs, parts):  # pids present in each batch, from the pid row ranges
         sub.__dict__["_present_mask"] = has & (starts[:-1] >= a) & (starts[:-1] < b)
 
-    # two persistent device buffer sets (double buffering): stable addresses
+    # per worker (one context and stream each, batches k = w, w + W, ...): two
+    # persistent device buffer sets (double buffering) whose stable addresses
     # keep every batch's captured pipeline graph valid across calls
+    W = max(1, min(int(workers), len(parts)))
+    engines = [_engine.get_aux(eng.device, w) for w in range(W)]
     cols = ("start", "dur", "pid", "tid", "cat", "name", "corr", "has_corr")
     rows_max = max(b - a for a, b in parts)
-    key = (eng.device, rows_max)
-    bufs = _PIPE_BUFS.get(key)
-    if bufs is None:
+    lay = (ct._pinned or {}).get("_packed")
+    pcols = ("start", "dur", "pid", "tid", "name", "corr", "catf")
+    key = (eng.device, rows_max, W, tuple(lay.widths[c] for c in pcols) if lay is not None else None)
+    state = _PIPE_BUFS.get(key)
+    if state is None:
         _PIPE_BUFS.clear()
-        bufs = [{c: torch.empty(rows_max, dtype=_engine.torch_dtype(getattr(ct, c).dtype), device=dev) for c in cols}
-                for _ in range(2)]
-        _PIPE_BUFS[key] = bufs
+        state = []
+        for w in range(W):
+            st = {"bufs": [{c: torch.empty(rows_max, dtype=_engine.torch_dtype(getattr(ct, c).dtype), device=dev)
+                            for c in cols} for _ in range(2)]}
+            if lay is not None:
+                st["pbufs"] = [{c: torch.empty(rows_max * lay.widths[c] + 16, dtype=torch.uint8, device=dev)
+                                for c in pcols} for _ in range(2)]
+                for pb in st["pbufs"]:
+                    pb["start_base"] = torch.empty((rows_max // 256 + 2) * 8, dtype=torch.uint8, device=dev)
+            state.append(st)
+        _PIPE_BUFS[key] = state
+    for w in range(W):
+        state[w]["copy"] = torch.cuda.Stream(dev)
+        state[w]["compute"] = torch.cuda.Stream(dev)
     tables = {"group_pid": torch.from_numpy(np.ascontiguousarray(ct.group_pid, np.int32)).to(dev),
               "pid_has_meta": torch.from_numpy(np.ascontiguousarray(ct.pid_has_meta, np.uint8)).to(dev)}
-    lay = (ct._pinned or {}).get("_packed")
     if lay is not None:  # packed pinned block: per batch, DMA the row slices, widen on the copy stream
-        pcols = ("start", "dur", "pid", "tid", "name", "corr", "catf")
-        pkey = (eng.device, rows_max, tuple(lay.widths[c] for c in pcols))
-        pbufs = _PIPE_BUFS.get(pkey)
-        if pbufs is None:
-            pbufs = [{c: torch.empty(rows_max * lay.widths[c] + 16, dtype=torch.uint8, device=dev) for c in pcols}
-                     for _ in range(2)]
-            for pb in pbufs:
-                pb["start_base"] = torch.empty((rows_max // 256 + 2) * 8, dtype=torch.uint8, device=dev)
-            _PIPE_BUFS[pkey] = pbufs
         block = ct._pinned["_block"]
         e0 = lay.offsets["exc_row"]  # the exception table (rows, values, columns: adjacent), whole, once per call
         exc_dev = block[e0:e0 + max(lay.offsets["exc_col"] + lay.nbytes["exc_col"] - e0, 16)].to(dev, non_blocking=True)
+    ready = torch.cuda.Event()
+    ready.record(torch.cuda.current_stream(dev))
 
-    def upload(k):
+    def upload(k, w):
         a, b = parts[k]
-        buf = bufs[k % 2]
+        st = state[w]
+        par = (k // W) % 2
+        buf, copy, e = st["bufs"][par], st["copy"], engines[w]
         with torch.cuda.stream(copy):
+            copy.wait_event(ready)
             tens = {c: buf[c][: b - a] for c in cols}
             if lay is not None:
-                pb = pbufs[k % 2]
+                pb = st["pbufs"][par]
                 for c in pcols:
-                    o, w = lay.offsets[c], lay.widths[c]
-                    pb[c][: (b - a) * w].copy_(block[o + a * w:o + b * w], non_blocking=True)
+                    o, wd = lay.offsets[c], lay.widths[c]
+                    pb[c][: (b - a) * wd].copy_(block[o + a * wd:o + b * wd], non_blocking=True)
                 o, b0, b1 = lay.offsets["start_base"], a // 256, (b - 1) // 256 + 1
                 if lay.widths["start"] == 4:
                     pb["start_base"][: (b1 - b0) * 8].copy_(block[o + b0 * 8:o + b1 * 8], non_blocking=True)
                 ptrs = {c: t.data_ptr() for c, t in pb.items()}
                 ptrs.update({c: exc_dev.data_ptr() + lay.offsets[c] - lay.offsets["exc_row"]
                              for c in ("exc_row", "exc_val", "exc_col")})
-                _engine.unpack_into(eng, lay, ptrs, a, b, SimpleNamespace(**tens), stream=copy)
+                _engine.unpack_into(e, lay, ptrs, a, b, SimpleNamespace(**tens), stream=copy)
             else:
                 for c in cols:
                     src = subs[k]._pinned[c] if subs[k]._pinned is not None else \
@@ -290,13 +299,39 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     if dev_out is None:
         dev_out = tuple(torch.empty(ct.n, dtype=torch.int64, device=dev) for _ in range(2))
         _PIPE_BUFS[okey] = dev_out
+    results = [None] * len(parts)
+
+    def worker(w):
+        with torch.cuda.stream(state[w]["compute"]):
+            _pipelined_batches(ct, engines[w], parts, list(range(w, len(parts), W)), subs, upload, w,
+                               state[w]["compute"], scaled, attr, out, dev_out, results)
+
+    try:
+        if W == 1:
+            worker(0)
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+
+            with ThreadPoolExecutor(W) as pool:  # (ctypes calls release the GIL: the contexts run concurrently)
+                for f in [pool.submit(worker, w) for w in range(W)]:
+                    f.result()
+    finally:  # every batch's corrected columns are in `out` (also when a batch raised)
+        for e in engines:
+            e.host_copy_wait()
     rep = CorrectionReport()
     bd_all = None
     raws = []
-    try:
-        bd_all = _pipelined_batches(ct, eng, parts, subs, upload, compute, scaled, attr, out, dev_out, rep, raws)
-    finally:  # every batch's corrected columns are in `out` (also when a batch raised)
-        eng.host_copy_wait()
+    for k, (r, ov, bd) in enumerate(results):
+        rep.removed_ns.update(r.removed_ns)
+        rep.shortfall_ns.update(r.shortfall_ns)
+        rep.original_total_ns += r.original_total_ns
+        rep.corrected_total_ns += r.corrected_total_ns
+        raws.append((subs[k], ov))
+        if bd_all is None:
+            bd_all = bd
+        else:
+            bd_all.spans.update(bd.spans)
+            bd_all.untracked.update(bd.untracked)
 
     def build():  # the cells dict, on first access (pids are disjoint across batches)
         cells = {}
@@ -308,17 +343,17 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     return out[0], out[1], rep, bd_all
 
 
-def _pipelined_batches(ct, eng, parts, subs, upload, compute, scaled, attr, out, dev_out, rep, raws):
+def _pipelined_batches(ct, eng, parts, ks, subs, upload, w, compute, scaled, attr, out, dev_out, results):
     from .overlap import _decode_breakdown
 
-    bd_all = None
-    nxt = upload(0)
-    for k, (a, b) in enumerate(parts):
+    nxt = upload(ks[0], w)
+    for i, k in enumerate(ks):
+        a, b = parts[k]
         dt, ev = nxt
         compute.wait_event(ev)
-        if k + 1 < len(parts):
-            nxt = upload(k + 1)  # overlaps the analysis below
-        try:  # the batch's D2H overlaps the next batch's analysis (waited for once, below)
+        if i + 1 < len(ks):
+            nxt = upload(ks[i + 1], w)  # overlaps the analysis below
+        try:  # the batch's D2H overlaps the next batch's analysis (waited for by the caller)
             raw = eng.correct(dt, scaled, attr, host_out=(out[0][a:b], out[1][a:b]),
                               dev_out=(dev_out[0][a:b], dev_out[1][a:b]), async_copy=True)
         except _engine.UncalibratedEvent as exc:
@@ -328,18 +363,6 @@ def _pipelined_batches(ct, eng, parts, subs, upload, compute, scaled, attr, out,
             if exc.status == _lib.XS_INVALID_TRACE:
                 raise InvalidTraceError(format_violations(ct.to_trace())) from None
             raise
-        r = _report(subs[k], raw)
-        rep.removed_ns.update(r.removed_ns)
-        rep.shortfall_ns.update(r.shortfall_ns)
-        rep.original_total_ns += r.original_total_ns
-        rep.corrected_total_ns += r.corrected_total_ns
         ov = eng.fetch_overlap()
-        raws.append((subs[k], ov))
-        bd = _decode_breakdown(subs[k], ov)
-        if bd_all is None:
-            bd_all = bd
-        else:
-            bd_all.spans.update(bd.spans)
-            bd_all.untracked.update(bd.untracked)
+        results[k] = (_report(subs[k], raw), ov, _decode_breakdown(subs[k], ov))
         del dt
-    return bd_all

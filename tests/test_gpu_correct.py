@@ -218,10 +218,11 @@ def test_pipelined_analyze_equals_one_call():
     for ct, prof in ((synth.config3_trace(processes=7, events_per_pid=30_000), synth.exact_profile()),
                      (synth.adversarial_trace(150_000, pids=12), synth.adversarial_profile())):
         s0, d0, rep0, bd0 = analyze_columnar(ct, prof)
-        for pin in (ct.pinned(), ct.pinned(packed=False), ct):
+        for pin, workers in ((ct.pinned(), 2), (ct.pinned(), 1), (ct.pinned(), 3), (ct.pinned(packed=False), 2),
+                             (ct, 2)):
             hs = torch.empty(ct.n, dtype=torch.int64).pin_memory()
             hd = torch.empty(ct.n, dtype=torch.int64).pin_memory()
-            s1, d1, rep1, bd1 = analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=4)
+            s1, d1, rep1, bd1 = analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=4, workers=workers)
             assert np.array_equal(hs.numpy(), s0.cpu().numpy()) and np.array_equal(hd.numpy(), d0.cpu().numpy())
             assert rep1.removed_ns == rep0.removed_ns and rep1.shortfall_ns == rep0.shortfall_ns
             assert rep1.original_total_ns == rep0.original_total_ns
