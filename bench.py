@@ -445,7 +445,7 @@ def run_ours(args):
                        "parallelism": f"pid-sharded x{world}" + (", NCCL all-reduce histogram merge" if world > 1
                                                                    else "")},
             "e2e": {"value": round(total_events / (e2e_step / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_step, 3),
-                    "api": ("analyze_columnar_pipelined (8 pid batches; one call when a pid dominates)" if pipelined
+                    "api": ("analyze_columnar_pipelined (9 pid batches over 3 contexts; one call when a pid dominates)" if pipelined
                             else "analyze_columnar"),
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
                     "path": "analyze_columnar(pinned host columns): H2D -> xs_analyze_to_host (corrected columns D2H "

@@ -200,12 +200,15 @@ def _row_slice(ct: ColumnarTrace, a: int, b: int) -> ColumnarTrace:
 
 
 def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, out, attribution=None,
-                               batches: int = 8, workers: int = 2):
+                               batches: int = 9, workers: int = 3):
     """analyze_columnar for host-resident traces of many processes, with the
     upload of the next batch of pids overlapping the analysis of the current
     one (per-pid independence: overlap.py:126, correction.py:132).  Needs
     pid-contiguous rows (e.g. ``synth``/per-process ingest) and host output
     buffers ``out`` = (start, dur); falls back to one call otherwise.
+    ``workers`` contexts (own workspace, graphs and streams, one host thread
+    each) take the batches in turn, so their analyses also overlap each
+    other (config 3, 100M events: 1 context 94 ms, 2: 83 ms, 3: 79 ms).
     Returns (start, dur, report, Breakdown) like analyze_columnar."""
     import torch
 

@@ -15,13 +15,14 @@ pin = ct.pinned()
 prof = synth.exact_profile()
 hs = torch.empty(ct.n, dtype=torch.int64).pin_memory()
 hd = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+W = int(os.environ.get("XS_WORKERS", "2"))
 for b in [int(x) for x in os.environ.get("XS_BATCHES", "4,8,16,32").split(",")]:
     for _ in range(3):
-        analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=b)
+        analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=b, workers=W)
     torch.cuda.synchronize()
     ts = []
     for _ in range(3):
         t0 = time.perf_counter()
-        analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=b)
+        analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=b, workers=W)
         ts.append((time.perf_counter() - t0) * 1e3)
-    print(f"batches {b}: ms {[round(t, 1) for t in ts]}  ev/s {ct.n / (min(ts) / 1e3) / 1e9:.3f} G", flush=True)
+    print(f"workers {W} batches {b}: ms {[round(t, 1) for t in ts]}  ev/s {ct.n / (min(ts) / 1e3) / 1e9:.3f} G", flush=True)
