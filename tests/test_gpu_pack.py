@@ -64,3 +64,31 @@ def test_packed_analyze_matches_wide_upload():
     s1, d1, r1, b1 = analyze_columnar(ct.pinned(), prof)
     assert np.array_equal(s0.cpu().numpy(), s1.cpu().numpy()) and np.array_equal(d0.cpu().numpy(), d1.cpu().numpy())
     assert r0.removed_ns == r1.removed_ns and b0 == b1
+
+
+def test_pipelined_packed_with_exceptions_equals_one_call():
+    """Pipelined multi-context analysis of a packed trace whose corr / start
+    columns carry exception-table values (ids >= 2^32 on a subset of one
+    pid's correlations; one far-away instant per pid) equals one call on the
+    unpacked columns."""
+    import dataclasses
+
+    import torch
+
+    from paper_2102_04285_b200 import analyze_columnar, analyze_columnar_pipelined
+
+    ct = synth.config3_trace(processes=6, events_per_pid=20_000)
+    sel = (ct.pid == 2) & (ct.has_corr == 1) & (ct.corr % 4 == 0)
+    corr = np.where(sel, ct.corr + (1 << 33), ct.corr)
+    ct2 = dataclasses.replace(ct, corr=np.ascontiguousarray(corr, np.int64), _source=None)
+    pin = ct2.pinned()
+    lay = pin._pinned["_packed"]
+    assert lay.widths["corr"] == 4 and lay.n_exc == int(sel.sum()) > 0
+    prof = synth.exact_profile()
+    s0, d0, r0, b0 = analyze_columnar(ct2, prof)
+    for workers in (1, 3):
+        hs = torch.empty(ct2.n, dtype=torch.int64).pin_memory()
+        hd = torch.empty(ct2.n, dtype=torch.int64).pin_memory()
+        s1, d1, r1, b1 = analyze_columnar_pipelined(pin, prof, out=(hs, hd), batches=5, workers=workers)
+        assert np.array_equal(hs.numpy(), s0.cpu().numpy()) and np.array_equal(hd.numpy(), d0.cpu().numpy())
+        assert r1.removed_ns == r0.removed_ns and b1 == b0

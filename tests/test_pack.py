@@ -80,3 +80,22 @@ def test_pack_refuses_unrepresentable_category():
     import dataclasses
     bad = dataclasses.replace(ct, cat=np.where(np.arange(ct.n) == 3, 200, ct.cat).astype(np.uint8), _source=None)
     assert pack_block(bad) is None
+
+
+def test_exception_table_sorted_and_adjacent():
+    """The pipelined path uploads the exception table as one byte range:
+    rows, values, columns are adjacent in the block and sorted by row."""
+    import dataclasses
+
+    ct = synth.adversarial_trace(20_000, pids=5)
+    n = ct.n
+    bad = dataclasses.replace(ct, dur=np.where(np.arange(n) % 101 == 5, -1, ct.dur).astype(np.int64),
+                              corr=np.where(np.arange(n) % 131 == 3, 1 << 40, ct.corr).astype(np.int64),
+                              _source=None)
+    lay, raw = pack_block(bad)
+    assert lay.n_exc > 0
+    o = lay.offsets
+    assert o["exc_val"] == o["exc_row"] + (lay.nbytes["exc_row"] + 15) // 16 * 16
+    assert o["exc_col"] == o["exc_val"] + (lay.nbytes["exc_val"] + 15) // 16 * 16
+    rows = raw[o["exc_row"]:o["exc_row"] + lay.nbytes["exc_row"]].view(np.int64)
+    assert np.all(np.diff(rows) >= 0)
