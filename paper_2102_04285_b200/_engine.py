@@ -71,25 +71,34 @@ class DeviceTrace:
         pinned = ct._pinned or {}
         block = pinned.get("_block")
         lay = pinned.get("_packed")
-        if lay is not None:  # packed pinned block: one DMA of ~17-22 B/event, widened by xs_unpack
-            dblock = block.to(dev, non_blocking=True)
-            self._dblock = dblock
+        if lay is not None:  # packed pinned block: one DMA of ~16 B/event, widened by xs_unpack
+            # the device staging (packed block + wide columns) is kept with the
+            # pinned trace and refilled by every DeviceTrace of it: the content
+            # is the same trace, and repeated calls skip ~10 tensor allocations
             n = ct.n
-            self._wide = torch.empty(max(n, 1) * 38 + 64, dtype=torch.uint8, device=dev)
-            cols = {}
-            off = 0
-            for k, dt, w in (("start", torch.int64, 8), ("dur", torch.int64, 8), ("corr", torch.int64, 8),
-                             ("pid", torch.int32, 4), ("tid", torch.int32, 4), ("name", torch.int32, 4),
-                             ("cat", torch.uint8, 1), ("has_corr", torch.uint8, 1)):
-                cols[k] = self._wide[off:off + max(n, 1) * w].view(dt)
-                off += (max(n, 1) * w + 15) // 16 * 16
+            cache = pinned.get("_dev_cache")
+            if cache is None or cache[0] != device:
+                dblock = torch.empty_like(block, device=dev)
+                wide = torch.empty(max(n, 1) * 38 + 64, dtype=torch.uint8, device=dev)
+                cols = {}
+                off = 0
+                for k, dt, w in (("start", torch.int64, 8), ("dur", torch.int64, 8), ("corr", torch.int64, 8),
+                                 ("pid", torch.int32, 4), ("tid", torch.int32, 4), ("name", torch.int32, 4),
+                                 ("cat", torch.uint8, 1), ("has_corr", torch.uint8, 1)):
+                    cols[k] = wide[off:off + max(n, 1) * w].view(dt)
+                    off += (max(n, 1) * w + 15) // 16 * 16
+                for k, dt in (("group_pid", torch.int32), ("pid_has_meta", torch.uint8)):
+                    o, nb = lay.offsets[k], lay.nbytes[k]
+                    cols[k] = dblock[o:o + nb].view(dt) if nb else torch.zeros(1, dtype=dt, device=dev)
+                cache = (device, dblock, wide, cols, packed_ptrs(lay, dblock))
+                pinned["_dev_cache"] = cache
+            _, dblock, self._wide, cols, ptrs = cache
+            self._dblock = dblock
+            dblock.copy_(block, non_blocking=True)
             for k, t in cols.items():
                 setattr(self, k, t)
-            for k, dt in (("group_pid", torch.int32), ("pid_has_meta", torch.uint8)):
-                o, nb = lay.offsets[k], lay.nbytes[k]
-                setattr(self, k, dblock[o:o + nb].view(dt) if nb else torch.zeros(1, dtype=dt, device=dev))
             if n:
-                unpack_into(get(device), lay, packed_ptrs(lay, dblock), 0, n, self)
+                unpack_into(get(device), lay, ptrs, 0, n, self)
             return
         if block is not None:  # one pinned block (ColumnarTrace.pinned): one DMA, device views
             dblock = block.to(dev, non_blocking=True)

@@ -337,13 +337,16 @@ int xs_overlap_fetch(xs_ctx_t* ctx, int32_t* cell_pid, int32_t* cell_node, int32
   XS_TRY(cp(span_lo, W_SPAN_LO, np * 8));
   XS_TRY(cp(span_hi, W_SPAN_HI, np * 8));
   XS_TRY(cp(tracked, W_TRACKED, np * 8));
-  if (has_events && np) {
-    std::vector<int64_t> lo(np);
-    XS_CUDA(cudaMemcpyAsync(lo.data(), ctx->ptr[W_SPAN_LO], np * 8, cudaMemcpyDeviceToHost, s));
-    XS_CUDA(cudaStreamSynchronize(s));
-    for (size_t p = 0; p < np; p++) has_events[p] = lo[p] != INT64_MAX;
+  std::vector<int64_t> lo_tmp;  // has_events derives from the span starts: one sync for everything
+  const int64_t* lo = span_lo;
+  if (has_events && np && !span_lo) {
+    lo_tmp.resize(np);
+    XS_TRY(cp(lo_tmp.data(), W_SPAN_LO, np * 8));
+    lo = lo_tmp.data();
   }
   XS_CUDA(cudaStreamSynchronize(s));
+  if (has_events)
+    for (size_t p = 0; p < np; p++) has_events[p] = lo[p] != INT64_MAX;
   return XS_OK;
 }
 
