@@ -211,7 +211,8 @@ int xs_chunk_decode(const uint8_t* buf, int64_t len, const char* context, const 
  * xs_unpack widens rows [row0, row0 + n) of a packed trace (device pointers,
  * possibly a slice) into the xs_events_t columns (device buffers of n rows).
  * Replaces the per-column host -> device copies of the reference's in-process
- * Trace (model.py:92): the result is bit-identical to the unpacked columns. */
+ * Trace (model.py:78-88, the events tuple): the result is bit-identical to the
+ * unpacked columns. */
 typedef struct {
   int64_t n;                 /* rows to widen                                     */
   int64_t row0;              /* global row of the first (start bases are per 256 */
