@@ -262,3 +262,31 @@ def test_to_host_copies_follow_graph_replays():
         if async_copy:
             eng.host_copy_wait()
         assert np.array_equal(hs.numpy(), want[k][0]) and np.array_equal(hd.numpy(), want[k][1]), (i, k)
+
+
+def test_pipelined_errors_surface_after_copies_drain():
+    """A batch that fails validation (a negative duration in one pid) or
+    lacks a calibrated hook raises the reference's exception from the
+    pipelined multi-context path, after every in-flight read-back drained;
+    the next call on the same contexts is unaffected."""
+    import dataclasses
+
+    import torch
+
+    from paper_2102_04285_b200 import analyze_columnar, analyze_columnar_pipelined
+
+    ct = synth.config3_trace(processes=6, events_per_pid=20_000)
+    prof = synth.exact_profile()
+    rows = np.flatnonzero(ct.pid == 4)
+    bad = dataclasses.replace(ct, dur=np.where(np.arange(ct.n) == rows[100], -7, ct.dur).astype(np.int64),
+                              _source=None)
+    hs = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+    hd = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+    with pytest.raises(InvalidTraceError):
+        analyze_columnar_pipelined(bad.pinned(), prof, out=(hs, hd), batches=5, workers=3)
+    thin = dataclasses.replace(prof, api_internal_ns={})
+    with pytest.raises(UncalibratedHookError):
+        analyze_columnar_pipelined(ct.pinned(), thin, out=(hs, hd), batches=5, workers=3)
+    s0, d0, r0, b0 = analyze_columnar(ct, prof)
+    analyze_columnar_pipelined(ct.pinned(), prof, out=(hs, hd), batches=5, workers=3)
+    assert np.array_equal(hs.numpy(), s0.cpu().numpy()) and np.array_equal(hd.numpy(), d0.cpu().numpy())
