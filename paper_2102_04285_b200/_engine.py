@@ -79,14 +79,20 @@ class DeviceTrace:
             cache = pinned.get("_dev_cache")
             if cache is None or cache[0] != device:
                 dblock = torch.empty_like(block, device=dev)
-                wide = torch.empty(max(n, 1) * 38 + 64, dtype=torch.uint8, device=dev)
+                m = max(n, 1)
+                spec = (("start", torch.int64, 8), ("dur", torch.int64, 8), ("corr", torch.int64, 8),
+                        ("pid", torch.int32, 4), ("tid", torch.int32, 4), ("name", torch.int32, 4),
+                        ("cat", torch.uint8, 1), ("has_corr", torch.uint8, 1))
+                # every column starts 16-byte aligned: size the block as the
+                # sum of the ROUNDED column sizes (38*m would be short by up to
+                # 7*15 bytes of padding)
+                wide = torch.empty(sum((m * w + 15) // 16 * 16 for _, _, w in spec), dtype=torch.uint8, device=dev)
                 cols = {}
                 off = 0
-                for k, dt, w in (("start", torch.int64, 8), ("dur", torch.int64, 8), ("corr", torch.int64, 8),
-                                 ("pid", torch.int32, 4), ("tid", torch.int32, 4), ("name", torch.int32, 4),
-                                 ("cat", torch.uint8, 1), ("has_corr", torch.uint8, 1)):
-                    cols[k] = wide[off:off + max(n, 1) * w].view(dt)
-                    off += (max(n, 1) * w + 15) // 16 * 16
+                for k, dt, w in spec:
+                    cols[k] = wide[off:off + m * w].view(dt)
+                    assert cols[k].numel() == m, (k, cols[k].numel(), m)
+                    off += (m * w + 15) // 16 * 16
                 for k, dt in (("group_pid", torch.int32), ("pid_has_meta", torch.uint8)):
                     o, nb = lay.offsets[k], lay.nbytes[k]
                     cols[k] = dblock[o:o + nb].view(dt) if nb else torch.zeros(1, dtype=dt, device=dev)

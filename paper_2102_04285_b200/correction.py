@@ -321,6 +321,20 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     finally:  # every batch's corrected columns are in `out` (also when a batch raised)
         for e in engines:
             e.host_copy_wait()
+        # an upload queued for a batch that never ran may still be writing the
+        # persistent buffers: drain every copy stream before they are reused
+        for st in state:
+            st["copy"].synchronize()
+    # errors in trace order, like the reference's whole-trace require_valid
+    # followed by collect_sites: any invalid batch wins over an uncalibrated
+    # hook; among uncalibrated hooks the smallest global row is reported
+    errs = [r for r in results if isinstance(r, _BatchError)]
+    if errs:
+        if any(e.kind == "invalid" for e in errs):
+            raise InvalidTraceError(format_violations(ct.to_trace()))
+        first = min(errs, key=lambda e: e.row)
+        name = ct.names[int(ct.name[first.row])]
+        raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile")
     rep = CorrectionReport()
     bd_all = None
     raws = []
@@ -346,6 +360,14 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     return out[0], out[1], rep, bd_all
 
 
+@dataclass
+class _BatchError:
+    """A batch of analyze_columnar_pipelined that failed (kind, global row)."""
+
+    kind: str  # "invalid" | "uncalibrated"
+    row: int
+
+
 def _pipelined_batches(ct, eng, parts, ks, subs, upload, w, compute, scaled, attr, out, dev_out, results):
     from .overlap import _decode_breakdown
 
@@ -359,12 +381,13 @@ def _pipelined_batches(ct, eng, parts, ks, subs, upload, w, compute, scaled, att
         try:  # the batch's D2H overlaps the next batch's analysis (waited for by the caller)
             raw = eng.correct(dt, scaled, attr, host_out=(out[0][a:b], out[1][a:b]),
                               dev_out=(dev_out[0][a:b], dev_out[1][a:b]), async_copy=True)
-        except _engine.UncalibratedEvent as exc:
-            name = ct.names[int(subs[k].name[exc.index])]
-            raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile") from None
+        except _engine.UncalibratedEvent as exc:  # keep going: a later batch may hold an invalid event
+            results[k] = _BatchError("uncalibrated", a + int(exc.index))
+            continue
         except _engine.XsError as exc:
             if exc.status == _lib.XS_INVALID_TRACE:
-                raise InvalidTraceError(format_violations(ct.to_trace())) from None
+                results[k] = _BatchError("invalid", a)
+                continue
             raise
         ov = eng.fetch_overlap()
         results[k] = (_report(subs[k], raw), ov, _decode_breakdown(subs[k], ov))

@@ -247,8 +247,10 @@ void xs_ctx_destroy(xs_ctx_t* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
-  for (auto& kv : ctx->graphs)
+  for (auto& kv : ctx->graphs) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (cudaEvent_t e : kv.second.events) cudaEventDestroy(e);
+  }
   if (ctx->priv_stream) cudaStreamDestroy(ctx->priv_stream);
   for (int b = 0; b < 2; b++) {
     if (ctx->br_stream[b]) cudaStreamDestroy(ctx->br_stream[b]);

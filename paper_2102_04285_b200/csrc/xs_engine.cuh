@@ -208,10 +208,15 @@ struct xs_ctx {
     std::vector<cudaEvent_t> prof_a, prof_b;
     long long launches = 0;
     xs::OpsState ops;
+    long long generation = 0;  // workspace generation the graph's pointers belong to
+    unsigned long long used = 0;  // LRU tick
+    std::vector<cudaEvent_t> events;  // timing events owned by this graph
   };
   std::map<std::string, GraphEntry> graphs;
   std::set<std::string> graph_seen, graph_bad;
-  std::vector<cudaEvent_t> graph_events;  // events owned by captured graphs
+  std::vector<cudaEvent_t> graph_events;  // events of the capture in progress
+  unsigned long long graph_tick = 0;
+  long long graph_generation = 0;  // generation the cache was last purged at
   bool capturing = false;
   // speculative overlap pass of xs_analyze: ops selected by the original
   // durations, pass-1 counts kept from the original, k_parent_nodes guarded

@@ -9,6 +9,12 @@
 // second is captured into a graph, and later calls replay the graph.  A
 // segment that tries to allocate or synchronize while being captured is
 // marked non-capturable and keeps running eagerly.
+//
+// The cache is bounded: graphs of an older workspace generation hold freed
+// pointers and are dropped as soon as the workspace grows, and at most
+// kMaxGraphs graphs (least recently replayed first out) are kept, so a
+// long-running process analysing many distinct traces does not grow without
+// bound.  The sighting and non-capturable sets are bounded the same way.
 #include "xs_engine.cuh"
 
 #include <cstdio>
@@ -32,12 +38,52 @@ static bool graphs_enabled() {
   return en == 1;
 }
 
+static constexpr size_t kMaxGraphs = 64, kMaxKeys = 4096;
+
+static void drop_graph(xs_ctx* ctx, std::map<std::string, xs_ctx::GraphEntry>::iterator it) {
+  if (!ctx->pend_stage.empty()) prof_flush(ctx);  // (pending timings may name this graph's events)
+  if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+  for (cudaEvent_t e : it->second.events) cudaEventDestroy(e);
+  ctx->graphs.erase(it);
+}
+
+// drop graphs of older workspace generations; keep the cache under kMaxGraphs
+static void trim_graphs(xs_ctx* ctx, cudaStream_t s) {
+  if (ctx->graph_generation != ctx->ws_generation) {
+    bool any = false;
+    for (auto it = ctx->graphs.begin(); it != ctx->graphs.end();) {
+      auto nx = std::next(it);
+      if (it->second.generation != ctx->ws_generation) {
+        if (!any) cudaStreamSynchronize(s);  // (a replay of it may still be in flight)
+        any = true;
+        drop_graph(ctx, it);
+      }
+      it = nx;
+    }
+    ctx->graph_generation = ctx->ws_generation;
+  }
+  while (ctx->graphs.size() >= kMaxGraphs) {
+    auto victim = ctx->graphs.begin();
+    for (auto it = ctx->graphs.begin(); it != ctx->graphs.end(); ++it)
+      if (it->second.used < victim->second.used) victim = it;
+    cudaStreamSynchronize(s);
+    drop_graph(ctx, victim);
+  }
+  if (ctx->graph_seen.size() > kMaxKeys) ctx->graph_seen.clear();
+  if (ctx->graph_bad.size() > kMaxKeys) ctx->graph_bad.clear();
+}
+
 static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
                           const std::function<int(cudaStream_t)>& body0) {
   auto body = [&]() { return body0(s); };
   if (ctx->graph_bad.count(key)) return body();
   auto it = ctx->graphs.find(key);
+  if (it != ctx->graphs.end() && it->second.generation != ctx->ws_generation) {
+    trim_graphs(ctx, s);  // stale pointers: never replay
+    it = ctx->graphs.end();
+  }
   if (it != ctx->graphs.end()) {
+    it->second.used = ++ctx->graph_tick;
     XS_CUDA(cudaGraphLaunch(it->second.exec, s));
     ctx->ops = it->second.ops;
     ctx->launches += it->second.launches;
@@ -51,9 +97,15 @@ static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
   }
   static const bool dbg = getenv("XS_DEBUG_GRAPH") != nullptr;
   if (dbg) fprintf(stderr, "[xs graph] %s miss (%zu graphs)\n", key.c_str(), ctx->graphs.size());
-  // A miss is captured at once.  If the workspace must grow, the capture
+  // First sighting: eager (a one-off trace never pays capture + instantiate).
+  // Second sighting: captured.  If the workspace must grow, the capture
   // aborts at the first allocation (ws_get) and the segment runs eagerly,
   // sizing the workspace; the next call (new generation in its key) captures.
+  if (!ctx->graph_seen.count(key)) {
+    ctx->graph_seen.insert(key);
+    return body();
+  }
+  trim_graphs(ctx, s);
   const long long l0 = ctx->launches;
   const size_t p0 = ctx->pend_stage.size();
   if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
@@ -62,8 +114,11 @@ static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
     return body();
   }
   ctx->capturing = true;
+  ctx->graph_events.clear();
   const int st = body();
   ctx->capturing = false;
+  std::vector<cudaEvent_t> cap_events;
+  cap_events.swap(ctx->graph_events);
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(s, &g);
   cudaGraphExec_t exec = nullptr;
@@ -81,6 +136,7 @@ static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
   ctx->pend_b.resize(p0);
   if (st != XS_OK || e != cudaSuccess || !exec) {  // workspace growth, or not capturable: eager
     if (exec) cudaGraphExecDestroy(exec);
+    for (cudaEvent_t ev : cap_events) cudaEventDestroy(ev);
     cudaGetLastError();
     ctx->err.clear();
     ctx->launches = l0;
@@ -90,6 +146,8 @@ static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
   ge.exec = exec;
   ge.launches = ctx->launches - l0;
   ge.ops = ctx->ops;
+  ge.generation = ctx->ws_generation;
+  ge.events = std::move(cap_events);
   ctx->launches = l0;
   ctx->graphs[key] = ge;
   return run_segment_on(ctx, s, key, body0);  // replay it now

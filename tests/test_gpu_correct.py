@@ -290,3 +290,52 @@ def test_pipelined_errors_surface_after_copies_drain():
     s0, d0, r0, b0 = analyze_columnar(ct, prof)
     analyze_columnar_pipelined(ct.pinned(), prof, out=(hs, hd), batches=5, workers=3)
     assert np.array_equal(hs.numpy(), s0.cpu().numpy()) and np.array_equal(hd.numpy(), d0.cpu().numpy())
+
+
+def test_pipelined_mixed_errors_follow_trace_order():
+    """Errors of different batches resolve like the reference's whole-trace
+    order: an invalid event in a LATE batch wins over an uncalibrated hook in
+    an early one (require_valid runs first, correction.py:121), and among
+    uncalibrated hooks in several batches the first row in trace order names
+    the hook (collect_sites walks events in order, correction.py:86-100)."""
+    import dataclasses
+
+    import torch
+
+    from paper_2102_04285_b200 import analyze_columnar, analyze_columnar_pipelined
+
+    ct = synth.config3_trace(processes=6, events_per_pid=20_000)
+    prof = synth.exact_profile()
+    api = [i for i, nm in enumerate(ct.names) if nm in prof.api_internal_ns]
+    other = [i for i, nm in enumerate(ct.names) if nm not in prof.api_internal_ns]
+    assert api and other
+    is_api = (ct.cat == 4) & np.isin(ct.name, api)
+
+    def rename(name_col, pid, new):
+        r = np.flatnonzero(is_api & (ct.pid == pid))[50]
+        name_col[r] = new
+        return r
+
+    name = ct.name.copy()
+    rename(name, 1, other[0])  # uncalibrated in the first batch
+    late = np.flatnonzero(ct.pid == 5)[100]
+    mixed = dataclasses.replace(ct, name=name, _source=None,
+                                dur=np.where(np.arange(ct.n) == late, -7, ct.dur).astype(np.int64))
+    hs = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+    hd = torch.empty(ct.n, dtype=torch.int64).pin_memory()
+    for workers in (1, 3):
+        with pytest.raises(InvalidTraceError):
+            analyze_columnar_pipelined(mixed.pinned(), prof, out=(hs, hd), batches=5, workers=workers)
+    name = ct.name.copy()
+    rename(name, 5, other[-1])
+    rename(name, 2, other[0])  # earlier in trace order: this one is reported
+    two = dataclasses.replace(ct, name=name, _source=None)
+    with pytest.raises(UncalibratedHookError) as one_call:
+        analyze_columnar(two, prof)
+    for workers in (1, 3):
+        with pytest.raises(UncalibratedHookError) as piped:
+            analyze_columnar_pipelined(two.pinned(), prof, out=(hs, hd), batches=5, workers=workers)
+        assert str(piped.value) == str(one_call.value) and repr(ct.names[other[0]]) in str(piped.value)
+    s0, d0, r0, b0 = analyze_columnar(ct, prof)
+    analyze_columnar_pipelined(ct.pinned(), prof, out=(hs, hd), batches=5, workers=3)
+    assert np.array_equal(hs.numpy(), s0.cpu().numpy()) and np.array_equal(hd.numpy(), d0.cpu().numpy())
