@@ -49,6 +49,8 @@ def parse():
                     help="BASELINE.json config: 2 (default, the metric's workload), 3 (100M events, 100 pids, "
                          "nested), 5 (adversarial 10M)")
     ap.add_argument("--events", type=int, default=0, help="events per GPU for --config 3/5 (default 100M / 10M)")
+    ap.add_argument("--ref-budget", type=float, default=120.0,
+                    help="--impl reference: stop the timed steps once this many seconds are spent")
     return ap.parse_args()
 
 
@@ -169,33 +171,45 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def stage_bytes(stage: str, n: int, nnz: int, ns: int, key_bits_main: int, key_bits_site: int) -> float:
-    """Algorithmic DRAM bytes of one occurrence of a stage ('Roofline')."""
-    def passes(bits):
-        return max(1, -(-bits // 8))
-    if stage == "endpoint_sort":   # keys-only onesweep over 2n keys: 1 histogram read + P x (read+write)
-        return 2 * n * (8 + 16 * passes(key_bits_main))
-    if stage == "sweep_scan_hist":  # one read of the sorted nonzero endpoints
-        return 2 * nnz * 8
-    if stage == "endpoint_keygen":  # read start/dur/pid/cat/has_corr, write 2 keys
-        return n * (8 + 8 + 4 + 1 + 1) + 2 * n * 8
-    if stage == "site_sort":        # two (key8,val4) pair sorts over the sites + generation
-        return 2 * ns * (8 + 24 * passes(key_bits_site)) + n * 21
-    if stage == "remap":            # read start/dur/pid/cat, write start'/dur'
-        return n * (8 + 8 + 4 + 1) + n * 16
-    if stage == "quantize_scan":
-        return ns * (8 + 4 + 4 + 1 + 8)
-    if stage == "removal_scan":
-        return ns * (8 + 4 + 8 + 1) + ns * 24
-    if stage == "pass1_validate_spans":
-        return n * (8 + 8 + 4 + 4 + 1 + 1 + 4)
-    if stage == "transition_sort":  # two (key8,val4) pair sorts over ~0.3n records (B/S queries + H endpoints)
-        return 0.0
+def stage_bytes(stage: str, n: int, nnz: int, ns: int, nrec: int) -> float:
+    """Algorithmic DRAM bytes of one occurrence of a stage as implemented
+    (DESIGN.md section 3): the bytes its kernels must read and write once --
+    n events, nnz nonzero-duration events, ns hook sites, nrec transition
+    records.  The endpoint keys are 8 bytes (pid | t_rel | 4-bit code: the
+    4-byte payload of SURVEY 8(d)'s canonical 12-byte record lives in the
+    code bits); record sorts are bucketed (histogram read of the key, one
+    scatter pass and one in-bucket pass over (key, value))."""
+    if stage == "pass1_validate_spans":  # start, dur, pid, tid, cat, has_corr, name
+        return 30.0 * n
+    if stage == "endpoint_keygen":      # k_bk_hist: start, dur, pid, cat -> bucket counts
+        return 21.0 * n
+    if stage == "endpoint_sort":        # k_bk_scatter: the same reads, 2 keys written per nonzero event
+        return 21.0 * n + 16.0 * nnz
+    if stage == "sweep_scan_hist":      # k_bk_sweep: one read of the 2 sorted keys per nonzero event
+        return 16.0 * nnz
+    if stage == "site_sort":            # count + generate (35 B/event) + (k8,v4) site records: write 13,
+        return 35.0 * n + 69.0 * ns     # histogram 8, scatter 24, in-bucket 24
+    if stage == "transition_sort":      # record generation (21 B/event) + (k8,v4) records: write 12,
+        return 21.0 * n + 68.0 * nrec   # histogram 8, scatter 24, in-bucket 24
+    if stage == "remap":                # start, dur, pid, cat in; start', dur' out
+        return 37.0 * n
+    if stage == "quantize_scan":        # site key 8, slot 4, owner 4, subkind 1, amount 8
+        return 25.0 * ns
+    if stage == "removal_scan":         # site key, slot, amount, subkind + extents (a, len, E)
+        return 45.0 * ns
     return 0.0
 
 
-def traffic_from_profiles(stage: str):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def transition_records(ct) -> int:
+    """Records of the correction's transition pass (H -> B, H -> S): two
+    endpoints per nonzero HIGH_LEVEL event, one query per BACKEND/SIMULATOR."""
+    return int(2 * np.count_nonzero((ct.cat == 1) & (ct.dur > 0)) + np.count_nonzero((ct.cat == 2) | (ct.cat == 3)))
+
+
+def traffic_from_profiles(stage: str, config: int):
+    """ncu DRAM bytes per launch of the stage's kernel, from this config's
+    capture (profiles/ncu_traffic_c<config>.json), else None."""
+    p = os.path.join(ROOT, "profiles", f"ncu_traffic_c{config}.json")
     if not os.path.exists(p):
         return None
     with open(p) as fh:
@@ -267,6 +281,60 @@ def cpu_baseline_port(ct, profile, seconds: float):
 
 
 # ---------------------------------------------------------------------------
+def _analyze_e2e(ct, profile, out, pipelined):
+    from paper_2102_04285_b200 import analyze_columnar, analyze_columnar_pipelined
+    if pipelined:
+        return analyze_columnar_pipelined(ct, profile, out=out)
+    return analyze_columnar(ct, profile, out=out)
+
+
+def first_calls(ct_pin, profile, out, pipelined, k: int = 3):
+    """Wall time of this process's first k analysis calls on the bench trace
+    (public API, pinned host columns): the first pays context creation,
+    workspace allocation and an eager run, the second captures the pipeline
+    graphs, later calls replay them."""
+    import torch
+    ms = []
+    for _ in range(k):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _analyze_e2e(ct_pin, profile, out, pipelined)
+        ms.append(round((time.perf_counter() - t0) * 1e3, 3))
+    return ms
+
+
+def time_e2e(fn, flush, steps):
+    import torch
+    ms = []
+    res = None
+    for _ in range(steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = fn()
+        ms.append((time.perf_counter() - t0) * 1e3)
+    return float(np.median(ms)), res
+
+
+def trace_api_e2e(ct, profile, reps: int = 2):
+    """The reference's own call sequence through the drop-in API, from a
+    Trace of Python Event objects: correct_trace(trace, profile) then
+    compute_overlap(corrected) (cli.py:168-171).  Returns (median ms, phases)."""
+    from paper_2102_04285_b200 import compute_overlap, correct_trace
+    trace = ct.to_trace()
+    ms, last = [], None
+    for _ in range(reps + 1):
+        t0 = time.perf_counter()
+        corrected, _rep = correct_trace(trace, profile)
+        t1 = time.perf_counter()
+        bd = compute_overlap(corrected)
+        _ = len(bd.cells)
+        t2 = time.perf_counter()
+        ms.append((t2 - t0) * 1e3)
+        last = {"correct_trace_ms": round((t1 - t0) * 1e3, 1), "compute_overlap_ms": round((t2 - t1) * 1e3, 1)}
+    return float(np.median(ms[1:])), last
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -278,15 +346,21 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
-    from paper_2102_04285_b200 import _engine, synth
+    from paper_2102_04285_b200 import _engine
     from paper_2102_04285_b200.distributed import merge_breakdown_raw
-    from paper_2102_04285_b200.overlap import decode_breakdown
 
     ct, un, profile = make_workload(args, rank)
+    n = ct.n
+    pipelined = ct.n_pids >= 8  # many processes: upload the next pid batch while analysing this one
+    # the caller's trace columns in page-locked host memory (the e2e input)
+    ct_pin = ct.pinned(packed=False)
+    out_s = torch.empty(n, dtype=torch.int64).pin_memory()
+    out_d = torch.empty(n, dtype=torch.int64).pin_memory()
+    first_ms = first_calls(ct_pin, profile, (out_s, out_d), pipelined)
+
     scaled = profile.scaled(ct.names)
     eng = _engine.get(local)
-    dt_dev = _engine.DeviceTrace(ct, local)
-    n = ct.n
+    dt_dev = _engine.DeviceTrace(ct_pin, local)
     nnz = int((ct.dur > 0).sum())
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
@@ -308,7 +382,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     for _ in range(args.steps):
-        flush.fill_(1.0)  # L2 flush between steps (inputs 37 MB < L2)
+        flush.fill_(1.0)  # L2 flush between steps
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -319,6 +393,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks.__exit__(None, None, None)
     launches = eng.launches() - launches0
+    import ctypes as C
+    from paper_2102_04285_b200 import _lib
+    info = _lib.XsCorrectInfo()  # sites of the timed call (before any other analysis on this context)
+    eng.lib.xs_correct_report(eng.ctx, C.byref(info), None, None, eng.stream())
+    ns_sites = int(info.n_sites)
     # per-stage device times come from a separate pass: the timing events
     # themselves must not sit inside the timed region
     eng.lib.xs_profile_enable(eng.ctx, 1)
@@ -340,45 +419,38 @@ def run_ours(args):
     total_events = n * world
     value = total_events / (ms_per_step / 1e3)
 
-    # end-to-end through the public API (analyze_columnar) with host buffers:
-    # the user's columns in pinned memory, uploaded every step, the corrected
-    # columns read back into pinned buffers, the Breakdown decoded on the host
-    from paper_2102_04285_b200 import analyze_columnar
-    ct_host = ct.pinned()
-    out_s = torch.empty(n, dtype=torch.int64).pin_memory()
-    out_d = torch.empty(n, dtype=torch.int64).pin_memory()
-    h2d = int(ct_host._pinned["_block"].numel())  # the one pinned block uploaded per step
+    # e2e (headline) through the public API: the trace's columns sit in
+    # page-locked host memory; every step uploads them (38 B/event), analyses,
+    # reads the corrected columns back into pinned buffers and decodes the
+    # Breakdown (spans/untracked; the cells dict is built on first access)
+    h2d = int(ct_pin._pinned["_block"].numel())
 
-    from paper_2102_04285_b200 import analyze_columnar_pipelined
-    pipelined = ct.n_pids >= 8  # many processes: upload the next pid batch while analysing this one
-
-    def step_e2e():
+    def step_e2e(src):
         f0 = eng.fetched_bytes
-        if pipelined:
-            s_, d_, rep, bd = analyze_columnar_pipelined(ct_host, profile, out=(out_s, out_d))
-        else:
-            s_, d_, rep, bd = analyze_columnar(ct_host, profile, out=(out_s, out_d))
+        _, _, _, bd = _analyze_e2e(src, profile, (out_s, out_d), pipelined)
         d2h = 16 * n + (eng.fetched_bytes - f0) + 8 * 4 * ct.n_pids * 2  # columns + overlap arrays + report
         return d2h, bd
 
-    for _ in range(2):
-        step_e2e()
-    e2e_ms = []
-    d2h = 0
-    for _ in range(max(3, args.steps // 2)):
-        flush.fill_(1.0)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        d2h, bd = step_e2e()
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_step = float(np.median(e2e_ms))
+    e2e_steps = max(3, args.steps // 2)
+    step_e2e(ct_pin)
+    e2e_step, (d2h, bd) = time_e2e(lambda: step_e2e(ct_pin), flush, e2e_steps)
+    # the same from ordinary (pageable) numpy columns: the native builder packs
+    # them into page-locked staging inside every step (16 B/event on the wire)
+    step_e2e(ct)
+    np_step, _ = time_e2e(lambda: step_e2e(ct), flush, e2e_steps)
     if world > 1:
-        t = torch.tensor([e2e_step], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_step, np_step], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_step = float(t.item())
+        e2e_step, np_step = (float(x) for x in t.tolist())
+    api = None
+    if args.config == 2 and world == 1:
+        api_ms, phases = trace_api_e2e(ct, profile)
+        api = {"value": round(n / (api_ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(api_ms, 1),
+               "path": "correct_trace(Trace of Event objects) + compute_overlap(corrected Trace), the "
+                       "reference's call sequence (cli.py:168-171) through the drop-in API", **phases}
 
-    # correctness of the measured step: closure against the uninstrumented twin
-    # (configs 2/3), or the oracle on a bounded sample of pids (config 5)
+    # correctness of the measured result: closure against the uninstrumented
+    # twin (configs 2/3), or the oracle on a bounded sample of pids (config 5)
     check = {}
     if un is not None:
         check["closure_exact"] = bool(np.array_equal(out_s.numpy(), un.start) and np.array_equal(out_d.numpy(), un.dur))
@@ -388,43 +460,42 @@ def run_ours(args):
 
     # roofline for the dominant stage
     peak, peak_kind = load_peaks()
-    tb = int(max(1, int((ct.start + ct.dur).max() - ct.start.min())).bit_length())
-    key_bits_main = tb + 4 + max(0, (ct.n_pids - 1).bit_length())
-    key_bits_site = tb + 3 + max(0, (ct.n_pids - 1).bit_length())
+    nrec = transition_records(ct)
     stages = {}
     for i, nm in enumerate(stage_names):
         if calls_arr[i]:
             stages[nm] = {"ms_total": round(float(ms_arr[i]), 4), "occurrences": int(calls_arr[i]),
                           "ms_avg": round(float(ms_arr[i]) / int(calls_arr[i]), 5)}
-    import ctypes as C
-    from paper_2102_04285_b200 import _lib
-    info = _lib.XsCorrectInfo()
-    eng.lib.xs_correct_report(eng.ctx, C.byref(info), None, None, eng.stream())
-    ns_sites = int(info.n_sites)
     # roofline of the dominant kernel: among the stages that are one main
     # kernel per occurrence (so ncu's per-launch DRAM bytes map onto them),
     # the one with the largest share of the step; every modeled stage is
     # listed in stage_rooflines
     single = ("sweep_scan_hist", "endpoint_keygen", "endpoint_sort", "pass1_validate_spans", "quantize_scan",
               "removal_scan", "remap")
-    modeled = [k for k in stages if stage_bytes(k, n, nnz, ns_sites, key_bits_main, key_bits_site) > 0]
+    modeled = [k for k in stages if stage_bytes(k, n, nnz, ns_sites, nrec) > 0]
 
     def roof_of(k):
-        algo = stage_bytes(k, n, nnz, ns_sites, key_bits_main, key_bits_site)
+        algo = stage_bytes(k, n, nnz, ns_sites, nrec)
         achieved = algo / (stages[k]["ms_avg"] / 1e3) / 1e9
         return {"kernel": k, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "algorithmic_bytes_per_launch": algo,
-                "traffic": traffic_from_profiles(k),
+                "traffic": traffic_from_profiles(k, args.config),
                 "share_of_step": round(stages[k]["ms_total"] / total_ms, 3) if total_ms else None}
 
     cands = [k for k in modeled if k in single] or modeled
     dom = max(cands, key=lambda k: stages[k]["ms_total"]) if cands else None
     roof = roof_of(dom) if dom else None
     stage_roofs = {k: {f: roof_of(k)[f] for f in ("achieved", "frac", "traffic")} for k in modeled}
-    pipe_bytes = sum(stage_bytes(k, n, nnz, ns_sites, key_bits_main, key_bits_site) * v["occurrences"]
+    pipe_bytes = sum(stage_bytes(k, n, nnz, ns_sites, nrec) * v["occurrences"]
                      for k, v in stages.items()) / args.steps
+    s_per_ev = ns_sites / max(n, 1)
+    survey_b = 325 + 45 + s_per_ev * 400 + 32  # B_ov (P=5) + B_corr (P_s=6)
     pipeline = {"model_bytes_per_event": round(pipe_bytes / n, 1),
                 "achieved_GBps": round(pipe_bytes / (ms_per_step / 1e3) / 1e9, 1),
+                "frac": round(pipe_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4),
+                "survey_model_bytes_per_event": round(survey_b, 1),
+                "survey_model_GBps": round(survey_b * n / (ms_per_step / 1e3) / 1e9, 1),
+                "survey_model_frac": round(survey_b * n / (ms_per_step / 1e3) / 1e9 / peak, 4),
                 "compulsory_bytes_per_event": 45 + 21}
 
     cpu = None
@@ -432,27 +503,37 @@ def run_ours(args):
         cpu = cpu_baseline_port(ct, profile, args.cpu_seconds)
         cpu["cores_available"] = os.cpu_count()
 
-    in_mb = h2d / 1e6
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "step_ms": [round(t, 4) for t in times], "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "step_ms": [round(t, 4) for t in times],
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config],
                        "events_per_gpu": n, "pids_per_gpu": ct.n_pids, "events_total": total_events,
                        "attribution": "instant",
-                       "l2": f"flushed (256 MB write) between timed steps; inputs {in_mb:.0f} MB/GPU",
+                       "l2": f"flushed (256 MB write) between timed steps; inputs {h2d / 1e6:.0f} MB/GPU",
                        "parallelism": f"pid-sharded x{world}" + (", NCCL all-reduce histogram merge" if world > 1
                                                                    else "")},
-            "e2e": {"value": round(total_events / (e2e_step / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_step, 3),
-                    "api": ("analyze_columnar_pipelined (9 pid batches over 3 contexts; one call when a pid dominates)" if pipelined
-                            else "analyze_columnar"),
+            "e2e": {"value": round(total_events / (e2e_step / 1e3), 1), "unit": UNIT,
+                    "ms_per_step": round(e2e_step, 3),
+                    "api": ("analyze_columnar_pipelined (9 pid batches over 3 contexts; one call when a pid dominates)"
+                            if pipelined else "analyze_columnar"),
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
-                    "path": "analyze_columnar(pinned host columns): H2D -> xs_analyze_to_host (corrected columns D2H "
+                    "path": "the trace's columns in page-locked host memory (ColumnarTrace.pinned(packed=False)) -> "
+                            "H2D of every column inside the step -> xs_analyze_to_host (corrected columns D2H "
                             "overlapped with the overlap pass) -> D2H cell arrays -> Breakdown (spans/untracked "
                             "decoded; the cells dict of OverlapKeys is built on first access)"},
+            "e2e_from_numpy": {"value": round(total_events / (np_step / 1e3), 1), "unit": UNIT,
+                               "ms_per_step": round(np_step, 3),
+                               "path": "ordinary numpy columns: native host packing into page-locked staging "
+                                       "(xs_pack_plan/xs_pack_fill, host threads) + one DMA of the packed block "
+                                       "inside every step, then as e2e"},
+            "e2e_trace_api": api,
+            "first_calls_ms": first_ms,
             "gpu_launches": int(launches / args.steps),
             "roofline": roof, "stage_rooflines": stage_roofs, "pipeline_roofline": pipeline, "stages_ms": stages,
+            "sites": ns_sites, "transition_records": nrec,
             "cpu_baseline": cpu, "clocks": clocks.summary(), **check,
         }
         print(json.dumps(line))
@@ -463,23 +544,28 @@ def run_ours(args):
 
 # ---------------------------------------------------------------------------
 def _ref_sample(config: int, worker: int, iterations: int, events: int):
-    """Worker w's bounded sample of the bench workload (distinct seeds/pids)."""
+    """Worker w's input: the identical bench trace (config 2), or one process
+    of the identical config-3 / config-5 trace (same seeds: those pids' events
+    are exactly the bench trace's)."""
     from paper_2102_04285_b200 import synth
-    if config == 2:  # 1/10 of the 1M-event trace
-        return make_trace(max(1, iterations // 10), worker), synth.exact_profile(), "1/10 of the config-2 trace"
-    if config == 3:  # one 100k-event pid of config 3
-        return (synth.config3_trace(processes=1, events_per_pid=100_000, first_pid=worker + 1),
-                synth.exact_profile(), "one 100k-event config-3 pid")
-    n = max(64 * 32, (events or 10_000_000) // 100)
-    return (synth.adversarial_trace(n, pids=64, seed=1234 + worker), synth.adversarial_profile(),
-            f"1/100 of the config-5 trace ({n} events, 64 pids)")
+    if config == 2:
+        return make_trace(iterations, 0), synth.exact_profile(), "the identical config-2 trace (whole)"
+    if config == 3:
+        return (synth.config3_trace(processes=1, events_per_pid=1_000_000, first_pid=worker + 1),
+                synth.exact_profile(), f"pid {worker + 1} of the identical config-3 trace")
+    ev = events or 10_000_000
+    sizes = synth.zipf_sizes(ev, 64, 1.5)
+    small = [p + 1 for p in sorted(range(64), key=lambda p: -sizes[p]) if sizes[p] <= 300_000]
+    pid = small[worker % len(small)]
+    return (synth.adversarial_trace(ev, pids=64, only=[pid]), synth.adversarial_profile(),
+            f"pid {pid} of the identical config-5 trace")
 
 
 def _ref_worker(args):
     """One host core: build the reference's own Trace of Event objects
     (untimed), then time correct_trace + compute_overlap(corrected) through
     the unmodified reference package (oracle/_ref, native Cython sweep)."""
-    config, worker, iterations, events, warmup, steps, barrier = args
+    config, worker, iterations, events, warmup, steps, barrier, stop, budget = args
     ref = os.path.join(ROOT, "oracle", "_ref")
     sys.path.insert(0, ref)
     from xstrace import model as RM
@@ -504,19 +590,30 @@ def _ref_worker(args):
 
     for _ in range(warmup):
         step()
-    barrier.wait()
-    t0 = time.perf_counter()
+    spans = []
+    t_begin = None
     for _ in range(steps):
+        barrier.wait()  # every worker runs the same number of steps
+        if stop.value:
+            break
+        t0 = time.perf_counter()
+        t_begin = t_begin or t0
         step()
-    t1 = time.perf_counter()
-    return ct.n * steps, t0, t1, what, HAVE_NATIVE_SWEEP, ct.n
+        t1 = time.perf_counter()
+        spans.append((t0, t1))
+        if worker == 0 and (t1 - t_begin) + (t1 - t0) > budget:
+            stop.value = 1  # (set before the next barrier: every worker sees it)
+    return ct.n, spans, what, HAVE_NATIVE_SWEEP
 
 
 def run_reference(args):
-    """The reference's own CPU implementation of the path on all host cores:
-    one worker process per core, each analysing its own bounded sample of the
-    workload through the unmodified reference package; throughput = all
-    events / wall time of the common timed phase."""
+    """The reference's own CPU implementation of the path on all host cores,
+    on the same workload: one worker process per core, each analysing its
+    own copy of the identical bench trace (config 2; configs 3 / 5: one of
+    the identical trace's processes each) through the unmodified reference
+    package; throughput = all events analysed / wall time of the common timed
+    phase.  A step is ~10-30 s of CPU work, so warm-up is capped at one step
+    and the timed steps stop once ~--ref-budget seconds are spent."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -529,20 +626,30 @@ def run_reference(args):
     ctx = mp.get_context("fork")
     mgr = ctx.Manager()
     barrier = mgr.Barrier(cores)
+    stop = mgr.Value("i", 0)
+    warm = min(max(args.warmup, 0), 1)
     with ctx.Pool(cores) as pool:
-        res = pool.map(_ref_worker, [(args.config, w, args.iterations, args.events, max(args.warmup, 1), args.steps,
-                                      barrier) for w in range(cores)], chunksize=1)
-    total = sum(r[0] for r in res)
-    wall = max(r[2] for r in res) - min(r[1] for r in res)
+        res = pool.map(_ref_worker, [(args.config, w, args.iterations, args.events, warm, args.steps, barrier, stop,
+                                      args.ref_budget) for w in range(cores)], chunksize=1)
+    steps_run = min(len(r[1]) for r in res)
+    total = sum(r[0] * steps_run for r in res)
+    wall = max(r[1][steps_run - 1][1] for r in res) - min(r[1][0][0] for r in res)
     value = total / wall
-    per_step_events = sum(r[5] for r in res)
-    sample = (f"{cores} worker processes x {res[0][3]} ({res[0][5]} events each), reference xstrace "
-              f"correct_trace + compute_overlap, native sweep={res[0][4]}")
+    step_s = sorted(b - a for r in res for a, b in r[1][:steps_run])
+    single = res[0][0] / step_s[len(step_s) // 2]
+    sample = (f"{cores} worker processes x {res[0][2]} ({res[0][0]} events each), reference xstrace "
+              f"correct_trace + compute_overlap, native sweep={res[0][3]}, {steps_run} timed step(s) after {warm} "
+              f"warm-up")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "events_per_step": per_step_events},
+        "steps": steps_run, "steps_requested": args.steps, "warmup": warm, "warmup_requested": args.warmup,
+        "ms_per_step": round(wall / steps_run * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "events_per_step": sum(r[0] for r in res),
+                   "same_config": args.config == 2,
+                   "same_trace": "every worker analyses the identical bench trace" if args.config == 2 else
+                   "every worker analyses one process of the identical bench trace"},
+        "single_process_events_per_s": round(single, 1),
         "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -69,16 +69,24 @@ typedef struct {
   const uint8_t* pid_has_meta;/* [n_pids] pid has a ProcessMeta              */
 } xs_events_t;
 
-/* Calibration profile as exact integers over one common denominator L
- * (fractions.Fraction in the reference, calibration.py:142-149). */
+/* Calibration profile, exact (fractions.Fraction in the reference,
+ * calibration.py:142-149; per-site amounts correction.py:90-100): every
+ * amount a is split as a = whole + frac / L with 0 <= frac < L, where L is the
+ * common denominator of all amounts, held as `words` little-endian 64-bit
+ * words (words = 1, 2, 4 or 8; L < 2^(64 words - 1)).  quantize_amounts
+ * (_timeline.py:57-67) then needs only the fractional parts' running sum
+ * modulo L: q_i = whole_i + [ (sum_{j<=i} frac_j mod L) < frac_i ], so no
+ * profile is too fine-grained for the device. */
 typedef struct {
-  int64_t L;
-  int64_t ann_start;          /* annotation/2 * L            (ANN_START)   */
-  int64_t ann_end;            /* (annotation - annotation/2) * L (ANN_END) */
-  int64_t transition;         /* transition * L                            */
-  int64_t interception;       /* api_interception * L                      */
-  const int64_t* internal;    /* DEVICE [n_names] api_internal[name] * L   */
-  const uint8_t* has_internal;/* DEVICE [n_names]                          */
+  int32_t words;
+  int32_t reserved;
+  const uint64_t* L;           /* DEVICE [words]                                               */
+  int64_t whole[4];            /* floor of ANN_START (annotation/2), ANN_END (annotation -     */
+                               /* annotation/2), transition, api_interception                  */
+  const uint64_t* frac;        /* DEVICE [(4 + n_names) * words]: (amount - whole) * L, rows   */
+                               /* in the order of `whole`, then api_internal[name] per name    */
+  const int64_t* internal;     /* DEVICE [n_names] floor(api_internal[name])                    */
+  const uint8_t* has_internal; /* DEVICE [n_names]                                              */
 } xs_profile_t;
 
 /* Sizes of the last overlap result held by the context. */
@@ -233,6 +241,28 @@ typedef struct {
 } xs_packed_t;
 int xs_unpack(xs_ctx_t* ctx, const xs_packed_t* pk, int64_t* start, int64_t* dur, int32_t* pid, int32_t* tid,
               uint8_t* cat, int32_t* name, int64_t* corr, uint8_t* has_corr, xs_stream_t stream);
+
+/* Host-side builder of the packed format (no device work; host threads).
+ * `ev` holds HOST pointers to the engine-dtype columns.  xs_pack_plan reads
+ * every column once and fixes widths, exception count and the block layout:
+ * 13 sections, 16-byte aligned, in the order start, start_base, dur, corr,
+ * pid, tid, name, catf, group_pid, pid_has_meta, exc_row, exc_val, exc_col
+ * (the layout ColumnarTrace.pinned documents).  XS_UNSUPPORTED: cat >= 128 or
+ * has_corr > 1 (not packable; upload the wide columns).  xs_pack_fill writes
+ * the block (normally page-locked) with the same row partition; padding
+ * bytes are zero.  n_threads <= 0 uses every hardware thread.  Replaces the
+ * reference's in-process Trace hand-off (model.py:78-88) as the staging of
+ * an analysis call's input. */
+#define XS_PACK_MAX_THREADS 64
+typedef struct {
+  int64_t n, n_exc, total;
+  int32_t start_w, dur_w, corr_w, pid_w, tid_w, name_w;
+  int32_t n_threads, reserved;
+  int64_t offset[13], nbytes[13];
+  int64_t thread_exc[XS_PACK_MAX_THREADS]; /* first exception slot of each thread */
+} xs_pack_layout_t;
+int xs_pack_plan(const xs_events_t* ev, int n_threads, xs_pack_layout_t* lay);
+int xs_pack_fill(const xs_events_t* ev, const xs_pack_layout_t* lay, void* block, int64_t block_bytes);
 
 /* Number of kernel launches issued by the library since context creation
  * (instrumentation for the bench's gpu_launches field). */

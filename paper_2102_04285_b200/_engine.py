@@ -71,15 +71,27 @@ class DeviceTrace:
         pinned = ct._pinned or {}
         block = pinned.get("_block")
         lay = pinned.get("_packed")
+        staged = None
+        if not pinned and ct.n:
+            # ordinary host columns: the native builder packs them into the
+            # engine's page-locked staging block (host threads), then the
+            # packed path below uploads it in one DMA
+            staged = get(device).stage_packed(ct)
+            if staged is not None:
+                lay, block, pinned = staged
         if lay is not None:  # packed pinned block: one DMA of ~16 B/event, widened by xs_unpack
             # the device staging (packed block + wide columns) is kept with the
             # pinned trace and refilled by every DeviceTrace of it: the content
             # is the same trace, and repeated calls skip ~10 tensor allocations
+            # (staged traces: one grow-only set per engine, capacity-sized)
             n = ct.n
             cache = pinned.get("_dev_cache")
-            if cache is None or cache[0] != device:
-                dblock = torch.empty_like(block, device=dev)
-                m = max(n, 1)
+            need = (lay.total, n)
+            if cache is None or cache[0] != device or (staged is not None and (cache[5][0] < need[0] or
+                                                                               cache[5][1] < need[1])):
+                cap = (max(need[0], int(need[0] * 1.25)), max(n, int(n * 1.25))) if staged is not None else need
+                dblock = torch.empty(max(cap[0], 16), dtype=torch.uint8, device=dev)
+                m = max(cap[1], 1)
                 spec = (("start", torch.int64, 8), ("dur", torch.int64, 8), ("corr", torch.int64, 8),
                         ("pid", torch.int32, 4), ("tid", torch.int32, 4), ("name", torch.int32, 4),
                         ("cat", torch.uint8, 1), ("has_corr", torch.uint8, 1))
@@ -94,14 +106,22 @@ class DeviceTrace:
                     assert cols[k].numel() == m, (k, cols[k].numel(), m)
                     off += (m * w + 15) // 16 * 16
                 for k, dt in (("group_pid", torch.int32), ("pid_has_meta", torch.uint8)):
-                    o, nb = lay.offsets[k], lay.nbytes[k]
-                    cols[k] = dblock[o:o + nb].view(dt) if nb else torch.zeros(1, dtype=dt, device=dev)
-                cache = (device, dblock, wide, cols, packed_ptrs(lay, dblock))
+                    cols[k] = torch.zeros(1, dtype=dt, device=dev)  # (empty table; else a view, per call)
+                cache = (device, dblock, wide, cols, None, cap)
                 pinned["_dev_cache"] = cache
-            _, dblock, self._wide, cols, ptrs = cache
+            _, dblock, self._wide, cols, _, _ = cache
             self._dblock = dblock
-            dblock.copy_(block, non_blocking=True)
+            ptrs = packed_ptrs(lay, dblock)
+            nb = max(lay.total, 16)
+            dblock[:nb].copy_(block[:nb], non_blocking=True)
+            if staged is not None:
+                get(device).staged_upload_done()
             for k, t in cols.items():
+                if k in ("group_pid", "pid_has_meta"):
+                    o, nbk = lay.offsets[k], lay.nbytes[k]
+                    t = dblock[o:o + nbk].view(t.dtype) if nbk else t
+                else:
+                    t = t[:max(n, 1)]
                 setattr(self, k, t)
             if n:
                 unpack_into(get(device), lay, ptrs, 0, n, self)
@@ -246,6 +266,40 @@ class Engine:
             msg = self.lib.xs_last_error(self.ctx).decode(errors="replace")
             raise XsError(st, f"{what}: {self.lib.xs_status_str(st).decode()} {msg}".strip())
 
+    def stage_packed(self, ct: ColumnarTrace):
+        """Pack host columns into this engine's page-locked staging block
+        (native builder, host threads).  Returns (layout, block tensor, the
+        staging state dict that keeps the device buffers) or None when the
+        trace is not packable.  The block is reused by the next call once the
+        DMA recorded by staged_upload_done has finished."""
+        from .columnar import pack_native
+
+        torch = _torch()
+        st = self.__dict__.setdefault("_staging", {})
+        ev = st.get("event")
+        if ev is not None:
+            ev.synchronize()  # the previous upload out of the block is done
+
+        def alloc(nbytes):
+            blk = st.get("block")
+            if blk is None or blk.numel() < nbytes:
+                blk = torch.empty(max(nbytes, int(nbytes * 1.25)), dtype=torch.uint8, pin_memory=True)
+                st["block"] = blk
+            return blk.numpy()[:nbytes]
+
+        got = pack_native(ct, alloc)
+        if got is None:
+            return None
+        lay, _ = got
+        return lay, st["block"], st
+
+    def staged_upload_done(self) -> None:
+        torch = _torch()
+        st = self._staging
+        ev = st.get("event") or torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        st["event"] = ev
+
     def launches(self) -> int:
         return int(self.lib.xs_launch_count(self.ctx))
 
@@ -312,9 +366,12 @@ class Engine:
         if len(dt.ct.names):
             internal.copy_(torch.from_numpy(np.array(scaled.internal, np.int64)))
             has.copy_(torch.from_numpy(np.array(scaled.has_internal, np.uint8)))
-        prof = _lib.XsProfile(scaled.L, scaled.ann_start, scaled.ann_end, scaled.transition, scaled.interception,
+        words = np.array(scaled.words_of(scaled.L) + [int(x) for x in scaled.frac_table()], np.uint64)
+        tab = torch.from_numpy(words.view(np.int64)).to(dev)  # [L words | frac rows]
+        w = scaled.words
+        prof = _lib.XsProfile(w, 0, tab.data_ptr(), (C.c_int64 * 4)(*scaled.whole), tab.data_ptr() + 8 * w,
                               internal.data_ptr(), has.data_ptr())
-        return prof, (internal, has)
+        return prof, (internal, has, tab)
 
     def correct(self, dt: DeviceTrace, scaled, analyze_attribution: Optional[int] = None,
                 host_out=None, dev_out=None, async_copy: bool = False) -> CorrectRaw:

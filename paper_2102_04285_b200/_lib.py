@@ -43,11 +43,19 @@ class XsPacked(C.Structure):
     ]
 
 
+class XsPackLayout(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("n_exc", C.c_int64), ("total", C.c_int64),
+        ("start_w", C.c_int32), ("dur_w", C.c_int32), ("corr_w", C.c_int32), ("pid_w", C.c_int32),
+        ("tid_w", C.c_int32), ("name_w", C.c_int32), ("n_threads", C.c_int32), ("reserved", C.c_int32),
+        ("offset", C.c_int64 * 13), ("nbytes", C.c_int64 * 13), ("thread_exc", C.c_int64 * 64),
+    ]
+
+
 class XsProfile(C.Structure):
     _fields_ = [
-        ("L", C.c_int64), ("ann_start", C.c_int64), ("ann_end", C.c_int64),
-        ("transition", C.c_int64), ("interception", C.c_int64),
-        ("internal", C.c_void_p), ("has_internal", C.c_void_p),
+        ("words", C.c_int32), ("reserved", C.c_int32), ("L", C.c_void_p), ("whole", C.c_int64 * 4),
+        ("frac", C.c_void_p), ("internal", C.c_void_p), ("has_internal", C.c_void_p),
     ]
 
 
@@ -94,6 +102,8 @@ SIGNATURES = {
     "xs_chunk_info": (C.c_int, [P, C.c_int64, C.c_char_p, P, P, P, C.c_char_p, C.c_int]),
     "xs_chunk_decode": (C.c_int, [P, C.c_int64, C.c_char_p, P, P, P, P, P, P, P, P, P, P, C.c_char_p, C.c_int]),
     "xs_unpack": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P]),
+    "xs_pack_plan": (C.c_int, [C.POINTER(XsEvents), C.c_int, C.POINTER(XsPackLayout)]),
+    "xs_pack_fill": (C.c_int, [C.POINTER(XsEvents), C.POINTER(XsPackLayout), P, C.c_int64]),
     "xs_launch_count": (C.c_int64, [P]),
     "xs_profile_enable": (C.c_int, [P, C.c_int]),
     "xs_profile_read": (C.c_int, [P, P, P, C.c_int]),

@@ -139,64 +139,67 @@ INT64_MAX = 2**63 - 1
 
 @dataclass(frozen=True)
 class ScaledProfile:
-    """Amounts as integers over the common denominator ``L``.
+    """The profile's per-site amounts in the device's exact form.
 
-    The per-site amounts the reference draws (correction.py:90-100):
+    The amounts the reference draws per site (correction.py:90-100):
     ``annotation/2`` at ANN_START, ``annotation - annotation/2`` at ANN_END,
-    ``transition``, ``api_interception`` and ``api_internal[name]``.  Every
-    one is ``k / L`` exactly, so ``floor(sum)`` in ``quantize_amounts``
-    (_timeline.py:57-67) equals ``floor(sum_k / L)`` over int128 on the
-    device.
+    ``transition``, ``api_interception`` and ``api_internal[name]``.  Each is
+    split as ``whole + frac / L`` (``0 <= frac < L``, L the common denominator
+    of all of them) and L / frac are held in ``words`` 64-bit words, so
+    ``quantize_amounts``' floor of exact Fraction running sums
+    (_timeline.py:57-67) is reproduced for any denominator: the device keeps
+    the fractional running sum modulo L and adds 1 where it wraps.
     """
 
+    words: int
     L: int
-    ann_start: int
-    ann_end: int
-    transition: int
-    interception: int
-    internal: np.ndarray      # int64 [n_names]
+    whole: tuple          # 4 ints: ANN_START, ANN_END, TRANSITION, API_INTERCEPT
+    frac: tuple           # 4 ints, same order
+    internal: np.ndarray      # int64 [n_names] whole parts of api_internal
+    internal_frac: tuple      # ints [n_names]
     has_internal: np.ndarray  # uint8 [n_names]
 
     @classmethod
     def build(cls, profile: CalibrationProfile, names: Sequence[str]) -> "ScaledProfile":
         ann = Fraction(profile.annotation_ns)
         half = ann / 2
-        rest = ann - half
-        base = [half, rest, Fraction(profile.transition_ns), Fraction(profile.api_interception_ns)]
+        base = [half, ann - half, Fraction(profile.transition_ns), Fraction(profile.api_interception_ns)]
         internal = {k: Fraction(v) for k, v in profile.api_internal_ns.items()}
         den = 1
         for v in base + [internal[n] for n in names if n in internal]:
             den = den * v.denominator // math.gcd(den, v.denominator)
-        scaled = [int(v * den) for v in base]
+        words = next((w for w in (1, 2, 4, 8) if den.bit_length() <= 64 * w - 1), None)
+        if words is None:
+            raise ValueError(f"calibration profile common denominator has {den.bit_length()} bits; "
+                             "the device supports up to 511")
+
+        def split(v: Fraction):
+            w = math.floor(v)
+            _check64(w)
+            return w, int((v - w) * den)
+
+        whole, frac = zip(*[split(v) for v in base])
         ints = np.zeros(len(names), dtype=np.int64)
+        ifrac = [0] * len(names)
         has = np.zeros(len(names), dtype=np.uint8)
         for i, n in enumerate(names):
             if n in internal:
-                v = int(internal[n] * den)
-                _check64(v)
-                ints[i] = v
+                ints[i], ifrac[i] = split(internal[n])
                 has[i] = 1
-        for v in scaled + [den]:
-            _check64(v)
         ints.flags.writeable = False  # immutable: engines keep a device copy per profile
         has.flags.writeable = False
-        return cls(den, scaled[0], scaled[1], scaled[2], scaled[3], ints, has)
+        return cls(words, den, tuple(whole), tuple(frac), ints, tuple(ifrac), has)
 
-    def max_abs(self) -> int:
-        vals = [self.ann_start, self.ann_end, self.transition, self.interception]
-        if self.internal.size:
-            vals += [int(np.abs(self.internal).max())]
-        return max(abs(v) for v in vals)
+    def words_of(self, v: int) -> list:
+        return [(v >> (64 * k)) & 0xFFFFFFFFFFFFFFFF for k in range(self.words)]
 
-    def check_int128(self, n_sites: int) -> None:
-        """The device running sum is int128: |sum| <= n_sites * max|amount|."""
-        if (max(n_sites, 1) * max(self.max_abs(), 1)).bit_length() >= 126:
-            raise ValueError(
-                "calibration profile denominators too large for exact int128 accumulation "
-                f"(L={self.L}, {n_sites} sites)"
-            )
+    def frac_table(self) -> np.ndarray:
+        """uint64 [(4 + n_names) * words]: the fractional numerators, rows in
+        xs_profile_t order."""
+        rows = list(self.frac) + list(self.internal_frac)
+        return np.array([x for r in rows for x in self.words_of(r)], dtype=np.uint64)
 
 
 def _check64(v: int) -> None:
     if abs(v) > INT64_MAX:
-        raise ValueError("scaled calibration amount exceeds int64; profile denominators too large")
+        raise ValueError("calibration amount exceeds int64 nanoseconds")

@@ -157,10 +157,15 @@ class ColumnarTrace:
         import torch
 
         if packed:
-            lay = _pack_layout(self)
-            if lay is not None:
-                block = torch.empty(max(lay.total, 16), dtype=torch.uint8).pin_memory()
-                lay.fill(block.numpy())
+            hold = {}
+
+            def alloc(nbytes):
+                hold["block"] = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+                return hold["block"].numpy()
+
+            got = pack_native(self, alloc)  # native builder, host threads
+            if got is not None:
+                lay, block = got[0], hold["block"]
                 return ColumnarTrace(self.clock_domain, self.start, self.dur, self.pid, self.tid, self.cat,
                                      self.name, self.corr, self.has_corr, self.pids, self.group_pid, self.group_tid,
                                      self.names, self.processes, self.pid_has_meta, self._source,
@@ -246,6 +251,19 @@ class PackedLayout:
         self.nbytes = {k: a.nbytes for k, a in arrays.items()}
         self.n_exc = int(arrays["exc_row"].size)
 
+    @classmethod
+    def from_native(cls, nat) -> "PackedLayout":
+        lay = cls.__new__(cls)
+        lay.n = int(nat.n)
+        lay.widths = {"start": nat.start_w, "dur": nat.dur_w, "corr": nat.corr_w, "pid": nat.pid_w,
+                      "tid": nat.tid_w, "name": nat.name_w, "catf": 1}
+        lay.arrays = None
+        lay.offsets = {k: int(nat.offset[i]) for i, k in enumerate(_SECTIONS)}
+        lay.nbytes = {k: int(nat.nbytes[i]) for i, k in enumerate(_SECTIONS)}
+        lay.total = int(nat.total)
+        lay.n_exc = int(nat.n_exc)
+        return lay
+
     def fill(self, raw: np.ndarray) -> None:
         for k, a in self.arrays.items():
             o = self.offsets[k]
@@ -315,6 +333,50 @@ def _pack_layout(ct: "ColumnarTrace"):
     order = np.argsort(rows, kind="stable")
     arrays["exc_row"], arrays["exc_val"], arrays["exc_col"] = rows[order], vals[order], cols[order]
     return PackedLayout(n, arrays, widths)
+
+
+_SECTIONS = ("start", "start_base", "dur", "corr", "pid", "tid", "name", "catf", "group_pid", "pid_has_meta",
+             "exc_row", "exc_val", "exc_col")  # xs_pack_layout_t section order
+
+
+def _host_events(ct: "ColumnarTrace"):
+    """xs_events_t over HOST column pointers (engine dtypes) + the arrays it references."""
+    from . import _lib
+
+    cols = [np.ascontiguousarray(getattr(ct, k), dt) for k, dt in
+            (("start", np.int64), ("dur", np.int64), ("pid", np.int32), ("tid", np.int32), ("cat", np.uint8),
+             ("name", np.int32), ("corr", np.int64), ("has_corr", np.uint8), ("group_pid", np.int32),
+             ("pid_has_meta", np.uint8))]
+    p = [a.ctypes.data if a.size else None for a in cols]
+    ev = _lib.XsEvents(ct.n, *p[:8], ct.n_pids, ct.n_groups, len(ct.names), 0, p[8], p[9])
+    return ev, cols
+
+
+def pack_native(ct: "ColumnarTrace", alloc=None, n_threads: int = 0):
+    """The packed block built by the native host builder (xs_pack_plan /
+    xs_pack_fill, host threads; byte-identical to pack_block with zeroed
+    padding).  ``alloc(nbytes)`` returns a writable uint8 numpy view (e.g. of
+    a page-locked tensor) -- default: ordinary memory.  Returns (layout,
+    block view) or None when the trace is not packable."""
+    import ctypes as C
+
+    from . import _lib
+
+    lib = _lib.load()
+    ev, keep = _host_events(ct)
+    nat = _lib.XsPackLayout()
+    st = lib.xs_pack_plan(C.byref(ev), int(n_threads), C.byref(nat))
+    if st == _lib.XS_UNSUPPORTED:
+        return None
+    if st != 0:
+        raise RuntimeError(f"xs_pack_plan: {lib.xs_status_str(st).decode()}")
+    size = max(int(nat.total), 16)
+    raw = alloc(size) if alloc is not None else np.empty(size, np.uint8)
+    st = lib.xs_pack_fill(C.byref(ev), C.byref(nat), raw.ctypes.data, size)
+    if st != 0:
+        raise RuntimeError(f"xs_pack_fill: {lib.xs_status_str(st).decode()}")
+    del keep
+    return PackedLayout.from_native(nat), raw
 
 
 def pack_block(ct: "ColumnarTrace"):

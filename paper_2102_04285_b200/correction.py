@@ -17,7 +17,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import _engine, _lib
+from . import _engine, _lib, _split
 from .calibration import HOOK_KINDS, CalibrationProfile
 from .columnar import ColumnarTrace
 from .model import Event, InvalidTraceError, ProcessMeta, Trace, format_violations, meta_violations
@@ -60,7 +60,6 @@ def _run(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: Optio
     if meta_violations(ct.processes):
         raise InvalidTraceError(format_violations(_source(src, ct)))
     scaled = profile.scaled(ct.names)
-    scaled.check_int128(3 * ct.n + 8)
     eng = _engine.get()
     dt = device_trace if device_trace is not None else _engine.DeviceTrace(ct, eng.device)
     try:
@@ -115,9 +114,69 @@ def _remap_processes(eng, ct: ColumnarTrace) -> tuple:
     return tuple(procs)
 
 
+def _batched(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: Optional[int]):
+    """correct_trace (+ compute_overlap of the corrected trace when
+    ``attribution`` is given) over pid batches (_split: more rows than one
+    call takes, or keys wider than 64 bits over all pids).  Exact: sites,
+    quantization, slabs and the removal map are per pid (correction.py:132-157).
+    Errors keep the whole-trace semantics: any invalid batch raises the whole
+    trace's violations; otherwise the uncalibrated hook of the smallest row.
+    Returns (start, dur, report, processes, Breakdown or None)."""
+    from .overlap import decode_breakdown, merge_breakdowns
+
+    if meta_violations(ct.processes):
+        raise InvalidTraceError(format_violations(_source(src, ct)))
+    eng = _engine.get()
+    rows_by_pid = _split.pid_rows(ct)
+    start = np.empty(ct.n, np.int64)
+    dur = np.empty(ct.n, np.int64)
+    rep = CorrectionReport()
+    procs = {}
+    parts, errs = [], []
+    for pids in _split.plan_batches(ct):
+        sub, rows = _split.sub_trace(ct, pids, rows_by_pid)
+        scaled = profile.scaled(sub.names)
+        try:
+            raw = eng.correct(_engine.DeviceTrace(sub, eng.device), scaled, attribution)
+        except _engine.UncalibratedEvent as exc:
+            errs.append(_BatchError("uncalibrated", int(rows[exc.index])))
+            continue
+        except _engine.XsError as exc:
+            if exc.status == _lib.XS_INVALID_TRACE:
+                errs.append(_BatchError("invalid", int(rows[0])))
+                continue
+            raise
+        if attribution is not None:
+            parts.append(decode_breakdown(sub, eng.fetch_overlap(), lazy=False))
+        start[rows] = raw.start.cpu().numpy()
+        dur[rows] = raw.dur.cpu().numpy()
+        r = _report(sub, raw)
+        rep.removed_ns.update(r.removed_ns)
+        rep.shortfall_ns.update(r.shortfall_ns)
+        rep.original_total_ns += r.original_total_ns
+        rep.corrected_total_ns += r.corrected_total_ns
+        live = set(sub.pids.tolist())
+        for k, m in enumerate(_remap_processes(eng, sub)):
+            if m.pid in live:
+                procs[k] = m
+    if errs:
+        if any(e.kind == "invalid" for e in errs):
+            raise InvalidTraceError(format_violations(_source(src, ct)))
+        first = min(errs, key=lambda e: e.row)
+        name = ct.names[int(ct.name[first.row])]
+        raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile")
+    processes = tuple(procs.get(k, m) for k, m in enumerate(ct.processes))
+    return start, dur, rep, processes, (merge_breakdowns(parts) if attribution is not None else None)
+
+
 def correct_trace_columnar(ct: ColumnarTrace, profile: CalibrationProfile, device_trace=None,
                            _src=None) -> tuple:
     """Columnar correct_trace: returns (corrected ColumnarTrace, CorrectionReport)."""
+    if device_trace is None and _split.needs_split(ct):
+        start, dur, rep, procs, _ = _batched(ct, profile, _src if _src is not None else ct, None)
+        out = ColumnarTrace(ct.clock_domain, start, dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr,
+                            ct.pids, ct.group_pid, ct.group_tid, ct.names, procs, ct.pid_has_meta)
+        return out, rep
     eng, dt, raw = _run(ct, profile, _src if _src is not None else ct, None, device_trace)
     procs = _remap_processes(eng, ct)
     start = raw.start.cpu().numpy()
@@ -155,6 +214,15 @@ def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution
     from .overlap import Attribution, decode_breakdown
 
     attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
+    if device_trace is None and _split.needs_split(ct):
+        start, dur, rep, _, bd = _batched(ct, profile, ct, attr)
+        if out is not None:
+            np.asarray(out[0])[...] = start
+            np.asarray(out[1])[...] = dur
+            return out[0], out[1], rep, bd
+        import torch
+        dev = torch.device("cuda", _engine.get().device)
+        return torch.from_numpy(start).to(dev), torch.from_numpy(dur).to(dev), rep, bd
     eng, dt, raw = _run(ct, profile, ct, attr, device_trace, host_out=out)
     bd = decode_breakdown(ct, eng.fetch_overlap())
     if out is not None:
@@ -224,7 +292,6 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
     eng = _engine.get()
     dev = torch.device("cuda", eng.device)
     scaled = profile.scaled(ct.names)
-    scaled.check_int128(3 * ct.n + 8)
     subs = [_row_slice(ct, a, b) for a, b in parts]
     starts = ct.__dict__["_pid_starts"]
     has = starts[1:] > starts[:-1]
@@ -287,6 +354,8 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
                 ptrs.update({c: exc_dev.data_ptr() + lay.offsets[c] - lay.offsets["exc_row"]
                              for c in ("exc_row", "exc_val", "exc_col")})
                 _engine.unpack_into(e, lay, ptrs, a, b, SimpleNamespace(**tens), stream=copy)
+            elif subs[k]._pinned is None and _stage_batch(subs[k], st, par, e, tens, copy, b - a, W):
+                pass  # ordinary host columns: packed natively into this worker's page-locked staging
             else:
                 for c in cols:
                     src = subs[k]._pinned[c] if subs[k]._pinned is not None else \
@@ -358,6 +427,43 @@ def analyze_columnar_pipelined(ct: ColumnarTrace, profile: CalibrationProfile, o
 
     bd_all._lazy = build
     return out[0], out[1], rep, bd_all
+
+
+def _stage_batch(sub: ColumnarTrace, st: dict, par: int, eng, tens: dict, copy, rows: int, workers: int) -> bool:
+    """Pack one batch's host columns (native builder, this worker's share of
+    the host threads) into the worker's page-locked staging block of this
+    parity, DMA it on the copy stream and widen it into ``tens``.  False when
+    the batch is not packable (the caller copies the wide columns)."""
+    import os
+
+    import torch
+
+    from .columnar import pack_native
+
+    sp = st.setdefault("stage", [{}, {}])[par]
+    if sp.get("ev") is not None:
+        sp["ev"].synchronize()  # the last DMA out of this staging block is done
+
+    def alloc(nbytes):
+        h = sp.get("host")
+        if h is None or h.numel() < nbytes:
+            h = sp["host"] = torch.empty(int(nbytes * 1.25) + 16, dtype=torch.uint8, pin_memory=True)
+        return h.numpy()[:nbytes]
+
+    got = pack_native(sub, alloc, n_threads=max(1, (os.cpu_count() or 1) // max(workers, 1)))
+    if got is None:
+        return False
+    lay = got[0]
+    nb = max(lay.total, 16)
+    d = sp.get("dev")
+    if d is None or d.numel() < nb:
+        d = sp["dev"] = torch.empty(int(nb * 1.25) + 16, dtype=torch.uint8, device=tens["start"].device)
+    d[:nb].copy_(sp["host"][:nb], non_blocking=True)
+    ev = sp.get("ev") or torch.cuda.Event()
+    ev.record(copy)
+    sp["ev"] = ev
+    _engine.unpack_into(eng, lay, _engine.packed_ptrs(lay, d), 0, rows, SimpleNamespace(**tens), stream=copy)
+    return True
 
 
 @dataclass

@@ -113,71 +113,152 @@ __global__ void k_tie_fix(EventView v, const uint64_t* k1, uint32_t* slot, int64
   }
 }
 
-__device__ __forceinline__ int64_t site_amount(const xs_profile_t& pr, const EventView& v, int i, int sub) {
+// the quantize scan's element: the fractional parts' running sum modulo L
+// (W little-endian words; L < 2^(64W-1), so a sum of two residues never
+// overflows W words), segmented per pid by a head flag
+template <int W>
+struct SegMod {
+  uint64_t w[W];
+  int head;
+  int pad;
+};
+
+template <int W>
+__device__ __forceinline__ bool mw_less(const uint64_t* a, const uint64_t* b) {
+#pragma unroll
+  for (int i = W - 1; i >= 0; i--)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return false;
+}
+
+template <int W>
+struct SegModOp {
+  uint64_t L[W];
+  __device__ SegMod<W> operator()(const SegMod<W>& a, const SegMod<W>& b) const {
+    SegMod<W> r;
+    r.head = a.head | b.head;
+    r.pad = 0;
+    if (b.head) {
+#pragma unroll
+      for (int i = 0; i < W; i++) r.w[i] = b.w[i];
+      return r;
+    }
+    add_mod(a.w, b.w, r.w);
+    return r;
+  }
+  __device__ void add_mod(const uint64_t* a, const uint64_t* b, uint64_t* r) const {
+    unsigned long long c = 0;
+#pragma unroll
+    for (int i = 0; i < W; i++) {  // r = a + b (< 2L <= 2^(64W): no carry out)
+      const unsigned long long s = a[i] + c;
+      const unsigned long long c1 = s < c;
+      r[i] = s + b[i];
+      c = c1 + (r[i] < s);
+    }
+    if (!mw_less<W>(r, L)) {  // r -= L
+      unsigned long long br = 0;
+#pragma unroll
+      for (int i = 0; i < W; i++) {
+        const unsigned long long d = r[i] - L[i];
+        const unsigned long long b1 = r[i] < L[i];
+        r[i] = d - br;
+        br = b1 | (d < br);
+      }
+    }
+  }
+};
+
+// site subkind -> row of the profile's whole / frac tables (API_INTERNAL:
+// 4 + the event's name)
+__device__ __forceinline__ int amount_row(int sub, int name) {
   switch (sub) {
-    case ANN_START: return pr.ann_start;
-    case ANN_END: return pr.ann_end;
-    case TRANSITION_HOOK: return pr.transition;
-    case API_INTERCEPT: return pr.interception;
-    default: return pr.internal[v.ev.name[i]];
+    case ANN_START: return 0;
+    case ANN_END: return 1;
+    case TRANSITION_HOOK: return 2;
+    case API_INTERCEPT: return 3;
+    default: return 4 + name;
   }
 }
 
 constexpr int Q_ITEMS = 8;
-__global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
-                                                       EventView v, xs_profile_t pr, const int* site_ev,
-                                                       const uint8_t* site_sub, int64_t* qslot,
-                                                       TileDesc<SegI128>* desc, int* flags, int* tile_ctr) {
+// quantize_amounts (_timeline.py:57-67) per pid in site order:
+// q_i = floor(S_i) - floor(S_{i-1}) with S the running sum of exact amounts
+// = whole_i + [ P_i < frac_i ], P_i the inclusive running sum of the
+// fractional numerators modulo L (a carry past L is exactly the floor step)
+template <int W>
+__global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns,
+                                                       int tb, EventView v, xs_profile_t pr, const int* site_ev,
+                                                       int64_t* qslot, TileDesc<SegMod<W>>* desc, int* flags,
+                                                       int* tile_ctr) {
   const int tile = next_tile(tile_ctr);
   const int64_t ns = *d_ns;
   if ((int64_t)tile * XS_BLOCK * Q_ITEMS >= ns) return;  // tail tiles of the upper-bound grid
   const int64_t base = (int64_t)tile * XS_BLOCK * Q_ITEMS + (int64_t)threadIdx.x * Q_ITEMS;
-  int64_t amt[Q_ITEMS];
+  SegModOp<W> op;
+#pragma unroll
+  for (int i = 0; i < W; i++) op.L[i] = pr.L[i];
+  int row[Q_ITEMS];
   int hd[Q_ITEMS];
-  SegI128Op op;
-  SegI128 agg;
-  agg.v = 0;
-  agg.head = 0;
-  agg.pad[0] = agg.pad[1] = agg.pad[2] = 0;
+  SegMod<W> id;
+#pragma unroll
+  for (int i = 0; i < W; i++) id.w[i] = 0;
+  id.head = 0;
+  id.pad = 0;
+  SegMod<W> agg = id;
   const int pshift = tb + 3;
 #pragma unroll
   for (int j = 0; j < Q_ITEMS; j++) {
-    int64_t q = base + j;
-    amt[j] = 0;
+    const int64_t q = base + j;
+    row[j] = -1;
     hd[j] = 0;
     if (q < ns) {
       // the subkind is the key's low 3 bits: only API_INTERNAL sites gather
       // their event (for the API name); the rest are profile constants
       const uint64_t kq = k1[q];
       const int sub = (int)(kq & 7u);
-      amt[j] = sub == API_INTERNAL ? pr.internal[v.ev.name[site_ev[slot[q]]]] : site_amount(pr, v, 0, sub);
+      row[j] = amount_row(sub, sub == API_INTERNAL ? v.ev.name[site_ev[slot[q]]] : 0);
       hd[j] = q == 0 || (k1[q - 1] >> pshift) != (kq >> pshift);
-      SegI128 e;
-      e.v = amt[j];
+      SegMod<W> e;
+#pragma unroll
+      for (int i = 0; i < W; i++) e.w[i] = pr.frac[(int64_t)row[j] * W + i];
       e.head = hd[j];
-      e.pad[0] = e.pad[1] = e.pad[2] = 0;
+      e.pad = 0;
       agg = op(agg, e);
     }
   }
-  SegI128 id;
-  id.v = 0;
-  id.head = 0;
-  id.pad[0] = id.pad[1] = id.pad[2] = 0;
-  SegI128 cur = grid_exclusive(agg, op, id, tile, desc, flags);
-  __int128 run = cur.v;
-  const int64_t L = pr.L;
+  SegMod<W> run = grid_exclusive(agg, op, id, tile, desc, flags);
 #pragma unroll
   for (int j = 0; j < Q_ITEMS; j++) {
-    int64_t q = base + j;
+    const int64_t q = base + j;
     if (q >= ns) break;
-    __int128 before = hd[j] ? (__int128)0 : run;
-    __int128 after = before + amt[j];
-    int64_t qv;
-    if (L == 1) qv = (int64_t)(after - before);
-    else qv = floor_div(after, L) - floor_div(before, L);
-    qslot[slot[q]] = qv;
-    run = after;
+    uint64_t f[W], after[W];
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+      f[i] = pr.frac[(int64_t)row[j] * W + i];
+      if (hd[j]) run.w[i] = 0;
+    }
+    op.add_mod(run.w, f, after);
+    const int64_t whole = row[j] < 4 ? pr.whole[row[j]] : pr.internal[row[j] - 4];
+    qslot[slot[q]] = whole + (mw_less<W>(after, f) ? 1 : 0);
+#pragma unroll
+    for (int i = 0; i < W; i++) run.w[i] = after[i];
   }
+}
+
+template <int W>
+static int launch_quantize(xs_ctx* ctx, int64_t tiles, cudaStream_t s, const uint64_t* k1, const uint32_t* sl,
+                           const int64_t* d_ns, int tb, const EventView& v, const xs_profile_t& pr,
+                           const int* site_ev, int64_t* qslot) {
+  TileDesc<SegMod<W>>* desc;
+  int *flags, *tctr;
+  XS_TRY(ws(ctx, W_QSCAN_DESC, tiles + 1, s, &desc));
+  XS_TRY(ws(ctx, W_QSCAN_FLAGS, tiles + 1, s, &flags));
+  XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
+  XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
+  XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+  XS_LAUNCH(ctx, k_quantize<W>, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, v, pr, site_ev, qslot, desc, flags,
+            tctr);
+  return XS_OK;
 }
 
 // per owner: budget caps (correction.py:139-153) + shortfall per (pid, hook);
@@ -643,15 +724,12 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     XS_TRY(ws(ctx, W_QVAL, ns + 1, s, &qslot));
     {
       const int64_t tiles = (ns + XS_BLOCK * Q_ITEMS - 1) / (XS_BLOCK * Q_ITEMS);
-      TileDesc<SegI128>* desc;
-      int *flags, *tctr;
-      XS_TRY(ws(ctx, W_QSCAN_DESC, tiles + 1, s, &desc));
-      XS_TRY(ws(ctx, W_QSCAN_FLAGS, tiles + 1, s, &flags));
-      XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
-      XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
-      XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
-      XS_LAUNCH(ctx, k_quantize, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, v, *prof, site_ev, site_sub, qslot, desc,
-                flags, tctr);
+      switch (prof->words) {
+        case 1: XS_TRY(launch_quantize<1>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_ev, qslot)); break;
+        case 2: XS_TRY(launch_quantize<2>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_ev, qslot)); break;
+        case 4: XS_TRY(launch_quantize<4>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_ev, qslot)); break;
+        default: XS_TRY(launch_quantize<8>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_ev, qslot)); break;
+      }
     }
     ps_q.end();
     // 4. budget caps per owner

@@ -147,8 +147,17 @@ int run_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s
     }
     if (ctx->h_stats->n_bad) return XS_INVALID_TRACE;
     if (ctx->h_stats->depth_overflow) {
-      ctx->err = "merged multi-tid operation path deeper than the device limit";
-      return XS_UNSUPPORTED;
+      // merged multi-tid stacks deeper than the register-sized merge: re-run
+      // with a global scratch that holds the deepest one (no depth limit)
+      long long need = ctx->h_stats->pad[7];
+      long long cap = 1024;
+      while (cap < need) cap <<= 1;
+      if (cap <= ctx->deep_cap) {
+        ctx->err = "deep operation-path scratch could not be sized";
+        return XS_NO_MEMORY;
+      }
+      ctx->deep_cap = cap;
+      continue;
     }
     if (!ctx->h_stats->table_full) {
       ctx->have_overlap = true;
@@ -424,7 +433,8 @@ static int correct_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
                           int64_t* out_dur, int64_t* bad_event, cudaStream_t s, bool corrected_spans) {
   ctx->have_correct = false;
   if (bad_event) *bad_event = -1;
-  if (!prof || prof->L <= 0) return XS_BAD_ARGUMENT;
+  if (!prof || !prof->L || !prof->frac || (prof->words != 1 && prof->words != 2 && prof->words != 4 && prof->words != 8))
+    return XS_BAD_ARGUMENT;
   if (ev->n > 0 && (!out_start || !out_dur)) return XS_BAD_ARGUMENT;
   EventView v{*ev, ev->start, ev->dur};
   XS_TRY(stage_events(ctx, v, s, false, true, prof));  // (sync: sizes; per-event rule violations stop here)
@@ -544,7 +554,8 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
   ctx->have_correct = false;
   ctx->have_overlap = false;
   if (bad_event) *bad_event = -1;
-  if (!prof || prof->L <= 0) return XS_BAD_ARGUMENT;
+  if (!prof || !prof->L || !prof->frac || (prof->words != 1 && prof->words != 2 && prof->words != 4 && prof->words != 8))
+    return XS_BAD_ARGUMENT;
   if (ev->n > 0 && (!out_start_dev || !out_dur_dev)) return XS_BAD_ARGUMENT;
   EventView v{*ev, ev->start, ev->dur};
   EventView vc{*ev, out_start_dev, out_dur_dev};

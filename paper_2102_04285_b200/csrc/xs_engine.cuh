@@ -68,6 +68,7 @@ enum Slot : int {
   W_BS_COUNTS, W_BS_OFFS, W_BS_TAIL, W_BS_CHUNK, W_RMAP_IDX,
   W_CUB_TEMP2, W_OPG, W_OPG_INV, W_TGRP_FLAG, W_TGRP_IDX, W_TILE_CTR_B, W_CUB_TEMP_B, W_BS_COUNTS_B, W_BS_OFFS_B, W_BS_TAIL_B, W_BS_CHUNK_B,
   W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
+  W_DEEP_OVF, W_DEEP_SCRATCH,
   W_NUM_SLOTS
 };
 
@@ -190,6 +191,7 @@ struct xs_ctx {
   // last transitions
   long long n_trans_out = 0;
   int trie_cap_log2 = 12;
+  long long deep_cap = 0;  // ints of global scratch per thread for merged op stacks deeper than MAXD
   bool force_lsd = false;  // bucketed sort overflowed on this input: use the LSD path
   xs::OpsState ops;
   // optional per-stage device timing (CUDA events on the launching stream)

@@ -27,7 +27,8 @@ std::string segment_key(xs_ctx* ctx, const char* tag, const void* extra, size_t 
   k.push_back('\0');
   k.append(reinterpret_cast<const char*>(ctx->h_stats), sizeof(Stats));
   k.append(reinterpret_cast<const char*>(extra), extra_bytes);
-  const long long misc[4] = {ctx->ws_generation, ctx->trie_cap_log2, ctx->force_lsd ? 1 : 0, ctx->prof_on ? 1 : 0};
+  const long long misc[5] = {ctx->ws_generation, ctx->trie_cap_log2, ctx->force_lsd ? 1 : 0, ctx->prof_on ? 1 : 0,
+                             ctx->deep_cap};
   k.append(reinterpret_cast<const char*>(misc), sizeof(misc));
   return k;
 }

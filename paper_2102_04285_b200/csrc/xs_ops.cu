@@ -292,12 +292,71 @@ __global__ void k_pid_keys(const uint64_t* skeys, int64_t n2, const int32_t* gro
 
 constexpr int MAXD = 256;
 
-// general case: rank-merge of every tid's chain at each run end of the pid order
+// innermost op of group g active just after time tt (its chain to the root
+// is the group's active stack), or -1
+__device__ __forceinline__ int group_ctx(int g, const int* group_ops, const int64_t* gs_off, const uint64_t* skeys,
+                                         const uint32_t* svals, const int* parent, uint64_t tt, uint64_t tmask) {
+  const int cnt = group_ops[g];
+  if (!cnt) return -1;
+  int64_t a = gs_off[g], b = a + 2 * (int64_t)cnt;
+  // last j in [a,b) with time <= tt
+  int64_t lo = a, hi = b;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (((skeys[mid] >> 1) & tmask) <= tt) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo == a) return -1;
+  const int64_t j = lo - 1;
+  const uint32_t r = svals[j];
+  return (skeys[j] & 1ull) ? (int)r : parent[r];
+}
+
+// merge the rank-ordered chains (ops[cs[c] .. end of chain c], leaf first,
+// head[c] = its root end) root-down in rank order (start, -end, group, name,
+// index -- overlap.py:96-99), interning the adjacent-deduplicated name path
+// (path_of, _sweep_py.py:16-26) in the trie as we go
+__device__ __forceinline__ int kway_merge(const int* ops, const int* cs, int* head, int nctx, int n,
+                                          const int* rank_ev, const EventView& v, TrieView t) {
+  int cur = 0;
+  for (int done = 0; done < n; done++) {
+    int best = -1;
+    int64_t bs = 0, be = 0;
+    int bg = 0, bn = 0, bi = 0;
+    for (int c = 0; c < nctx; c++) {
+      if (head[c] < cs[c]) continue;
+      const int ix = rank_ev[ops[head[c]]];
+      const int64_t xs_ = v.start[ix], xe = v.start[ix] + v.dur[ix];
+      const int xg = v.ev.tid[ix], xn = v.ev.name[ix];
+      const bool less = best < 0 || (xs_ != bs ? xs_ < bs : xe != be ? xe > be : xg != bg ? xg < bg
+                                                                  : xn != bn ? xn < bn : ix < bi);
+      if (less) {
+        best = c;
+        bs = xs_;
+        be = xe;
+        bg = xg;
+        bn = xn;
+        bi = ix;
+      }
+    }
+    head[best]--;
+    cur = trie_intern(cur, bn, t);
+  }
+  return cur;
+}
+
+// general case: rank-merge of every tid's chain at each run end of the pid
+// order.  Endpoints whose merged stack exceeds the register-sized arrays
+// (more than 64 op tids active, or more than MAXD ops) go to an overflow
+// list served by k_pidpath_deep from a global scratch of deep_cap ints per
+// thread; when deep_cap is too small the need is recorded (Stats pad[7]) and
+// the host re-runs the attempt with a scratch that fits -- no depth limit.
 __global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const int* pid_group0, const int* opg,
                                   const int* opg_inv, const int* group_ops,
                                   const int64_t* gs_off, const uint64_t* skeys, const uint32_t* svals,
                                   const int* parent, const int* node, const int* rank_ev, EventView v,
-                                  int* pidpath, TrieView t, Stats* st) {
+                                  int* pidpath, TrieView t, Stats* st, int* ovf_list, int* ovf_count,
+                                  long long deep_cap) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n2) return;
   if (pk[k] == ~0ull) {  // sentinel tail
@@ -314,85 +373,93 @@ __global__ void k_pidpath_general(const uint64_t* pk, int64_t n2, int tb, const 
   uint64_t tt = key & tmask;
   int ctxs[64];
   int nctx = 0;
+  bool over = false;
   // only the pid's op-carrying groups (dense numbering): a pid with hundreds
   // of GPU-stream tids has a handful of op tids
   const int x0 = opg[pid_group0[p]], x1 = opg[pid_group0[p + 1]];
-  for (int x = x0; x < x1; x++) {
-    const int g = opg_inv[x];
-    int cnt = group_ops[g];
-    if (!cnt) continue;
-    int64_t a = gs_off[g], b = a + 2 * (int64_t)cnt;
-    // last j in [a,b) with time <= tt
-    int64_t lo = a, hi = b;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (((skeys[mid] >> 1) & tmask) <= tt) lo = mid + 1;
-      else hi = mid;
-    }
-    if (lo == a) continue;
-    int64_t j = lo - 1;
-    uint32_t r = svals[j];
-    int o = (skeys[j] & 1ull) ? (int)r : parent[r];
+  for (int x = x0; x < x1 && !over; x++) {
+    const int o = group_ctx(opg_inv[x], group_ops, gs_off, skeys, svals, parent, tt, tmask);
     if (o < 0) continue;
-    if (nctx == 64) {
-      atomicAdd((unsigned long long*)&st->depth_overflow, 1ull);
-      pidpath[k] = 0;
-      return;
-    }
-    ctxs[nctx++] = o;
+    if (nctx == 64) over = true;
+    else ctxs[nctx++] = o;
   }
-  if (nctx == 0) {
+  if (!over && nctx == 0) {
     pidpath[k] = 0;
     return;
   }
-  if (nctx == 1) {
+  if (!over && nctx == 1) {
     pidpath[k] = node[ctxs[0]];
     return;
   }
-  // every chain is already in rank order (a parent precedes its children);
-  // k-way merge of the chains from their roots, interning root-down as we go
-  // (was: gather + insertion sort, O(depth^2) rank comparisons per endpoint)
   int ops[MAXD];
   int cs[64], head[64];
   int n = 0;
-  for (int c = 0; c < nctx; c++) {
+  for (int c = 0; c < nctx && !over; c++) {
     cs[c] = n;
-    for (int o = ctxs[c]; o >= 0; o = parent[o]) {
-      if (n == MAXD) {
-        atomicAdd((unsigned long long*)&st->depth_overflow, 1ull);
-        pidpath[k] = 0;
-        return;
-      }
-      ops[n++] = o;
+    for (int o = ctxs[c]; o >= 0 && !over; o = parent[o]) {
+      if (n == MAXD) over = true;
+      else ops[n++] = o;
     }
     head[c] = n - 1;  // root end of chain c (chain c is ops[cs[c] .. n), leaf first)
   }
-  int cur = 0;
-  for (int done = 0; done < n; done++) {
-    int best = -1;
-    int64_t bs = 0, be = 0;
-    int bg = 0, bn = 0, bi = 0;
-    for (int c = 0; c < nctx; c++) {
-      if (head[c] < cs[c]) continue;
-      const int ix = rank_ev[ops[head[c]]];
-      const int64_t xs_ = v.start[ix], xe = v.start[ix] + v.dur[ix];
-      const int xg = v.ev.tid[ix], xn = v.ev.name[ix];
-      // rank order (start, -end, group, name, index) -- overlap.py:96-99
-      const bool less = best < 0 || (xs_ != bs ? xs_ < bs : xe != be ? xe > be : xg != bg ? xg < bg
-                                                                  : xn != bn ? xn < bn : ix < bi);
-      if (less) {
-        best = c;
-        bs = xs_;
-        be = xe;
-        bg = xg;
-        bn = xn;
-        bi = ix;
-      }
+  if (over) {  // needs 3 ints per active op tid + one per stacked op
+    long long need = 0;
+    for (int x = x0; x < x1; x++) {
+      int o = group_ctx(opg_inv[x], group_ops, gs_off, skeys, svals, parent, tt, tmask);
+      if (o < 0) continue;
+      need += 3;
+      for (; o >= 0; o = parent[o]) need++;
     }
-    head[best]--;
-    cur = trie_intern(cur, bn, t);
+    pidpath[k] = 0;
+    if (need <= deep_cap) {
+      ovf_list[atomicAdd(ovf_count, 1)] = (int)k;
+    } else {
+      atomicMax((unsigned long long*)&st->pad[7], (unsigned long long)need);
+      atomicAdd((unsigned long long*)&st->depth_overflow, 1ull);
+    }
+    return;
   }
-  pidpath[k] = cur;
+  pidpath[k] = kway_merge(ops, cs, head, nctx, n, rank_ev, v, t);
+}
+
+// the overflow endpoints of k_pidpath_general, each with deep_cap ints of
+// global scratch: [ctx | cs | head] (nctx each) then the stacked ops
+__global__ void k_pidpath_deep(const uint64_t* pk, int tb, const int* pid_group0, const int* opg, const int* opg_inv,
+                               const int* group_ops, const int64_t* gs_off, const uint64_t* skeys,
+                               const uint32_t* svals, const int* parent, const int* rank_ev, EventView v,
+                               int* pidpath, TrieView t, const int* ovf_list, const int* ovf_count, int* scratch,
+                               long long deep_cap) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int* mem = scratch + tid * deep_cap;
+  const uint64_t tmask = (1ull << tb) - 1;
+  const int total = *ovf_count;
+  for (int64_t i = tid; i < total; i += stride) {
+    const int64_t k = ovf_list[i];
+    const uint64_t key = pk[k] >> 1;
+    const int p = (int)(key >> tb);
+    const uint64_t tt = key & tmask;
+    const int x0 = opg[pid_group0[p]], x1 = opg[pid_group0[p + 1]];
+    int nctx = 0;
+    for (int x = x0; x < x1; x++)
+      nctx += group_ctx(opg_inv[x], group_ops, gs_off, skeys, svals, parent, tt, tmask) >= 0;
+    int* ctxs = mem;
+    int* cs = mem + nctx;
+    int* head = mem + 2 * nctx;
+    int* ops = mem + 3 * nctx;
+    int c = 0;
+    for (int x = x0; x < x1; x++) {
+      const int o = group_ctx(opg_inv[x], group_ops, gs_off, skeys, svals, parent, tt, tmask);
+      if (o >= 0) ctxs[c++] = o;
+    }
+    int n = 0;
+    for (c = 0; c < nctx; c++) {
+      cs[c] = n;
+      for (int o = ctxs[c]; o >= 0; o = parent[o]) ops[n++] = o;
+      head[c] = n - 1;
+    }
+    pidpath[k] = kway_merge(ops, cs, head, nctx, n, rank_ev, v, t);
+  }
 }
 
 __global__ void k_trie_init(uint64_t* keys, int* vals, int64_t cap, int* parent, int* name, int* count) {
@@ -471,6 +538,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
     XS_CUDA(cudaMemsetAsync(&stp->table_full, 0, sizeof(long long), s));
     XS_CUDA(cudaMemsetAsync(&stp->depth_overflow, 0, sizeof(long long), s));
     XS_CUDA(cudaMemsetAsync(&stp->pad[3], 0, sizeof(long long), s));
+    XS_CUDA(cudaMemsetAsync(&stp->pad[7], 0, sizeof(long long), s));
   }
   const Stats& H = *ctx->h_stats;
   const int64_t m = H.n_ops_nz;
@@ -604,8 +672,20 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
     XS_TRY(ws(ctx, W_GS_OFF, ng + 1, s, &gs_off));
     XS_LAUNCH(ctx, k_gs_off, 1, 1024, 0, s, group_ops_pos, ng, gs_off);
     XS_TRY(sort_keys_u64(ctx, &pk, &pk_alt, 2 * m, pb + tb + 1, s));
+    int* ovf;  // [count | list of overflow endpoints]
+    XS_TRY(ws(ctx, W_DEEP_OVF, 2 * m + 4, s, &ovf));
+    XS_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), s));
     XS_LAUNCH(ctx, k_pidpath_general, grid_for(2 * m, 128), 128, 0, s, pk, 2 * m, tb, (int*)ctx->ptr[W_PID_GROUP0],
-              opg, opg_inv, group_ops_pos, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st);
+              opg, opg_inv, group_ops_pos, gs_off, sk, sv, parent, node, rank_ev, v, pidpath, os.trie, st, ovf + 1,
+              ovf, ctx->deep_cap);
+    if (ctx->deep_cap > 0) {  // a previous attempt overflowed: serve the deep stacks
+      const int threads = (int)std::max<long long>(32, std::min<long long>(148 * 128, (1ll << 28) / ctx->deep_cap));
+      int* scratch;
+      XS_TRY(ws(ctx, W_DEEP_SCRATCH, (int64_t)threads * ctx->deep_cap, s, &scratch));
+      XS_LAUNCH(ctx, k_pidpath_deep, (threads + 127) / 128, 128, 0, s, pk, tb, (int*)ctx->ptr[W_PID_GROUP0], opg,
+                opg_inv, group_ops_pos, gs_off, sk, sv, parent, rank_ev, v, pidpath, os.trie, ovf + 1, ovf, scratch,
+                ctx->deep_cap);
+    }
     os.pk = pk;
   }
   return XS_OK;

@@ -19,7 +19,7 @@ from enum import Enum
 
 import numpy as np
 
-from . import _engine, _lib
+from . import _engine, _lib, _split
 from .columnar import ColumnarTrace
 from .model import Category, InvalidTraceError, Trace, format_violations, meta_violations
 
@@ -216,6 +216,8 @@ def compute_overlap_columnar(ct: ColumnarTrace, attribution: Attribution = Attri
     """compute_overlap over a ColumnarTrace (or an already-uploaded DeviceTrace)."""
     if meta_violations(ct.processes):
         _raise_invalid(_source if _source is not None else ct, ct)
+    if device_trace is None and _split.needs_split(ct):
+        return _overlap_batched(ct, attribution, _source)
     eng = _engine.get()
     dt = device_trace if device_trace is not None else _engine.DeviceTrace(ct, eng.device)
     attr = 1 if Attribution(attribution) is Attribution.CORRELATION else 0
@@ -226,6 +228,36 @@ def compute_overlap_columnar(ct: ColumnarTrace, attribution: Attribution = Attri
             _raise_invalid(_source if _source is not None else ct, ct)
         raise
     return decode_breakdown(ct, raw)
+
+
+def merge_breakdowns(parts) -> Breakdown:
+    """Breakdowns of disjoint pid sets -> one Breakdown."""
+    bd = Breakdown()
+    for b in parts:
+        bd.cells.update(b.cells)
+        bd.spans.update(b.spans)
+        bd.untracked.update(b.untracked)
+    return bd
+
+
+def _overlap_batched(ct: ColumnarTrace, attribution, _source) -> Breakdown:
+    """compute_overlap over pid batches (_split: more rows than one call
+    takes, or keys wider than 64 bits over all pids); exact because every
+    cell, span and untracked value is per pid (overlap.py:126)."""
+    eng = _engine.get()
+    attr = 1 if Attribution(attribution) is Attribution.CORRELATION else 0
+    rows_by_pid = _split.pid_rows(ct)
+    parts = []
+    for pids in _split.plan_batches(ct):
+        sub, _ = _split.sub_trace(ct, pids, rows_by_pid)
+        try:
+            raw = eng.overlap(_engine.DeviceTrace(sub, eng.device), attr)
+        except _engine.XsError as exc:
+            if exc.status == _lib.XS_INVALID_TRACE:
+                _raise_invalid(_source if _source is not None else ct, ct)
+            raise
+        parts.append(decode_breakdown(sub, raw, lazy=False))
+    return merge_breakdowns(parts)
 
 
 def compute_overlap(trace, attribution: Attribution = Attribution.INSTANT, kernel=None) -> Breakdown:
@@ -292,13 +324,17 @@ def sweep_pid(starts, ends, cats, ranks, fixed_paths, add_order, rem_order, rank
     ColumnarTrace; each operation sits on its own tid numbered by its rank,
     so the device's (start, -end, tid, name) rank order reproduces the given
     ``ranks`` and its multi-tid path merge is ``path_of``'s rank-ordered,
-    adjacent-deduplicated name list.  GPU events pinned to launch-site paths
-    (``fixed_paths`` >= 0, CORRELATION) are computed by compute_overlap
-    itself from correlations; this shim serves INSTANT inputs.
-    """
-    if any(fp >= 0 for fp in fixed_paths):
-        raise NotImplementedError("sweep_pid shim: fixed (CORRELATION) paths are resolved inside compute_overlap")
-    cur = path_table.get_id(())
+    adjacent-deduplicated name list.
+
+    GPU events pinned to a launch-site path (``fixed_paths[i] >= 0``,
+    CORRELATION, _sweep_py.py:70-79, 93-99, 107-111) run through the device's
+    CORRELATION attribution: each distinct fixed path p gets a private instant
+    after the pid's events where operations named ``path_table.paths[p]``
+    (rank-ordered by tid) are the only active events, and a zero-duration
+    ACCEL_API launcher there carries a correlation id shared with the pinned
+    GPU events.  Operation-only intervals are untracked and zero-duration
+    events add no cells, so the extra region changes nothing but the span,
+    and ``tracked`` is read directly."""
     idx = list(add_order)
     n = len(idx)
     if n == 0:
@@ -306,17 +342,48 @@ def sweep_pid(starts, ends, cats, ranks, fixed_paths, add_order, rem_order, rank
     s = np.array([starts[i] for i in idx], np.int64)
     e = np.array([ends[i] for i in idx], np.int64)
     c = np.array([cats[i] for i in idx], np.uint8)
+    fx = np.array([fixed_paths[i] for i in idx], np.int64)
     is_op = c == 0
     rk = np.array([ranks[i] for i in idx], np.int64)
-    nid = np.array([rank_name_ids[r] if op else 0 for r, op in zip(rk.tolist(), is_op.tolist())], np.int64)
-    names = sorted({str(x) for x in nid[is_op].tolist()} | {"_"})
-    nrank = {x: k for k, x in enumerate(names)}
-    name = np.array([nrank[str(x)] if op else nrank["_"] for x, op in zip(nid.tolist(), is_op.tolist())], np.int32)
+    nid = [rank_name_ids[r] if op else None for r, op in zip(rk.tolist(), is_op.tolist())]
     tid = np.where(is_op, rk + 1, 0)
+    corr = np.zeros(n, np.int64)
+    has = np.zeros(n, np.uint8)
+    pinned = sorted({int(p) for p in fx.tolist() if p >= 0})
+    extra = []  # (start, dur, cat, tid, name id, corr, has_corr)
+    if pinned:
+        slot = {p: k for k, p in enumerate(pinned)}
+        sel = fx >= 0
+        corr[sel] = [slot[int(p)] + 1 for p in fx[sel].tolist()]
+        has[sel] = 1
+        t0 = int(e.max()) + 2
+        tid_base = int(tid.max()) + 1
+        for p in pinned:
+            tp = t0 + 3 * slot[p]
+            for j, name_id in enumerate(path_table.paths[p]):  # rank order = tid order (equal intervals)
+                extra.append((tp, 2, 0, tid_base + j, name_id, 0, 0))
+            extra.append((tp + 1, 0, 4, 0, None, slot[p] + 1, 1))  # the launcher
+    names_used = {str(x) for x in nid if x is not None} | {str(x[4]) for x in extra if x[4] is not None} | {"_"}
+    names = sorted(names_used)
+    nrank = {x: k for k, x in enumerate(names)}
+    name = np.array([nrank[str(x)] if x is not None else nrank["_"] for x in nid], np.int32)
+    if extra:
+        xs = list(zip(*extra))
+        s = np.concatenate([s, np.array(xs[0], np.int64)])
+        d = np.concatenate([e - s[:n], np.array(xs[1], np.int64)])
+        c = np.concatenate([c, np.array(xs[2], np.uint8)])
+        tid = np.concatenate([tid, np.array(xs[3], np.int64)])
+        name = np.concatenate([name, np.array([nrank[str(x)] if x is not None else nrank["_"] for x in xs[4]],
+                                              np.int32)])
+        corr = np.concatenate([corr, np.array(xs[5], np.int64)])
+        has = np.concatenate([has, np.array(xs[6], np.uint8)])
+    else:
+        d = e - s
     from .model import ProcessMeta
-    ct = ColumnarTrace.from_arrays(0, s, e - s, np.ones(n, np.int64), tid, c, name, names,
+    m = s.shape[0]
+    ct = ColumnarTrace.from_arrays(0, s, d, np.ones(m, np.int64), tid, c, name, names, corr=corr, has_corr=has,
                                    processes=(ProcessMeta(1, "pid"),))
-    bd = compute_overlap_columnar(ct)
+    bd = compute_overlap_columnar(ct, Attribution.CORRELATION if pinned else Attribution.INSTANT)
     cells = {}
     for key, ns in bd.cells.items():
         pid_path = path_table.get_id(tuple(int(x) for x in key.path))
@@ -324,5 +391,4 @@ def sweep_pid(starts, ends, cats, ranks, fixed_paths, add_order, rem_order, rank
         cells[(pid_path << 6) | mask] = ns
     lo, hi = bd.spans[1]
     tracked = (hi - lo) - bd.untracked[1]
-    del cur
     return cells, tracked

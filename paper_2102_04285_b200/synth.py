@@ -420,11 +420,13 @@ def zipf_sizes(total: int, pids: int, s: float) -> list:
 
 
 def adversarial_trace(n_events: int = 10_000_000, pids: int = 64, seed: int = 1234, zipf: float = 1.5,
-                      depth: int = 64, streams: int = 256, workers: int = 0) -> ColumnarTrace:
+                      depth: int = 64, streams: int = 256, workers: int = 0, only=None) -> ColumnarTrace:
     """Config 5: ``n_events`` over ``pids`` processes with Zipf(``zipf``)
     sizes (s=1.5 puts ~42% of the events in the largest pid at 64 pids),
     recursive ops to ``depth``, ``streams`` concurrent GPU streams, 1%
-    zero-duration events, 10% duplicate correlation ids."""
+    zero-duration events, 10% duplicate correlation ids.  ``only``: pid
+    values (1-based) to generate -- exactly those processes of the full trace."""
     sizes = zipf_sizes(n_events, pids, zipf)
-    res = _map(_adv_pid, [(seed, p + 1, sizes[p], depth, streams) for p in range(pids)], workers)
+    keep = range(pids) if only is None else [p - 1 for p in only]
+    res = _map(_adv_pid, [(seed, p + 1, sizes[p], depth, streams) for p in keep], workers)
     return assemble([r[0] for r in res], adversarial_names(depth), [r[1] for r in res])

@@ -116,6 +116,8 @@ def test_sweep_pid_plugin_shim_matches_reference_kernel(k):
 
     case = SWEEP[k]
     pt = _PathTable()
+    for path in case.get("paths", []):  # CORRELATION calls: the ids fixed_paths refer to
+        pt.get_id(tuple(path))
     cells, tracked = sweep_pid(*case["args"], pt)
     got = sorted([list(pt.paths[key >> 6]), key & 63, v] for key, v in cells.items())
     assert got == case["cells"] and tracked == case["tracked"]

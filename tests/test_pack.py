@@ -99,3 +99,40 @@ def test_exception_table_sorted_and_adjacent():
     assert o["exc_col"] == o["exc_val"] + (lay.nbytes["exc_val"] + 15) // 16 * 16
     rows = raw[o["exc_row"]:o["exc_row"] + lay.nbytes["exc_row"]].view(np.int64)
     assert np.all(np.diff(rows) >= 0)
+
+
+def _native_equal(ct, threads):
+    from paper_2102_04285_b200.columnar import pack_native
+    ref = pack_block(ct)
+    got = pack_native(ct, n_threads=threads)
+    if ref is None:
+        assert got is None
+        return
+    (l1, r1), (l2, r2) = ref, got
+    assert l1.offsets == l2.offsets and l1.nbytes == l2.nbytes and l1.widths == l2.widths
+    assert l1.total == l2.total and l1.n_exc == l2.n_exc
+    assert np.array_equal(r1, r2)
+
+
+def test_native_pack_matches_numpy_builder():
+    """xs_pack_plan / xs_pack_fill (host threads) write the same bytes as the
+    numpy builder, for every thread count (the row partition and the
+    per-thread exception slots must not change the block)."""
+    import os
+
+    from paper_2102_04285_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        import pytest
+        pytest.skip("library not built")
+    for name, base, cols in _variants():
+        ct = _replace(base, cols) if cols else base
+        for threads in (1, 3, 8):
+            _native_equal(ct, threads)
+    for m in (0, 1, 255, 256, 257, 70_000):
+        sub = ColumnarTrace.from_arrays(0, np.arange(m) * 7, np.ones(m), np.ones(m), np.ones(m),
+                                        np.zeros(m, np.uint8), np.zeros(m), ["a"])
+        _native_equal(sub, 4)
+    import dataclasses
+    ct = synth.ddpg_trace(20)
+    _native_equal(dataclasses.replace(ct, cat=np.where(np.arange(ct.n) == 3, 200, ct.cat).astype(np.uint8),
+                                      _source=None), 2)
