@@ -233,10 +233,9 @@ static int bucket_sort_pairs_impl(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_
   XS_LAUNCH(ctx, k_bucket_chunks, grid_for(32 * n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, chunk);
   XS_LAUNCH(ctx, k_bs_scatter, grid_for(n), XS_BLOCK, 0, s, *keys, *vals, n, key_bits, g.shift, counts, offs,
             g.nbuckets, tail, *keys_alt, *vals_alt);
-  static bool attr_set = false;
-  if (!attr_set) {
+  if (!(ctx->attr_done & 2u)) {  // (per context: a context is bound to one device)
     XS_CUDA(cudaFuncSetAttribute(k_bs_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BsSmem)));
-    attr_set = true;
+    ctx->attr_done |= 2u;
   }
   // chunks sort from the alt buffers back into the primary ones; the sentinel
   // tail is copied over unchanged

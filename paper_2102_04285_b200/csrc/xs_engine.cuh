@@ -191,7 +191,8 @@ struct xs_ctx {
   // last transitions
   long long n_trans_out = 0;
   int trie_cap_log2 = 12;
-  long long deep_cap = 0;  // ints of global scratch per thread for merged op stacks deeper than MAXD
+  long long deep_cap = 0;
+  unsigned attr_done = 0;  // kernels whose >48 KB dynamic shared memory attribute is set on this ctx's device  // ints of global scratch per thread for merged op stacks deeper than MAXD
   bool force_lsd = false;  // bucketed sort overflowed on this input: use the LSD path
   xs::OpsState ops;
   // optional per-stage device timing (CUDA events on the launching stream)

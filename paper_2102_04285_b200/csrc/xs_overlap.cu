@@ -897,13 +897,12 @@ static int bucket_sweep(xs_ctx* ctx, const EventView& v, const BkPlan& plan, int
   XS_CUDA(cudaMemsetAsync(flags, 0, (n_chunks + 1) * sizeof(int), s));
   XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
   ProfScope ps(ctx, ST_SWEEP, s);
-  static bool attr_set = false;
-  if (!attr_set) {
+  if (!(ctx->attr_done & 1u)) {  // (per context: a context is bound to one device)
     XS_CUDA(cudaFuncSetAttribute(k_bk_sweep<HT_SMALL, XS_SWEEP_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(BkSmemT<HT_SMALL>)));
     XS_CUDA(cudaFuncSetAttribute(k_bk_sweep<HT_BIG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(BkSmemT<HT_BIG>)));
-    attr_set = true;
+    ctx->attr_done |= 1u;
   }
   // direct-indexed block table when every chunk holds one pid (the path-count
   // condition is checked in the kernel); the big hashed table for traces whose

@@ -254,7 +254,12 @@ def _ddpg_pid(args):
 def _map(fn, jobs, workers: int):
     if workers and workers > 1 and len(jobs) > 1:
         import multiprocessing as mp
-        with mp.get_context("fork").Pool(min(workers, len(jobs))) as pool:
+        import sys
+        # fork is cheapest, but forking a process that already holds a CUDA
+        # context (and its helper threads) can abort the child: spawn then
+        torch = sys.modules.get("torch")
+        cuda_up = torch is not None and torch.cuda.is_initialized()
+        with mp.get_context("spawn" if cuda_up else "fork").Pool(min(workers, len(jobs))) as pool:
             return pool.map(fn, jobs, chunksize=1)
     return [fn(j) for j in jobs]
 

@@ -25,9 +25,6 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "oracle", "_ref")
 
-_G: dict = {}
-
-
 def have_reference() -> bool:
     return os.path.isdir(os.path.join(REF, "xstrace"))
 
@@ -55,38 +52,56 @@ def cells_by_pid(bd) -> dict:
     return out
 
 
-def _oracle_worker(pids):
+def _oracle_worker(job):
+    """One pid batch vs the C oracle (runs in a spawned process: everything
+    it needs arrives in ``job``)."""
     import oracle
     from paper_2102_04285_b200 import ColumnarTrace
-    g = _G
-    ct, prof, bounds = g["ct"], g["profile"], g["bounds"]
-    sub, rows = sub_trace(ct, pids, bounds)
+    sub, prof, rows, pids = job["sub"], job["profile"], job["rows"], job["pids"]
     errs = []
     if prof is not None:
         s, d, rep, _ = oracle.correct(sub, prof)
-        if not (np.array_equal(g["start"][rows], s) and np.array_equal(g["dur"][rows], d)):
-            bad = np.flatnonzero((g["start"][rows] != s) | (g["dur"][rows] != d))
+        if not (np.array_equal(job["start"], s) and np.array_equal(job["dur"], d)):
+            bad = np.flatnonzero((job["start"] != s) | (job["dur"] != d))
             errs.append(f"pids {pids}: corrected columns differ at {len(bad)} rows, first row {rows[bad[0]]}")
         for pv, hooks in rep["removed_ns"].items():
-            if g["removed"].get(pv) != hooks:
-                errs.append(f"pid {pv}: removed_ns {g['removed'].get(pv)} != oracle {hooks}")
+            if job["removed"].get(pv) != hooks:
+                errs.append(f"pid {pv}: removed_ns {job['removed'].get(pv)} != oracle {hooks}")
         for pv, hooks in rep["shortfall_ns"].items():
-            if g["shortfall"].get(pv) != hooks:
-                errs.append(f"pid {pv}: shortfall_ns {g['shortfall'].get(pv)} != oracle {hooks}")
+            if job["shortfall"].get(pv) != hooks:
+                errs.append(f"pid {pv}: shortfall_ns {job['shortfall'].get(pv)} != oracle {hooks}")
         sub = ColumnarTrace(sub.clock_domain, s, d, sub.pid, sub.tid, sub.cat, sub.name, sub.corr, sub.has_corr,
                             sub.pids, sub.group_pid, sub.group_tid, sub.names, sub.processes, sub.pid_has_meta)
-    cells, spans, untracked = oracle.overlap(sub, g["attribution"])
+    cells, spans, untracked = oracle.overlap(sub, job["attribution"])
     per: dict = {}
     for (pv, path, cats), ns in cells.items():
         per.setdefault(pv, {})[(path, cats)] = ns
-    for p in pids:
-        pv = int(ct.pids[p])
-        if per.get(pv, {}) != g["cells"].get(pv, {}):
-            errs.append(f"pid {pv}: {len(g['cells'].get(pv, {}))} cells vs oracle {len(per.get(pv, {}))}, differ")
-        if spans.get(pv) != g["spans"].get(pv) or untracked.get(pv) != g["untracked"].get(pv):
-            errs.append(f"pid {pv}: span/untracked {g['spans'].get(pv)}/{g['untracked'].get(pv)} vs oracle "
+    for pv in pids:
+        if per.get(pv, {}) != job["cells"].get(pv, {}):
+            errs.append(f"pid {pv}: {len(job['cells'].get(pv, {}))} cells vs oracle {len(per.get(pv, {}))}, differ")
+        if spans.get(pv) != job["spans"].get(pv) or untracked.get(pv) != job["untracked"].get(pv):
+            errs.append(f"pid {pv}: span/untracked {job['spans'].get(pv)}/{job['untracked'].get(pv)} vs oracle "
                         f"{spans.get(pv)}/{untracked.get(pv)}")
     return errs
+
+
+def _job(ct, bounds, pid_idx, bd_cells, bd, profile, start, dur, report, attribution):
+    sub, rows = sub_trace(ct, pid_idx, bounds)
+    pvs = [int(ct.pids[p]) for p in pid_idx]
+    job = {"sub": sub, "rows": rows, "pids": pvs, "profile": profile, "attribution": attribution,
+           "cells": {pv: bd_cells.get(pv, {}) for pv in pvs},
+           "spans": {pv: bd.spans.get(pv) for pv in pvs}, "untracked": {pv: bd.untracked.get(pv) for pv in pvs}}
+    if profile is not None:
+        job.update(start=np.asarray(start)[rows], dur=np.asarray(dur)[rows],
+                   removed={pv: report.removed_ns.get(pv) for pv in pvs},
+                   shortfall={pv: report.shortfall_ns.get(pv) for pv in pvs})
+    return job
+
+
+def _pool(n):
+    # spawned workers: forking a process that holds a CUDA context and
+    # helper threads can deadlock or abort the child
+    return mp.get_context("spawn").Pool(max(1, n))
 
 
 def _batches(ct, bounds, max_events: int) -> list:
@@ -109,62 +124,53 @@ def oracle_check(ct, bd, profile=None, start=None, dur=None, report=None, attrib
                  workers: int = 0, max_events: int = 2_000_000) -> list:
     """Every pid of the device result vs the C oracle; returns mismatches."""
     bounds = pid_bounds(ct)
-    _G.clear()
-    _G.update(ct=ct, profile=profile, bounds=bounds, attribution=attribution, cells=cells_by_pid(bd),
-              spans=dict(bd.spans), untracked=dict(bd.untracked))
-    if profile is not None:
-        _G.update(start=np.asarray(start), dur=np.asarray(dur), removed=report.removed_ns,
-                  shortfall=report.shortfall_ns)
-    jobs = _batches(ct, bounds, max_events)
+    cells = cells_by_pid(bd)
+    jobs = [_job(ct, bounds, j, cells, bd, profile, start, dur, report, attribution)
+            for j in _batches(ct, bounds, max_events)]
     workers = workers or min(len(jobs), os.cpu_count() or 1)
-    try:
-        if workers <= 1:
-            res = [_oracle_worker(j) for j in jobs]
-        else:
-            with mp.get_context("fork").Pool(workers) as pool:
-                res = pool.map(_oracle_worker, jobs, chunksize=1)
-    finally:
-        _G.clear()
+    if workers <= 1:
+        res = [_oracle_worker(j) for j in jobs]
+    else:
+        with _pool(min(workers, len(jobs))) as pool:
+            res = pool.map(_oracle_worker, jobs, chunksize=1)
     return [e for r in res for e in r]
 
 
 # ---------------------------------------------------------------------------
-def _ref_worker(pid_idx):
+def _ref_worker(job):
     sys.path.insert(0, REF)
     from xstrace import model as RM
     from xstrace.calibration import CalibrationProfile as RP
     from xstrace.correction import correct_trace as ref_correct
     from xstrace.overlap import compute_overlap as ref_overlap
 
-    g = _G
-    ct, prof, bounds = g["ct"], g["profile"], g["bounds"]
-    sub, rows = sub_trace(ct, [pid_idx], bounds)
+    sub, prof = job["sub"], job["profile"]
+    (pv,) = job["pids"]
     cats = [RM.Category(c) for c in range(6)]
-    names = ct.names
-    events = [RM.Event(int(ct.pids[p]), int(ct.group_tid[t]), cats[c], names[nm], s, d, k if h else None)
+    names = sub.names
+    events = [RM.Event(int(sub.pids[p]), int(sub.group_tid[t]), cats[c], names[nm], s, d, k if h else None)
               for p, t, c, nm, s, d, k, h in zip(sub.pid.tolist(), sub.tid.tolist(), sub.cat.tolist(),
                                                  sub.name.tolist(), sub.start.tolist(), sub.dur.tolist(),
                                                  sub.corr.tolist(), sub.has_corr.tolist())]
-    pv = int(ct.pids[pid_idx])
-    metas = [RM.ProcessMeta(m.pid, m.name, m.parent, m.fork_ns, m.join_ns) for m in ct.processes]
-    trace = RM.Trace(ct.clock_domain, events, metas)
+    metas = [RM.ProcessMeta(m.pid, m.name, m.parent, m.fork_ns, m.join_ns) for m in sub.processes]
+    trace = RM.Trace(sub.clock_domain, events, metas)
     errs = []
     if prof is not None:
         rp = RP(prof.annotation_ns, prof.transition_ns, prof.api_interception_ns, dict(prof.api_internal_ns))
         out, rep = ref_correct(trace, rp)
         rs = np.fromiter((e.start for e in out.events), np.int64, len(out.events))
         rd = np.fromiter((e.duration for e in out.events), np.int64, len(out.events))
-        if not (np.array_equal(rs, g["start"][rows]) and np.array_equal(rd, g["dur"][rows])):
+        if not (np.array_equal(rs, job["start"]) and np.array_equal(rd, job["dur"])):
             errs.append(f"pid {pv}: corrected columns differ from the reference")
-        if dict(rep.removed_ns.get(pv, {})) != g["removed"].get(pv) or \
-                dict(rep.shortfall_ns.get(pv, {})) != g["shortfall"].get(pv):
+        if dict(rep.removed_ns.get(pv, {})) != job["removed"].get(pv) or \
+                dict(rep.shortfall_ns.get(pv, {})) != job["shortfall"].get(pv):
             errs.append(f"pid {pv}: report rows differ from the reference")
         trace = out
     bd = ref_overlap(trace)
     cells = {(tuple(k.path), frozenset(int(c) for c in k.categories)): v for k, v in bd.cells.items()}
-    if cells != g["cells"].get(pv, {}):
-        errs.append(f"pid {pv}: cells differ from the reference ({len(cells)} vs {len(g['cells'].get(pv, {}))})")
-    if bd.spans.get(pv) != g["spans"].get(pv) or bd.untracked.get(pv) != g["untracked"].get(pv):
+    if cells != job["cells"].get(pv, {}):
+        errs.append(f"pid {pv}: cells differ from the reference ({len(cells)} vs {len(job['cells'].get(pv, {}))})")
+    if bd.spans.get(pv) != job["spans"].get(pv) or bd.untracked.get(pv) != job["untracked"].get(pv):
         errs.append(f"pid {pv}: span/untracked differ from the reference")
     return errs, len(events)
 
@@ -173,15 +179,8 @@ def reference_check(ct, bd, pid_indices, profile=None, start=None, dur=None, rep
     """Sampled pids of the device result vs the unmodified reference;
     returns (mismatches, events checked)."""
     bounds = pid_bounds(ct)
-    _G.clear()
-    _G.update(ct=ct, profile=profile, bounds=bounds, cells=cells_by_pid(bd), spans=dict(bd.spans),
-              untracked=dict(bd.untracked))
-    if profile is not None:
-        _G.update(start=np.asarray(start), dur=np.asarray(dur), removed=report.removed_ns,
-                  shortfall=report.shortfall_ns)
-    try:
-        with mp.get_context("fork").Pool(max(1, min(len(pid_indices), os.cpu_count() or 1))) as pool:
-            res = pool.map(_ref_worker, list(pid_indices), chunksize=1)
-    finally:
-        _G.clear()
+    cells = cells_by_pid(bd)
+    jobs = [_job(ct, bounds, [p], cells, bd, profile, start, dur, report, 0) for p in pid_indices]
+    with _pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+        res = pool.map(_ref_worker, jobs, chunksize=1)
     return [e for r, _ in res for e in r], sum(n for _, n in res)
