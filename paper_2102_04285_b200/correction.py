@@ -133,7 +133,9 @@ def _batched(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: O
     rep = CorrectionReport()
     procs = {}
     parts, errs = [], []
-    for pids in _split.plan_batches(ct):
+    todo = list(reversed(_split.plan_batches(ct)))
+    while todo:
+        pids = todo.pop()
         sub, rows = _split.sub_trace(ct, pids, rows_by_pid)
         scaled = profile.scaled(sub.names)
         try:
@@ -144,6 +146,10 @@ def _batched(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: O
         except _engine.XsError as exc:
             if exc.status == _lib.XS_INVALID_TRACE:
                 errs.append(_BatchError("invalid", int(rows[0])))
+                continue
+            if exc.status == _lib.XS_UNSUPPORTED and len(pids) > 1:  # (CORRELATION keys also hold path bits)
+                h = len(pids) // 2
+                todo += [pids[h:], pids[:h]]
                 continue
             raise
         if attribution is not None:
@@ -177,7 +183,14 @@ def correct_trace_columnar(ct: ColumnarTrace, profile: CalibrationProfile, devic
         out = ColumnarTrace(ct.clock_domain, start, dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr,
                             ct.pids, ct.group_pid, ct.group_tid, ct.names, procs, ct.pid_has_meta)
         return out, rep
-    eng, dt, raw = _run(ct, profile, _src if _src is not None else ct, None, device_trace)
+    try:
+        eng, dt, raw = _run(ct, profile, _src if _src is not None else ct, None, device_trace)
+    except _engine.XsError as exc:
+        if exc.status != _lib.XS_UNSUPPORTED or device_trace is not None or ct.n_pids < 2:
+            raise
+        start, dur, rep, procs, _ = _batched(ct, profile, _src if _src is not None else ct, None)
+        return ColumnarTrace(ct.clock_domain, start, dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr,
+                             ct.pids, ct.group_pid, ct.group_tid, ct.names, procs, ct.pid_has_meta), rep
     procs = _remap_processes(eng, ct)
     start = raw.start.cpu().numpy()
     dur = raw.dur.cpu().numpy()
@@ -214,7 +227,7 @@ def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution
     from .overlap import Attribution, decode_breakdown
 
     attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
-    if device_trace is None and _split.needs_split(ct):
+    def batched():
         start, dur, rep, _, bd = _batched(ct, profile, ct, attr)
         if out is not None:
             np.asarray(out[0])[...] = start
@@ -223,7 +236,15 @@ def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution
         import torch
         dev = torch.device("cuda", _engine.get().device)
         return torch.from_numpy(start).to(dev), torch.from_numpy(dur).to(dev), rep, bd
-    eng, dt, raw = _run(ct, profile, ct, attr, device_trace, host_out=out)
+
+    if device_trace is None and _split.needs_split(ct):
+        return batched()
+    try:
+        eng, dt, raw = _run(ct, profile, ct, attr, device_trace, host_out=out)
+    except _engine.XsError as exc:
+        if exc.status != _lib.XS_UNSUPPORTED or device_trace is not None or ct.n_pids < 2:
+            raise
+        return batched()  # keys too wide for all pids at once (CORRELATION keys also hold path bits)
     bd = decode_breakdown(ct, eng.fetch_overlap())
     if out is not None:
         return out[0], out[1], _report(ct, raw), bd

@@ -16,9 +16,11 @@ namespace xs {
 constexpr int64_t kNegInf = INT64_MIN / 4;  // -inf for (max,+) scans; survives + of any real ns
 
 __host__ __device__ inline int bits_for(uint64_t v) {  // bits needed to hold values 0..v
-  int b = 0;
-  while (b < 64 && (v >> b) != 0) b++;
-  return b;
+#ifdef __CUDA_ARCH__
+  return 64 - __clzll((long long)v);
+#else
+  return v ? 64 - __builtin_clzll(v) : 0;
+#endif
 }
 
 __device__ __forceinline__ int64_t ld_cg(const int64_t* p) { return __ldcg(reinterpret_cast<const long long*>(p)); }

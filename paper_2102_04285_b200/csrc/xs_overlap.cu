@@ -512,6 +512,7 @@ struct BkSmemT {
   unsigned h_lo[kHT];
   unsigned h_hi[kHT];
   uint32_t last[BK_THREADS];
+  uint32_t head[BK_CAP / 32];  // bit i of word w: key 32w+i starts a bucket run (first key of its bucket)
   SwState warp_agg[BK_THREADS / 32];
   SwState tile_pre;
   int big;
@@ -595,20 +596,28 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
     if (t == 0) atomicAdd((unsigned long long*)&st->pad[3], 1ull);
     cnt = 0;
   }
-  // 1. load (striped, coalesced) + order-independent aggregate
+  // 1. load (striped, coalesced) + order-independent aggregate; lane i of
+  // warp w holds key j*BK_THREADS + 32w + i, so one ballot per item gives a
+  // word of the run-head bitmap (a key whose bucket differs from its left
+  // neighbour's starts a run; neighbours across words come from a shuffle)
   SwState agg = sw_identity();
   uint32_t kmax = 0;
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
+    uint32_t kr = 0;
     if (idx < cnt) {
       const uint64_t k = keys[s0 + idx];
-      const uint32_t kr = (uint32_t)(k - base);
+      kr = (uint32_t)(k - base);
       S.k[idx] = kr;
       sw_apply(agg, kr & 15u);
       kmax = kr > kmax ? kr : kmax;
       agg.has = 1;
     }
+    const uint32_t left = __shfl_up_sync(0xffffffffu, kr, 1);
+    bool hd = idx < cnt && (lane == 0 || (left >> shift) != (kr >> shift));
+    const unsigned bits = __ballot_sync(0xffffffffu, hd);
+    if (lane == 0) S.head[idx >> 5] = bits;  // (bit 0 is provisional: fixed below against the previous word)
   }
   agg.last = base + kmax;
   SwMaxOp mop;
@@ -631,29 +640,44 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
     if (lane == 0) tile_publish_agg((int)c, tile_agg, desc, flags);
   }
   XS_STAMP(2);
-  // 2. rank inside buckets (a bucket is the run of equal k >> shift in k[])
+  // 2. rank inside buckets (a bucket is the run of equal k >> shift in k[]):
+  // run bounds from the head bitmap (clz / ffs on one or two words), then one
+  // compare per run member -- O(run length), no per-step bucket test
+  __syncthreads();
+  for (int w = t; w < (cnt + 31) >> 5; w += BK_THREADS)  // bit 0: against the last key of the previous word
+    if (w > 0 && (S.k[32 * w] >> shift) == (S.k[32 * w - 1] >> shift)) atomicAnd(&S.head[w], ~1u);
+  if (t == 0 && cnt > 0) atomicOr(&S.head[0], 1u);
+  __syncthreads();
   bool big = false;
 #pragma unroll 2
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
     if (idx >= cnt) break;
     const uint32_t k = S.k[idx];
-    const uint32_t bk = k >> shift;
-    const bool left = idx > 0 && (S.k[idx - 1] >> shift) == bk;
-    const bool right = idx + 1 < cnt && (S.k[idx + 1] >> shift) == bk;
-    if (!left && !right) {
+    // run start: last head <= idx
+    int w = idx >> 5;
+    unsigned m = S.head[w] & (0xffffffffu >> (31 - (idx & 31)));
+    while (!m) m = S.head[--w];
+    const int rs = 32 * w + 31 - __clz(m);
+    // run end: first head > idx (or cnt)
+    w = idx >> 5;
+    m = (idx & 31) == 31 ? 0u : S.head[w] & (0xfffffffeu << (idx & 31));
+    while (!m && 32 * (w + 1) < cnt) m = S.head[++w];
+    const int re = m ? min(32 * w + __ffs(m) - 1, cnt) : cnt;
+    if (re - rs == 1) {
       S.sorted[idx] = k;
       continue;
     }
-    int r = 0, q = idx - 1, steps = 0;
-    for (; q >= 0 && steps < BK_RANK_MAX && (S.k[q] >> shift) == bk; q--, steps++) r += S.k[q] <= k;
-    big |= steps == BK_RANK_MAX && q >= 0 && (S.k[q] >> shift) == bk;
-    const int start = q + 1;
-    int q2 = idx + 1;
-    steps = 0;
-    for (; q2 < cnt && steps < BK_RANK_MAX && (S.k[q2] >> shift) == bk; q2++, steps++) r += S.k[q2] < k;
-    big |= steps == BK_RANK_MAX && q2 < cnt && (S.k[q2] >> shift) == bk;
-    S.sorted[start + r] = k;
+    if (re - rs > 2 * BK_RANK_MAX) {
+      big = true;
+      continue;
+    }
+    int r = 0;
+    for (int q = rs; q < re; q++) {
+      const uint32_t o = S.k[q];
+      r += (o < k) | ((o == k) & (q < idx));
+    }
+    S.sorted[rs + r] = k;
   }
   if (big) S.big = 1;
   __syncthreads();
@@ -814,7 +838,11 @@ static int bucket_prepare(xs_ctx* ctx, const EventView& v, const int64_t* lo, in
                           const uint64_t* extra, int64_t n_extra, int64_t nvalid, int key_bits, cudaStream_t s,
                           BkPlan* plan) {
   const int64_t n = v.ev.n;
-  const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(nvalid, key_bits, 26));
+  static const int max_bits = [] {
+    const char* e = getenv("XS_BK_MAX_BITS");  // (tuning experiments)
+    return e ? atoi(e) : 26;
+  }();
+  const BucketGeom g = bucket_geom(key_bits, bucket_bits_for(nvalid, key_bits, max_bits));
   unsigned* counts;
   int64_t *offs, *chunk;
   uint64_t* keys;

@@ -7,11 +7,12 @@ per-rank results:
 
 * path ids are internal to each rank's trie, so ranks first agree on a global
   path table (an all-gather of the name tuples their cells use -- a few KB);
-* every rank scatters its cells into a dense int64 histogram
-  [pid][global path][32 masks] (+ tracked in mask 0 of path 0) and one
-  ``all_reduce(SUM)`` over NCCL merges them; integer sums are order
-  independent, so the merge is bit-exact;
-* spans merge with MIN/MAX all-reduces.
+* every rank turns its nonzero cells into exact int64 keys (pid, global
+  path, mask) with their ns; one variable-length all-gather over NCCL
+  exchanges them (bounded by the nonzero cells, not by pids x paths x 32)
+  and every rank sums them by key -- integer sums are order independent, so
+  the merge is bit-exact;
+* spans and tracked time travel the same way, merged by MIN / MAX / SUM.
 
 The same code runs on ``gloo`` (CPU tensors) for the world-size-2 tests.
 """
@@ -54,30 +55,50 @@ def local_cells(ct: ColumnarTrace, raw) -> tuple:
 _TABLES = {"paths": (), "pids": ()}  # global path / pid tables agreed by earlier merges (identical on all ranks)
 
 
-def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
-    """Merge every rank's overlap result into one Breakdown (all ranks get it).
-
-    Path ids are per-rank trie nodes, so ranks agree on a global table of path
-    tuples (and pid values).  The table is cached across calls: once every
-    rank's paths are in it (one MIN all-reduce of a flag says so) a merge is
-    two tensor collectives -- SUM of the dense histogram + tracked, MIN of
-    (lo, -hi) -- and no object all-gather.  Integer sums commute, so the
-    merge is bit-exact."""
+def _gather_var(x, device, world):
+    """all_gather of a variable-length 1-D int64 tensor: sizes first, then
+    the padded payloads; returns the concatenation in rank order."""
     import torch
     import torch.distributed as dist
 
-    rows, per_pid = local_cells(ct, raw)
+    n = torch.tensor([x.numel()], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    sizes = [int(t.item()) for t in sizes]
+    m = max(max(sizes), 1)
+    buf = torch.zeros(m, dtype=torch.int64, device=device)
+    buf[: x.numel()] = x
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf)
+    return torch.cat([o[:k] for o, k in zip(out, sizes)])
+
+
+def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
+    """Merge every rank's overlap result into one Breakdown (all ranks get it).
+
+    Path ids are per-rank trie nodes, so ranks first agree on a global table
+    of the path tuples their cells use (an object all-gather of a few KB,
+    cached: later merges skip it once one MIN all-reduce says every rank's
+    paths are known).  Each nonzero cell then becomes one exact int64 key
+    (pid value, global path, mask) with its ns; the keys and values of all
+    ranks are all-gathered (variable length: the exchange is bounded by the
+    nonzero cells, not by pids x paths x 32) and summed by key -- integer sums
+    commute, so the merge is bit-exact and identical on every rank.  Per-pid
+    spans and tracked time travel the same way (MIN / MAX / SUM by pid)."""
+    import torch
+    import torch.distributed as dist
+
     world = dist.get_world_size() if dist.is_initialized() else 1
-    my_paths = {r[1] for r in rows} | {()}
-    my_pids = set(per_pid)
+    paths = decode_paths(ct, raw.node_parent, raw.node_name)
+    node_ids = np.unique(raw.cell_node) if raw.cell_node.size else np.zeros(0, np.int32)
+    my_paths = {paths[i] for i in node_ids.tolist()} | {()}
+    my_pids = set(ct.pids[np.nonzero(raw.has_events)[0]].tolist())
     known = my_paths <= set(_TABLES["paths"]) and my_pids <= set(_TABLES["pids"])
     if world > 1:
         flag = torch.tensor([1 if known else 0], dtype=torch.int64, device=device)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         known = bool(flag.item())
-    if not known:  # grow the tables (first merge, or new paths): tiny object all-gather
-        if len(_TABLES["paths"]) * max(len(_TABLES["pids"]), 1) > (1 << 20):  # bound the dense merge buffer
-            _TABLES["paths"], _TABLES["pids"] = (), ()
+    if not known:  # grow the table (first merge, or new paths): tiny object all-gather
         mine = (sorted(my_paths), sorted(my_pids))
         gathered = [None] * world
         if world > 1:
@@ -88,36 +109,38 @@ def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
         _TABLES["pids"] = tuple(sorted(set(_TABLES["pids"]) | {p for g in gathered for p in g[1]}))
     all_paths, all_pids = _TABLES["paths"], _TABLES["pids"]
     path_ix = {p: i for i, p in enumerate(all_paths)}
+    Q = len(all_paths)
+    node_to_q = np.zeros(max(len(paths), 1), np.int64)
+    for i in node_ids.tolist():
+        node_to_q[i] = path_ix[paths[i]]
     pid_ix = {p: i for i, p in enumerate(all_pids)}
-    P, Q = len(all_pids), len(all_paths)
-    # one SUM buffer: histogram [pid][path][32] then tracked[pid]; one MIN buffer: lo[pid] then -hi[pid]
-    sums = np.zeros(P * Q * 32 + P, np.int64)
-    mins = np.full(2 * max(P, 1), np.iinfo(np.int64).max, np.int64)
-    if rows:
-        idx = np.array([(pid_ix[r[0]] * Q + path_ix[r[1]]) * 32 + r[2] for r in rows], np.int64)
-        np.add.at(sums, idx, np.array([r[3] for r in rows], np.int64))
-    for pv, (a, b, t) in per_pid.items():
-        k = pid_ix[pv]
-        sums[P * Q * 32 + k] += t
-        mins[k] = a
-        mins[max(P, 1) + k] = -b
+    pv = np.array([pid_ix.get(int(p), 0) for p in ct.pids.tolist()], np.int64)  # global pid index
+    keys = (pv[raw.cell_pid] * Q + node_to_q[raw.cell_node]) * 32 + raw.cell_mask.astype(np.int64)
+    vals = raw.cell_ns.astype(np.int64)
+    has = np.nonzero(raw.has_events)[0]
+    pid_rows = np.stack([pv[has], raw.span_lo[has].astype(np.int64), raw.span_hi[has].astype(np.int64),
+                         raw.tracked[has].astype(np.int64)], axis=1).reshape(-1) if has.size else np.zeros(0, np.int64)
     if world > 1:
-        ts = torch.from_numpy(sums).to(device)
-        tm = torch.from_numpy(mins).to(device)
-        dist.all_reduce(ts, op=dist.ReduceOp.SUM)
-        dist.all_reduce(tm, op=dist.ReduceOp.MIN)
-        sums, mins = ts.cpu().numpy(), tm.cpu().numpy()
+        tk, tv, tp = (_gather_var(torch.from_numpy(np.ascontiguousarray(a)).to(device), device, world)
+                      for a in (keys, vals, pid_rows))
+        keys, vals, pid_rows = tk.cpu().numpy(), tv.cpu().numpy(), tp.cpu().numpy()
+    uk, inv = np.unique(keys, return_inverse=True)
+    sums = np.zeros(uk.shape[0], np.int64)
+    np.add.at(sums, inv, vals)
     bd = Breakdown()
-    h = sums[: P * Q * 32]
-    for i in np.nonzero(h)[0].tolist():
-        p, q = divmod(i >> 5, Q)
-        bd.cells[OverlapKey(all_pids[p], all_paths[q], _MASK_CATS[i & 31])] = int(h[i])
-    for k, pv in enumerate(all_pids):
-        lo, hi = int(mins[k]), -int(mins[max(P, 1) + k])
-        if lo == np.iinfo(np.int64).max:
-            continue  # (a pid in the table that no rank has events for)
-        bd.spans[pv] = (lo, hi)
-        bd.untracked[pv] = (hi - lo) - int(sums[P * Q * 32 + k])
+    for k, v in zip(uk.tolist(), sums.tolist()):
+        if v:
+            pid_q, m = divmod(k, 32)
+            p, q = divmod(pid_q, Q)
+            bd.cells[OverlapKey(all_pids[p], all_paths[q], _MASK_CATS[m])] = v
+    spans, tracked = {}, {}
+    for p, lo, hi, t in pid_rows.reshape(-1, 4).tolist():
+        a, b = spans.get(p, (lo, hi))
+        spans[p] = (min(a, lo), max(b, hi))
+        tracked[p] = tracked.get(p, 0) + t
+    for p in sorted(spans):
+        bd.spans[all_pids[p]] = spans[p]
+        bd.untracked[all_pids[p]] = (spans[p][1] - spans[p][0]) - tracked[p]
     return bd
 
 

@@ -226,6 +226,8 @@ def compute_overlap_columnar(ct: ColumnarTrace, attribution: Attribution = Attri
     except _engine.XsError as exc:
         if exc.status == _lib.XS_INVALID_TRACE:
             _raise_invalid(_source if _source is not None else ct, ct)
+        if exc.status == _lib.XS_UNSUPPORTED and device_trace is None and ct.n_pids > 1:
+            return _overlap_batched(ct, attribution, _source)  # keys too wide for all pids at once
         raise
     return decode_breakdown(ct, raw)
 
@@ -248,13 +250,19 @@ def _overlap_batched(ct: ColumnarTrace, attribution, _source) -> Breakdown:
     attr = 1 if Attribution(attribution) is Attribution.CORRELATION else 0
     rows_by_pid = _split.pid_rows(ct)
     parts = []
-    for pids in _split.plan_batches(ct):
+    todo = list(reversed(_split.plan_batches(ct)))
+    while todo:
+        pids = todo.pop()
         sub, _ = _split.sub_trace(ct, pids, rows_by_pid)
         try:
             raw = eng.overlap(_engine.DeviceTrace(sub, eng.device), attr)
         except _engine.XsError as exc:
             if exc.status == _lib.XS_INVALID_TRACE:
                 _raise_invalid(_source if _source is not None else ct, ct)
+            if exc.status == _lib.XS_UNSUPPORTED and len(pids) > 1:  # (CORRELATION keys also hold path bits)
+                h = len(pids) // 2
+                todo += [pids[h:], pids[:h]]
+                continue
             raise
         parts.append(decode_breakdown(sub, raw, lazy=False))
     return merge_breakdowns(parts)

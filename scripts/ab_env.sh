@@ -1,7 +1,6 @@
 #!/bin/bash
-# A/B timing of the analyse step under environment variants (GPU box).
-# usage: scripts/ab_env.sh "VAR=a" "VAR=b" ...
+# A/B of env knobs on the per-stage device times: ab_env.sh "ENV=a ENV2=b" "ENV=c" ...
 for v in "$@"; do
   echo "== $v"
-  env $v python scripts/step_timeline.py 2>/dev/null | grep analyze
+  env $v python scripts/stage_times.py 2>&1 | tail -2
 done

@@ -14,14 +14,25 @@ cfg = int(os.environ.get("XS_CONFIG", "2"))
 if cfg == 3:
     ev = int(os.environ.get("XS_EVENTS", "30000000"))
     ct = synth.config3_trace(processes=ev // 1_000_000, events_per_pid=1_000_000, workers=os.cpu_count())
+elif cfg == 5:
+    ct = synth.adversarial_trace(int(os.environ.get("XS_EVENTS", "10000000")), pids=64, workers=os.cpu_count())
 else:
     ct = synth.ddpg_trace(27027)
 eng = _engine.get(0)
 dt = _engine.DeviceTrace(ct, 0)
-sc = synth.exact_profile().scaled(ct.names)
+sc = (synth.adversarial_profile() if cfg == 5 else synth.exact_profile()).scaled(ct.names)
 for _ in range(3):
     eng.correct(dt, sc, analyze_attribution=0)
 torch.cuda.synchronize()
+tt = []
+for _ in range(5):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    eng.correct(dt, sc, analyze_attribution=0)
+    e1.record()
+    e1.synchronize()
+    tt.append(e0.elapsed_time(e1))
+print("step ms", " ".join(f"{t:.3f}" for t in tt), "events", ct.n)
 eng.lib.xs_profile_enable(eng.ctx, 1)
 K = 5
 for _ in range(K):
