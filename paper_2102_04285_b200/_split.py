@@ -48,20 +48,11 @@ def pid_spans_host(ct: ColumnarTrace):
 
 
 def needs_split(ct: ColumnarTrace) -> bool:
-    """A cheap pre-check: too many rows, or pid bits + span bits + code bits
-    over 64 (only computed when the span could be that wide)."""
-    if ct.n > MAX_EVENTS_PER_CALL:
-        return True
-    if ct.n == 0:
-        return False
-    pb = max(_bits(max(ct.n_pids - 1, 0)), _bits(max(ct.n_groups - 1, 0)))
-    tmax = int(ct.start.max()) + int(ct.dur.max()) - int(ct.start.min())
-    if pb + _bits(max(tmax, 0)) + CODE_BITS <= 64:
-        return False
-    lo, hi = pid_spans_host(ct)
-    has = lo <= hi
-    span = int((hi[has] - lo[has]).max()) if has.any() else 0
-    return pb + _bits(span) + CODE_BITS > 64
+    """More rows than one call takes (O(1)).  Keys too wide for all pids at
+    once are found by the device itself (XS_UNSUPPORTED after pass 1): the
+    callers then fall back to plan_batches -- no host pass over the columns
+    on the common path."""
+    return ct.n > MAX_EVENTS_PER_CALL
 
 
 def plan_batches(ct: ColumnarTrace, max_events: int = 0) -> list:

@@ -221,15 +221,8 @@ static int bucket_sort_pairs_impl(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_
   XS_CUDA(cudaMemsetAsync(counts, 0, g.nbuckets * 4, s));
   XS_CUDA(cudaMemsetAsync(tail, 0, 8, s));
   XS_LAUNCH(ctx, k_bs_hist, grid_for(n), XS_BLOCK, 0, s, *keys, n, key_bits, g.shift, counts);
-  {
-    size_t temp = 0;
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, counts, offs, (int)g.nbuckets, s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, counts, offs, (int)g.nbuckets, s));
-    ctx->launches += 2;
-  }
-  XS_LAUNCH(ctx, k_bk_total, 1, 32, 0, s, offs, counts, (int64_t)g.nbuckets);
+  // bucket offsets + offs[nb] = total, one pass
+  XS_TRY(scan_exclusive<int64_t>(ctx, ArrayIn<unsigned>{counts}, offs, g.nbuckets, s, offs + g.nbuckets));
   XS_LAUNCH(ctx, k_bucket_chunks, grid_for(32 * n_chunks), XS_BLOCK, 0, s, offs, g.nbuckets, n_chunks, chunk);
   XS_LAUNCH(ctx, k_bs_scatter, grid_for(n), XS_BLOCK, 0, s, *keys, *vals, n, key_bits, g.shift, counts, offs,
             g.nbuckets, tail, *keys_alt, *vals_alt);

@@ -15,6 +15,7 @@
 // through the LSD path (never silently wrong).
 #pragma once
 #include "xs_engine.cuh"
+#include "xs_prims.cuh"
 
 namespace xs {
 

@@ -19,6 +19,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "xs_engine.cuh"
+#include "xs_prims.cuh"
 
 namespace xs {
 
@@ -687,12 +688,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
   ProfScope ps_sites(ctx, ST_SITE_SORT, s);
   if (n) {
     XS_LAUNCH(ctx, k_site_count, grid_for(n), XS_BLOCK, 0, s, v, n, tflag, cnt);
-    size_t temp = 0;
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, cnt, pos, (int)n, s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, cnt, pos, (int)n, s));
-    ctx->launches += 2;
+    XS_TRY(scan_exclusive<int>(ctx, ArrayIn<int>{cnt}, pos, n, s));
     XS_LAUNCH(ctx, k_site_total, 1, 32, 0, s, pos, cnt, n, d_ns);
   }
   int64_t *slab_a, *slab_b, *slab_pre;

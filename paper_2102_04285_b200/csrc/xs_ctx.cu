@@ -18,6 +18,9 @@ int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
       case W_BS_OFFS: slot = W_BS_OFFS_B; break;
       case W_BS_TAIL: slot = W_BS_TAIL_B; break;
       case W_BS_CHUNK: slot = W_BS_CHUNK_B; break;
+      case W_PSCAN_DESC: slot = W_PSCAN_DESC_B; break;
+      case W_PSCAN_FLAGS: slot = W_PSCAN_FLAGS_B; break;
+      case W_PSCAN_CTR: slot = W_PSCAN_CTR_B; break;
       default: break;
     }
   }
@@ -53,8 +56,63 @@ int fetch_stats(xs_ctx* ctx, cudaStream_t s) {
   return XS_OK;
 }
 
+// One CTA sorts up to SMALL_SORT_MAX (key, value) pairs in shared memory:
+// a bitonic network on (key, input position), so the result is STABLE like
+// the radix sorts it stands in for (some callers rely on input order among
+// equal keys).  Sentinel keys (>= 2^bits) are larger than every real key.
+constexpr int SMALL_SORT_MAX = 8192;
+
+__global__ void __launch_bounds__(1024) k_small_sort(uint64_t* keys, uint32_t* vals, int n, int P) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(raw);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + P);
+  uint16_t* sp = reinterpret_cast<uint16_t*>(sv + P);
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    sk[i] = i < n ? keys[i] : ~0ull;
+    sv[i] = i < n && vals ? vals[i] : 0u;
+    sp[i] = (uint16_t)i;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int x = i ^ j;
+        if (x > i) {
+          const uint64_t a = sk[i], b = sk[x];
+          const uint16_t pa = sp[i], pb = sp[x];
+          const bool gt = a > b || (a == b && pa > pb);
+          if (gt == ((i & k) == 0)) {
+            const uint32_t va = sv[i];
+            sk[i] = b, sk[x] = a;
+            sp[i] = pb, sp[x] = pa;
+            sv[i] = sv[x], sv[x] = va;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    keys[i] = sk[i];
+    if (vals) vals[i] = sv[i];
+  }
+}
+
+static int small_sort(xs_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t n, cudaStream_t s) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  const int smem = P * 14;
+  if (!(ctx->attr_done & 4u)) {  // (per context: a context is bound to one device)
+    XS_CUDA(cudaFuncSetAttribute(k_small_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SORT_MAX * 14));
+    ctx->attr_done |= 4u;
+  }
+  XS_LAUNCH(ctx, k_small_sort, 1, 1024, smem, s, keys, vals, (int)n, P);
+  return XS_OK;
+}
+
 int sort_pairs_u64_u32(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals, uint32_t** vals_alt,
                        int64_t n, int bits, cudaStream_t s) {
+  if (n > 1 && n <= SMALL_SORT_MAX && !getenv("XS_NO_SMALL_SORT")) return small_sort(ctx, *keys, *vals, n, s);
   if (n <= 1 || bits <= 0) return XS_OK;
   if (bits > 64) bits = 64;
   static const bool no_bsort = getenv("XS_NO_BSORT") != nullptr;  // (debug switch)
@@ -80,6 +138,13 @@ int sort_pairs_u64_u32(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32
 int sort_keys_u64(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, int64_t n, int bits, cudaStream_t s) {
   if (n <= 1 || bits <= 0) return XS_OK;
   if (bits > 64) bits = 64;
+  if (n <= SMALL_SORT_MAX) return small_sort(ctx, *keys, nullptr, n, s);
+  if (!ctx->force_lsd && n < ((int64_t)1 << 31)) {  // the bucketed pair sort with a scratch value column
+    uint32_t *v, *v_alt;
+    XS_TRY(ws(ctx, W_KSORT_VAL, n + 1, s, &v));
+    XS_TRY(ws(ctx, W_KSORT_VAL_ALT, n + 1, s, &v_alt));
+    return bucket_sort_pairs(ctx, keys, keys_alt, &v, &v_alt, n, bits, s);
+  }
   cub::DoubleBuffer<uint64_t> k(*keys, *keys_alt);
   size_t temp = 0;
   XS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, k, (int)n, 0, bits, s));

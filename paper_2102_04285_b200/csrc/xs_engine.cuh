@@ -69,6 +69,8 @@ enum Slot : int {
   W_CUB_TEMP2, W_OPG, W_OPG_INV, W_TGRP_FLAG, W_TGRP_IDX, W_TILE_CTR_B, W_CUB_TEMP_B, W_BS_COUNTS_B, W_BS_OFFS_B, W_BS_TAIL_B, W_BS_CHUNK_B,
   W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
   W_DEEP_OVF, W_DEEP_SCRATCH,
+  W_PSCAN_DESC, W_PSCAN_FLAGS, W_PSCAN_CTR, W_PSCAN_DESC_B, W_PSCAN_FLAGS_B, W_PSCAN_CTR_B, W_SEL_COUNT,
+  W_KSORT_VAL, W_KSORT_VAL_ALT,
   W_NUM_SLOTS
 };
 

@@ -4,9 +4,11 @@
 // handful of host syncs, so host launch latency, not the GPU, bounds the step.
 // Each segment between syncs is a deterministic function of what the host
 // knows at its start: the input/output pointers and sizes, the statistics of
-// the preceding sync, the workspace generation and the retry flags.  Keyed on
-// exactly that, the first sighting runs eagerly (and sizes the workspace), the
-// second is captured into a graph, and later calls replay the graph.  A
+// the preceding sync and the retry flags.  Keyed on exactly that, the first
+// sighting runs eagerly (and sizes the workspace), the second is captured into
+// a graph, and later calls replay the graph; a graph remembers the workspace
+// generation it was captured in and is never replayed after the workspace
+// moved (the next sighting captures again).  A
 // segment that tries to allocate or synchronize while being captured is
 // marked non-capturable and keeps running eagerly.
 //
@@ -27,8 +29,10 @@ std::string segment_key(xs_ctx* ctx, const char* tag, const void* extra, size_t 
   k.push_back('\0');
   k.append(reinterpret_cast<const char*>(ctx->h_stats), sizeof(Stats));
   k.append(reinterpret_cast<const char*>(extra), extra_bytes);
-  const long long misc[5] = {ctx->ws_generation, ctx->trie_cap_log2, ctx->force_lsd ? 1 : 0, ctx->prof_on ? 1 : 0,
-                             ctx->deep_cap};
+  // (no workspace generation: a graph records it and is never replayed
+  // across a generation change, and a key seen before a workspace growth is
+  // still "seen" -- its next call captures instead of starting over eagerly)
+  const long long misc[4] = {ctx->trie_cap_log2, ctx->force_lsd ? 1 : 0, ctx->prof_on ? 1 : 0, ctx->deep_cap};
   k.append(reinterpret_cast<const char*>(misc), sizeof(misc));
   return k;
 }
@@ -101,7 +105,7 @@ static int run_segment_on(xs_ctx* ctx, cudaStream_t s, const std::string& key,
   // First sighting: eager (a one-off trace never pays capture + instantiate).
   // Second sighting: captured.  If the workspace must grow, the capture
   // aborts at the first allocation (ws_get) and the segment runs eagerly,
-  // sizing the workspace; the next call (new generation in its key) captures.
+  // sizing the workspace; the next call captures.
   if (!ctx->graph_seen.count(key)) {
     ctx->graph_seen.insert(key);
     return body();

@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include "xs_engine.cuh"
+#include "xs_prims.cuh"
 
 namespace xs {
 
@@ -154,6 +155,7 @@ struct IsEnd {
 int run_union(xs_ctx* ctx, const EventView& v, int cat, int per_pid, int64_t period, int64_t* out_ns,
               int64_t* utilized, int64_t* n_intervals, int64_t* span_lo, int64_t* span_hi, cudaStream_t s) {
   XS_TRY(stage_events(ctx, v, s, false, false, nullptr));
+  XS_CUDA(cudaMemsetAsync(&((Stats*)ctx->ptr[W_STATS])->pad[3], 0, 8, s));
   const Stats& H = *ctx->h_stats;
   const int np = v.ev.n_pids;
   const int64_t n = v.ev.n;
@@ -195,13 +197,7 @@ int run_union(xs_ctx* ctx, const EventView& v, int cat, int per_pid, int64_t per
     XS_LAUNCH(ctx, k_union_keys, grid_for(n), XS_BLOCK, 0, s, v, n, cat, per_pid, lo, gspan, tb, k, cnt);
     XS_TRY(sort_keys_u64(ctx, &k, &k_alt, m, (per_pid ? pb : 0) + tb + 1, s));
     {
-      cub::TransformInputIterator<int, UnionDelta, const uint64_t*> it(k, UnionDelta());
-      size_t temp = 0;
-      XS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, it, depth, (int)m, s));
-      void* t;
-      XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-      XS_CUDA(cub::DeviceScan::InclusiveSum(t, temp, it, depth, (int)m, s));
-      ctx->launches += 2;
+      XS_TRY(scan_inclusive<int>(ctx, map_in((const uint64_t*)k, UnionDelta()), depth, m, s));
     }
     XS_LAUNCH(ctx, k_union_reduce, grid_for(m), XS_BLOCK, 0, s, k, depth, m, tb, per_pid, gspan, period, seg_ns,
               acc, (int64_t*)nullptr, (int64_t*)nullptr);
@@ -215,7 +211,10 @@ int run_union(xs_ctx* ctx, const EventView& v, int cat, int per_pid, int64_t per
   }
   ctx->un_intervals = per_pid ? -1 : h_acc[1];
   if (out_ns) XS_CUDA(cudaMemcpyAsync(out_ns, seg_ns, nseg * 8, cudaMemcpyDeviceToHost, s));
+  long long ovf = 0;  // a bucketed key sort overflowed: the caller re-runs through the LSD sort
+  XS_CUDA(cudaMemcpyAsync(&ovf, &((Stats*)ctx->ptr[W_STATS])->pad[3], 8, cudaMemcpyDeviceToHost, s));
   XS_CUDA(cudaStreamSynchronize(s));
+  if (ovf && !ctx->force_lsd) return XS_RETRY_LSD;
   if (utilized) *utilized = h_acc[0];
   if (n_intervals) *n_intervals = h_acc[1];
   return XS_OK;
@@ -235,16 +234,8 @@ int fetch_union_intervals(xs_ctx* ctx, int64_t* out_lo, int64_t* out_hi, cudaStr
   XS_TRY(ws(ctx, W_UN_IV, 2 * ni, s, &dlo));
   dhi = dlo + ni;
   {  // exclusive prefix counts of starts / ends = output slots
-    cub::CountingInputIterator<int64_t> ci(0);
-    cub::TransformInputIterator<int, IsStart, cub::CountingInputIterator<int64_t>> its(ci, IsStart{ctx->un_depth});
-    cub::TransformInputIterator<int, IsEnd, cub::CountingInputIterator<int64_t>> ite(ci, IsEnd{ctx->un_depth});
-    size_t temp = 0;
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, its, rs, (int)m, s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, its, rs, (int)m, s));
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, ite, re, (int)m, s));
-    ctx->launches += 4;
+    XS_TRY(scan_exclusive<int>(ctx, IsStart{ctx->un_depth}, rs, m, s));
+    XS_TRY(scan_exclusive<int>(ctx, IsEnd{ctx->un_depth}, re, m, s));
   }
   const int64_t* gspan = (const int64_t*)ctx->ptr[W_UN_GSPAN];
   XS_LAUNCH(ctx, k_union_intervals, grid_for(m), XS_BLOCK, 0, s, ctx->un_keys, ctx->un_depth, m, ctx->un_tb, gspan,
@@ -266,7 +257,9 @@ int xs_union(xs_ctx_t* ctx, const xs_events_t* ev, int category, int per_pid, in
   if (!ctx || !ev || category < 0 || category > 5) return XS_BAD_ARGUMENT;
   cudaSetDevice(ctx->device);
   EventView v{*ev, ev->start, ev->dur};
-  return run_union(ctx, v, category, per_pid, 0, out_ns, nullptr, nullptr, span_lo, span_hi, (cudaStream_t)stream);
+  return with_lsd_retry(ctx, [&] {
+    return run_union(ctx, v, category, per_pid, 0, out_ns, nullptr, nullptr, span_lo, span_hi, (cudaStream_t)stream);
+  });
 }
 
 int xs_utilization(xs_ctx_t* ctx, const xs_events_t* ev, int64_t period_ns, int64_t* utilized, int64_t* n_intervals,
@@ -275,7 +268,9 @@ int xs_utilization(xs_ctx_t* ctx, const xs_events_t* ev, int64_t period_ns, int6
   cudaSetDevice(ctx->device);
   EventView v{*ev, ev->start, ev->dur};
   int64_t ns = 0;
-  return run_union(ctx, v, 5, 0, period_ns, &ns, utilized, n_intervals, span_lo, span_hi, (cudaStream_t)stream);
+  return with_lsd_retry(ctx, [&] {
+    return run_union(ctx, v, 5, 0, period_ns, &ns, utilized, n_intervals, span_lo, span_hi, (cudaStream_t)stream);
+  });
 }
 
 int xs_union_intervals_fetch(xs_ctx_t* ctx, int64_t* out_lo, int64_t* out_hi, xs_stream_t stream) {

@@ -27,6 +27,7 @@
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include "xs_engine.cuh"
+#include "xs_prims.cuh"
 
 namespace xs {
 
@@ -577,15 +578,9 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   XS_TRY(ws(ctx, W_OP_EV, m + 1, s, &op_ev));
   {
     int* nsel;
-    XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &nsel));
+    XS_TRY(ws(ctx, W_SEL_COUNT, 4, s, &nsel));
     OpPred pred{v.ev.cat, ctx->spec_select_dur ? ctx->spec_select_dur : v.dur};
-    size_t temp = 0;
-    cub::CountingInputIterator<int> it(0);
-    XS_CUDA(cub::DeviceSelect::If(nullptr, temp, it, op_ev, nsel, (int)v.ev.n, pred, s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceSelect::If(t, temp, it, op_ev, nsel, (int)v.ev.n, pred, s));
-    ctx->launches += 2;
+    XS_TRY(select_indices(ctx, pred, v.ev.n, op_ev, nsel, s));
   }
   // 2. endpoint stream per (pid, tid) group: one sort + local tie order
   uint64_t *sk, *sk_alt;
@@ -601,13 +596,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   XS_TRY(ws(ctx, W_OPG, ng + 1, s, &opg));
   XS_TRY(ws(ctx, W_OPG_INV, nog + 1, s, &opg_inv));
   {
-    cub::TransformInputIterator<int, HasOps, const int*> it(group_ops, HasOps());
-    size_t temp = 0;
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, it, opg, ng, s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, it, opg, ng, s));
-    ctx->launches += 2;
+    XS_TRY(scan_exclusive<int>(ctx, map_in(group_ops, HasOps()), opg, ng, s));
   }
   XS_LAUNCH(ctx, k_op_groups, grid_for(ng), XS_BLOCK, 0, s, group_ops, ng, opg, opg_inv);
   XS_LAUNCH(ctx, k_endpoints, grid_for(m), XS_BLOCK, 0, s, op_ev, m, v, lo, tb, opg, ctx->spec_zero_sentinel ? 1 : 0,
@@ -626,13 +615,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   XS_TRY(ws(ctx, W_DCLOSE, m + 1, s, &d_close));
   XS_TRY(ws(ctx, W_PARENT, m + 1, s, &parent));
   {
-    cub::TransformInputIterator<int, DepthDelta, const uint64_t*> it(sk, DepthDelta());
-    size_t temp = 0;
-    XS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, it, depth, (int)(2 * m), s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceScan::InclusiveSum(t, temp, it, depth, (int)(2 * m), s));
-    ctx->launches += 2;
+    XS_TRY(scan_inclusive<int>(ctx, map_in((const uint64_t*)sk, DepthDelta()), depth, 2 * m, s));
   }
   XS_LAUNCH(ctx, k_depth_scatter, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, depth, 2 * m, d_open, pos_open, d_close);
   XS_LAUNCH(ctx, k_depth_check, grid_for(m), XS_BLOCK, 0, s, d_open, d_close, m, st);

@@ -619,24 +619,26 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
     const unsigned bits = __ballot_sync(0xffffffffu, hd);
     if (lane == 0) S.head[idx >> 5] = bits;  // (bit 0 is provisional: fixed below against the previous word)
   }
-  agg.last = base + kmax;
-  SwMaxOp mop;
+  // chunk aggregate: warp reductions in hardware (redux.sync), then 8 warps
+  {
+    SwState w;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    SwState other = shfl_down_T(agg, o);
-    agg = mop(agg, other);
+    for (int i = 0; i < 8; i++) w.c[i] = __reduce_add_sync(0xffffffffu, agg.c[i]);
+    const unsigned wmax = __reduce_max_sync(0xffffffffu, kmax);
+    w.has = __any_sync(0xffffffffu, agg.has);
+    w.last = base + wmax;
+    w.pad = 0;
+    if (lane == 0) S.warp_agg[warp] = w;
   }
-  if (lane == 0) S.warp_agg[warp] = agg;
   __syncthreads();
   SwState tile_agg = sw_identity();
   if (warp == 0) {
-    SwState w = lane < BK_THREADS / 32 ? S.warp_agg[lane] : sw_identity();
+    const SwState w = lane < BK_THREADS / 32 ? S.warp_agg[lane] : sw_identity();
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      SwState other = shfl_down_T(w, o);
-      w = mop(w, other);
-    }
-    tile_agg = shfl_idx_T(w, 0);
+    for (int i = 0; i < 8; i++) tile_agg.c[i] = __reduce_add_sync(0xffffffffu, w.c[i]);
+    const unsigned rel = lane < BK_THREADS / 32 && w.has ? (unsigned)(w.last - base) : 0u;
+    tile_agg.last = base + __reduce_max_sync(0xffffffffu, rel);
+    tile_agg.has = __any_sync(0xffffffffu, w.has);
     if (lane == 0) tile_publish_agg((int)c, tile_agg, desc, flags);
   }
   XS_STAMP(2);
@@ -755,6 +757,15 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
   int c_pid = -1;
   int64_t c_ob = 0, c_oc = -1;
   int c_path = 0;
+  // path of the op count oc is pidpath[oc - 1]; consecutive op endpoints read
+  // consecutive entries, so the entry after the current one is loaded one op
+  // endpoint ahead (its latency hides behind the keys in between)
+  int64_t pf_oc = cur.c[6];
+  int pf_cur = 0, pf_nxt = 0;
+  if (pidpath && my0 < cnt) {
+    pf_cur = pf_oc >= 1 ? pidpath[pf_oc - 1] : 0;
+    pf_nxt = pidpath[pf_oc];  // (allocated 2m + 2: in bounds even past the last endpoint)
+  }
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const bool in = my0 + j < cnt;  // (no early exit: the warp steps together)
@@ -784,7 +795,20 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
         const int64_t oc = cur.c[6];
         if (oc != c_oc) {  // the path only changes at OPERATION endpoints
           c_oc = oc;
-          c_path = oc > c_ob ? pidpath[oc - 1] : 0;
+          int val;
+          if (oc == pf_oc) {
+            val = pf_cur;
+          } else if (oc == pf_oc + 1) {
+            val = pf_cur = pf_nxt;
+            pf_oc = oc;
+            pf_nxt = pidpath[oc];
+          } else {
+            val = oc >= 1 ? pidpath[oc - 1] : 0;
+            pf_oc = oc;
+            pf_cur = val;
+            pf_nxt = pidpath[oc];
+          }
+          c_path = oc > c_ob ? val : 0;
         }
         const unsigned long long key = ((unsigned long long)p * n_nodes + (unsigned long long)c_path) * 32ull + mask;
         if (key == run_k) {
@@ -865,25 +889,15 @@ static int bucket_prepare(xs_ctx* ctx, const EventView& v, const int64_t* lo, in
   }
   {
     ProfScope ps(ctx, ST_MAIN_SORT, s);
-    size_t temp = 0;
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, counts, offs, (int)g.nbuckets, s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, counts, offs, (int)g.nbuckets, s));
-    XS_LAUNCH(ctx, k_bk_total, 1, 32, 0, s, offs, counts, (int64_t)g.nbuckets);
-    ctx->launches += 2;
+    // bucket offsets + offs[nb] = total, one pass
+    XS_TRY(scan_exclusive<int64_t>(ctx, ArrayIn<unsigned>{counts}, offs, g.nbuckets, s, offs + g.nbuckets));
     if (pid_chunks) {
       int64_t *ccnt, *cpre;
       XS_TRY(ws(ctx, W_BK_CFIRST, 2 * np_b + 4, s, &ccnt));
       cpre = ccnt + np_b + 2;
       XS_LAUNCH(ctx, k_pid_chunk_counts, grid_for(np_b + 1), XS_BLOCK, 0, s, offs, (int64_t)g.nbuckets, pb_buckets,
                 np_b, ccnt);
-      size_t temp2 = 0;
-      XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp2, ccnt, cpre, (int)(np_b + 1), s));
-      void* t2;
-      XS_TRY(ws_get(ctx, W_CUB_TEMP2, temp2, s, &t2));
-      XS_CUDA(cub::DeviceScan::ExclusiveSum(t2, temp2, ccnt, cpre, (int)(np_b + 1), s));
-      ctx->launches += 2;
+      XS_TRY(scan_exclusive<int64_t>(ctx, ArrayIn<int64_t>{ccnt}, cpre, np_b + 1, s));
       XS_LAUNCH(ctx, k_bucket_chunks_pid, grid_for(32 * n_chunks), XS_BLOCK, 0, s, offs, (int64_t)g.nbuckets,
                 pb_buckets, np_b, cpre, n_chunks, chunk);
     } else {

@@ -19,6 +19,7 @@
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include "xs_engine.cuh"
+#include "xs_prims.cuh"
 
 namespace xs {
 
@@ -239,13 +240,7 @@ int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mas
   XS_TRY(ws(ctx, W_TGRP_IDX, ng + 1, s, &tg));
   {
     const uint8_t* tflag = (const uint8_t*)ctx->ptr[W_TGRP_FLAG];
-    cub::TransformInputIterator<int, FlagToInt, const uint8_t*> it(tflag, FlagToInt());
-    size_t temp = 0;
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, it, tg, ng, s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, it, tg, ng, s));
-    ctx->launches += 2;
+    XS_TRY(scan_exclusive<int>(ctx, map_in(tflag, FlagToInt()), tg, ng, s));
   }
   const int tgb = bits_for((uint64_t)(H.pad[6] > 1 ? H.pad[6] - 1 : 0));
   XS_LAUNCH(ctx, k_trec, grid_for(n), XS_BLOCK, 0, s, v, n, lo, tb, src_mask, dst_mask, tg, key, val, cnt);
@@ -362,14 +357,7 @@ int xs_transition_sites(xs_ctx_t* ctx, const xs_events_t* ev, int pair_mask, int
   XS_TRY(ws(ctx, W_SITE_CNT, n + 1, s, &cnt));
   XS_TRY(ws(ctx, W_SITE_POS, n + 1, s, &pos));
   XS_LAUNCH(ctx, k_tr_count, grid_for(n), XS_BLOCK, 0, s, f, n, pair_mask, cnt);
-  {
-    size_t temp = 0;
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, cnt, pos, (int)n, s));
-    void* t;
-    XS_TRY(ws_get(ctx, W_CUB_TEMP, temp, s, &t));
-    XS_CUDA(cub::DeviceScan::ExclusiveSum(t, temp, cnt, pos, (int)n, s));
-    ctx->launches += 2;
-  }
+  XS_TRY(scan_exclusive<int>(ctx, ArrayIn<int>{cnt}, pos, n, s));
   int lp = 0, lc = 0;
   XS_CUDA(cudaMemcpyAsync(&lp, pos + n - 1, 4, cudaMemcpyDeviceToHost, s));
   XS_CUDA(cudaMemcpyAsync(&lc, cnt + n - 1, 4, cudaMemcpyDeviceToHost, s));

@@ -363,3 +363,108 @@ def merge_raw_list(parts: list) -> Breakdown:
         bd.spans[pv] = (a, b)
         bd.untracked[pv] = (b - a) - tracked[pv]
     return bd
+
+
+# ---------------------------------------------------------------------------
+# correct_trace + compute_overlap(corrected) over ranks (the analyze path)
+
+def merge_reports(local_rep, device):
+    """CorrectionReport rows of disjoint pid sets -> one report on every rank
+    (tiny: 8 ints per pid, one object all-gather); totals add up because
+    original/corrected totals are sums of per-pid spans (correction.py:159-186)."""
+    import torch.distributed as dist
+
+    from .correction import CorrectionReport
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    mine = (local_rep.removed_ns, local_rep.shortfall_ns, local_rep.original_total_ns, local_rep.corrected_total_ns)
+    parts = [None] * world
+    if world > 1:
+        dist.all_gather_object(parts, mine)
+    else:
+        parts = [mine]
+    rep = CorrectionReport()
+    for rm, sf, o, c in parts:
+        rep.removed_ns.update(rm)
+        rep.shortfall_ns.update(sf)
+        rep.original_total_ns += o
+        rep.corrected_total_ns += c
+    rep.removed_ns = dict(sorted(rep.removed_ns.items()))
+    rep.shortfall_ns = dict(sorted(rep.shortfall_ns.items()))
+    return rep
+
+
+def analyze_sharded(ct: ColumnarTrace, profile, attribution=None, device=None, gather_columns: bool = False):
+    """``xstrace analyze --profile`` over ``world`` ranks, one GPU each:
+    correct_trace then compute_overlap of the corrected trace, sharded by
+    whole processes (LPT on event counts; per-pid independence,
+    correction.py:132-157, overlap.py:126).  Every rank returns the merged
+    CorrectionReport and Breakdown (bit-exact: integer sums).  The corrected
+    columns come back as this rank's rows (``rows``, ``start``, ``dur``) or,
+    with ``gather_columns``, as the whole trace's columns on every rank.
+    Errors keep whole-trace semantics on every rank: an invalid trace raises
+    InvalidTraceError; else the uncalibrated hook of the smallest row raises
+    UncalibratedHookError.  Returns (rows, start, dur, report, Breakdown)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _engine, _lib
+    from .correction import UncalibratedHookError, _report, _run
+    from .model import InvalidTraceError, format_violations, meta_violations
+    from .overlap import Attribution
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    eng = _engine.get(torch.cuda.current_device())
+    dev = device or torch.device("cuda", eng.device)
+    attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
+    shards = shard_pids(ct, world)
+    keep = np.isin(ct.pid, np.asarray(shards[rank], np.int32))
+    rows = np.nonzero(keep)[0]
+    local = ct.select_pids(shards[rank])
+    bad_invalid = 1 if meta_violations(ct.processes) else 0
+    bad_row = np.iinfo(np.int64).max
+    raw_c = raw_o = None
+    if not bad_invalid:
+        try:
+            _, _, raw_c = _run(local, profile, local, attr)
+            raw_o = eng.fetch_overlap()
+        except InvalidTraceError:
+            bad_invalid = 1
+        except UncalibratedHookError:  # (_run maps the event; recover its row here)
+            raw_c = None
+            bad_row = _first_uncalibrated_row(local, profile, rows)
+    if world > 1:
+        flags = torch.tensor([bad_invalid, -bad_row], dtype=torch.int64, device=dev)
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX)
+        bad_invalid, bad_row = int(flags[0].item()), -int(flags[1].item())
+    if bad_invalid:
+        raise InvalidTraceError(format_violations(ct.to_trace()))
+    if bad_row != np.iinfo(np.int64).max:
+        name = ct.names[int(ct.name[bad_row])]
+        raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile")
+    start = raw_c.start.cpu().numpy()
+    dur = raw_c.dur.cpu().numpy()
+    rep = merge_reports(_report(local, raw_c), dev)
+    bd = merge_breakdown_raw(local, raw_o, dev)
+    if gather_columns:
+        full_s = np.zeros(ct.n, np.int64)
+        full_d = np.zeros(ct.n, np.int64)
+        if world > 1:
+            gr, gs, gd = (_gather_var(torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(dev), dev, world)
+                          for a in (rows, start, dur))
+            rows_all, s_all, d_all = gr.cpu().numpy(), gs.cpu().numpy(), gd.cpu().numpy()
+        else:
+            rows_all, s_all, d_all = rows, start, dur
+        full_s[rows_all] = s_all
+        full_d[rows_all] = d_all
+        return np.arange(ct.n), full_s, full_d, rep, bd
+    return rows, start, dur, rep, bd
+
+
+def _first_uncalibrated_row(local: ColumnarTrace, profile, rows) -> int:
+    """Global row of the first ACCEL_API event whose name the profile lacks."""
+    have = set(profile.api_internal_ns)
+    bad_names = np.array([nm not in have for nm in local.names], bool)
+    sel = np.nonzero((local.cat == 4) & bad_names[local.name])[0] if len(local.names) else np.zeros(0, np.int64)
+    return int(rows[sel[0]]) if sel.size else np.iinfo(np.int64).max

@@ -203,3 +203,48 @@ def test_gloo_window_split_collective_merge():
     exp = oracle.overlap(synth.adversarial_trace(30_000, pids=5, streams=16), 0)
     for _, c, s, u in results:
         assert (c, s, u) == exp
+
+
+def _report_worker(rank, world, port, q):
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2102_04285_b200 import synth
+    from paper_2102_04285_b200.correction import CorrectionReport
+    from paper_2102_04285_b200.distributed import merge_reports, shard_pids
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        ct = synth.adversarial_trace(30_000, pids=5, streams=16)
+        local = ct.select_pids(shard_pids(ct, world)[rank])
+        _, _, r, _ = oracle.correct(local, synth.adversarial_profile())
+        rep = merge_reports(CorrectionReport(r["removed_ns"], r["shortfall_ns"], r["original_total_ns"],
+                                             r["corrected_total_ns"]), torch.device("cpu"))
+        q.put((rank, rep.removed_ns, rep.shortfall_ns, rep.original_total_ns, rep.corrected_total_ns))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_report_merge_equals_single_process():
+    """The correction report of pid-sharded ranks merges to the whole trace's."""
+    sys.path[:0] = [os.path.join(ROOT, "oracle")]
+    import oracle
+    from paper_2102_04285_b200 import synth
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_report_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, _, r, _ = oracle.correct(synth.adversarial_trace(30_000, pids=5, streams=16), synth.adversarial_profile())
+    for _, rm, sf, o, c in results:
+        assert rm == r["removed_ns"] and sf == r["shortfall_ns"]
+        assert o == r["original_total_ns"] and c == r["corrected_total_ns"]

@@ -127,3 +127,16 @@ def test_config5_window_split_shards_on_device(world):
         parts.append((local, eng.overlap(_engine.DeviceTrace(local, 0), 0)))
     bd = merge_raw_list(parts)
     assert bd.cells == whole.cells and bd.spans == whole.spans and bd.untracked == whole.untracked
+
+
+def test_analyze_sharded_single_rank_equals_analyze():
+    """analyze_sharded (no process group: world 1) returns analyze_columnar's
+    report, Breakdown and corrected columns."""
+    from paper_2102_04285_b200.distributed import analyze_sharded
+
+    ct = synth.adversarial_trace(120_000, pids=9, workers=4)
+    prof = synth.adversarial_profile()
+    s0, d0, rep0, bd0 = analyze_columnar(ct, prof)
+    rows, s1, d1, rep1, bd1 = analyze_sharded(ct, prof, gather_columns=True)
+    assert np.array_equal(s1, s0.cpu().numpy()) and np.array_equal(d1, d0.cpu().numpy())
+    assert rep1 == rep0 and bd1 == bd0
