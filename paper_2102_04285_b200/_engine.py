@@ -60,7 +60,14 @@ def unpack_into(eng, lay, ptrs: dict, a: int, b: int, dst, stream=None) -> None:
 
 
 class DeviceTrace:
-    """Columns of a ColumnarTrace resident in device memory."""
+    """Columns of a ColumnarTrace resident in device memory.
+
+    A pinned trace (ColumnarTrace.pinned) keeps its own device copy.  An
+    ordinary host trace is staged through the engine's page-locked block and
+    its device columns live in the engine's staging buffers: such a
+    DeviceTrace is valid until the next ordinary-trace DeviceTrace on the same
+    device (the public entry points use one at a time; to keep several
+    resident at once, pin the traces)."""
 
     def __init__(self, ct: ColumnarTrace, device: int = 0, non_blocking: bool = False):
         torch = _torch()

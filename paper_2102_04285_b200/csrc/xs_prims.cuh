@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(XS_BLOCK) k_scan_excl(In in, Out* out, int64_t
 // over tens of thousands of small tiles is latency-bound.
 constexpr int RTS_GRID = 148 * 4;
 constexpr int RTS_TILE = XS_BLOCK * PS_ITEMS;
+constexpr int64_t RTS_MIN_N = (int64_t)16 * RTS_TILE;  // below: one single-pass look-back kernel
 
 template <class Out, class F>
 __global__ void __launch_bounds__(XS_BLOCK) k_rts_reduce(F f, int64_t n, int64_t per, Out* sums) {
@@ -182,8 +183,8 @@ int scan_exclusive(xs_ctx* ctx, In in, Out* out, int64_t n, cudaStream_t s, Out*
     if (total) XS_CUDA(cudaMemsetAsync(total, 0, sizeof(Out), s));
     return XS_OK;
   }
-  if (n >= (int64_t)RTS_GRID * RTS_TILE) {
-    const int64_t per = ((n + RTS_GRID - 1) / RTS_GRID + RTS_TILE - 1) / RTS_TILE * RTS_TILE;
+  if (n >= RTS_MIN_N) {
+    const int64_t per = ((n + RTS_GRID - 1) / RTS_GRID + RTS_TILE - 1) / RTS_TILE * RTS_TILE;  // (>= 1 tile)
     const int g = (int)((n + per - 1) / per);
     Out* sums;
     XS_TRY(ws(ctx, W_PSCAN_DESC, (size_t)RTS_GRID + 1, s, &sums));
@@ -278,8 +279,8 @@ int select_indices(xs_ctx* ctx, Pred pred, int64_t n, int* out, int* count, cuda
     XS_CUDA(cudaMemsetAsync(count, 0, sizeof(int), s));
     return XS_OK;
   }
-  if (n >= (int64_t)RTS_GRID * RTS_TILE) {
-    const int64_t per = ((n + RTS_GRID - 1) / RTS_GRID + RTS_TILE - 1) / RTS_TILE * RTS_TILE;
+  if (n >= RTS_MIN_N) {
+    const int64_t per = ((n + RTS_GRID - 1) / RTS_GRID + RTS_TILE - 1) / RTS_TILE * RTS_TILE;  // (>= 1 tile)
     const int g = (int)((n + per - 1) / per);
     int* sums;
     XS_TRY(ws(ctx, W_PSCAN_DESC, (size_t)RTS_GRID + 1, s, &sums));

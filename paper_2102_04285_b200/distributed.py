@@ -74,13 +74,21 @@ def _gather_var(x, device, world):
 
 
 def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
-    """Merge every rank's overlap result into one Breakdown (all ranks get it).
+    """Merge every rank's overlap result into one Breakdown (all ranks get it);
+    see merge_breakdown_parts."""
+    return merge_breakdown_parts([(ct, raw)], device)
 
-    Path ids are per-rank trie nodes, so ranks first agree on a global table
+
+def merge_breakdown_parts(parts: list, device) -> Breakdown:
+    """Merge every rank's overlap results -- each rank passes its list of
+    (trace, raw device result) parts, e.g. one per pid batch -- into one
+    Breakdown on every rank.
+
+    Path ids are per-call trie nodes, so ranks first agree on a global table
     of the path tuples their cells use (an object all-gather of a few KB,
     cached: later merges skip it once one MIN all-reduce says every rank's
     paths are known).  Each nonzero cell then becomes one exact int64 key
-    (pid value, global path, mask) with its ns; the keys and values of all
+    (global pid, global path, mask) with its ns; the keys and values of all
     ranks are all-gathered (variable length: the exchange is bounded by the
     nonzero cells, not by pids x paths x 32) and summed by key -- integer sums
     commute, so the merge is bit-exact and identical on every rank.  Per-pid
@@ -89,16 +97,20 @@ def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
     import torch.distributed as dist
 
     world = dist.get_world_size() if dist.is_initialized() else 1
-    paths = decode_paths(ct, raw.node_parent, raw.node_name)
-    node_ids = np.unique(raw.cell_node) if raw.cell_node.size else np.zeros(0, np.int32)
-    my_paths = {paths[i] for i in node_ids.tolist()} | {()}
-    my_pids = set(ct.pids[np.nonzero(raw.has_events)[0]].tolist())
+    decoded = []
+    my_paths, my_pids = {()}, set()
+    for ct, raw in parts:
+        paths = decode_paths(ct, raw.node_parent, raw.node_name)
+        node_ids = np.unique(raw.cell_node) if raw.cell_node.size else np.zeros(0, np.int32)
+        my_paths |= {paths[i] for i in node_ids.tolist()}
+        my_pids |= set(ct.pids[np.nonzero(raw.has_events)[0]].tolist())
+        decoded.append((ct, raw, paths, node_ids))
     known = my_paths <= set(_TABLES["paths"]) and my_pids <= set(_TABLES["pids"])
     if world > 1:
         flag = torch.tensor([1 if known else 0], dtype=torch.int64, device=device)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         known = bool(flag.item())
-    if not known:  # grow the table (first merge, or new paths): tiny object all-gather
+    if not known:  # grow the tables (first merge, or new paths): tiny object all-gather
         mine = (sorted(my_paths), sorted(my_pids))
         gathered = [None] * world
         if world > 1:
@@ -109,17 +121,23 @@ def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
         _TABLES["pids"] = tuple(sorted(set(_TABLES["pids"]) | {p for g in gathered for p in g[1]}))
     all_paths, all_pids = _TABLES["paths"], _TABLES["pids"]
     path_ix = {p: i for i, p in enumerate(all_paths)}
-    Q = len(all_paths)
-    node_to_q = np.zeros(max(len(paths), 1), np.int64)
-    for i in node_ids.tolist():
-        node_to_q[i] = path_ix[paths[i]]
     pid_ix = {p: i for i, p in enumerate(all_pids)}
-    pv = np.array([pid_ix.get(int(p), 0) for p in ct.pids.tolist()], np.int64)  # global pid index
-    keys = (pv[raw.cell_pid] * Q + node_to_q[raw.cell_node]) * 32 + raw.cell_mask.astype(np.int64)
-    vals = raw.cell_ns.astype(np.int64)
-    has = np.nonzero(raw.has_events)[0]
-    pid_rows = np.stack([pv[has], raw.span_lo[has].astype(np.int64), raw.span_hi[has].astype(np.int64),
-                         raw.tracked[has].astype(np.int64)], axis=1).reshape(-1) if has.size else np.zeros(0, np.int64)
+    Q = len(all_paths)
+    keys_l, vals_l, rows_l = [], [], []
+    for ct, raw, paths, node_ids in decoded:
+        node_to_q = np.zeros(max(len(paths), 1), np.int64)
+        for i in node_ids.tolist():
+            node_to_q[i] = path_ix[paths[i]]
+        pv = np.array([pid_ix.get(int(p), 0) for p in ct.pids.tolist()], np.int64)  # global pid index
+        keys_l.append((pv[raw.cell_pid] * Q + node_to_q[raw.cell_node]) * 32 + raw.cell_mask.astype(np.int64))
+        vals_l.append(raw.cell_ns.astype(np.int64))
+        has = np.nonzero(raw.has_events)[0]
+        if has.size:
+            rows_l.append(np.stack([pv[has], raw.span_lo[has].astype(np.int64), raw.span_hi[has].astype(np.int64),
+                                    raw.tracked[has].astype(np.int64)], axis=1).reshape(-1))
+    keys = np.concatenate(keys_l) if keys_l else np.zeros(0, np.int64)
+    vals = np.concatenate(vals_l) if vals_l else np.zeros(0, np.int64)
+    pid_rows = np.concatenate(rows_l) if rows_l else np.zeros(0, np.int64)
     if world > 1:
         tk, tv, tp = (_gather_var(torch.from_numpy(np.ascontiguousarray(a)).to(device), device, world)
                       for a in (keys, vals, pid_rows))
@@ -128,11 +146,12 @@ def merge_breakdown_raw(ct: ColumnarTrace, raw, device) -> Breakdown:
     sums = np.zeros(uk.shape[0], np.int64)
     np.add.at(sums, inv, vals)
     bd = Breakdown()
+    mk = tuple.__new__
     for k, v in zip(uk.tolist(), sums.tolist()):
         if v:
             pid_q, m = divmod(k, 32)
             p, q = divmod(pid_q, Q)
-            bd.cells[OverlapKey(all_pids[p], all_paths[q], _MASK_CATS[m])] = v
+            bd.cells[mk(OverlapKey, (all_pids[p], all_paths[q], _MASK_CATS[m]))] = v
     spans, tracked = {}, {}
     for p, lo, hi, t in pid_rows.reshape(-1, 4).tolist():
         a, b = spans.get(p, (lo, hi))
