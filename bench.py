@@ -394,7 +394,7 @@ def run_ours(args):
     settle_clocks(dev)
     for _ in range(max(args.warmup, 1)):
         flush.fill_(1.0)  # (the same L2 state as the timed steps)
-        raw, _ = step_device()
+        step_device()  # (results dropped: every call gets the same output buffers, as in the timed loop)
     torch.cuda.synchronize()
     launches0 = eng.launches()
     times = []

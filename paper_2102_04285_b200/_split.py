@@ -5,7 +5,9 @@ Every result of the path is per process (overlap.py:126, correction.py:132;
 analysed as consecutive calls over disjoint pid batches and the results
 merged exactly.  Two cases need it:
 
-* more than ``MAX_EVENTS_PER_CALL`` events (the C ABI's per-call row bound);
+* more than ``MAX_EVENTS_PER_CALL`` events: the C ABI takes up to 2^30 rows
+  per call, and the default bound (2^28) keeps one call's workspace plus its
+  columns well inside one B200's 180 GB;
 * endpoint keys wider than 64 bits: a call's keys are
   ``pid index | time relative to the pid's first event | code``, so
   ``bits(#pids - 1) + bits(max per-pid span) + 4`` must fit 64 bits.  A batch
@@ -23,7 +25,7 @@ import numpy as np
 
 from .columnar import ColumnarTrace
 
-MAX_EVENTS_PER_CALL = 1 << 30
+MAX_EVENTS_PER_CALL = 1 << 28
 CODE_BITS = 4  # endpoint code bits of the widest key family (overlap endpoints)
 
 
