@@ -46,11 +46,11 @@ __global__ void __launch_bounds__(XS_BLOCK) k_bs_scatter(const uint64_t* __restr
   const int64_t slot = bucket_slot(counts, offs, (uint32_t)(k >> shift), valid);
   if (valid) {
     okeys[slot] = k;
-    ovals[slot] = vals[i];
+    if (vals) ovals[slot] = vals[i];
   } else if (in) {  // sentinel: after all real keys
     const int64_t at = offs[nb] + (int64_t)atomicAdd(tail, 1ull);
     okeys[at] = k;
-    ovals[at] = vals[i];
+    if (vals) ovals[at] = vals[i];
   }
 }
 
@@ -60,7 +60,7 @@ __global__ void k_bs_tail(const uint64_t* __restrict__ keys, const uint32_t* __r
   for (int64_t i = *total + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     okeys[i] = keys[i];
-    ovals[i] = vals[i];
+    if (vals) ovals[i] = vals[i];
   }
 }
 
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
     const int idx = j * BK_THREADS + t;
     if (idx < cnt) {
       S.k[idx] = keys[s0 + idx] - base;
-      S.v[idx] = vals[s0 + idx];
+      S.v[idx] = vals ? vals[s0 + idx] : 0u;
     }
   }
   __syncthreads();
@@ -116,12 +116,14 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
     }
     int r = 0, q = idx - 1, steps = 0;
     for (; q >= 0 && steps < BK_RANK_MAX && (S.k[q] >> shift) == bk; q--, steps++) r += S.k[q] <= k;
-    big |= steps == BK_RANK_MAX && q >= 0 && (S.k[q] >> shift) == bk;
+    bool trunc = steps == BK_RANK_MAX && q >= 0 && (S.k[q] >> shift) == bk;
     const int start = q + 1;
     int q2 = idx + 1;
     steps = 0;
     for (; q2 < cnt && steps < BK_RANK_MAX && (S.k[q2] >> shift) == bk; q2++, steps++) r += S.k[q2] < k;
-    big |= steps == BK_RANK_MAX && q2 < cnt && (S.k[q2] >> shift) == bk;
+    trunc |= steps == BK_RANK_MAX && q2 < cnt && (S.k[q2] >> shift) == bk;
+    big |= trunc;
+    if (trunc) continue;  // (a truncated rank is no position: the block sort below places this chunk)
     S.sk[start + r] = k;
     S.sv[start + r] = S.v[idx];
   }
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
     const int idx = j * BK_THREADS + t;
     if (idx < cnt) {
       okeys[s0 + idx] = base + S.sk[idx];
-      ovals[s0 + idx] = S.sv[idx];
+      if (ovals) ovals[s0 + idx] = S.sv[idx];
     }
   }
 }
@@ -170,7 +172,7 @@ static int bucket_sort_pairs_impl(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_
 int bucket_sort_pairs(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, uint32_t** vals, uint32_t** vals_alt,
                       int64_t n, int key_bits, cudaStream_t s) {
   static const bool check = getenv("XS_CHECK_BSORT") != nullptr;
-  if (!check) return bucket_sort_pairs_impl(ctx, keys, keys_alt, vals, vals_alt, n, key_bits, s);
+  if (!check || !*vals) return bucket_sort_pairs_impl(ctx, keys, keys_alt, vals, vals_alt, n, key_bits, s);
   std::vector<uint64_t> in(n), out(n);
   std::vector<uint32_t> vin(n), vout(n);
   XS_CUDA(cudaMemcpyAsync(in.data(), *keys, n * 8, cudaMemcpyDeviceToHost, s));

@@ -139,10 +139,8 @@ int sort_keys_u64(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_alt, int64_t n, 
   if (n <= 1 || bits <= 0) return XS_OK;
   if (bits > 64) bits = 64;
   if (n <= SMALL_SORT_MAX) return small_sort(ctx, *keys, nullptr, n, s);
-  if (!ctx->force_lsd && n < ((int64_t)1 << 31)) {  // the bucketed pair sort with a scratch value column
-    uint32_t *v, *v_alt;
-    XS_TRY(ws(ctx, W_KSORT_VAL, n + 1, s, &v));
-    XS_TRY(ws(ctx, W_KSORT_VAL_ALT, n + 1, s, &v_alt));
+  if (!ctx->force_lsd && n < ((int64_t)1 << 31)) {  // the bucketed sort, keys only (no value column)
+    uint32_t *v = nullptr, *v_alt = nullptr;
     return bucket_sort_pairs(ctx, keys, keys_alt, &v, &v_alt, n, bits, s);
   }
   cub::DoubleBuffer<uint64_t> k(*keys, *keys_alt);

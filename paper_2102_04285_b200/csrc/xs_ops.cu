@@ -640,6 +640,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   // 6. path of every op segment, indexed in (pid, t) order
   int* pidpath;
   XS_TRY(ws(ctx, W_PIDPATH, 2 * m + 2, s, &pidpath));
+  XS_CUDA(cudaMemsetAsync(pidpath + 2 * m, 0, 2 * sizeof(int), s));  // (the sweep prefetches one past the last)
   os.pidpath = pidpath;
   uint64_t *pk, *pk_alt;
   XS_TRY(ws(ctx, W_PK, 2 * m + 2, s, &pk));

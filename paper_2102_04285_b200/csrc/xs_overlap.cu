@@ -462,6 +462,32 @@ struct SwOp {
   }
 };
 
+// 7 signed 16-bit counters (the SwState counts c[0..6]) in two words:
+// a = c0 | c1 | c2 | c3, b = c4 | c5 | c6; added lane-wise without carries
+struct P7 {
+  unsigned long long a, b;
+};
+__device__ __forceinline__ unsigned long long swar16_add(unsigned long long x, unsigned long long y) {
+  constexpr unsigned long long H = 0x8000800080008000ull;
+  return ((x & ~H) + (y & ~H)) ^ ((x ^ y) & H);
+}
+struct P7Add {
+  __device__ P7 operator()(const P7& x, const P7& y) const { return P7{swar16_add(x.a, y.a), swar16_add(x.b, y.b)}; }
+};
+__device__ __forceinline__ void p7_apply(P7& s, uint32_t code) {  // sw_apply on the packed lanes
+  const uint32_t cat = code & 7u;
+  if (cat == 7u) return;  // (no such code; sw_apply ignores it too)
+  const int lane = cat == 0 ? 6 : (int)cat - 1;
+  const unsigned short d = cat == 0 ? 1 : ((code & 8u) ? 0xFFFFu : 1u);
+  const unsigned long long dv = (unsigned long long)d << (16 * (lane & 3));
+  if (lane < 4) s.a = swar16_add(s.a, dv);
+  else s.b = swar16_add(s.b, dv);
+}
+__device__ __forceinline__ int p7_lane(const P7& s, int i) {
+  const unsigned long long w = i < 4 ? s.a : s.b;
+  return (int)(short)(unsigned short)(w >> (16 * (i & 3)));
+}
+
 __device__ __forceinline__ void sw_apply(SwState& s, uint32_t code) {
   const uint32_t cat = code & 7u;
   const int d = (code & 8u) ? -1 : 1;
@@ -704,31 +730,35 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
   }
   __syncthreads();
   XS_STAMP(3);
-  // 3. thread prefix over the sorted (blocked) items + chunk prefix
+  // 3. thread prefix over the sorted (blocked) items + chunk prefix.  Inside
+  // a chunk every partial count is bounded by the chunk size (|x| <= 4096),
+  // so the block scan runs on 7 signed 16-bit lanes packed in two 64-bit
+  // words (lane-wise SWAR adds: 2 shuffles per step instead of 12); only the
+  // chunk prefix from the look-back is a full 32-bit state.
   uint32_t kb[BK_ITEMS];
-  SwState ta = sw_identity();
   const int my0 = t * BK_ITEMS;
   uint32_t tlast = 0;
+  P7 ta{0ull, 0ull};
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     kb[j] = my0 + j < cnt ? S.sorted[my0 + j] : 0;
     if (my0 + j < cnt) {
-      sw_apply(ta, kb[j] & 15u);
+      p7_apply(ta, kb[j] & 15u);
       tlast = kb[j];
-      ta.has = 1;
     }
   }
-  ta.last = base + tlast;
   S.last[t] = tlast;
-  SwState dummy;
-  SwState excl = block_exclusive_fast(ta, SwOp(), sw_identity(), S.warp_agg, &dummy);
+  P7 dummy;
+  const P7 excl = block_exclusive_fast(ta, P7Add(), P7{0ull, 0ull}, reinterpret_cast<P7*>(S.warp_agg), &dummy);
   if (warp == 0) {
     SwState pre = tile_lookback_published((int)c, tile_agg, desc, flags, SwOp(), sw_identity());
     if (lane == 0) S.tile_pre = pre;
   }
   __syncthreads();
   XS_STAMP(4);
-  SwState cur = SwOp()(S.tile_pre, excl);
+  SwState cur = S.tile_pre;
+#pragma unroll
+  for (int i = 0; i < 7; i++) cur.c[i] += p7_lane(excl, i);
   uint64_t prev = 0;
   bool have_prev = false;
   if (t == 0) {

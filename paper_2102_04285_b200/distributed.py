@@ -138,13 +138,14 @@ def merge_breakdown_parts(parts: list, device) -> Breakdown:
     keys = np.concatenate(keys_l) if keys_l else np.zeros(0, np.int64)
     vals = np.concatenate(vals_l) if vals_l else np.zeros(0, np.int64)
     pid_rows = np.concatenate(rows_l) if rows_l else np.zeros(0, np.int64)
+    # exchange and sum by key on the device (NCCL all-gather, then one
+    # sort-unique + index_add over the gathered cells)
+    tk, tv, tp = (torch.from_numpy(np.ascontiguousarray(a)).to(device) for a in (keys, vals, pid_rows))
     if world > 1:
-        tk, tv, tp = (_gather_var(torch.from_numpy(np.ascontiguousarray(a)).to(device), device, world)
-                      for a in (keys, vals, pid_rows))
-        keys, vals, pid_rows = tk.cpu().numpy(), tv.cpu().numpy(), tp.cpu().numpy()
-    uk, inv = np.unique(keys, return_inverse=True)
-    sums = np.zeros(uk.shape[0], np.int64)
-    np.add.at(sums, inv, vals)
+        tk, tv, tp = (_gather_var(x, device, world) for x in (tk, tv, tp))
+    uk_t, inv_t = torch.unique(tk, sorted=True, return_inverse=True)
+    sums_t = torch.zeros(uk_t.shape[0], dtype=torch.int64, device=tk.device).index_add_(0, inv_t, tv)
+    uk, sums, pid_rows = uk_t.cpu().numpy(), sums_t.cpu().numpy(), tp.cpu().numpy()
     bd = Breakdown()
     mk = tuple.__new__
     for k, v in zip(uk.tolist(), sums.tolist()):
