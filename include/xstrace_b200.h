@@ -264,6 +264,35 @@ typedef struct {
 int xs_pack_plan(const xs_events_t* ev, int n_threads, xs_pack_layout_t* lay);
 int xs_pack_fill(const xs_events_t* ev, const xs_pack_layout_t* lay, void* block, int64_t block_bytes);
 
+/* Device synthetic generator (TEST / BENCH INFRASTRUCTURE, SURVEY 8(f4);
+ * synth.py:246-375 shape): n_pids processes x `iterations` DDPG-style
+ * iterations, both twins at once (uninstrumented start/dur and the
+ * instrumented start_inst/dur_inst with the given constant hook amounts).
+ * xs_synth_plan sizes it (one sync) and returns the row count;
+ * xs_synth_generate writes the columns (device buffers of that many rows,
+ * pid-contiguous; tid = (pid, tid) group index with groups 0, [1], 1000 per
+ * pid) and span[2*p] / span[2*p+1] = the end of pid p's uninstrumented /
+ * instrumented timeline (every pid starts at 0).  names: DEVICE int32[11],
+ * the name-table ranks of kernel, script, launch, memcpy, inference,
+ * inference_backend, simulation, simulation_sim, backprop, backprop_backend,
+ * and the outer op. */
+typedef struct {
+  int64_t iterations;
+  uint64_t seed;
+  int32_t n_pids;
+  int32_t outer_op;          /* wrap each iteration's phases in one more op      */
+  int32_t second_tid_ops;    /* mirror every phase op on tid 1                    */
+  int32_t first_pid;         /* pid value of the first process (random streams   */
+                             /* are per pid value: any block of pids regenerates */
+                             /* the same processes)                               */
+  int64_t ann_start, ann_end, transition, interception, launch, memcpy;
+  const int32_t* names;
+} xs_synth_spec_t;
+int xs_synth_plan(xs_ctx_t* ctx, const xs_synth_spec_t* spec, int64_t* n_events, xs_stream_t stream);
+int xs_synth_generate(xs_ctx_t* ctx, const xs_synth_spec_t* spec, int64_t* start, int64_t* dur, int64_t* start_inst,
+                      int64_t* dur_inst, int32_t* pid, int32_t* tid, uint8_t* cat, int32_t* name, int64_t* corr,
+                      uint8_t* has_corr, int64_t* span, xs_stream_t stream);
+
 /* Number of kernel launches issued by the library since context creation
  * (instrumentation for the bench's gpu_launches field). */
 int64_t xs_launch_count(xs_ctx_t* ctx);

@@ -52,6 +52,15 @@ class XsPackLayout(C.Structure):
     ]
 
 
+class XsSynthSpec(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int64), ("seed", C.c_uint64), ("n_pids", C.c_int32), ("outer_op", C.c_int32),
+        ("second_tid_ops", C.c_int32), ("first_pid", C.c_int32), ("ann_start", C.c_int64), ("ann_end", C.c_int64),
+        ("transition", C.c_int64), ("interception", C.c_int64), ("launch", C.c_int64), ("memcpy", C.c_int64),
+        ("names", C.c_void_p),
+    ]
+
+
 class XsProfile(C.Structure):
     _fields_ = [
         ("words", C.c_int32), ("reserved", C.c_int32), ("L", C.c_void_p), ("whole", C.c_int64 * 4),
@@ -104,6 +113,8 @@ SIGNATURES = {
     "xs_unpack": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P]),
     "xs_pack_plan": (C.c_int, [C.POINTER(XsEvents), C.c_int, C.POINTER(XsPackLayout)]),
     "xs_pack_fill": (C.c_int, [C.POINTER(XsEvents), C.POINTER(XsPackLayout), P, C.c_int64]),
+    "xs_synth_plan": (C.c_int, [P, C.POINTER(XsSynthSpec), C.POINTER(C.c_int64), P]),
+    "xs_synth_generate": (C.c_int, [P, C.POINTER(XsSynthSpec), P, P, P, P, P, P, P, P, P, P, P, P]),
     "xs_launch_count": (C.c_int64, [P]),
     "xs_profile_enable": (C.c_int, [P, C.c_int]),
     "xs_profile_read": (C.c_int, [P, P, P, C.c_int]),

@@ -70,7 +70,7 @@ enum Slot : int {
   W_UN_GSPAN, W_UN_ACC, W_UN_SEG, W_UN_KEY, W_UN_KEY_ALT, W_UN_DEPTH, W_UN_RANK, W_UN_IV,
   W_DEEP_OVF, W_DEEP_SCRATCH,
   W_PSCAN_DESC, W_PSCAN_FLAGS, W_PSCAN_CTR, W_PSCAN_DESC_B, W_PSCAN_FLAGS_B, W_PSCAN_CTR_B, W_SEL_COUNT,
-  W_KSORT_VAL, W_KSORT_VAL_ALT,
+  W_KSORT_VAL, W_KSORT_VAL_ALT, W_SYN_IT, W_SYN_NK, W_SYN_PID, W_SYN_K,
   W_NUM_SLOTS
 };
 
@@ -194,7 +194,8 @@ struct xs_ctx {
   long long n_trans_out = 0;
   int trie_cap_log2 = 12;
   long long deep_cap = 0;
-  unsigned attr_done = 0;  // kernels whose >48 KB dynamic shared memory attribute is set on this ctx's device  // ints of global scratch per thread for merged op stacks deeper than MAXD
+  unsigned attr_done = 0;
+  int64_t syn_events = 0, syn_kernels = 0;  // sizes of the last xs_synth_plan  // kernels whose >48 KB dynamic shared memory attribute is set on this ctx's device  // ints of global scratch per thread for merged op stacks deeper than MAXD
   bool force_lsd = false;  // bucketed sort overflowed on this input: use the LSD path
   xs::OpsState ops;
   // optional per-stage device timing (CUDA events on the launching stream)

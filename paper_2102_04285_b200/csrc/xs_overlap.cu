@@ -1056,7 +1056,10 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   // (no sync), else the real node count (one sync)
   const Stats& H = *ctx->h_stats;
   int n_nodes;
-  if ((int64_t)np * os.trie.node_cap * 32 <= ((int64_t)1 << 21)) {
+  // (CORRELATION keys also carry the node bits: the trie's capacity may be
+  // far above its node count after an earlier deep-path call -- use the count)
+  const bool corr_wide = attribution == 1 && pb + bits_for((uint64_t)(os.trie.node_cap - 1)) + tb + 2 > 64;
+  if ((int64_t)np * os.trie.node_cap * 32 <= ((int64_t)1 << 21) && !corr_wide) {
     n_nodes = os.trie.node_cap;
   } else {
     XS_LAUNCH(ctx, k_trie_count_to_stats, 1, 32, 0, s, os.trie.count, st);

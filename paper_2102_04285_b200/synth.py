@@ -435,3 +435,102 @@ def adversarial_trace(n_events: int = 10_000_000, pids: int = 64, seed: int = 12
     keep = range(pids) if only is None else [p - 1 for p in only]
     res = _map(_adv_pid, [(seed, p + 1, sizes[p], depth, streams) for p in keep], workers)
     return assemble([r[0] for r in res], adversarial_names(depth), [r[1] for r in res])
+
+
+# ---------------------------------------------------------------------------
+# Device generator (csrc/xs_synth.cu, test/bench infrastructure)
+
+_SYN_NAMES = ("kernel", "script", "launch", "memcpy", "inference", "inference_backend", "simulation",
+              "simulation_sim", "backprop", "backprop_backend")
+
+
+@dataclass
+class DeviceSynth:
+    """Both twins of a generated trace resident on the device: ``cols[twin]``
+    (twin "un" / "inst") maps column names to device tensors; ``meta`` holds
+    the tables (pids, (pid, tid) groups, names, processes) of each twin."""
+
+    meta: dict
+    cols: dict
+    n: int
+
+    def columnar(self, twin: str = "inst") -> ColumnarTrace:
+        """The twin as an ordinary host ColumnarTrace (copies the columns)."""
+        c = self.cols[twin]
+        m = self.meta[twin]
+        return ColumnarTrace(1, c["start"].cpu().numpy(), c["dur"].cpu().numpy(), c["pid"].cpu().numpy(),
+                             c["tid"].cpu().numpy(), c["cat"].cpu().numpy(), c["name"].cpu().numpy(),
+                             c["corr"].cpu().numpy(), c["has_corr"].cpu().numpy(), m["pids"], m["group_pid"],
+                             m["group_tid"], m["names"], m["processes"], m["pid_has_meta"])
+
+    def device_trace(self, twin: str = "inst", device: int = 0):
+        """A DeviceTrace over the resident columns (no host copy): the host
+        trace object only carries the tables and the row count."""
+        from . import _engine
+        m = self.meta[twin]
+        z64 = np.broadcast_to(np.int64(0), (self.n,))
+        z32 = np.broadcast_to(np.int32(0), (self.n,))
+        z8 = np.broadcast_to(np.uint8(0), (self.n,))
+        ct = ColumnarTrace(1, z64, z64, z32, z32, z8, z32, z64, z8, m["pids"], m["group_pid"], m["group_tid"],
+                           m["names"], m["processes"], m["pid_has_meta"])
+        return _engine.DeviceTrace.from_tensors(ct, dict(self.cols[twin], group_pid=m["group_pid_dev"],
+                                                         pid_has_meta=m["pid_has_meta_dev"]), device)
+
+
+def device_ddpg_trace(iterations: int, processes: int = 1, seed: int = 1234, outer_op: str = None,
+                      second_tid_ops: bool = False, first_pid: int = 1, device: int = 0) -> DeviceSynth:
+    """The DDPG-style workload (ddpg_trace / config3_trace shape: the same
+    phases, durations, kernel probability, in-order stream, outer op and tid-1
+    mirrors) generated on the device in both twins (xs_synth_plan /
+    xs_synth_generate); instrumented with the exact profile's amounts, so
+    correct_trace(inst, exact_profile()) == un bit for bit."""
+    import ctypes as C
+
+    import torch
+
+    from . import _engine, _lib
+
+    eng = _engine.get(device)
+    dev = torch.device("cuda", device)
+    names = ddpg_names(outer_op)
+    rank = {x: i for i, x in enumerate(names)}
+    sym = [rank[x] for x in _SYN_NAMES] + [rank[outer_op] if outer_op else 0]
+    names_dev = torch.tensor(sym, dtype=torch.int32, device=dev)
+    ann = EXACT["annotation"]
+    spec = _lib.XsSynthSpec(iterations, seed, processes, 1 if outer_op else 0,
+                            1 if second_tid_ops else 0, first_pid, ann // 2, ann - ann // 2, EXACT["transition"],
+                            EXACT["api_interception"], EXACT["launch"], EXACT["memcpy"], names_dev.data_ptr())
+    n = C.c_int64(0)
+    eng.check(eng.lib.xs_synth_plan(eng.ctx, C.byref(spec), C.byref(n), eng.stream()), "xs_synth_plan")
+    n = int(n.value)
+    t = {k: torch.empty(n, dtype=dt, device=dev) for k, dt in
+         (("su", torch.int64), ("du", torch.int64), ("si", torch.int64), ("di", torch.int64), ("pid", torch.int32),
+          ("tid", torch.int32), ("cat", torch.uint8), ("name", torch.int32), ("corr", torch.int64),
+          ("has_corr", torch.uint8))}
+    span = torch.empty(2 * processes, dtype=torch.int64, device=dev)
+    eng.check(eng.lib.xs_synth_generate(eng.ctx, C.byref(spec), *(t[k].data_ptr() for k in (
+        "su", "du", "si", "di", "pid", "tid", "cat", "name", "corr", "has_corr")), span.data_ptr(), eng.stream()),
+        "xs_synth_generate")
+    ends = span.cpu().numpy().reshape(processes, 2)
+    del names_dev
+    pids = np.arange(first_pid, first_pid + processes, dtype=np.int64)
+    tids = [0, 1, GPU_TID] if second_tid_ops else [0, GPU_TID]
+    group_pid = np.repeat(np.arange(processes, dtype=np.int32), len(tids))
+    group_tid = np.tile(np.array(tids, np.int64), processes)
+    shared = {"pids": pids, "group_pid": group_pid, "group_tid": group_tid, "names": names,
+              "pid_has_meta": np.ones(processes, np.uint8),
+              "group_pid_dev": torch.from_numpy(group_pid).to(dev),
+              "pid_has_meta_dev": torch.ones(processes, dtype=torch.uint8, device=dev)}
+    meta = {}
+    for twin, col in (("un", 0), ("inst", 1)):
+        procs = []
+        for k, pv in enumerate(pids.tolist()):
+            if pv == 1 or processes == 1:
+                procs.append(ProcessMeta(pv, "ddpg_root" if processes > 1 else "ddpg"))
+            else:
+                procs.append(ProcessMeta(pv, f"ddpg_worker_{pv - 2}", parent=1, fork_ns=0,
+                                         join_ns=int(ends[k, col])))
+        meta[twin] = dict(shared, processes=tuple(procs))
+    common = {k: t[k] for k in ("pid", "tid", "cat", "name", "corr", "has_corr")}
+    cols = {"un": dict(common, start=t["su"], dur=t["du"]), "inst": dict(common, start=t["si"], dur=t["di"])}
+    return DeviceSynth(meta, cols, n)
