@@ -33,18 +33,19 @@ def test_device_generator_twins_valid_and_close_exactly(gen):
 
 
 def test_device_generator_matches_host_generator_shape(gen):
-    dev = gen.columnar("un")
-    host = synth.ddpg_trace(300, processes=3, outer_op="iteration", second_tid_ops=True)
+    dev, dev_i = gen.columnar("un"), gen.columnar("inst")
+    host, host_i = synth.ddpg_trace(300, processes=3, outer_op="iteration", second_tid_ops=True, both=True)
     for p in range(3):
         dc = np.bincount(dev.cat[dev.pid == p], minlength=6)
         hc = np.bincount(host.cat[host.pid == p], minlength=6)
         assert np.array_equal(dc[:5], hc[:5])                      # CPU structure: identical counts
         n_api = dc[4]
         assert abs(dc[5] - 0.7 * n_api) < 5 * np.sqrt(n_api * 0.21)  # kernel probability 0.7
-    for cat in (2, 3, 4, 5):
-        dm = dev.dur[dev.cat == cat].mean()
-        hm = host.dur[host.cat == cat].mean()
-        assert abs(dm - hm) / hm < 0.03, (cat, dm, hm)
+    for d, h in ((dev, host), (dev_i, host_i)):  # both twins
+        for cat in (2, 3, 4, 5):
+            dm = d.dur[d.cat == cat].mean()
+            hm = h.dur[h.cat == cat].mean()
+            assert abs(dm - hm) / hm < 0.03, (cat, dm, hm)
     names = [dev.names[i] for i in np.unique(dev.name)]
     assert sorted(names) == sorted(host.names[i] for i in np.unique(host.name))
 
