@@ -49,6 +49,9 @@ def parse():
                     help="BASELINE.json config: 2 (default, the metric's workload), 3 (100M events, 100 pids, "
                          "nested), 4 (1B events, 1000 pids, strong-scaled over the ranks), 5 (adversarial 10M)")
     ap.add_argument("--events", type=int, default=0, help="events per GPU for --config 3/5 (default 100M / 10M)")
+    ap.add_argument("--device-gen", action="store_true",
+                    help="--config 4: generate the trace on the device (xs_synth: ~1B events in ~4 s) instead of "
+                         "the host generator (~200 s); the reference arm always uses the host generator")
     ap.add_argument("--ref-budget", type=float, default=120.0,
                     help="--impl reference: stop the timed steps once this many seconds are spent")
     return ap.parse_args()
@@ -707,16 +710,26 @@ def run_config4(args):
     gen_s = 0.0
     for a in range(lo, hi, 100):
         t0 = time.time()
-        ct = synth.config3_trace(processes=min(100, hi - a), events_per_pid=1_000_000, first_pid=a + 1,
-                                 workers=os.cpu_count())
+        if args.device_gen:  # both twins generated in HBM; the instrumented one is analysed in place
+            g = synth.device_ddpg_trace(synth.CONFIG3_ITERS_PER_1M, processes=min(100, hi - a), first_pid=a + 1,
+                                        outer_op="iteration", second_tid_ops=True, device=local)
+            torch.cuda.synchronize()
+            dt = g.device_trace("inst", local)
+            ct = dt.ct
+            del g.cols["un"]
+            keep = g  # (owns the columns)
+        else:
+            ct = synth.config3_trace(processes=min(100, hi - a), events_per_pid=1_000_000, first_pid=a + 1,
+                                     workers=os.cpu_count())
+            keep = ct.pinned()  # (a pinned trace keeps its own device copy: batches never alias)
+            dt = _engine.DeviceTrace(keep, local)
         gen_s += time.time() - t0
-        pin = ct.pinned()  # (a pinned trace keeps its own device copy: batches never alias)
-        batches.append((ct, _engine.DeviceTrace(pin, local), prof.scaled(ct.names)))
+        batches.append((ct, dt, prof.scaled(ct.names), keep))
     n_local = sum(b[0].n for b in batches)
 
     def step():
         parts = []
-        for ct, dt, sc in batches:
+        for ct, dt, sc, _ in batches:
             eng.correct(dt, sc, analyze_attribution=0)
             parts.append((ct, eng.fetch_overlap()))
         return merge_breakdown_parts(parts, dev)
@@ -763,7 +776,9 @@ def run_config4(args):
                        "batches_per_rank": len(batches), "l2": "inputs 38 GB/rank > L2",
                        "parallelism": f"contiguous pid blocks x{world}, NCCL sparse merge"},
             "gpu_launches": int(launches / args.steps), "merged_pids": len(bd.spans), "conservation": conserve,
-            "generation_s_rank0": round(gen_s, 1), "clocks": clocks.summary()}))
+            "generation_s_rank0": round(gen_s, 1),
+            "generator": "device (xs_synth)" if args.device_gen else "host (synth.config3_trace)",
+            "clocks": clocks.summary()}))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
