@@ -788,7 +788,48 @@ int corrected_total_from_spans(xs_ctx* ctx, cudaStream_t s) {
 
 using namespace xs;
 
+// The operation stage of the ORIGINAL trace serves the overlap pass of the
+// corrected one when the removal map is strictly increasing on every pid's
+// op endpoint times: then the corrected endpoints keep their order and ties
+// (equal times stay equal, distinct ones distinct), so the (start, -end, tid,
+// name) ranks, the merged paths and the per-pid op counts are unchanged.
+// pk = the original's op endpoints in (pid, t) order (pid | t_rel | flag,
+// t_rel relative to the original lo, the removal map's own origin); a pair
+// of neighbours of one pid with t < t' but rmap(t) >= rmap(t') sets pad[8]
+// (the host then redoes the overlap pass with its own operation stage).
+namespace xs {
+__global__ void k_ops_strict(const uint64_t* pk, int64_t n2, int tb, const int64_t* sa, const int64_t* sb,
+                             const int64_t* spre, const int64_t* slab_base, const int64_t* ptotal, int np,
+                             Stats* st) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j + 1 >= n2) return;
+  const uint64_t a = pk[j], b = pk[j + 1];
+  if (a == ~0ull || b == ~0ull) return;
+  const uint64_t pa = a >> (tb + 1), pb = b >> (tb + 1);
+  if (pa != pb || (int)pa >= np) return;
+  const uint64_t tmask = (1ull << tb) - 1;
+  const int64_t ta = (int64_t)((a >> 1) & tmask), tb_ = (int64_t)((b >> 1) & tmask);
+  if (ta == tb_) return;
+  const int p = (int)pa;
+  const int64_t base = slab_base[p], K = slab_base[p + 1] - base;
+  const int64_t ca = ta - rmap_removed(ta, sa, sb, spre, base, K, ptotal[p]);
+  const int64_t cb = tb_ - rmap_removed(tb_, sa, sb, spre, base, K, ptotal[p]);
+  if (ca >= cb) atomicOr((unsigned long long*)&st->pad[8], 1ull);
+}
+
+int ops_reuse_check(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
+  const OpsState& os = ctx->ops;
+  if (os.m <= 0 || !os.pk) return XS_OK;
+  XS_LAUNCH(ctx, k_ops_strict, grid_for(2 * os.m), XS_BLOCK, 0, s, os.pk, 2 * os.m, os.tb,
+            (const int64_t*)ctx->ptr[W_SLAB_A], (const int64_t*)ctx->ptr[W_SLAB_B],
+            (const int64_t*)ctx->ptr[W_SLAB_PRE], (const int64_t*)ctx->ptr[W_SLAB_BASE],
+            (const int64_t*)ctx->ptr[W_PTOTAL], v.ev.n_pids, (Stats*)ctx->ptr[W_STATS]);
+  return XS_OK;
+}
+}  // namespace xs
+
 extern "C" {
+
 
 int xs_remap(xs_ctx_t* ctx, int64_t n, const int32_t* pid_dev, const int64_t* val_dev, int64_t* out_dev,
              xs_stream_t stream) {

@@ -436,6 +436,7 @@ static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* pro
     XS_CUDA(cudaMemsetAsync(&stp->table_full, 0, sizeof(long long), w));
     XS_CUDA(cudaMemsetAsync(&stp->depth_overflow, 0, sizeof(long long), w));
     XS_CUDA(cudaMemsetAsync(&stp->pad[3], 0, sizeof(long long), w));
+    XS_CUDA(cudaMemsetAsync(&stp->pad[7], 0, 2 * sizeof(long long), w));  // (deep-path need, reuse verdict)
   }
   XS_CUDA(cudaEventRecord(ctx->br_fork, w));
   XS_CUDA(cudaStreamWaitEvent(ctx->br_stream[0], ctx->br_fork, 0));
@@ -456,12 +457,15 @@ static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* pro
     Join join{ctx, w};
     XS_TRY(stage_corr_table(ctx, v, ctx->br_stream[0], false));
     ctx->skip_ops_reset = true;
-    XS_TRY(stage_ops(ctx, v, ctx->br_stream[1], false));  // OPERATION nesting is part of require_valid
+    // OPERATION nesting is part of require_valid; with reuse_ops the stage
+    // also builds the paths the corrected trace's overlap pass will use
+    XS_TRY(stage_ops(ctx, v, ctx->br_stream[1], ctx->reuse_ops));
     ctx->skip_ops_reset = false;
     ctx->bank = 1;
     XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, w));
   }
-  return stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, w);
+  XS_TRY(stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, w));
+  return ctx->reuse_ops ? ops_reuse_check(ctx, v, w) : XS_OK;
 }
 
 static int correct_verdict(xs_ctx* ctx, const Stats* h, int64_t* bad_event) {
@@ -629,11 +633,21 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
   XS_TRY(ws(ctx, W_STATS, 1, s, &st));
   XS_TRY(ws(ctx, W_STATS_SAVE, 1, s, &saved));
   const bool spec = !ctx->force_lsd && !getenv("XS_NO_SPECULATE");  // (the env switch is for tests)
+  const bool no_reuse = getenv("XS_NO_REUSE_OPS") != nullptr;  // (A/B and test switch)
+  struct ReuseScope {
+    xs_ctx* c;
+    ~ReuseScope() { c->reuse_ops = false; }
+  } reuse_scope{ctx};
+  // a trace whose removal map collapsed op endpoints once (the overlap pass
+  // was redone) does not try the reuse again: the same trace would pay the
+  // redo on every call
+  ctx->reuse_ops = spec && attribution == 0 && !no_reuse && !(ev->n == ctx->reuse_bad_n && ev->n_pids == ctx->reuse_bad_pids);
   std::string key = segment_key(ctx, "analyze", &v, sizeof(v));
   key.append(reinterpret_cast<const char*>(prof), sizeof(*prof));
   key.append(reinterpret_cast<const char*>(&vc), sizeof(vc));
   key.append(reinterpret_cast<const char*>(&attribution), sizeof(attribution));
   key.push_back(spec ? 1 : 0);
+  key.push_back(ctx->reuse_ops ? 1 : 0);
   key.append(reinterpret_cast<const char*>(&out_start_host), sizeof(out_start_host));
   key.append(reinterpret_cast<const char*>(&out_dur_host), sizeof(out_dur_host));
   const bool to_host = out_start_host && ev->n > 0;
@@ -648,7 +662,8 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     // correlations are untouched by the correction: the original's dangling
     // check stands, and only CORRELATION attribution needs launch instants
     if (attribution == 1) XS_TRY(stage_corr_table(ctx, vc, w, true));
-    XS_TRY(ops_with_overlap_pre(ctx, vc, attribution, w));
+    if (ctx->reuse_ops) XS_TRY(stage_overlap_pre(ctx, vc, w));  // paths: the original's (checked below)
+    else XS_TRY(ops_with_overlap_pre(ctx, vc, attribution, w));
     XS_TRY(stage_overlap(ctx, vc, attribution, w));
     ctx->res_pids = ev->n_pids;
     return corrected_total_from_spans(ctx, w);
@@ -684,7 +699,9 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     // everything the pass was sized by (the original's pass 1) bounds the
     // corrected trace's counts; INSTANT tolerates ops shrunk to zero length
     const bool shrink_ok = attribution == 0;
-    bool same = c.n_bad == 0 && !c.table_full && !c.depth_overflow && !c.pad[3] &&
+    // reused op stage: the original's path flags and the strictness verdict
+    const bool reuse_ok = !ctx->reuse_ops || (!hc->pad[8] && !hc->table_full && !hc->depth_overflow);
+    bool same = reuse_ok && c.n_bad == 0 && !c.table_full && !c.depth_overflow && !c.pad[3] &&
                 (shrink_ok ? c.n_ops_nz <= orig.n_ops_nz : c.n_ops_nz == orig.n_ops_nz) &&
                 (shrink_ok ? c.n_nonzero <= orig.n_nonzero : c.n_nonzero == orig.n_nonzero) &&
                 (shrink_ok ? c.multi_op_pids <= orig.multi_op_pids : c.multi_op_pids == orig.multi_op_pids) &&
@@ -693,6 +710,10 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     if (getenv("XS_DEBUG_STATS"))
       fprintf(stderr, "xs_analyze speculative overlap %s: bad %lld full %lld depth_ovf %lld lsd %lld\n",
               same ? "kept" : "redone", c.n_bad, c.table_full, c.depth_overflow, c.pad[3]);
+    if (ctx->reuse_ops && !reuse_ok) {
+      ctx->reuse_bad_n = ev->n;
+      ctx->reuse_bad_pids = ev->n_pids;
+    }
     if (same) {
       ctx->have_overlap = true;
       ctx->n_cells = c.pad[4];

@@ -193,9 +193,12 @@ struct xs_ctx {
   // last transitions
   long long n_trans_out = 0;
   int trie_cap_log2 = 12;
-  long long deep_cap = 0;
-  unsigned attr_done = 0;
-  int64_t syn_events = 0, syn_kernels = 0;  // sizes of the last xs_synth_plan  // kernels whose >48 KB dynamic shared memory attribute is set on this ctx's device  // ints of global scratch per thread for merged op stacks deeper than MAXD
+  long long deep_cap = 0;  // ints of global scratch per thread for merged op stacks deeper than MAXD
+  bool reuse_ops = false;  // analyze: the original's op stage builds the paths the corrected overlap reuses
+  int64_t reuse_bad_n = -1;  // (n, n_pids) of the last trace whose reuse verdict failed
+  int reuse_bad_pids = -1;
+  unsigned attr_done = 0;  // kernels whose >48 KB dynamic shared memory attribute is set on this ctx's device
+  int64_t syn_events = 0, syn_kernels = 0;  // sizes of the last xs_synth_plan
   bool force_lsd = false;  // bucketed sort overflowed on this input: use the LSD path
   xs::OpsState ops;
   // optional per-stage device timing (CUDA events on the launching stream)
@@ -366,6 +369,7 @@ int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr
 int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_start);
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths);
 int stage_overlap_pre(xs_ctx* ctx, const EventView& v, cudaStream_t s);
+int ops_reuse_check(xs_ctx* ctx, const EventView& v, cudaStream_t s);
 int ops_with_overlap_pre(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t w);
 int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
 int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mask, cudaStream_t s);

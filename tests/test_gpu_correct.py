@@ -73,9 +73,13 @@ def test_correction_matches_reference(case, monkeypatch):
     assert rep.corrected_total_ns == exp["corrected_total_ns"]
     assert enc_breakdown(compute_overlap(out)) == exp["overlap_corrected"]
     # one-call analyze path (correct + overlap(corrected)) gives the same,
-    # with the overlap pass launched speculatively (default) or after a sync
-    for spec in (True, False):
-        if not spec:
+    # with the overlap pass launched speculatively reusing the original's
+    # operation stage (default), speculatively with its own operation stage,
+    # or after a sync
+    for mode in ("reuse", "spec", "sync"):
+        if mode == "spec":
+            monkeypatch.setenv("XS_NO_REUSE_OPS", "1")
+        if mode == "sync":
             monkeypatch.setenv("XS_NO_SPECULATE", "1")
         s, d, rep2, bd = analyze_columnar(ColumnarTrace.from_trace(trace), prof)
         assert s.cpu().numpy().tolist() == exp["start"]
