@@ -8,9 +8,10 @@
 //   1. histogram of key >> shift into ~2 buckets per key       [read keys]
 //   2. exclusive scan -> bucket offsets, chunk table
 //   3. scatter (key, value) into bucket order                   [read, write]
-//   4. one CTA per chunk (<= BK_CAP records): rank each record inside its
-//      bucket (direct comparison; a block radix sort when some bucket is
-//      dense) and write the chunk back in order                 [read, write]
+//   4. one CTA per chunk (<= BK_CAP records): a counting pass over local
+//      bins spanning the chunk's key range, then direct comparison inside
+//      each bin (a block radix sort when some bin is dense); the chunk is
+//      written back in order                                     [read, write]
 // Keys >= 2^key_bits (the callers' "unused slot" sentinels) go to the tail,
 // after every real key, in any order.  The order among equal keys is
 // unspecified: every caller breaks ties with its own total order afterwards
@@ -64,21 +65,36 @@ __global__ void k_bs_tail(const uint64_t* __restrict__ keys, const uint32_t* __r
   }
 }
 
+constexpr int BS_NB = 4096, BS_LOG_NB = 12;  // local counting-sort bins per chunk
+constexpr int BS_BIN_BIG = 256;                // a bin holding more records sends the chunk to the block radix sort
+
 struct BsSmem {
-  uint64_t k[BK_CAP];  // keys relative to the chunk base, bucket order (as scattered); radix scratch with v[]
+  uint64_t k[BK_CAP];  // keys relative to the chunk base: load order, then sorted; radix scratch with v[]
   uint32_t v[BK_CAP];
-  uint64_t sk[BK_CAP];  // sorted
+  uint64_t sk[BK_CAP];  // grouped by local bin
   uint32_t sv[BK_CAP];
-  int big;
+  int bins[BS_NB];  // counts, then exclusive starts
+  uint64_t wmin[BK_THREADS / 32], wmax[BK_THREADS / 32];
+  int scan[32];
 };
 
+struct BsIAdd {
+  __device__ int operator()(int x, int y) const { return x + y; }
+};
+
+// One CTA per chunk (a contiguous key range of <= BK_CAP records).  Sorted in
+// shared memory by one counting pass over BS_NB bins spanning exactly the
+// chunk's [min key, max key] (the bins follow how the keys cluster), then by
+// direct comparison inside each bin -- a handful of records, none when a bin
+// holds one key value.  A bin denser than BS_BIN_BIG sends the chunk to a
+// block radix sort on the chunk's key bits.
 __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __restrict__ keys,
                                                            const uint32_t* __restrict__ vals,
                                                            const int64_t* __restrict__ chunk, int shift,
                                                            uint64_t* okeys, uint32_t* ovals, Stats* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BsSmem& S = *reinterpret_cast<BsSmem*>(smem_raw);
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t c = blockIdx.x;
   const int64_t s0 = chunk[4 * c + 0];
   if (s0 < 0) return;
@@ -90,77 +106,139 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
     if (t == 0) atomicAdd((unsigned long long*)&st->pad[3], 1ull);
     return;
   }
-  if (t == 0) S.big = 0;
+  {
+    int4* b4 = reinterpret_cast<int4*>(S.bins);
+    for (int i = t; i < BS_NB / 4; i += BK_THREADS) b4[i] = make_int4(0, 0, 0, 0);
+  }
+  uint64_t kmin = ~0ull, kmax = 0;
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
     if (idx < cnt) {
-      S.k[idx] = keys[s0 + idx] - base;
+      const uint64_t k = keys[s0 + idx] - base;
+      S.k[idx] = k;
       S.v[idx] = vals ? vals[s0 + idx] : 0u;
+      kmin = k < kmin ? k : kmin;
+      kmax = k > kmax ? k : kmax;
     }
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+    kmin = a < kmin ? a : kmin;
+    kmax = b > kmax ? b : kmax;
+  }
+  if (lane == 0) {
+    S.wmin[warp] = kmin;
+    S.wmax[warp] = kmax;
+  }
   __syncthreads();
-  // rank inside the bucket (a bucket is a run of equal k >> shift in k[])
-  bool big = false;
+#pragma unroll
+  for (int w = 0; w < BK_THREADS / 32; w++) {
+    kmin = S.wmin[w] < kmin ? S.wmin[w] : kmin;
+    kmax = S.wmax[w] > kmax ? S.wmax[w] : kmax;
+  }
+  const int rbits = cnt > 0 ? bits_for(kmax - kmin) : 0;
+  const int s2 = rbits > BS_LOG_NB ? rbits - BS_LOG_NB : 0;
+  uint32_t slot[BK_ITEMS / 2];  // two 16-bit slots per word
+#pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
-    if (idx >= cnt) break;
-    const uint64_t k = S.k[idx];
-    const uint64_t bk = k >> shift;
-    const bool left = idx > 0 && (S.k[idx - 1] >> shift) == bk;
-    const bool right = idx + 1 < cnt && (S.k[idx + 1] >> shift) == bk;
-    if (!left && !right) {
-      S.sk[idx] = k;
-      S.sv[idx] = S.v[idx];
-      continue;
-    }
-    int r = 0, q = idx - 1, steps = 0;
-    for (; q >= 0 && steps < BK_RANK_MAX && (S.k[q] >> shift) == bk; q--, steps++) r += S.k[q] <= k;
-    bool trunc = steps == BK_RANK_MAX && q >= 0 && (S.k[q] >> shift) == bk;
-    const int start = q + 1;
-    int q2 = idx + 1;
-    steps = 0;
-    for (; q2 < cnt && steps < BK_RANK_MAX && (S.k[q2] >> shift) == bk; q2++, steps++) r += S.k[q2] < k;
-    trunc |= steps == BK_RANK_MAX && q2 < cnt && (S.k[q2] >> shift) == bk;
-    big |= trunc;
-    if (trunc) continue;  // (a truncated rank is no position: the block sort below places this chunk)
-    S.sk[start + r] = k;
-    S.sv[start + r] = S.v[idx];
+    const uint32_t sl = idx < cnt ? (uint32_t)atomicAdd(&S.bins[(int)((S.k[idx] - kmin) >> s2)], 1) : 0u;
+    if (j & 1) slot[j >> 1] |= sl << 16;
+    else slot[j >> 1] = sl;
   }
-  if (big) S.big = 1;
   __syncthreads();
-  if (S.big) {  // a dense bucket: block radix sort of the whole chunk on lbits
-    using BRS = cub::BlockRadixSort<uint64_t, BK_THREADS, BK_ITEMS, uint32_t, 4>;
-    static_assert(sizeof(typename BRS::TempStorage) <= sizeof(S.k) + sizeof(S.v), "radix scratch");
-    uint64_t kk[BK_ITEMS];
-    uint32_t vv[BK_ITEMS];
+  bool big = false;
+  {
+    constexpr int BPT = BS_NB / BK_THREADS;
+    int v[BPT];
+    int4* b4 = reinterpret_cast<int4*>(S.bins + t * BPT);
 #pragma unroll
+    for (int q = 0; q < BPT / 4; q++) {
+      const int4 x = b4[q];
+      v[4 * q] = x.x;
+      v[4 * q + 1] = x.y;
+      v[4 * q + 2] = x.z;
+      v[4 * q + 3] = x.w;
+    }
+    int sum = 0;
+#pragma unroll
+    for (int q = 0; q < BPT; q++) {
+      big |= v[q] > BS_BIN_BIG;
+      const int x = v[q];
+      v[q] = sum;
+      sum += x;
+    }
+    int dummy;
+    const int pre = block_exclusive_fast(sum, BsIAdd(), 0, S.scan, &dummy);
+#pragma unroll
+    for (int q = 0; q < BPT / 4; q++)
+      b4[q] = make_int4(pre + v[4 * q], pre + v[4 * q + 1], pre + v[4 * q + 2], pre + v[4 * q + 3]);
+  }
+  big = __syncthreads_or(big) != 0;
+#pragma unroll
+  for (int j = 0; j < BK_ITEMS; j++) {
+    const int idx = j * BK_THREADS + t;
+    if (idx < cnt) {
+      const uint64_t k = S.k[idx];
+      const int at = S.bins[(int)((k - kmin) >> s2)] + (int)((slot[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+      S.sk[at] = k;
+      S.sv[at] = S.v[idx];
+    }
+  }
+  __syncthreads();
+  if (!big) {
+#pragma unroll 4
     for (int j = 0; j < BK_ITEMS; j++) {
-      const int idx = t * BK_ITEMS + j;  // blocked
-      kk[j] = idx < cnt ? S.k[idx] : ~0ull;
-      vv[j] = idx < cnt ? S.v[idx] : 0u;
+      const int i = j * BK_THREADS + t;
+      if (i >= cnt) break;
+      const uint64_t k = S.sk[i];
+      int at = i;
+      if (s2 > 0) {
+        const int b = (int)((k - kmin) >> s2);
+        const int bs = S.bins[b], be = b + 1 < BS_NB ? S.bins[b + 1] : cnt;
+        int r = 0;
+        for (int q = bs; q < be; q++) {
+          const uint64_t o = S.sk[q];
+          r += (o < k) | ((o == k) & (q < i));
+        }
+        at = bs + r;
+      }
+      S.k[at] = k;
+      S.v[at] = S.sv[i];
     }
     __syncthreads();
-    typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(S.k);
-    // padding (~0, blocked at the end) stays after equal real keys: the sort is stable
-    BRS(tmp).Sort(kk, vv, 0, lbits < 1 ? 1 : lbits);
-    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < BK_ITEMS; j++) {
-      const int idx = t * BK_ITEMS + j;
+    for (int j = 0; j < BK_ITEMS; j++) {  // coalesced write-back
+      const int idx = j * BK_THREADS + t;
       if (idx < cnt) {
-        S.sk[idx] = kk[j];
-        S.sv[idx] = vv[j];
+        okeys[s0 + idx] = base + S.k[idx];
+        if (ovals) ovals[s0 + idx] = S.v[idx];
       }
     }
-    __syncthreads();
+    return;
   }
+  // a dense bin: block radix sort of the whole chunk on lbits
+  using BRS = cub::BlockRadixSort<uint64_t, BK_THREADS, BK_ITEMS, uint32_t, 4>;
+  static_assert(sizeof(typename BRS::TempStorage) <= sizeof(S.k) + sizeof(S.v), "radix scratch");
+  uint64_t kk[BK_ITEMS];
+  uint32_t vv[BK_ITEMS];
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
-    const int idx = j * BK_THREADS + t;
+    const int idx = t * BK_ITEMS + j;  // blocked
+    kk[j] = idx < cnt ? S.sk[idx] : ~0ull;
+    vv[j] = idx < cnt ? S.sv[idx] : 0u;
+  }
+  typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(S.k);
+  // padding (~0, blocked at the end) stays after equal real keys: the sort is stable
+  BRS(tmp).Sort(kk, vv, 0, lbits < 1 ? 1 : lbits);
+#pragma unroll
+  for (int j = 0; j < BK_ITEMS; j++) {
+    const int idx = t * BK_ITEMS + j;
     if (idx < cnt) {
-      okeys[s0 + idx] = base + S.sk[idx];
-      if (ovals) ovals[s0 + idx] = S.sv[idx];
+      okeys[s0 + idx] = base + kk[j];
+      if (ovals) ovals[s0 + idx] = vv[j];
     }
   }
 }

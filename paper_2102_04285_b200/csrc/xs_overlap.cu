@@ -462,48 +462,56 @@ struct SwOp {
   }
 };
 
-// 7 signed 16-bit counters (the SwState counts c[0..6]) in two words:
-// a = c0 | c1 | c2 | c3, b = c4 | c5 | c6; added lane-wise without carries
-struct P7 {
-  unsigned long long a, b;
+// Packed endpoint counters.  Seven counters (categories 1..6 = lanes 0..5,
+// OPERATION endpoints = lane 6) as 16-bit lanes of two words, summed as
+// plain 64-bit integers: a sum of per-key deltas is the polynomial
+// sum c_i 2^(16 i), exact as long as every true lane value fits in
+// [-2^15, 2^15) -- a chunk holds <= BK_CAP keys, so chunk-local partial
+// counts always do.  Decoding propagates the borrows lane by lane.
+struct P2 {
+  unsigned long long a, b;  // lanes 0..3 | lanes 4..6
 };
-__device__ __forceinline__ unsigned long long swar16_add(unsigned long long x, unsigned long long y) {
-  constexpr unsigned long long H = 0x8000800080008000ull;
-  return ((x & ~H) + (y & ~H)) ^ ((x ^ y) & H);
-}
-struct P7Add {
-  __device__ P7 operator()(const P7& x, const P7& y) const { return P7{swar16_add(x.a, y.a), swar16_add(x.b, y.b)}; }
+struct IAdd {
+  __device__ int operator()(int x, int y) const { return x + y; }
 };
-__device__ __forceinline__ void p7_apply(P7& s, uint32_t code) {  // sw_apply on the packed lanes
+struct P2Add {
+  __device__ P2 operator()(const P2& x, const P2& y) const { return P2{x.a + y.a, x.b + y.b}; }
+};
+__device__ __forceinline__ void p2_apply(P2& s, uint32_t code) {
   const uint32_t cat = code & 7u;
-  if (cat == 7u) return;  // (no such code; sw_apply ignores it too)
-  const int lane = cat == 0 ? 6 : (int)cat - 1;
-  const unsigned short d = cat == 0 ? 1 : ((code & 8u) ? 0xFFFFu : 1u);
-  const unsigned long long dv = (unsigned long long)d << (16 * (lane & 3));
-  if (lane < 4) s.a = swar16_add(s.a, dv);
-  else s.b = swar16_add(s.b, dv);
+  const uint32_t lane = cat == 0 ? 6u : cat - 1u;
+  const unsigned long long one = 1ull << (16 * (lane & 3u));
+  const unsigned long long d = (cat != 0 && (code & 8u)) ? 0ull - one : one;  // (ops count both endpoints)
+  if (lane < 4) s.a += d;
+  else s.b += d;
 }
-__device__ __forceinline__ int p7_lane(const P7& s, int i) {
-  const unsigned long long w = i < 4 ? s.a : s.b;
-  return (int)(short)(unsigned short)(w >> (16 * (i & 3)));
-}
-
-__device__ __forceinline__ void sw_apply(SwState& s, uint32_t code) {
-  const uint32_t cat = code & 7u;
-  const int d = (code & 8u) ? -1 : 1;
+__device__ __forceinline__ void p2_decode(P2 s, int* c /*[7]*/) {
 #pragma unroll
-  for (int i = 0; i < 6; i++) s.c[i] += (cat == (uint32_t)(i + 1)) ? d : 0;
-  s.c[6] += cat == 0 ? 1 : 0;
+  for (int i = 0; i < 4; i++) {
+    const int v = (int)(short)(unsigned short)(s.a & 0xFFFFu);
+    c[i] = v;
+    s.a = (s.a - (unsigned long long)(long long)v) >> 16;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    const int v = (int)(short)(unsigned short)(s.b & 0xFFFFu);
+    c[4 + i] = v;
+    s.b = (s.b - (unsigned long long)(long long)v) >> 16;
+  }
 }
 
-
-// Shared-memory cell table with native 32-bit adds (a 64-bit shared atomicAdd
-// is a CAS loop on sm_100): value = hi:lo, the carry of each add goes to hi.
-__device__ __forceinline__ void smem_add64(unsigned* lo, unsigned* hi, unsigned long long v) {
-  const unsigned vl = (unsigned)v, vh = (unsigned)(v >> 32);
-  const unsigned old = atomicAdd(lo, vl);
-  const unsigned carry = (old + vl) < old ? 1u : 0u;
-  if (vh | carry) atomicAdd(hi, vh + carry);
+// Shared-memory cell table: every add is a length < 2^28 (an interval inside
+// one chunk, whose relative keys span < 2^32 = 2^28 ns), split into its low
+// 16 bits and the rest, each added to its own 32-bit counter without reading
+// it back (fire-and-forget RED; a 64-bit shared atomicAdd is a CAS loop on
+// sm_100).  A chunk makes <= BK_CAP adds per cell, so neither counter can
+// wrap: value = lo + (hi << 16).
+__device__ __forceinline__ void smem_add_split(unsigned* lo, unsigned* hi, unsigned v) {
+  atomicAdd(lo, v & 0xFFFFu);
+  if (v >> 16) atomicAdd(hi, v >> 16);
+}
+__device__ __forceinline__ unsigned long long split_value(unsigned lo, unsigned hi) {
+  return (unsigned long long)lo + ((unsigned long long)hi << 16);
 }
 
 template <int kHT>
@@ -511,7 +519,7 @@ struct CellTableT {  // open addressing in shared memory, spill to global
   unsigned long long* key;
   unsigned* lo;
   unsigned* hi;
-  __device__ void add(unsigned long long idx, unsigned long long v, const GHist& hist) {
+  __device__ __noinline__ void add(unsigned long long idx, unsigned v, const GHist& hist) {
     unsigned h = (unsigned)(mix64(idx) & (kHT - 1));
 #pragma unroll 1
     for (int probe = 0; probe < 16; probe++) {
@@ -521,7 +529,7 @@ struct CellTableT {  // open addressing in shared memory, spill to global
         k = prev == ~0ull ? idx : prev;
       }
       if (k == idx) {
-        smem_add64(&lo[h], &hi[h], v);
+        smem_add_split(&lo[h], &hi[h], v);
         return;
       }
       h = (h + 1) & (kHT - 1);
@@ -532,34 +540,32 @@ struct CellTableT {  // open addressing in shared memory, spill to global
 
 template <int kHT>
 struct BkSmemT {
-  uint32_t k[BK_CAP];       // chunk keys relative to the chunk base, bucket order (as scattered)
-  uint32_t sorted[BK_CAP];  // fully sorted (also block-radix-sort scratch together with k[])
-  unsigned long long h_key[kHT];
-  unsigned h_lo[kHT];
-  unsigned h_hi[kHT];
-  uint32_t last[BK_THREADS];
-  uint32_t head[BK_CAP / 32];  // bit i of word w: key 32w+i starts a bucket run (first key of its bucket)
-  SwState warp_agg[BK_THREADS / 32];
+  static constexpr int NBINS = 4 * kHT;  // local counting-sort bins: exactly the cell table's bytes
+  // chunk keys relative to the chunk base: load order, then fully sorted at
+  // bk_sw(position) (one pad word per 16: a thread's 16 consecutive items are
+  // conflict-free across the warp)
+  uint32_t k[BK_CAP + BK_CAP / 16];
+  uint32_t sorted[BK_CAP];  // keys grouped by local bin (also block-radix-sort scratch together with k[])
+  union {
+    struct {
+      unsigned long long h_key[kHT];
+      unsigned h_lo[kHT];
+      unsigned h_hi[kHT];
+    } t;
+    int bins[NBINS];  // counts, then exclusive starts (dead before the table is initialised)
+  } u;
+  P2 warp_p2[BK_THREADS / 32];
+  uint32_t wmin[BK_THREADS / 32], wmax[BK_THREADS / 32];
   SwState tile_pre;
-  int big;
+  SwState tile_agg;
 };
 
 // the shared cell table of the fused sweep: 1K slots (4 CTAs/SM) when a chunk's
 // cells index it directly, 4K slots (2 CTAs/SM) for many-path traces whose
 // cells must hash (deep recursive operations: fewer spills to the global table)
 constexpr int HT_SMALL = 1024, HT_BIG = 4096;
-
-struct SwMaxOp {  // chunk aggregate: counts add, last = max key (order independent)
-  __device__ SwState operator()(const SwState& a, const SwState& b) const {
-    SwState r;
-#pragma unroll
-    for (int i = 0; i < 8; i++) r.c[i] = a.c[i] + b.c[i];
-    r.last = a.last > b.last ? a.last : b.last;
-    r.has = a.has | b.has;
-    r.pad = 0;
-    return r;
-  }
-};
+constexpr int BK_BIN_BIG = 256;  // a local bin holding more keys sends the chunk to the block radix sort
+__device__ __forceinline__ int bk_sw(int p) { return p + (p >> 4); }
 
 __device__ __forceinline__ SwState sw_identity() {
   SwState id;
@@ -571,17 +577,21 @@ __device__ __forceinline__ SwState sw_identity() {
   return id;
 }
 
-// One CTA per chunk.  The chunk arrives grouped by fine bucket (scatter
-// order), keys stored 32-bit relative to the chunk's first bucket.  Keys are
-// ranked inside their bucket (singletons directly, small buckets by direct
-// comparison, a block radix sort if some bucket is large), then the sweep
-// runs on the sorted tile.  The chunk aggregate (counts, max key) does not
-// depend on order and is published before sorting, so the look-back chain
-// never waits on a sort.  Every interval [t_prev, t) is accounted by the first
-// endpoint of the run at t with the state after everything up to t_prev;
-// across chunk boundaries t_prev and that state come from the look-back.
+// One CTA per chunk (a contiguous key range, <= BK_CAP keys, arriving grouped
+// by global bucket).  The chunk is sorted in shared memory by one counting
+// pass over 4*kHT local bins spanning exactly [min key, max key] of the chunk
+// (so the bins adapt to how the keys cluster), then by direct comparison
+// inside each bin (a few keys; one bin per distinct key when the chunk's range
+// fits the bins).  The chunk aggregate (counts, max key) does not depend on
+// order and is published right after the load, so the look-back chain never
+// waits on a sort.  The walk keeps the six category counters as 8-bit lanes
+// of one word clamped to BK_ITEMS + 1 (a thread applies at most BK_ITEMS
+// endpoints, so "count > 0" is exact), the mask is a SWAR test, and every
+// interval [t_prev, t) is accounted by the first endpoint of the run at t
+// with the state after everything up to t_prev; across chunk boundaries
+// t_prev and that state come from the look-back.
 #ifndef XS_SWEEP_MINB
-#define XS_SWEEP_MINB 4  // 4 CTAs per SM (64 registers, small spills): more chunks in flight
+#define XS_SWEEP_MINB 4  // 4 CTAs per SM (64 registers): more chunks in flight
 #endif
 template <int kHT, int kMinB>
 __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
@@ -592,6 +602,10 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
   using BkSmem = BkSmemT<kHT>;
   using CellTable = CellTableT<kHT>;
   constexpr int HT = kHT;
+  constexpr int NB = BkSmem::NBINS;
+  constexpr int LOG_NB = kHT == 1024 ? 12 : 14;
+  static_assert((1 << LOG_NB) == NB, "bins");
+  constexpr int BPT = NB / BK_THREADS;  // bins per thread in the bin scan
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -599,117 +613,152 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
   // the paths actually interned fit the table (decided on the device: the
   // host only knows the trie's capacity without a sync)
   const int direct = direct_ok && trie_count && (int64_t)(*trie_count) * 32 <= kHT;
-  unsigned long long tstamp[8];
-#define XS_STAMP(i) if (ptrace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tstamp[i]));
-  XS_STAMP(0);
-  for (int i = t; i < HT; i += BK_THREADS) {
-    S.h_key[i] = ~0ull;
-    S.h_lo[i] = 0;
-    S.h_hi[i] = 0;
+  // developer timing: per-phase globaltimer stamps of every CTA (XS_TRACE_SWEEP)
+  unsigned long long ts0 = 0;
+  if (ptrace && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
+#define XS_STAMP(i)                                                  \
+  if (ptrace && t == 0) {                                            \
+    unsigned long long ts_;                                          \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_));          \
+    ptrace[c * 8 + (i)] = ts_;                                       \
   }
-  if (t == 0) S.big = 0;
-  CellTable T{S.h_key, S.h_lo, S.h_hi};
-  const int64_t c = next_tile(tile_ctr);  // (barrier inside)
+  {
+    int4* b4 = reinterpret_cast<int4*>(S.u.bins);
+    for (int i = t; i < NB / 4; i += BK_THREADS) b4[i] = make_int4(0, 0, 0, 0);
+  }
+  const int64_t c = next_tile(tile_ctr);  // (barrier inside: also orders the bin reset)
+  if (ptrace && t == 0) ptrace[c * 8] = ts0;
   XS_STAMP(1);
   const int64_t s0 = chunk[4 * c + 0];
   int cnt = s0 < 0 ? 0 : (int)(chunk[4 * c + 1] - s0);
   const int64_t b0 = chunk[4 * c + 2], b1 = chunk[4 * c + 3];
-  // base aligned to 16 (keeps the 4-bit endpoint code) and to 2^shift (keeps
-  // bucket grouping of the relative keys)
+  // base aligned to 16 (keeps the 4-bit endpoint code) and to 2^shift
   const uint64_t base = ((uint64_t)b0 << shift) & ~15ull;
   const int lbits = bits_for(((uint64_t)(b1 > b0 ? b1 : b0 + 1) << shift) - 1 - base);
   if (cnt > BK_CAP || (cnt > 0 && lbits > 32)) {  // host re-runs this call through the LSD path
     if (t == 0) atomicAdd((unsigned long long*)&st->pad[3], 1ull);
     cnt = 0;
   }
-  // 1. load (striped, coalesced) + order-independent aggregate; lane i of
-  // warp w holds key j*BK_THREADS + 32w + i, so one ballot per item gives a
-  // word of the run-head bitmap (a key whose bucket differs from its left
-  // neighbour's starts a run; neighbours across words come from a shuffle)
-  SwState agg = sw_identity();
-  uint32_t kmax = 0;
+  // 1. load (striped, coalesced) + the order-independent chunk aggregate
+  P2 agg{0ull, 0ull};
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
-    uint32_t kr = 0;
     if (idx < cnt) {
-      const uint64_t k = keys[s0 + idx];
-      kr = (uint32_t)(k - base);
+      const uint32_t kr = (uint32_t)(keys[s0 + idx] - base);
       S.k[idx] = kr;
-      sw_apply(agg, kr & 15u);
+      p2_apply(agg, kr);
+      kmin = kr < kmin ? kr : kmin;
       kmax = kr > kmax ? kr : kmax;
-      agg.has = 1;
     }
-    const uint32_t left = __shfl_up_sync(0xffffffffu, kr, 1);
-    bool hd = idx < cnt && (lane == 0 || (left >> shift) != (kr >> shift));
-    const unsigned bits = __ballot_sync(0xffffffffu, hd);
-    if (lane == 0) S.head[idx >> 5] = bits;  // (bit 0 is provisional: fixed below against the previous word)
   }
-  // chunk aggregate: warp reductions in hardware (redux.sync), then 8 warps
-  {
-    SwState w;
 #pragma unroll
-    for (int i = 0; i < 8; i++) w.c[i] = __reduce_add_sync(0xffffffffu, agg.c[i]);
-    const unsigned wmax = __reduce_max_sync(0xffffffffu, kmax);
-    w.has = __any_sync(0xffffffffu, agg.has);
-    w.last = base + wmax;
-    w.pad = 0;
-    if (lane == 0) S.warp_agg[warp] = w;
+  for (int o = 16; o; o >>= 1) {
+    agg.a += __shfl_xor_sync(0xffffffffu, agg.a, o);
+    agg.b += __shfl_xor_sync(0xffffffffu, agg.b, o);
+  }
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (lane == 0) {
+    S.warp_p2[warp] = agg;
+    S.wmin[warp] = kmin;
+    S.wmax[warp] = kmax;
   }
   __syncthreads();
-  SwState tile_agg = sw_identity();
-  if (warp == 0) {
-    const SwState w = lane < BK_THREADS / 32 ? S.warp_agg[lane] : sw_identity();
 #pragma unroll
-    for (int i = 0; i < 8; i++) tile_agg.c[i] = __reduce_add_sync(0xffffffffu, w.c[i]);
-    const unsigned rel = lane < BK_THREADS / 32 && w.has ? (unsigned)(w.last - base) : 0u;
-    tile_agg.last = base + __reduce_max_sync(0xffffffffu, rel);
-    tile_agg.has = __any_sync(0xffffffffu, w.has);
-    if (lane == 0) tile_publish_agg((int)c, tile_agg, desc, flags);
+  for (int w = 0; w < BK_THREADS / 32; w++) {
+    kmin = S.wmin[w] < kmin ? S.wmin[w] : kmin;
+    kmax = S.wmax[w] > kmax ? S.wmax[w] : kmax;
+  }
+  if (warp == 0) {
+    SwState tile_agg = sw_identity();
+    P2 ta{0ull, 0ull};
+#pragma unroll
+    for (int w = 0; w < BK_THREADS / 32; w++) ta = P2Add()(ta, S.warp_p2[w]);
+    int cc[7];
+    p2_decode(ta, cc);
+#pragma unroll
+    for (int i = 0; i < 7; i++) tile_agg.c[i] = cc[i];
+    tile_agg.has = cnt > 0;
+    tile_agg.last = cnt > 0 ? base + kmax : 0;
+    if (lane == 0) {
+      tile_publish_agg((int)c, tile_agg, desc, flags);
+      S.tile_agg = tile_agg;  // (kept for the look-back: not live in registers through the sort)
+    }
   }
   XS_STAMP(2);
-  // 2. rank inside buckets (a bucket is the run of equal k >> shift in k[]):
-  // run bounds from the head bitmap (clz / ffs on one or two words), then one
-  // compare per run member -- O(run length), no per-step bucket test
-  __syncthreads();
-  for (int w = t; w < (cnt + 31) >> 5; w += BK_THREADS)  // bit 0: against the last key of the previous word
-    if (w > 0 && (S.k[32 * w] >> shift) == (S.k[32 * w - 1] >> shift)) atomicAnd(&S.head[w], ~1u);
-  if (t == 0 && cnt > 0) atomicOr(&S.head[0], 1u);
-  __syncthreads();
-  bool big = false;
-#pragma unroll 2
+  // 2. counting pass over the local bins (kr - kmin) >> s2
+  const int rbits = cnt > 0 ? bits_for((uint64_t)(kmax - kmin)) : 0;
+  const int s2 = rbits > LOG_NB ? rbits - LOG_NB : 0;
+  uint32_t slot[BK_ITEMS / 2];  // two 16-bit slots per word (a slot is < BK_CAP)
+#pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
-    if (idx >= cnt) break;
-    const uint32_t k = S.k[idx];
-    // run start: last head <= idx
-    int w = idx >> 5;
-    unsigned m = S.head[w] & (0xffffffffu >> (31 - (idx & 31)));
-    while (!m) m = S.head[--w];
-    const int rs = 32 * w + 31 - __clz(m);
-    // run end: first head > idx (or cnt)
-    w = idx >> 5;
-    m = (idx & 31) == 31 ? 0u : S.head[w] & (0xfffffffeu << (idx & 31));
-    while (!m && 32 * (w + 1) < cnt) m = S.head[++w];
-    const int re = m ? min(32 * w + __ffs(m) - 1, cnt) : cnt;
-    if (re - rs == 1) {
-      S.sorted[idx] = k;
-      continue;
-    }
-    if (re - rs > 2 * BK_RANK_MAX) {
-      big = true;
-      continue;
-    }
-    int r = 0;
-    for (int q = rs; q < re; q++) {
-      const uint32_t o = S.k[q];
-      r += (o < k) | ((o == k) & (q < idx));
-    }
-    S.sorted[rs + r] = k;
+    const uint32_t sl = idx < cnt ? (uint32_t)atomicAdd(&S.u.bins[(S.k[idx] - kmin) >> s2], 1) : 0u;
+    if (j & 1) slot[j >> 1] |= sl << 16;
+    else slot[j >> 1] = sl;
   }
-  if (big) S.big = 1;
   __syncthreads();
-  if (S.big) {  // a dense bucket: block radix sort of the whole chunk on lbits
+  bool big = false;
+  {  // exclusive bin starts: BPT consecutive bins per thread + a block scan
+    int v[BPT];
+    int4* b4 = reinterpret_cast<int4*>(S.u.bins + t * BPT);
+#pragma unroll
+    for (int q = 0; q < BPT / 4; q++) {
+      const int4 x = b4[q];
+      v[4 * q] = x.x;
+      v[4 * q + 1] = x.y;
+      v[4 * q + 2] = x.z;
+      v[4 * q + 3] = x.w;
+    }
+    int sum = 0;
+#pragma unroll
+    for (int q = 0; q < BPT; q++) {
+      big |= v[q] > BK_BIN_BIG;
+      const int x = v[q];
+      v[q] = sum;
+      sum += x;
+    }
+    int dummy;
+    const int pre = block_exclusive_fast(sum, IAdd(), 0, reinterpret_cast<int*>(S.warp_p2), &dummy);
+#pragma unroll
+    for (int q = 0; q < BPT / 4; q++) b4[q] = make_int4(pre + v[4 * q], pre + v[4 * q + 1], pre + v[4 * q + 2], pre + v[4 * q + 3]);
+  }
+  big = __syncthreads_or(big) != 0;
+  // scatter into bin order
+#pragma unroll
+  for (int j = 0; j < BK_ITEMS; j++) {
+    const int idx = j * BK_THREADS + t;
+    if (idx < cnt) {
+      const uint32_t kr = S.k[idx];
+      S.sorted[S.u.bins[(kr - kmin) >> s2] + ((slot[j >> 1] >> (16 * (j & 1))) & 0xFFFFu)] = kr;
+    }
+  }
+  __syncthreads();
+  XS_STAMP(3);
+  if (!big) {
+    // 3. order inside each bin: a bin of one key value (s2 == 0) is already
+    // in place; otherwise rank by direct comparison (ties by position)
+#pragma unroll 4
+    for (int j = 0; j < BK_ITEMS; j++) {
+      const int i = j * BK_THREADS + t;
+      if (i >= cnt) break;
+      const uint32_t k = S.sorted[i];
+      if (s2 == 0) {
+        S.k[bk_sw(i)] = k;
+        continue;
+      }
+      const int b = (int)((k - kmin) >> s2);
+      const int bs = S.u.bins[b], be = b + 1 < NB ? S.u.bins[b + 1] : cnt;
+      int r = 0;
+      for (int q = bs; q < be; q++) {
+        const uint32_t o = S.sorted[q];
+        r += (o < k) | ((o == k) & (q < i));
+      }
+      S.k[bk_sw(bs + r)] = k;
+    }
+  } else {  // a dense bin: block radix sort of the whole chunk on lbits
     using BRS = cub::BlockRadixSort<uint32_t, BK_THREADS, BK_ITEMS, cub::NullType, 4>;
     static_assert(sizeof(typename BRS::TempStorage) <= 2 * sizeof(uint32_t) * BK_CAP, "radix scratch");
     typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(S.k);
@@ -717,7 +766,7 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
 #pragma unroll
     for (int j = 0; j < BK_ITEMS; j++) {
       const int idx = j * BK_THREADS + t;
-      kk[j] = idx < cnt ? S.k[idx] : 0xFFFFFFFFu;
+      kk[j] = idx < cnt ? S.sorted[idx] : 0xFFFFFFFFu;
     }
     __syncthreads();
     BRS(tmp).Sort(kk, 0, lbits < 1 ? 1 : lbits);
@@ -725,161 +774,202 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
 #pragma unroll
     for (int j = 0; j < BK_ITEMS; j++) {
       const int idx = t * BK_ITEMS + j;  // blocked output
-      if (idx < cnt) S.sorted[idx] = kk[j];
+      if (idx < cnt) S.k[bk_sw(idx)] = kk[j];
     }
   }
   __syncthreads();
-  XS_STAMP(3);
-  // 3. thread prefix over the sorted (blocked) items + chunk prefix.  Inside
-  // a chunk every partial count is bounded by the chunk size (|x| <= 4096),
-  // so the block scan runs on 7 signed 16-bit lanes packed in two 64-bit
-  // words (lane-wise SWAR adds: 2 shuffles per step instead of 12); only the
-  // chunk prefix from the look-back is a full 32-bit state.
-  uint32_t kb[BK_ITEMS];
-  const int my0 = t * BK_ITEMS;
-  uint32_t tlast = 0;
-  P7 ta{0ull, 0ull};
-#pragma unroll
-  for (int j = 0; j < BK_ITEMS; j++) {
-    kb[j] = my0 + j < cnt ? S.sorted[my0 + j] : 0;
-    if (my0 + j < cnt) {
-      p7_apply(ta, kb[j] & 15u);
-      tlast = kb[j];
-    }
+  // the cell table takes over the bins' bytes
+  for (int i = t; i < HT; i += BK_THREADS) {
+    S.u.t.h_key[i] = ~0ull;
+    S.u.t.h_lo[i] = 0;
+    S.u.t.h_hi[i] = 0;
   }
-  S.last[t] = tlast;
-  P7 dummy;
-  const P7 excl = block_exclusive_fast(ta, P7Add(), P7{0ull, 0ull}, reinterpret_cast<P7*>(S.warp_agg), &dummy);
+  XS_STAMP(4);
+  // 4. thread prefix over this thread's sorted items + chunk prefix
+  const int my0 = t * BK_ITEMS;
+  const int nmine = cnt - my0 < 0 ? 0 : (cnt - my0 > BK_ITEMS ? BK_ITEMS : cnt - my0);
+  const uint32_t* mine = S.k + bk_sw(my0);  // (a thread's items never straddle a pad word)
+  P2 ta{0ull, 0ull};
+#pragma unroll 4
+  for (int j = 0; j < nmine; j++) p2_apply(ta, mine[j]);
+  P2 dummy;
+  const P2 excl = block_exclusive_fast(ta, P2Add(), P2{0ull, 0ull}, S.warp_p2, &dummy);
   if (warp == 0) {
-    SwState pre = tile_lookback_published((int)c, tile_agg, desc, flags, SwOp(), sw_identity());
+    SwState pre = tile_lookback_published((int)c, S.tile_agg, desc, flags, SwOp(), sw_identity());
     if (lane == 0) S.tile_pre = pre;
   }
   __syncthreads();
-  XS_STAMP(4);
-  SwState cur = S.tile_pre;
+  XS_STAMP(5);
+  int ex[7];
+  p2_decode(excl, ex);
+  // six category counters as 8-bit lanes, clamped (exact for "> 0" over this
+  // thread's <= BK_ITEMS endpoints); OPERATION endpoints counted exactly
+  unsigned long long x = 0;
 #pragma unroll
-  for (int i = 0; i < 7; i++) cur.c[i] += p7_lane(excl, i);
-  uint64_t prev = 0;
-  bool have_prev = false;
-  if (t == 0) {
-    have_prev = S.tile_pre.has;
-    prev = S.tile_pre.last;
-  } else if (my0 < cnt) {
-    have_prev = true;
-    prev = base + S.last[t - 1];
+  for (int i = 0; i < 6; i++) {
+    const int v = S.tile_pre.c[i] + ex[i];
+    x |= (unsigned long long)(v < BK_ITEMS + 1 ? v : BK_ITEMS + 1) << (8 * i);
   }
-  // 4. the sweep over this thread's items
+  int64_t oc = (int64_t)S.tile_pre.c[6] + ex[6];
+  // 5. the sweep over this thread's items
   const uint64_t tmask = (1ull << tb) - 1;
   const int pshift = tb + 4;
-  // cells: every lane merges runs of consecutive equal cells in registers;
-  // a finished run goes to the block table: direct-indexed shared counters
-  // (cell - pid base) when the chunk holds one pid and its paths fit the
-  // table, else the shared hash (CellTable) -- no probing, no CAS on the
-  // direct path.
-  const unsigned long long pbase = (unsigned long long)(base >> pshift) * (unsigned long long)n_nodes * 32ull;
-  unsigned long long run_k = ~0ull, run_v = 0;
-  auto add_cell = [&](unsigned long long key, unsigned long long v) {
-    if (direct) smem_add64(&S.h_lo[key - pbase], &S.h_hi[key - pbase], v);
-    else T.add(key, v, hist);
+  constexpr unsigned long long L7F = 0x7F7F7F7F7F7Full, H6 = 0x808080808080ull, H5 = 0x8080808080ull;
+  // lanes 0..4 of a positive-lane word -> mask bits 0..4 (bit 8i lands on 28 + i)
+  auto mask_of = [](unsigned long long m5) -> unsigned { return (unsigned)((((m5 >> 7) * 0x10204081ull) >> 28) & 31u); };
+  auto apply = [&](uint32_t code) {
+    const uint32_t cat = code & 7u;
+    if (cat == 0) {
+      oc++;
+    } else {
+      const unsigned long long one = 1ull << (8 * (cat - 1));
+      x = (code & 8u) ? x - one : x + one;
+    }
   };
-  int tr_pid = -1;
-  long long tr_len[1] = {0};
-  int c_pid = -1;
-  int64_t c_ob = 0, c_oc = -1;
-  int c_path = 0;
   // path of the op count oc is pidpath[oc - 1]; consecutive op endpoints read
   // consecutive entries, so the entry after the current one is loaded one op
   // endpoint ahead (its latency hides behind the keys in between)
-  int64_t pf_oc = cur.c[6];
+  int64_t pf_oc = oc;
   int pf_cur = 0, pf_nxt = 0;
-  if (pidpath && my0 < cnt) {
+  if (pidpath && nmine > 0) {
     pf_cur = pf_oc >= 1 ? pidpath[pf_oc - 1] : 0;
     pf_nxt = pidpath[pf_oc];  // (allocated 2m + 2: in bounds even past the last endpoint)
   }
-#pragma unroll
-  for (int j = 0; j < BK_ITEMS; j++) {
-    const bool in = my0 + j < cnt;  // (no early exit: the warp steps together)
-    const uint64_t k = base + kb[j];
-    bool fin = false;
-    unsigned long long fin_k = 0, fin_v = 0;
-    if (in && have_prev && (prev >> 4) != (k >> 4) && (prev >> pshift) == (k >> pshift)) {
-      const unsigned long long len = ((k >> 4) & tmask) - ((prev >> 4) & tmask);
-      const int p = (int)(k >> pshift);
-      unsigned mask = 0;
-#pragma unroll
-      for (int q = 0; q < 5; q++) mask |= (cur.c[q] > 0 ? 1u : 0u) << q;
-      if (mask || cur.c[5] > 0) {
-        if (p != tr_pid) {
-          if (tr_pid >= 0 && tr_len[0]) add_cell((unsigned long long)tr_pid * n_nodes * 32ull, (unsigned long long)tr_len[0]);
-          tr_pid = p;
-          tr_len[0] = 0;
-        }
-        tr_len[0] += (long long)len;
-      }
-      if (mask) {
-        if (p != c_pid) {  // op count base of the pid, cached
-          c_pid = p;
-          c_ob = opbase[p];
-          c_oc = -1;
-        }
-        const int64_t oc = cur.c[6];
-        if (oc != c_oc) {  // the path only changes at OPERATION endpoints
-          c_oc = oc;
-          int val;
-          if (oc == pf_oc) {
-            val = pf_cur;
-          } else if (oc == pf_oc + 1) {
-            val = pf_cur = pf_nxt;
-            pf_oc = oc;
-            pf_nxt = pidpath[oc];
-          } else {
-            val = oc >= 1 ? pidpath[oc - 1] : 0;
-            pf_oc = oc;
-            pf_cur = val;
-            pf_nxt = pidpath[oc];
-          }
-          c_path = oc > c_ob ? val : 0;
-        }
-        const unsigned long long key = ((unsigned long long)p * n_nodes + (unsigned long long)c_path) * 32ull + mask;
-        if (key == run_k) {
-          run_v += len;
-        } else {
-          fin = run_k != ~0ull;
-          fin_k = run_k;
-          fin_v = run_v;
-          run_k = key;
-          run_v = len;
+  auto path_at = [&](int64_t o) -> int {
+    if (o == pf_oc) return pf_cur;
+    if (o == pf_oc + 1) {
+      pf_cur = pf_nxt;
+    } else {
+      pf_cur = o >= 1 ? pidpath[o - 1] : 0;
+    }
+    pf_oc = o;
+    pf_nxt = pidpath[o];
+    return pf_cur;
+  };
+  CellTable T{S.u.t.h_key, S.u.t.h_lo, S.u.t.h_hi};
+  const uint64_t first_pid = (base + kmin) >> pshift;
+  const bool single = cnt > 0 && first_pid == ((base + kmax) >> pshift);  // (block-uniform)
+  const unsigned long long pbase = first_pid * (unsigned long long)n_nodes * 32ull;
+  if (single) {
+    const int p = (int)first_pid;
+    const int64_t ob = opbase[p];
+    // the interval from the previous chunk's last endpoint (thread 0's first
+    // item) can be longer than 2^28: straight to the global histogram
+    if (t == 0 && nmine > 0 && S.tile_pre.has) {
+      const uint64_t prev = S.tile_pre.last, k = base + mine[0];
+      if ((prev >> pshift) == (uint64_t)p && (prev >> 4) != (k >> 4)) {
+        const unsigned long long pos = (x + L7F) & H6;
+        if (pos) {
+          const unsigned long long len = ((k >> 4) & tmask) - ((prev >> 4) & tmask);
+          hist.add(pbase, len);
+          const unsigned long long m5 = pos & H5;
+          if (m5) hist.add(pbase + (unsigned long long)(oc > ob ? path_at(oc) : 0) * 32ull + mask_of(m5), len);
         }
       }
     }
-    if (in) {
-      sw_apply(cur, (uint32_t)(k & 15u));
+    // everything else: 32-bit times relative to the chunk base
+    uint32_t tprev = t > 0 && nmine > 0 ? S.k[bk_sw(my0 - 1)] >> 4 : 0;
+    bool hp = t > 0;
+    unsigned tracked = 0;
+    int64_t c_oc = -1;
+    unsigned c_cell = 0;
+    unsigned run_k = ~0u, run_v = 0;
+    auto flush_run = [&](unsigned key, unsigned v) {
+      if (direct) smem_add_split(&S.u.t.h_lo[key], &S.u.t.h_hi[key], v);
+      else T.add(pbase + key, v, hist);
+    };
+#pragma unroll 4
+    for (int j = 0; j < nmine; j++) {
+      const uint32_t kr = mine[j], tr = kr >> 4;
+      if (hp && tr != tprev) {
+        const unsigned long long pos = (x + L7F) & H6;
+        if (pos) {
+          const unsigned len = tr - tprev;
+          tracked += len;
+          const unsigned long long m5 = pos & H5;
+          if (m5) {
+            if (oc != c_oc) {  // the path only changes at OPERATION endpoints
+              c_oc = oc;
+              c_cell = (unsigned)(oc > ob ? path_at(oc) : 0) * 32u;
+            }
+            const unsigned key = c_cell + mask_of(m5);
+            if (key == run_k) {
+              run_v += len;
+            } else {
+              if (run_k != ~0u) flush_run(run_k, run_v);
+              run_k = key;
+              run_v = len;
+            }
+          }
+        }
+      }
+      apply(kr);
+      tprev = tr;
+      hp = true;
+    }
+    XS_STAMP(6);
+    if (run_k != ~0u) flush_run(run_k, run_v);
+    // tracked time: one per chunk (cell 0 of the pid = path 0, mask 0)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tracked += __shfl_xor_sync(0xffffffffu, tracked, o);
+    if (lane == 0 && tracked) flush_run(0u, tracked);
+  } else {
+    // chunks holding several pids (traces with more pids than buckets):
+    // 64-bit keys, every cell through the hashed table
+    uint64_t prev = 0;
+    bool have_prev = false;
+    if (t == 0) {
+      have_prev = S.tile_pre.has;
+      prev = S.tile_pre.last;
+    } else if (nmine > 0) {
+      have_prev = true;
+      prev = base + S.k[bk_sw(my0 - 1)];
+    }
+    int c_pid = -1;
+    int64_t c_ob = 0, c_oc = -1;
+    unsigned long long c_cell = 0;
+#pragma unroll 1
+    for (int j = 0; j < nmine; j++) {
+      const uint64_t k = base + mine[j];
+      if (have_prev && (prev >> 4) != (k >> 4) && (prev >> pshift) == (k >> pshift)) {
+        const unsigned long long pos = (x + L7F) & H6;
+        if (pos) {
+          const unsigned long long len = ((k >> 4) & tmask) - ((prev >> 4) & tmask);
+          const int p = (int)(k >> pshift);
+          const unsigned long long pb = (unsigned long long)p * n_nodes * 32ull;
+          hist.add(pb, len);  // (rare path: no run merging)
+          const unsigned long long m5 = pos & H5;
+          if (m5) {
+            if (p != c_pid) {
+              c_pid = p;
+              c_ob = opbase[p];
+              c_oc = -1;
+            }
+            if (oc != c_oc) {
+              c_oc = oc;
+              c_cell = pb + (unsigned long long)(oc > c_ob ? path_at(oc) : 0) * 32ull;
+            }
+            hist.add(c_cell + mask_of(m5), len);
+          }
+        }
+      }
+      apply(mine[j]);
       prev = k;
       have_prev = true;
     }
-    if (fin) add_cell(fin_k, fin_v);
+    XS_STAMP(6);
   }
-  XS_STAMP(5);
-  if (run_k != ~0ull) add_cell(run_k, run_v);
-  block_keyed_flush<1>(tr_pid, tr_len, [&](int p, const long long* x) {
-    if (x[0]) add_cell((unsigned long long)p * n_nodes * 32ull, (unsigned long long)x[0]);
-  });
   __syncthreads();
-  XS_STAMP(6);
   for (int i = t; i < HT; i += BK_THREADS) {
-    const unsigned long long v = ((unsigned long long)S.h_hi[i] << 32) | S.h_lo[i];
+    const unsigned long long v = split_value(S.u.t.h_lo[i], S.u.t.h_hi[i]);
     if (direct) {
       if (v) hist.add(pbase + (unsigned long long)i, v);
     } else {
-      const unsigned long long key = S.h_key[i];
+      const unsigned long long key = S.u.t.h_key[i];
       if (key != ~0ull) hist.add(key, v);
     }
   }
-  __syncthreads();
   XS_STAMP(7);
-  if (ptrace && t == 0) {
-    for (int i = 0; i < 8; i++) ptrace[c * 8 + i] = tstamp[i];
-  }
 #undef XS_STAMP
 }
 
@@ -1011,8 +1101,8 @@ static int bucket_sweep(xs_ctx* ctx, const EventView& v, const BkPlan& plan, int
       t1 = std::max(t1, h[c * 8 + 7]);
       for (int i = 0; i < 7; i++) ph[i] += (double)(h[c * 8 + i + 1] - h[c * 8 + i]);
     }
-    fprintf(stderr, "k_bk_sweep trace: chunks %lld span %.1f us; avg per CTA (us): tile %.2f load+pub %.2f rank %.2f "
-            "scan+lookback %.2f walk %.2f flush %.2f table %.2f\n", (long long)n_chunks, (t1 - t0) / 1e3,
+    fprintf(stderr, "k_bk_sweep trace: chunks %lld span %.1f us; avg per CTA (us): tile %.2f load+pub %.2f bins %.2f "
+            "rank %.2f scan+lookback %.2f walk %.2f flush+table %.2f\n", (long long)n_chunks, (t1 - t0) / 1e3,
             ph[0] / n_chunks / 1e3, ph[1] / n_chunks / 1e3, ph[2] / n_chunks / 1e3, ph[3] / n_chunks / 1e3,
             ph[4] / n_chunks / 1e3, ph[5] / n_chunks / 1e3, ph[6] / n_chunks / 1e3);
   }
