@@ -65,7 +65,8 @@ __global__ void k_bs_tail(const uint64_t* __restrict__ keys, const uint32_t* __r
   }
 }
 
-constexpr int BS_NB = 4096, BS_LOG_NB = 12;  // local counting-sort bins per chunk
+constexpr int BS_NBW = 4096;                     // words of local counting-sort bins per chunk
+constexpr int BS_NB = 2 * BS_NBW, BS_LOG_NB = 13;  // 16-bit bins (a count or start is <= BK_CAP)
 constexpr int BS_BIN_BIG = 256;                // a bin holding more records sends the chunk to the block radix sort
 
 struct BsSmem {
@@ -73,7 +74,7 @@ struct BsSmem {
   uint32_t v[BK_CAP];
   uint64_t sk[BK_CAP];  // grouped by local bin
   uint32_t sv[BK_CAP];
-  int bins[BS_NB];  // counts, then exclusive starts
+  unsigned bins[BS_NBW];  // 16-bit counts, then exclusive starts
   uint64_t wmin[BK_THREADS / 32], wmax[BK_THREADS / 32];
   int scan[32];
 };
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
   }
   {
     int4* b4 = reinterpret_cast<int4*>(S.bins);
-    for (int i = t; i < BS_NB / 4; i += BK_THREADS) b4[i] = make_int4(0, 0, 0, 0);
+    for (int i = t; i < BS_NBW / 4; i += BK_THREADS) b4[i] = make_int4(0, 0, 0, 0);
   }
   uint64_t kmin = ~0ull, kmax = 0;
 #pragma unroll
@@ -144,37 +145,42 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
-    const uint32_t sl = idx < cnt ? (uint32_t)atomicAdd(&S.bins[(int)((S.k[idx] - kmin) >> s2)], 1) : 0u;
+    uint32_t sl = 0;
+    if (idx < cnt) {
+      const uint32_t b = (uint32_t)((S.k[idx] - kmin) >> s2), h = 16 * (b & 1);
+      sl = (atomicAdd(&S.bins[b >> 1], 1u << h) >> h) & 0xFFFFu;
+    }
     if (j & 1) slot[j >> 1] |= sl << 16;
     else slot[j >> 1] = sl;
   }
   __syncthreads();
   bool big = false;
-  {
-    constexpr int BPT = BS_NB / BK_THREADS;
-    int v[BPT];
-    int4* b4 = reinterpret_cast<int4*>(S.bins + t * BPT);
+  {  // exclusive bin starts: 2 * WPT consecutive bins per thread + a block scan
+    constexpr int WPT = BS_NBW / BK_THREADS;
+    unsigned w[WPT];
+    uint4* b4 = reinterpret_cast<uint4*>(S.bins + t * WPT);
 #pragma unroll
-    for (int q = 0; q < BPT / 4; q++) {
-      const int4 x = b4[q];
-      v[4 * q] = x.x;
-      v[4 * q + 1] = x.y;
-      v[4 * q + 2] = x.z;
-      v[4 * q + 3] = x.w;
+    for (int q = 0; q < WPT / 4; q++) {
+      const uint4 x = b4[q];
+      w[4 * q] = x.x;
+      w[4 * q + 1] = x.y;
+      w[4 * q + 2] = x.z;
+      w[4 * q + 3] = x.w;
     }
     int sum = 0;
 #pragma unroll
-    for (int q = 0; q < BPT; q++) {
-      big |= v[q] > BS_BIN_BIG;
-      const int x = v[q];
-      v[q] = sum;
-      sum += x;
+    for (int q = 0; q < WPT; q++) {
+      const unsigned lo = w[q] & 0xFFFFu, hi = w[q] >> 16;
+      big |= lo > BS_BIN_BIG || hi > BS_BIN_BIG;
+      w[q] = (unsigned)sum | ((unsigned)(sum + lo) << 16);
+      sum += lo + hi;
     }
     int dummy;
     const int pre = block_exclusive_fast(sum, BsIAdd(), 0, S.scan, &dummy);
+    const unsigned pp = (unsigned)pre | ((unsigned)pre << 16);
 #pragma unroll
-    for (int q = 0; q < BPT / 4; q++)
-      b4[q] = make_int4(pre + v[4 * q], pre + v[4 * q + 1], pre + v[4 * q + 2], pre + v[4 * q + 3]);
+    for (int q = 0; q < WPT / 4; q++)
+      b4[q] = make_uint4(w[4 * q] + pp, w[4 * q + 1] + pp, w[4 * q + 2] + pp, w[4 * q + 3] + pp);
   }
   big = __syncthreads_or(big) != 0;
 #pragma unroll
@@ -182,7 +188,8 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
     const int idx = j * BK_THREADS + t;
     if (idx < cnt) {
       const uint64_t k = S.k[idx];
-      const int at = S.bins[(int)((k - kmin) >> s2)] + (int)((slot[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+      const uint32_t b = (uint32_t)((k - kmin) >> s2);
+      const int at = (int)((S.bins[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) + (int)((slot[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
       S.sk[at] = k;
       S.sv[at] = S.v[idx];
     }
@@ -197,7 +204,8 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
       int at = i;
       if (s2 > 0) {
         const int b = (int)((k - kmin) >> s2);
-        const int bs = S.bins[b], be = b + 1 < BS_NB ? S.bins[b + 1] : cnt;
+        const int bs = (int)((S.bins[b >> 1] >> (16 * (b & 1))) & 0xFFFFu);
+        const int be = b + 1 < BS_NB ? (int)((S.bins[(b + 1) >> 1] >> (16 * ((b + 1) & 1))) & 0xFFFFu) : cnt;
         int r = 0;
         for (int q = bs; q < be; q++) {
           const uint64_t o = S.sk[q];

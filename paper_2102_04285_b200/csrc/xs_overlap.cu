@@ -540,7 +540,8 @@ struct CellTableT {  // open addressing in shared memory, spill to global
 
 template <int kHT>
 struct BkSmemT {
-  static constexpr int NBINS = 4 * kHT;  // local counting-sort bins: exactly the cell table's bytes
+  static constexpr int NBW = 4 * kHT;     // words of local counting-sort bins: exactly the cell table's bytes
+  static constexpr int NBINS = 2 * NBW;  // 16-bit bins (a count or start is <= BK_CAP)
   // chunk keys relative to the chunk base: load order, then fully sorted at
   // bk_sw(position) (one pad word per 16: a thread's 16 consecutive items are
   // conflict-free across the warp)
@@ -552,7 +553,7 @@ struct BkSmemT {
       unsigned h_lo[kHT];
       unsigned h_hi[kHT];
     } t;
-    int bins[NBINS];  // counts, then exclusive starts (dead before the table is initialised)
+    unsigned bins[NBW];  // 16-bit counts, then exclusive starts (dead before the table is initialised)
   } u;
   P2 warp_p2[BK_THREADS / 32];
   uint32_t wmin[BK_THREADS / 32], wmax[BK_THREADS / 32];
@@ -603,9 +604,10 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
   using CellTable = CellTableT<kHT>;
   constexpr int HT = kHT;
   constexpr int NB = BkSmem::NBINS;
-  constexpr int LOG_NB = kHT == 1024 ? 12 : 14;
+  constexpr int NBW = BkSmem::NBW;
+  constexpr int LOG_NB = kHT == 1024 ? 13 : 15;
   static_assert((1 << LOG_NB) == NB, "bins");
-  constexpr int BPT = NB / BK_THREADS;  // bins per thread in the bin scan
+  constexpr int WPT = NBW / BK_THREADS;  // bin words per thread in the bin scan
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -624,7 +626,7 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
   }
   {
     int4* b4 = reinterpret_cast<int4*>(S.u.bins);
-    for (int i = t; i < NB / 4; i += BK_THREADS) b4[i] = make_int4(0, 0, 0, 0);
+    for (int i = t; i < NBW / 4; i += BK_THREADS) b4[i] = make_int4(0, 0, 0, 0);
   }
   const int64_t c = next_tile(tile_ctr);  // (barrier inside: also orders the bin reset)
   if (ptrace && t == 0) ptrace[c * 8] = ts0;
@@ -695,35 +697,41 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
-    const uint32_t sl = idx < cnt ? (uint32_t)atomicAdd(&S.u.bins[(S.k[idx] - kmin) >> s2], 1) : 0u;
+    uint32_t sl = 0;
+    if (idx < cnt) {
+      const uint32_t b = (S.k[idx] - kmin) >> s2, h = 16 * (b & 1);
+      sl = (atomicAdd(&S.u.bins[b >> 1], 1u << h) >> h) & 0xFFFFu;
+    }
     if (j & 1) slot[j >> 1] |= sl << 16;
     else slot[j >> 1] = sl;
   }
   __syncthreads();
   bool big = false;
-  {  // exclusive bin starts: BPT consecutive bins per thread + a block scan
-    int v[BPT];
-    int4* b4 = reinterpret_cast<int4*>(S.u.bins + t * BPT);
+  {  // exclusive bin starts: 2 * WPT consecutive bins per thread + a block scan
+    unsigned w[WPT];
+    uint4* b4 = reinterpret_cast<uint4*>(S.u.bins + t * WPT);
 #pragma unroll
-    for (int q = 0; q < BPT / 4; q++) {
-      const int4 x = b4[q];
-      v[4 * q] = x.x;
-      v[4 * q + 1] = x.y;
-      v[4 * q + 2] = x.z;
-      v[4 * q + 3] = x.w;
+    for (int q = 0; q < WPT / 4; q++) {
+      const uint4 x = b4[q];
+      w[4 * q] = x.x;
+      w[4 * q + 1] = x.y;
+      w[4 * q + 2] = x.z;
+      w[4 * q + 3] = x.w;
     }
     int sum = 0;
 #pragma unroll
-    for (int q = 0; q < BPT; q++) {
-      big |= v[q] > BK_BIN_BIG;
-      const int x = v[q];
-      v[q] = sum;
-      sum += x;
+    for (int q = 0; q < WPT; q++) {
+      const unsigned lo = w[q] & 0xFFFFu, hi = w[q] >> 16;
+      big |= lo > BK_BIN_BIG || hi > BK_BIN_BIG;
+      w[q] = (unsigned)sum | ((unsigned)(sum + lo) << 16);  // (starts relative to this thread's first bin)
+      sum += lo + hi;
     }
     int dummy;
     const int pre = block_exclusive_fast(sum, IAdd(), 0, reinterpret_cast<int*>(S.warp_p2), &dummy);
+    const unsigned pp = (unsigned)pre | ((unsigned)pre << 16);
 #pragma unroll
-    for (int q = 0; q < BPT / 4; q++) b4[q] = make_int4(pre + v[4 * q], pre + v[4 * q + 1], pre + v[4 * q + 2], pre + v[4 * q + 3]);
+    for (int q = 0; q < WPT / 4; q++)
+      b4[q] = make_uint4(w[4 * q] + pp, w[4 * q + 1] + pp, w[4 * q + 2] + pp, w[4 * q + 3] + pp);
   }
   big = __syncthreads_or(big) != 0;
   // scatter into bin order
@@ -732,7 +740,8 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
     const int idx = j * BK_THREADS + t;
     if (idx < cnt) {
       const uint32_t kr = S.k[idx];
-      S.sorted[S.u.bins[(kr - kmin) >> s2] + ((slot[j >> 1] >> (16 * (j & 1))) & 0xFFFFu)] = kr;
+      const uint32_t b = (kr - kmin) >> s2;
+      S.sorted[((S.u.bins[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) + ((slot[j >> 1] >> (16 * (j & 1))) & 0xFFFFu)] = kr;
     }
   }
   __syncthreads();
@@ -750,7 +759,8 @@ __global__ void __launch_bounds__(BK_THREADS, kMinB) k_bk_sweep(
         continue;
       }
       const int b = (int)((k - kmin) >> s2);
-      const int bs = S.u.bins[b], be = b + 1 < NB ? S.u.bins[b + 1] : cnt;
+      const int bs = (int)((S.u.bins[b >> 1] >> (16 * (b & 1))) & 0xFFFFu);
+      const int be = b + 1 < NB ? (int)((S.u.bins[(b + 1) >> 1] >> (16 * ((b + 1) & 1))) & 0xFFFFu) : cnt;
       int r = 0;
       for (int q = bs; q < be; q++) {
         const uint32_t o = S.sorted[q];
