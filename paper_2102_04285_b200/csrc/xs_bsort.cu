@@ -306,8 +306,7 @@ static int bucket_sort_pairs_impl(xs_ctx* ctx, uint64_t** keys, uint64_t** keys_
   XS_TRY(ws(ctx, W_BS_TAIL, 1, s, &tail));
   const int64_t n_chunks = (n + BK_T - 1) / BK_T;
   XS_TRY(ws(ctx, W_BS_CHUNK, 4 * n_chunks + 4, s, &chunk));
-  XS_CUDA(cudaMemsetAsync(counts, 0, g.nbuckets * 4, s));
-  XS_CUDA(cudaMemsetAsync(tail, 0, 8, s));
+  XS_TRY(fill_many(ctx, s, {{counts, (unsigned long long)g.nbuckets * 4, 0}, {tail, 8, 0}}));
   XS_LAUNCH(ctx, k_bs_hist, grid_for(n), XS_BLOCK, 0, s, *keys, n, key_bits, g.shift, counts);
   // bucket offsets + offs[nb] = total, one pass
   XS_TRY(scan_exclusive<int64_t>(ctx, ArrayIn<unsigned>{counts}, offs, g.nbuckets, s, offs + g.nbuckets));

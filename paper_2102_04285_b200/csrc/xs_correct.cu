@@ -255,8 +255,7 @@ static int launch_quantize(xs_ctx* ctx, int64_t tiles, cudaStream_t s, const uin
   XS_TRY(ws(ctx, W_QSCAN_DESC, tiles + 1, s, &desc));
   XS_TRY(ws(ctx, W_QSCAN_FLAGS, tiles + 1, s, &flags));
   XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
-  XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
-  XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+  XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
   XS_LAUNCH(ctx, k_quantize<W>, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, v, pr, site_ev, qslot, desc, flags,
             tctr);
   return XS_OK;
@@ -667,10 +666,13 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
   XS_TRY(ws(ctx, W_PTOTAL, np + 1, s, &ptotal));
   XS_TRY(ws(ctx, W_SLAB_BASE, np + 2, s, &slab_base));
   XS_TRY(ws(ctx, W_PID_SLABS, np + 1, s, &pid_slabs));
-  XS_CUDA(cudaMemsetAsync(removed, 0, ((int64_t)np * 4 + 1) * 8, s));
-  XS_CUDA(cudaMemsetAsync(shortfall, 0, ((int64_t)np * 4 + 1) * 8, s));
-  XS_CUDA(cudaMemsetAsync(ptotal, 0, (np + 1) * 8, s));
-  XS_CUDA(cudaMemsetAsync(pid_slabs, 0, (np + 1) * 4, s));
+  int64_t* d_ns;
+  XS_TRY(ws(ctx, W_NS_DEV, 1, s, &d_ns));
+  XS_TRY(fill_many(ctx, s, {{removed, ((unsigned long long)np * 4 + 1) * 8, 0},
+                            {shortfall, ((unsigned long long)np * 4 + 1) * 8, 0},
+                            {ptotal, (unsigned long long)(np + 1) * 8, 0},
+                            {pid_slabs, (unsigned long long)(np + 1) * 4, 0},
+                            {d_ns, 8, 0}}));
   XS_LAUNCH(ctx, k_zero_pad, 1, 32, 0, s, st);
   XS_LAUNCH(ctx, k_totals, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, np, st, 1);
 
@@ -682,9 +684,6 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
   // <= 1 per BACKEND/SIMULATOR); the exact count stays on the device
   const Stats& Hc = *ctx->h_stats;
   const int64_t ns = 2 * Hc.cat_all[0] + 2 * Hc.cat_all[4] + Hc.cat_all[2] + Hc.cat_all[3];
-  int64_t* d_ns;
-  XS_TRY(ws(ctx, W_NS_DEV, 1, s, &d_ns));
-  XS_CUDA(cudaMemsetAsync(d_ns, 0, 8, s));
   ProfScope ps_sites(ctx, ST_SITE_SORT, s);
   if (n) {
     XS_LAUNCH(ctx, k_site_count, grid_for(n), XS_BLOCK, 0, s, v, n, tflag, cnt);
@@ -739,8 +738,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
       XS_TRY(ws(ctx, W_RSCAN_DESC, tiles + 1, s, &desc));
       XS_TRY(ws(ctx, W_RSCAN_FLAGS, tiles + 1, s, &flags));
       XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
-      XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
-      XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+      XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
       XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, lenslot, site_sub, lo, hi, removed,
                 slab_a, slab_b, slab_pre, pid_slabs, ptotal, desc, flags, tctr);
     }
@@ -817,13 +815,13 @@ __global__ void k_ops_strict(const uint64_t* pk, int64_t n2, int tb, const int64
   if (ca >= cb) atomicOr((unsigned long long*)&st->pad[8], 1ull);
 }
 
-int ops_reuse_check(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
+int ops_reuse_check(xs_ctx* ctx, const EventView& v, Stats* verdict, cudaStream_t s) {
   const OpsState& os = ctx->ops;
   if (os.m <= 0 || !os.pk) return XS_OK;
   XS_LAUNCH(ctx, k_ops_strict, grid_for(2 * os.m), XS_BLOCK, 0, s, os.pk, 2 * os.m, os.tb,
             (const int64_t*)ctx->ptr[W_SLAB_A], (const int64_t*)ctx->ptr[W_SLAB_B],
             (const int64_t*)ctx->ptr[W_SLAB_PRE], (const int64_t*)ctx->ptr[W_SLAB_BASE],
-            (const int64_t*)ctx->ptr[W_PTOTAL], v.ev.n_pids, (Stats*)ctx->ptr[W_STATS]);
+            (const int64_t*)ctx->ptr[W_PTOTAL], v.ev.n_pids, verdict);
   return XS_OK;
 }
 }  // namespace xs

@@ -1,3 +1,4 @@
+#include <chrono>
 #include <algorithm>
 #include <cstdio>
 // xs_ctx.cu -- C ABI entry points, workspace and sort plumbing.
@@ -8,6 +9,48 @@
 using namespace xs;
 
 namespace xs {
+
+__global__ void k_fill_many(FillArgs a) {
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (int i = 0; i < a.n; i++) {
+    unsigned char* p = (unsigned char*)a.f[i].p;
+    const unsigned long long nb = a.f[i].bytes;
+    const unsigned v8 = (unsigned)a.f[i].val & 0xFFu;
+    const unsigned v32 = v8 * 0x01010101u;
+    if (((uintptr_t)p & 15) == 0) {  // 16-byte stores + a byte tail
+      const unsigned long long n16 = nb >> 4;
+      uint4* q = reinterpret_cast<uint4*>(p);
+      for (unsigned long long j = tid; j < n16; j += stride) q[j] = make_uint4(v32, v32, v32, v32);
+      for (unsigned long long j = (n16 << 4) + tid; j < nb; j += stride) p[j] = (unsigned char)v8;
+    } else if (((uintptr_t)p & 7) == 0 && (nb & 7) == 0) {
+      unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
+      const unsigned long long v64 = ((unsigned long long)v32 << 32) | v32;
+      for (unsigned long long j = tid; j < (nb >> 3); j += stride) q[j] = v64;
+    } else {
+      for (unsigned long long j = tid; j < nb; j += stride) p[j] = (unsigned char)v8;
+    }
+  }
+}
+
+int fill_many(xs_ctx* ctx, cudaStream_t s, std::initializer_list<FillSpec> specs) {
+  FillArgs a{};
+  unsigned long long most = 0;
+  for (const FillSpec& f : specs) {
+    if (!f.p || !f.bytes) continue;
+    if (a.n == XS_FILL_MAX) {
+      ctx->err = "fill_many: too many regions";
+      return XS_BAD_ARGUMENT;
+    }
+    a.f[a.n++] = f;
+    most = f.bytes > most ? f.bytes : most;
+  }
+  if (!a.n) return XS_OK;
+  const unsigned long long blocks = (most / 16 + XS_BLOCK - 1) / XS_BLOCK;
+  const int grid = (int)(blocks < 1 ? 1 : (blocks > 148 * 8 ? 148 * 8 : blocks));
+  XS_LAUNCH(ctx, k_fill_many, grid, XS_BLOCK, 0, s, a);
+  return XS_OK;
+}
 
 int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
   if (ctx->bank == 1) {  // a concurrent branch's private scratch
@@ -424,8 +467,7 @@ int xs_overlap_fetch(xs_ctx_t* ctx, int32_t* cell_pid, int32_t* cell_node, int32
   return XS_OK;
 }
 
-static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start,
-                        int64_t* out_dur, bool corrected_spans, cudaStream_t w) {
+static int correct_branches(xs_ctx* ctx, const EventView& v, cudaStream_t w) {
   // three independent latency-bound stages run as concurrent branches (graph
   // branches when captured): the correlation table, the OPERATION nesting
   // check (part of require_valid) and the wrapper-transition sites; the
@@ -433,10 +475,9 @@ static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* pro
   XS_TRY(ensure_branches(ctx));
   {  // flags the branches raise start clear before they fork
     Stats* stp = (Stats*)ctx->ptr[W_STATS];
-    XS_CUDA(cudaMemsetAsync(&stp->table_full, 0, sizeof(long long), w));
-    XS_CUDA(cudaMemsetAsync(&stp->depth_overflow, 0, sizeof(long long), w));
-    XS_CUDA(cudaMemsetAsync(&stp->pad[3], 0, sizeof(long long), w));
-    XS_CUDA(cudaMemsetAsync(&stp->pad[7], 0, 2 * sizeof(long long), w));  // (deep-path need, reuse verdict)
+    XS_TRY(fill_many(ctx, w, {{&stp->table_full, sizeof(long long), 0}, {&stp->depth_overflow, sizeof(long long), 0},
+                              {&stp->pad[3], sizeof(long long), 0},
+                              {&stp->pad[7], 2 * sizeof(long long), 0}}));  // (deep-path need, reuse verdict)
   }
   XS_CUDA(cudaEventRecord(ctx->br_fork, w));
   XS_CUDA(cudaStreamWaitEvent(ctx->br_stream[0], ctx->br_fork, 0));
@@ -464,8 +505,13 @@ static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* pro
     ctx->bank = 1;
     XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, w));
   }
-  XS_TRY(stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, w));
-  return ctx->reuse_ops ? ops_reuse_check(ctx, v, w) : XS_OK;
+  return XS_OK;
+}
+
+static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start,
+                        int64_t* out_dur, bool corrected_spans, cudaStream_t w) {
+  XS_TRY(correct_branches(ctx, v, w));
+  return stage_correct(ctx, v, prof, out_start, out_dur, corrected_spans, w);
 }
 
 static int correct_verdict(xs_ctx* ctx, const Stats* h, int64_t* bad_event) {
@@ -626,7 +672,10 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
   if (ev->n > 0 && (!out_start_dev || !out_dur_dev)) return XS_BAD_ARGUMENT;
   EventView v{*ev, ev->start, ev->dur};
   EventView vc{*ev, out_start_dev, out_dur_dev};
+  static const bool host_timing = getenv("XS_HOST_TIMING") != nullptr;  // (developer diagnostics)
+  const auto ht0 = std::chrono::steady_clock::now();
   XS_TRY(stage_events(ctx, v, s, false, true, prof));  // (sync: sizes; per-event rule violations stop here)
+  const auto ht1 = std::chrono::steady_clock::now();
   const Stats orig = *ctx->h_stats;
   Stats* st = nullptr;
   Stats* saved = nullptr;
@@ -658,6 +707,23 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     SpecScope sp(ctx, ev->dur, attribution == 1 ? &st->n_ops_nz : nullptr,
                  attribution == 1 ? &saved->n_ops_nz : nullptr);
     ctx->spec_zero_sentinel = attribution == 0;
+    // the reuse verdict (is the removal map strictly increasing on the op
+    // endpoints?) runs on a side branch: it is only read after the final sync
+    struct CheckJoin {
+      xs_ctx* c;
+      cudaStream_t w;
+      bool on;
+      ~CheckJoin() {
+        if (!on) return;
+        cudaEventRecord(c->br_join[0], c->br_stream[0]);
+        cudaStreamWaitEvent(w, c->br_join[0], 0);
+      }
+    } check_join{ctx, w, ctx->reuse_ops};
+    if (ctx->reuse_ops) {
+      XS_CUDA(cudaEventRecord(ctx->br_fork, w));
+      XS_CUDA(cudaStreamWaitEvent(ctx->br_stream[0], ctx->br_fork, 0));
+      XS_TRY(ops_reuse_check(ctx, v, saved, ctx->br_stream[0]));  // (into the correction's saved statistics)
+    }
     XS_TRY(stage_events_async(ctx, vc, w, false, nullptr));
     // correlations are untouched by the correction: the original's dangling
     // check stands, and only CORRELATION attribution needs launch instants
@@ -668,24 +734,33 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     ctx->res_pids = ev->n_pids;
     return corrected_total_from_spans(ctx, w);
   };
+  const auto ht2 = std::chrono::steady_clock::now();
+  // Three graph segments launched back to back: a graph's host launch cost
+  // grows with its node count (~40 us for the whole step at config 2), and
+  // the device starts the first segment while the host submits the rest.
+  XS_TRY(run_segment(ctx, s, key + "B", true, [&](cudaStream_t w) -> int { return correct_branches(ctx, v, w); }));
+  const auto ht3 = std::chrono::steady_clock::now();
+  XS_TRY(run_segment(ctx, s, key + "C", true, [&](cudaStream_t w) -> int {
+    return stage_correct(ctx, v, prof, out_start_dev, out_dur_dev, false, w);
+  }));
   if (!to_host) {
-    XS_TRY(run_segment(ctx, s, key, true, [&](cudaStream_t w) -> int {
-      XS_TRY(correct_body(ctx, v, prof, out_start_dev, out_dur_dev, false, w));
-      return spec ? spec_body(w) : XS_OK;
-    }));
+    if (spec) XS_TRY(run_segment(ctx, s, key + "O", true, spec_body));
   } else {
-    // two graph segments: the corrected columns are final after the first,
-    // and their D2H on the copy stream overlaps the overlap pass -- and, for
+    // the corrected columns are final after the second segment: their D2H on
+    // the copy stream overlaps the overlap pass -- and, for
     // xs_analyze_to_host_async, the caller's next call
-    XS_TRY(run_segment(ctx, s, key + "C", true, [&](cudaStream_t w) -> int {
-      return correct_body(ctx, v, prof, out_start_dev, out_dur_dev, false, w);
-    }));
     XS_CUDA(cudaEventRecord(ctx->d2h_fork, s));
     XS_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->d2h_fork, 0));
     XS_CUDA(cudaMemcpyAsync(out_start_host, out_start_dev, ev->n * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
     XS_CUDA(cudaMemcpyAsync(out_dur_host, out_dur_dev, ev->n * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
     XS_CUDA(cudaEventRecord(ctx->d2h_join, ctx->d2h_stream));
     if (spec) XS_TRY(run_segment(ctx, s, key + "O", true, spec_body));
+  }
+  if (host_timing) {
+    const auto ht4 = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    fprintf(stderr, "[xs host] pass1+sync %.1f us, key %.1f us, first segment launch %.1f us, all launches %.1f us\n",
+            us(ht0, ht1), us(ht1, ht2), us(ht2, ht3), us(ht2, ht4));
   }
   ctx->corr_pids = ev->n_pids;
   if (spec) XS_CUDA(cudaMemcpyAsync(ctx->h_stats + 1, saved, sizeof(Stats), cudaMemcpyDeviceToHost, s));

@@ -1,5 +1,6 @@
 // xs_engine.cuh -- context, workspace and the host-side pipeline contracts.
 #pragma once
+#include <initializer_list>
 #include <cstdio>
 #include <functional>
 #include <map>
@@ -335,6 +336,21 @@ struct Run {
     }                                                                                  \
   } while (0)
 
+// Several small fills as ONE kernel launch: inside a captured graph every
+// cudaMemsetAsync is its own node (~5 us of dependency latency each on the
+// step's critical path; the look-back kernels alone need two per launch).
+struct FillSpec {
+  void* p;
+  unsigned long long bytes;
+  int val;  // byte value
+};
+constexpr int XS_FILL_MAX = 8;
+struct FillArgs {
+  FillSpec f[XS_FILL_MAX];
+  int n;
+};
+int fill_many(xs_ctx* ctx, cudaStream_t s, std::initializer_list<FillSpec> specs);
+
 // grow-only workspace slot
 int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out);
 template <class T>
@@ -369,7 +385,7 @@ int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr
 int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_start);
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths);
 int stage_overlap_pre(xs_ctx* ctx, const EventView& v, cudaStream_t s);
-int ops_reuse_check(xs_ctx* ctx, const EventView& v, cudaStream_t s);
+int ops_reuse_check(xs_ctx* ctx, const EventView& v, Stats* verdict, cudaStream_t s);
 int ops_with_overlap_pre(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t w);
 int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t s);
 int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mask, cudaStream_t s);

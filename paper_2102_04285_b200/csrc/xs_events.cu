@@ -506,10 +506,9 @@ int stage_events_async(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool che
   XS_TRY(ws(ctx, alt ? W_PID_GROUP0_ALT : W_PID_GROUP0, np + 2, s, &pid_group0));
   XS_LAUNCH(ctx, k_init_stats, 1, 32, 0, s, st);
   XS_LAUNCH(ctx, k_init_pid, grid_for(np + 1), XS_BLOCK, 0, s, lo, hi, pid_ops, np + 1);
-  XS_CUDA(cudaMemsetAsync(group_ops, 0, (ng + 1) * sizeof(int), s));
   uint8_t* tflag;  // groups with HIGH_LEVEL/BACKEND/SIMULATOR/ACCEL_API events (dense transition-key groups)
   XS_TRY(ws(ctx, W_TGRP_FLAG, ng + 1, s, &tflag));
-  XS_CUDA(cudaMemsetAsync(tflag, 0, ng + 1, s));
+  XS_TRY(fill_many(ctx, s, {{group_ops, (unsigned long long)(ng + 1) * sizeof(int), 0}, {tflag, (unsigned long long)ng + 1, 0}}));
   if (n > 0) {
     ProfScope ps(ctx, ST_PASS1, s);
     const uint8_t* hasint = (check_api && prof) ? prof->has_internal : nullptr;

@@ -536,10 +536,8 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   ProfScope ps(ctx, ST_OPS, s);
   if (!ctx->skip_ops_reset) {  // retry-able flags start clear on every attempt
     Stats* stp = (Stats*)ctx->ptr[W_STATS];
-    XS_CUDA(cudaMemsetAsync(&stp->table_full, 0, sizeof(long long), s));
-    XS_CUDA(cudaMemsetAsync(&stp->depth_overflow, 0, sizeof(long long), s));
-    XS_CUDA(cudaMemsetAsync(&stp->pad[3], 0, sizeof(long long), s));
-    XS_CUDA(cudaMemsetAsync(&stp->pad[7], 0, sizeof(long long), s));
+    XS_TRY(fill_many(ctx, s, {{&stp->table_full, sizeof(long long), 0}, {&stp->depth_overflow, sizeof(long long), 0},
+                              {&stp->pad[3], sizeof(long long), 0}, {&stp->pad[7], sizeof(long long), 0}}));
   }
   const Stats& H = *ctx->h_stats;
   const int64_t m = H.n_ops_nz;
@@ -628,8 +626,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   XS_TRY(ws(ctx, W_READY, 2 * m + 2, s, &pready));
   nready = pready + (m + 1);
   XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &ctr));
-  XS_CUDA(cudaMemsetAsync(pready, 0, (2 * m + 2) * sizeof(int), s));
-  XS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), s));
+  XS_TRY(fill_many(ctx, s, {{pready, (unsigned long long)(2 * m + 2) * sizeof(int), 0}, {ctr, sizeof(int), 0}}));
   {
     int blocks = (int)std::min<int64_t>((2 * m + 255) / 256, 148 * 8);
     XS_LAUNCH(ctx, k_parent_nodes, blocks, XS_BLOCK, 0, s, sk, sv, 2 * m, depth, pos_open, op_ev, v.ev.name, tb,

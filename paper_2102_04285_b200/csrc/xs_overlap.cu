@@ -1066,8 +1066,7 @@ static int bucket_sweep(xs_ctx* ctx, const EventView& v, const BkPlan& plan, int
   XS_TRY(ws(ctx, W_MSCAN_DESC, n_chunks + 1, s, &desc));
   XS_TRY(ws(ctx, W_MSCAN_FLAGS, n_chunks + 1, s, &flags));
   XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
-  XS_CUDA(cudaMemsetAsync(flags, 0, (n_chunks + 1) * sizeof(int), s));
-  XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+  XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(n_chunks + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
   ProfScope ps(ctx, ST_SWEEP, s);
   if (!(ctx->attr_done & 1u)) {  // (per context: a context is bound to one device)
     XS_CUDA(cudaFuncSetAttribute(k_bk_sweep<HT_SMALL, XS_SWEEP_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1229,9 +1228,8 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
     XS_TRY(ws(ctx, W_FXSCAN_DESC, tiles + 1, s, &desc));
     XS_TRY(ws(ctx, W_FXSCAN_FLAGS, tiles + 1, s, &flags));
     XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
-    XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
-    XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
-    XS_CUDA(cudaMemsetAsync(cnt + 1, 0, 8, s));
+    XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0},
+                              {cnt + 1, 8, 0}}));
     if (tiles)
       XS_LAUNCH(ctx, k_fx_scan, (int)tiles, XS_BLOCK, 0, s, fx, nfx, tb, nodeb, n_nodes, hist, pieces, cnt + 1, desc,
                 flags, tctr);
@@ -1274,8 +1272,7 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
     XS_TRY(ws(ctx, W_MSCAN_DESC, tiles + 1, s, &desc));
     XS_TRY(ws(ctx, W_MSCAN_FLAGS, tiles + 1, s, &flags));
     XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
-    XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
-    XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+    XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
     ProfScope ps(ctx, ST_SWEEP, s);
     XS_LAUNCH(ctx, k_sweep, (int)tiles, XS_BLOCK, 0, s, mk, nvalid, tb, os.pidpath, os.opbase, n_nodes, hist, desc,
               flags, tctr);
@@ -1291,8 +1288,7 @@ int stage_overlap(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t
   XS_TRY(ws(ctx, W_CELL_MASK, cells_cap, s, &cm));
   XS_TRY(ws(ctx, W_CELL_NS, cells_cap, s, &cns));
   XS_TRY(ws(ctx, W_TRACKED, np + 1, s, &tracked));
-  XS_CUDA(cudaMemsetAsync(tracked, 0, (np + 1) * 8, s));
-  XS_CUDA(cudaMemsetAsync(ccount, 0, 8, s));
+  XS_TRY(fill_many(ctx, s, {{tracked, (unsigned long long)(np + 1) * 8, 0}, {ccount, 8, 0}}));
   ProfScope ps_compact(ctx, ST_COMPACT, s);
   if (hist_n)
     XS_LAUNCH(ctx, k_compact_cells, grid_for(hist_n), XS_BLOCK, 0, s, hist, hist_n, n_nodes, cp, cn, cm, cns, tracked,

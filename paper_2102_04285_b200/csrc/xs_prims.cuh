@@ -199,8 +199,7 @@ int scan_exclusive(xs_ctx* ctx, In in, Out* out, int64_t n, cudaStream_t s, Out*
   XS_TRY(ws(ctx, W_PSCAN_DESC, (size_t)tiles + 1, s, &desc));
   XS_TRY(ws(ctx, W_PSCAN_FLAGS, (size_t)tiles + 1, s, &flags));
   XS_TRY(ws(ctx, W_PSCAN_CTR, 4, s, &ctr));
-  XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
-  XS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), s));
+  XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {ctr, sizeof(int), 0}}));
   XS_LAUNCH(ctx, (k_scan_excl<Out, In, kIncl>), (int)tiles, XS_BLOCK, 0, s, in, out, n, total, desc, flags, ctr);
   return XS_OK;
 }
@@ -295,8 +294,7 @@ int select_indices(xs_ctx* ctx, Pred pred, int64_t n, int* out, int* count, cuda
   XS_TRY(ws(ctx, W_PSCAN_DESC, (size_t)tiles + 1, s, &desc));
   XS_TRY(ws(ctx, W_PSCAN_FLAGS, (size_t)tiles + 1, s, &flags));
   XS_TRY(ws(ctx, W_PSCAN_CTR, 4, s, &ctr));
-  XS_CUDA(cudaMemsetAsync(flags, 0, (tiles + 1) * sizeof(int), s));
-  XS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), s));
+  XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {ctr, sizeof(int), 0}}));
   XS_LAUNCH(ctx, k_select<Pred>, (int)tiles, XS_BLOCK, 0, s, pred, n, out, count, desc, flags, ctr);
   return XS_OK;
 }

@@ -258,8 +258,7 @@ int stage_transitions(xs_ctx* ctx, const EventView& v, int src_mask, int dst_mas
   XS_TRY(ws(ctx, W_TSCAN_FLAGS, tiles + 1, s, &tflags));
   XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
   XS_TRY(ws(ctx, W_HEADPOS, m + 1, s, &headpos));
-  XS_CUDA(cudaMemsetAsync(tflags, 0, (tiles + 1) * sizeof(int), s));
-  XS_CUDA(cudaMemsetAsync(tctr, 0, sizeof(int), s));
+  XS_TRY(fill_many(ctx, s, {{tflags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
   ps_sort.end();
   ProfScope ps(ctx, ST_TRANS_SCAN, s);
   XS_LAUNCH(ctx, k_tscan, (int)tiles, XS_BLOCK, 0, s, k1, v1, m, tb, v, site_flag, headpos, desc, tflags, tctr,
