@@ -181,7 +181,10 @@ __device__ __forceinline__ int amount_row(int sub, int name) {
   }
 }
 
-constexpr int Q_ITEMS = 8;
+#ifndef XS_Q_ITEMS
+#define XS_Q_ITEMS 8
+#endif
+constexpr int Q_ITEMS = XS_Q_ITEMS;
 // quantize_amounts (_timeline.py:57-67) per pid in site order:
 // q_i = floor(S_i) - floor(S_{i-1}) with S the running sum of exact amounts
 // = whole_i + [ P_i < frac_i ], P_i the inclusive running sum of the
@@ -336,7 +339,10 @@ __device__ __forceinline__ int hook_of(int sub) {
   return sub == TRANSITION_HOOK ? H_TRANS : sub == API_INTERCEPT ? H_IC : sub == API_INTERNAL ? H_INT : H_ANN;
 }
 
-constexpr int R_ITEMS = 8;
+#ifndef XS_R_ITEMS
+#define XS_R_ITEMS 8
+#endif
+constexpr int R_ITEMS = XS_R_ITEMS;
 __global__ void __launch_bounds__(XS_BLOCK) k_removal(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
                                                       const int64_t* lenslot, const uint8_t* site_sub,
                                                       const int64_t* lo, const int64_t* hi, int64_t* removed,

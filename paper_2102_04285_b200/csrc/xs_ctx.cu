@@ -52,6 +52,35 @@ int fill_many(xs_ctx* ctx, cudaStream_t s, std::initializer_list<FillSpec> specs
   return XS_OK;
 }
 
+__global__ void k_copy_many(CopyArgs a) {
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (int i = 0; i < a.n; i++) {
+    unsigned long long* d = (unsigned long long*)a.c[i].dst;
+    const unsigned long long* x = (const unsigned long long*)a.c[i].src;
+    for (unsigned long long j = tid; j < (a.c[i].bytes >> 3); j += stride) d[j] = x[j];
+  }
+}
+
+int to_host_many(xs_ctx* ctx, cudaStream_t s, std::initializer_list<CopySpec> specs) {
+  CopyArgs a{};
+  unsigned long long most = 0;
+  for (const CopySpec& c : specs) {
+    if (!c.dst || !c.src || !c.bytes) continue;
+    if (a.n == XS_FILL_MAX || (c.bytes & 7) || ((uintptr_t)c.dst & 7) || ((uintptr_t)c.src & 7)) {
+      ctx->err = "to_host_many: bad region";
+      return XS_BAD_ARGUMENT;
+    }
+    a.c[a.n++] = c;
+    most = c.bytes > most ? c.bytes : most;
+  }
+  if (!a.n) return XS_OK;
+  const unsigned long long blocks = (most / 8 + XS_BLOCK - 1) / XS_BLOCK;
+  const int grid = (int)(blocks < 1 ? 1 : (blocks > 148 ? 148 : blocks));
+  XS_LAUNCH(ctx, k_copy_many, grid, XS_BLOCK, 0, s, a);
+  return XS_OK;
+}
+
 int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
   if (ctx->bank == 1) {  // a concurrent branch's private scratch
     switch (slot) {
@@ -93,7 +122,7 @@ int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
 int fetch_stats(xs_ctx* ctx, cudaStream_t s) {
   Stats* d = nullptr;
   XS_TRY(ws(ctx, W_STATS, 1, s, &d));
-  XS_CUDA(cudaMemcpyAsync(ctx->h_stats, d, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  XS_TRY(to_host_many(ctx, s, {{ctx->h_stats, d, sizeof(Stats)}}));
   XS_CUDA(cudaStreamSynchronize(s));
   if (!ctx->pend_stage.empty()) prof_flush(ctx);
   return XS_OK;
@@ -498,14 +527,38 @@ static int correct_branches(xs_ctx* ctx, const EventView& v, cudaStream_t w) {
     Join join{ctx, w};
     XS_TRY(stage_corr_table(ctx, v, ctx->br_stream[0], false));
     ctx->skip_ops_reset = true;
-    // OPERATION nesting is part of require_valid; with reuse_ops the stage
-    // also builds the paths the corrected trace's overlap pass will use
-    XS_TRY(stage_ops(ctx, v, ctx->br_stream[1], ctx->reuse_ops));
+    // OPERATION nesting is part of require_valid (with reuse_ops, the paths
+    // the corrected trace's overlap pass will use are built from this
+    // stage's sorted stream concurrently with the correction: correct_paths)
+    XS_TRY(stage_ops(ctx, v, ctx->br_stream[1], false));
     ctx->skip_ops_reset = false;
     ctx->bank = 1;
     XS_TRY(stage_transitions(ctx, v, 0x2 /*HIGH_LEVEL*/, 0xC /*BACKEND|SIMULATOR*/, w));
   }
   return XS_OK;
+}
+
+// stage_correct on w; with reuse_ops the original trace's op paths are built
+// on a side branch meanwhile (private scratch bank), joined before the end
+static int correct_with_paths(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start,
+                              int64_t* out_dur, cudaStream_t w) {
+  if (!ctx->reuse_ops) return stage_correct(ctx, v, prof, out_start, out_dur, false, w);
+  XS_TRY(ensure_branches(ctx));
+  XS_CUDA(cudaEventRecord(ctx->br_fork, w));
+  XS_CUDA(cudaStreamWaitEvent(ctx->br_stream[1], ctx->br_fork, 0));
+  struct Join {
+    xs_ctx* c;
+    cudaStream_t w;
+    ~Join() {
+      c->bank = 0;
+      cudaEventRecord(c->br_join[1], c->br_stream[1]);
+      cudaStreamWaitEvent(w, c->br_join[1], 0);
+    }
+  } join{ctx, w};
+  ctx->bank = 1;
+  XS_TRY(stage_ops_paths(ctx, v, ctx->br_stream[1]));
+  ctx->bank = 0;
+  return stage_correct(ctx, v, prof, out_start, out_dur, false, w);
 }
 
 static int correct_body(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int64_t* out_start,
@@ -525,8 +578,10 @@ static int correct_verdict(xs_ctx* ctx, const Stats* h, int64_t* bad_event) {
 }
 
 // queue the D2H of what xs_correct_report returns, to land with the next sync
-static int prefetch_report(xs_ctx* ctx, cudaStream_t s) {
+// the report's host buffer, grown to the current pid count
+static int report_buffer(xs_ctx* ctx, size_t* bytes) {
   const size_t b = (size_t)ctx->corr_pids * 4 * 8;
+  *bytes = b;
   if (2 * b > ctx->h_report_cap) {
     if (ctx->h_report) XS_CUDA(cudaFreeHost(ctx->h_report));
     ctx->h_report = nullptr;
@@ -534,12 +589,15 @@ static int prefetch_report(xs_ctx* ctx, cudaStream_t s) {
     XS_CUDA(cudaMallocHost(&ctx->h_report, 2 * b));
     ctx->h_report_cap = 2 * b;
   }
-  XS_CUDA(cudaMemcpyAsync(ctx->h_totals, ctx->ptr[W_CORR_TOTALS], 4 * 8, cudaMemcpyDeviceToHost, s));
-  if (b) {
-    XS_CUDA(cudaMemcpyAsync(ctx->h_report, ctx->ptr[W_REMOVED], b, cudaMemcpyDeviceToHost, s));
-    XS_CUDA(cudaMemcpyAsync(ctx->h_report + b / 8, ctx->ptr[W_SHORTFALL], b, cudaMemcpyDeviceToHost, s));
-  }
   return XS_OK;
+}
+
+static int prefetch_report(xs_ctx* ctx, cudaStream_t s) {
+  size_t b = 0;
+  XS_TRY(report_buffer(ctx, &b));
+  return to_host_many(ctx, s, {{ctx->h_totals, ctx->ptr[W_CORR_TOTALS], 4 * 8},
+                               {ctx->h_report, ctx->ptr[W_REMOVED], b},
+                               {ctx->h_report + b / 8, ctx->ptr[W_SHORTFALL], b}});
 }
 
 static int correct_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int64_t* out_start,
@@ -741,7 +799,7 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
   XS_TRY(run_segment(ctx, s, key + "B", true, [&](cudaStream_t w) -> int { return correct_branches(ctx, v, w); }));
   const auto ht3 = std::chrono::steady_clock::now();
   XS_TRY(run_segment(ctx, s, key + "C", true, [&](cudaStream_t w) -> int {
-    return stage_correct(ctx, v, prof, out_start_dev, out_dur_dev, false, w);
+    return correct_with_paths(ctx, v, prof, out_start_dev, out_dur_dev, w);
   }));
   if (!to_host) {
     if (spec) XS_TRY(run_segment(ctx, s, key + "O", true, spec_body));
@@ -763,9 +821,17 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
             us(ht0, ht1), us(ht1, ht2), us(ht2, ht3), us(ht2, ht4));
   }
   ctx->corr_pids = ev->n_pids;
-  if (spec) XS_CUDA(cudaMemcpyAsync(ctx->h_stats + 1, saved, sizeof(Stats), cudaMemcpyDeviceToHost, s));
-  XS_TRY(prefetch_report(ctx, s));
-  XS_TRY(fetch_stats(ctx, s));
+  {  // every small result in one copy kernel, one sync
+    size_t b = 0;
+    XS_TRY(report_buffer(ctx, &b));
+    XS_TRY(to_host_many(ctx, s, {{ctx->h_stats + 1, spec ? saved : nullptr, sizeof(Stats)},
+                                 {ctx->h_totals, ctx->ptr[W_CORR_TOTALS], 4 * 8},
+                                 {ctx->h_report, ctx->ptr[W_REMOVED], b},
+                                 {ctx->h_report + b / 8, ctx->ptr[W_SHORTFALL], b},
+                                 {ctx->h_stats, ctx->ptr[W_STATS], sizeof(Stats)}}));
+    XS_CUDA(cudaStreamSynchronize(s));
+    if (!ctx->pend_stage.empty()) prof_flush(ctx);
+  }
   const Stats* hc = spec ? ctx->h_stats + 1 : ctx->h_stats;  // the correction part's statistics
   if (hc->pad[3] && !ctx->force_lsd) return XS_RETRY_LSD;
   XS_TRY(correct_verdict(ctx, hc, bad_event));

@@ -350,6 +350,20 @@ struct FillArgs {
   int n;
 };
 int fill_many(xs_ctx* ctx, cudaStream_t s, std::initializer_list<FillSpec> specs);
+// Small device -> page-locked host copies as ONE kernel storing straight into
+// the (unified-address) host buffers: each D2H memcpy costs several us of
+// copy-engine latency on the step's tail.  Visible to the host after the
+// stream synchronises.
+struct CopySpec {
+  void* dst;  // page-locked host memory (cudaMallocHost)
+  const void* src;
+  unsigned long long bytes;  // multiple of 8, both pointers 8-aligned
+};
+struct CopyArgs {
+  CopySpec c[XS_FILL_MAX];
+  int n;
+};
+int to_host_many(xs_ctx* ctx, cudaStream_t s, std::initializer_list<CopySpec> specs);
 
 // grow-only workspace slot
 int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out);
@@ -384,6 +398,7 @@ int stage_events(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_corr
 // launch instants when need_start (CORRELATION attribution)
 int stage_corr_table(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool need_start);
 int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths);
+int stage_ops_paths(xs_ctx* ctx, const EventView& v, cudaStream_t s);
 int stage_overlap_pre(xs_ctx* ctx, const EventView& v, cudaStream_t s);
 int ops_reuse_check(xs_ctx* ctx, const EventView& v, Stats* verdict, cudaStream_t s);
 int ops_with_overlap_pre(xs_ctx* ctx, const EventView& v, int attribution, cudaStream_t w);

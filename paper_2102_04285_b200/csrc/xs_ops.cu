@@ -618,7 +618,35 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
   XS_LAUNCH(ctx, k_depth_scatter, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, depth, 2 * m, d_open, pos_open, d_close);
   XS_LAUNCH(ctx, k_depth_check, grid_for(m), XS_BLOCK, 0, s, d_open, d_close, m, st);
   if (!build_paths) return XS_OK;  // nesting verdict is read at the caller's next sync
+  return stage_ops_paths(ctx, v, s);
+}
 
+// The path half of the operation stage, from the sorted endpoint stream and
+// depths the first half left in the workspace (it may run on another stream
+// later, e.g. concurrently with the correction when analyze reuses the
+// original trace's paths).
+int stage_ops_paths(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
+  const Stats& H = *ctx->h_stats;
+  OpsState& os = ctx_ops(ctx);
+  const int64_t m = os.m;
+  if (m == 0) {
+    XS_TRY(trie_setup(ctx, s, &os.trie));
+    return XS_OK;
+  }
+  const int np = v.ev.n_pids, ng = v.ev.n_groups;
+  const int tb = os.tb;
+  const int pb = bits_for((uint64_t)(np > 0 ? np - 1 : 0));
+  int* group_ops_pos = ctx->spec_zero_sentinel ? (int*)ctx->ptr[W_GROUP_OPS_ALT] : (int*)ctx->ptr[W_GROUP_OPS];
+  Stats* st = (Stats*)ctx->ptr[W_STATS];
+  uint64_t* sk = const_cast<uint64_t*>(os.skeys);
+  uint32_t* sv = const_cast<uint32_t*>(os.svals);
+  const int* op_ev = os.rank_ev;
+  int* depth = (int*)ctx->ptr[W_DEPTH_SCAN_DESC];
+  int* pos_open = (int*)ctx->ptr[W_POPEN];
+  int* parent = (int*)ctx->ptr[W_PARENT];
+  int* opg = (int*)ctx->ptr[W_OPG];
+  int* opg_inv = (int*)ctx->ptr[W_OPG_INV];
+  const int* rank_ev = op_ev;
   // 3-5. parents + node(op) in one dependency-ordered pass over the stream
   XS_TRY(trie_setup(ctx, s, &os.trie));
   int *node, *pready, *nready, *ctr;

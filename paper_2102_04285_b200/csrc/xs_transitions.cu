@@ -104,7 +104,10 @@ __global__ void k_trec_tiefix(const uint64_t* key, uint32_t* val, int64_t m, Eve
   }
 }
 
-constexpr int T_ITEMS = 4;
+#ifndef XS_T_ITEMS
+#define XS_T_ITEMS 4
+#endif
+constexpr int T_ITEMS = XS_T_ITEMS;
 __global__ void __launch_bounds__(XS_BLOCK) k_tscan(const uint64_t* __restrict__ key, const uint32_t* __restrict__ val,
                                                     int64_t m, int tb, EventView v, uint8_t* flags_out,
                                                     int32_t* headpos_out, TileDesc<TState>* desc, int* flags,

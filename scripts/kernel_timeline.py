@@ -29,31 +29,33 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(2):
         eng.correct(dt, sc, analyze_attribution=0)
     torch.cuda.synchronize()
-evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
-ks = sorted([(e.time_range.start, e.time_range.end, e.name) for e in evs if "xs::" in e.name or "k_" in e.name])
-# the second step: from the second k_init_stats-like first kernel
+import json  # noqa: E402
+import tempfile  # noqa: E402
+
+path = os.path.join(tempfile.mkdtemp(), "trace.json")
+prof.export_chrome_trace(path)
+tr = json.load(open(path))
+acts = [e for e in tr["traceEvents"] if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memset", "gpu_memcpy")]
+ks = sorted((float(e["ts"]), float(e["ts"]) + float(e.get("dur", 0)), e["name"], e.get("args", {}).get("stream", -1),
+             e["cat"]) for e in acts)
+# the second step starts at the second-to-last k_init_stats pair: take the last third of the list
 firsts = [i for i, k in enumerate(ks) if "k_init_stats" in k[2]]
 start = firsts[len(firsts) // 2] if len(firsts) >= 2 else 0
 ks = ks[start:]
 t0 = ks[0][0]
 end = max(k[1] for k in ks)
-print(f"kernels {len(ks)}  span {end - t0:.1f} us")
-busy = 0.0
-cur_end = t0
-for s, e, n in ks:
-    if s > cur_end:
-        busy += 0
+print(f"activities {len(ks)}  span {end - t0:.1f} us")
+for s_, e_, n, st, cat in ks:
     short = n.split("(")[0].replace("void ", "")[:60]
-    print(f"{s - t0:8.1f} {e - t0:8.1f} {e - s:7.1f}  {short}")
-# idle time: union of kernel intervals vs span
-iv = sorted((s, e) for s, e, _ in ks)
+    print(f"{s_ - t0:8.1f} {e_ - t0:8.1f} {e_ - s_:7.1f}  s{st:<3} {'M ' if cat != 'kernel' else '  '}{short}")
+iv = sorted((s_, e_) for s_, e_, _, _, _ in ks)
 u = 0.0
 cs, ce = iv[0]
-for s, e in iv[1:]:
-    if s > ce:
+for s_, e_ in iv[1:]:
+    if s_ > ce:
         u += ce - cs
-        cs, ce = s, e
+        cs, ce = s_, e_
     else:
-        ce = max(ce, e)
+        ce = max(ce, e_)
 u += ce - cs
-print(f"device busy (union of kernels) {u:.1f} us of {end - t0:.1f} us")
+print(f"device busy (union of activities) {u:.1f} us of {end - t0:.1f} us")
