@@ -343,7 +343,10 @@ __device__ __forceinline__ int hook_of(int sub) {
 #define XS_R_ITEMS 8
 #endif
 constexpr int R_ITEMS = XS_R_ITEMS;
-__global__ void __launch_bounds__(XS_BLOCK) k_removal(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
+#ifndef XS_REMOVAL_MINB
+#define XS_REMOVAL_MINB 4  // 4 CTAs per SM (64 registers, small spills): 1.99 -> 1.61 ms at 30M events
+#endif
+__global__ void __launch_bounds__(XS_BLOCK, XS_REMOVAL_MINB) k_removal(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
                                                       const int64_t* lenslot, const uint8_t* site_sub,
                                                       const int64_t* lo, const int64_t* hi, int64_t* removed,
                                                       int64_t* slab_a, int64_t* slab_b, int64_t* slab_pre,
@@ -759,6 +762,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     while (logw > 4 && ((int64_t)np << logw) > ((int64_t)1 << 24)) logw--;
     int32_t* ridx;
     XS_TRY(ws(ctx, W_RMAP_IDX, ((int64_t)np << logw) + 1, s, &ridx));
+    ctx->rmap_logw = logw;
     XS_LAUNCH(ctx, k_rmap_index, grid_for((int64_t)np << logw), XS_BLOCK, 0, s, np, logw, lo, hi, slab_b, slab_base,
               ridx);
     XS_LAUNCH(ctx, k_remap, grid_for(n), XS_BLOCK, 0, s, v, n, lo, hi, slab_a, slab_b, slab_pre, slab_base, ptotal,
@@ -802,32 +806,50 @@ using namespace xs;
 // of neighbours of one pid with t < t' but rmap(t) >= rmap(t') sets pad[8]
 // (the host then redoes the overlap pass with its own operation stage).
 namespace xs {
-__global__ void k_ops_strict(const uint64_t* pk, int64_t n2, int tb, const int64_t* sa, const int64_t* sb,
-                             const int64_t* spre, const int64_t* slab_base, const int64_t* ptotal, int np,
-                             Stats* st) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j + 1 >= n2) return;
-  const uint64_t a = pk[j], b = pk[j + 1];
-  if (a == ~0ull || b == ~0ull) return;
-  const uint64_t pa = a >> (tb + 1), pb = b >> (tb + 1);
-  if (pa != pb || (int)pa >= np) return;
-  const uint64_t tmask = (1ull << tb) - 1;
-  const int64_t ta = (int64_t)((a >> 1) & tmask), tb_ = (int64_t)((b >> 1) & tmask);
-  if (ta == tb_) return;
-  const int p = (int)pa;
+__device__ __forceinline__ int64_t ops_strict_map(uint64_t key, int tb, const int64_t* lo, const int64_t* hi,
+                                                  const int64_t* sa, const int64_t* sb, const int64_t* spre,
+                                                  const int64_t* slab_base, const int64_t* ptotal, const int32_t* idx,
+                                                  int logw) {
+  const int p = (int)(key >> (tb + 1));
+  const int64_t t = (int64_t)((key >> 1) & ((1ull << tb) - 1));
   const int64_t base = slab_base[p], K = slab_base[p + 1] - base;
-  const int64_t ca = ta - rmap_removed(ta, sa, sb, spre, base, K, ptotal[p]);
-  const int64_t cb = tb_ - rmap_removed(tb_, sa, sb, spre, base, K, ptotal[p]);
-  if (ca >= cb) atomicOr((unsigned long long*)&st->pad[8], 1ull);
+  return t - rmap_removed_idx(t, sa, sb, spre, base, K, ptotal[p], idx + ((int64_t)p << logw), logw,
+                              rmap_shift(lo, hi, p, logw));
+}
+
+// one sampled-index lookup per endpoint; the right neighbour's value comes
+// from the next lane (the warp's last lane looks its neighbour up itself)
+__global__ void k_ops_strict(const uint64_t* pk, int64_t n2, int tb, const int64_t* lo, const int64_t* hi,
+                             const int64_t* sa, const int64_t* sb, const int64_t* spre, const int64_t* slab_base,
+                             const int64_t* ptotal, const int32_t* idx, int logw, int np, Stats* st) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint64_t a = j < n2 ? pk[j] : ~0ull;
+  const bool va = a != ~0ull && (int)(a >> (tb + 1)) < np;
+  const int64_t ca = va ? ops_strict_map(a, tb, lo, hi, sa, sb, spre, slab_base, ptotal, idx, logw) : 0;
+  int64_t cb = __shfl_down_sync(0xffffffffu, ca, 1);
+  uint64_t b = __shfl_down_sync(0xffffffffu, a, 1);
+  if (lane == 31) {
+    b = j + 1 < n2 ? pk[j + 1] : ~0ull;
+    const bool vb = b != ~0ull && (int)(b >> (tb + 1)) < np;
+    cb = vb ? ops_strict_map(b, tb, lo, hi, sa, sb, spre, slab_base, ptotal, idx, logw) : 0;
+  }
+  if (!va || j + 1 >= n2 || b == ~0ull) return;
+  if ((a >> (tb + 1)) != (b >> (tb + 1))) return;  // different pids
+  if (((a ^ b) >> 1) & ((1ull << tb) - 1)) {      // distinct times must stay distinct and ordered
+    if (ca >= cb) atomicOr((unsigned long long*)&st->pad[8], 1ull);
+  }
 }
 
 int ops_reuse_check(xs_ctx* ctx, const EventView& v, Stats* verdict, cudaStream_t s) {
   const OpsState& os = ctx->ops;
   if (os.m <= 0 || !os.pk) return XS_OK;
   XS_LAUNCH(ctx, k_ops_strict, grid_for(2 * os.m), XS_BLOCK, 0, s, os.pk, 2 * os.m, os.tb,
+            (const int64_t*)ctx->ptr[W_CORR_LO], (const int64_t*)ctx->ptr[W_CORR_HI],
             (const int64_t*)ctx->ptr[W_SLAB_A], (const int64_t*)ctx->ptr[W_SLAB_B],
             (const int64_t*)ctx->ptr[W_SLAB_PRE], (const int64_t*)ctx->ptr[W_SLAB_BASE],
-            (const int64_t*)ctx->ptr[W_PTOTAL], v.ev.n_pids, verdict);
+            (const int64_t*)ctx->ptr[W_PTOTAL], (const int32_t*)ctx->ptr[W_RMAP_IDX], ctx->rmap_logw, v.ev.n_pids,
+            verdict);
   return XS_OK;
 }
 }  // namespace xs

@@ -130,8 +130,11 @@ constexpr int kP1Unroll = XS_P1_UNROLL;  // vector steps in flight per thread  /
 // vector steps of 4 (16-byte loads of start/dur/pid, one 4-byte load of the
 // categories) when the columns are aligned for it.  Counters reduce per warp
 // into shared memory, then one global atomic per counter per CTA.
+#ifndef XS_PASS1_MINB
+#define XS_PASS1_MINB 1
+#endif
 template <bool kVec>
-__global__ void __launch_bounds__(XS_BLOCK) k_pass1(EventView v, int64_t n, const uint8_t* __restrict__ has_meta,
+__global__ void __launch_bounds__(XS_BLOCK, XS_PASS1_MINB) k_pass1(EventView v, int64_t n, const uint8_t* __restrict__ has_meta,
                                                     const uint8_t* __restrict__ has_internal, int check_api,
                                                     Stats* st, int64_t* lo_out, int64_t* hi_out, int* pid_ops,
                                                     int* group_ops, uint8_t* tflag) {
