@@ -26,6 +26,17 @@ namespace xs {
 enum { ANN_START = 0, TRANSITION_HOOK = 1, API_INTERCEPT = 2, API_INTERNAL = 3, ANN_END = 4 };
 enum { H_ANN = 0, H_TRANS = 1, H_IC = 2, H_INT = 3 };
 
+// profile amount row of a site: 0..3 by subkind, 4 + name for API_INTERNAL
+__device__ __forceinline__ int amount_row(int sub, int name) {
+  switch (sub) {
+    case ANN_START: return 0;
+    case ANN_END: return 1;
+    case TRANSITION_HOOK: return 2;
+    case API_INTERCEPT: return 3;
+    default: return 4 + name;
+  }
+}
+
 __global__ void k_site_count(EventView v, int64_t n, const uint8_t* tflag, int* cnt) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -35,7 +46,7 @@ __global__ void k_site_count(EventView v, int64_t n, const uint8_t* tflag, int* 
 
 // slot layout: pos[i] (+1) for event i; primary key (pid | anchor | subkind)
 __global__ void k_site_gen(EventView v, int64_t n, const int* cnt, const int* pos, const int64_t* lo, int tb,
-                           int* site_ev, uint8_t* site_sub, uint64_t* k1) {
+                           int* site_ev, int* site_row, uint64_t* k1) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || cnt[i] == 0) return;
   const int c = v.ev.cat[i];
@@ -46,21 +57,21 @@ __global__ void k_site_gen(EventView v, int64_t n, const int* cnt, const int* po
   if (c == 0) {
     const uint64_t e_rel = s_rel + (uint64_t)v.dur[i];
     site_ev[at] = (int)i;
-    site_sub[at] = ANN_START;
+    site_row[at] = amount_row(ANN_START, 0);
     k1[at] = pb | (s_rel << 3) | ANN_START;
     site_ev[at + 1] = (int)i;
-    site_sub[at + 1] = ANN_END;
+    site_row[at + 1] = amount_row(ANN_END, 0);
     k1[at + 1] = pb | (e_rel << 3) | ANN_END;
   } else if (c == 4) {
     site_ev[at] = (int)i;
-    site_sub[at] = API_INTERCEPT;
+    site_row[at] = amount_row(API_INTERCEPT, 0);
     k1[at] = pb | (s_rel << 3) | API_INTERCEPT;
     site_ev[at + 1] = (int)i;
-    site_sub[at + 1] = API_INTERNAL;
+    site_row[at + 1] = amount_row(API_INTERNAL, v.ev.name[i]);
     k1[at + 1] = pb | (s_rel << 3) | API_INTERNAL;
   } else {
     site_ev[at] = (int)i;
-    site_sub[at] = TRANSITION_HOOK;
+    site_row[at] = amount_row(TRANSITION_HOOK, 0);
     k1[at] = pb | (s_rel << 3) | TRANSITION_HOOK;
   }
 }
@@ -171,15 +182,6 @@ struct SegModOp {
 
 // site subkind -> row of the profile's whole / frac tables (API_INTERNAL:
 // 4 + the event's name)
-__device__ __forceinline__ int amount_row(int sub, int name) {
-  switch (sub) {
-    case ANN_START: return 0;
-    case ANN_END: return 1;
-    case TRANSITION_HOOK: return 2;
-    case API_INTERCEPT: return 3;
-    default: return 4 + name;
-  }
-}
 
 #ifndef XS_Q_ITEMS
 #define XS_Q_ITEMS 8
@@ -191,7 +193,7 @@ constexpr int Q_ITEMS = XS_Q_ITEMS;
 // fractional numerators modulo L (a carry past L is exactly the floor step)
 template <int W>
 __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns,
-                                                       int tb, EventView v, xs_profile_t pr, const int* site_ev,
+                                                       int tb, EventView v, xs_profile_t pr, const int* site_row,
                                                        int64_t* qslot, TileDesc<SegMod<W>>* desc, int* flags,
                                                        int* tile_ctr) {
   const int tile = next_tile(tile_ctr);
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const
       // their event (for the API name); the rest are profile constants
       const uint64_t kq = k1[q];
       const int sub = (int)(kq & 7u);
-      row[j] = amount_row(sub, sub == API_INTERNAL ? v.ev.name[site_ev[slot[q]]] : 0);
+      row[j] = sub == API_INTERNAL ? site_row[slot[q]] : amount_row(sub, 0);
       hd[j] = q == 0 || (k1[q - 1] >> pshift) != (kq >> pshift);
       SegMod<W> e;
 #pragma unroll
@@ -252,14 +254,14 @@ __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const
 template <int W>
 static int launch_quantize(xs_ctx* ctx, int64_t tiles, cudaStream_t s, const uint64_t* k1, const uint32_t* sl,
                            const int64_t* d_ns, int tb, const EventView& v, const xs_profile_t& pr,
-                           const int* site_ev, int64_t* qslot) {
+                           const int* site_row, int64_t* qslot) {
   TileDesc<SegMod<W>>* desc;
   int *flags, *tctr;
   XS_TRY(ws(ctx, W_QSCAN_DESC, tiles + 1, s, &desc));
   XS_TRY(ws(ctx, W_QSCAN_FLAGS, tiles + 1, s, &flags));
   XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
   XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
-  XS_LAUNCH(ctx, k_quantize<W>, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, v, pr, site_ev, qslot, desc, flags,
+  XS_LAUNCH(ctx, k_quantize<W>, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, v, pr, site_row, qslot, desc, flags,
             tctr);
   return XS_OK;
 }
@@ -347,7 +349,7 @@ constexpr int R_ITEMS = XS_R_ITEMS;
 #define XS_REMOVAL_MINB 4  // 4 CTAs per SM (64 registers, small spills): 1.99 -> 1.61 ms at 30M events
 #endif
 __global__ void __launch_bounds__(XS_BLOCK, XS_REMOVAL_MINB) k_removal(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
-                                                      const int64_t* lenslot, const uint8_t* site_sub,
+                                                      const int64_t* lenslot,
                                                       const int64_t* lo, const int64_t* hi, int64_t* removed,
                                                       int64_t* slab_a, int64_t* slab_b, int64_t* slab_pre,
                                                       int* pid_slabs, int64_t* ptotal, TileDesc<RM>* desc,
@@ -705,7 +707,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
   XS_TRY(ws(ctx, W_SLAB_PRE, ns + 1, s, &slab_pre));
   if (ns > 0) {
     int* site_ev;
-    uint8_t* site_sub;
+    int* site_row;
     uint64_t *k1, *k1_alt;
     uint32_t *sl, *sl_alt;
     XS_TRY(ws(ctx, W_SITE_K, ns + 1, s, &k1));
@@ -713,9 +715,9 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     XS_TRY(ws(ctx, W_SITE_V, ns + 1, s, &sl));
     XS_TRY(ws(ctx, W_SITE_V_ALT, ns + 1, s, &sl_alt));
     XS_TRY(ws(ctx, W_SITE_EV, ns + 1, s, &site_ev));
-    XS_TRY(ws(ctx, W_SITE_SUB, ns + 1, s, &site_sub));
+    XS_TRY(ws(ctx, W_SITE_SUB, ns + 1, s, &site_row));
     XS_CUDA(cudaMemsetAsync(k1, 0xFF, ns * 8, s));  // unused slots: sentinel keys sort last
-    XS_LAUNCH(ctx, k_site_gen, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, lo, tb, site_ev, site_sub, k1);
+    XS_LAUNCH(ctx, k_site_gen, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, lo, tb, site_ev, site_row, k1);
     // 2. Site.order_key: one sort on (pid, anchor, subkind) + local tie order
     XS_LAUNCH(ctx, k_iota_u32, grid_for(ns), XS_BLOCK, 0, s, sl, ns);
     XS_TRY(sort_pairs_u64_u32(ctx, &k1, &k1_alt, &sl, &sl_alt, ns, pb + tb + 3, s));
@@ -729,10 +731,10 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     {
       const int64_t tiles = (ns + XS_BLOCK * Q_ITEMS - 1) / (XS_BLOCK * Q_ITEMS);
       switch (prof->words) {
-        case 1: XS_TRY(launch_quantize<1>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_ev, qslot)); break;
-        case 2: XS_TRY(launch_quantize<2>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_ev, qslot)); break;
-        case 4: XS_TRY(launch_quantize<4>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_ev, qslot)); break;
-        default: XS_TRY(launch_quantize<8>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_ev, qslot)); break;
+        case 1: XS_TRY(launch_quantize<1>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_row, qslot)); break;
+        case 2: XS_TRY(launch_quantize<2>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_row, qslot)); break;
+        case 4: XS_TRY(launch_quantize<4>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_row, qslot)); break;
+        default: XS_TRY(launch_quantize<8>(ctx, tiles, s, k1, sl, d_ns, tb, v, *prof, site_row, qslot)); break;
       }
     }
     ps_q.end();
@@ -748,7 +750,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
       XS_TRY(ws(ctx, W_RSCAN_FLAGS, tiles + 1, s, &flags));
       XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
       XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
-      XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, lenslot, site_sub, lo, hi, removed,
+      XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, lenslot, lo, hi, removed,
                 slab_a, slab_b, slab_pre, pid_slabs, ptotal, desc, flags, tctr);
     }
   }
