@@ -70,9 +70,7 @@ constexpr int BS_NB = 2 * BS_NBW, BS_LOG_NB = 13;  // 16-bit bins (a count or st
 constexpr int BS_BIN_BIG = 256;                // a bin holding more records sends the chunk to the block radix sort
 
 struct BsSmem {
-  uint64_t k[BK_CAP];  // keys relative to the chunk base: load order, then sorted; radix scratch with v[]
-  uint32_t v[BK_CAP];
-  uint64_t sk[BK_CAP];  // grouped by local bin
+  uint64_t sk[BK_CAP];  // keys relative to the chunk base, grouped by local bin; radix scratch with sv[]
   uint32_t sv[BK_CAP];
   unsigned bins[BS_NBW];  // 16-bit counts, then exclusive starts
   uint64_t wmin[BK_THREADS / 32], wmax[BK_THREADS / 32];
@@ -83,13 +81,16 @@ struct BsIAdd {
   __device__ int operator()(int x, int y) const { return x + y; }
 };
 
-// One CTA per chunk (a contiguous key range of <= BK_CAP records).  Sorted in
-// shared memory by one counting pass over BS_NB bins spanning exactly the
-// chunk's [min key, max key] (the bins follow how the keys cluster), then by
-// direct comparison inside each bin -- a handful of records, none when a bin
-// holds one key value.  A bin denser than BS_BIN_BIG sends the chunk to a
-// block radix sort on the chunk's key bits.
-__global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __restrict__ keys,
+// One CTA per chunk (a contiguous key range of <= BK_CAP records).  The
+// keys stay in registers from the load to the bin scatter; sorted by one
+// counting pass over BS_NB bins spanning exactly the chunk's [min key, max
+// key] (the bins follow how the keys cluster), then by direct comparison
+// inside each bin -- a handful of records, none when a bin holds one key
+// value -- and written straight to their final slot (every write lands in the
+// chunk's own window of the output).  Two shared arrays + the bins (~64 KB):
+// 3 CTAs per SM.  A bin denser than BS_BIN_BIG sends the chunk to a block
+// radix sort on the chunk's key bits.
+__global__ void __launch_bounds__(BK_THREADS, 3) k_bs_local(const uint64_t* __restrict__ keys,
                                                            const uint32_t* __restrict__ vals,
                                                            const int64_t* __restrict__ chunk, int shift,
                                                            uint64_t* okeys, uint32_t* ovals, Stats* st) {
@@ -111,16 +112,16 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
     int4* b4 = reinterpret_cast<int4*>(S.bins);
     for (int i = t; i < BS_NBW / 4; i += BK_THREADS) b4[i] = make_int4(0, 0, 0, 0);
   }
+  uint64_t kr[BK_ITEMS];
   uint64_t kmin = ~0ull, kmax = 0;
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
+    kr[j] = 0;
     if (idx < cnt) {
-      const uint64_t k = keys[s0 + idx] - base;
-      S.k[idx] = k;
-      S.v[idx] = vals ? vals[s0 + idx] : 0u;
-      kmin = k < kmin ? k : kmin;
-      kmax = k > kmax ? k : kmax;
+      kr[j] = keys[s0 + idx] - base;
+      kmin = kr[j] < kmin ? kr[j] : kmin;
+      kmax = kr[j] > kmax ? kr[j] : kmax;
     }
   }
 #pragma unroll
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
     const int idx = j * BK_THREADS + t;
     uint32_t sl = 0;
     if (idx < cnt) {
-      const uint32_t b = (uint32_t)((S.k[idx] - kmin) >> s2), h = 16 * (b & 1);
+      const uint32_t b = (uint32_t)((kr[j] - kmin) >> s2), h = 16 * (b & 1);
       sl = (atomicAdd(&S.bins[b >> 1], 1u << h) >> h) & 0xFFFFu;
     }
     if (j & 1) slot[j >> 1] |= sl << 16;
@@ -183,15 +184,16 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
       b4[q] = make_uint4(w[4 * q] + pp, w[4 * q + 1] + pp, w[4 * q + 2] + pp, w[4 * q + 3] + pp);
   }
   big = __syncthreads_or(big) != 0;
+  // values are read only now (coalesced, like the keys): they never occupy
+  // registers through the bin pass
 #pragma unroll
   for (int j = 0; j < BK_ITEMS; j++) {
     const int idx = j * BK_THREADS + t;
     if (idx < cnt) {
-      const uint64_t k = S.k[idx];
-      const uint32_t b = (uint32_t)((k - kmin) >> s2);
+      const uint32_t b = (uint32_t)((kr[j] - kmin) >> s2);
       const int at = (int)((S.bins[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) + (int)((slot[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
-      S.sk[at] = k;
-      S.sv[at] = S.v[idx];
+      S.sk[at] = kr[j];
+      S.sv[at] = vals ? vals[s0 + idx] : 0u;
     }
   }
   __syncthreads();
@@ -213,23 +215,14 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
         }
         at = bs + r;
       }
-      S.k[at] = k;
-      S.v[at] = S.sv[i];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < BK_ITEMS; j++) {  // coalesced write-back
-      const int idx = j * BK_THREADS + t;
-      if (idx < cnt) {
-        okeys[s0 + idx] = base + S.k[idx];
-        if (ovals) ovals[s0 + idx] = S.v[idx];
-      }
+      okeys[s0 + at] = base + k;
+      if (ovals) ovals[s0 + at] = S.sv[i];
     }
     return;
   }
   // a dense bin: block radix sort of the whole chunk on lbits
   using BRS = cub::BlockRadixSort<uint64_t, BK_THREADS, BK_ITEMS, uint32_t, 4>;
-  static_assert(sizeof(typename BRS::TempStorage) <= sizeof(S.k) + sizeof(S.v), "radix scratch");
+  static_assert(sizeof(typename BRS::TempStorage) <= sizeof(S.sk) + sizeof(S.sv) + sizeof(S.bins), "radix scratch");
   uint64_t kk[BK_ITEMS];
   uint32_t vv[BK_ITEMS];
 #pragma unroll
@@ -238,7 +231,8 @@ __global__ void __launch_bounds__(BK_THREADS, 2) k_bs_local(const uint64_t* __re
     kk[j] = idx < cnt ? S.sk[idx] : ~0ull;
     vv[j] = idx < cnt ? S.sv[idx] : 0u;
   }
-  typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(S.k);
+  __syncthreads();
+  typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(S.sk);
   // padding (~0, blocked at the end) stays after equal real keys: the sort is stable
   BRS(tmp).Sort(kk, vv, 0, lbits < 1 ? 1 : lbits);
 #pragma unroll
