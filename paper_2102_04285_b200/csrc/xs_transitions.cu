@@ -60,7 +60,7 @@ __global__ void k_trec(EventView v, int64_t n, const int64_t* lo, int tb, int sr
   bool is_src = i < n && c >= 1 && c <= 3 && ((src_mask >> c) & 1) && v.dur[i] > 0;
   bool is_dst = i < n && c >= 2 && c <= 4 && ((dst_mask >> c) & 1);
   int k = (is_src ? 2 : 0) + (is_dst ? 1 : 0);
-  unsigned long long at = warp_reserve(count, (unsigned)k);  // whole warp participates
+  unsigned long long at = block_reserve(count, (unsigned)k);  // whole block participates
   if (!k) return;
   int p = v.ev.pid[i];
   uint64_t g = (uint64_t)tg[v.ev.tid[i]];  // dense over the groups carrying such events (order kept)
