@@ -231,7 +231,6 @@ __global__ void k_compact_cells(GHist hist, int64_t total, int n_nodes, int* cel
                                 int* cell_node, int* cell_mask, int64_t* cell_ns, int64_t* tracked,
                                 unsigned long long* count) {
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot - threadIdx.x % 32 >= total) return;  // (whole warps leave together)
   const unsigned long long vv = slot < total ? hist.val[slot] : 0ull;
   int p = 0, node = 0, mask = 0;
   if (vv) {
@@ -242,16 +241,10 @@ __global__ void k_compact_cells(GHist hist, int64_t total, int n_nodes, int* cel
     node = (int)(row % n_nodes);
     if (mask == 0 && node == 0) tracked[p] = (int64_t)vv;
   }
-  // one counter atomic per warp: lanes with a cell take consecutive slots
+  // one counter atomic per block: threads with a cell take consecutive slots
   const bool cell = vv && mask != 0;
-  const unsigned ballot = __ballot_sync(0xffffffffu, cell);
-  if (!ballot) return;
-  const int lane = threadIdx.x % 32;
-  unsigned long long base = 0;
-  if (lane == __ffs(ballot) - 1) base = atomicAdd(count, (unsigned long long)__popc(ballot));
-  base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+  const unsigned long long at = block_reserve(count, cell ? 1u : 0u);
   if (!cell) return;
-  const unsigned long long at = base + __popc(ballot & ((1u << lane) - 1));
   cell_pid[at] = p;
   cell_node[at] = node;
   cell_mask[at] = mask;
