@@ -101,13 +101,26 @@ __device__ __forceinline__ bool site_less(const EventView& v, int ix, int iy, bo
   return ix < iy;
 }
 
-__global__ void k_tie_fix(EventView v, const uint64_t* k1, uint32_t* slot, int64_t ns, const int* site_ev) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// sort values = slot ids; the unused tail of the upper-bound site arrays
+// ([device count, ns)) gets sentinel keys that sort last
+__global__ void k_site_tail(uint64_t* k1, uint32_t* sl, int64_t ns, const int64_t* d_ns) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= ns) return;
-  const uint64_t k = k1[q];
-  if (k == ~0ull) return;  // unused upper-bound slots sort last
-  if (q > 0 && k1[q - 1] == k) return;
-  if (q + 1 >= ns || k1[q + 1] != k) return;
+  sl[q] = (uint32_t)q;
+  if (q >= *d_ns) k1[q] = ~0ull;
+}
+
+__global__ void k_tie_fix(EventView v, const uint64_t* k1, uint32_t* slot, int64_t ns, const int* site_ev) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  // run starts from one key load per thread: neighbours by shuffle
+  const uint64_t k = q < ns ? k1[q] : ~0ull;
+  uint64_t kp = __shfl_up_sync(0xffffffffu, k, 1), kn = __shfl_down_sync(0xffffffffu, k, 1);
+  if (lane == 0) kp = q > 0 && q < ns ? k1[q - 1] : ~k;
+  if (lane == 31) kn = q + 1 < ns ? k1[q + 1] : ~k;
+  if (q >= ns || k == ~0ull) return;  // unused upper-bound slots sort last
+  if (q > 0 && kp == k) return;
+  if (q + 1 >= ns || kn != k) return;
   int64_t e = q + 1;
   while (e < ns && k1[e] == k) e++;
   const bool transition = (k & 7u) == TRANSITION_HOOK;
@@ -310,6 +323,11 @@ __global__ void k_caps(EventView v, int64_t n, const int* cnt, const int* pos, c
     if (sf[h]) atomic_add_i64(&shortfall[(int64_t)p * 4 + h], sf[h]);
 }
 
+// one nonzero removal slab: [a, b) and the total slab length before it
+struct Slab {
+  int64_t a, b, pre, pad;
+};
+
 // (max,+) RemovalMap scan, segmented by pid; slab count is global
 struct RM {
   int64_t P;  // sum of max(0, len)
@@ -351,7 +369,7 @@ constexpr int R_ITEMS = XS_R_ITEMS;
 __global__ void __launch_bounds__(XS_BLOCK, XS_REMOVAL_MINB) k_removal(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
                                                       const int64_t* lenslot,
                                                       const int64_t* lo, const int64_t* hi, int64_t* removed,
-                                                      int64_t* slab_a, int64_t* slab_b, int64_t* slab_pre,
+                                                      Slab* slabs,
                                                       int* pid_slabs, int64_t* ptotal, TileDesc<RM>* desc,
                                                       int* flags, int* tile_ctr) {
   const int tile = next_tile(tile_ctr);
@@ -413,9 +431,7 @@ __global__ void __launch_bounds__(XS_BLOCK, XS_REMOVAL_MINB) k_removal(const uin
     acc[hook_of(sub[j])] += mb - ma;
     if (len[j] > 0) {
       const int64_t at = cur.cnt;
-      slab_a[at] = a;
-      slab_b[at] = b;
-      slab_pre[at] = cur.P;
+      slabs[at] = Slab{a, b, cur.P, 0};
       nsl++;
       tot += len[j];
     }
@@ -443,17 +459,18 @@ __global__ void k_slab_base(const int* pid_slabs, int np, int64_t* slab_base) {
 }
 
 // RemovalMap.__call__ (_timeline.py:112-117) on a relative coordinate
-__device__ __forceinline__ int64_t rmap_removed(int64_t y, const int64_t* sa, const int64_t* sb, const int64_t* spre,
+__device__ __forceinline__ int64_t rmap_removed(int64_t y, const Slab* sl,
                                                 int64_t base, int64_t K, int64_t total) {
   int64_t lo = 0, hi = K;  // bisect_right(ends, y)
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
-    if (sb[base + mid] <= y) lo = mid + 1;
+    if (sl[base + mid].b <= y) lo = mid + 1;
     else hi = mid;
   }
   if (lo == K) return total;
-  int64_t r = spre[base + lo];
-  int64_t a = sa[base + lo];
+  const Slab x = sl[base + lo];  // (a, b, prefix in one 32-byte sector)
+  int64_t r = x.pre;
+  int64_t a = x.a;
   if (a < y) r += y - a;
   return r;
 }
@@ -468,7 +485,7 @@ __device__ __forceinline__ int rmap_shift(const int64_t* lo, const int64_t* hi, 
   return b > logw ? b - logw : 0;
 }
 
-__global__ void k_rmap_index(int np, int logw, const int64_t* lo, const int64_t* hi, const int64_t* sb,
+__global__ void k_rmap_index(int np, int logw, const int64_t* lo, const int64_t* hi, const Slab* sl,
                              const int64_t* slab_base, int32_t* idx) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t W = (int64_t)1 << logw;
@@ -484,32 +501,33 @@ __global__ void k_rmap_index(int np, int logw, const int64_t* lo, const int64_t*
   int64_t a = 0, b = K;  // bisect_right(ends, x)
   while (a < b) {
     const int64_t m = (a + b) >> 1;
-    if ((uint64_t)sb[base + m] <= x) a = m + 1;
+    if ((uint64_t)sl[base + m].b <= x) a = m + 1;
     else b = m;
   }
   idx[t] = (int32_t)a;
 }
 
-__device__ __forceinline__ int64_t rmap_removed_idx(int64_t y, const int64_t* sa, const int64_t* sb,
-                                                    const int64_t* spre, int64_t base, int64_t K, int64_t total,
+__device__ __forceinline__ int64_t rmap_removed_idx(int64_t y, const Slab* sl, int64_t base, int64_t K,
+                                                    int64_t total,
                                                     const int32_t* pidx, int logw, int shift) {
   const int64_t W = (int64_t)1 << logw;
   const int64_t w = y >> shift;  // y in [0, span]: w < W
   int64_t a = pidx[w], b = w + 1 < W ? pidx[w + 1] : K;
   while (a < b) {
     const int64_t m = (a + b) >> 1;
-    if (sb[base + m] <= y) a = m + 1;
+    if (sl[base + m].b <= y) a = m + 1;
     else b = m;
   }
   if (a == K) return total;
-  int64_t r = spre[base + a];
-  const int64_t s = sa[base + a];
+  const Slab x = sl[base + a];
+  int64_t r = x.pre;
+  const int64_t s = x.a;
   if (s < y) r += y - s;
   return r;
 }
 
-__global__ void k_remap(EventView v, int64_t n, const int64_t* lo, const int64_t* hi, const int64_t* sa,
-                        const int64_t* sb, const int64_t* spre, const int64_t* slab_base, const int64_t* ptotal,
+__global__ void k_remap(EventView v, int64_t n, const int64_t* lo, const int64_t* hi, const Slab* sl,
+                        const int64_t* slab_base, const int64_t* ptotal,
                         const int32_t* idx, int logw, int64_t* out_start, int64_t* out_dur) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -519,18 +537,18 @@ __global__ void k_remap(EventView v, int64_t n, const int64_t* lo, const int64_t
   int64_t l = lo[p];
   const int shift = rmap_shift(lo, hi, p, logw);
   const int32_t* pidx = idx + ((int64_t)p << logw);
-  int64_t s2 = s - rmap_removed_idx(s - l, sa, sb, spre, base, K, tot, pidx, logw, shift);
+  int64_t s2 = s - rmap_removed_idx(s - l, sl, base, K, tot, pidx, logw, shift);
   out_start[i] = s2;
   if (v.ev.cat[i] == 5) {
     out_dur[i] = d;
   } else {
     int64_t e = s + d;
-    out_dur[i] = (e - rmap_removed_idx(e - l, sa, sb, spre, base, K, tot, pidx, logw, shift)) - s2;
+    out_dur[i] = (e - rmap_removed_idx(e - l, sl, base, K, tot, pidx, logw, shift)) - s2;
   }
 }
 
 __global__ void k_remap_queries(int64_t n, const int32_t* qp, const int64_t* qv, int64_t* out, const int64_t* lo,
-                                const int64_t* sa, const int64_t* sb, const int64_t* spre, const int64_t* slab_base,
+                                const Slab* sl, const int64_t* slab_base,
                                 const int64_t* ptotal, int np) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -541,7 +559,7 @@ __global__ void k_remap_queries(int64_t n, const int32_t* qp, const int64_t* qv,
     return;
   }
   int64_t base = slab_base[p], K = slab_base[p + 1] - base;
-  out[i] = y - rmap_removed(y - lo[p], sa, sb, spre, base, K, ptotal[p]);
+  out[i] = y - rmap_removed(y - lo[p], sl, base, K, ptotal[p]);
 }
 
 __global__ void k_totals(const int64_t* lo, const int64_t* hi, int np, Stats* st, int which) {
@@ -701,10 +719,8 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     XS_TRY(scan_exclusive<int>(ctx, ArrayIn<int>{cnt}, pos, n, s));
     XS_LAUNCH(ctx, k_site_total, 1, 32, 0, s, pos, cnt, n, d_ns);
   }
-  int64_t *slab_a, *slab_b, *slab_pre;
-  XS_TRY(ws(ctx, W_SLAB_A, ns + 1, s, &slab_a));
-  XS_TRY(ws(ctx, W_SLAB_B, ns + 1, s, &slab_b));
-  XS_TRY(ws(ctx, W_SLAB_PRE, ns + 1, s, &slab_pre));
+  Slab* slabs;  // (a, b, prefix) per nonzero slab, interleaved
+  XS_TRY(ws(ctx, W_SLAB_A, ns + 1, s, &slabs));
   if (ns > 0) {
     int* site_ev;
     int* site_row;
@@ -716,10 +732,9 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     XS_TRY(ws(ctx, W_SITE_V_ALT, ns + 1, s, &sl_alt));
     XS_TRY(ws(ctx, W_SITE_EV, ns + 1, s, &site_ev));
     XS_TRY(ws(ctx, W_SITE_SUB, ns + 1, s, &site_row));
-    XS_CUDA(cudaMemsetAsync(k1, 0xFF, ns * 8, s));  // unused slots: sentinel keys sort last
     XS_LAUNCH(ctx, k_site_gen, grid_for(n), XS_BLOCK, 0, s, v, n, cnt, pos, lo, tb, site_ev, site_row, k1);
+    XS_LAUNCH(ctx, k_site_tail, grid_for(ns), XS_BLOCK, 0, s, k1, sl, ns, d_ns);
     // 2. Site.order_key: one sort on (pid, anchor, subkind) + local tie order
-    XS_LAUNCH(ctx, k_iota_u32, grid_for(ns), XS_BLOCK, 0, s, sl, ns);
     XS_TRY(sort_pairs_u64_u32(ctx, &k1, &k1_alt, &sl, &sl_alt, ns, pb + tb + 3, s));
     XS_LAUNCH(ctx, k_tie_fix, grid_for(ns), XS_BLOCK, 0, s, v, k1, sl, ns, site_ev);
     ps_sites.end();
@@ -751,7 +766,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
       XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
       XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
       XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, lenslot, lo, hi, removed,
-                slab_a, slab_b, slab_pre, pid_slabs, ptotal, desc, flags, tctr);
+                slabs, pid_slabs, ptotal, desc, flags, tctr);
     }
   }
   XS_LAUNCH(ctx, k_slab_base, 1, 32, 0, s, pid_slabs, np, slab_base);
@@ -765,9 +780,9 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
     int32_t* ridx;
     XS_TRY(ws(ctx, W_RMAP_IDX, ((int64_t)np << logw) + 1, s, &ridx));
     ctx->rmap_logw = logw;
-    XS_LAUNCH(ctx, k_rmap_index, grid_for((int64_t)np << logw), XS_BLOCK, 0, s, np, logw, lo, hi, slab_b, slab_base,
+    XS_LAUNCH(ctx, k_rmap_index, grid_for((int64_t)np << logw), XS_BLOCK, 0, s, np, logw, lo, hi, slabs, slab_base,
               ridx);
-    XS_LAUNCH(ctx, k_remap, grid_for(n), XS_BLOCK, 0, s, v, n, lo, hi, slab_a, slab_b, slab_pre, slab_base, ptotal,
+    XS_LAUNCH(ctx, k_remap, grid_for(n), XS_BLOCK, 0, s, v, n, lo, hi, slabs, slab_base, ptotal,
               ridx, logw, out_start, out_dur);
   }
   if (corrected_spans) {
@@ -809,32 +824,32 @@ using namespace xs;
 // (the host then redoes the overlap pass with its own operation stage).
 namespace xs {
 __device__ __forceinline__ int64_t ops_strict_map(uint64_t key, int tb, const int64_t* lo, const int64_t* hi,
-                                                  const int64_t* sa, const int64_t* sb, const int64_t* spre,
+                                                  const Slab* sl,
                                                   const int64_t* slab_base, const int64_t* ptotal, const int32_t* idx,
                                                   int logw) {
   const int p = (int)(key >> (tb + 1));
   const int64_t t = (int64_t)((key >> 1) & ((1ull << tb) - 1));
   const int64_t base = slab_base[p], K = slab_base[p + 1] - base;
-  return t - rmap_removed_idx(t, sa, sb, spre, base, K, ptotal[p], idx + ((int64_t)p << logw), logw,
+  return t - rmap_removed_idx(t, sl, base, K, ptotal[p], idx + ((int64_t)p << logw), logw,
                               rmap_shift(lo, hi, p, logw));
 }
 
 // one sampled-index lookup per endpoint; the right neighbour's value comes
 // from the next lane (the warp's last lane looks its neighbour up itself)
 __global__ void k_ops_strict(const uint64_t* pk, int64_t n2, int tb, const int64_t* lo, const int64_t* hi,
-                             const int64_t* sa, const int64_t* sb, const int64_t* spre, const int64_t* slab_base,
+                             const Slab* sl, const int64_t* slab_base,
                              const int64_t* ptotal, const int32_t* idx, int logw, int np, Stats* st) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const uint64_t a = j < n2 ? pk[j] : ~0ull;
   const bool va = a != ~0ull && (int)(a >> (tb + 1)) < np;
-  const int64_t ca = va ? ops_strict_map(a, tb, lo, hi, sa, sb, spre, slab_base, ptotal, idx, logw) : 0;
+  const int64_t ca = va ? ops_strict_map(a, tb, lo, hi, sl, slab_base, ptotal, idx, logw) : 0;
   int64_t cb = __shfl_down_sync(0xffffffffu, ca, 1);
   uint64_t b = __shfl_down_sync(0xffffffffu, a, 1);
   if (lane == 31) {
     b = j + 1 < n2 ? pk[j + 1] : ~0ull;
     const bool vb = b != ~0ull && (int)(b >> (tb + 1)) < np;
-    cb = vb ? ops_strict_map(b, tb, lo, hi, sa, sb, spre, slab_base, ptotal, idx, logw) : 0;
+    cb = vb ? ops_strict_map(b, tb, lo, hi, sl, slab_base, ptotal, idx, logw) : 0;
   }
   if (!va || j + 1 >= n2 || b == ~0ull) return;
   if ((a >> (tb + 1)) != (b >> (tb + 1))) return;  // different pids
@@ -848,8 +863,7 @@ int ops_reuse_check(xs_ctx* ctx, const EventView& v, Stats* verdict, cudaStream_
   if (os.m <= 0 || !os.pk) return XS_OK;
   XS_LAUNCH(ctx, k_ops_strict, grid_for(2 * os.m), XS_BLOCK, 0, s, os.pk, 2 * os.m, os.tb,
             (const int64_t*)ctx->ptr[W_CORR_LO], (const int64_t*)ctx->ptr[W_CORR_HI],
-            (const int64_t*)ctx->ptr[W_SLAB_A], (const int64_t*)ctx->ptr[W_SLAB_B],
-            (const int64_t*)ctx->ptr[W_SLAB_PRE], (const int64_t*)ctx->ptr[W_SLAB_BASE],
+            (const Slab*)ctx->ptr[W_SLAB_A], (const int64_t*)ctx->ptr[W_SLAB_BASE],
             (const int64_t*)ctx->ptr[W_PTOTAL], (const int32_t*)ctx->ptr[W_RMAP_IDX], ctx->rmap_logw, v.ev.n_pids,
             verdict);
   return XS_OK;
@@ -865,8 +879,7 @@ int xs_remap(xs_ctx_t* ctx, int64_t n, const int32_t* pid_dev, const int64_t* va
   if (n <= 0) return XS_OK;
   cudaStream_t s = (cudaStream_t)stream;
   XS_LAUNCH(ctx, k_remap_queries, grid_for(n), XS_BLOCK, 0, s, n, pid_dev, val_dev, out_dev,
-            (const int64_t*)ctx->ptr[W_CORR_LO], (const int64_t*)ctx->ptr[W_SLAB_A],
-            (const int64_t*)ctx->ptr[W_SLAB_B], (const int64_t*)ctx->ptr[W_SLAB_PRE],
+            (const int64_t*)ctx->ptr[W_CORR_LO], (const Slab*)ctx->ptr[W_SLAB_A],
             (const int64_t*)ctx->ptr[W_SLAB_BASE], (const int64_t*)ctx->ptr[W_PTOTAL], ctx->corr_pids);
   return XS_OK;
 }
