@@ -201,8 +201,10 @@ static __global__ void k_bucket_chunks(const int64_t* offs, int64_t nb, int64_t 
     s = offs[b];
     e = bn < nb ? offs[bn] : total;
     // half 0: bucket holding key s; half 1: bucket holding key e-1, plus one
-    const int64_t r2 = h1 ? half_search_i64<true>(offs, b, nb + 1, e - 1)
-                          : half_search_i64<true>(offs, b, nb + 1, s) - 1;
+    // both lie in [b, bn]: offs[bn] >= e (or bn = nb, offs[nb] = total = e)
+    const int64_t hi = (bn < nb ? bn : nb) + 1;
+    const int64_t r2 = h1 ? half_search_i64<true>(offs, b, hi, e - 1)
+                          : half_search_i64<true>(offs, b, hi, s) - 1;
     b0 = __shfl_sync(0xffffffffu, r2, 0);
     b1 = __shfl_sync(0xffffffffu, r2, 16);
   }
