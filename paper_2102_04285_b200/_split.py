@@ -21,6 +21,8 @@ RuntimeError naming the limit.
 
 from __future__ import annotations
 
+from typing import Optional
+
 import numpy as np
 
 from .columnar import ColumnarTrace
@@ -102,3 +104,127 @@ def sub_trace(ct: ColumnarTrace, pids: list, rows_by_pid: list):
                         ct.pids[pids], pid_map[ct.group_pid[gsel]], ct.group_tid[gsel], ct.names, ct.processes,
                         ct.pid_has_meta[pids])
     return sub, rows
+
+
+# ---------------------------------------------------------------------------
+# Processes too wide for one call's keys (compute_overlap only)
+#
+# A process whose span needs more than WIDE_BITS bits cannot be keyed even
+# alone (time + 4 code bits > 64).  Its overlap is computed over time windows
+# [c_k, c_{k+1}) of span < 2^WIDE_BITS cut at instants where:
+#   * no OPERATION strictly contains the cut (ranks, nesting and paths are
+#     then window-local: overlap.py:96-99, 132-142 only compare operations
+#     active at one instant), nor a correlated GPU event;
+#   * no correlated GPU event sits on the other side of the cut from its
+#     launcher (the launcher -- the earliest ACCEL_API with the id,
+#     overlap.py:144-163 -- and the path at its start are then in the GPU
+#     event's window, and the dangling-correlation rule is window-local).
+# Resource events are clipped to each window they overlap; operations and
+# zero-duration events go to the window holding their start.  The sweep of a
+# window accounts exactly its part of the timeline (_sweep_py.py:29-115 is a
+# function of the active set at each instant), so cells and tracked time add
+# up over windows and the span is the union of the window spans.
+# ---------------------------------------------------------------------------
+WIDE_BITS = 59
+
+
+def wide_pids(ct: ColumnarTrace) -> list:
+    """Pid indices whose own span needs more than WIDE_BITS bits."""
+    if ct.n == 0:
+        return []
+    lo, hi = pid_spans_host(ct)
+    return [p for p in range(ct.n_pids) if hi[p] >= lo[p] and _bits(int(hi[p]) - int(lo[p])) > WIDE_BITS]
+
+
+def _forbidden(sub: ColumnarTrace) -> np.ndarray:
+    """[k, 2] closed integer ranges of instants that may not be cuts (merged,
+    sorted): (start, end) of every operation and correlated GPU event,
+    (first, last] of every launcher / correlated GPU event pair."""
+    rng = []
+    # operations and correlated GPU events are never cut (a clipped GPU piece
+    # would lose its launcher -- the fixed path -- and its dangling check)
+    op = (sub.cat == 0) | ((sub.cat == 5) & (sub.has_corr == 1))
+    s, e = sub.start[op], sub.start[op] + sub.dur[op]
+    m = e - s > 1
+    if m.any():
+        rng.append(np.stack([s[m] + 1, e[m] - 1], axis=1))
+    api = (sub.cat == 4) & (sub.has_corr == 1)
+    gpu = (sub.cat == 5) & (sub.has_corr == 1)
+    if api.any() and gpu.any():
+        # launcher = earliest ACCEL_API per id by Event.sort_key; its start
+        # is what matters, and the earliest start is a lower bound for it
+        ac, ast = sub.corr[api], sub.start[api]
+        order = np.lexsort((ast, ac))
+        ac, ast = ac[order], ast[order]
+        first = np.r_[True, ac[1:] != ac[:-1]]
+        ids, lstart = ac[first], ast[first]
+        gc, gs = sub.corr[gpu], sub.start[gpu]
+        k = np.searchsorted(ids, gc)
+        ok = (k < ids.size) & (ids[np.minimum(k, ids.size - 1)] == gc)
+        ls = lstart[np.minimum(k, ids.size - 1)][ok]
+        g = gs[ok]
+        a, b = np.minimum(ls, g), np.maximum(ls, g)
+        m = b > a
+        if m.any():
+            rng.append(np.stack([a[m] + 1, b[m]], axis=1))
+    if not rng:
+        return np.zeros((0, 2), np.int64)
+    r = np.concatenate(rng)
+    r = r[np.argsort(r[:, 0], kind="stable")]
+    out = []
+    cs, ce = int(r[0, 0]), int(r[0, 1])
+    for a, b in r[1:]:
+        a, b = int(a), int(b)
+        if a <= ce + 1:
+            ce = max(ce, b)
+        else:
+            out.append((cs, ce))
+            cs, ce = a, b
+    out.append((cs, ce))
+    return np.asarray(out, np.int64)
+
+
+def wide_cuts(sub: ColumnarTrace) -> list:
+    """Cut instants for a one-process trace so that every window spans fewer
+    than 2^WIDE_BITS ns; ValueError when a forbidden range (a long operation,
+    or a launcher far from its kernel) is itself that wide."""
+    lo = int(sub.start.min())
+    hi = int((sub.start + sub.dur).max())
+    step = 1 << (WIDE_BITS - 1)
+    bad = _forbidden(sub)
+    cuts, prev = [], lo
+    while hi - prev >= (1 << WIDE_BITS) - 1:
+        target = prev + step
+        # the largest valid instant in (prev, target]: target itself unless a
+        # forbidden range holds it, then just before that range
+        k = int(np.searchsorted(bad[:, 0], target, side="right")) - 1 if bad.size else -1
+        c = target
+        if k >= 0 and bad[k, 1] >= target:
+            c = int(bad[k, 0]) - 1
+        if c <= prev:  # a forbidden range covers (prev, target]: cut right after it
+            c = int(bad[k, 1]) + 1
+            if c - prev >= 1 << WIDE_BITS:
+                raise ValueError("a single operation (or a launcher / kernel pair) spans >= 2^59 ns: "
+                                 "no operation-free instant to cut the process at")
+        cuts.append(c)
+        prev = c
+    return cuts
+
+
+def window_trace(sub: ColumnarTrace, a: Optional[int], b: Optional[int]) -> ColumnarTrace:
+    """The events of a one-process trace in window [a, b): resource events
+    clipped to it, operations and zero-duration events by their start."""
+    lo = np.iinfo(np.int64).min if a is None else a
+    hi = np.iinfo(np.int64).max if b is None else b
+    end = sub.start + sub.dur
+    point = ((sub.dur == 0) | (sub.cat == 0)) & (sub.start >= lo) & (sub.start < hi)
+    span = (sub.dur > 0) & (sub.cat != 0) & (sub.start < hi) & (end > lo)
+    rows = np.nonzero(point | span)[0]
+    s = sub.start[rows]
+    e = end[rows]
+    clip = (sub.cat[rows] != 0) & (sub.dur[rows] > 0)
+    s2 = np.where(clip, np.maximum(s, lo), s)
+    e2 = np.where(clip, np.minimum(e, hi), e)
+    return ColumnarTrace(sub.clock_domain, s2, e2 - s2, sub.pid[rows], sub.tid[rows], sub.cat[rows], sub.name[rows],
+                         sub.corr[rows], sub.has_corr[rows], sub.pids, sub.group_pid, sub.group_tid, sub.names,
+                         sub.processes, sub.pid_has_meta)

@@ -226,7 +226,7 @@ def compute_overlap_columnar(ct: ColumnarTrace, attribution: Attribution = Attri
     except _engine.XsError as exc:
         if exc.status == _lib.XS_INVALID_TRACE:
             _raise_invalid(_source if _source is not None else ct, ct)
-        if exc.status == _lib.XS_UNSUPPORTED and device_trace is None and ct.n_pids > 1:
+        if exc.status == _lib.XS_UNSUPPORTED and device_trace is None:
             return _overlap_batched(ct, attribution, _source)  # keys too wide for all pids at once
         raise
     return decode_breakdown(ct, raw)
@@ -242,15 +242,65 @@ def merge_breakdowns(parts) -> Breakdown:
     return bd
 
 
+def _merge_windows(parts) -> Breakdown:
+    """Breakdowns of time windows of the same pids -> one Breakdown: cells
+    and tracked time add up, spans are unions."""
+    bd = Breakdown()
+    cells, tracked = {}, {}
+    for b in parts:
+        for k, v in b.cells.items():
+            cells[k] = cells.get(k, 0) + v
+        for pid, (lo, hi) in b.spans.items():
+            tracked[pid] = tracked.get(pid, 0) + (hi - lo) - b.untracked[pid]
+            if pid in bd.spans:
+                l0, h0 = bd.spans[pid]
+                bd.spans[pid] = (min(l0, lo), max(h0, hi))
+            else:
+                bd.spans[pid] = (lo, hi)
+    bd.cells = cells
+    for pid, (lo, hi) in bd.spans.items():
+        bd.untracked[pid] = (hi - lo) - tracked[pid]
+    return bd
+
+
+def _overlap_wide(ct: ColumnarTrace, p: int, rows_by_pid, attr: int, _source) -> Breakdown:
+    """One process too wide for one call's keys, over operation-free time
+    windows (_split.wide_cuts / window_trace)."""
+    eng = _engine.get()
+    sub, _ = _split.sub_trace(ct, [p], rows_by_pid)
+    try:
+        cuts = _split.wide_cuts(sub)
+    except ValueError as exc:
+        raise _engine.XsError(_lib.XS_UNSUPPORTED, f"xs_overlap: unsupported input {exc}") from None
+    bounds = [None] + cuts + [None]
+    parts = []
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        win = _split.window_trace(sub, a, b)
+        if win.n == 0:
+            continue
+        try:
+            raw = eng.overlap(_engine.DeviceTrace(win, eng.device), attr)
+        except _engine.XsError as exc:
+            if exc.status == _lib.XS_INVALID_TRACE:
+                _raise_invalid(_source if _source is not None else ct, ct)
+            raise
+        parts.append(decode_breakdown(win, raw, lazy=False))
+    return _merge_windows(parts)
+
+
 def _overlap_batched(ct: ColumnarTrace, attribution, _source) -> Breakdown:
     """compute_overlap over pid batches (_split: more rows than one call
     takes, or keys wider than 64 bits over all pids); exact because every
-    cell, span and untracked value is per pid (overlap.py:126)."""
+    cell, span and untracked value is per pid (overlap.py:126).  A process
+    too wide for one call's keys by itself goes through time windows."""
     eng = _engine.get()
     attr = 1 if Attribution(attribution) is Attribution.CORRELATION else 0
     rows_by_pid = _split.pid_rows(ct)
     parts = []
-    todo = list(reversed(_split.plan_batches(ct)))
+    wide = _split.wide_pids(ct)
+    for p in wide:
+        parts.append(_overlap_wide(ct, p, rows_by_pid, attr, _source))
+    todo = list(reversed([b for b in ([q for q in batch if q not in wide] for batch in _split.plan_batches(ct)) if b]))
     while todo:
         pids = todo.pop()
         sub, _ = _split.sub_trace(ct, pids, rows_by_pid)
