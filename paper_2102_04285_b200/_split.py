@@ -228,3 +228,116 @@ def window_trace(sub: ColumnarTrace, a: Optional[int], b: Optional[int]) -> Colu
     return ColumnarTrace(sub.clock_domain, s2, e2 - s2, sub.pid[rows], sub.tid[rows], sub.cat[rows], sub.name[rows],
                          sub.corr[rows], sub.has_corr[rows], sub.pids, sub.group_pid, sub.group_tid, sub.names,
                          sub.processes, sub.pid_has_meta)
+
+
+# ---------------------------------------------------------------------------
+# Correction of processes too wide for one call's keys: exact gap compression
+#
+# correct_trace depends on times only through their order (site order,
+# transition maximality and coverage, the remap's bisection), owner budgets
+# (durations), and slab extents a = max(anchor, E), b = a + len
+# (_timeline.py:93-117, correction.py:139-157).  Let B bound the process's
+# total removable time (sum over its sites of |amount| + 1).  Shrinking every
+# gap between consecutive event endpoints that is longer than L = B + 1 to
+# length L changes none of these: order is kept (a strictly increasing map),
+# a budget spanning a gap stays >= L > any one site's amounts, and the slab
+# chain E can overrun an anchor by at most B < L, so no slab reaches a
+# shrunk part and the slabs after a gap start at their anchors as before.
+# The correction of the compressed process, shifted back by the compression
+# offset of every endpoint, is the correction of the process
+# (rmap(y) = rmap'(y') + offset(y); a time inside a shrunk gap maps with the
+# gap's slope-1 tail).  Report totals are recomputed from the spans.
+# ---------------------------------------------------------------------------
+class Compression:
+    """Per-pid gap compression: points[p] (sorted endpoints) and cum[p]
+    (offset removed at or before each point), L[p]."""
+
+    def __init__(self):
+        self.points, self.cum, self.L = {}, {}, {}
+
+    def offset_of(self, p: int, t: np.ndarray) -> np.ndarray:
+        """Compression offset of endpoint times of pid p (every t is a point)."""
+        pts, cum = self.points[p], self.cum[p]
+        return cum[np.searchsorted(pts, t)]
+
+    def compress_time(self, p: int, t: int) -> tuple:
+        """(t', offset, tail) for an arbitrary time t of pid p: t' = the
+        compressed time, and the corrected t = rmap'(t') + offset + tail."""
+        pts, cum, L = self.points[p], self.cum[p], self.L[p]
+        k = int(np.searchsorted(pts, t, side="right")) - 1
+        if k < 0:
+            return int(t), 0, 0
+        base = int(pts[k])
+        tail = max(0, int(t) - base - L)
+        return int(t) - tail - int(cum[k]), int(cum[k]), tail
+
+
+def removable_bound(ct: ColumnarTrace, rows: np.ndarray, profile) -> int:
+    """Upper bound on the total time correct_trace can remove from these
+    rows: every site's |amount| + 1 (correction.py:79-112)."""
+    from fractions import Fraction
+    import math
+
+    cat = ct.cat[rows]
+    n_op = int((cat == 0).sum())
+    n_api = int((cat == 4).sum())
+    n_bs = int(((cat == 2) | (cat == 3)).sum())
+    ann = abs(Fraction(profile.annotation_ns))
+    internal = max((abs(Fraction(v)) for v in profile.api_internal_ns.values()), default=Fraction(0))
+    per_op = math.ceil(ann) + 2
+    per_api = math.ceil(abs(Fraction(profile.api_interception_ns))) + math.ceil(internal) + 2
+    per_bs = math.ceil(abs(Fraction(profile.transition_ns))) + 1
+    return n_op * per_op + n_api * per_api + n_bs * per_bs
+
+
+def compress_wide(ct: ColumnarTrace, pids: list, profile) -> tuple:
+    """(compressed trace, Compression) for the given pid indices; the other
+    pids' rows are unchanged.  ValueError when a compressed process is still
+    too wide (its endpoints alone span 2^WIDE_BITS ns at gap length L)."""
+    rows_by_pid = pid_rows(ct)
+    start = ct.start.copy()
+    end = ct.start + ct.dur
+    new_end = end.copy()
+    comp = Compression()
+    for p in pids:
+        rows = rows_by_pid[p]
+        L = removable_bound(ct, rows, profile) + 1
+        pts = np.unique(np.concatenate([ct.start[rows], end[rows]]))
+        d = np.diff(pts)
+        cum = np.concatenate([[0], np.cumsum(np.where(d > L, d - L, 0))]).astype(np.int64)
+        comp.points[p], comp.cum[p], comp.L[p] = pts, cum, L
+        start[rows] = ct.start[rows] - comp.offset_of(p, ct.start[rows])
+        new_end[rows] = end[rows] - comp.offset_of(p, end[rows])
+        if _bits(int(pts[-1] - cum[-1]) - int(pts[0])) > WIDE_BITS:
+            raise ValueError("a process spans >= 2^59 ns even with every idle gap shrunk")
+    procs = []
+    pid_index = {int(v): i for i, v in enumerate(ct.pids.tolist())}
+    from .model import ProcessMeta
+    for m in ct.processes:
+        p = pid_index.get(m.pid)
+        if p in comp.points:
+            fk = None if m.fork_ns is None else comp.compress_time(p, m.fork_ns)[0]
+            jn = None if m.join_ns is None else comp.compress_time(p, m.join_ns)[0]
+            m = ProcessMeta(m.pid, m.name, m.parent, fk, jn)
+        procs.append(m)
+    out = ColumnarTrace(ct.clock_domain, start, new_end - start, ct.pid, ct.tid, ct.cat, ct.name, ct.corr,
+                        ct.has_corr, ct.pids, ct.group_pid, ct.group_tid, ct.names, tuple(procs), ct.pid_has_meta)
+    return out, comp
+
+
+def uncompress_columns(ct: ColumnarTrace, comp: Compression, start_c: np.ndarray, dur_c: np.ndarray) -> tuple:
+    """Corrected columns of the compressed trace -> corrected columns of ct."""
+    start = np.array(start_c, np.int64, copy=True)
+    dur = np.array(dur_c, np.int64, copy=True)
+    rows_by_pid = pid_rows(ct)
+    end = ct.start + ct.dur
+    for p in comp.points:
+        rows = rows_by_pid[p]
+        s_off = comp.offset_of(p, ct.start[rows])
+        e_off = comp.offset_of(p, end[rows])
+        new_s = start[rows] + s_off
+        gpu = ct.cat[rows] == 5
+        new_e = start[rows] + dur[rows] + e_off
+        start[rows] = new_s
+        dur[rows] = np.where(gpu, ct.dur[rows], new_e - new_s)  # GPU events shift only (_timeline.py:120-132)
+    return start, dur

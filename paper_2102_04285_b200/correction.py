@@ -175,6 +175,55 @@ def _batched(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: O
     return start, dur, rep, processes, (merge_breakdowns(parts) if attribution is not None else None)
 
 
+def _span_total(pid: np.ndarray, start: np.ndarray, end: np.ndarray, n_pids: int) -> int:
+    lo = np.full(n_pids, np.iinfo(np.int64).max, np.int64)
+    hi = np.full(n_pids, np.iinfo(np.int64).min, np.int64)
+    np.minimum.at(lo, pid, start)
+    np.maximum.at(hi, pid, end)
+    m = hi >= lo
+    return int(sum(int(h) - int(l) for l, h in zip(lo[m].tolist(), hi[m].tolist())))
+
+
+def _correct_wide(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: Optional[int]):
+    """correct_trace (+ compute_overlap of the result) for a trace holding a
+    process too wide for one call's keys (>= 2^59 ns): exact gap compression
+    (_split.compress_wide), the device correction of the compressed trace,
+    the columns shifted back; the overlap of the corrected trace goes through
+    operation-free time windows.  Returns what _batched returns."""
+    wide = _split.wide_pids(ct)
+    try:
+        ctc, comp = _split.compress_wide(ct, wide, profile)
+    except ValueError as exc:
+        raise _engine.XsError(_lib.XS_UNSUPPORTED, f"xs_correct: unsupported input {exc}") from None
+    try:
+        start_c, dur_c, rep, procs_c, _ = _batched(ctc, profile, ctc, None)
+    except InvalidTraceError:
+        raise InvalidTraceError(format_violations(_source(src, ct))) from None
+    start, dur = _split.uncompress_columns(ct, comp, start_c, dur_c)
+    pid_index = {int(v): i for i, v in enumerate(ct.pids.tolist())}
+    procs = []
+    for m0, m in zip(ct.processes, procs_c):
+        p = pid_index.get(m0.pid)
+        if p in comp.points:
+            def back(t0, t1):
+                if t0 is None:
+                    return None
+                _, off, tail = comp.compress_time(p, t0)
+                return int(t1) + off + tail
+            m = ProcessMeta(m.pid, m.name, m.parent, back(m0.fork_ns, m.fork_ns), back(m0.join_ns, m.join_ns))
+        procs.append(m)
+    rep.original_total_ns = _span_total(ct.pid, ct.start, ct.start + ct.dur, ct.n_pids)
+    rep.corrected_total_ns = _span_total(ct.pid, start, start + dur, ct.n_pids)
+    bd = None
+    if attribution is not None:
+        from .overlap import Attribution, compute_overlap_columnar
+
+        out = ColumnarTrace(ct.clock_domain, start, dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr,
+                            ct.pids, ct.group_pid, ct.group_tid, ct.names, tuple(procs), ct.pid_has_meta)
+        bd = compute_overlap_columnar(out, Attribution.CORRELATION if attribution == 1 else Attribution.INSTANT)
+    return start, dur, rep, tuple(procs), bd
+
+
 def correct_trace_columnar(ct: ColumnarTrace, profile: CalibrationProfile, device_trace=None,
                            _src=None) -> tuple:
     """Columnar correct_trace: returns (corrected ColumnarTrace, CorrectionReport)."""
@@ -186,9 +235,14 @@ def correct_trace_columnar(ct: ColumnarTrace, profile: CalibrationProfile, devic
     try:
         eng, dt, raw = _run(ct, profile, _src if _src is not None else ct, None, device_trace)
     except _engine.XsError as exc:
-        if exc.status != _lib.XS_UNSUPPORTED or device_trace is not None or ct.n_pids < 2:
+        if exc.status != _lib.XS_UNSUPPORTED or device_trace is not None:
             raise
-        start, dur, rep, procs, _ = _batched(ct, profile, _src if _src is not None else ct, None)
+        if _split.wide_pids(ct):
+            start, dur, rep, procs, _ = _correct_wide(ct, profile, _src if _src is not None else ct, None)
+        elif ct.n_pids < 2:
+            raise
+        else:
+            start, dur, rep, procs, _ = _batched(ct, profile, _src if _src is not None else ct, None)
         return ColumnarTrace(ct.clock_domain, start, dur, ct.pid, ct.tid, ct.cat, ct.name, ct.corr, ct.has_corr,
                              ct.pids, ct.group_pid, ct.group_tid, ct.names, procs, ct.pid_has_meta), rep
     procs = _remap_processes(eng, ct)
@@ -227,8 +281,8 @@ def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution
     from .overlap import Attribution, decode_breakdown
 
     attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
-    def batched():
-        start, dur, rep, _, bd = _batched(ct, profile, ct, attr)
+    def batched(wide: bool = False):
+        start, dur, rep, _, bd = (_correct_wide if wide else _batched)(ct, profile, ct, attr)
         if out is not None:
             np.asarray(out[0])[...] = start
             np.asarray(out[1])[...] = dur
@@ -242,7 +296,11 @@ def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution
     try:
         eng, dt, raw = _run(ct, profile, ct, attr, device_trace, host_out=out)
     except _engine.XsError as exc:
-        if exc.status != _lib.XS_UNSUPPORTED or device_trace is not None or ct.n_pids < 2:
+        if exc.status != _lib.XS_UNSUPPORTED or device_trace is not None:
+            raise
+        if _split.wide_pids(ct):
+            return batched(wide=True)  # a process too wide for one call's keys by itself
+        if ct.n_pids < 2:
             raise
         return batched()  # keys too wide for all pids at once (CORRELATION keys also hold path bits)
     bd = decode_breakdown(ct, eng.fetch_overlap())

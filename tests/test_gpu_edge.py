@@ -15,27 +15,20 @@ from paper_2102_04285_b200 import Attribution, ColumnarTrace, analyze_columnar, 
 pytestmark = pytest.mark.gpu
 
 EDGE = load("edge_cases.json.gz")
-# a single process spanning >= 2^60 ns: its endpoint keys cannot fit 64 bits
-# even alone.  compute_overlap cuts it into operation-free time windows
-# (_split.wide_cuts); the correction of such a process is the documented
-# limit, an error, never a wrong result
-_WIDE_ONE = pytest.mark.xfail(raises=RuntimeError, strict=True,
-                              reason="correction of a single process spanning >= 2^60 ns (DESIGN.md 7)")
+# a single process spanning >= 2^60 ns (its endpoint keys cannot fit 64 bits
+# even alone): compute_overlap cuts it into operation-free time windows
+# (_split.wide_cuts), correct_trace shrinks its idle gaps exactly
+# (_split.compress_wide) -- both return the reference's results
 
 
-def _cases(wide_fails: bool):
-    return [pytest.param(c, marks=_WIDE_ONE) if wide_fails and c["name"] == "single_pid_span_2e62" else c
-            for c in EDGE]
-
-
-@pytest.mark.parametrize("case", _cases(False), ids=[c["name"] for c in EDGE])
+@pytest.mark.parametrize("case", EDGE, ids=[c["name"] for c in EDGE])
 def test_edge_overlap_matches_reference(case):
     trace = dec_trace(case["trace"])
     assert enc_breakdown(compute_overlap(trace)) == case["overlap"]["instant"]
     assert enc_breakdown(compute_overlap(trace, Attribution.CORRELATION)) == case["overlap"]["correlation"]
 
 
-@pytest.mark.parametrize("case", _cases(True), ids=[c["name"] for c in EDGE])
+@pytest.mark.parametrize("case", EDGE, ids=[c["name"] for c in EDGE])
 def test_edge_correction_matches_reference(case):
     trace = dec_trace(case["trace"])
     for exp in case["corrections"]:
