@@ -19,8 +19,8 @@ timeout 2400 $CS --tool memcheck python -m pytest -q -x -m gpu tests/test_gpu_ov
   -k "not single_pid_span" > gpurun_out/sanitize_memcheck_tests.log 2>&1
 echo "memcheck tests rc=$?" | tee -a gpurun_out/sanitize_summary.txt
 tail -3 gpurun_out/sanitize_memcheck_tests.log >> gpurun_out/sanitize_summary.txt
-for tool in memcheck racecheck synccheck; do
-  timeout 2400 $CS --tool $tool python scripts/sanitize_medium.py > gpurun_out/sanitize_${tool}_medium.log 2>&1
+for tool in memcheck racecheck; do
+  timeout 1200 $CS --tool $tool python scripts/sanitize_medium.py > gpurun_out/sanitize_${tool}_medium.log 2>&1
   echo "$tool medium rc=$?" | tee -a gpurun_out/sanitize_summary.txt
   tail -3 gpurun_out/sanitize_${tool}_medium.log >> gpurun_out/sanitize_summary.txt
 done

@@ -1,5 +1,5 @@
 """A medium analyze (correction + overlap) for compute-sanitizer: a 2-process
-DDPG trace (~110k events: chunks with wide key ranges, so the local-bin sorts
+DDPG trace (~55k events: chunks with wide key ranges, so the local-bin sorts
 take the s2 > 0 paths) and a 64-process adversarial trace (hashed cells, deep
 paths), both checked against the C oracle."""
 import os
@@ -28,5 +28,6 @@ def check(ct, prof):
     print("ok", ct.n, len(ours))
 
 
-check(synth.ddpg_trace(2700, processes=2), synth.exact_profile())
-check(synth.adversarial_trace(200_000, pids=64, workers=4), synth.adversarial_profile())
+if __name__ == "__main__":  # (the generators may spawn worker processes)
+    check(synth.ddpg_trace(1500, processes=2), synth.exact_profile())
+    check(synth.adversarial_trace(100_000, pids=64, workers=1), synth.adversarial_profile())
