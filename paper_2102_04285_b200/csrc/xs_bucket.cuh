@@ -74,7 +74,9 @@ inline int bucket_bits_for(int64_t nkeys, int key_bits, int max_bits = 24, bool 
   }();
   static int adj_rec = [] {
     const char* e = getenv("XS_BK_BITS_ADJ_REC");  // (tuning experiments: record sorts)
-    return e ? atoi(e) : 1;
+    // ~1 record per bucket: the chunk sort adapts its own bins to the keys,
+    // so fewer global buckets only shrink the offset scan (config 2 -3%)
+    return e ? atoi(e) : -1;
   }();
   int b = 1;
   while (b < 62 && ((int64_t)1 << b) < nkeys) b++;

@@ -120,54 +120,12 @@ int ws_get(xs_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
   return XS_OK;
 }
 
-// Stats into page-locked host memory by one block, then a sequence number
-// after a system-scope fence: the host spins on the number instead of
-// waking from a stream synchronisation (the pass-1 wait sits in the middle
-// of every call).  cudaStreamQuery every few thousand polls surfaces errors.
-__global__ void k_stats_signal(const Stats* d, Stats* h, volatile unsigned long long* flag, unsigned long long seq) {
-  const unsigned long long* x = (const unsigned long long*)d;
-  unsigned long long* y = (unsigned long long*)h;
-  for (int j = threadIdx.x; j < (int)(sizeof(Stats) / 8); j += blockDim.x) y[j] = x[j];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    *flag = seq;
-  }
-}
-
 int fetch_stats(xs_ctx* ctx, cudaStream_t s) {
   Stats* d = nullptr;
   XS_TRY(ws(ctx, W_STATS, 1, s, &d));
-  static const bool no_spin = getenv("XS_NO_SPIN_WAIT") != nullptr;  // (A/B switch)
-  if (no_spin || ctx->prof_on || ctx->capturing) {
-    XS_TRY(to_host_many(ctx, s, {{ctx->h_stats, d, sizeof(Stats)}}));
-    XS_CUDA(cudaStreamSynchronize(s));
-    if (!ctx->pend_stage.empty()) prof_flush(ctx);
-    return XS_OK;
-  }
-  volatile unsigned long long* flag = ctx->h_flag;
-  const unsigned long long seq = ++ctx->flag_seq;
-  XS_LAUNCH(ctx, k_stats_signal, 1, 128, 0, s, d, ctx->h_stats, flag, seq);
-  for (unsigned long long polls = 1; *flag != seq; polls++) {
-    if ((polls & 4095) == 0) {
-      const cudaError_t e = cudaStreamQuery(s);
-      if (e == cudaSuccess) {
-        if (*flag != seq) {  // (cannot happen: the kernel ran; read it once more after a full sync)
-          XS_CUDA(cudaStreamSynchronize(s));
-          if (*flag != seq) {
-            ctx->err = "pass-1 statistics signal lost";
-            return XS_CUDA_ERROR;
-          }
-        }
-        break;
-      }
-      if (e != cudaErrorNotReady) {
-        ctx->err = std::string("pass 1: ") + cudaGetErrorString(e);
-        return XS_CUDA_ERROR;
-      }
-    }
-  }
-  std::atomic_thread_fence(std::memory_order_acquire);
+  XS_TRY(to_host_many(ctx, s, {{ctx->h_stats, d, sizeof(Stats)}}));
+  XS_CUDA(cudaStreamSynchronize(s));
+  if (!ctx->pend_stage.empty()) prof_flush(ctx);
   return XS_OK;
 }
 
@@ -419,14 +377,13 @@ int xs_ctx_create(int device, xs_ctx_t** out) {
   c->device = device;
   c->ptr.assign(W_NUM_SLOTS, nullptr);
   c->cap.assign(W_NUM_SLOTS, 0);
-  e = cudaMallocHost(&c->h_stats, 2 * sizeof(Stats) + 6 * sizeof(int64_t));
+  e = cudaMallocHost(&c->h_stats, 2 * sizeof(Stats) + 4 * sizeof(int64_t));
   if (e != cudaSuccess) {
     delete c;
     return XS_CUDA_ERROR;
   }
-  memset(c->h_stats, 0, 2 * sizeof(Stats) + 6 * sizeof(int64_t));
+  memset(c->h_stats, 0, 2 * sizeof(Stats) + 4 * sizeof(int64_t));
   c->h_totals = reinterpret_cast<int64_t*>(c->h_stats + 2);
-  c->h_flag = reinterpret_cast<unsigned long long*>(c->h_totals + 4);  // (8-aligned, after the 4 totals)
   *out = c;
   return XS_OK;
 }

@@ -198,8 +198,6 @@ struct xs_ctx {
   bool reuse_ops = false;  // analyze: the original's op stage builds the paths the corrected overlap reuses
   int64_t reuse_bad_n = -1;  // (n, n_pids) of the last trace whose reuse verdict failed
   int reuse_bad_pids = -1;
-  unsigned long long* h_flag = nullptr;  // page-locked: pass-1 statistics arrival (fetch_stats)
-  unsigned long long flag_seq = 0;
   int rmap_logw = 4;  // the last correction's sampled slab-index width (windows per pid, log2)
   unsigned attr_done = 0;  // kernels whose >48 KB dynamic shared memory attribute is set on this ctx's device
   int64_t syn_events = 0, syn_kernels = 0;  // sizes of the last xs_synth_plan
