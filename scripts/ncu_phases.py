@@ -14,6 +14,10 @@ lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
 rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
 h = rows[0]
+# a report holding several kernels repeats the header (and a kernel-name
+# line) before each: keep the first kernel's rows only
+cut = next((i for i, r in enumerate(rows[1:], 1) if r and (r[0] == "Address" or r[0] == "Kernel Name")), len(rows))
+rows = rows[:cut]
 ix = {n: i for i, n in enumerate(h)}
 stalls = [n for n in h if n.startswith("stall_") and "Not Issued" not in n]
 tot_s = sum(int(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in rows[1:] if len(r) == len(h))
