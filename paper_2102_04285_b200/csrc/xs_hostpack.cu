@@ -14,8 +14,17 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
+
+#include <unistd.h>
+#if defined(__x86_64__) || defined(_M_X64)
+#include <immintrin.h>
+#define XS_NT_STORES 1
+#endif
 
 #include "xstrace_b200.h"
 
@@ -34,6 +43,26 @@ inline int64_t off_of(int64_t s, int64_t base) {  // s - base with int64 wrap (n
 
 inline int index_width(int64_t hi) { return hi < (1 << 8) ? 1 : hi < (1 << 16) ? 2 : 4; }
 
+// Copy into the staging block with non-temporal stores: the block is DMA'd
+// to the device right after, and a block left dirty in the CPU caches is
+// read by the DMA at ~20 GB/s instead of the link's ~55 (every line is
+// snooped); streaming stores also skip the read-for-ownership of each line.
+// dst is 16-byte aligned at every 256-row segment (sections are 16-aligned,
+// segments start at multiples of 256 rows).
+inline void nt_copy(uint8_t* dst, const void* src_v, int64_t n) {
+  const uint8_t* src = (const uint8_t*)src_v;
+#ifdef XS_NT_STORES
+  int64_t i = 0;
+  if (((uintptr_t)dst & 15) == 0) {
+    for (; i + 16 <= n; i += 16)
+      _mm_stream_si128((__m128i*)(dst + i), _mm_loadu_si128((const __m128i*)(src + i)));
+  }
+  if (i < n) memcpy(dst + i, src + i, n - i);
+#else
+  memcpy(dst, src, n);
+#endif
+}
+
 struct Part {
   int64_t r0, r1;
   int64_t max_pid = 0, max_tid = 0, max_name = 0;
@@ -49,17 +78,76 @@ int threads_for(int64_t n, int n_threads) {
   return std::max(t, 1);
 }
 
+// A persistent worker pool: spawning ~15 threads per pass cost more than the
+// pass itself at 1M rows.  Workers are detached and park on a condition
+// variable between jobs; a forked child (no threads) starts a new pool.
+class Pool {
+ public:
+  void run(int T, const std::function<void(int)>& f) {
+    std::unique_lock<std::mutex> lk(m_);
+    if (owner_ != getpid()) {  // first use, or a fork: the threads are gone
+      owner_ = getpid();
+      nthreads_ = 0;
+      gen_ = 0;
+    }
+    while (nthreads_ < T - 1) {
+      std::thread(&Pool::worker, this, gen_).detach();
+      ++nthreads_;
+    }
+    job_ = &f;
+    ntask_ = T;
+    next_ = 1;
+    pending_ = T - 1;
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    f(0);
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void worker(unsigned long long seen) {
+    std::unique_lock<std::mutex> lk(m_);
+    const pid_t me = owner_;
+    for (;;) {
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      if (owner_ != me) return;  // (a forked child's pool: not ours)
+      seen = gen_;
+      while (next_ < ntask_) {
+        const int t = next_++;
+        const std::function<void(int)>* job = job_;
+        lk.unlock();
+        (*job)(t);
+        lk.lock();
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  unsigned long long gen_ = 0;
+  int ntask_ = 0, next_ = 0, pending_ = 0, nthreads_ = 0;
+  pid_t owner_ = 0;
+};
+
+Pool& pool() {
+  static Pool* p = new Pool();  // (never destroyed: detached workers may still park on it at exit)
+  return *p;
+}
+
 template <class F>
 void run_parts(int T, F&& f) {
   if (T == 1) {
     f(0);
     return;
   }
-  std::vector<std::thread> th;
-  th.reserve(T - 1);
-  for (int t = 1; t < T; ++t) th.emplace_back(f, t);
-  f(0);
-  for (auto& x : th) x.join();
+  static std::mutex serial;  // one pass at a time through the pool (callers may be concurrent threads)
+  std::lock_guard<std::mutex> g(serial);
+  const std::function<void(int)> fn = f;
+  pool().run(T, fn);
 }
 
 void part_range(int64_t n, int T, int t, int64_t* r0, int64_t* r1) {
@@ -196,25 +284,41 @@ extern "C" int xs_pack_fill(const xs_events_t* ev, const xs_pack_layout_t* lay, 
       const int64_t b1 = std::min(r1, b0 + kRows);
       // column by column over the 256-row block (branch-free, vectorisable);
       // the rare block with a misfit gets a row-ordered exception pass
+      // each column segment is built in a local buffer (cache-resident),
+      // then streamed into the block
+      alignas(16) uint8_t seg[kRows * 8];
+      const int64_t m = b1 - b0;
       bool bad = false;
       int64_t base = 0;
       if (s4) {
         base = s[b0];
         for (int64_t i = b0 + 1; i < b1; ++i) base = std::min(base, s[i]);
         ((int64_t*)sec[S_BASE])[b0 / kRows] = base;
-        bad |= narrow32((uint32_t*)sec[S_START], s, b0, b1, base);
+        bad |= narrow32((uint32_t*)seg - b0, s, b0, b1, base);
+        nt_copy(sec[S_START] + b0 * 4, seg, m * 4);
       } else {
-        memcpy((int64_t*)sec[S_START] + b0, s + b0, (b1 - b0) * 8);
+        nt_copy(sec[S_START] + b0 * 8, s + b0, m * 8);
       }
-      if (d4) bad |= narrow32((uint32_t*)sec[S_DUR], d, b0, b1, 0);
-      else memcpy((int64_t*)sec[S_DUR] + b0, d + b0, (b1 - b0) * 8);
-      if (c4) bad |= narrow32((uint32_t*)sec[S_CORR], c, b0, b1, 0);
-      else memcpy((int64_t*)sec[S_CORR] + b0, c + b0, (b1 - b0) * 8);
-      put_index(sec[S_PID], ev->pid, b0, b1, lay->pid_w);
-      put_index(sec[S_TID], ev->tid, b0, b1, lay->tid_w);
-      put_index(sec[S_NAME], ev->name, b0, b1, lay->name_w);
-      uint8_t* cf = sec[S_CATF];
-      for (int64_t i = b0; i < b1; ++i) cf[i] = (uint8_t)(ev->cat[i] | (ev->has_corr[i] << 7));
+      if (d4) {
+        bad |= narrow32((uint32_t*)seg - b0, d, b0, b1, 0);
+        nt_copy(sec[S_DUR] + b0 * 4, seg, m * 4);
+      } else {
+        nt_copy(sec[S_DUR] + b0 * 8, d + b0, m * 8);
+      }
+      if (c4) {
+        bad |= narrow32((uint32_t*)seg - b0, c, b0, b1, 0);
+        nt_copy(sec[S_CORR] + b0 * 4, seg, m * 4);
+      } else {
+        nt_copy(sec[S_CORR] + b0 * 8, c + b0, m * 8);
+      }
+      put_index(seg - b0 * lay->pid_w, ev->pid, b0, b1, lay->pid_w);
+      nt_copy(sec[S_PID] + b0 * lay->pid_w, seg, m * lay->pid_w);
+      put_index(seg - b0 * lay->tid_w, ev->tid, b0, b1, lay->tid_w);
+      nt_copy(sec[S_TID] + b0 * lay->tid_w, seg, m * lay->tid_w);
+      put_index(seg - b0 * lay->name_w, ev->name, b0, b1, lay->name_w);
+      nt_copy(sec[S_NAME] + b0 * lay->name_w, seg, m * lay->name_w);
+      for (int64_t i = b0; i < b1; ++i) seg[i - b0] = (uint8_t)(ev->cat[i] | (ev->has_corr[i] << 7));
+      nt_copy(sec[S_CATF] + b0, seg, m);
       if (!bad) continue;
       for (int64_t i = b0; i < b1; ++i) {  // exceptions: row order, then column 0 / 1 / 2
         if (s4 && !fits32(off_of(s[i], base))) erow[e] = i, eval[e] = s[i], ecol[e] = 0, ++e;
@@ -222,6 +326,9 @@ extern "C" int xs_pack_fill(const xs_events_t* ev, const xs_pack_layout_t* lay, 
         if (c4 && !fits32(c[i])) erow[e] = i, eval[e] = c[i], ecol[e] = 2, ++e;
       }
     }
+#ifdef XS_NT_STORES
+    _mm_sfence();  // streaming stores visible before the caller's DMA
+#endif
   });
   if (!s4) memset(sec[S_BASE], 0, 8);
   if (lay->nbytes[S_GPID]) memcpy(sec[S_GPID], ev->group_pid, lay->nbytes[S_GPID]);

@@ -626,7 +626,7 @@ int stage_ops(xs_ctx* ctx, const EventView& v, cudaStream_t s, bool build_paths)
 // later, e.g. concurrently with the correction when analyze reuses the
 // original trace's paths).
 int stage_ops_paths(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
-  const Stats& H = *ctx->h_stats;
+  const Stats& H = *ctx->h_stats;  // (the original trace's pass 1)
   OpsState& os = ctx_ops(ctx);
   const int64_t m = os.m;
   if (m == 0) {
@@ -672,7 +672,7 @@ int stage_ops_paths(xs_ctx* ctx, const EventView& v, cudaStream_t s) {
   XS_TRY(ws(ctx, W_PK_ALT, 2 * m + 2, s, &pk_alt));
   // op endpoints relabelled group -> pid (monotone, so order is kept)
   XS_LAUNCH(ctx, k_pid_keys, grid_for(2 * m), XS_BLOCK, 0, s, sk, 2 * m, v.ev.group_pid, opg_inv, tb, pk);
-  if (ctx->h_stats->multi_op_pids == 0) {
+  if (H.multi_op_pids == 0) {
     // one op tid per pid: pid order == group order
     XS_LAUNCH(ctx, k_pidpath_simple, grid_for(2 * m), XS_BLOCK, 0, s, sk, sv, 2 * m, parent, node, pidpath);
     os.pk = pk;
