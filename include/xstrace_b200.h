@@ -87,6 +87,20 @@ typedef struct {
                                /* in the order of `whole`, then api_internal[name] per name    */
   const int64_t* internal;     /* DEVICE [n_names] floor(api_internal[name])                    */
   const uint8_t* has_internal; /* DEVICE [n_names]                                              */
+  /* Window carries (a process corrected as consecutive time windows, each a
+   * pid of its own in the call: distributed.analyze_sharded).  Both NULL for
+   * the reference's whole-process semantics.
+   *   residue_in  DEVICE [n_pids * words] or NULL: the running fractional sum
+   *               (mod L, < L) of the process's amounts before this window --
+   *               quantize_amounts' `cum` (_timeline.py:61-66) does not
+   *               restart at a window;
+   *   span_end_in DEVICE [n_pids] or NULL: absolute time at which removed_ns
+   *               is clipped instead of the window's own last end (the
+   *               process's span end, correction.py:155-156; the next cut
+   *               for an inner window, which makes a slab running past the
+   *               cut visible as removed < total slab length). */
+  const uint64_t* residue_in;
+  const int64_t* span_end_in;
 } xs_profile_t;
 
 /* Sizes of the last overlap result held by the context. */

@@ -50,6 +50,7 @@ class XoProfile(C.Structure):
         ("L", C.c_int64), ("ann_start", C.c_int64), ("ann_end", C.c_int64),
         ("transition", C.c_int64), ("interception", C.c_int64),
         ("internal", C.c_void_p), ("has_internal", C.c_void_p),
+        ("residue_in", C.c_void_p), ("span_end_in", C.c_void_p),
     ]
 
 
@@ -179,12 +180,22 @@ def scale_profile(profile, names):
 HOOKS = ("annotation", "transition", "api_interception", "api_internal")
 
 
-def correct(ct, profile, queries=()):
-    """correct_trace restated; returns (start', dur', report dict, query results)."""
+def correct(ct, profile, queries=(), residue_in=None, span_end_in=None, arrays=False):
+    """correct_trace restated; returns (start', dur', report dict, query results).
+    ``residue_in`` ([n_pids] Fractions in [0, 1)) and ``span_end_in``
+    ([n_pids] ints) are the window carries of the sharded window correction
+    (None: the reference's whole-process semantics)."""
     ev, _keep = _events(ct)
     L, base, ints, has = scale_profile(profile, ct.names)
+    res = spe = None
+    if residue_in is not None:
+        res = np.array([int(r * L) for r in residue_in], np.int64)
+        assert all(int(r * L) == r * L and 0 <= r < 1 for r in residue_in)
+    if span_end_in is not None:
+        spe = np.ascontiguousarray(span_end_in, np.int64)
     prof = XoProfile(L, base[0], base[1], base[2], base[3], _ptr(ints) if ints.size else None,
-                     _ptr(has) if has.size else None)
+                     _ptr(has) if has.size else None, _ptr(res) if res is not None else None,
+                     _ptr(spe) if spe is not None else None)
     P = ct.n_pids
     removed = np.zeros(max(P, 1) * 4, np.int64)
     shortfall = np.zeros(max(P, 1) * 4, np.int64)
@@ -202,6 +213,8 @@ def correct(ct, profile, queries=()):
         raise OracleUncalibrated(int(rep.bad_event))
     if st != 0:
         raise RuntimeError(f"oracle correct failed: {st}")
+    if arrays:  # per pid index: (start', dur', removed [P, 4], shortfall [P, 4])
+        return out_s[: ct.n], out_d[: ct.n], removed[: P * 4].reshape(P, 4), shortfall[: P * 4].reshape(P, 4)
     present = np.zeros(P, bool)
     present[np.unique(ct.pid)] = True
     report = {

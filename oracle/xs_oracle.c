@@ -914,10 +914,10 @@ int xo_correct(const xo_events_t* ev, const xo_profile_t* prof, int64_t* out_sta
       if (ev->start[E[i]] < lo) lo = ev->start[E[i]];
       if (ev_end(ev, E[i]) > hi) hi = ev_end(ev, E[i]);
     }
-    int64_t span_end = hi;
+    int64_t span_end = prof->span_end_in ? prof->span_end_in[p] : hi;
     rep->original_total += hi - lo;
     /* quantize_amounts (_timeline.py:57-67) + caps (correction.py:139-153) */
-    __int128 cum = 0;
+    __int128 cum = prof->residue_in ? prof->residue_in[p] : 0; /* floor(residue / L) = 0 */
     int64_t prev = 0;
     for (int64_t q = s0; q < sp; q++) {
       const site_t* s = &sites[order[q]];

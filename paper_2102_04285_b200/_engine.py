@@ -381,7 +381,7 @@ class Engine:
         return prof, (internal, has, tab)
 
     def correct(self, dt: DeviceTrace, scaled, analyze_attribution: Optional[int] = None,
-                host_out=None, dev_out=None, async_copy: bool = False) -> CorrectRaw:
+                host_out=None, dev_out=None, async_copy: bool = False, carries=None) -> CorrectRaw:
         """xs_correct, or xs_analyze when analyze_attribution is given.  With
         ``host_out`` = (start, dur) host int64 buffers (pinned for overlap)
         the corrected columns are also copied there, overlapped with the
@@ -396,6 +396,13 @@ class Engine:
             out_d = torch.empty(n, dtype=torch.int64, device=dev)
         ev = dt.struct()
         prof, keep = self._profile(dt, scaled)
+        if carries is not None:  # window carries (xs_profile_t.residue_in / span_end_in), per pid of the call
+            residue, span_end = carries
+            t_res = torch.from_numpy(np.ascontiguousarray(residue, np.uint64).view(np.int64)).to(dev)
+            t_end = torch.from_numpy(np.ascontiguousarray(span_end, np.int64)).to(dev)
+            prof = _lib.XsProfile.from_buffer_copy(prof)
+            prof.residue_in, prof.span_end_in = t_res.data_ptr(), t_end.data_ptr()
+            keep = (keep, t_res, t_end)
         bad = C.c_int64(-1)
         if analyze_attribution is None:
             st = self.lib.xs_correct(self.ctx, C.byref(ev), C.byref(prof), out_s.data_ptr(), out_d.data_ptr(),
@@ -411,13 +418,13 @@ class Engine:
         if st == _lib.XS_UNCALIBRATED:
             raise UncalibratedEvent(int(bad.value))
         self.check(st, "xs_correct")
-        del keep
         P = dt.ct.n_pids
         removed = np.zeros(max(P, 1) * 4, np.int64)
         shortfall = np.zeros(max(P, 1) * 4, np.int64)
         info = _lib.XsCorrectInfo()
         self.check(self.lib.xs_correct_report(self.ctx, C.byref(info), removed.ctypes.data, shortfall.ctypes.data,
                                               self.stream()), "xs_correct_report")
+        del keep  # (the report read-back has synchronised the call's stream)
         return CorrectRaw(out_s[: dt.ct.n], out_d[: dt.ct.n], removed[: P * 4].reshape(P, 4),
                           shortfall[: P * 4].reshape(P, 4), int(info.original_total), int(info.corrected_total),
                           int(info.n_sites), int(info.n_slabs))

@@ -65,6 +65,7 @@ class XsProfile(C.Structure):
     _fields_ = [
         ("words", C.c_int32), ("reserved", C.c_int32), ("L", C.c_void_p), ("whole", C.c_int64 * 4),
         ("frac", C.c_void_p), ("internal", C.c_void_p), ("has_internal", C.c_void_p),
+        ("residue_in", C.c_void_p), ("span_end_in", C.c_void_p),
     ]
 
 

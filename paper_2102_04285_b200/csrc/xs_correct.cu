@@ -240,6 +240,16 @@ __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const
       SegMod<W> e;
 #pragma unroll
       for (int i = 0; i < W; i++) e.w[i] = pr.frac[(int64_t)row[j] * W + i];
+      if (hd[j] && pr.residue_in) {  // a window's segment starts from the carried residue
+        uint64_t r0[W], f0[W];
+        const int64_t pp = (int64_t)(kq >> pshift);
+#pragma unroll
+        for (int i = 0; i < W; i++) {
+          r0[i] = pr.residue_in[pp * W + i];
+          f0[i] = e.w[i];
+        }
+        op.add_mod(r0, f0, e.w);
+      }
       e.head = hd[j];
       e.pad = 0;
       agg = op(agg, e);
@@ -254,7 +264,7 @@ __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const
 #pragma unroll
     for (int i = 0; i < W; i++) {
       f[i] = pr.frac[(int64_t)row[j] * W + i];
-      if (hd[j]) run.w[i] = 0;
+      if (hd[j]) run.w[i] = pr.residue_in ? pr.residue_in[(int64_t)(k1[q] >> pshift) * W + i] : 0;
     }
     op.add_mod(run.w, f, after);
     const int64_t whole = row[j] < 4 ? pr.whole[row[j]] : pr.internal[row[j] - 4];
@@ -368,7 +378,8 @@ constexpr int R_ITEMS = XS_R_ITEMS;
 #endif
 __global__ void __launch_bounds__(XS_BLOCK, XS_REMOVAL_MINB) k_removal(const uint64_t* k1, const uint32_t* slot, const int64_t* d_ns, int tb,
                                                       const int64_t* lenslot,
-                                                      const int64_t* lo, const int64_t* hi, int64_t* removed,
+                                                      const int64_t* lo, const int64_t* hi,
+                                                      const int64_t* span_end_in, int64_t* removed,
                                                       Slab* slabs,
                                                       int* pid_slabs, int64_t* ptotal, TileDesc<RM>* desc,
                                                       int* flags, int* tile_ctr) {
@@ -425,7 +436,7 @@ __global__ void __launch_bounds__(XS_BLOCK, XS_REMOVAL_MINB) k_removal(const uin
       acc[0] = acc[1] = acc[2] = acc[3] = 0;
       nsl = tot = 0;
     }
-    const int64_t span_end = hi[p] - lo[p];
+    const int64_t span_end = (span_end_in ? span_end_in[p] : hi[p]) - lo[p];
     const int64_t mb = b < span_end ? b : span_end;
     const int64_t ma = a < span_end ? a : span_end;
     acc[hook_of(sub[j])] += mb - ma;
@@ -765,7 +776,7 @@ int stage_correct(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, int
       XS_TRY(ws(ctx, W_RSCAN_FLAGS, tiles + 1, s, &flags));
       XS_TRY(ws(ctx, W_TILE_CTR, 4, s, &tctr));
       XS_TRY(fill_many(ctx, s, {{flags, (unsigned long long)(tiles + 1) * sizeof(int), 0}, {tctr, sizeof(int), 0}}));
-      XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, lenslot, lo, hi, removed,
+      XS_LAUNCH(ctx, k_removal, (int)tiles, XS_BLOCK, 0, s, k1, sl, d_ns, tb, lenslot, lo, hi, prof->span_end_in, removed,
                 slabs, pid_slabs, ptotal, desc, flags, tctr);
     }
   }

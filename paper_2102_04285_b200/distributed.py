@@ -414,11 +414,15 @@ def merge_reports(local_rep, device):
     return rep
 
 
-def analyze_sharded(ct: ColumnarTrace, profile, attribution=None, device=None, gather_columns: bool = False):
+def analyze_sharded(ct: ColumnarTrace, profile, attribution=None, device=None, gather_columns: bool = False,
+                    split: int = 2, runner=None):
     """``xstrace analyze --profile`` over ``world`` ranks, one GPU each:
     correct_trace then compute_overlap of the corrected trace, sharded by
-    whole processes (LPT on event counts; per-pid independence,
-    correction.py:132-157, overlap.py:126).  Every rank returns the merged
+    processes (LPT on event counts; per-pid independence,
+    correction.py:132-157, overlap.py:126); with ``split`` > 0 a process
+    holding more than n / (world * split) events is corrected as time
+    windows spread over ranks, with the window carries (see
+    _analyze_windows).  Every rank returns the merged
     CorrectionReport and Breakdown (bit-exact: integer sums).  The corrected
     columns come back as this rank's rows (``rows``, ``start``, ``dur``) or,
     with ``gather_columns``, as the whole trace's columns on every rank.
@@ -438,6 +442,13 @@ def analyze_sharded(ct: ColumnarTrace, profile, attribution=None, device=None, g
     eng = _engine.get(torch.cuda.current_device())
     dev = device or torch.device("cuda", eng.device)
     attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
+    if split > 0:
+        out = _analyze_windows(ct, profile, attr, dev, world, rank, split, runner or DeviceWindowRunner(eng))
+        if out is not None:
+            rows, start, dur, rep, bd = out
+            if gather_columns:
+                return _gather_columns(ct, rows, start, dur, dev, world) + (rep, bd)
+            return rows, start, dur, rep, bd
     shards = shard_pids(ct, world)
     keep = np.isin(ct.pid, np.asarray(shards[rank], np.int32))
     rows = np.nonzero(keep)[0]
@@ -453,7 +464,7 @@ def analyze_sharded(ct: ColumnarTrace, profile, attribution=None, device=None, g
             bad_invalid = 1
         except UncalibratedHookError:  # (_run maps the event; recover its row here)
             raw_c = None
-            bad_row = _first_uncalibrated_row(local, profile, rows)
+            bad_row = _first_uncalibrated_row(local, profile, lrows)
     if world > 1:
         flags = torch.tensor([bad_invalid, -bad_row], dtype=torch.int64, device=dev)
         dist.all_reduce(flags, op=dist.ReduceOp.MAX)
@@ -468,18 +479,25 @@ def analyze_sharded(ct: ColumnarTrace, profile, attribution=None, device=None, g
     rep = merge_reports(_report(local, raw_c), dev)
     bd = merge_breakdown_raw(local, raw_o, dev)
     if gather_columns:
-        full_s = np.zeros(ct.n, np.int64)
-        full_d = np.zeros(ct.n, np.int64)
-        if world > 1:
-            gr, gs, gd = (_gather_var(torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(dev), dev, world)
-                          for a in (rows, start, dur))
-            rows_all, s_all, d_all = gr.cpu().numpy(), gs.cpu().numpy(), gd.cpu().numpy()
-        else:
-            rows_all, s_all, d_all = rows, start, dur
-        full_s[rows_all] = s_all
-        full_d[rows_all] = d_all
-        return np.arange(ct.n), full_s, full_d, rep, bd
+        return _gather_columns(ct, rows, start, dur, dev, world) + (rep, bd)
     return rows, start, dur, rep, bd
+
+
+def _gather_columns(ct: ColumnarTrace, rows, start, dur, dev, world: int) -> tuple:
+    """Every rank's corrected rows -> the whole trace's columns on every rank."""
+    import torch
+
+    full_s = np.zeros(ct.n, np.int64)
+    full_d = np.zeros(ct.n, np.int64)
+    if world > 1:
+        gr, gs, gd = (_gather_var(torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(dev), dev, world)
+                      for a in (rows, start, dur))
+        rows_all, s_all, d_all = gr.cpu().numpy(), gs.cpu().numpy(), gd.cpu().numpy()
+    else:
+        rows_all, s_all, d_all = rows, start, dur
+    full_s[rows_all] = s_all
+    full_d[rows_all] = d_all
+    return np.arange(ct.n), full_s, full_d
 
 
 def _first_uncalibrated_row(local: ColumnarTrace, profile, rows) -> int:
@@ -488,3 +506,457 @@ def _first_uncalibrated_row(local: ColumnarTrace, profile, rows) -> int:
     bad_names = np.array([nm not in have for nm in local.names], bool)
     sel = np.nonzero((local.cat == 4) & bad_names[local.name])[0] if len(local.names) else np.zeros(0, np.int64)
     return int(rows[sel[0]]) if sel.size else np.iinfo(np.int64).max
+
+
+# ---------------------------------------------------------------------------
+# Window-split correction of giant pids (SURVEY.md 8e: correction carries)
+#
+# correct_trace walks each pid's sites in order with two running states
+# (correction.py:132-157): quantize_amounts' rational sum `cum`
+# (_timeline.py:57-67) and the RemovalMap's slab chain end E
+# (_timeline.py:90-117).  A giant pid is cut at instants c that no event of
+# the pid reaches across (every event starting before c ends before c) and
+# that no launcher -> GPU kernel correlation pair straddles.  Then, per window:
+#   * sites, owners' budgets, transition maximality / coverage and operation
+#     nesting are window-local (no event crosses a cut; the strict end < c
+#     keeps every earlier window's site before every later one in
+#     Site.order_key);
+#   * `cum` enters as a carry: the fractional part of the amounts of all
+#     earlier windows (their site counts per amount row; one all-gather),
+#     passed to the device as xs_profile_t.residue_in;
+#   * if no slab of an earlier window runs past the cut (E <= c), the
+#     window's slabs are its local ones and the global map is the local map
+#     minus P_in, the total slab length before the window (a second tiny
+#     all-gather); the device clips removed_ns at the next cut
+#     (xs_profile_t.span_end_in), so removed == total slab length proves it;
+#   * the corrected window trace is overlapped on its own: exact when no
+#     corrected event crosses the mapped cut (GPU events keep their duration
+#     while CPU time shrinks: checked as the corrected window end <= the
+#     locally mapped cut).
+# Any failed check (rare: removable time larger than the idle gap at a cut)
+# re-runs the analysis with whole-pid shards -- exact either way.
+# ---------------------------------------------------------------------------
+
+
+def correction_cut_gaps(ct: ColumnarTrace, p: int, gpu_free: bool = False) -> np.ndarray:
+    """[k, 2] closed intervals of valid window cuts for pid index p: instants
+    c that no OPERATION reaches (start < c <= end: its ANN_END site must
+    order before the next window's sites at c), no BACKEND / SIMULATOR /
+    ACCEL_API event strictly straddles (start < c < end), and no correlated
+    launcher / GPU pair sits across.  HIGH_LEVEL events may straddle: they
+    own no site and are only the outer side of the wrapper transitions, so
+    they are clipped into every window they cover.  GPU events may straddle
+    too: the correction only shifts them by their start (_timeline.py:
+    120-132); their parts past a window's mapped cut join the next windows'
+    overlap passes as clipped pieces -- except with ``gpu_free`` (CORRELATION
+    attribution: a clipped kernel piece would lose its launcher's path), where
+    GPU events may not straddle either."""
+    sel = np.nonzero(ct.pid == p)[0]
+    s = ct.start[sel]
+    e = s + ct.dur[sel]
+    cat = ct.cat[sel]
+    op = cat == 0
+    mid = (cat >= 2) & (cat <= (5 if gpu_free else 4))
+    lo_r = [s[op] + 1, s[mid] + 1]
+    hi_r = [e[op], e[mid] - 1]
+    api = sel[(cat == 4) & (ct.has_corr[sel] == 1)]
+    gpu = sel[(cat == 5) & (ct.has_corr[sel] == 1)]
+    if api.size and gpu.size:
+        ac, ast = ct.corr[api], ct.start[api]
+        o = np.lexsort((ast, ac))
+        ac, ast = ac[o], ast[o]
+        first = np.r_[True, ac[1:] != ac[:-1]]
+        ids, lstart = ac[first], ast[first]
+        gc, gs = ct.corr[gpu], ct.start[gpu]
+        k = np.minimum(np.searchsorted(ids, gc), ids.size - 1)
+        ok = ids[k] == gc
+        lo_r.append(np.minimum(lstart[k], gs)[ok] + 1)
+        hi_r.append(np.maximum(lstart[k], gs)[ok])
+    lo_a, hi_a = np.concatenate(lo_r), np.concatenate(hi_r)
+    m = hi_a >= lo_a
+    lo_a, hi_a = lo_a[m], hi_a[m]
+    big = np.iinfo(np.int64).max
+    if lo_a.size == 0:
+        return np.array([[-big, big]], np.int64)
+    o = np.argsort(lo_a, kind="stable")
+    lo_a, hi_a = lo_a[o], hi_a[o]
+    run = np.maximum.accumulate(hi_a)
+    gap_after = np.nonzero(run[:-1] + 1 < lo_a[1:])[0]  # [run + 1, next lo - 1] is free
+    glo = np.concatenate([[-big], run[gap_after] + 1, [run[-1] + 1]])
+    ghi = np.concatenate([[lo_a[0] - 1], lo_a[gap_after + 1] - 1, [big]])
+    return np.stack([glo, ghi], axis=1)
+
+
+def correction_window_cuts(ct: ColumnarTrace, p: int, parts: int, gpu_free: bool = False) -> list:
+    """Up to parts-1 cuts for pid index p near its event-count quantiles.
+    A cut is the last valid instant of its gap (the next blocking event's
+    start), leaving the whole idle room before it to the slabs of the
+    window's last sites (the window check needs E <= c)."""
+    if parts <= 1:
+        return []
+    starts = np.sort(ct.start[ct.pid == p])
+    if starts.size == 0:
+        return []
+    gaps = correction_cut_gaps(ct, p, gpu_free)
+    his = gaps[:, 1]
+    his = his[(his > starts[0]) & (his <= starts[-1])]
+    cuts = []
+    for j in range(1, parts):
+        if his.size == 0:
+            break
+        q = int(starts[min(starts.size - 1, j * starts.size // parts)])
+        k = int(np.searchsorted(his, q))
+        cand = [int(his[x]) for x in (k - 1, k) if 0 <= x < his.size]
+        best = min(cand, key=lambda c: (abs(c - q), c))
+        if not cuts or best > cuts[-1]:
+            cuts.append(best)
+    return cuts
+
+
+def plan_correction_shards(ct: ColumnarTrace, world: int, split: int = 2, gpu_free: bool = False) -> list:
+    """Per rank, shards (pid index, lo, hi): whole pids (None, None) or the
+    correction windows [lo, hi) of giant pids; LPT-packed by event count."""
+    counts = np.bincount(ct.pid, minlength=ct.n_pids) if ct.n else np.zeros(ct.n_pids, np.int64)
+    target = max(1, -(-ct.n // max(1, world * split)))
+    items = []
+    for p in range(ct.n_pids):
+        c = int(counts[p])
+        if c == 0:
+            continue
+        parts = min(world * split, -(-c // target)) if split > 0 else 1
+        cuts = correction_window_cuts(ct, p, parts, gpu_free) if parts > 1 else []
+        if not cuts:
+            items.append((c, p, None, None))
+            continue
+        st = np.sort(ct.start[ct.pid == p])
+        bounds = [None] + cuts + [None]
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            i0 = 0 if a is None else int(np.searchsorted(st, a, side="left"))
+            i1 = st.size if b is None else int(np.searchsorted(st, b, side="left"))
+            items.append((i1 - i0, p, a, b))
+    loads = [0] * world
+    out: list = [[] for _ in range(world)]
+    for c, p, a, b in sorted(items, key=lambda x: (-x[0], x[1], -(2**63) if x[2] is None else x[2])):
+        r = min(range(world), key=lambda k: (loads[k], k))
+        out[r].append((p, a, b))
+        loads[r] += c
+    return out
+
+
+def piece_trace(ct: ColumnarTrace, shards: list) -> tuple:
+    """One device pid per shard (a whole pid, or one window [a, b) of a giant
+    pid): (local trace, global row per local row, head, tail, pieces).  A
+    window holds the pid's events starting in [a, b) plus the HIGH_LEVEL
+    events reaching into it from earlier windows, each HIGH_LEVEL event
+    clipped to [a, b); ``head`` marks the piece holding an event's start,
+    ``tail`` the piece holding its end.  Rows keep trace order; each piece has
+    its own (pid, tid) groups, so the correction's per-pid scans restart
+    (with the carries) at every window."""
+    neg = -(2**63)
+    big = np.iinfo(np.int64).max
+    pieces = sorted(shards, key=lambda s: (s[0], neg if s[1] is None else s[1]))
+    order = np.argsort(ct.pid, kind="stable")
+    bounds = np.searchsorted(ct.pid[order], np.arange(ct.n_pids + 1, dtype=np.int32))
+    row_l, piece_l, s_l, e_l, head_l, tail_l = [], [], [], [], [], []
+    for k, (p, a, b) in enumerate(pieces):
+        r = order[bounds[p]:bounds[p + 1]]
+        lo = neg if a is None else a
+        hi = big if b is None else b
+        st = ct.start[r]
+        en = st + ct.dur[r]
+        hl = ct.cat[r] == 1
+        own = (st >= lo) & (st < hi)
+        ghost = hl & (st < lo) & (en > lo)
+        keep = own | ghost
+        r, st, en, hl, own = r[keep], st[keep], en[keep], hl[keep], own[keep]
+        clip_e = hl & (en > hi)
+        row_l.append(r)
+        piece_l.append(np.full(r.shape[0], k, np.int32))
+        s_l.append(np.where(own, st, lo))
+        e_l.append(np.where(clip_e, hi, en))
+        head_l.append(own)
+        tail_l.append(~clip_e)
+    cat_ = lambda xs, dt: np.concatenate(xs) if xs else np.zeros(0, dt)
+    rows, piece = cat_(row_l, np.int64), cat_(piece_l, np.int32)
+    st, en = cat_(s_l, np.int64), cat_(e_l, np.int64)
+    head, tail = cat_(head_l, bool), cat_(tail_l, bool)
+    o = np.lexsort((piece, rows))  # trace order (a clipped row's pieces by window)
+    rows, piece, st, en, head, tail = rows[o], piece[o], st[o], en[o], head[o], tail[o]
+    G = max(ct.n_groups, 1)
+    key = piece.astype(np.int64) * G + ct.tid[rows]
+    ukey, new_tid = np.unique(key, return_inverse=True)
+    pidx = np.array([p for p, _, _ in pieces], np.int64)
+    local = ColumnarTrace(ct.clock_domain, st, en - st, piece, new_tid.astype(np.int32),
+                          ct.cat[rows], ct.name[rows], ct.corr[rows], ct.has_corr[rows], ct.pids[pidx],
+                          (ukey // G).astype(np.int32), ct.group_tid[ukey % G], ct.names, (),
+                          ct.pid_has_meta[pidx] if ct.pid_has_meta is not None else None)
+    return local, rows, head, tail, pieces
+
+
+def _amount_sums(local: ColumnarTrace, profile, n_trans: np.ndarray):
+    """Exact sum of the requested amounts of each piece's sites
+    (collect_sites, correction.py:79-112)."""
+    from fractions import Fraction
+
+    P = local.n_pids
+    ann = Fraction(profile.annotation_ns)
+    ic = Fraction(profile.api_interception_ns)
+    tr = Fraction(profile.transition_ns)
+    n_op = np.bincount(local.pid[local.cat == 0], minlength=P)
+    api = local.cat == 4
+    n_api = np.bincount(local.pid[api], minlength=P)
+    out = [ann * int(n_op[k]) + ic * int(n_api[k]) + tr * int(n_trans[k]) for k in range(P)]
+    if api.any():
+        nm = local.name[api].astype(np.int64)
+        pk = local.pid[api].astype(np.int64)
+        key, cnt = np.unique(pk * max(len(local.names), 1) + nm, return_counts=True)
+        table = profile.api_internal_ns
+        for kk, c in zip(key.tolist(), cnt.tolist()):
+            k, n = divmod(kk, max(len(local.names), 1))
+            v = table.get(local.names[n])
+            if v is not None:
+                out[k] += Fraction(v) * c
+    return out
+
+
+def _gather_objects(obj, world):
+    import torch.distributed as dist
+
+    if world == 1:
+        return [obj]
+    parts = [None] * world
+    dist.all_gather_object(parts, obj)
+    return parts
+
+
+class DeviceWindowRunner:
+    """The device side of the window analysis (tests substitute the C
+    oracle): the wrapper transitions, one xs_correct call over this rank's
+    pieces with the carries, one xs_overlap call over the corrected pieces."""
+
+    def __init__(self, eng):
+        self.eng = eng
+        self.dt = None
+
+    def _dt(self, local):
+        from . import _engine
+
+        if self.dt is None or self.dt.ct is not local:
+            self.dt = _engine.DeviceTrace(local, self.eng.device)
+        return self.dt
+
+    def transition_rows(self, local: ColumnarTrace) -> np.ndarray:
+        _, ev = self.eng.transition_sites(self._dt(local), 0x3)  # WRAPPER_PAIRS (overlap.py:200-203)
+        return np.asarray(ev, np.int64)
+
+    def correct(self, local: ColumnarTrace, profile, r_in: list, span_end: np.ndarray):
+        """-> (start, dur, removed [P, 4], shortfall [P, 4])."""
+        scaled = profile.scaled(local.names)
+        residue = np.zeros(max(local.n_pids, 1) * scaled.words, np.uint64)
+        for k, r in enumerate(r_in):
+            v = r * scaled.L
+            assert v.denominator == 1 and 0 <= v < scaled.L
+            residue[k * scaled.words:(k + 1) * scaled.words] = scaled.words_of(int(v))
+        raw = self.eng.correct(self._dt(local), scaled, None, carries=(residue, span_end))
+        return raw.start.cpu().numpy(), raw.dur.cpu().numpy(), raw.removed, raw.shortfall
+
+    def overlap(self, trace: ColumnarTrace, attr: int):
+        from . import _engine
+
+        return self.eng.overlap(_engine.DeviceTrace(trace, self.eng.device), attr)
+
+
+def _analyze_windows(ct: ColumnarTrace, profile, attr: int, dev, world: int, rank: int, split: int, runner):
+    """analyze_sharded with giant pids corrected as windows (see above).
+    Returns (rows, start, dur, report, Breakdown), or None when nothing was
+    split or a window check failed on some rank (the caller then shards whole
+    pids).  Raises like the reference on invalid / uncalibrated traces."""
+    import math
+    from fractions import Fraction
+
+    import torch
+
+    from . import _engine, _lib
+    from ._split import pid_spans_host
+    from .calibration import HOOK_KINDS
+    from .correction import CorrectionReport, UncalibratedHookError
+    from .model import InvalidTraceError, format_violations, meta_violations
+
+    plan = plan_correction_shards(ct, world, split, gpu_free=attr == 1)
+    if not any(a is not None or b is not None for sh in plan for _, a, b in sh):
+        return None
+    local, lrows, head, tail, pieces = piece_trace(ct, plan[rank])
+    rows = lrows[head]
+    P = local.n_pids
+    neg, big = -(2**63), np.iinfo(np.int64).max
+    win = [k for k, (_, a, b) in enumerate(pieces) if a is not None or b is not None]
+    bad_invalid = 1 if meta_violations(ct.processes) else 0
+    bad_row = big
+    # phase A: each window's exact amount sum (its wrapper transitions
+    # counted on the device); only the fractional parts travel
+    n_trans = np.zeros(max(P, 1), np.int64)
+    if win and not bad_invalid:
+        try:
+            n_trans = np.bincount(local.pid[runner.transition_rows(local)], minlength=max(P, 1))
+        except _engine.XsError as exc:
+            if exc.status != _lib.XS_INVALID_TRACE:
+                raise
+            bad_invalid = 1
+    sums = _amount_sums(local, profile, n_trans)
+    mine = [(pieces[k][0], neg if pieces[k][1] is None else pieces[k][1], sums[k] - math.floor(sums[k]))
+            for k in win]
+    fr = {}
+    for part in _gather_objects(mine, world):
+        for p, a, f in part:
+            fr.setdefault(p, []).append((a, f))
+    r_in = [Fraction(0)] * P
+    for k in win:
+        p, a, _ = pieces[k]
+        a0 = neg if a is None else a
+        r = sum((f for aa, f in fr[p] if aa < a0), Fraction(0))
+        r_in[k] = r - math.floor(r)
+    span_end = np.zeros(max(P, 1), np.int64)
+    if local.n:
+        span_end[:] = np.iinfo(np.int64).min
+        np.maximum.at(span_end, local.pid, local.start + local.dur)
+    for k in win:
+        if pieces[k][2] is not None:
+            span_end[k] = pieces[k][2]  # inner window: clip at the next cut
+    res = None
+    if not bad_invalid and P:
+        try:
+            res = runner.correct(local, profile, r_in, span_end)
+        except _engine.UncalibratedEvent:
+            bad_row = _first_uncalibrated_row(local, profile, lrows)
+        except _engine.XsError as exc:
+            if exc.status != _lib.XS_INVALID_TRACE:
+                raise
+            bad_invalid = 1
+    if world > 1:
+        import torch.distributed as dist
+
+        flags = torch.tensor([bad_invalid, -bad_row], dtype=torch.int64, device=dev)
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX)
+        bad_invalid, bad_row = int(flags[0].item()), -int(flags[1].item())
+    if bad_invalid:
+        raise InvalidTraceError(format_violations(ct.to_trace()))
+    if bad_row != big:
+        name = ct.names[int(ct.name[bad_row])]
+        raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile")
+    if res is not None:
+        start, dur, removed, shortfall = res
+        start = np.array(start, np.int64, copy=True)
+        dur = np.asarray(dur, np.int64)
+    else:
+        start = dur = np.zeros(0, np.int64)
+        removed = shortfall = np.zeros((0, 4), np.int64)
+    # phase B: total slab length per window -> P_in; no slab may run past a cut
+    summ = []
+    for k in win:
+        p, a, b = pieces[k]
+        T = math.floor(r_in[k] + sums[k]) - int(shortfall[k].sum())
+        ok = b is None or int(removed[k].sum()) == T  # (E <= c: removed is clipped at the cut)
+        summ.append((p, neg if a is None else a, T, ok))
+    allw = [x for part in _gather_objects(summ, world) for x in part]
+    if not all(ok for *_, ok in allw):
+        return None
+    # shift each window by P_in; the mapped cuts [cut_lo, cut_hi) of each piece
+    cut_lo = np.full(max(P, 1), neg, np.int64)
+    cut_hi = np.full(max(P, 1), big, np.int64)
+    for k in win:
+        p, a, b = pieces[k]
+        a0 = neg if a is None else a
+        p_in = sum(T for pp, aa, T, _ in allw if pp == p and aa < a0)
+        T_k = next(T for pp, aa, T, _ in allw if pp == p and aa == a0)
+        if p_in:
+            start[local.pid == k] -= p_in  # every event shifts: GPU events keep dur (_timeline.py:120-132)
+        if a is not None:
+            cut_lo[k] = a - p_in
+        if b is not None:
+            cut_hi[k] = b - p_in - T_k
+    end = start + dur
+    # GPU events running past their window's mapped cut: clipped pieces for the
+    # later windows' overlap passes (INSTANT reads no GPU correlation beyond
+    # the dangling rule, which the unclipped originals keep)
+    lp = local.pid[: start.shape[0]]
+    over = np.nonzero(end > cut_hi[lp])[0] if start.size else np.zeros(0, np.int64)
+    strad = [(int(pieces[lp[i]][0]), int(start[i]), int(end[i]), int(local.group_tid[local.tid[i]]),
+              int(local.cat[i]), int(local.name[i]), int(local.has_corr[i])) for i in over.tolist()]
+    strad = [x for part in _gather_objects(strad, world) for x in part]
+    if attr == 1 and any(x[6] for x in strad):
+        return None  # a correlated kernel's clipped part would lose its launcher's path
+    o_e = end.copy()
+    clip = (local.cat[: start.size] != 0) & (o_e > cut_hi[lp])
+    o_e[clip] = cut_hi[lp][clip]
+    g_rows = []
+    for k in win:
+        p = pieces[k][0]
+        for pp, s0, e0, tv, c, nm, _ in strad:
+            if pp == p and s0 < cut_lo[k] < e0:
+                g_rows.append((k, int(cut_lo[k]), min(e0, int(cut_hi[k])), tv, c, nm))
+    otrace = _overlap_trace(local, start, o_e, g_rows) if P else local
+    raw_o = runner.overlap(otrace, attr) if P else _empty_raw()
+    bd = merge_breakdown_raw(otrace, raw_o, dev)
+    # a clipped HIGH_LEVEL event: start from its first piece, end from its last
+    cont = [(int(r), int(x)) for r, x in zip(lrows[tail & ~head].tolist(), end[tail & ~head].tolist())]
+    ends = dict(x for part in _gather_objects(cont, world) for x in part)
+    out_end = end[head].copy()
+    for i in np.nonzero(~tail[head])[0].tolist():
+        out_end[i] = ends[int(rows[i])]
+    out_start = start[head]
+    start, dur = out_start, out_end - out_start
+    # report: per-pid sums over windows and ranks; totals from the spans
+    acc = {}
+    for k in (np.nonzero(local.present_pid_mask())[0].tolist() if P else []):
+        pv = int(local.pids[k])
+        r0, s0 = acc.get(pv, (np.zeros(4, np.int64), np.zeros(4, np.int64)))
+        acc[pv] = (r0 + removed[k], s0 + shortfall[k])
+    merged = {}
+    for part in _gather_objects({p: (r.tolist(), s.tolist()) for p, (r, s) in acc.items()}, world):
+        for p, (r, s) in part.items():
+            r0, s0 = merged.get(p, ([0] * 4, [0] * 4))
+            merged[p] = ([x + y for x, y in zip(r0, r)], [x + y for x, y in zip(s0, s)])
+    rep = CorrectionReport()
+    for p in sorted(merged):
+        rep.removed_ns[p] = dict(zip(HOOK_KINDS, merged[p][0]))
+        rep.shortfall_ns[p] = dict(zip(HOOK_KINDS, merged[p][1]))
+    lo, hi = pid_spans_host(ct)
+    has = ct.present_pid_mask()
+    rep.original_total_ns = int(sum(int(hi[p]) - int(lo[p]) for p in range(ct.n_pids) if has[p]))
+    rep.corrected_total_ns = int(sum(b - a for a, b in bd.spans.values()))
+    return rows, start, dur, rep, bd
+
+
+def _overlap_trace(local: ColumnarTrace, o_s, o_e, g_rows: list) -> ColumnarTrace:
+    """The corrected pieces (resources clipped at their mapped cut) plus the
+    clipped GPU pieces from earlier windows, placed after the rows of the
+    piece they join."""
+    n = local.n
+    if not g_rows:
+        return ColumnarTrace(local.clock_domain, o_s, o_e - o_s, local.pid, local.tid, local.cat, local.name,
+                             local.corr, local.has_corr, local.pids, local.group_pid, local.group_tid,
+                             local.names, (), local.pid_has_meta)
+    g = np.array(g_rows, np.int64)
+    piece = np.concatenate([local.pid.astype(np.int64), g[:, 0]])
+    tidv = np.concatenate([local.group_tid[local.tid].astype(np.int64), g[:, 3]])
+    ukey, new_tid = np.unique(np.stack([piece, tidv], axis=1), axis=0, return_inverse=True)
+    new_tid = new_tid.reshape(-1)
+    s = np.concatenate([o_s, g[:, 1]])
+    e = np.concatenate([o_e, g[:, 2]])
+    cat = np.concatenate([local.cat, g[:, 4].astype(np.uint8)])
+    name = np.concatenate([local.name, g[:, 5].astype(np.int32)])
+    corr = np.concatenate([local.corr, np.zeros(len(g_rows), np.int64)])
+    hc = np.concatenate([local.has_corr, np.zeros(len(g_rows), np.uint8)])
+    order = np.lexsort((np.r_[np.arange(n), np.full(len(g_rows), n)], piece))
+    return ColumnarTrace(local.clock_domain, s[order], (e - s)[order], piece[order].astype(np.int32),
+                         new_tid[order].astype(np.int32), cat[order], name[order], corr[order], hc[order],
+                         local.pids, ukey[:, 0].astype(np.int32), ukey[:, 1], local.names, (),
+                         local.pid_has_meta)
+
+
+def _empty_raw():
+    from ._engine import OverlapRaw
+
+    z32, z64 = np.zeros(0, np.int32), np.zeros(0, np.int64)
+    return OverlapRaw(z32, z32, z32, z64, np.array([-1], np.int32), np.array([-1], np.int32), z64, z64, z64,
+                      np.zeros(0, np.uint8))
