@@ -46,7 +46,7 @@ def test_analyze_sharded_split_public(kind, attr):
     correlated kernel crossing a mapped cut) equals the whole-trace oracle."""
     ct = _trace(kind)
     profile = _profiles()["ladder"]
-    out = analyze_sharded(ct, profile, attribution=attr, split=8)
+    out = analyze_sharded(ct, profile, attribution=("instant", "correlation")[attr], split=8)
     _check(ct, out, _whole(ct, profile, attr))
 
 
