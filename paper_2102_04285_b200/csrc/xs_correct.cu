@@ -193,6 +193,38 @@ struct SegModOp {
   }
 };
 
+// A thread's ITEMS consecutive site keys and slots (ITEMS % 4 == 0, base a
+// multiple of ITEMS): 16-byte loads when the run is whole, scalar at the tail.
+// `prev` is the key before the run (head detection without re-reading k1).
+template <int ITEMS>
+__device__ __forceinline__ void load_site_run(const uint64_t* k1, const uint32_t* slot, int64_t base, int64_t ns,
+                                              uint64_t (&kv)[ITEMS], uint32_t (&sv)[ITEMS], uint64_t& prev) {
+  static_assert(ITEMS % 4 == 0, "vector site loads need ITEMS % 4 == 0");
+  prev = base > 0 && base < ns ? k1[base - 1] : 0;  // (no read past the live keys)
+  if (base + ITEMS <= ns) {
+#pragma unroll
+    for (int j = 0; j < ITEMS; j += 2) {
+      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(k1 + base + j);
+      kv[j] = x.x;
+      kv[j + 1] = x.y;
+    }
+#pragma unroll
+    for (int j = 0; j < ITEMS; j += 4) {
+      const uint4 x = *reinterpret_cast<const uint4*>(slot + base + j);
+      sv[j] = x.x;
+      sv[j + 1] = x.y;
+      sv[j + 2] = x.z;
+      sv[j + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < ITEMS; j++) {
+      kv[j] = base + j < ns ? k1[base + j] : 0;
+      sv[j] = base + j < ns ? slot[base + j] : 0;
+    }
+  }
+}
+
 // site subkind -> row of the profile's whole / frac tables (API_INTERNAL:
 // 4 + the event's name)
 
@@ -225,6 +257,9 @@ __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const
   id.pad = 0;
   SegMod<W> agg = id;
   const int pshift = tb + 3;
+  uint64_t kv[Q_ITEMS], prevk;
+  uint32_t sv[Q_ITEMS];
+  load_site_run<Q_ITEMS>(k1, slot, base, ns, kv, sv, prevk);
 #pragma unroll
   for (int j = 0; j < Q_ITEMS; j++) {
     const int64_t q = base + j;
@@ -233,10 +268,11 @@ __global__ void __launch_bounds__(XS_BLOCK) k_quantize(const uint64_t* k1, const
     if (q < ns) {
       // the subkind is the key's low 3 bits: only API_INTERNAL sites gather
       // their event (for the API name); the rest are profile constants
-      const uint64_t kq = k1[q];
+      const uint64_t kq = kv[j];
       const int sub = (int)(kq & 7u);
-      row[j] = sub == API_INTERNAL ? site_row[slot[q]] : amount_row(sub, 0);
-      hd[j] = q == 0 || (k1[q - 1] >> pshift) != (kq >> pshift);
+      row[j] = sub == API_INTERNAL ? site_row[sv[j]] : amount_row(sub, 0);
+      hd[j] = q == 0 || (prevk >> pshift) != (kq >> pshift);
+      prevk = kq;
       SegMod<W> e;
 #pragma unroll
       for (int i = 0; i < W; i++) e.w[i] = pr.frac[(int64_t)row[j] * W + i];
@@ -393,17 +429,20 @@ __global__ void __launch_bounds__(XS_BLOCK, XS_REMOVAL_MINB) k_removal(const uin
   int hd[R_ITEMS], sub[R_ITEMS], pp[R_ITEMS];
   RMOp op;
   RM agg{0, kNegInf, 0, 0, 0};
+  uint64_t kv[R_ITEMS], prevk;
+  uint32_t sv[R_ITEMS];
+  load_site_run<R_ITEMS>(k1, slot, base, ns, kv, sv, prevk);
 #pragma unroll
   for (int j = 0; j < R_ITEMS; j++) {
     int64_t q = base + j;
     if (q < ns) {
-      uint64_t kk = k1[q];
-      uint32_t sl = slot[q];
+      const uint64_t kk = kv[j];
       anc[j] = (int64_t)((kk >> 3) & tmask);
       pp[j] = (int)(kk >> pshift);
       sub[j] = (int)(kk & 7u);  // (the key's subkind bits; no gather)
-      len[j] = lenslot[sl];
-      hd[j] = q == 0 || (k1[q - 1] >> pshift) != (kk >> pshift);
+      len[j] = lenslot[sv[j]];
+      hd[j] = q == 0 || (prevk >> pshift) != (kk >> pshift);
+      prevk = kk;
       RM e{len[j] > 0 ? len[j] : 0, anc[j] + len[j], len[j] > 0 ? 1 : 0, hd[j], 0};
       agg = op(agg, e);
     }
