@@ -213,8 +213,9 @@ def correct(ct, profile, queries=(), residue_in=None, span_end_in=None, arrays=F
         raise OracleUncalibrated(int(rep.bad_event))
     if st != 0:
         raise RuntimeError(f"oracle correct failed: {st}")
-    if arrays:  # per pid index: (start', dur', removed [P, 4], shortfall [P, 4])
-        return out_s[: ct.n], out_d[: ct.n], removed[: P * 4].reshape(P, 4), shortfall[: P * 4].reshape(P, 4)
+    if arrays:  # per pid index: (start', dur', removed [P, 4], shortfall [P, 4], query results)
+        return (out_s[: ct.n], out_d[: ct.n], removed[: P * 4].reshape(P, 4), shortfall[: P * 4].reshape(P, 4),
+                q_out[: len(queries)].tolist())
     present = np.zeros(P, bool)
     present[np.unique(ct.pid)] = True
     report = {

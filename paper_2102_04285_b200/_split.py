@@ -211,6 +211,27 @@ def wide_cuts(sub: ColumnarTrace) -> list:
     return cuts
 
 
+def row_cuts(sub: ColumnarTrace, max_rows: int) -> list:
+    """Cut instants for a one-process trace holding more than ``max_rows``
+    events: near every max_rows/2-th start, moved out of the forbidden ranges
+    (_forbidden); windows then hold about half a call each."""
+    starts = np.sort(sub.start)
+    bad = _forbidden(sub)
+    step = max(1, max_rows // 2)
+    cuts, prev = [], None
+    for j in range(step, starts.size, step):
+        c = int(starts[j])
+        k = int(np.searchsorted(bad[:, 0], c, side="right")) - 1 if bad.size else -1
+        if k >= 0 and bad[k, 1] >= c:  # inside a forbidden range: just before it, else just after it
+            c = int(bad[k, 0]) - 1
+            if prev is not None and c <= prev:
+                c = int(bad[k, 1]) + 1
+        if (prev is None or c > prev) and c > int(starts[0]):
+            cuts.append(c)
+            prev = c
+    return cuts
+
+
 def window_trace(sub: ColumnarTrace, a: Optional[int], b: Optional[int]) -> ColumnarTrace:
     """The events of a one-process trace in window [a, b): resource events
     clipped to it, operations and zero-duration events by their start."""

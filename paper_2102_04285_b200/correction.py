@@ -136,6 +136,26 @@ def _batched(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: O
     todo = list(reversed(_split.plan_batches(ct)))
     while todo:
         pids = todo.pop()
+        if len(pids) == 1 and rows_by_pid[pids[0]].shape[0] > _split.MAX_EVENTS_PER_CALL:
+            try:  # one process larger than a call: its time windows, call by call, with the carries
+                r, s_, d_, r_rep, r_bd, r_procs = _huge_process(ct, pids[0], rows_by_pid, profile, attribution, eng)
+            except InvalidTraceError:
+                errs.append(_BatchError("invalid", int(rows_by_pid[pids[0]][0])))
+                continue
+            except UncalibratedHookError:
+                from .distributed import _first_uncalibrated_row
+                sub, rows = _split.sub_trace(ct, pids, rows_by_pid)
+                errs.append(_BatchError("uncalibrated", _first_uncalibrated_row(sub, profile, rows)))
+                continue
+            start[r], dur[r] = s_, d_
+            rep.removed_ns.update(r_rep.removed_ns)
+            rep.shortfall_ns.update(r_rep.shortfall_ns)
+            rep.original_total_ns += r_rep.original_total_ns
+            rep.corrected_total_ns += r_rep.corrected_total_ns
+            procs.update(r_procs)
+            if attribution is not None:
+                parts.append(r_bd)
+            continue
         sub, rows = _split.sub_trace(ct, pids, rows_by_pid)
         scaled = profile.scaled(sub.names)
         try:
@@ -173,6 +193,45 @@ def _batched(ct: ColumnarTrace, profile: CalibrationProfile, src, attribution: O
         raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile")
     processes = tuple(procs.get(k, m) for k, m in enumerate(ct.processes))
     return start, dur, rep, processes, (merge_breakdowns(parts) if attribution is not None else None)
+
+
+def _huge_process(ct: ColumnarTrace, p: int, rows_by_pid, profile: CalibrationProfile, attribution, eng):
+    """correct_trace (+ overlap) of ONE process holding more rows than a
+    device call takes: cut into time windows of about half a call and run
+    window by window on this GPU with the window carries (quantize residue,
+    slab-length prefix; distributed._analyze_windows).  Exact; raises
+    XsError(XS_UNSUPPORTED) when the process has no usable cuts.  Returns
+    (rows, start, dur, report, Breakdown, {process index: ProcessMeta})."""
+    import torch
+
+    from .distributed import SequentialWindowRunner, _analyze_windows
+
+    sub, rows = _split.sub_trace(ct, [p], rows_by_pid)
+    max_rows = _split.MAX_EVENTS_PER_CALL
+    split = -(-sub.n // max(1, max_rows // 2))
+    pv = int(ct.pids[p])
+    qs, slots = [], []
+    for k, m in enumerate(ct.processes):
+        if m.pid == pv:
+            for which in ("fork_ns", "join_ns"):
+                if getattr(m, which) is not None:
+                    qs.append((0, int(getattr(m, which))))
+                    slots.append((k, which))
+    qout: list = []
+    out = _analyze_windows(sub, profile, 0 if attribution is None else attribution,
+                           torch.device("cuda", eng.device), 1, 0, split, SequentialWindowRunner(eng),
+                           queries=qs, query_out=qout, max_rows=max_rows)
+    if out is None:
+        raise _engine.XsError(_lib.XS_UNSUPPORTED, f"process {pv} has more than {max_rows} events and no time "
+                                                   "window cuts that keep every window below that")
+    r, s_, d_, rep, bd = out
+    new: dict = {}
+    for (k, which), v in zip(slots, qout):
+        new.setdefault(k, {})[which] = v
+    procs = {k: ProcessMeta(m.pid, m.name, m.parent, new.get(k, {}).get("fork_ns", m.fork_ns),
+                            new.get(k, {}).get("join_ns", m.join_ns))
+             for k, m in enumerate(ct.processes) if m.pid == pv}
+    return rows[r], s_, d_, rep, bd, procs
 
 
 def _span_total(pid: np.ndarray, start: np.ndarray, end: np.ndarray, n_pids: int) -> int:

@@ -415,14 +415,15 @@ def merge_reports(local_rep, device):
 
 
 def analyze_sharded(ct: ColumnarTrace, profile, attribution=None, device=None, gather_columns: bool = False,
-                    split: int = 2, runner=None):
+                    split=None, runner=None):
     """``xstrace analyze --profile`` over ``world`` ranks, one GPU each:
     correct_trace then compute_overlap of the corrected trace, sharded by
     processes (LPT on event counts; per-pid independence,
     correction.py:132-157, overlap.py:126); with ``split`` > 0 a process
     holding more than n / (world * split) events is corrected as time
     windows spread over ranks, with the window carries (see
-    _analyze_windows).  Every rank returns the merged
+    _analyze_windows); default 2 when world > 1, 0 (whole processes: one
+    fused device call) on a single rank.  Every rank returns the merged
     CorrectionReport and Breakdown (bit-exact: integer sums).  The corrected
     columns come back as this rank's rows (``rows``, ``start``, ``dur``) or,
     with ``gather_columns``, as the whole trace's columns on every rank.
@@ -442,6 +443,8 @@ def analyze_sharded(ct: ColumnarTrace, profile, attribution=None, device=None, g
     eng = _engine.get(torch.cuda.current_device())
     dev = device or torch.device("cuda", eng.device)
     attr = 1 if attribution is not None and Attribution(attribution) is Attribution.CORRELATION else 0
+    if split is None:
+        split = 2 if world > 1 else 0
     if split > 0:
         out = _analyze_windows(ct, profile, attr, dev, world, rank, split, runner or DeviceWindowRunner(eng))
         if out is not None:
@@ -749,16 +752,16 @@ class DeviceWindowRunner:
         _, ev = self.eng.transition_sites(self._dt(local), 0x3)  # WRAPPER_PAIRS (overlap.py:200-203)
         return np.asarray(ev, np.int64)
 
-    def correct(self, local: ColumnarTrace, profile, r_in: list, span_end: np.ndarray):
-        """-> (start, dur, removed [P, 4], shortfall [P, 4])."""
+    def correct(self, local: ColumnarTrace, profile, r_in: list, span_end: np.ndarray, queries=()):
+        """-> (start, dur, removed [P, 4], shortfall [P, 4], mapped queries):
+        ``queries`` = (piece, time) pairs mapped by that piece's local
+        RemovalMap (xs_remap; fork / join instants)."""
         scaled = profile.scaled(local.names)
-        residue = np.zeros(max(local.n_pids, 1) * scaled.words, np.uint64)
-        for k, r in enumerate(r_in):
-            v = r * scaled.L
-            assert v.denominator == 1 and 0 <= v < scaled.L
-            residue[k * scaled.words:(k + 1) * scaled.words] = scaled.words_of(int(v))
+        residue = _residue_words(r_in, scaled, local.n_pids)
         raw = self.eng.correct(self._dt(local), scaled, None, carries=(residue, span_end))
-        return raw.start.cpu().numpy(), raw.dur.cpu().numpy(), raw.removed, raw.shortfall
+        q = list(self.eng.remap(np.array([k for k, _ in queries], np.int32),
+                                np.array([y for _, y in queries], np.int64))) if queries else []
+        return raw.start.cpu().numpy(), raw.dur.cpu().numpy(), raw.removed, raw.shortfall, q
 
     def overlap(self, trace: ColumnarTrace, attr: int):
         from . import _engine
@@ -766,11 +769,80 @@ class DeviceWindowRunner:
         return self.eng.overlap(_engine.DeviceTrace(trace, self.eng.device), attr)
 
 
-def _analyze_windows(ct: ColumnarTrace, profile, attr: int, dev, world: int, rank: int, split: int, runner):
+def _residue_words(r_in: list, scaled, n_pids: int) -> np.ndarray:
+    """xs_profile_t.residue_in: each piece's carried residue * L in words."""
+    residue = np.zeros(max(n_pids, 1) * scaled.words, np.uint64)
+    for k, r in enumerate(r_in):
+        v = r * scaled.L
+        assert v.denominator == 1 and 0 <= v < scaled.L
+        residue[k * scaled.words:(k + 1) * scaled.words] = scaled.words_of(int(v))
+    return residue
+
+
+class SequentialWindowRunner(DeviceWindowRunner):
+    """One device call per window (consecutive calls on one GPU): a single
+    process with more rows than one call takes (_split.MAX_EVENTS_PER_CALL)
+    is corrected window by window with the same carries."""
+
+    def _pieces(self, trace: ColumnarTrace):
+        from ._split import pid_rows, sub_trace
+
+        by = pid_rows(trace)
+        for k in range(trace.n_pids):
+            sub, rows = sub_trace(trace, [k], by)
+            yield k, sub, rows
+
+    def transition_rows(self, local: ColumnarTrace) -> np.ndarray:
+        from . import _engine
+
+        out = []
+        for _, sub, rows in self._pieces(local):
+            if sub.n:
+                _, ev = self.eng.transition_sites(_engine.DeviceTrace(sub, self.eng.device), 0x3)
+                out.append(rows[np.asarray(ev, np.int64)])
+        return np.sort(np.concatenate(out)) if out else np.zeros(0, np.int64)
+
+    def correct(self, local: ColumnarTrace, profile, r_in: list, span_end: np.ndarray, queries=()):
+        from . import _engine
+
+        scaled = profile.scaled(local.names)
+        P = local.n_pids
+        start = np.zeros(local.n, np.int64)
+        dur = np.zeros(local.n, np.int64)
+        removed = np.zeros((max(P, 1), 4), np.int64)
+        shortfall = np.zeros((max(P, 1), 4), np.int64)
+        q = [0] * len(queries)
+        for k, sub, rows in self._pieces(local):
+            if not sub.n:
+                continue
+            raw = self.eng.correct(_engine.DeviceTrace(sub, self.eng.device), scaled, None,
+                                   carries=(_residue_words([r_in[k]], scaled, 1), span_end[k:k + 1]))
+            start[rows] = raw.start.cpu().numpy()
+            dur[rows] = raw.dur.cpu().numpy()
+            removed[k], shortfall[k] = raw.removed[0], raw.shortfall[0]
+            mine = [i for i, (kk, _) in enumerate(queries) if kk == k]
+            if mine:
+                got = self.eng.remap(np.zeros(len(mine), np.int32), np.array([queries[i][1] for i in mine], np.int64))
+                for i, v in zip(mine, list(got)):
+                    q[i] = int(v)
+        return start, dur, removed, shortfall, q
+
+    def overlap(self, trace: ColumnarTrace, attr: int):
+        from . import _engine
+
+        return [(sub, self.eng.overlap(_engine.DeviceTrace(sub, self.eng.device), attr))
+                for _, sub, _ in self._pieces(trace) if sub.n]
+
+
+def _analyze_windows(ct: ColumnarTrace, profile, attr: int, dev, world: int, rank: int, split: int, runner,
+                     queries=None, query_out=None, max_rows: int = 0):
     """analyze_sharded with giant pids corrected as windows (see above).
     Returns (rows, start, dur, report, Breakdown), or None when nothing was
-    split or a window check failed on some rank (the caller then shards whole
-    pids).  Raises like the reference on invalid / uncalibrated traces."""
+    split, a window holds more than ``max_rows`` rows, or a window check
+    failed on some rank (the caller then shards whole pids).  Raises like the
+    reference on invalid / uncalibrated traces.  ``queries`` = (pid index,
+    time) pairs (world 1) are mapped by the corrected process's RemovalMap
+    into ``query_out`` (fork / join instants, correction.py:172-180)."""
     import math
     from fractions import Fraction
 
@@ -787,6 +859,12 @@ def _analyze_windows(ct: ColumnarTrace, profile, attr: int, dev, world: int, ran
         return None
     local, lrows, head, tail, pieces = piece_trace(ct, plan[rank])
     rows = lrows[head]
+    if max_rows and local.n and int(np.bincount(local.pid).max()) > max_rows:
+        return None
+    rq = []
+    for p, y in (queries or ()):
+        ks = [k for k, (pp, a, b) in enumerate(pieces) if pp == p and (a is None or a <= y) and (b is None or y < b)]
+        rq.append((ks[0], int(y)))
     P = local.n_pids
     neg, big = -(2**63), np.iinfo(np.int64).max
     win = [k for k, (_, a, b) in enumerate(pieces) if a is not None or b is not None]
@@ -825,7 +903,7 @@ def _analyze_windows(ct: ColumnarTrace, profile, attr: int, dev, world: int, ran
     res = None
     if not bad_invalid and P:
         try:
-            res = runner.correct(local, profile, r_in, span_end)
+            res = runner.correct(local, profile, r_in, span_end, rq)
         except _engine.UncalibratedEvent:
             bad_row = _first_uncalibrated_row(local, profile, lrows)
         except _engine.XsError as exc:
@@ -844,12 +922,13 @@ def _analyze_windows(ct: ColumnarTrace, profile, attr: int, dev, world: int, ran
         name = ct.names[int(ct.name[bad_row])]
         raise UncalibratedHookError(f"uncalibrated hook: API_INTERNAL({name!r}) missing from profile")
     if res is not None:
-        start, dur, removed, shortfall = res
+        start, dur, removed, shortfall, qv = res
         start = np.array(start, np.int64, copy=True)
         dur = np.asarray(dur, np.int64)
     else:
         start = dur = np.zeros(0, np.int64)
         removed = shortfall = np.zeros((0, 4), np.int64)
+        qv = []
     # phase B: total slab length per window -> P_in; no slab may run past a cut
     summ = []
     for k in win:
@@ -896,7 +975,12 @@ def _analyze_windows(ct: ColumnarTrace, profile, attr: int, dev, world: int, ran
                 g_rows.append((k, int(cut_lo[k]), min(e0, int(cut_hi[k])), tv, c, nm))
     otrace = _overlap_trace(local, start, o_e, g_rows) if P else local
     raw_o = runner.overlap(otrace, attr) if P else _empty_raw()
-    bd = merge_breakdown_raw(otrace, raw_o, dev)
+    bd = merge_breakdown_parts(raw_o if isinstance(raw_o, list) else [(otrace, raw_o)], dev)
+    if queries is not None:  # mapped by the window holding the instant, then shifted by its P_in
+        for (k, _), v in zip(rq, qv):
+            p, a, _ = pieces[k]
+            a0 = neg if a is None else a
+            query_out.append(int(v) - sum(T for pp, aa, T, _ in allw if pp == p and aa < a0))
     # a clipped HIGH_LEVEL event: start from its first piece, end from its last
     cont = [(int(r), int(x)) for r, x in zip(lrows[tail & ~head].tolist(), end[tail & ~head].tolist())]
     ends = dict(x for part in _gather_objects(cont, world) for x in part)

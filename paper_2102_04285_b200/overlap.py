@@ -264,14 +264,17 @@ def _merge_windows(parts) -> Breakdown:
 
 
 def _overlap_wide(ct: ColumnarTrace, p: int, rows_by_pid, attr: int, _source) -> Breakdown:
-    """One process too wide for one call's keys, over operation-free time
-    windows (_split.wide_cuts / window_trace)."""
+    """One process too wide for one call's keys, or holding more rows than
+    one call takes, over operation-free time windows (_split.wide_cuts /
+    row_cuts / window_trace)."""
     eng = _engine.get()
     sub, _ = _split.sub_trace(ct, [p], rows_by_pid)
     try:
         cuts = _split.wide_cuts(sub)
     except ValueError as exc:
         raise _engine.XsError(_lib.XS_UNSUPPORTED, f"xs_overlap: unsupported input {exc}") from None
+    if sub.n > _split.MAX_EVENTS_PER_CALL:
+        cuts = sorted(set(cuts) | set(_split.row_cuts(sub, _split.MAX_EVENTS_PER_CALL)))
     bounds = [None] + cuts + [None]
     parts = []
     for a, b in zip(bounds[:-1], bounds[1:]):
@@ -298,6 +301,8 @@ def _overlap_batched(ct: ColumnarTrace, attribution, _source) -> Breakdown:
     rows_by_pid = _split.pid_rows(ct)
     parts = []
     wide = _split.wide_pids(ct)
+    counts = np.bincount(ct.pid, minlength=ct.n_pids)
+    wide += [p for p in np.nonzero(counts > _split.MAX_EVENTS_PER_CALL)[0].tolist() if p not in wide]
     for p in wide:
         parts.append(_overlap_wide(ct, p, rows_by_pid, attr, _source))
     todo = list(reversed([b for b in ([q for q in batch if q not in wide] for batch in _split.plan_batches(ct)) if b]))

@@ -38,10 +38,10 @@ class OracleRunner:
         res = oracle.transition_sites(local, 0x3)
         return np.array(sorted(e for v in res.values() for e in v), np.int64)
 
-    def correct(self, local, profile, r_in, span_end):
+    def correct(self, local, profile, r_in, span_end, queries=()):
         import oracle
 
-        return oracle.correct(local, profile, residue_in=r_in, span_end_in=span_end, arrays=True)
+        return oracle.correct(local, profile, queries=queries, residue_in=r_in, span_end_in=span_end, arrays=True)
 
     def overlap(self, trace, attr):
         from paper_2102_04285_b200.columnar import ColumnarTrace
@@ -208,3 +208,22 @@ def test_gloo_two_rank_windows(kind, prof, attr, split):
         assert rm == wrep["removed_ns"] and sf == wrep["shortfall_ns"]
         assert ot == wrep["original_total_ns"] and cot == wrep["corrected_total_ns"]
         assert c == cells and sp == spans and un == untracked
+
+
+def test_window_fork_join_queries():
+    """Fork / join instants of a windowed process are mapped by the window
+    holding them, shifted by its slab-length prefix (correction.py:172-180)."""
+    import oracle
+    import torch
+    from paper_2102_04285_b200.distributed import _analyze_windows
+
+    ct = _trace("ddpg1")
+    profile = _profiles()["ladder"]
+    lo, hi = int(ct.start.min()), int((ct.start + ct.dur).max())
+    ys = [lo - 5, lo, lo + (hi - lo) // 3, (lo + hi) // 2, hi - 1, hi, hi + 7]
+    q = []
+    out = _analyze_windows(ct, profile, 0, torch.device("cpu"), 1, 0, 6, OracleRunner(),
+                           queries=[(0, y) for y in ys], query_out=q)
+    assert out is not None
+    _, _, _, want = oracle.correct(ct, profile, queries=[(0, y) for y in ys])
+    assert q == want
