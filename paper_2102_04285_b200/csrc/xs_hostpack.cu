@@ -84,6 +84,9 @@ int threads_for(int64_t n, int n_threads) {
 class Pool {
  public:
   void run(int T, const std::function<void(int)>& f) {
+    // one job at a time: concurrent callers (the pipelined analysis packs
+    // from several host threads) would overwrite job_ / pending_ mid-job
+    std::lock_guard<std::mutex> one(run_m_);
     std::unique_lock<std::mutex> lk(m_);
     if (owner_ != getpid()) {  // first use, or a fork: the threads are gone
       owner_ = getpid();
@@ -125,7 +128,7 @@ class Pool {
       }
     }
   }
-  std::mutex m_;
+  std::mutex m_, run_m_;
   std::condition_variable cv_, done_;
   const std::function<void(int)>* job_ = nullptr;
   unsigned long long gen_ = 0;
@@ -144,9 +147,7 @@ void run_parts(int T, F&& f) {
     f(0);
     return;
   }
-  static std::mutex serial;  // one pass at a time through the pool (callers may be concurrent threads)
-  std::lock_guard<std::mutex> g(serial);
-  const std::function<void(int)> fn = f;
+  const std::function<void(int)> fn = f;  // (Pool::run admits one pass at a time)
   pool().run(T, fn);
 }
 

@@ -4,6 +4,7 @@ through the host restatement of xs_unpack (columnar.unpack_block); the CUDA
 widening is checked against the same columns in tests/test_gpu_pack.py."""
 
 import numpy as np
+import pytest
 
 from paper_2102_04285_b200 import synth
 from paper_2102_04285_b200.columnar import ColumnarTrace, pack_block, unpack_block
@@ -136,3 +137,38 @@ def test_native_pack_matches_numpy_builder():
     ct = synth.ddpg_trace(20)
     _native_equal(dataclasses.replace(ct, cat=np.where(np.arange(ct.n) == 3, 200, ct.cat).astype(np.uint8),
                                       _source=None), 2)
+
+
+@pytest.mark.timeout(300)
+def test_native_pack_concurrent_callers():
+    """Several host threads packing at once (analyze_columnar_pipelined packs
+    each worker's next batch concurrently): the shared worker pool takes one
+    pass at a time -- no hang, no corrupted blocks."""
+    import threading
+
+    from paper_2102_04285_b200.columnar import pack_native
+    from paper_2102_04285_b200.correction import _pid_batches, _row_slice
+
+    ct = synth.config3_trace(processes=9, events_per_pid=150_000, workers=4)
+    parts = _pid_batches(ct, 9)
+    want = {}
+    for k, (a, b) in enumerate(parts):
+        lay, blk = pack_block(_row_slice(ct, a, b))
+        want[k] = bytes(np.frombuffer(blk, np.uint8)[: lay.total]) if not isinstance(blk, np.ndarray) else \
+            bytes(blk[: lay.total])
+    bad = []
+
+    def work(w):
+        for _ in range(4):
+            for k, (a, b) in enumerate(parts):
+                if k % 3 == w:
+                    lay, blk = pack_native(_row_slice(ct, a, b), None, n_threads=3)
+                    if bytes(blk[: lay.total]) != want[k]:
+                        bad.append(k)
+
+    ths = [threading.Thread(target=work, args=(w,)) for w in range(3)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not bad
