@@ -218,6 +218,29 @@ class ColumnarTrace:
                              self.names, self.processes, self.pid_has_meta)
 
 
+# -- columns of Traces this package produced --------------------------------
+# A Trace is immutable (frozen dataclass, events in a tuple), so the columns a
+# correction produced stay valid for the Trace built from them:
+# compute_overlap(correct_trace(t)[0]) -- the reference's call sequence
+# (cli.py:168-171) -- then skips re-interning a million Event objects.
+_PRODUCED: dict = {}
+
+
+def remember_columnar(trace, ct: "ColumnarTrace") -> None:
+    import weakref
+
+    key = id(trace)
+    _PRODUCED[key] = (weakref.ref(trace), ct)
+    weakref.finalize(trace, _PRODUCED.pop, key, None)
+
+
+def produced_columnar(trace) -> Optional["ColumnarTrace"]:
+    hit = _PRODUCED.get(id(trace))
+    if hit is not None and hit[0]() is trace:
+        return hit[1]
+    return None
+
+
 # -- packed upload format (xs_packed_t) -------------------------------------
 PACK_ROWS = 256  # rows per start base
 

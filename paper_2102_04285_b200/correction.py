@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _engine, _lib, _split
 from .calibration import HOOK_KINDS, CalibrationProfile
-from .columnar import ColumnarTrace
+from .columnar import ColumnarTrace, remember_columnar
 from .model import Event, InvalidTraceError, ProcessMeta, Trace, format_violations, meta_violations
 
 
@@ -324,7 +324,9 @@ def correct_trace(trace, profile: CalibrationProfile) -> tuple:
         return out, rep
     events = [Event(e.pid, e.tid, e.category, e.name, s, d, e.correlation)
               for e, s, d in zip(trace.events, out.start.tolist(), out.dur.tolist())]
-    return Trace(trace.clock_domain, events, out.processes), rep
+    res = Trace(trace.clock_domain, events, out.processes)
+    remember_columnar(res, out)  # (compute_overlap(corrected) reuses the columns just produced)
+    return res, rep
 
 
 def analyze_columnar(ct: ColumnarTrace, profile: CalibrationProfile, attribution=None, device_trace=None,

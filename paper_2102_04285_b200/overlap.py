@@ -20,7 +20,7 @@ from enum import Enum
 import numpy as np
 
 from . import _engine, _lib, _split
-from .columnar import ColumnarTrace
+from .columnar import ColumnarTrace, produced_columnar
 from .model import Category, InvalidTraceError, Trace, format_violations, meta_violations
 
 
@@ -142,7 +142,10 @@ _MASK_CATS = [frozenset(_CATS[c] for c in range(1, 6) if m & (1 << (c - 1))) for
 
 
 def _as_columnar(trace) -> ColumnarTrace:
-    return trace if isinstance(trace, ColumnarTrace) else ColumnarTrace.from_trace(trace)
+    if isinstance(trace, ColumnarTrace):
+        return trace
+    ct = produced_columnar(trace)  # (a Trace correct_trace returned: its columns are at hand)
+    return ct if ct is not None else ColumnarTrace.from_trace(trace)
 
 
 def _source_trace(trace, ct: ColumnarTrace) -> Trace:
