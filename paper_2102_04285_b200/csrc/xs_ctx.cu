@@ -601,6 +601,25 @@ static int prefetch_report(xs_ctx* ctx, cudaStream_t s) {
                                {ctx->h_report + b / 8, ctx->ptr[W_SHORTFALL], b}});
 }
 
+// Pass 1 + its statistics read-back as one graph segment (six eager launches
+// left the device waiting on the host for ~18 us at 1M events), then the
+// call's one sync: sizes; per-event rule violations stop here.
+static int pass1_sync(xs_ctx* ctx, const EventView& v, const xs_profile_t* prof, cudaStream_t s) {
+  std::string k1("pass1");
+  k1.push_back('\0');
+  k1.append(reinterpret_cast<const char*>(&v), sizeof(v));
+  k1.append(reinterpret_cast<const char*>(&prof->has_internal), sizeof(prof->has_internal));
+  XS_TRY(run_segment(ctx, s, k1, true, [&](cudaStream_t w) -> int {
+    XS_TRY(stage_events_async(ctx, v, w, true, prof));
+    Stats* d = nullptr;
+    XS_TRY(ws(ctx, W_STATS, 1, w, &d));
+    return to_host_many(ctx, w, {{ctx->h_stats, d, sizeof(Stats)}});
+  }));
+  XS_CUDA(cudaStreamSynchronize(s));
+  if (!ctx->pend_stage.empty()) prof_flush(ctx);
+  return ctx->h_stats->n_bad ? XS_INVALID_TRACE : XS_OK;
+}
+
 static int correct_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t* prof, int64_t* out_start,
                           int64_t* out_dur, int64_t* bad_event, cudaStream_t s, bool corrected_spans) {
   ctx->have_correct = false;
@@ -609,7 +628,7 @@ static int correct_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
     return XS_BAD_ARGUMENT;
   if (ev->n > 0 && (!out_start || !out_dur)) return XS_BAD_ARGUMENT;
   EventView v{*ev, ev->start, ev->dur};
-  XS_TRY(stage_events(ctx, v, s, false, true, prof));  // (sync: sizes; per-event rule violations stop here)
+  XS_TRY(pass1_sync(ctx, v, prof, s));
   // the pipeline is safe on a trace whose nesting / correlations / API names
   // turn out bad, so the verdict is read once, after this sync-free segment
   std::string key = segment_key(ctx, "correct", &v, sizeof(v));
@@ -733,7 +752,7 @@ static int analyze_once(xs_ctx_t* ctx, const xs_events_t* ev, const xs_profile_t
   EventView vc{*ev, out_start_dev, out_dur_dev};
   static const bool host_timing = getenv("XS_HOST_TIMING") != nullptr;  // (developer diagnostics)
   const auto ht0 = std::chrono::steady_clock::now();
-  XS_TRY(stage_events(ctx, v, s, false, true, prof));  // (sync: sizes; per-event rule violations stop here)
+  XS_TRY(pass1_sync(ctx, v, prof, s));
   const auto ht1 = std::chrono::steady_clock::now();
   const Stats orig = *ctx->h_stats;
   Stats* st = nullptr;
