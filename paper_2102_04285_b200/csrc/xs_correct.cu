@@ -369,9 +369,11 @@ __global__ void k_caps(EventView v, int64_t n, const int* cnt, const int* pos, c
     if (sf[h]) atomic_add_i64(&shortfall[(int64_t)p * 4 + h], sf[h]);
 }
 
-// one nonzero removal slab: [a, b) and the total slab length before it
-struct Slab {
-  int64_t a, b, pre, pad;
+// one nonzero removal slab: its start a and the total slab length before it
+// (16 bytes; its end b = a + the next slab's pre - pre, the slabs being
+// disjoint and ordered: RemovalMap.extents, _timeline.py:90-111)
+struct __align__(16) Slab {
+  int64_t a, pre;
 };
 
 // (max,+) RemovalMap scan, segmented by pid; slab count is global
@@ -481,7 +483,7 @@ __global__ void __launch_bounds__(XS_BLOCK, XS_REMOVAL_MINB) k_removal(const uin
     acc[hook_of(sub[j])] += mb - ma;
     if (len[j] > 0) {
       const int64_t at = cur.cnt;
-      slabs[at] = Slab{a, b, cur.P, 0};
+      slabs[at] = Slab{a, cur.P};
       nsl++;
       tot += len[j];
     }
@@ -508,26 +510,33 @@ __global__ void k_slab_base(const int* pid_slabs, int np, int64_t* slab_base) {
   }
 }
 
-// RemovalMap.__call__ (_timeline.py:112-117) on a relative coordinate
-__device__ __forceinline__ int64_t rmap_removed(int64_t y, const Slab* sl,
-                                                int64_t base, int64_t K, int64_t total) {
-  int64_t lo = 0, hi = K;  // bisect_right(ends, y)
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (sl[base + mid].b <= y) lo = mid + 1;
-    else hi = mid;
-  }
-  if (lo == K) return total;
-  const Slab x = sl[base + lo];  // (a, b, prefix in one 32-byte sector)
-  int64_t r = x.pre;
-  int64_t a = x.a;
-  if (a < y) r += y - a;
-  return r;
+// RemovalMap.__call__ (_timeline.py:112-117) on a relative coordinate, over
+// the slab starts: with j = #slabs starting before y, slabs 0..j-2 lie wholly
+// before y and slab j-1 is removed up to y (the sum of full slabs with b <= y
+// plus the part of the one holding y, as bisect_right over the ends gives)
+__device__ __forceinline__ int64_t rmap_tail(int64_t y, const Slab* sl, int64_t base, int64_t K, int64_t total,
+                                             int64_t j) {
+  if (j == 0) return 0;
+  const Slab x = sl[base + j - 1];
+  const int64_t next = j < K ? sl[base + j].pre : total;  // (the next record: mostly the same sector)
+  const int64_t part = y - x.a, len = next - x.pre;
+  return x.pre + (part < len ? part : len);
 }
 
-// Sampled index over each pid's slab ends: the pid's time range [0, span]
-// is cut into W = 2^logw windows of 2^shift ns; idx[p*W + w] =
-// bisect_right(ends, w << shift).  A query y in window w then bisects only
+__device__ __forceinline__ int64_t rmap_removed(int64_t y, const Slab* sl,
+                                                int64_t base, int64_t K, int64_t total) {
+  int64_t lo = 0, hi = K;  // j = #starts < y
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (sl[base + mid].a < y) lo = mid + 1;
+    else hi = mid;
+  }
+  return rmap_tail(y, sl, base, K, total, lo);
+}
+
+// Sampled index over each pid's slab starts: the pid's time range [0, span]
+// is cut into W = 2^logw windows of 2^shift ns; idx[p*W + w] = #starts <
+// (w << shift).  A query y in window w then bisects only
 // [idx[w], idx[w+1]] -- a few slabs instead of all of them.
 __device__ __forceinline__ int rmap_shift(const int64_t* lo, const int64_t* hi, int p, int logw) {
   const int64_t span = hi[p] > lo[p] ? hi[p] - lo[p] : 0;
@@ -548,10 +557,10 @@ __global__ void k_rmap_index(int np, int logw, const int64_t* lo, const int64_t*
     return;
   }
   const uint64_t x = (uint64_t)w << rmap_shift(lo, hi, p, logw);
-  int64_t a = 0, b = K;  // bisect_right(ends, x)
+  int64_t a = 0, b = K;  // #starts < x
   while (a < b) {
     const int64_t m = (a + b) >> 1;
-    if ((uint64_t)sl[base + m].b <= x) a = m + 1;
+    if ((uint64_t)sl[base + m].a < x) a = m + 1;
     else b = m;
   }
   idx[t] = (int32_t)a;
@@ -565,15 +574,10 @@ __device__ __forceinline__ int64_t rmap_removed_idx(int64_t y, const Slab* sl, i
   int64_t a = pidx[w], b = w + 1 < W ? pidx[w + 1] : K;
   while (a < b) {
     const int64_t m = (a + b) >> 1;
-    if (sl[base + m].b <= y) a = m + 1;
+    if (sl[base + m].a < y) a = m + 1;
     else b = m;
   }
-  if (a == K) return total;
-  const Slab x = sl[base + a];
-  int64_t r = x.pre;
-  const int64_t s = x.a;
-  if (s < y) r += y - s;
-  return r;
+  return rmap_tail(y, sl, base, K, total, a);
 }
 
 __global__ void k_remap(EventView v, int64_t n, const int64_t* lo, const int64_t* hi, const Slab* sl,
