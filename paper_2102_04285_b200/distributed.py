@@ -859,6 +859,7 @@ def _analyze_windows(ct: ColumnarTrace, profile, attr: int, dev, world: int, ran
         return None
     local, lrows, head, tail, pieces = piece_trace(ct, plan[rank])
     rows = lrows[head]
+    assert world == 1 or not max_rows  # (a per-rank early return would desynchronise the collectives)
     if max_rows and local.n and int(np.bincount(local.pid).max()) > max_rows:
         return None
     rq = []
